@@ -1,0 +1,302 @@
+// ref_shim.cpp -- TEST INFRASTRUCTURE ONLY.
+//
+// Compiles the UNMODIFIED reference headers in place
+// (-I/root/reference/proj/include; nothing is copied into this repo) and
+// exposes their byte path through a C ABI so tests/ can generate golden
+// vectors and bench.py can time the reference CPU codec (--impl reference,
+// cpu_baseline.kind = "reference"). Built by oracle/Makefile into
+// oracle/_ref/libghostserve_ref.so (git-ignored, travels with gpurun).
+//
+// Timing follows the reference bench convention (tools/ghostserve.cpp:262-283):
+// steady_clock around the encode / reconstruct call only.
+//
+// The *_striped entry points are OUR wrapper, not the reference's: they call
+// ghostserve::encode / reconstruct on disjoint byte stripes from T threads,
+// which is valid because XOR and RS are position-wise (coding.hpp:143-172).
+#include <chrono>
+#include <cstdint>
+#include <cstring>
+#include <map>
+#include <span>
+#include <stdexcept>
+#include <thread>
+#include <vector>
+
+// kv_layout.hpp must precede parity_store.hpp (parity_store.hpp:15 vs :33).
+#include "ghostserve/kv_layout.hpp"
+#include "ghostserve/coding.hpp"
+#include "ghostserve/gf256.hpp"
+#include "ghostserve/parity_store.hpp"
+
+using namespace ghostserve;
+
+namespace {
+
+int map_exception() {
+  try {
+    throw;
+  } catch (const UnrecoverableError&) {
+    return 2;
+  } catch (const std::domain_error&) {
+    return 3;
+  } catch (const std::invalid_argument&) {
+    return 1;
+  } catch (const std::logic_error&) {
+    return 1;
+  } catch (...) {
+    return 2;
+  }
+}
+
+CodingScheme scheme_of(int kind, int n, int k) {
+  CodingScheme s;
+  s.kind = kind == 0 ? CodeKind::kXor : kind == 1 ? CodeKind::kRdp : CodeKind::kReedSolomon;
+  s.n = n;
+  s.k = k;
+  return s;
+}
+
+double seconds_since(std::chrono::steady_clock::time_point t0) {
+  return std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+}
+
+int encode_range(const CodingScheme& s, const uint8_t* const* data, size_t off, size_t len,
+                 uint8_t* const* parity) {
+  std::vector<ConstShardSpan> spans;
+  for (int j = 0; j < s.n; ++j) spans.emplace_back(data[j] + off, len);
+  auto out = encode(s, spans);
+  for (int i = 0; i < s.k; ++i)
+    if (len) std::memcpy(parity[i] + off, out[static_cast<size_t>(i)].data(), len);
+  return 0;
+}
+
+int reconstruct_range(const CodingScheme& s, const uint8_t* const* shards, const int* lost,
+                      int n_lost, size_t off, size_t len, uint8_t* const* out, int* n_out) {
+  ErasurePattern pattern(std::vector<int>(lost, lost + n_lost));
+  std::map<int, ConstShardSpan> surviving;
+  for (int idx = 0; idx < s.n + s.k; ++idx)
+    if (shards[idx] != nullptr) surviving[idx] = ConstShardSpan(shards[idx] + off, len);
+  auto rebuilt = reconstruct(s, surviving, pattern);
+  int b = 0;
+  for (auto& [idx, bytes] : rebuilt) {
+    (void)idx;
+    if (len) std::memcpy(out[b] + off, bytes.data(), len);
+    ++b;
+  }
+  *n_out = b;
+  return 0;
+}
+
+}  // namespace
+
+extern "C" {
+
+uint8_t ghs_gf_mul(uint8_t a, uint8_t b) { return gf256::mul(a, b); }
+
+int ghs_gf_inv(uint8_t a, uint8_t* out) {
+  try {
+    *out = gf256::inv(a);
+    return 0;
+  } catch (...) {
+    return map_exception();
+  }
+}
+
+void ghs_gf_tables(uint8_t* exp_out, uint8_t* log_out) {
+  std::memcpy(exp_out, gf256::kTables.exp.data(), 512);
+  std::memcpy(log_out, gf256::kTables.log.data(), 256);
+}
+
+void ghs_mul_table(uint8_t* out /* 65536 */) {
+  for (unsigned c = 0; c < 256; ++c) std::memcpy(out + c * 256, gf256::mul_row(static_cast<uint8_t>(c)), 256);
+}
+
+int ghs_validate(int kind, int n, int k) {
+  try {
+    scheme_of(kind, n, k).validate();
+    return 0;
+  } catch (...) {
+    return map_exception();
+  }
+}
+
+int ghs_max_tolerance(int kind, int n, int k) { return max_tolerance(scheme_of(kind, n, k)); }
+
+int ghs_encoding_matrix(int kind, int n, int k, uint8_t* coef) {
+  try {
+    auto m = build_encoding_matrix(scheme_of(kind, n, k));
+    std::memcpy(coef, m.coef.data(), m.coef.size());
+    return 0;
+  } catch (...) {
+    return map_exception();
+  }
+}
+
+int ghs_encode(int kind, int n, int k, const uint8_t* const* data, size_t len,
+               uint8_t* const* parity, double* secs) {
+  try {
+    const auto s = scheme_of(kind, n, k);
+    std::vector<ConstShardSpan> spans;
+    for (int j = 0; j < n; ++j) spans.emplace_back(data[j], len);
+    const auto t0 = std::chrono::steady_clock::now();
+    auto out = encode(s, spans);
+    if (secs) *secs = seconds_since(t0);
+    for (int i = 0; i < k; ++i)
+      if (len) std::memcpy(parity[i], out[static_cast<size_t>(i)].data(), len);
+    return 0;
+  } catch (...) {
+    return map_exception();
+  }
+}
+
+int ghs_reconstruct(int kind, int n, int k, const uint8_t* const* shards, const int* lost,
+                    int n_lost, size_t len, uint8_t* const* out, int* n_out, double* secs) {
+  try {
+    const auto s = scheme_of(kind, n, k);
+    ErasurePattern pattern(std::vector<int>(lost, lost + n_lost));
+    std::map<int, ConstShardSpan> surviving;
+    for (int idx = 0; idx < n + k; ++idx)
+      if (shards[idx] != nullptr) surviving[idx] = ConstShardSpan(shards[idx], len);
+    const auto t0 = std::chrono::steady_clock::now();
+    auto rebuilt = reconstruct(s, surviving, pattern);
+    if (secs) *secs = seconds_since(t0);
+    int b = 0;
+    for (auto& [idx, bytes] : rebuilt) {
+      (void)idx;
+      if (len) std::memcpy(out[b], bytes.data(), len);
+      ++b;
+    }
+    *n_out = b;
+    return 0;
+  } catch (...) {
+    return map_exception();
+  }
+}
+
+// Striped multi-thread wrappers (ours): T threads over disjoint 64-B aligned
+// byte ranges, each calling the reference codec on its sub-spans.
+int ghs_encode_striped(int kind, int n, int k, const uint8_t* const* data, size_t len,
+                       uint8_t* const* parity, int threads, double* secs) {
+  try {
+    const auto s = scheme_of(kind, n, k);
+    s.validate();
+    if (threads < 1) threads = 1;
+    size_t per = (len + threads - 1) / threads;
+    per = (per + 63) & ~size_t{63};
+    std::vector<std::thread> pool;
+    std::vector<int> status(static_cast<size_t>(threads), 0);
+    const auto t0 = std::chrono::steady_clock::now();
+    for (int t = 0; t < threads; ++t) {
+      const size_t off = std::min(len, per * t), end = std::min(len, per * (t + 1));
+      pool.emplace_back([&, t, off, end] {
+        try {
+          encode_range(s, data, off, end - off, parity);
+        } catch (...) {
+          status[static_cast<size_t>(t)] = map_exception();
+        }
+      });
+    }
+    for (auto& th : pool) th.join();
+    if (secs) *secs = seconds_since(t0);
+    for (int st : status)
+      if (st) return st;
+    return 0;
+  } catch (...) {
+    return map_exception();
+  }
+}
+
+int ghs_reconstruct_striped(int kind, int n, int k, const uint8_t* const* shards,
+                            const int* lost, int n_lost, size_t len, uint8_t* const* out,
+                            int* n_out, int threads, double* secs) {
+  try {
+    const auto s = scheme_of(kind, n, k);
+    if (threads < 1) threads = 1;
+    size_t per = (len + threads - 1) / threads;
+    per = (per + 63) & ~size_t{63};
+    std::vector<std::thread> pool;
+    std::vector<int> status(static_cast<size_t>(threads), 0), counts(static_cast<size_t>(threads), 0);
+    const auto t0 = std::chrono::steady_clock::now();
+    for (int t = 0; t < threads; ++t) {
+      const size_t off = std::min(len, per * t), end = std::min(len, per * (t + 1));
+      pool.emplace_back([&, t, off, end] {
+        try {
+          reconstruct_range(s, shards, lost, n_lost, off, end - off, out,
+                            &counts[static_cast<size_t>(t)]);
+        } catch (...) {
+          status[static_cast<size_t>(t)] = map_exception();
+        }
+      });
+    }
+    for (auto& th : pool) th.join();
+    if (secs) *secs = seconds_since(t0);
+    for (int st : status)
+      if (st) return st;
+    *n_out = counts[0];
+    return 0;
+  } catch (...) {
+    return map_exception();
+  }
+}
+
+int ghs_slice_bytes(int layers, int kv_heads, int head_dim, int tp, uint32_t chunk_size,
+                    uint64_t* out) {
+  try {
+    ModelConfig m;
+    m.layers = layers;
+    m.kv_heads = kv_heads;
+    m.head_dim = head_dim;
+    m.tp_degree = tp;
+    *out = slice_bytes(m, chunk_size);
+    return 0;
+  } catch (...) {
+    return map_exception();
+  }
+}
+
+int ghs_make_ground_truth_slice(uint64_t seed, uint64_t req, uint32_t chunk, int worker,
+                                int layers, int kv_heads, int head_dim, int tp,
+                                uint32_t chunk_size, uint32_t valid, uint8_t* out) {
+  try {
+    ModelConfig m;
+    m.layers = layers;
+    m.kv_heads = kv_heads;
+    m.head_dim = head_dim;
+    m.tp_degree = tp;
+    auto s = make_ground_truth_slice(seed, req, ChunkId{chunk}, worker, m, chunk_size, valid);
+    std::memcpy(out, s.bytes.data(), s.bytes.size());
+    return 0;
+  } catch (...) {
+    return map_exception();
+  }
+}
+
+uint64_t ghs_fnv1a64(const uint8_t* bytes, size_t len, uint64_t h) {
+  return fnv1a64(std::span<const uint8_t>(bytes, len), h);
+}
+
+// checkpoint_chunk's byte work (checkpoint.hpp:143-147): encode + seal.
+// Returns the sealed checksum; *secs covers encode + seal.
+int ghs_encode_and_seal(int kind, int n, int k, const uint8_t* const* data, size_t len,
+                        uint8_t* const* parity, uint64_t* checksum, double* secs) {
+  try {
+    const auto s = scheme_of(kind, n, k);
+    std::vector<ConstShardSpan> spans;
+    for (int j = 0; j < n; ++j) spans.emplace_back(data[j], len);
+    const auto t0 = std::chrono::steady_clock::now();
+    ParityChunk pc;
+    pc.scheme = s;
+    pc.slice_len = len;
+    pc.parity = encode(s, spans);
+    pc.seal();
+    if (secs) *secs = seconds_since(t0);
+    *checksum = pc.checksum;
+    for (int i = 0; i < k; ++i)
+      if (len) std::memcpy(parity[i], pc.parity[static_cast<size_t>(i)].data(), len);
+    return 0;
+  } catch (...) {
+    return map_exception();
+  }
+}
+
+}  // extern "C"
