@@ -1,0 +1,224 @@
+// ghostserve_gpu/coding.hpp -- drop-in C++ facade over gs_capi.h with the
+// reference's signatures (/root/reference/proj/include/ghostserve/coding.hpp):
+//
+//   ghostserve_gpu::encode(const CodingScheme&, std::span<const ConstShardSpan>)
+//       -> std::vector<std::vector<uint8_t>>                       (coding.hpp:313)
+//   ghostserve_gpu::encode(const CodingScheme&, const std::vector<std::vector<uint8_t>>&)  (:332)
+//   ghostserve_gpu::reconstruct(const CodingScheme&, const std::map<int, ConstShardSpan>&,
+//                               const ErasurePattern&) -> std::map<int, std::vector<uint8_t>> (:458)
+//   build_encoding_matrix / max_tolerance / memory_overhead_ratio / CodingScheme /
+//   ErasurePattern / EncodingMatrix / UnrecoverableError                (:17-137)
+//
+// Status codes map back to the reference exception types:
+//   GS_INVALID_ARGUMENT -> std::invalid_argument, GS_UNRECOVERABLE ->
+//   UnrecoverableError, GS_DOMAIN_ERROR -> std::domain_error, others ->
+//   std::runtime_error. A consumer switches by changing the namespace (or a
+//   `namespace ghostserve = ghostserve_gpu;` alias) and linking
+//   libghostserve_b200.so; every byte is computed by the sm_100a kernels.
+#pragma once
+
+#include <algorithm>
+#include <cstdint>
+#include <map>
+#include <mutex>
+#include <span>
+#include <stdexcept>
+#include <string>
+#include <tuple>
+#include <vector>
+
+#include "../gs_capi.h"
+
+namespace ghostserve_gpu {
+
+enum class CodeKind { kXor = GS_XOR, kRdp = GS_RDP, kReedSolomon = GS_RS };
+
+inline const char* to_string(CodeKind k) {
+  switch (k) {
+    case CodeKind::kXor: return "xor";
+    case CodeKind::kRdp: return "rdp";
+    case CodeKind::kReedSolomon: return "rs";
+  }
+  return "?";
+}
+
+class UnrecoverableError : public std::runtime_error {
+ public:
+  using std::runtime_error::runtime_error;
+};
+
+namespace detail {
+inline void check(int status, const char* what) {
+  if (status == GS_OK) return;
+  std::string msg = std::string(what) + ": " + gs_last_error();
+  switch (status) {
+    case GS_INVALID_ARGUMENT: throw std::invalid_argument(msg);
+    case GS_UNRECOVERABLE: throw UnrecoverableError(msg);
+    case GS_DOMAIN_ERROR: throw std::domain_error(msg);
+    default: throw std::runtime_error(msg);
+  }
+}
+}  // namespace detail
+
+struct CodingScheme {
+  CodeKind kind = CodeKind::kXor;
+  int n = 1;
+  int k = 1;
+
+  void validate() const { detail::check(gs_scheme_validate(static_cast<int>(kind), n, k), "coding"); }
+  static CodingScheme xor_code(int n) { return {CodeKind::kXor, n, 1}; }
+  static CodingScheme rdp(int n) { return {CodeKind::kRdp, n, 2}; }
+  static CodingScheme reed_solomon(int n, int k) { return {CodeKind::kReedSolomon, n, k}; }
+  bool operator==(const CodingScheme&) const = default;
+};
+
+inline int max_tolerance(const CodingScheme& s) { return gs_max_tolerance(static_cast<int>(s.kind), s.n, s.k); }
+
+inline double memory_overhead_ratio(const CodingScheme& s) {
+  return static_cast<double>(s.k) / static_cast<double>(s.n);
+}
+
+struct EncodingMatrix {
+  int rows = 0;
+  int cols = 0;
+  std::vector<std::uint8_t> coef;
+  std::uint8_t at(int r, int c) const { return coef[static_cast<std::size_t>(r) * cols + c]; }
+};
+
+inline EncodingMatrix build_encoding_matrix(const CodingScheme& s) {
+  EncodingMatrix m;
+  s.validate();
+  m.rows = s.k;
+  m.cols = s.n;
+  m.coef.assign(static_cast<std::size_t>(s.k) * s.n, 0);
+  detail::check(gs_encoding_matrix(static_cast<int>(s.kind), s.n, s.k, m.coef.data()), "coding");
+  return m;
+}
+
+struct ErasurePattern {
+  std::vector<int> lost;
+  explicit ErasurePattern(std::vector<int> indices = {}) : lost(std::move(indices)) {
+    std::sort(lost.begin(), lost.end());
+    lost.erase(std::unique(lost.begin(), lost.end()), lost.end());
+  }
+  bool contains(int idx) const { return std::binary_search(lost.begin(), lost.end(), idx); }
+};
+
+using ConstShardSpan = std::span<const std::uint8_t>;
+
+namespace detail {
+
+struct Handles {
+  std::mutex mu;
+  std::map<std::tuple<int, int, int, std::vector<int>, bool>, gs_codec*> codecs;
+  gs_pipeline* pipe = nullptr;
+  ~Handles() {
+    for (auto& kv : codecs) gs_codec_destroy(kv.second);
+    if (pipe) gs_pipeline_destroy(pipe);
+  }
+};
+
+inline Handles& handles() {
+  static Handles h;
+  return h;
+}
+
+inline gs_pipeline* pipeline() {
+  auto& h = handles();
+  if (!h.pipe) check(gs_pipeline_create(0, std::size_t{128} << 20, &h.pipe), "pipeline");
+  return h.pipe;
+}
+
+inline gs_codec* codec(const CodingScheme& s, const std::vector<int>* lost) {
+  auto& h = handles();
+  auto key = std::make_tuple(static_cast<int>(s.kind), s.n, s.k, lost ? *lost : std::vector<int>{}, lost != nullptr);
+  auto it = h.codecs.find(key);
+  if (it != h.codecs.end()) return it->second;
+  gs_codec* c = nullptr;
+  if (lost)
+    check(gs_decoder_create(static_cast<int>(s.kind), s.n, s.k, lost->data(), static_cast<int>(lost->size()), &c),
+          "reconstruct");
+  else
+    check(gs_encoder_create(static_cast<int>(s.kind), s.n, s.k, &c), "encode");
+  h.codecs.emplace(key, c);
+  return c;
+}
+
+}  // namespace detail
+
+// coding.hpp:313-330
+inline std::vector<std::vector<std::uint8_t>> encode(const CodingScheme& scheme,
+                                                     std::span<const ConstShardSpan> data) {
+  scheme.validate();
+  if (static_cast<int>(data.size()) != scheme.n)
+    throw std::invalid_argument("coding: expected " + std::to_string(scheme.n) + " data shards, got " +
+                                std::to_string(data.size()));
+  for (std::size_t i = 1; i < data.size(); ++i)
+    if (data[i].size() != data[0].size())
+      throw std::invalid_argument("coding: shard buffers must all have the same length");
+  const std::size_t len = data.empty() ? 0 : data[0].size();
+  std::vector<std::vector<std::uint8_t>> parity(static_cast<std::size_t>(scheme.k));
+  for (auto& p : parity) p.assign(len, 0);
+  if (len == 0) return parity;
+  std::lock_guard<std::mutex> lk(detail::handles().mu);
+  gs_codec* c = detail::codec(scheme, nullptr);
+  std::vector<const void*> in;
+  std::vector<void*> out;
+  for (const auto& d : data) in.push_back(d.data());
+  for (auto& p : parity) out.push_back(p.data());
+  detail::check(gs_encode_host(detail::pipeline(), c, in.data(), out.data(), len), "encode");
+  return parity;
+}
+
+// coding.hpp:332-336
+inline std::vector<std::vector<std::uint8_t>> encode(const CodingScheme& scheme,
+                                                     const std::vector<std::vector<std::uint8_t>>& data) {
+  std::vector<ConstShardSpan> spans(data.begin(), data.end());
+  return encode(scheme, spans);
+}
+
+// coding.hpp:458-571
+inline std::map<int, std::vector<std::uint8_t>> reconstruct(const CodingScheme& scheme,
+                                                            const std::map<int, ConstShardSpan>& surviving,
+                                                            const ErasurePattern& lost) {
+  scheme.validate();
+  const int total = scheme.n + scheme.k;
+  for (int idx : lost.lost)
+    if (idx < 0 || idx >= total) throw std::invalid_argument("coding: lost shard index out of range");
+  if (static_cast<int>(lost.lost.size()) > max_tolerance(scheme))
+    throw UnrecoverableError("coding: " + std::to_string(lost.lost.size()) + " erasures exceed tolerance " +
+                             std::to_string(max_tolerance(scheme)) + " for scheme " + to_string(scheme.kind));
+  std::size_t len = 0;
+  bool have = false;
+  std::vector<const void*> slots(static_cast<std::size_t>(total), nullptr);
+  for (int idx = 0; idx < total; ++idx) {
+    if (lost.contains(idx)) continue;
+    auto it = surviving.find(idx);
+    if (it == surviving.end())
+      throw std::invalid_argument("coding: surviving shard " + std::to_string(idx) + " missing from input");
+    if (!have) {
+      len = it->second.size();
+      have = true;
+    } else if (it->second.size() != len) {
+      throw std::invalid_argument("coding: shard buffers must all have the same length");
+    }
+    slots[static_cast<std::size_t>(idx)] = it->second.data();
+  }
+  std::map<int, std::vector<std::uint8_t>> out;
+  std::lock_guard<std::mutex> lk(detail::handles().mu);
+  gs_codec* c = detail::codec(scheme, &lost.lost);
+  int n_out = 0;
+  std::vector<int> idx(256);
+  detail::check(gs_codec_info(c, &n_out, idx.data(), nullptr, nullptr), "reconstruct");
+  if (n_out == 0) return out;
+  std::vector<void*> dst;
+  for (int i = 0; i < n_out; ++i) {
+    auto& v = out[idx[static_cast<std::size_t>(i)]];
+    v.assign(len, 0);
+  }
+  for (int i = 0; i < n_out; ++i) dst.push_back(out[idx[static_cast<std::size_t>(i)]].data());
+  if (len) detail::check(gs_reconstruct_host(detail::pipeline(), c, slots.data(), dst.data(), len), "reconstruct");
+  return out;
+}
+
+}  // namespace ghostserve_gpu

@@ -1,0 +1,182 @@
+/*
+ * gs_capi.h -- C ABI of the B200-native GhostServe shadow-checkpointing byte
+ * path (libghostserve_b200.so). Plain pointers and sizes only: no C++ or
+ * torch types cross this boundary, no exceptions escape it.
+ *
+ * Each entry point names the reference interface it replaces
+ * (/root/reference/proj/include/ghostserve/...). The reference API itself is
+ * mirrored on top of this ABI by include/ghostserve_gpu/coding.hpp (C++) and
+ * paper_2605_00831_b200/coding.py (Python); see INTEGRATION.md.
+ *
+ * Conventions
+ *  - Return value: gs_status. GS_OK = 0. The message for the last failure on
+ *    the calling thread is gs_last_error().
+ *  - Status <-> reference exception: GS_INVALID_ARGUMENT = std::invalid_argument,
+ *    GS_UNRECOVERABLE = ghostserve::UnrecoverableError, GS_DOMAIN_ERROR =
+ *    std::domain_error, GS_CUDA_ERROR / GS_UNSUPPORTED have no reference twin.
+ *  - Shard numbering is the reference's: data shards 0..n-1, parity shards
+ *    n..n+k-1 (coding.hpp:126-137, recovery.hpp:117-121).
+ *  - "stream" arguments are cudaStream_t passed as void* (NULL = legacy
+ *    default stream); they are caller-owned.
+ *  - Device pointers may point into a peer GPU's memory (cudaIpcOpenMemHandle
+ *    or peer access enabled): kernels then load/store over NVLink directly.
+ *  - There is no CPU fallback: every byte of parity or rebuilt KV comes out of
+ *    a CUDA kernel. Without a CUDA device the compute calls return
+ *    GS_CUDA_ERROR.
+ */
+#ifndef GS_CAPI_H
+#define GS_CAPI_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+  GS_OK = 0,
+  GS_INVALID_ARGUMENT = 1,
+  GS_UNRECOVERABLE = 2,
+  GS_DOMAIN_ERROR = 3,
+  GS_CUDA_ERROR = 4,
+  GS_UNSUPPORTED = 5
+} gs_status;
+
+/* CodeKind (coding.hpp:19). RDP is out of scope on this path: accepted by
+ * validation, rejected with GS_UNSUPPORTED by codec creation. */
+typedef enum { GS_XOR = 0, GS_RDP = 1, GS_RS = 2 } gs_code_kind;
+
+typedef struct gs_codec gs_codec;       /* immutable coefficient plan + kernel choice */
+typedef struct gs_pipeline gs_pipeline; /* per-device staging ring + events for host-link overlap */
+
+/* ---- diagnostics ------------------------------------------------------- */
+const char* gs_status_string(int status);
+const char* gs_last_error(void);
+int gs_abi_version(void);
+/* Number of kernels this library launched in this process (all devices). */
+uint64_t gs_kernel_launches(void);
+/* 1 if a CUDA device is usable from this process. */
+int gs_cuda_available(void);
+
+/* ---- GF(2^8) and scheme (host) ----------------------------------------- */
+/* gf256.hpp:42-61 */
+uint8_t gs_gf_mul(uint8_t a, uint8_t b);
+int gs_gf_inv(uint8_t a, uint8_t* out);            /* GS_DOMAIN_ERROR for 0 */
+int gs_gf_div(uint8_t a, uint8_t b, uint8_t* out); /* GS_DOMAIN_ERROR for b == 0 */
+/* CodingScheme::validate (coding.hpp:44-60) */
+int gs_scheme_validate(int kind, int n, int k);
+/* max_tolerance (coding.hpp:69-76); -1 for an unknown kind */
+int gs_max_tolerance(int kind, int n, int k);
+/* build_encoding_matrix (coding.hpp:96-118): k*n row-major into coef */
+int gs_encoding_matrix(int kind, int n, int k, uint8_t* coef);
+
+/* ---- codecs ---------------------------------------------------------------
+ * Encoder for a scheme: replaces the matrix build + dispatch of encode()
+ * (coding.hpp:313-336, 269-275). Outputs = k parity shards. */
+int gs_encoder_create(int kind, int n, int k, gs_codec** out);
+/* Decoder for (scheme, erasure pattern): replaces the per-call planning in
+ * reconstruct() (coding.hpp:458-571): validation, tolerance, row choice
+ * (:540-544), e x e Gauss-Jordan inverse on the HOST (:545-551, 187-223)
+ * and coefficient folding (:554-566). `lost` is deduplicated like
+ * ErasurePattern (:131-134). Outputs = the lost DATA shards, ascending. */
+int gs_decoder_create(int kind, int n, int k, const int* lost, int n_lost, gs_codec** out);
+/* Same, with flags: GS_FLAG_DECODER selects gs_decoder_create semantics,
+ * GS_FLAG_GENERIC forces the runtime-coefficient kernel (used by the tests
+ * to cross-check the two kernel back ends). */
+#define GS_FLAG_GENERIC 1
+#define GS_FLAG_DECODER 2
+int gs_codec_create_ex(int kind, int n, int k, const int* lost, int n_lost, int flags, gs_codec** out);
+int gs_codec_destroy(gs_codec* c);
+/* Shape of a codec: number of outputs and, per output, the shard index it
+ * produces; number of shard slots it reads (n for encoders, n+k for
+ * decoders); 1 in *specialised when a compile-time kernel serves it. */
+int gs_codec_info(const gs_codec* c, int* n_out, int* out_index, int* n_slots,
+                  int* specialised);
+/* Coefficients as applied: n_out x n_slots row-major (0 = slot unused). */
+int gs_codec_coefficients(const gs_codec* c, uint8_t* coef);
+
+/* ---- device path (K1 / K2), asynchronous on `stream` ----------------------
+ * Applies the codec to n_stripes independent stripes of `len` bytes each.
+ *  slots[s * n_slots + j] : device pointer of shard slot j of stripe s
+ *                           (encoder: data 0..n-1; decoder: shard index
+ *                           0..n+k-1, NULL allowed for lost / unused slots)
+ *  outs[s * n_out + i]    : device pointer receiving output i of stripe s
+ * Replaces encode() (coding.hpp:313) / reconstruct() (:458) byte loops. */
+int gs_apply_device(const gs_codec* c, int n_stripes, const void* const* slots,
+                    void* const* outs, size_t len, void* stream);
+
+/* ---- host-link pipelines ----------------------------------------------------
+ * A pipeline owns device staging (`staging_bytes`, split into a ring) and
+ * events on `device`. Not thread-safe; one per (device, caller thread). */
+int gs_pipeline_create(int device, size_t staging_bytes, gs_pipeline** out);
+int gs_pipeline_destroy(gs_pipeline* p);
+
+/* Checkpoint offload (PAPER Alg.1 / checkpoint.hpp:143-146 + the host tier of
+ * parity_store.hpp:77-90): encode device-resident data into staging on
+ * `compute`, D2H each finished piece to `h_parity` (pinned host; k per
+ * stripe) on `copy`, pieces overlapped. Returns once work is ENQUEUED;
+ * completion = `copy` stream. */
+int gs_encode_offload(gs_pipeline* p, const gs_codec* enc, int n_stripes,
+                      const void* const* d_data, void* const* h_parity, size_t len,
+                      void* compute, void* copy);
+
+/* Recovery upload (recovery.hpp:100-133 byte path): parity slots of `slots`
+ * are HOST pointers (pinned), data slots DEVICE pointers (local or peer).
+ * Used parity rows are H2D'd piecewise on `copy` into staging; the rebuild
+ * kernel runs per piece on `compute` and writes `outs` (device, may be a
+ * peer's KV buffer). Returns once enqueued; completion = `compute`. */
+int gs_reconstruct_upload(gs_pipeline* p, const gs_codec* dec, int n_stripes,
+                          const void* const* slots, void* const* outs, size_t len,
+                          void* compute, void* copy);
+
+/* Drop-in host-buffer calls (synchronous): the byte semantics of
+ * ghostserve::encode (coding.hpp:313) and ghostserve::reconstruct (:458) with
+ * host inputs and outputs; H2D, kernel and D2H overlapped through `p`.
+ * For reconstruct, slots are host pointers (n+k, NULL for lost). */
+int gs_encode_host(gs_pipeline* p, const gs_codec* enc, const void* const* h_data,
+                   void* const* h_parity, size_t len);
+int gs_reconstruct_host(gs_pipeline* p, const gs_codec* dec, const void* const* h_slots,
+                        void* const* h_out, size_t len);
+
+/* ---- KV data model (kv_layout.hpp) ------------------------------------- */
+/* slice_bytes (kv_layout.hpp:40-45), validate (:21-28) */
+int gs_slice_bytes(int layers, int kv_heads, int head_dim, int tp, uint32_t chunk_size,
+                   uint64_t* out);
+/* make_ground_truth_slice (kv_layout.hpp:110-134) generated on the device,
+ * bit-identical to the reference stream, pad_partial included. */
+int gs_ground_truth_slice_device(uint64_t kv_seed, uint64_t request_id, uint32_t chunk,
+                                 int worker, int layers, int kv_heads, int head_dim, int tp,
+                                 uint32_t chunk_size, uint32_t valid_tokens, void* d_out,
+                                 void* stream);
+/* pad_partial (kv_layout.hpp:73-84) on a device slice */
+int gs_pad_partial_device(void* d_slice, int layers, int kv_heads, int head_dim, int tp,
+                          uint32_t chunk_size, uint32_t valid_tokens, void* stream);
+
+/* ---- parity seal (parity_store.hpp:19-53), host ------------------------ */
+uint64_t gs_fnv1a64(const void* bytes, size_t len, uint64_t h);
+/* ParityChunk::compute_checksum: FNV-1a chained over k buffers in order */
+uint64_t gs_parity_checksum(const void* const* parity, int k, size_t len);
+/* Seal many chunks concurrently on up to `threads` host threads:
+ * out[c] = checksum of parity[c*k .. c*k+k-1]. */
+int gs_parity_checksum_batch(const void* const* parity, int n_chunks, int k, size_t len,
+                             int threads, uint64_t* out);
+
+/* ---- peer memory over NVLink (multi-GPU striping) ---------------------- */
+#define GS_IPC_HANDLE_BYTES 64
+int gs_ipc_handle(const void* d_ptr, void* handle_out /* 64 bytes */);
+int gs_ipc_open(const void* handle, int device, void** d_ptr);
+int gs_ipc_close(void* d_ptr);
+int gs_peer_enable(int device, int peer);
+/* Byte range [*off, *off + *len) of a shard of `total` bytes owned by rank
+ * `rank` of `world` when the range is striped 4 KiB-aligned. */
+int gs_stripe_range(uint64_t total, int rank, int world, uint64_t* off, uint64_t* len);
+
+/* ---- pinned host memory for the parity host tier ----------------------- */
+int gs_host_alloc(size_t bytes, void** out);
+int gs_host_free(void* p);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* GS_CAPI_H */

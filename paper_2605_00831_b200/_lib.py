@@ -1,0 +1,105 @@
+"""ctypes binding of libghostserve_b200.so (include/gs_capi.h).
+
+The library is built in-tree by ``make -C paper_2605_00831_b200/csrc`` (or
+``__graft_entry__.build()``). Loading fails loudly when it is missing: there
+is no CPU fallback anywhere in this package.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+import threading
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "_lib", "libghostserve_b200.so")
+
+GS_OK, GS_INVALID_ARGUMENT, GS_UNRECOVERABLE, GS_DOMAIN_ERROR, GS_CUDA_ERROR, GS_UNSUPPORTED = range(6)
+GS_XOR, GS_RDP, GS_RS = 0, 1, 2
+IPC_HANDLE_BYTES = 64
+
+# Every symbol include/gs_capi.h declares: (name, restype, argtypes).
+_vp, _vpp, _i, _sz, _u8, _u32, _u64 = (C.c_void_p, C.POINTER(C.c_void_p), C.c_int, C.c_size_t,
+                                       C.c_uint8, C.c_uint32, C.c_uint64)
+_ip = C.POINTER(C.c_int)
+_u8p = C.POINTER(C.c_uint8)
+_u64p = C.POINTER(C.c_uint64)
+SIGNATURES = {
+    "gs_status_string": (C.c_char_p, [_i]),
+    "gs_last_error": (C.c_char_p, []),
+    "gs_abi_version": (_i, []),
+    "gs_kernel_launches": (_u64, []),
+    "gs_cuda_available": (_i, []),
+    "gs_gf_mul": (_u8, [_u8, _u8]),
+    "gs_gf_inv": (_i, [_u8, _u8p]),
+    "gs_gf_div": (_i, [_u8, _u8, _u8p]),
+    "gs_scheme_validate": (_i, [_i, _i, _i]),
+    "gs_max_tolerance": (_i, [_i, _i, _i]),
+    "gs_encoding_matrix": (_i, [_i, _i, _i, _u8p]),
+    "gs_encoder_create": (_i, [_i, _i, _i, _vpp]),
+    "gs_decoder_create": (_i, [_i, _i, _i, _ip, _i, _vpp]),
+    "gs_codec_create_ex": (_i, [_i, _i, _i, _ip, _i, _i, _vpp]),
+    "gs_codec_destroy": (_i, [_vp]),
+    "gs_codec_info": (_i, [_vp, _ip, _ip, _ip, _ip]),
+    "gs_codec_coefficients": (_i, [_vp, _u8p]),
+    "gs_apply_device": (_i, [_vp, _i, _vpp, _vpp, _sz, _vp]),
+    "gs_pipeline_create": (_i, [_i, _sz, _vpp]),
+    "gs_pipeline_destroy": (_i, [_vp]),
+    "gs_encode_offload": (_i, [_vp, _vp, _i, _vpp, _vpp, _sz, _vp, _vp]),
+    "gs_reconstruct_upload": (_i, [_vp, _vp, _i, _vpp, _vpp, _sz, _vp, _vp]),
+    "gs_encode_host": (_i, [_vp, _vp, _vpp, _vpp, _sz]),
+    "gs_reconstruct_host": (_i, [_vp, _vp, _vpp, _vpp, _sz]),
+    "gs_slice_bytes": (_i, [_i, _i, _i, _i, _u32, _u64p]),
+    "gs_ground_truth_slice_device": (_i, [_u64, _u64, _u32, _i, _i, _i, _i, _i, _u32, _u32, _vp, _vp]),
+    "gs_pad_partial_device": (_i, [_vp, _i, _i, _i, _i, _u32, _u32, _vp]),
+    "gs_fnv1a64": (_u64, [_vp, _sz, _u64]),
+    "gs_parity_checksum": (_u64, [_vpp, _i, _sz]),
+    "gs_parity_checksum_batch": (_i, [_vpp, _i, _i, _sz, _i, _u64p]),
+    "gs_ipc_handle": (_i, [_vp, _vp]),
+    "gs_ipc_open": (_i, [_vp, _i, _vpp]),
+    "gs_ipc_close": (_i, [_vp]),
+    "gs_peer_enable": (_i, [_i, _i]),
+    "gs_stripe_range": (_i, [_u64, _i, _i, _u64p, _u64p]),
+    "gs_host_alloc": (_i, [_sz, _vpp]),
+    "gs_host_free": (_i, [_vp]),
+}
+
+_lib = None
+_lock = threading.Lock()
+
+
+class GhostServeError(Exception):
+    """Base of the errors raised from C-ABI status codes."""
+
+    status = -1
+
+
+def lib() -> C.CDLL:
+    """Load (once) and return the native library; raise if it is missing."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    with _lock:
+        if _lib is None:
+            if not os.path.exists(LIB_PATH):
+                raise ImportError(
+                    f"libghostserve_b200.so not built at {LIB_PATH}; run "
+                    "`make -C paper_2605_00831_b200/csrc` (no CPU fallback exists)")
+            handle = C.CDLL(LIB_PATH)
+            for name, (res, args) in SIGNATURES.items():
+                fn = getattr(handle, name)
+                fn.restype = res
+                fn.argtypes = args
+            _lib = handle
+    return _lib
+
+
+def last_error() -> str:
+    msg = lib().gs_last_error()
+    return msg.decode() if msg else ""
+
+
+def ptr_array(values):
+    arr = (C.c_void_p * max(len(values), 1))()
+    for i, v in enumerate(values):
+        arr[i] = v
+    return arr

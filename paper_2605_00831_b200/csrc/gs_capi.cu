@@ -1,0 +1,1019 @@
+// gs_capi.cu -- host side of libghostserve_b200.so: the C ABI of
+// include/gs_capi.h. Coefficient planning (Cauchy matrix, decode-matrix
+// inversion) happens here on the host; every byte of parity / rebuilt KV is
+// produced by the kernels of gs_kernels.cuh / gs_special.cuh.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <atomic>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <map>
+#include <mutex>
+#include <string>
+#include <thread>
+#include <vector>
+
+#include "../../include/gs_capi.h"
+#include "gs_field.hpp"
+#include "gs_kernels.cuh"
+#include "gs_kv.cuh"
+#include "gs_special.cuh"
+
+namespace gsb {
+int special_encoders(SpecialEntry* out);
+int special_decoders_kxor_2_1(SpecialEntry* out);
+int special_decoders_kxor_4_1(SpecialEntry* out);
+int special_decoders_kxor_8_1(SpecialEntry* out);
+int special_decoders_kreedsolomon_4_1(SpecialEntry* out);
+int special_decoders_kreedsolomon_4_2(SpecialEntry* out);
+int special_decoders_kreedsolomon_6_2(SpecialEntry* out);
+int special_decoders_kreedsolomon_8_2(SpecialEntry* out);
+}  // namespace gsb
+
+using namespace gsb;
+
+// ============================================================================
+// errors
+// ============================================================================
+namespace {
+
+thread_local std::string g_err;
+std::atomic<uint64_t> g_launches{0};
+
+int fail(int status, const char* fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  std::vsnprintf(buf, sizeof buf, fmt, ap);
+  va_end(ap);
+  g_err = buf;
+  return status;
+}
+
+#define GS_CUDA(call)                                                                   \
+  do {                                                                                  \
+    cudaError_t e_ = (call);                                                            \
+    if (e_ != cudaSuccess)                                                              \
+      return fail(GS_CUDA_ERROR, "%s failed: %s (%s:%d)", #call, cudaGetErrorString(e_), \
+                  __FILE__, __LINE__);                                                  \
+  } while (0)
+
+int validate_scheme(int kind, int n, int k) {
+  // coding.hpp:44-60, same order of checks and the same outcome classes.
+  if (n < 1) return fail(GS_INVALID_ARGUMENT, "coding: data shard count must be positive");
+  if (k < 1) return fail(GS_INVALID_ARGUMENT, "coding: parity shard count must be positive");
+  if (n + k > 255)
+    return fail(GS_INVALID_ARGUMENT, "coding: n + k exceeds the GF(2^8) bound of 255");
+  switch (kind) {
+    case GS_XOR:
+      if (k != 1) return fail(GS_INVALID_ARGUMENT, "coding: xor requires exactly one parity shard");
+      return GS_OK;
+    case GS_RDP:
+      if (k != 2) return fail(GS_INVALID_ARGUMENT, "coding: rdp requires exactly two parity shards");
+      return GS_OK;
+    case GS_RS:
+      if (k > n) return fail(GS_INVALID_ARGUMENT, "coding: reed-solomon requires k <= n");
+      return GS_OK;
+    default:
+      return fail(GS_INVALID_ARGUMENT, "coding: unknown code kind %d", kind);
+  }
+}
+
+int tolerance(int kind, int k) { return kind == GS_XOR ? 1 : kind == GS_RDP ? 2 : k; }
+
+// Per-device properties cached once.
+struct DeviceInfo {
+  int sms = 0;
+};
+std::mutex g_dev_mu;
+std::map<int, DeviceInfo> g_dev;
+std::map<std::pair<int, const void*>, int> g_occ;  // (device, kernel) -> blocks per SM
+
+int device_sms(int dev) {
+  std::lock_guard<std::mutex> lk(g_dev_mu);
+  auto it = g_dev.find(dev);
+  if (it != g_dev.end()) return it->second.sms;
+  int sms = 0;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  g_dev[dev].sms = sms > 0 ? sms : 148;
+  return g_dev[dev].sms;
+}
+
+int blocks_per_sm(int dev, const void* kernel, size_t smem) {
+  std::lock_guard<std::mutex> lk(g_dev_mu);
+  auto key = std::make_pair(dev, kernel);
+  auto it = g_occ.find(key);
+  if (it != g_occ.end()) return it->second;
+  int b = 0;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, kernel, kThreads, smem) != cudaSuccess || b < 1)
+    b = 1;
+  g_occ[key] = b;
+  return b;
+}
+
+// Registry of compile-time kernels, built once.
+struct Registry {
+  std::vector<SpecialEntry> entries;
+  Registry() {
+    std::vector<SpecialEntry> buf(4096);
+    int c = 0;
+    c += special_encoders(buf.data() + c);
+    c += special_decoders_kxor_2_1(buf.data() + c);
+    c += special_decoders_kxor_4_1(buf.data() + c);
+    c += special_decoders_kxor_8_1(buf.data() + c);
+    c += special_decoders_kreedsolomon_4_1(buf.data() + c);
+    c += special_decoders_kreedsolomon_4_2(buf.data() + c);
+    c += special_decoders_kreedsolomon_6_2(buf.data() + c);
+    c += special_decoders_kreedsolomon_8_2(buf.data() + c);
+    entries.assign(buf.begin(), buf.begin() + c);
+  }
+  const SpecialEntry* find(bool decoder, int kind, int n, int k, uint64_t mask) const {
+    for (const auto& e : entries)
+      if (e.decoder == decoder && e.kind == kind && e.n == n && e.k == k && e.mask == mask) return &e;
+    return nullptr;
+  }
+};
+
+const Registry& registry() {
+  static const Registry r;
+  return r;
+}
+
+}  // namespace
+
+// ============================================================================
+// codec
+// ============================================================================
+struct gs_codec {
+  bool decoder = false;
+  int kind = 0, n = 0, k = 0;
+  int n_out = 0;                 // outputs produced
+  int n_slots = 0;               // shard slots read (n or n+k)
+  std::vector<int> out_index;    // shard index per output
+  std::vector<uint8_t> coef;     // n_out x n_slots
+  std::vector<int> used;         // slots with a nonzero coefficient (generic path)
+  const SpecialEntry* special = nullptr;
+  std::vector<CoefWords> words;  // n_out x used.size(), generic path table
+  mutable std::mutex mu;
+  mutable std::map<int, CoefWords*> dev_words;  // device -> uploaded table
+
+  ~gs_codec() {
+    for (auto& kv : dev_words) {
+      int prev = 0;
+      cudaGetDevice(&prev);
+      cudaSetDevice(kv.first);
+      cudaFree(kv.second);
+      cudaSetDevice(prev);
+    }
+  }
+};
+
+namespace {
+
+void finish_codec(gs_codec* c) {
+  for (int j = 0; j < c->n_slots; ++j) {
+    bool any = false;
+    for (int i = 0; i < c->n_out; ++i) any |= c->coef[static_cast<size_t>(i) * c->n_slots + j] != 0;
+    if (any) c->used.push_back(j);
+  }
+  c->words.resize(static_cast<size_t>(c->n_out) * c->used.size());
+  for (int i = 0; i < c->n_out; ++i)
+    for (size_t u = 0; u < c->used.size(); ++u)
+      c->words[static_cast<size_t>(i) * c->used.size() + u] =
+          make_coef_words(c->coef[static_cast<size_t>(i) * c->n_slots + c->used[u]]);
+}
+
+// coding.hpp:187-223 (Gauss-Jordan over GF(2^8)); false if singular.
+bool invert(std::vector<uint8_t> m, int dim, std::vector<uint8_t>& out) {
+  out.assign(static_cast<size_t>(dim) * dim, 0);
+  for (int i = 0; i < dim; ++i) out[static_cast<size_t>(i) * dim + i] = 1;
+  auto at = [dim](std::vector<uint8_t>& v, int r, int c) -> uint8_t& {
+    return v[static_cast<size_t>(r) * dim + c];
+  };
+  for (int col = 0; col < dim; ++col) {
+    int piv = -1;
+    for (int r = col; r < dim && piv < 0; ++r)
+      if (at(m, r, col)) piv = r;
+    if (piv < 0) return false;
+    if (piv != col)
+      for (int c = 0; c < dim; ++c) {
+        std::swap(at(m, piv, c), at(m, col, c));
+        std::swap(at(out, piv, c), at(out, col, c));
+      }
+    const uint8_t pi = gf_inv(at(m, col, col));
+    for (int c = 0; c < dim; ++c) {
+      at(m, col, c) = gf_mul(at(m, col, c), pi);
+      at(out, col, c) = gf_mul(at(out, col, c), pi);
+    }
+    for (int r = 0; r < dim; ++r) {
+      if (r == col) continue;
+      const uint8_t f = at(m, r, col);
+      if (!f) continue;
+      for (int c = 0; c < dim; ++c) {
+        at(m, r, c) ^= gf_mul(f, at(m, col, c));
+        at(out, r, c) ^= gf_mul(f, at(out, col, c));
+      }
+    }
+  }
+  return true;
+}
+
+int current_device(int* dev) {
+  GS_CUDA(cudaGetDevice(dev));
+  return GS_OK;
+}
+
+int upload_words(const gs_codec* c, int dev, const CoefWords** out) {
+  std::lock_guard<std::mutex> lk(c->mu);
+  auto it = c->dev_words.find(dev);
+  if (it != c->dev_words.end()) {
+    *out = it->second;
+    return GS_OK;
+  }
+  CoefWords* d = nullptr;
+  const size_t bytes = std::max<size_t>(c->words.size(), 1) * sizeof(CoefWords);
+  GS_CUDA(cudaMalloc(&d, bytes));
+  GS_CUDA(cudaMemcpy(d, c->words.data(), c->words.size() * sizeof(CoefWords), cudaMemcpyHostToDevice));
+  c->dev_words[dev] = d;
+  *out = d;
+  return GS_OK;
+}
+
+bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
+
+template <int KB>
+cudaError_t launch_generic_kb(const void* const* ptrs, int count, const TileGeom& g, int grid,
+                              cudaStream_t st, const CoefWords* coef, int ns) {
+  PtrTable<kPtrCap> tab;
+  for (int i = 0; i < count; ++i) tab.p[i] = static_cast<const uint8_t*>(ptrs[i]);
+  const size_t smem = static_cast<size_t>(KB) * ns * sizeof(CoefWords);
+  k_apply_generic<KB, kPtrCap><<<grid, kThreads, smem, st>>>(tab, g, coef, ns);
+  return cudaGetLastError();
+}
+
+const void* generic_kernel(int kb) {
+  switch (kb) {
+    case 1: return reinterpret_cast<const void*>(&k_apply_generic<1, kPtrCap>);
+    case 2: return reinterpret_cast<const void*>(&k_apply_generic<2, kPtrCap>);
+    case 3: return reinterpret_cast<const void*>(&k_apply_generic<3, kPtrCap>);
+    default: return reinterpret_cast<const void*>(&k_apply_generic<4, kPtrCap>);
+  }
+}
+
+// Launch the codec over stripes. slot_ptr(s, j) / out_ptr(s, i) give the
+// (already offset) pointers; every stripe has `len` bytes.
+template <class SlotFn, class OutFn>
+int run_codec(const gs_codec* c, int n_stripes, SlotFn slot_ptr, OutFn out_ptr, uint64_t len,
+              cudaStream_t st) {
+  if (len == 0 || n_stripes == 0 || c->n_out == 0) return GS_OK;
+  int dev = 0;
+  if (int s = current_device(&dev)) return s;
+  const int sms = device_sms(dev);
+
+  bool aligned = true;
+  for (int s = 0; s < n_stripes; ++s) {
+    for (int j : c->used) {
+      const void* p = slot_ptr(s, j);
+      if (p == nullptr)
+        return fail(GS_INVALID_ARGUMENT, "apply: shard slot %d of stripe %d is NULL but required", j, s);
+      aligned &= aligned16(p);
+    }
+    for (int i = 0; i < c->n_out; ++i) {
+      const void* p = out_ptr(s, i);
+      if (p == nullptr) return fail(GS_INVALID_ARGUMENT, "apply: output %d of stripe %d is NULL", i, s);
+      aligned &= aligned16(p);
+    }
+  }
+  const uint64_t tps64 = (len + kTile - 1) / kTile;
+  std::vector<const void*> ptrs;
+
+  if (c->special) {
+    const int stride = c->n_slots + c->n_out;
+    const int per = kPtrCap / stride;
+    const int occ = blocks_per_sm(dev, c->special->kernel, 0);
+    for (int s0 = 0; s0 < n_stripes; s0 += per) {
+      const int cnt = std::min(per, n_stripes - s0);
+      ptrs.assign(static_cast<size_t>(cnt) * stride, nullptr);
+      for (int s = 0; s < cnt; ++s) {
+        for (int j = 0; j < c->n_slots; ++j) ptrs[s * stride + j] = slot_ptr(s0 + s, j);
+        for (int i = 0; i < c->n_out; ++i) ptrs[s * stride + c->n_slots + i] = out_ptr(s0 + s, i);
+      }
+      const uint64_t total = tps64 * cnt;
+      if (total > 0xFFFFFFFFull) return fail(GS_INVALID_ARGUMENT, "apply: too many tiles in one launch");
+      TileGeom g{len, static_cast<uint32_t>(tps64), static_cast<uint32_t>(total), stride, c->n_slots,
+                 aligned ? 1 : 0};
+      const int grid = static_cast<int>(std::min<uint64_t>(total, static_cast<uint64_t>(occ) * sms));
+      cudaError_t e = c->special->launch(ptrs.data(), cnt * stride, g, grid, st);
+      if (e != cudaSuccess) return fail(GS_CUDA_ERROR, "special kernel launch: %s", cudaGetErrorString(e));
+      g_launches.fetch_add(1, std::memory_order_relaxed);
+    }
+    return GS_OK;
+  }
+
+  const CoefWords* dw = nullptr;
+  if (int s = upload_words(c, dev, &dw)) return s;
+  const int ns = static_cast<int>(c->used.size());
+  const int stride = ns + c->n_out;
+  const int per = kPtrCap / stride;
+  if (per < 1) return fail(GS_INVALID_ARGUMENT, "apply: stripe needs %d pointers (> %d)", stride, kPtrCap);
+  for (int s0 = 0; s0 < n_stripes; s0 += per) {
+    const int cnt = std::min(per, n_stripes - s0);
+    ptrs.assign(static_cast<size_t>(cnt) * stride, nullptr);
+    for (int s = 0; s < cnt; ++s) {
+      for (int u = 0; u < ns; ++u) ptrs[s * stride + u] = slot_ptr(s0 + s, c->used[u]);
+      for (int i = 0; i < c->n_out; ++i) ptrs[s * stride + ns + i] = out_ptr(s0 + s, i);
+    }
+    const uint64_t total = tps64 * cnt;
+    if (total > 0xFFFFFFFFull) return fail(GS_INVALID_ARGUMENT, "apply: too many tiles in one launch");
+    for (int r0 = 0; r0 < c->n_out; r0 += kMaxGenericRows) {
+      const int kb = std::min(kMaxGenericRows, c->n_out - r0);
+      TileGeom g{len, static_cast<uint32_t>(tps64), static_cast<uint32_t>(total), stride, ns + r0,
+                 aligned ? 1 : 0};
+      const size_t smem = static_cast<size_t>(kb) * ns * sizeof(CoefWords);
+      const int occ = blocks_per_sm(dev, generic_kernel(kb), smem);
+      const int grid = static_cast<int>(std::min<uint64_t>(total, static_cast<uint64_t>(occ) * sms));
+      const CoefWords* cw = dw + static_cast<size_t>(r0) * ns;
+      cudaError_t e;
+      switch (kb) {
+        case 1: e = launch_generic_kb<1>(ptrs.data(), cnt * stride, g, grid, st, cw, ns); break;
+        case 2: e = launch_generic_kb<2>(ptrs.data(), cnt * stride, g, grid, st, cw, ns); break;
+        case 3: e = launch_generic_kb<3>(ptrs.data(), cnt * stride, g, grid, st, cw, ns); break;
+        default: e = launch_generic_kb<4>(ptrs.data(), cnt * stride, g, grid, st, cw, ns); break;
+      }
+      if (e != cudaSuccess) return fail(GS_CUDA_ERROR, "generic kernel launch: %s", cudaGetErrorString(e));
+      g_launches.fetch_add(1, std::memory_order_relaxed);
+    }
+  }
+  return GS_OK;
+}
+
+}  // namespace
+
+// ============================================================================
+// pipeline (staging ring for host-link overlap)
+// ============================================================================
+struct gs_pipeline {
+  int device = 0;
+  size_t bytes = 0;
+  uint8_t* staging = nullptr;
+  static constexpr int kSlots = 4;
+  cudaEvent_t ready[kSlots]{}, done[kSlots]{}, drained[kSlots]{};
+  cudaStream_t s_h2d = nullptr, s_comp = nullptr, s_d2h = nullptr;  // for the *_host calls
+  int next = 0;
+  size_t slot_bytes() const { return bytes / kSlots / 4096 * 4096; }
+};
+
+namespace {
+
+struct DeviceGuard {
+  int prev = -1;
+  explicit DeviceGuard(int dev) {
+    cudaGetDevice(&prev);
+    if (prev != dev) cudaSetDevice(dev);
+  }
+  ~DeviceGuard() {
+    int cur = -1;
+    cudaGetDevice(&cur);
+    if (prev >= 0 && cur != prev) cudaSetDevice(prev);
+  }
+};
+
+// Choose the byte range per piece: as large as the slot allows, at least one
+// 4 KiB tile, rounded to 4 KiB so every piece but the last stays aligned.
+uint64_t piece_len(uint64_t len, size_t slot, int per_byte) {
+  uint64_t r = slot / static_cast<uint64_t>(per_byte);
+  r = r / 4096 * 4096;
+  if (r == 0) r = 4096;
+  return std::min<uint64_t>(r, len);
+}
+
+// Copy a list of (dst, src, bytes) with adjacent runs merged.
+struct CopyOp {
+  uint8_t* dst;
+  const uint8_t* src;
+  size_t bytes;
+};
+
+int issue_copies(std::vector<CopyOp>& ops, cudaMemcpyKind kind, cudaStream_t st) {
+  size_t i = 0;
+  while (i < ops.size()) {
+    CopyOp cur = ops[i];
+    size_t j = i + 1;
+    while (j < ops.size() && ops[j].dst == cur.dst + cur.bytes && ops[j].src == cur.src + cur.bytes) {
+      cur.bytes += ops[j].bytes;
+      ++j;
+    }
+    if (cur.bytes) GS_CUDA(cudaMemcpyAsync(cur.dst, cur.src, cur.bytes, kind, st));
+    i = j;
+  }
+  ops.clear();
+  return GS_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+// ============================================================================
+// diagnostics
+// ============================================================================
+const char* gs_status_string(int status) {
+  switch (status) {
+    case GS_OK: return "ok";
+    case GS_INVALID_ARGUMENT: return "invalid argument";
+    case GS_UNRECOVERABLE: return "unrecoverable";
+    case GS_DOMAIN_ERROR: return "domain error";
+    case GS_CUDA_ERROR: return "cuda error";
+    case GS_UNSUPPORTED: return "unsupported";
+    default: return "unknown status";
+  }
+}
+const char* gs_last_error(void) { return g_err.c_str(); }
+int gs_abi_version(void) { return 1; }
+uint64_t gs_kernel_launches(void) { return g_launches.load(); }
+int gs_cuda_available(void) {
+  int n = 0;
+  return cudaGetDeviceCount(&n) == cudaSuccess && n > 0 ? 1 : 0;
+}
+
+// ============================================================================
+// field + scheme
+// ============================================================================
+uint8_t gs_gf_mul(uint8_t a, uint8_t b) { return gf_mul(a, b); }
+
+int gs_gf_inv(uint8_t a, uint8_t* out) {
+  if (a == 0) return fail(GS_DOMAIN_ERROR, "gf256: zero has no multiplicative inverse");
+  *out = gf_inv(a);
+  return GS_OK;
+}
+
+int gs_gf_div(uint8_t a, uint8_t b, uint8_t* out) {
+  if (b == 0) return fail(GS_DOMAIN_ERROR, "gf256: division by zero");
+  *out = a == 0 ? 0 : gf_mul(a, gf_inv(b));
+  return GS_OK;
+}
+
+int gs_scheme_validate(int kind, int n, int k) { return validate_scheme(kind, n, k); }
+
+int gs_max_tolerance(int kind, int n, int k) {
+  (void)n;
+  if (kind < GS_XOR || kind > GS_RS) return -1;
+  return tolerance(kind, k);
+}
+
+int gs_encoding_matrix(int kind, int n, int k, uint8_t* coef) {
+  if (int s = validate_scheme(kind, n, k)) return s;
+  for (int i = 0; i < k; ++i)
+    for (int j = 0; j < n; ++j)
+      coef[static_cast<size_t>(i) * n + j] = kind == GS_RS ? cauchy(k, i, j) : 1;
+  return GS_OK;
+}
+
+// ============================================================================
+// codecs
+// ============================================================================
+static int encoder_create(int kind, int n, int k, bool generic, gs_codec** out) {
+  if (!out) return fail(GS_INVALID_ARGUMENT, "encoder_create: out is NULL");
+  *out = nullptr;
+  if (int s = validate_scheme(kind, n, k)) return s;
+  if (kind == GS_RDP)
+    return fail(GS_UNSUPPORTED, "coding: rdp is not implemented on the GPU path (out of scope)");
+  auto* c = new gs_codec;
+  c->kind = kind;
+  c->n = n;
+  c->k = k;
+  c->n_out = k;
+  c->n_slots = n;
+  c->coef.resize(static_cast<size_t>(k) * n);
+  gs_encoding_matrix(kind, n, k, c->coef.data());
+  for (int i = 0; i < k; ++i) c->out_index.push_back(n + i);
+  c->special = generic ? nullptr : registry().find(false, kind, n, k, 0);
+  finish_codec(c);
+  *out = c;
+  return GS_OK;
+}
+
+static int decoder_create(int kind, int n, int k, const int* lost_in, int n_lost, bool generic,
+                          gs_codec** out) {
+  if (!out) return fail(GS_INVALID_ARGUMENT, "decoder_create: out is NULL");
+  *out = nullptr;
+  if (int s = validate_scheme(kind, n, k)) return s;
+  if (kind == GS_RDP)
+    return fail(GS_UNSUPPORTED, "coding: rdp is not implemented on the GPU path (out of scope)");
+  if (n_lost < 0 || (n_lost > 0 && lost_in == nullptr))
+    return fail(GS_INVALID_ARGUMENT, "decoder_create: bad lost list");
+  // ErasurePattern: sort + dedup (coding.hpp:131-134)
+  std::vector<int> lost(lost_in, lost_in + n_lost);
+  std::sort(lost.begin(), lost.end());
+  lost.erase(std::unique(lost.begin(), lost.end()), lost.end());
+  const int total = n + k;
+  for (int idx : lost)  // coding.hpp:463-465
+    if (idx < 0 || idx >= total) return fail(GS_INVALID_ARGUMENT, "coding: lost shard index out of range");
+  if (static_cast<int>(lost.size()) > tolerance(kind, k))  // :466-470
+    return fail(GS_UNRECOVERABLE, "coding: %zu erasures exceed tolerance %d for scheme %s", lost.size(),
+                tolerance(kind, k), kind == GS_XOR ? "xor" : "rs");
+  auto is_lost = [&](int idx) { return std::binary_search(lost.begin(), lost.end(), idx); };
+  std::vector<int> ld;
+  for (int idx : lost)
+    if (idx < n) ld.push_back(idx);
+  const int e = static_cast<int>(ld.size());
+
+  auto* c = new gs_codec;
+  c->decoder = true;
+  c->kind = kind;
+  c->n = n;
+  c->k = k;
+  c->n_out = e;
+  c->n_slots = total;
+  c->out_index = ld;
+  c->coef.assign(static_cast<size_t>(e) * total, 0);
+  if (e > 0) {
+    if (kind == GS_XOR) {  // coding.hpp:496-502
+      for (int s = 0; s < total; ++s)
+        if (!is_lost(s)) c->coef[s] = 1;
+    } else {  // coding.hpp:535-566
+      std::vector<int> rows;
+      for (int i = 0; i < k && static_cast<int>(rows.size()) < e; ++i)
+        if (!is_lost(n + i)) rows.push_back(i);
+      if (static_cast<int>(rows.size()) < e) {
+        delete c;
+        return fail(GS_UNRECOVERABLE, "coding: not enough surviving parity shards");
+      }
+      std::vector<uint8_t> sys(static_cast<size_t>(e) * e), inv;
+      for (int a = 0; a < e; ++a)
+        for (int b = 0; b < e; ++b) sys[static_cast<size_t>(a) * e + b] = cauchy(k, rows[a], ld[b]);
+      if (!invert(sys, e, inv)) {
+        delete c;
+        return fail(GS_UNRECOVERABLE, "coding: singular decode system");
+      }
+      for (int b = 0; b < e; ++b) {
+        for (int j = 0; j < n; ++j) {
+          if (is_lost(j)) continue;
+          uint8_t v = 0;
+          for (int a = 0; a < e; ++a) v ^= gf_mul(inv[static_cast<size_t>(b) * e + a], cauchy(k, rows[a], j));
+          c->coef[static_cast<size_t>(b) * total + j] = v;
+        }
+        for (int a = 0; a < e; ++a)
+          c->coef[static_cast<size_t>(b) * total + n + rows[a]] = inv[static_cast<size_t>(b) * e + a];
+      }
+    }
+    if (total <= 64 && !generic) {
+      uint64_t mask = 0;
+      for (int idx : lost) mask |= 1ull << idx;
+      c->special = registry().find(true, kind, n, k, canonical_mask(kind, n, k, mask));
+    }
+  }
+  finish_codec(c);
+  *out = c;
+  return GS_OK;
+}
+
+int gs_encoder_create(int kind, int n, int k, gs_codec** out) {
+  return encoder_create(kind, n, k, false, out);
+}
+
+int gs_decoder_create(int kind, int n, int k, const int* lost, int n_lost, gs_codec** out) {
+  return decoder_create(kind, n, k, lost, n_lost, false, out);
+}
+
+int gs_codec_create_ex(int kind, int n, int k, const int* lost, int n_lost, int flags, gs_codec** out) {
+  const bool generic = (flags & GS_FLAG_GENERIC) != 0;
+  if (flags & GS_FLAG_DECODER) return decoder_create(kind, n, k, lost, n_lost, generic, out);
+  return encoder_create(kind, n, k, generic, out);
+}
+
+int gs_codec_destroy(gs_codec* c) {
+  delete c;
+  return GS_OK;
+}
+
+int gs_codec_info(const gs_codec* c, int* n_out, int* out_index, int* n_slots, int* specialised) {
+  if (!c) return fail(GS_INVALID_ARGUMENT, "codec_info: NULL codec");
+  if (n_out) *n_out = c->n_out;
+  if (out_index)
+    for (int i = 0; i < c->n_out; ++i) out_index[i] = c->out_index[i];
+  if (n_slots) *n_slots = c->n_slots;
+  if (specialised) *specialised = c->special ? 1 : 0;
+  return GS_OK;
+}
+
+int gs_codec_coefficients(const gs_codec* c, uint8_t* coef) {
+  if (!c || !coef) return fail(GS_INVALID_ARGUMENT, "codec_coefficients: NULL argument");
+  std::memcpy(coef, c->coef.data(), c->coef.size());
+  return GS_OK;
+}
+
+// ============================================================================
+// device path
+// ============================================================================
+int gs_apply_device(const gs_codec* c, int n_stripes, const void* const* slots, void* const* outs,
+                    size_t len, void* stream) {
+  if (!c) return fail(GS_INVALID_ARGUMENT, "apply: NULL codec");
+  if (n_stripes < 0) return fail(GS_INVALID_ARGUMENT, "apply: negative stripe count");
+  if (len == 0 || n_stripes == 0 || c->n_out == 0) return GS_OK;
+  if (!slots || !outs) return fail(GS_INVALID_ARGUMENT, "apply: NULL pointer array");
+  auto slot = [&](int s, int j) -> const void* { return slots[static_cast<size_t>(s) * c->n_slots + j]; };
+  auto out = [&](int s, int i) -> const void* { return outs[static_cast<size_t>(s) * c->n_out + i]; };
+  return run_codec(c, n_stripes, slot, out, len, static_cast<cudaStream_t>(stream));
+}
+
+// ============================================================================
+// pipelines
+// ============================================================================
+int gs_pipeline_create(int device, size_t staging_bytes, gs_pipeline** out) {
+  if (!out) return fail(GS_INVALID_ARGUMENT, "pipeline_create: out is NULL");
+  *out = nullptr;
+  if (staging_bytes < gs_pipeline::kSlots * 4096ull)
+    return fail(GS_INVALID_ARGUMENT, "pipeline_create: staging must hold at least %d x 4 KiB",
+                gs_pipeline::kSlots);
+  DeviceGuard g(device);
+  auto* p = new gs_pipeline;
+  p->device = device;
+  p->bytes = staging_bytes;
+  cudaError_t e = cudaMalloc(&p->staging, staging_bytes);
+  if (e != cudaSuccess) {
+    delete p;
+    return fail(GS_CUDA_ERROR, "pipeline staging alloc (%zu B): %s", staging_bytes, cudaGetErrorString(e));
+  }
+  for (int i = 0; i < gs_pipeline::kSlots; ++i) {
+    cudaEventCreateWithFlags(&p->ready[i], cudaEventDisableTiming);
+    cudaEventCreateWithFlags(&p->done[i], cudaEventDisableTiming);
+    cudaEventCreateWithFlags(&p->drained[i], cudaEventDisableTiming);
+  }
+  cudaStreamCreateWithFlags(&p->s_h2d, cudaStreamNonBlocking);
+  cudaStreamCreateWithFlags(&p->s_comp, cudaStreamNonBlocking);
+  cudaStreamCreateWithFlags(&p->s_d2h, cudaStreamNonBlocking);
+  *out = p;
+  return GS_OK;
+}
+
+int gs_pipeline_destroy(gs_pipeline* p) {
+  if (!p) return GS_OK;
+  DeviceGuard g(p->device);
+  cudaDeviceSynchronize();
+  for (int i = 0; i < gs_pipeline::kSlots; ++i) {
+    cudaEventDestroy(p->ready[i]);
+    cudaEventDestroy(p->done[i]);
+    cudaEventDestroy(p->drained[i]);
+  }
+  cudaStreamDestroy(p->s_h2d);
+  cudaStreamDestroy(p->s_comp);
+  cudaStreamDestroy(p->s_d2h);
+  cudaFree(p->staging);
+  delete p;
+  return GS_OK;
+}
+
+// Encode device data, stage parity, D2H it piecewise (checkpoint offload).
+int gs_encode_offload(gs_pipeline* p, const gs_codec* c, int n_stripes, const void* const* d_data,
+                      void* const* h_parity, size_t len, void* compute, void* copy) {
+  if (!p || !c) return fail(GS_INVALID_ARGUMENT, "encode_offload: NULL pipeline/codec");
+  if (c->decoder) return fail(GS_INVALID_ARGUMENT, "encode_offload: codec is a decoder");
+  if (len == 0 || n_stripes == 0) return GS_OK;
+  if (!d_data || !h_parity) return fail(GS_INVALID_ARGUMENT, "encode_offload: NULL pointer array");
+  DeviceGuard g(p->device);
+  auto cs = static_cast<cudaStream_t>(compute);
+  auto ks = static_cast<cudaStream_t>(copy);
+  const int K = c->n_out, N = c->n_slots;
+  const size_t slot = p->slot_bytes();
+  const uint64_t rl_max = piece_len(len, slot, K);
+  std::vector<CopyOp> ops;
+  for (uint64_t r0 = 0; r0 < len; r0 += rl_max) {
+    const uint64_t rl = std::min<uint64_t>(rl_max, len - r0);
+    const int spp = static_cast<int>(std::max<uint64_t>(1, slot / (K * rl)));
+    for (int s0 = 0; s0 < n_stripes; s0 += spp) {
+      const int cnt = std::min(spp, n_stripes - s0);
+      const int sl = p->next;
+      p->next = (p->next + 1) % gs_pipeline::kSlots;
+      uint8_t* base = p->staging + static_cast<size_t>(sl) * slot;
+      GS_CUDA(cudaStreamWaitEvent(cs, p->drained[sl], 0));  // slot's previous D2H finished
+      auto src = [&](int s, int j) -> const void* {
+        return static_cast<const uint8_t*>(d_data[static_cast<size_t>(s0 + s) * N + j]) + r0;
+      };
+      auto dst = [&](int s, int i) -> const void* { return base + (static_cast<size_t>(s) * K + i) * rl; };
+      if (int st = run_codec(c, cnt, src, dst, rl, cs)) return st;
+      GS_CUDA(cudaEventRecord(p->done[sl], cs));
+      GS_CUDA(cudaStreamWaitEvent(ks, p->done[sl], 0));
+      for (int s = 0; s < cnt; ++s)
+        for (int i = 0; i < K; ++i)
+          ops.push_back({static_cast<uint8_t*>(h_parity[static_cast<size_t>(s0 + s) * K + i]) + r0,
+                         base + (static_cast<size_t>(s) * K + i) * rl, rl});
+      if (int st = issue_copies(ops, cudaMemcpyDeviceToHost, ks)) return st;
+      GS_CUDA(cudaEventRecord(p->drained[sl], ks));
+    }
+  }
+  return GS_OK;
+}
+
+// Rebuild lost shards: H2D used parity rows piecewise, rebuild per piece.
+int gs_reconstruct_upload(gs_pipeline* p, const gs_codec* c, int n_stripes, const void* const* slots,
+                          void* const* outs, size_t len, void* compute, void* copy) {
+  if (!p || !c) return fail(GS_INVALID_ARGUMENT, "reconstruct_upload: NULL pipeline/codec");
+  if (!c->decoder) return fail(GS_INVALID_ARGUMENT, "reconstruct_upload: codec is an encoder");
+  if (len == 0 || n_stripes == 0 || c->n_out == 0) return GS_OK;
+  if (!slots || !outs) return fail(GS_INVALID_ARGUMENT, "reconstruct_upload: NULL pointer array");
+  DeviceGuard g(p->device);
+  auto cs = static_cast<cudaStream_t>(compute);
+  auto ks = static_cast<cudaStream_t>(copy);
+  const int NS = c->n_slots, NO = c->n_out, n = c->n;
+  std::vector<int> host_slots;  // parity slots actually used
+  for (int j : c->used)
+    if (j >= n) host_slots.push_back(j);
+  const int H = std::max<int>(1, static_cast<int>(host_slots.size()));
+  const size_t slot = p->slot_bytes();
+  const uint64_t rl_max = piece_len(len, slot, H);
+  std::vector<CopyOp> ops;
+  for (uint64_t r0 = 0; r0 < len; r0 += rl_max) {
+    const uint64_t rl = std::min<uint64_t>(rl_max, len - r0);
+    const int spp = static_cast<int>(std::max<uint64_t>(1, slot / (H * rl)));
+    for (int s0 = 0; s0 < n_stripes; s0 += spp) {
+      const int cnt = std::min(spp, n_stripes - s0);
+      const int sl = p->next;
+      p->next = (p->next + 1) % gs_pipeline::kSlots;
+      uint8_t* base = p->staging + static_cast<size_t>(sl) * slot;
+      GS_CUDA(cudaStreamWaitEvent(ks, p->done[sl], 0));  // slot's previous kernel consumed it
+      for (int s = 0; s < cnt; ++s)
+        for (size_t h = 0; h < host_slots.size(); ++h) {
+          const void* hp = slots[static_cast<size_t>(s0 + s) * NS + host_slots[h]];
+          if (!hp) return fail(GS_INVALID_ARGUMENT, "reconstruct_upload: parity slot %d is NULL", host_slots[h]);
+          ops.push_back({base + (static_cast<size_t>(s) * H + h) * rl, static_cast<const uint8_t*>(hp) + r0, rl});
+        }
+      if (int st = issue_copies(ops, cudaMemcpyHostToDevice, ks)) return st;
+      GS_CUDA(cudaEventRecord(p->ready[sl], ks));
+      GS_CUDA(cudaStreamWaitEvent(cs, p->ready[sl], 0));
+      auto src = [&](int s, int j) -> const void* {
+        if (j >= n) {
+          const auto it = std::find(host_slots.begin(), host_slots.end(), j);
+          if (it == host_slots.end()) return nullptr;
+          return base + (static_cast<size_t>(s) * H + (it - host_slots.begin())) * rl;
+        }
+        const void* d = slots[static_cast<size_t>(s0 + s) * NS + j];
+        return d ? static_cast<const uint8_t*>(d) + r0 : nullptr;
+      };
+      auto dst = [&](int s, int i) -> const void* {
+        return static_cast<const uint8_t*>(outs[static_cast<size_t>(s0 + s) * NO + i]) + r0;
+      };
+      if (int st = run_codec(c, cnt, src, dst, rl, cs)) return st;
+      GS_CUDA(cudaEventRecord(p->done[sl], cs));
+    }
+  }
+  return GS_OK;
+}
+
+// Host buffers in, host buffers out: H2D data -> kernel -> D2H parity, per
+// piece, three streams so both copy directions and the kernel overlap.
+int gs_encode_host(gs_pipeline* p, const gs_codec* c, const void* const* h_data, void* const* h_parity,
+                   size_t len) {
+  if (!p || !c) return fail(GS_INVALID_ARGUMENT, "encode_host: NULL pipeline/codec");
+  if (c->decoder) return fail(GS_INVALID_ARGUMENT, "encode_host: codec is a decoder");
+  if (len == 0) return GS_OK;
+  if (!h_data || !h_parity) return fail(GS_INVALID_ARGUMENT, "encode_host: NULL pointer array");
+  for (int j = 0; j < c->n_slots; ++j)
+    if (!h_data[j]) return fail(GS_INVALID_ARGUMENT, "encode_host: data shard %d is NULL", j);
+  DeviceGuard g(p->device);
+  const int N = c->n_slots, K = c->n_out;
+  const size_t slot = p->slot_bytes();
+  const uint64_t rl_max = piece_len(len, slot, N + K);
+  std::vector<CopyOp> ops;
+  for (uint64_t r0 = 0; r0 < len; r0 += rl_max) {
+    const uint64_t rl = std::min<uint64_t>(rl_max, len - r0);
+    const int sl = p->next;
+    p->next = (p->next + 1) % gs_pipeline::kSlots;
+    uint8_t* in = p->staging + static_cast<size_t>(sl) * slot;
+    uint8_t* outb = in + static_cast<size_t>(N) * rl;
+    GS_CUDA(cudaStreamWaitEvent(p->s_h2d, p->drained[sl], 0));
+    for (int j = 0; j < N; ++j)
+      ops.push_back({in + static_cast<size_t>(j) * rl, static_cast<const uint8_t*>(h_data[j]) + r0, rl});
+    if (int st = issue_copies(ops, cudaMemcpyHostToDevice, p->s_h2d)) return st;
+    GS_CUDA(cudaEventRecord(p->ready[sl], p->s_h2d));
+    GS_CUDA(cudaStreamWaitEvent(p->s_comp, p->ready[sl], 0));
+    auto src = [&](int, int j) -> const void* { return in + static_cast<size_t>(j) * rl; };
+    auto dst = [&](int, int i) -> const void* { return outb + static_cast<size_t>(i) * rl; };
+    if (int st = run_codec(c, 1, src, dst, rl, p->s_comp)) return st;
+    GS_CUDA(cudaEventRecord(p->done[sl], p->s_comp));
+    GS_CUDA(cudaStreamWaitEvent(p->s_d2h, p->done[sl], 0));
+    for (int i = 0; i < K; ++i)
+      ops.push_back({static_cast<uint8_t*>(h_parity[i]) + r0, outb + static_cast<size_t>(i) * rl, rl});
+    if (int st = issue_copies(ops, cudaMemcpyDeviceToHost, p->s_d2h)) return st;
+    GS_CUDA(cudaEventRecord(p->drained[sl], p->s_d2h));
+  }
+  GS_CUDA(cudaStreamSynchronize(p->s_d2h));
+  GS_CUDA(cudaStreamSynchronize(p->s_comp));
+  return GS_OK;
+}
+
+int gs_reconstruct_host(gs_pipeline* p, const gs_codec* c, const void* const* h_slots, void* const* h_out,
+                        size_t len) {
+  if (!p || !c) return fail(GS_INVALID_ARGUMENT, "reconstruct_host: NULL pipeline/codec");
+  if (!c->decoder) return fail(GS_INVALID_ARGUMENT, "reconstruct_host: codec is an encoder");
+  if (len == 0 || c->n_out == 0) return GS_OK;
+  if (!h_slots || !h_out) return fail(GS_INVALID_ARGUMENT, "reconstruct_host: NULL pointer array");
+  for (int j : c->used)
+    if (!h_slots[j]) return fail(GS_INVALID_ARGUMENT, "coding: surviving shard %d missing from input", j);
+  DeviceGuard g(p->device);
+  const int U = static_cast<int>(c->used.size()), E = c->n_out;
+  const size_t slot = p->slot_bytes();
+  const uint64_t rl_max = piece_len(len, slot, U + E);
+  std::vector<CopyOp> ops;
+  for (uint64_t r0 = 0; r0 < len; r0 += rl_max) {
+    const uint64_t rl = std::min<uint64_t>(rl_max, len - r0);
+    const int sl = p->next;
+    p->next = (p->next + 1) % gs_pipeline::kSlots;
+    uint8_t* in = p->staging + static_cast<size_t>(sl) * slot;
+    uint8_t* outb = in + static_cast<size_t>(U) * rl;
+    GS_CUDA(cudaStreamWaitEvent(p->s_h2d, p->drained[sl], 0));
+    for (int u = 0; u < U; ++u)
+      ops.push_back({in + static_cast<size_t>(u) * rl, static_cast<const uint8_t*>(h_slots[c->used[u]]) + r0, rl});
+    if (int st = issue_copies(ops, cudaMemcpyHostToDevice, p->s_h2d)) return st;
+    GS_CUDA(cudaEventRecord(p->ready[sl], p->s_h2d));
+    GS_CUDA(cudaStreamWaitEvent(p->s_comp, p->ready[sl], 0));
+    auto src = [&](int, int j) -> const void* {
+      const auto it = std::find(c->used.begin(), c->used.end(), j);
+      return it == c->used.end() ? nullptr : in + static_cast<size_t>(it - c->used.begin()) * rl;
+    };
+    auto dst = [&](int, int i) -> const void* { return outb + static_cast<size_t>(i) * rl; };
+    if (int st = run_codec(c, 1, src, dst, rl, p->s_comp)) return st;
+    GS_CUDA(cudaEventRecord(p->done[sl], p->s_comp));
+    GS_CUDA(cudaStreamWaitEvent(p->s_d2h, p->done[sl], 0));
+    for (int i = 0; i < E; ++i)
+      ops.push_back({static_cast<uint8_t*>(h_out[i]) + r0, outb + static_cast<size_t>(i) * rl, rl});
+    if (int st = issue_copies(ops, cudaMemcpyDeviceToHost, p->s_d2h)) return st;
+    GS_CUDA(cudaEventRecord(p->drained[sl], p->s_d2h));
+  }
+  GS_CUDA(cudaStreamSynchronize(p->s_d2h));
+  GS_CUDA(cudaStreamSynchronize(p->s_comp));
+  return GS_OK;
+}
+
+// ============================================================================
+// KV data model
+// ============================================================================
+int gs_slice_bytes(int layers, int kv_heads, int head_dim, int tp, uint32_t chunk_size, uint64_t* out) {
+  if (layers < 1 || kv_heads < 1 || head_dim < 1 || tp < 1)
+    return fail(GS_INVALID_ARGUMENT, "model: all dimensions must be positive");
+  if ((static_cast<int64_t>(kv_heads) * head_dim) % tp != 0)
+    return fail(GS_INVALID_ARGUMENT, "model: kv_heads * head_dim must divide evenly across workers");
+  const uint64_t elems = static_cast<uint64_t>(kv_heads) * head_dim / tp;
+  *out = 2ull * layers * chunk_size * elems * 2ull;
+  return GS_OK;
+}
+
+static uint64_t splitmix_step(uint64_t& s) {
+  s += 0x9E3779B97F4A7C15ull;
+  uint64_t z = s;
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+  return z ^ (z >> 31);
+}
+
+int gs_ground_truth_slice_device(uint64_t kv_seed, uint64_t request_id, uint32_t chunk, int worker,
+                                 int layers, int kv_heads, int head_dim, int tp, uint32_t chunk_size,
+                                 uint32_t valid_tokens, void* d_out, void* stream) {
+  uint64_t len = 0;
+  if (int s = gs_slice_bytes(layers, kv_heads, head_dim, tp, chunk_size, &len)) return s;
+  if (valid_tokens > chunk_size) return fail(GS_INVALID_ARGUMENT, "kv: valid_tokens exceeds chunk size");
+  if (len == 0) return GS_OK;
+  if (!d_out) return fail(GS_INVALID_ARGUMENT, "ground_truth: NULL output");
+  // mix_key (kv_layout.hpp:96-103)
+  uint64_t a = request_id + 0x9E3779B97F4A7C15ull, b = chunk + 0xC2B2AE3D27D4EB4Full,
+           c = static_cast<uint64_t>(static_cast<int64_t>(worker)) + 0x165667B19E3779F9ull;
+  uint64_t state = kv_seed;
+  state ^= splitmix_step(a);
+  state ^= splitmix_step(b);
+  state ^= splitmix_step(c);
+  const uint64_t stride = static_cast<uint64_t>(kv_heads) * head_dim / tp * 2;
+  const uint64_t block = stride * chunk_size, keep = stride * valid_tokens;
+  int dev = 0;
+  if (int s = current_device(&dev)) return s;
+  const uint64_t words = (len + 7) / 8;
+  const int grid = static_cast<int>(std::min<uint64_t>((words + 255) / 256, device_sms(dev) * 8ull));
+  k_ground_truth<<<grid, 256, 0, static_cast<cudaStream_t>(stream)>>>(static_cast<uint8_t*>(d_out), len, state,
+                                                                      block, keep);
+  GS_CUDA(cudaGetLastError());
+  g_launches.fetch_add(1, std::memory_order_relaxed);
+  return GS_OK;
+}
+
+int gs_pad_partial_device(void* d_slice, int layers, int kv_heads, int head_dim, int tp, uint32_t chunk_size,
+                          uint32_t valid_tokens, void* stream) {
+  uint64_t len = 0;
+  if (int s = gs_slice_bytes(layers, kv_heads, head_dim, tp, chunk_size, &len)) return s;
+  if (valid_tokens > chunk_size) return fail(GS_INVALID_ARGUMENT, "kv: valid_tokens exceeds chunk size");
+  if (len == 0 || valid_tokens == chunk_size) return GS_OK;
+  const uint64_t stride = static_cast<uint64_t>(kv_heads) * head_dim / tp * 2;
+  int dev = 0;
+  if (int s = current_device(&dev)) return s;
+  const int grid = static_cast<int>(std::min<uint64_t>((len + 255) / 256, device_sms(dev) * 8ull));
+  k_pad_partial<<<grid, 256, 0, static_cast<cudaStream_t>(stream)>>>(static_cast<uint8_t*>(d_slice), len,
+                                                                     stride * chunk_size, stride * valid_tokens);
+  GS_CUDA(cudaGetLastError());
+  g_launches.fetch_add(1, std::memory_order_relaxed);
+  return GS_OK;
+}
+
+// ============================================================================
+// parity seal
+// ============================================================================
+uint64_t gs_fnv1a64(const void* bytes, size_t len, uint64_t h) {
+  const uint8_t* p = static_cast<const uint8_t*>(bytes);
+  for (size_t i = 0; i < len; ++i) {
+    h ^= p[i];
+    h *= 0x100000001b3ull;
+  }
+  return h;
+}
+
+uint64_t gs_parity_checksum(const void* const* parity, int k, size_t len) {
+  uint64_t h = 0xcbf29ce484222325ull;
+  for (int i = 0; i < k; ++i) h = gs_fnv1a64(parity[i], len, h);
+  return h;
+}
+
+int gs_parity_checksum_batch(const void* const* parity, int n_chunks, int k, size_t len, int threads,
+                             uint64_t* out) {
+  if (n_chunks < 0 || k < 1 || !out || (n_chunks > 0 && !parity))
+    return fail(GS_INVALID_ARGUMENT, "checksum_batch: bad arguments");
+  if (threads < 1) threads = 1;
+  threads = std::min(threads, std::max(1, n_chunks));
+  std::atomic<int> next{0};
+  auto work = [&] {
+    for (int c = next.fetch_add(1); c < n_chunks; c = next.fetch_add(1))
+      out[c] = gs_parity_checksum(parity + static_cast<size_t>(c) * k, k, len);
+  };
+  std::vector<std::thread> pool;
+  for (int t = 1; t < threads; ++t) pool.emplace_back(work);
+  work();
+  for (auto& t : pool) t.join();
+  return GS_OK;
+}
+
+// ============================================================================
+// peer memory
+// ============================================================================
+int gs_ipc_handle(const void* d_ptr, void* handle_out) {
+  if (!d_ptr || !handle_out) return fail(GS_INVALID_ARGUMENT, "ipc_handle: NULL argument");
+  cudaIpcMemHandle_t h;
+  GS_CUDA(cudaIpcGetMemHandle(&h, const_cast<void*>(d_ptr)));
+  static_assert(sizeof(h) == GS_IPC_HANDLE_BYTES, "IPC handle size");
+  std::memcpy(handle_out, &h, sizeof h);
+  return GS_OK;
+}
+
+int gs_ipc_open(const void* handle, int device, void** d_ptr) {
+  if (!handle || !d_ptr) return fail(GS_INVALID_ARGUMENT, "ipc_open: NULL argument");
+  DeviceGuard g(device);
+  cudaIpcMemHandle_t h;
+  std::memcpy(&h, handle, sizeof h);
+  GS_CUDA(cudaIpcOpenMemHandle(d_ptr, h, cudaIpcMemLazyEnablePeerAccess));
+  return GS_OK;
+}
+
+int gs_ipc_close(void* d_ptr) {
+  GS_CUDA(cudaIpcCloseMemHandle(d_ptr));
+  return GS_OK;
+}
+
+int gs_peer_enable(int device, int peer) {
+  if (device == peer) return GS_OK;
+  int can = 0;
+  GS_CUDA(cudaDeviceCanAccessPeer(&can, device, peer));
+  if (!can) return fail(GS_UNSUPPORTED, "peer access %d -> %d not supported", device, peer);
+  DeviceGuard g(device);
+  cudaError_t e = cudaDeviceEnablePeerAccess(peer, 0);
+  if (e == cudaErrorPeerAccessAlreadyEnabled) {
+    cudaGetLastError();
+    return GS_OK;
+  }
+  GS_CUDA(e);
+  return GS_OK;
+}
+
+int gs_stripe_range(uint64_t total, int rank, int world, uint64_t* off, uint64_t* len) {
+  if (world < 1 || rank < 0 || rank >= world || !off || !len)
+    return fail(GS_INVALID_ARGUMENT, "stripe_range: bad rank/world");
+  uint64_t per = (total + world - 1) / world;
+  per = (per + 4095) / 4096 * 4096;
+  const uint64_t o = std::min<uint64_t>(total, per * rank);
+  const uint64_t e = std::min<uint64_t>(total, o + per);
+  *off = o;
+  *len = e - o;
+  return GS_OK;
+}
+
+// ============================================================================
+// pinned host memory
+// ============================================================================
+int gs_host_alloc(size_t bytes, void** out) {
+  if (!out) return fail(GS_INVALID_ARGUMENT, "host_alloc: out is NULL");
+  GS_CUDA(cudaHostAlloc(out, bytes, cudaHostAllocPortable));
+  return GS_OK;
+}
+
+int gs_host_free(void* p) {
+  GS_CUDA(cudaFreeHost(p));
+  return GS_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,315 @@
+// gs_kernels.cuh -- sm_100a kernels for the shadow-checkpointing byte path.
+//
+//   K1 encode  : parity_i = sum_j C[i][j] * data_j          (coding.hpp:263-275)
+//   K2 rebuild : lost_b   = sum_s D[b][s] * shard_s          (coding.hpp:496-502, 554-566)
+//
+// Both are one operation -- "apply a GF(2^8) coefficient matrix to a set of
+// source shards, byte position by byte position" -- so one kernel family
+// serves both. Sources may live in local HBM or in a peer GPU's HBM (NVLink
+// P2P loads through a mapped pointer); outputs may be local staging (then
+// D2H'd on a copy stream) or a peer's KV buffer (P2P stores).
+//
+// Two arithmetic back ends, both HBM-streaming with 128-bit loads/stores:
+//
+//  * Specialised (compile-time coefficients, `k_apply_special`): Horner over
+//    the coefficient bits,  p = (((S7)*2 ^ S6)*2 ^ ...)*2 ^ S0,  where S_b is
+//    the XOR of the sources whose coefficient has bit b set. Multiply-by-2 on
+//    four packed bytes is 2 ALU + 2 FMA-pipe ops (xtime4). Cost per source
+//    word ~ rows*(28/ns + 2) ops -- about 11 for RS(8,2) encode.
+//
+//  * Generic (runtime coefficients, `k_apply_generic`): split-table lookups
+//    with PRMT. Byte b = lo3 | bit3 | hi3<<4 | bit7, so
+//      c*b = L_c[lo3] ^ H_c[hi3] ^ (bit3 ? c*8 : 0) ^ (bit7 ? c*128 : 0)
+//    with 8-entry tables L_c, H_c held in two registers each. Two data words
+//    are processed as a pair so each PRMT selector packs 4 nibbles without
+//    extra compaction; results accumulate in a byte-permuted domain that is
+//    undone once per output word.
+#pragma once
+
+#include <cstdint>
+
+#include "gs_field.hpp"
+
+namespace gsb {
+
+constexpr int kThreads = 256;
+constexpr int kVec = 16;                  // bytes per thread per source per tile
+constexpr int kTile = kThreads * kVec;    // 4 KiB of every shard per tile
+constexpr int kMaxGenericRows = 4;
+
+template <int CAP>
+struct PtrTable {
+  const uint8_t* p[CAP];
+};
+
+// ---- primitive ops -------------------------------------------------------
+
+// prmt.b32 in its default mode: selector nibble bit 3 = replicate the sign
+// of the selected byte (used to build per-byte bit masks in one op).
+__device__ __forceinline__ uint32_t prmt(uint32_t a, uint32_t b, uint32_t sel) {
+  uint32_t r;
+  asm("prmt.b32 %0, %1, %2, %3;" : "=r"(r) : "r"(a), "r"(b), "r"(sel));
+  return r;
+}
+
+// Multiply four packed field elements by 2 (x): shift, then fold x^8 back in
+// as 0x1D where the top bit was set. The fold uses the high half of a 32x32
+// product: (a & 0x80808080) * (0x1D << 25) >> 32 places 0x1D in exactly the
+// bytes whose msb was set, with no carries between bytes.
+__device__ __forceinline__ uint32_t xtime4(uint32_t a) {
+  const uint32_t fold = __umulhi(a & 0x80808080u, 0x3A000000u);
+  return ((a + a) & 0xFEFEFEFEu) ^ fold;
+}
+
+__device__ __forceinline__ uint4 ld_stream(const uint8_t* p) {
+  uint4 r;
+  asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
+               : "l"(p));
+  return r;
+}
+
+__device__ __forceinline__ void st_stream(uint8_t* p, const uint4& v) {
+  asm volatile("st.global.L1::no_allocate.v4.u32 [%0], {%1,%2,%3,%4};" ::"l"(p), "r"(v.x),
+               "r"(v.y), "r"(v.z), "r"(v.w)
+               : "memory");
+}
+
+__device__ __forceinline__ uint32_t& word(uint4& v, int w) {
+  return w == 0 ? v.x : w == 1 ? v.y : w == 2 ? v.z : v.w;
+}
+
+// Byte-granular load/store of up to 16 bytes (tail of a shard, or shards
+// whose base pointers are not 16-B aligned).
+__device__ __forceinline__ uint4 ld_partial(const uint8_t* p, int nbytes) {
+  uint32_t w[4] = {0, 0, 0, 0};
+  for (int b = 0; b < nbytes; ++b) w[b >> 2] |= static_cast<uint32_t>(p[b]) << (8 * (b & 3));
+  return make_uint4(w[0], w[1], w[2], w[3]);
+}
+
+__device__ __forceinline__ void st_partial(uint8_t* p, const uint4& v, int nbytes) {
+  const uint32_t w[4] = {v.x, v.y, v.z, v.w};
+  for (int b = 0; b < nbytes; ++b) p[b] = static_cast<uint8_t>(w[b >> 2] >> (8 * (b & 3)));
+}
+
+// ---- tile walk shared by both back ends ------------------------------------
+//
+// Work = n_stripes x ceil(len / 4 KiB) tiles, walked grid-stride so that
+// consecutive CTAs stream consecutive 4 KiB pieces of the same shards.
+
+struct TileGeom {
+  uint64_t len;        // bytes per shard
+  uint32_t tps;        // tiles per stripe
+  uint32_t total;      // tiles overall
+  int stride;          // pointers per stripe in the table
+  int out0;            // first output pointer within a stripe's entries
+  int aligned;         // all pointers 16-B aligned -> vector path allowed
+};
+
+// ---- specialised back end --------------------------------------------------
+
+// Spec provides: static constexpr CoefMatrix matrix(); NS (#columns), NO (#rows).
+template <class Spec>
+__device__ __forceinline__ void horner_apply(const uint4 (&src)[Spec::NS], uint4 (&out)[Spec::NO]) {
+  constexpr CoefMatrix m = Spec::matrix();
+#pragma unroll
+  for (int i = 0; i < Spec::NO; ++i) {
+#pragma unroll
+    for (int w = 0; w < 4; ++w) {
+      uint32_t acc = 0;
+      bool live = false;
+#pragma unroll
+      for (int b = 7; b >= 0; --b) {
+        if (live) acc = xtime4(acc);
+        uint32_t s = 0;
+        bool any = false;
+#pragma unroll
+        for (int j = 0; j < Spec::NS; ++j)
+          if ((m.c[i][j] >> b) & 1u) {
+            s ^= word(const_cast<uint4&>(src[j]), w);
+            any = true;
+          }
+        if (any) {
+          acc ^= s;
+          live = true;
+        }
+      }
+      word(out[i], w) = acc;
+    }
+  }
+}
+
+template <class Spec>
+__device__ constexpr bool column_used(int j) {
+  constexpr CoefMatrix m = Spec::matrix();
+  for (int i = 0; i < Spec::NO; ++i)
+    if (m.c[i][j]) return true;
+  return false;
+}
+
+template <class Spec, int CAP>
+__global__ void __launch_bounds__(kThreads) k_apply_special(const PtrTable<CAP> tab, const TileGeom g) {
+  for (uint32_t t = blockIdx.x; t < g.total; t += gridDim.x) {
+    const uint32_t s = t / g.tps;
+    const uint64_t off = static_cast<uint64_t>(t - s * g.tps) * kTile + threadIdx.x * kVec;
+    if (off >= g.len) continue;
+    const int base = static_cast<int>(s) * g.stride;
+    const bool full = g.aligned && off + kVec <= g.len;
+    const int nb = full ? kVec : static_cast<int>(g.len - off < kVec ? g.len - off : kVec);
+    uint4 src[Spec::NS];
+#pragma unroll
+    for (int j = 0; j < Spec::NS; ++j) {
+      if (column_used<Spec>(j)) {
+        const uint8_t* p = tab.p[base + j] + off;
+        src[j] = full ? ld_stream(p) : ld_partial(p, nb);
+      } else {
+        src[j] = make_uint4(0, 0, 0, 0);
+      }
+    }
+    uint4 out[Spec::NO];
+    horner_apply<Spec>(src, out);
+#pragma unroll
+    for (int i = 0; i < Spec::NO; ++i) {
+      uint8_t* p = const_cast<uint8_t*>(tab.p[base + g.out0 + i]) + off;
+      if (full)
+        st_stream(p, out[i]);
+      else
+        st_partial(p, out[i], nb);
+    }
+  }
+}
+
+// ---- generic back end ------------------------------------------------------
+
+// Per (row, source) coefficient c: {L0, L1, H0, H1, C8, C128, 0, 0} where
+// L = c*{0..7}, H = c*{0,16,..,112} (byte v of the 8-byte pair = entry v),
+// C8 = c*8 and C128 = c*128 replicated into all four bytes.
+struct CoefWords {
+  uint32_t l0, l1, h0, h1, c8, c128, pad0, pad1;
+};
+
+GS_HD inline CoefWords make_coef_words(uint8_t c) {
+  CoefWords w{};
+  uint32_t l[2] = {0, 0}, h[2] = {0, 0};
+  for (int v = 0; v < 8; ++v) {
+    l[v >> 2] |= static_cast<uint32_t>(gf_mul(c, static_cast<uint8_t>(v))) << (8 * (v & 3));
+    h[v >> 2] |= static_cast<uint32_t>(gf_mul(c, static_cast<uint8_t>(v << 4))) << (8 * (v & 3));
+  }
+  w.l0 = l[0];
+  w.l1 = l[1];
+  w.h0 = h[0];
+  w.h1 = h[1];
+  w.c8 = 0x01010101u * gf_mul(c, 8);
+  w.c128 = 0x01010101u * gf_mul(c, 128);
+  return w;
+}
+
+struct PairSel {
+  uint32_t loP, hiP, loQ, hiQ, m3P, m3Q, m7P, m7Q;
+};
+
+// Selectors for the pair of data words (x, y). Domain P holds byte order
+// [x0, y0, x1, y1], domain Q holds [x2, y2, x3, y3].
+__device__ __forceinline__ PairSel pair_setup(uint32_t x, uint32_t y) {
+  PairSel s;
+  const uint32_t lo = (x & 0x07070707u) | ((y & 0x07070707u) << 4);
+  const uint32_t hi = ((x >> 4) & 0x07070707u) | (y & 0x70707070u);
+  s.loP = lo;
+  s.loQ = lo >> 16;
+  s.hiP = hi;
+  s.hiQ = hi >> 16;
+  s.m7P = prmt(x, y, 0xD9C8u);
+  s.m7Q = prmt(x, y, 0xFBEAu);
+  const uint32_t x4 = x << 4, y4 = y << 4;
+  s.m3P = prmt(x4, y4, 0xD9C8u);
+  s.m3Q = prmt(x4, y4, 0xFBEAu);
+  return s;
+}
+
+__device__ __forceinline__ void pair_mac(uint32_t& accP, uint32_t& accQ, const PairSel& s,
+                                         const CoefWords& c) {
+  accP ^= prmt(c.l0, c.l1, s.loP) ^ prmt(c.h0, c.h1, s.hiP);
+  accP ^= s.m3P & c.c8;
+  accP ^= s.m7P & c.c128;
+  accQ ^= prmt(c.l0, c.l1, s.loQ) ^ prmt(c.h0, c.h1, s.hiQ);
+  accQ ^= s.m3Q & c.c8;
+  accQ ^= s.m7Q & c.c128;
+}
+
+// Undo the pair permutation: x = [P0, P2, Q0, Q2], y = [P1, P3, Q1, Q3].
+__device__ __forceinline__ void pair_finish(uint32_t accP, uint32_t accQ, uint32_t& x, uint32_t& y) {
+  x = prmt(accP, accQ, 0x6420u);
+  y = prmt(accP, accQ, 0x7531u);
+}
+
+// coef: rows x ns CoefWords for this launch's row group (row-major).
+template <int KB, int CAP>
+__global__ void __launch_bounds__(kThreads) k_apply_generic(const PtrTable<CAP> tab, const TileGeom g,
+                                                            const CoefWords* __restrict__ coef,
+                                                            int ns) {
+  extern __shared__ uint4 smem_coef[];
+  CoefWords* sc = reinterpret_cast<CoefWords*>(smem_coef);
+  for (int i = threadIdx.x; i < KB * ns; i += blockDim.x) sc[i] = coef[i];
+  __syncthreads();
+
+  for (uint32_t t = blockIdx.x; t < g.total; t += gridDim.x) {
+    const uint32_t s = t / g.tps;
+    const uint64_t off = static_cast<uint64_t>(t - s * g.tps) * kTile + threadIdx.x * kVec;
+    if (off >= g.len) continue;
+    const int base = static_cast<int>(s) * g.stride;
+    const bool full = g.aligned && off + kVec <= g.len;
+    const int nb = full ? kVec : static_cast<int>(g.len - off < kVec ? g.len - off : kVec);
+
+    uint32_t acc[KB][4];
+#pragma unroll
+    for (int r = 0; r < KB; ++r)
+#pragma unroll
+      for (int q = 0; q < 4; ++q) acc[r][q] = 0;
+
+    int j = 0;
+    for (; j + 4 <= ns; j += 4) {
+      uint4 d[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const uint8_t* p = tab.p[base + j + u] + off;
+        d[u] = full ? ld_stream(p) : ld_partial(p, nb);
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const PairSel s0 = pair_setup(d[u].x, d[u].y);
+        const PairSel s1 = pair_setup(d[u].z, d[u].w);
+#pragma unroll
+        for (int r = 0; r < KB; ++r) {
+          const CoefWords c = sc[r * ns + j + u];
+          pair_mac(acc[r][0], acc[r][1], s0, c);
+          pair_mac(acc[r][2], acc[r][3], s1, c);
+        }
+      }
+    }
+    for (; j < ns; ++j) {
+      const uint8_t* p = tab.p[base + j] + off;
+      const uint4 d = full ? ld_stream(p) : ld_partial(p, nb);
+      const PairSel s0 = pair_setup(d.x, d.y);
+      const PairSel s1 = pair_setup(d.z, d.w);
+#pragma unroll
+      for (int r = 0; r < KB; ++r) {
+        const CoefWords c = sc[r * ns + j];
+        pair_mac(acc[r][0], acc[r][1], s0, c);
+        pair_mac(acc[r][2], acc[r][3], s1, c);
+      }
+    }
+#pragma unroll
+    for (int r = 0; r < KB; ++r) {
+      uint4 o;
+      pair_finish(acc[r][0], acc[r][1], o.x, o.y);
+      pair_finish(acc[r][2], acc[r][3], o.z, o.w);
+      uint8_t* p = const_cast<uint8_t*>(tab.p[base + g.out0 + r]) + off;
+      if (full)
+        st_stream(p, o);
+      else
+        st_partial(p, o, nb);
+    }
+  }
+}
+
+}  // namespace gsb

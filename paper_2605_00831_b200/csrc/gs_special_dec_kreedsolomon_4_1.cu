@@ -1,0 +1,13 @@
+// Compile-time decoders (K2, Horner back end) for every canonical erasure
+// pattern of ReedSolomon(4,1); coefficients = coding.hpp:535-566 folded by the compiler.
+#include "gs_special.cuh"
+
+namespace gsb {
+
+int special_decoders_kreedsolomon_4_1(SpecialEntry* out) {
+  int c = 0;
+  add_decoders<kReedSolomon, 4, 1>(out, c);
+  return c;
+}
+
+}  // namespace gsb

@@ -1,0 +1,216 @@
+"""Device-resident API: K1 / K2 on torch CUDA tensors, plus the host-link
+pipelines (checkpoint offload, recovery upload).
+
+torch is plumbing here (device memory, streams, pinned host memory); the
+bytes are produced by libghostserve_b200.so kernels. Tensors are uint8 and
+contiguous in their last dimension; shapes:
+
+  encode   data  [n, L] | [S, n, L]   -> parity [k, L] | [S, k, L]
+  rebuild  shards {idx: [L] | [S, L]} -> {lost data idx: [L] | [S, L]}
+
+where S is the number of independent stripes (requests x chunks) launched
+together -- e.g. the 32 requests of a decode block, or the 64 chunks of a
+128K prefill.
+"""
+from __future__ import annotations
+
+import ctypes as C
+from typing import Dict, List, Mapping, Optional, Sequence, Union
+
+import torch
+
+from . import _lib as L
+from .coding import (CodingScheme, Codec, ErasurePattern, InvalidArgument, UnrecoverableError,
+                     check, decoder, encoder, max_tolerance, to_string)
+
+Tensor = torch.Tensor
+
+
+def _stream(stream) -> int:
+    if stream is None:
+        return torch.cuda.current_stream().cuda_stream
+    if isinstance(stream, torch.cuda.Stream):
+        return stream.cuda_stream
+    return int(stream)
+
+
+def _check_u8(t: Tensor, what: str) -> None:
+    if t.dtype != torch.uint8:
+        raise InvalidArgument(f"{what}: expected a uint8 tensor (view fp16/bf16 KV as bytes), got {t.dtype}")
+    if not t.is_cuda:
+        raise InvalidArgument(f"{what}: expected a CUDA tensor")
+    if t.stride(-1) != 1:
+        raise InvalidArgument(f"{what}: last dimension must be contiguous")
+
+
+def as_bytes(t: Tensor) -> Tensor:
+    """Bit-for-bit byte view of an fp16/bf16 (or any) tensor: fp16.hpp:20-21."""
+    return t.contiguous().view(torch.uint8)
+
+
+def apply(codec: Codec, slots: Sequence[Sequence[Optional[int]]], outs: Sequence[Sequence[int]],
+          length: int, stream=None) -> None:
+    """Raw launch: per-stripe lists of device pointers (gs_apply_device)."""
+    flat_s = [p for row in slots for p in row]
+    flat_o = [p for row in outs for p in row]
+    check(L.lib().gs_apply_device(codec.handle, len(slots), L.ptr_array(flat_s), L.ptr_array(flat_o),
+                                  length, _stream(stream)), "apply")
+
+
+def encode(scheme: CodingScheme, data: Union[Tensor, Sequence[Tensor]], out: Optional[Tensor] = None,
+           stream=None) -> Tensor:
+    """K1 on device: parity of n data shards (or of S stripes of n shards)."""
+    scheme.validate()
+    if not isinstance(data, Tensor):
+        shards = list(data)
+        if len(shards) != scheme.n:
+            raise InvalidArgument(f"coding: expected {scheme.n} data shards, got {len(shards)}")
+        ln = shards[0].numel() * shards[0].element_size()
+        for t in shards:
+            if t.numel() * t.element_size() != ln:
+                raise InvalidArgument("coding: shard buffers must all have the same length")
+            _check_u8(t, "encode")
+        if out is None:
+            out = torch.empty((scheme.k, ln), dtype=torch.uint8, device=shards[0].device)
+        apply(encoder(scheme), [[t.data_ptr() for t in shards]],
+              [[out[i].data_ptr() for i in range(scheme.k)]], ln, stream)
+        return out
+    _check_u8(data, "encode")
+    single = data.dim() == 2
+    d3 = data.unsqueeze(0) if single else data
+    if d3.dim() != 3 or d3.shape[1] != scheme.n:
+        raise InvalidArgument(f"coding: expected data of shape [n={scheme.n}, L] or [S, n, L], got "
+                              f"{tuple(data.shape)}")
+    S, _, ln = d3.shape
+    if out is None:
+        out = torch.empty((S, scheme.k, ln) if not single else (scheme.k, ln), dtype=torch.uint8,
+                          device=data.device)
+    o3 = out.unsqueeze(0) if single else out
+    _check_u8(o3, "encode(out)")
+    slots = [[d3[s, j].data_ptr() for j in range(scheme.n)] for s in range(S)]
+    outs = [[o3[s, i].data_ptr() for i in range(scheme.k)] for s in range(S)]
+    apply(encoder(scheme), slots, outs, ln, stream)
+    return out
+
+
+def reconstruct(scheme: CodingScheme, shards: Mapping[int, Tensor], lost: ErasurePattern,
+                out: Optional[Mapping[int, Tensor]] = None, stream=None) -> Dict[int, Tensor]:
+    """K2 on device: rebuild lost data shards from surviving device shards."""
+    scheme.validate()
+    total = scheme.n + scheme.k
+    for idx in lost.lost:
+        if idx < 0 or idx >= total:
+            raise InvalidArgument("coding: lost shard index out of range")
+    if len(lost.lost) > max_tolerance(scheme):
+        raise UnrecoverableError(f"coding: {len(lost.lost)} erasures exceed tolerance "
+                                 f"{max_tolerance(scheme)} for scheme {to_string(scheme.kind)}")
+    shape = None
+    for idx in range(total):
+        if lost.contains(idx):
+            continue
+        if idx not in shards:
+            raise InvalidArgument(f"coding: surviving shard {idx} missing from input")
+        t = shards[idx]
+        _check_u8(t, "reconstruct")
+        if shape is None:
+            shape = tuple(t.shape)
+        elif tuple(t.shape) != shape:
+            raise InvalidArgument("coding: shard buffers must all have the same length")
+    dec = decoder(scheme, lost)
+    ref = next(shards[i] for i in range(total) if not lost.contains(i))
+    res = dict(out) if out is not None else {i: torch.empty(shape, dtype=torch.uint8, device=ref.device)
+                                              for i in dec.out_index}
+    if dec.n_out == 0 or ref.numel() == 0:
+        return res
+    batched = len(shape) == 2
+    S = shape[0] if batched else 1
+    ln = shape[-1]
+
+    def ptr(t: Tensor, s: int) -> int:
+        return (t[s] if batched else t).data_ptr()
+
+    slots = [[None if lost.contains(j) else ptr(shards[j], s) for j in range(total)] for s in range(S)]
+    outs = [[ptr(res[i], s) for i in dec.out_index] for s in range(S)]
+    apply(dec, slots, outs, ln, stream)
+    return res
+
+
+# ---------------------------------------------------------------------------
+# host-link pipelines
+# ---------------------------------------------------------------------------
+class Pipeline:
+    """Staging ring on one device for encode->D2H and H2D->rebuild overlap."""
+
+    def __init__(self, device: int = 0, staging_bytes: int = 256 << 20):
+        h = C.c_void_p()
+        check(L.lib().gs_pipeline_create(device, staging_bytes, C.byref(h)), "pipeline")
+        self.handle = h.value
+        self.device = device
+
+    def close(self) -> None:
+        if self.handle:
+            L.lib().gs_pipeline_destroy(self.handle)
+            self.handle = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def encode_offload(self, scheme: CodingScheme, data: Tensor, h_parity: Tensor,
+                       compute=None, copy=None) -> None:
+        """Encode [S, n, L] device data; parity lands in pinned host [S, k, L].
+
+        Enqueue only: completion is the `copy` stream (default: compute)."""
+        _check_u8(data, "encode_offload")
+        if data.dim() == 2:
+            data = data.unsqueeze(0)
+        if h_parity.dim() == 2:
+            h_parity = h_parity.unsqueeze(0)
+        S, n, ln = data.shape
+        if n != scheme.n or tuple(h_parity.shape) != (S, scheme.k, ln):
+            raise InvalidArgument("encode_offload: shape mismatch")
+        if h_parity.is_cuda or not h_parity.is_pinned():
+            raise InvalidArgument("encode_offload: parity must be a pinned host tensor")
+        enc = encoder(scheme)
+        d = L.ptr_array([data[s, j].data_ptr() for s in range(S) for j in range(n)])
+        h = L.ptr_array([h_parity[s, i].data_ptr() for s in range(S) for i in range(scheme.k)])
+        cs = _stream(compute)
+        ks = _stream(copy) if copy is not None else cs
+        check(L.lib().gs_encode_offload(self.handle, enc.handle, S, d, h, ln, cs, ks), "encode_offload")
+
+    def reconstruct_upload(self, scheme: CodingScheme, lost: ErasurePattern,
+                           data: Mapping[int, Tensor], h_parity: Tensor,
+                           out: Mapping[int, Tensor], compute=None, copy=None) -> None:
+        """Rebuild lost data shards: data[j] device [S, L] (surviving data
+        shards, local or peer-mapped), h_parity pinned host [S, k, L],
+        out[lost j] device [S, L]. Enqueue only: completion = `compute`."""
+        dec = decoder(scheme, lost)
+        if h_parity.dim() == 2:
+            h_parity = h_parity.unsqueeze(0)
+        S, k, ln = h_parity.shape
+        if not h_parity.is_pinned():
+            raise InvalidArgument("reconstruct_upload: parity must be a pinned host tensor")
+        total = scheme.n + scheme.k
+        slots = []
+        for s in range(S):
+            for j in range(total):
+                if lost.contains(j):
+                    slots.append(None)
+                elif j < scheme.n:
+                    t = data[j]
+                    slots.append((t[s] if t.dim() == 2 else t).data_ptr())
+                else:
+                    slots.append(h_parity[s, j - scheme.n].data_ptr())
+        outs = [(out[i][s] if out[i].dim() == 2 else out[i]).data_ptr()
+                for s in range(S) for i in dec.out_index]
+        cs = _stream(compute)
+        ks = _stream(copy) if copy is not None else cs
+        check(L.lib().gs_reconstruct_upload(self.handle, dec.handle, S, L.ptr_array(slots),
+                                            L.ptr_array(outs), ln, cs, ks), "reconstruct_upload")
+
+
+def launches() -> int:
+    """Kernels launched by libghostserve_b200.so in this process."""
+    return int(L.lib().gs_kernel_launches())

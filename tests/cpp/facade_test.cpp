@@ -1,0 +1,118 @@
+// facade_test.cpp -- drives the drop-in C++ facade (include/ghostserve_gpu/
+// coding.hpp) exactly the way the reference's own suites drive
+// ghostserve::encode / reconstruct (coding_test.cpp:53-70, acceptance.cpp:
+// 100-137), and checks every byte against the CPU oracle (test
+// infrastructure). Exit code = number of failed checks. Needs a GPU.
+#include <cstdio>
+#include <cstdint>
+#include <map>
+#include <stdexcept>
+#include <vector>
+
+#include "ghostserve_gpu/coding.hpp"
+#include "../../oracle/gs_oracle.h"
+
+namespace gs = ghostserve_gpu;
+
+static int failures = 0;
+#define CHECK(cond, ...)                \
+  do {                                  \
+    if (!(cond)) {                      \
+      ++failures;                       \
+      std::fprintf(stderr, __VA_ARGS__); \
+      std::fprintf(stderr, "\n");       \
+    }                                   \
+  } while (0)
+
+static std::vector<std::vector<uint8_t>> shards(int n, size_t len, uint64_t seed) {
+  std::vector<std::vector<uint8_t>> out(static_cast<size_t>(n));
+  uint64_t s = seed;
+  for (auto& v : out) {
+    v.resize(len);
+    for (auto& b : v) {
+      s += 0x9E3779B97F4A7C15ull;
+      uint64_t z = s;
+      z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+      z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+      b = static_cast<uint8_t>(z ^ (z >> 31));
+    }
+  }
+  return out;
+}
+
+int main() {
+  const std::vector<gs::CodingScheme> schemes = {
+      gs::CodingScheme::xor_code(2), gs::CodingScheme::xor_code(8), gs::CodingScheme::reed_solomon(4, 1),
+      gs::CodingScheme::reed_solomon(4, 2), gs::CodingScheme::reed_solomon(8, 2),
+      gs::CodingScheme::reed_solomon(8, 3), gs::CodingScheme::reed_solomon(6, 2)};
+  uint64_t seed = 1;
+  for (const auto& sc : schemes) {
+    for (size_t len : {size_t{1}, size_t{17}, size_t{4096}, size_t{1} << 20}) {
+      const auto data = shards(sc.n, len, seed++);
+      const auto parity = gs::encode(sc, data);
+      // oracle parity
+      std::vector<const uint8_t*> dp;
+      for (auto& d : data) dp.push_back(d.data());
+      std::vector<std::vector<uint8_t>> want(static_cast<size_t>(sc.k), std::vector<uint8_t>(len));
+      std::vector<uint8_t*> wp;
+      for (auto& w : want) wp.push_back(w.data());
+      gso_encode(static_cast<int>(sc.kind), sc.n, sc.k, dp.data(), len, wp.data());
+      CHECK(parity == want, "%s(%d,%d) len=%zu parity mismatch", gs::to_string(sc.kind), sc.n, sc.k, len);
+      // every erasure pattern within tolerance (coding_test.cpp:36-70)
+      const int total = sc.n + sc.k, tol = gs::max_tolerance(sc);
+      for (unsigned mask = 1; mask < (1u << total); ++mask) {
+        if (__builtin_popcount(mask) > tol) continue;
+        std::vector<int> lost;
+        for (int i = 0; i < total; ++i)
+          if (mask & (1u << i)) lost.push_back(i);
+        gs::ErasurePattern pat(lost);
+        std::map<int, gs::ConstShardSpan> surv;
+        for (int i = 0; i < sc.n; ++i)
+          if (!pat.contains(i)) surv[i] = gs::ConstShardSpan(data[static_cast<size_t>(i)]);
+        for (int i = 0; i < sc.k; ++i)
+          if (!pat.contains(sc.n + i)) surv[sc.n + i] = gs::ConstShardSpan(parity[static_cast<size_t>(i)]);
+        auto rebuilt = gs::reconstruct(sc, surv, pat);
+        for (int idx : pat.lost) {
+          if (idx >= sc.n) continue;
+          CHECK(rebuilt.count(idx) && rebuilt.at(idx) == data[static_cast<size_t>(idx)],
+                "%s(%d,%d) len=%zu lost mask %x: shard %d not rebuilt", gs::to_string(sc.kind), sc.n, sc.k,
+                len, mask, idx);
+        }
+      }
+    }
+  }
+  // error classes (coding_test.cpp:161-197)
+  const auto rs = gs::CodingScheme::reed_solomon(8, 2);
+  const auto d8 = shards(8, 16, 99);
+  const auto p8 = gs::encode(rs, d8);
+  try {
+    gs::ErasurePattern lost({0, 1, 2});
+    std::map<int, gs::ConstShardSpan> s;
+    gs::reconstruct(rs, s, lost);
+    CHECK(false, "over-tolerance did not throw");
+  } catch (const gs::UnrecoverableError&) {
+  }
+  try {
+    gs::ErasurePattern lost({0});
+    std::map<int, gs::ConstShardSpan> s;
+    for (int i = 1; i < 8; ++i) s[i] = gs::ConstShardSpan(d8[static_cast<size_t>(i)]);
+    s[8] = gs::ConstShardSpan(p8[0]);  // parity 9 missing
+    gs::reconstruct(rs, s, lost);
+    CHECK(false, "missing survivor did not throw");
+  } catch (const std::invalid_argument&) {
+  }
+  try {
+    std::vector<std::vector<uint8_t>> ragged{{1, 2}, {3}};
+    gs::encode(gs::CodingScheme::xor_code(2), ragged);
+    CHECK(false, "ragged did not throw");
+  } catch (const std::invalid_argument&) {
+  }
+  try {
+    gs::CodingScheme{gs::CodeKind::kReedSolomon, 4, 5}.validate();
+    CHECK(false, "k>n did not throw");
+  } catch (const std::invalid_argument&) {
+  }
+  std::printf("facade_test: %d failure(s), %llu kernels launched\n", failures,
+              static_cast<unsigned long long>(gs_kernel_launches()));
+  return failures;
+}

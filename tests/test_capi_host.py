@@ -1,0 +1,164 @@
+"""C-ABI host-side checks (no GPU): the library loads, exports every symbol
+include/gs_capi.h declares, and its host planning (field, Cauchy matrix,
+decode-matrix inversion, validation, errors) matches the pinned oracle."""
+import ctypes as C
+import itertools
+import os
+import re
+
+import numpy as np
+import pytest
+
+from oracle import oracle as O
+from paper_2605_00831_b200 import _lib as L
+from paper_2605_00831_b200 import coding as G
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def declared_symbols():
+    src = open(os.path.join(ROOT, "include", "gs_capi.h")).read()
+    src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
+    return sorted(set(re.findall(r"\b(gs_[a-z0-9_]+)\s*\(", src)))
+
+
+def test_library_exports_every_declared_symbol():
+    lib = L.lib()
+    syms = declared_symbols()
+    assert len(syms) >= 30
+    for s in syms:
+        assert hasattr(lib, s), f"{s} declared in gs_capi.h but not exported"
+        assert s in L.SIGNATURES, f"{s} has no ctypes signature"
+    assert set(L.SIGNATURES) == set(syms)
+
+
+def test_gf_field_matches_oracle(port, golden):
+    lib = L.lib()
+    for a in range(256):
+        for b in range(0, 256, 3):
+            assert lib.gs_gf_mul(a, b) == port.gf_mul(a, b)
+    inv = bytes([0] + [G.gf256.inv(a) for a in range(1, 256)])
+    assert inv.hex() == golden["gf"]["inv_hex"]
+    with pytest.raises(G.DomainError):
+        G.gf256.inv(0)
+    with pytest.raises(G.DomainError):
+        G.gf256.div(3, 0)
+    assert G.gf256.div(0, 7) == 0
+    assert G.gf256.mul(G.gf256.div(0x53, 0xCA), 0xCA) == 0x53
+
+
+def test_encoding_matrices_match_reference(golden):
+    for key, hx in golden["matrices"].items():
+        kind, n, k = map(int, key.split("_"))
+        m = G.build_encoding_matrix(G.CodingScheme(G.CodeKind(kind), n, k))
+        assert m.coef.tobytes().hex() == hx, key
+        assert (m.rows, m.cols) == (k, n)
+
+
+def test_validation_statuses_match_reference(golden):
+    for rec in golden["errors"]:
+        if rec["op"] != "validate":
+            continue
+        assert L.lib().gs_scheme_validate(rec["kind"], rec["n"], rec["k"]) == rec["status"], rec
+    with pytest.raises(G.InvalidArgument):
+        G.CodingScheme.reed_solomon(4, 5).validate()
+    with pytest.raises(G.InvalidArgument):
+        G.build_encoding_matrix(G.CodingScheme.reed_solomon(300, 1))
+    assert G.max_tolerance(G.CodingScheme.reed_solomon(8, 3)) == 3
+    assert G.max_tolerance(G.CodingScheme.rdp(8)) == 2
+    assert G.memory_overhead_ratio(G.CodingScheme.reed_solomon(8, 2)) == 0.25
+
+
+@pytest.mark.parametrize("kind,n,k", [(O.XOR, 4, 1), (O.XOR, 8, 1), (O.RS, 4, 2), (O.RS, 6, 2),
+                                      (O.RS, 8, 2), (O.RS, 8, 3), (O.RS, 10, 4), (O.RS, 4, 1)])
+def test_decode_plans_match_oracle(port, kind, n, k):
+    """Host decode planning == coding.hpp:535-566 (via the pinned oracle) for
+    every erasure pattern within tolerance, for both kernel back ends."""
+    scheme = G.CodingScheme(G.CodeKind(kind), n, k)
+    tol = 1 if kind == O.XOR else k
+    for e in range(1, tol + 1):
+        for lost in itertools.combinations(range(n + k), e):
+            cd, cp = port.decode_matrix(kind, n, k, list(lost))
+            for generic in (False, True):
+                c = G.codec_ex(scheme, G.ErasurePattern(lost), generic=generic)
+                lost_data = [i for i in lost if i < n]
+                assert c.out_index == lost_data
+                got = c.coefficients()
+                if not lost_data:
+                    assert got.size == 0
+                    continue
+                want = np.concatenate([cd, cp], axis=1)
+                assert np.array_equal(got, want), (lost, generic)
+                if generic:
+                    assert not c.specialised
+
+
+def test_specialised_registry_covers_configs():
+    for n, k in [(4, 2), (8, 2), (6, 2), (8, 3), (4, 1)]:
+        assert G.encoder(G.CodingScheme.reed_solomon(n, k)).specialised
+    assert G.encoder(G.CodingScheme.xor_code(8)).specialised
+    for lost in ([0], [5], [3, 8], [0, 7], [8, 2]):
+        assert G.decoder(G.CodingScheme.reed_solomon(8, 2), G.ErasurePattern(lost)).specialised, lost
+    for pair in itertools.combinations(range(6), 2):
+        assert G.decoder(G.CodingScheme.reed_solomon(6, 2), G.ErasurePattern(pair)).specialised
+    # unusual shapes fall back to the generic GPU kernel, not to the CPU
+    assert not G.encoder(G.CodingScheme.reed_solomon(9, 2)).specialised
+    assert not G.decoder(G.CodingScheme.reed_solomon(8, 3), G.ErasurePattern([1])).specialised
+
+
+def test_decoder_errors_match_reference(golden):
+    for rec in golden["errors"]:
+        if rec["op"] != "reconstruct" or rec["drop"] is not None:
+            continue
+        h = C.c_void_p()
+        lost = rec["lost"]
+        arr = (C.c_int * len(lost))(*lost)
+        st = L.lib().gs_decoder_create(rec["kind"], rec["n"], rec["k"], arr, len(lost), C.byref(h))
+        assert st == rec["status"], rec
+        if st == 0:
+            c = G.Codec(h.value)
+            assert sorted(c.out_index) == rec["rebuilt"]
+
+
+def test_rdp_is_rejected_not_faked():
+    h = C.c_void_p()
+    assert L.lib().gs_encoder_create(1, 4, 2, C.byref(h)) == L.GS_UNSUPPORTED
+    with pytest.raises(G.Unsupported):
+        G.encoder(G.CodingScheme.rdp(4))
+
+
+def test_slice_bytes_and_seal(golden, port):
+    from paper_2605_00831_b200 import kv_layout as K
+    for rec in golden["slice_bytes"]:
+        Lr, H, D, tp = rec["model"]
+        assert K.slice_bytes(K.ModelConfig(Lr, H, D, 2, tp), rec["m"]) == rec["bytes"]
+    with pytest.raises(G.InvalidArgument):
+        K.slice_bytes(K.ModelConfig(2, 4, 8, 2, 3), 16)
+    assert K.chunk_count(5000, 2048) == 3
+    lib = L.lib()
+    buf = np.frombuffer(b"foobar", np.uint8)
+    assert f"{lib.gs_fnv1a64(buf.ctypes.data, 6, 0xCBF29CE484222325):016x}" == golden["fnv"]["foobar"]
+    parity = [np.frombuffer(os.urandom(777), np.uint8) for _ in range(12)]
+    out = (C.c_uint64 * 4)()
+    assert lib.gs_parity_checksum_batch(L.ptr_array([p.ctypes.data for p in parity]), 4, 3, 777, 3,
+                                        out) == 0
+    for c in range(4):
+        assert out[c] == port.parity_checksum(parity[3 * c: 3 * c + 3])
+
+
+def test_stripe_ranges_partition_exactly():
+    lib = L.lib()
+    for total in [0, 1, 4095, 4096, 83886080, 262144 * 32 + 17]:
+        for world in [1, 2, 3, 4, 8]:
+            spans = []
+            for r in range(world):
+                off, ln = C.c_uint64(), C.c_uint64()
+                assert lib.gs_stripe_range(total, r, world, C.byref(off), C.byref(ln)) == 0
+                spans.append((off.value, ln.value))
+            pos = 0
+            for off, ln in spans:
+                assert off == pos or ln == 0
+                if ln:
+                    assert off % 4096 == 0
+                pos = max(pos, off + ln)
+            assert sum(ln for _, ln in spans) == total

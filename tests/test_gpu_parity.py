@@ -1,0 +1,276 @@
+"""GPU parity: the CUDA path (through the C ABI) against the pinned CPU
+oracle and the reference's golden vectors. Bit-exact everywhere (integer /
+byte work)."""
+import itertools
+import os
+import subprocess
+
+import numpy as np
+import pytest
+
+from oracle import oracle as O
+from tests.golden.vectors import splitmix_bytes
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+from paper_2605_00831_b200 import coding as G  # noqa: E402
+from paper_2605_00831_b200 import device as D  # noqa: E402
+from paper_2605_00831_b200 import kv_layout as K  # noqa: E402
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+@pytest.fixture(scope="module", autouse=True)
+def cuda0():
+    if not torch.cuda.is_available():
+        pytest.fail("GPU test collected without a CUDA device")
+    torch.cuda.set_device(0)
+    yield
+
+
+def to_dev(arrs):
+    return torch.stack([torch.from_numpy(np.ascontiguousarray(a)) for a in arrs]).cuda()
+
+
+def scheme_of(kind, n, k):
+    return G.CodingScheme(G.CodeKind(kind), n, k)
+
+
+def fnv(a):
+    return f"{O.port().fnv1a64(np.ascontiguousarray(a)):016x}"
+
+
+def apply_codec(codec, slots, outs, ln):
+    D.apply(codec, slots, outs, ln)
+
+
+@pytest.mark.parametrize("generic", [False, True])
+def test_encode_golden_vectors(golden, generic):
+    for rec in golden["encode"]:
+        kind, n, k, ln, seed = rec["kind"], rec["n"], rec["k"], rec["len"], rec["seed"]
+        scheme = scheme_of(kind, n, k)
+        data = to_dev([splitmix_bytes(seed * 1000 + j, ln) for j in range(n)])
+        par = torch.empty((k, ln), dtype=torch.uint8, device="cuda")
+        codec = G.codec_ex(scheme, generic=generic)
+        apply_codec(codec, [[data[j].data_ptr() for j in range(n)]],
+                    [[par[i].data_ptr() for i in range(k)]], ln)
+        got = par.cpu().numpy()
+        assert [fnv(p) for p in got] == rec["parity_fnv"], (kind, n, k, ln, generic)
+        if "parity_hex" in rec:
+            assert [p.tobytes().hex() for p in got] == rec["parity_hex"]
+
+
+@pytest.mark.parametrize("generic", [False, True])
+def test_every_erasure_pattern_rebuilds(golden, generic):
+    for rec in golden["encode"]:
+        if "patterns" not in rec:
+            continue
+        kind, n, k, ln, seed = rec["kind"], rec["n"], rec["k"], rec["len"], rec["seed"]
+        for ln2 in (ln, 4096 + 48, 70001):
+            host = [splitmix_bytes(seed * 1000 + j, ln2) for j in range(n)]
+            par = O.port().encode(kind, n, k, host)
+            shards = to_dev(host + par)
+            for pat in rec["patterns"]:
+                lost = pat["lost"]
+                codec = G.codec_ex(scheme_of(kind, n, k), G.ErasurePattern(lost), generic=generic)
+                if codec.n_out == 0:
+                    continue
+                out = torch.zeros((codec.n_out, ln2), dtype=torch.uint8, device="cuda")
+                slots = [None if s in lost else shards[s].data_ptr() for s in range(n + k)]
+                apply_codec(codec, [slots], [[out[i].data_ptr() for i in range(codec.n_out)]], ln2)
+                got = out.cpu().numpy()
+                for i, idx in enumerate(codec.out_index):
+                    assert np.array_equal(got[i], host[idx]), (kind, n, k, ln2, lost, generic)
+                    if ln2 == ln:
+                        assert fnv(got[i]) == pat["rebuilt_fnv"][str(idx)]
+
+
+def test_host_api_matches_reference(golden):
+    """coding.encode / reconstruct: the reference-shaped API, host in/out."""
+    for rec in golden["encode"]:
+        kind, n, k, ln, seed = rec["kind"], rec["n"], rec["k"], rec["len"], rec["seed"]
+        scheme = scheme_of(kind, n, k)
+        data = [splitmix_bytes(seed * 1000 + j, ln) for j in range(n)]
+        par = G.encode(scheme, data)
+        assert [fnv(p) for p in par] == rec["parity_fnv"]
+        lost = G.ErasurePattern(list(range(min(G.max_tolerance(scheme), n))))
+        surv = {i: data[i] for i in range(n) if not lost.contains(i)}
+        surv.update({n + i: par[i] for i in range(k)})
+        got = G.reconstruct(scheme, surv, lost)
+        assert sorted(got) == lost.lost
+        for i, b in got.items():
+            assert np.array_equal(b, data[i])
+
+
+def test_host_api_errors():
+    rs = G.CodingScheme.reed_solomon(8, 2)
+    data = [splitmix_bytes(5 + j, 64) for j in range(8)]
+    par = G.encode(rs, data)
+    surv = {i: data[i] for i in range(8)}
+    surv.update({8: par[0], 9: par[1]})
+    with pytest.raises(G.UnrecoverableError):
+        G.reconstruct(rs, surv, G.ErasurePattern([0, 1, 2]))
+    with pytest.raises(G.InvalidArgument):
+        G.reconstruct(rs, {k: v for k, v in surv.items() if k != 9}, G.ErasurePattern([0]))
+    with pytest.raises(G.InvalidArgument):
+        G.encode(G.CodingScheme.xor_code(2), [b"\x01\x02", b"\x03"])
+    with pytest.raises(G.InvalidArgument):
+        G.encode(G.CodingScheme.reed_solomon(4, 2), [b"\x01", b"\x02"])
+    assert G.reconstruct(rs, {k: v for k, v in surv.items() if k not in (8, 9)},
+                         G.ErasurePattern([8, 9])) == {}
+    empty = G.encode(rs, [b""] * 8)
+    assert all(p.size == 0 for p in empty)
+
+
+@pytest.mark.parametrize("offset", [0, 1, 3, 8, 15])
+@pytest.mark.parametrize("ln", [1, 15, 16, 17, 4095, 4097, (1 << 20) + 3])
+def test_misaligned_and_ragged_tails(offset, ln):
+    for scheme in (G.CodingScheme.reed_solomon(8, 2), G.CodingScheme.reed_solomon(9, 3),
+                   G.CodingScheme.xor_code(4)):
+        n, k = scheme.n, scheme.k
+        host = [splitmix_bytes(31 * offset + j + ln, ln) for j in range(n)]
+        want = O.port().encode(int(scheme.kind), n, k, host)
+        buf = torch.zeros((n, ln + 32), dtype=torch.uint8, device="cuda")
+        for j in range(n):
+            buf[j, offset:offset + ln] = torch.from_numpy(host[j]).cuda()
+        out = torch.full((k, ln + 32), 0xAB, dtype=torch.uint8, device="cuda")
+        D.apply(G.encoder(scheme), [[buf[j, offset:].data_ptr() for j in range(n)]],
+                [[out[i, offset:].data_ptr() for i in range(k)]], ln)
+        got = out.cpu().numpy()
+        for i in range(k):
+            assert np.array_equal(got[i, offset:offset + ln], want[i])
+            assert (got[i, :offset] == 0xAB).all() and (got[i, offset + ln:] == 0xAB).all()
+
+
+def test_kv_ground_truth_and_parity_fingerprints(golden):
+    """Device-generated reference KV + parity == the reference's fingerprints
+    (includes C1 at 4 x 128 MiB and the 70B TP8 2K-token chunk)."""
+    for rec in golden["kv"]:
+        Lr, H, Dh, tp = rec["model"]
+        cfg = K.ModelConfig(Lr, H, Dh, 2, tp)
+        m = rec["chunk_size"]
+        slices = torch.stack([K.make_ground_truth_slice(rec["kv_seed"], rec["request"], rec["chunk"], w,
+                                                        cfg, m, rec["valid"], device="cuda")
+                              for w in range(rec["n"])])
+        assert slices.shape[1] == rec["slice_bytes"]
+        scheme = scheme_of(rec["kind"], rec["n"], rec["k"])
+        par = D.encode(scheme, slices)
+        hs = slices.cpu().numpy()
+        hp = par.cpu().numpy()
+        assert [s[:16].tobytes().hex() for s in hs] == rec["data_head_hex"], rec["name"]
+        assert [fnv(s) for s in hs] == rec["data_fnv"], rec["name"]
+        assert [fnv(p) for p in hp] == rec["parity_fnv"], rec["name"]
+        assert f"{O.port().parity_checksum(list(hp)):016x}" == rec["checksum"]
+
+
+def test_pad_partial_device_matches_oracle():
+    cfg = K.ModelConfig(2, 8, 8, 2, 4)
+    t = K.make_ground_truth_slice(9, 3, 1, 2, cfg, 16, 16, device="cuda")
+    K.pad_partial(t, cfg, 16, 5)
+    want = O.port().make_ground_truth_slice(9, 3, 1, 2, 2, 8, 8, 4, 16, 5)
+    assert np.array_equal(t.cpu().numpy(), want)
+
+
+def test_batched_decode_block_c2_shape():
+    """C2: Llama-3-8B TP=8, RS(8,2), one 16-token block for 32 requests, as
+    one batched launch; every request's parity == the oracle's."""
+    cfg = K.LLAMA3_8B
+    S, n = 32, 8
+    data = torch.stack([torch.stack([K.make_ground_truth_slice(3, r, 7, w, cfg, 16, 16, device="cuda")
+                                     for w in range(n)]) for r in range(S)])
+    scheme = G.CodingScheme.reed_solomon(8, 2)
+    par = D.encode(scheme, data)
+    hd, hp = data.cpu().numpy(), par.cpu().numpy()
+    for r in range(S):
+        want = O.port().encode(O.RS, 8, 2, list(hd[r]))
+        for i in range(2):
+            assert np.array_equal(hp[r, i], want[i]), r
+    lost = G.ErasurePattern([2, 6])
+    shards = {j: data[:, j] .contiguous() for j in range(n) if j not in (2, 6)}
+    shards.update({8 + i: par[:, i].contiguous() for i in range(2)})
+    got = D.reconstruct(scheme, shards, lost)
+    assert torch.equal(got[2], data[:, 2]) and torch.equal(got[6], data[:, 6])
+
+
+@pytest.mark.parametrize("staging", [64 << 10, 4 << 20, 256 << 20])
+def test_offload_and_upload_pipelines(staging):
+    """encode -> D2H into pinned host parity; H2D parity -> rebuild; pieces
+    overlapped through the staging ring (small rings force many pieces)."""
+    scheme = G.CodingScheme.reed_solomon(8, 2)
+    S, n, ln = 5, 8, 3 * 65536 + 4096 + 7
+    gen = torch.Generator(device="cuda").manual_seed(0)
+    data = torch.randint(0, 256, (S, n, ln), dtype=torch.uint8, device="cuda", generator=gen)
+    want = D.encode(scheme, data)
+    pipe = D.Pipeline(0, staging)
+    h_par = torch.zeros((S, 2, ln), dtype=torch.uint8).pin_memory()
+    comp, copy = torch.cuda.Stream(), torch.cuda.Stream()
+    comp.wait_stream(torch.cuda.current_stream())
+    pipe.encode_offload(scheme, data, h_par, compute=comp, copy=copy)
+    copy.synchronize()
+    assert torch.equal(h_par, want.cpu())
+    for lost in ([3], [0, 7], [1, 8], [5, 9]):
+        pat = G.ErasurePattern(lost)
+        dec = G.decoder(scheme, pat)
+        outs = {i: torch.zeros((S, ln), dtype=torch.uint8, device="cuda") for i in dec.out_index}
+        data_map = {j: data[:, j].contiguous() for j in range(n) if j not in lost}
+        pipe.reconstruct_upload(scheme, pat, data_map, h_par, outs, compute=comp, copy=copy)
+        comp.synchronize()
+        for i in dec.out_index:
+            assert torch.equal(outs[i], data[:, i]), lost
+    pipe.close()
+
+
+def test_fp16_bf16_kv_bit_patterns():
+    """fp16/bf16 KV (incl. NaN payloads, inf, -0, subnormals) coded as raw
+    bytes: parity == oracle, rebuilt tensors bit-identical (fp16.hpp)."""
+    g = torch.Generator().manual_seed(0)
+    for dt in (torch.float16, torch.bfloat16):
+        x = torch.randn((4, 32, 8, 128), generator=g).to(dt)
+        x.view(-1)[:6] = torch.tensor([float("nan"), float("inf"), -float("inf"), -0.0, 6e-8, 1e-40]).to(dt)
+        raw = x.view(torch.int16).view(-1)
+        raw[6] = 0x7E01  # NaN payload survives untouched
+        dev = x.cuda()
+        shards = D.as_bytes(dev).view(4, -1)
+        par = D.encode(G.CodingScheme.reed_solomon(4, 2), shards)
+        want = O.port().encode(O.RS, 4, 2, list(x.view(torch.uint8).view(4, -1).numpy()))
+        assert np.array_equal(par.cpu().numpy(), np.stack(want))
+        rebuilt = D.reconstruct(G.CodingScheme.reed_solomon(4, 2),
+                                {0: shards[0], 2: shards[2], 4: par[0], 5: par[1]}, G.ErasurePattern([1, 3]))
+        back = torch.stack([shards[0], rebuilt[1], shards[2], rebuilt[3]]).view(dt).view(x.shape)
+        assert torch.equal(back.view(torch.int16).cpu(), x.view(torch.int16))
+
+
+def test_full_size_properties_c1():
+    """C1 at full size (RS(4,2), 4 x 128 MiB): erase -> rebuild round trip for
+    every single and double loss, and linearity (size-independent checks)."""
+    cfg = K.ModelConfig(32, 8, 128, 2, 4)
+    data = torch.stack([K.make_ground_truth_slice(3, 0, 0, w, cfg, 4096, 4096, device="cuda")
+                        for w in range(4)])
+    scheme = G.CodingScheme.reed_solomon(4, 2)
+    par = D.encode(scheme, data)
+    for e in (1, 2):
+        for lost in itertools.combinations(range(6), e):
+            sh = {i: data[i] for i in range(4) if i not in lost}
+            sh.update({4 + i: par[i] for i in range(2) if 4 + i not in lost})
+            got = D.reconstruct(scheme, sh, G.ErasurePattern(lost))
+            for i, t in got.items():
+                assert torch.equal(t, data[i]), lost
+    other = torch.roll(data, 1, dims=1)
+    assert torch.equal(D.encode(scheme, data ^ other), par ^ D.encode(scheme, other))
+
+
+def test_cpp_facade_binary():
+    exe = os.path.join(ROOT, "tests", "cpp", "facade_test")
+    if not os.path.exists(exe):
+        subprocess.check_call(["make", "-s", "-C", os.path.join(ROOT, "tests", "cpp")])
+    r = subprocess.run([exe], capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stdout + r.stderr
+    assert "0 failure(s)" in r.stdout
+
+
+def test_native_library_is_what_ran():
+    D.encode(G.CodingScheme.reed_solomon(8, 2), torch.zeros((8, 4096), dtype=torch.uint8, device="cuda"))
+    maps = open("/proc/self/maps").read()
+    assert "libghostserve_b200.so" in maps
+    assert D.launches() > 0
