@@ -164,8 +164,12 @@ int gs_parity_checksum_batch(const void* const* parity, int n_chunks, int k, siz
 
 /* ---- peer memory over NVLink (multi-GPU striping) ---------------------- */
 #define GS_IPC_HANDLE_BYTES 64
-int gs_ipc_handle(const void* d_ptr, void* handle_out /* 64 bytes */);
-int gs_ipc_open(const void* handle, int device, void** d_ptr);
+/* Export the allocation holding d_ptr: handle (64 B) + byte offset of d_ptr
+ * inside it. The importer maps the allocation with gs_ipc_open and adds the
+ * offset. Replaces the paper's NCCL gather: peers' KV shards
+ * are read in place by K1/K2 over NVLink instead of being copied first. */
+int gs_ipc_handle(const void* d_ptr, void* handle_out, uint64_t* offset_out);
+int gs_ipc_open(const void* handle, int device, void** d_base);
 int gs_ipc_close(void* d_ptr);
 int gs_peer_enable(int device, int peer);
 /* Byte range [*off, *off + *len) of a shard of `total` bytes owned by rank

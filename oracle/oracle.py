@@ -180,6 +180,16 @@ class _Ref(_Lib):
         _check(st, "encode")
         return secs.value
 
+    def encode_batch_timed(self, kind, n, k, stripes, parities, threads: int) -> float:
+        """stripes[s] = n data arrays, parities[s] = k outputs; T threads over stripes."""
+        secs = C.c_double(0)
+        ln = int(stripes[0][0].size)
+        st = self.fn("encode_batch")(kind, n, k, len(stripes), _ptrs([d for row in stripes for d in row]),
+                                     C.c_size_t(ln), _ptrs([p for row in parities for p in row]), threads,
+                                     C.byref(secs))
+        _check(st, "encode_batch")
+        return secs.value
+
     def reconstruct_timed(self, kind, n, k, shards: List[Optional[np.ndarray]], lost, outs,
                           threads: int = 1) -> float:
         secs = C.c_double(0)

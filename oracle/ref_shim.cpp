@@ -13,6 +13,7 @@
 // The *_striped entry points are OUR wrapper, not the reference's: they call
 // ghostserve::encode / reconstruct on disjoint byte stripes from T threads,
 // which is valid because XOR and RS are position-wise (coding.hpp:143-172).
+#include <atomic>
 #include <chrono>
 #include <cstdint>
 #include <cstring>
@@ -233,6 +234,40 @@ int ghs_reconstruct_striped(int kind, int n, int k, const uint8_t* const* shards
     for (int st : status)
       if (st) return st;
     *n_out = counts[0];
+    return 0;
+  } catch (...) {
+    return map_exception();
+  }
+}
+
+// Batch of independent stripes (e.g. the 32 requests of a decode block) on
+// T threads, each thread taking whole stripes: the natural all-cores way to
+// drive the reference codec (ours, not the reference's). Pointers are
+// stripe-major: data[s*n + j], parity[s*k + i].
+int ghs_encode_batch(int kind, int n, int k, int n_stripes, const uint8_t* const* data, size_t len,
+                     uint8_t* const* parity, int threads, double* secs) {
+  try {
+    const auto s = scheme_of(kind, n, k);
+    s.validate();
+    if (threads < 1) threads = 1;
+    std::atomic<int> next{0};
+    std::vector<int> status(static_cast<size_t>(threads), 0);
+    const auto t0 = std::chrono::steady_clock::now();
+    auto work = [&](int t) {
+      try {
+        for (int st = next.fetch_add(1); st < n_stripes; st = next.fetch_add(1))
+          encode_range(s, data + static_cast<size_t>(st) * n, 0, len, parity + static_cast<size_t>(st) * k);
+      } catch (...) {
+        status[static_cast<size_t>(t)] = map_exception();
+      }
+    };
+    std::vector<std::thread> pool;
+    for (int t = 1; t < threads; ++t) pool.emplace_back(work, t);
+    work(0);
+    for (auto& th : pool) th.join();
+    if (secs) *secs = seconds_since(t0);
+    for (int st : status)
+      if (st) return st;
     return 0;
   } catch (...) {
     return map_exception();

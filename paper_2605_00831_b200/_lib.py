@@ -54,7 +54,7 @@ SIGNATURES = {
     "gs_fnv1a64": (_u64, [_vp, _sz, _u64]),
     "gs_parity_checksum": (_u64, [_vpp, _i, _sz]),
     "gs_parity_checksum_batch": (_i, [_vpp, _i, _i, _sz, _i, _u64p]),
-    "gs_ipc_handle": (_i, [_vp, _vp]),
+    "gs_ipc_handle": (_i, [_vp, _vp, _u64p]),
     "gs_ipc_open": (_i, [_vp, _i, _vpp]),
     "gs_ipc_close": (_i, [_vp]),
     "gs_peer_enable": (_i, [_i, _i]),

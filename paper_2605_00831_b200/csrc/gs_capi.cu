@@ -952,21 +952,37 @@ int gs_parity_checksum_batch(const void* const* parity, int n_chunks, int k, siz
 // ============================================================================
 // peer memory
 // ============================================================================
-int gs_ipc_handle(const void* d_ptr, void* handle_out) {
-  if (!d_ptr || !handle_out) return fail(GS_INVALID_ARGUMENT, "ipc_handle: NULL argument");
+int gs_ipc_handle(const void* d_ptr, void* handle_out, uint64_t* offset_out) {
+  if (!d_ptr || !handle_out || !offset_out) return fail(GS_INVALID_ARGUMENT, "ipc_handle: NULL argument");
+  // IPC handles name whole allocations; find the base of the allocation that
+  // holds d_ptr (e.g. inside a caching-allocator block) through the driver.
+  using AddrRangeFn = int (*)(unsigned long long*, size_t*, unsigned long long);
+  static AddrRangeFn range_fn = nullptr;
+  if (!range_fn) {
+    void* fn = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    GS_CUDA(cudaGetDriverEntryPoint("cuMemGetAddressRange", &fn, cudaEnableDefault, &q));
+    if (!fn) return fail(GS_CUDA_ERROR, "ipc_handle: cuMemGetAddressRange unavailable");
+    range_fn = reinterpret_cast<AddrRangeFn>(fn);
+  }
+  unsigned long long base = 0;
+  size_t size = 0;
+  if (range_fn(&base, &size, reinterpret_cast<unsigned long long>(d_ptr)) != 0)
+    return fail(GS_CUDA_ERROR, "ipc_handle: cuMemGetAddressRange failed for %p", d_ptr);
   cudaIpcMemHandle_t h;
-  GS_CUDA(cudaIpcGetMemHandle(&h, const_cast<void*>(d_ptr)));
+  GS_CUDA(cudaIpcGetMemHandle(&h, reinterpret_cast<void*>(base)));
   static_assert(sizeof(h) == GS_IPC_HANDLE_BYTES, "IPC handle size");
   std::memcpy(handle_out, &h, sizeof h);
+  *offset_out = reinterpret_cast<unsigned long long>(d_ptr) - base;
   return GS_OK;
 }
 
-int gs_ipc_open(const void* handle, int device, void** d_ptr) {
-  if (!handle || !d_ptr) return fail(GS_INVALID_ARGUMENT, "ipc_open: NULL argument");
+int gs_ipc_open(const void* handle, int device, void** d_base) {
+  if (!handle || !d_base) return fail(GS_INVALID_ARGUMENT, "ipc_open: NULL argument");
   DeviceGuard g(device);
   cudaIpcMemHandle_t h;
   std::memcpy(&h, handle, sizeof h);
-  GS_CUDA(cudaIpcOpenMemHandle(d_ptr, h, cudaIpcMemLazyEnablePeerAccess));
+  GS_CUDA(cudaIpcOpenMemHandle(d_base, h, cudaIpcMemLazyEnablePeerAccess));
   return GS_OK;
 }
 

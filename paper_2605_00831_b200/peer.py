@@ -1,0 +1,166 @@
+"""Multi-GPU striping over NVLink: one process per GPU, peers' KV shards read
+in place through IPC-mapped pointers.
+
+The paper gathers every worker's slice to one rotating encoder GPU with NCCL
+(checkpoint.hpp:21-30) and offloads the whole chunk's
+parity over that GPU's single PCIe link. Here every rank g encodes the byte
+range g of ALL shards -- reading the ranges it does not own straight out of
+the owners' HBM over NVLink inside K1 -- and D2H's parity range g on its own
+host link. No reduction is involved (NCCL has no GF(2^8) op); the only
+exchange is the peer loads, fused into the kernel. Recovery mirrors it: rank
+g uploads parity range g, pulls range g of the survivors and stores range g
+of the rebuilt shard directly into the replacement GPU's KV buffer.
+
+Layout: with W ranks and n TP workers (W | n), rank r holds workers
+[r*n/W, (r+1)*n/W) as a tensor [S, n/W, L] (S stripes = requests x chunks).
+"""
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass
+from typing import Dict, List, Optional, Sequence, Tuple
+
+from . import _lib as L
+from .coding import CodingScheme, ErasurePattern, InvalidArgument, check, decoder, encoder
+
+
+def stripe_range(total: int, rank: int, world: int) -> Tuple[int, int]:
+    """4 KiB-aligned contiguous split of [0, total) (gs_stripe_range)."""
+    off, ln = C.c_uint64(), C.c_uint64()
+    check(L.lib().gs_stripe_range(total, rank, world, C.byref(off), C.byref(ln)), "stripe_range")
+    return off.value, ln.value
+
+
+@dataclass(frozen=True)
+class ShardLayout:
+    n: int          # TP workers = data shards
+    world: int      # ranks (GPUs)
+    stripes: int    # S
+    length: int     # L bytes per shard per stripe
+
+    def __post_init__(self):
+        if self.world < 1 or self.n % self.world:
+            raise InvalidArgument(f"layout: {self.world} ranks must divide {self.n} workers")
+
+    @property
+    def n_local(self) -> int:
+        return self.n // self.world
+
+    def owner(self, worker: int) -> Tuple[int, int]:
+        return worker // self.n_local, worker % self.n_local
+
+    def shard_offset(self, stripe: int, worker: int) -> int:
+        """Byte offset of (stripe, worker) inside its owner's [S, n_local, L] tensor."""
+        _, jl = self.owner(worker)
+        return (stripe * self.n_local + jl) * self.length
+
+
+def striped_slots(layout: ShardLayout, bases: Sequence[int], rank: int,
+                  lost: Sequence[int] = ()) -> Tuple[int, int, List[List[Optional[int]]]]:
+    """Rank `rank`'s byte range and per-stripe data-shard pointers into the
+    owners' memory (`bases[r]` = rank r's tensor base as mapped locally).
+    Lost workers get None."""
+    off, ln = stripe_range(layout.length, rank, layout.world)
+    slots = []
+    for s in range(layout.stripes):
+        row = []
+        for j in range(layout.n):
+            if j in lost:
+                row.append(None)
+            else:
+                r, _ = layout.owner(j)
+                row.append(bases[r] + layout.shard_offset(s, j) + off)
+        slots.append(row)
+    return off, ln, slots
+
+
+class PeerGroup:
+    """IPC-maps every rank's buffer into every other rank (same node)."""
+
+    def __init__(self, group=None):
+        import torch
+        import torch.distributed as dist
+
+        self.dist = dist
+        self.group = group
+        self.rank = dist.get_rank(group)
+        self.world = dist.get_world_size(group)
+        self.device = torch.cuda.current_device()
+        self._opened: List[int] = []
+
+    def share(self, tensor) -> List[int]:
+        """All ranks' base pointers of `tensor` (collective)."""
+        handle = (C.c_uint8 * L.IPC_HANDLE_BYTES)()
+        off = C.c_uint64()
+        check(L.lib().gs_ipc_handle(tensor.data_ptr(), handle, C.byref(off)), "ipc_handle")
+        objs: List = [None] * self.world
+        self.dist.all_gather_object(objs, (bytes(handle), off.value), group=self.group)
+        ptrs = []
+        for r, (h, o) in enumerate(objs):
+            if r == self.rank:
+                ptrs.append(tensor.data_ptr())
+                continue
+            base = C.c_void_p()
+            hb = (C.c_uint8 * L.IPC_HANDLE_BYTES).from_buffer_copy(h)
+            check(L.lib().gs_ipc_open(hb, self.device, C.byref(base)), "ipc_open")
+            self._opened.append(base.value)
+            ptrs.append(base.value + o)
+        return ptrs
+
+    def close(self) -> None:
+        for p in self._opened:
+            L.lib().gs_ipc_close(p)
+        self._opened.clear()
+
+
+def encode_striped(scheme: CodingScheme, layout: ShardLayout, bases: Sequence[int], rank: int,
+                   parity_out, stream: int, pipeline=None, h_parity=None, copy_stream=None) -> Tuple[int, int]:
+    """K1 over this rank's byte range of all stripes.
+
+    Without a pipeline: parity range -> `parity_out` device [S, k, len_r].
+    With a pipeline: parity range -> pinned host `h_parity` [S, k, L] at the
+    range's offset (encode + D2H overlapped on this rank's host link)."""
+    enc = encoder(scheme)
+    off, ln, slots = striped_slots(layout, bases, rank)
+    if ln == 0:
+        return off, 0
+    flat = L.ptr_array([p for row in slots for p in row])
+    if pipeline is None:
+        outs = L.ptr_array([parity_out[s, i].data_ptr() for s in range(layout.stripes)
+                            for i in range(scheme.k)])
+        check(L.lib().gs_apply_device(enc.handle, layout.stripes, flat, outs, ln, stream), "encode_striped")
+    else:
+        outs = L.ptr_array([h_parity[s, i].data_ptr() + off for s in range(layout.stripes)
+                            for i in range(scheme.k)])
+        check(L.lib().gs_encode_offload(pipeline.handle, enc.handle, layout.stripes, flat, outs, ln, stream,
+                                        copy_stream if copy_stream is not None else stream),
+              "encode_striped")
+    return off, ln
+
+
+def reconstruct_striped(scheme: CodingScheme, layout: ShardLayout, bases: Sequence[int], rank: int,
+                        lost: ErasurePattern, h_parity, pipeline, stream: int,
+                        copy_stream: Optional[int] = None) -> Tuple[int, int]:
+    """K2 over this rank's byte range: parity range H2D'd from this rank's
+    pinned host slab, survivors pulled from peers, rebuilt bytes stored
+    straight into the lost workers' buffers (on their owners' GPUs)."""
+    dec = decoder(scheme, lost)
+    off, ln, slots = striped_slots(layout, bases, rank, lost.lost)
+    if ln == 0 or dec.n_out == 0:
+        return off, ln
+    n, k = scheme.n, scheme.k
+    full = []
+    for s in range(layout.stripes):
+        full.extend(slots[s])
+        for i in range(k):
+            full.append(None if lost.contains(n + i) else h_parity[s, i].data_ptr() + off)
+    outs = []
+    for s in range(layout.stripes):
+        for w in dec.out_index:
+            r, _ = layout.owner(w)
+            outs.append(bases[r] + layout.shard_offset(s, w) + off)
+    check(L.lib().gs_reconstruct_upload(pipeline.handle, dec.handle, layout.stripes, L.ptr_array(full),
+                                        L.ptr_array(outs), ln, stream,
+                                        copy_stream if copy_stream is not None else stream),
+          "reconstruct_striped")
+    return off, ln
