@@ -310,48 +310,63 @@ def run_ours(args):
             want = D.encode(scheme, ring[last, :2])
             ok_parity = torch.equal(want.cpu(), h_parity[:2])
 
-    # --- kernel-only K1 roofline (graph of launches over the ring) -----------
-    kern = {}
+    # --- kernel-only rooflines: K1 encode and K2 single-loss rebuild ---------
+    kern, kern2 = {}, {}
     if world == 1:
         par_dev = torch.empty((RING_BLOCKS, S, K_PARITY, SLICE), dtype=torch.uint8, device=dev)
+        rebuilt = torch.empty((RING_BLOCKS, S, SLICE), dtype=torch.uint8, device=dev)
         slots = [L.ptr_array([ring[b, s, j].data_ptr() for s in range(S) for j in range(N_SHARDS)])
                  for b in range(RING_BLOCKS)]
         outs = [L.ptr_array([par_dev[b, s, i].data_ptr() for s in range(S) for i in range(K_PARITY)])
                 for b in range(RING_BLOCKS)]
+        dec5 = decoder(scheme, ErasurePattern([5]))
+        dslots = [L.ptr_array([None if j == 5 else (ring[b, s, j].data_ptr() if j < N_SHARDS else
+                                                     par_dev[b, s, j - N_SHARDS].data_ptr())
+                               for s in range(S) for j in range(N_SHARDS + K_PARITY)])
+                  for b in range(RING_BLOCKS)]
+        douts = [L.ptr_array([rebuilt[b, s].data_ptr() for s in range(S)]) for b in range(RING_BLOCKS)]
+        peak, peak_src = load_peaks()
         ks = torch.cuda.Stream(device=dev)
 
-        def k1(b):
-            check(lib.gs_apply_device(enc.handle, S, slots[b], outs[b], SLICE, ks.cuda_stream), "k1")
-
-        with torch.cuda.stream(ks):
-            for b in range(RING_BLOCKS):
-                k1(b)
-        ks.synchronize()
-        reps = 4
-        g = torch.cuda.CUDAGraph()
-        with torch.cuda.graph(g, stream=ks):
-            for _ in range(reps):
+        def timed(launch, alg_bytes, name):
+            with torch.cuda.stream(ks):
                 for b in range(RING_BLOCKS):
-                    k1(b)
-        g.replay()
-        ks.synchronize()
-        n_graph = max(3, args.steps // (reps * RING_BLOCKS))
-        k0, k1e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        k0.record(ks)
-        for _ in range(n_graph):
-            g.replay()
-        k1e.record(ks)
-        k1e.synchronize()
-        per_launch_ms = k0.elapsed_time(k1e) / (n_graph * reps * RING_BLOCKS)
-        alg_bytes = S * (N_SHARDS + K_PARITY) * SLICE
-        peak, peak_src = load_peaks()
-        achieved = alg_bytes / (per_launch_ms * 1e-3) / 1e9
-        kern = {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
-                "frac": round(achieved / peak, 4), "traffic": args.traffic or ncu_traffic(),
-                "kernel": "k_apply_special<EncSpec<RS,8,2>> (K1)",
-                "per_launch_us": round(per_launch_ms * 1e3, 2),
-                "algorithmic_bytes_per_launch": alg_bytes, "peak_source": peak_src}
-        del par_dev, g
+                    launch(b)
+            ks.synchronize()
+            reps = 4
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g, stream=ks):
+                for _ in range(reps):
+                    for b in range(RING_BLOCKS):
+                        launch(b)
+            n_graph = max(3, args.steps // (reps * RING_BLOCKS))
+            with torch.cuda.stream(ks):
+                g.replay()
+                ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                ev0.record(ks)
+                for _ in range(n_graph):
+                    g.replay()
+                ev1.record(ks)
+            ev1.synchronize()
+            per_ms = ev0.elapsed_time(ev1) / (n_graph * reps * RING_BLOCKS)
+            achieved = alg_bytes / (per_ms * 1e-3) / 1e9
+            return {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
+                    "frac": round(achieved / peak, 4), "kernel": name,
+                    "per_launch_us": round(per_ms * 1e3, 2), "algorithmic_bytes_per_launch": alg_bytes,
+                    "peak_source": peak_src,
+                    "timing": f"CUDA graph of {reps * RING_BLOCKS} launches over {RING_BLOCKS} distinct "
+                              f"blocks, replayed {n_graph}x, events on the launch stream"}
+
+        kern = timed(lambda b: check(lib.gs_apply_device(enc.handle, S, slots[b], outs[b], SLICE,
+                                                         ks.cuda_stream), "k1"),
+                     S * (N_SHARDS + K_PARITY) * SLICE, "k_apply_special<EncSpec<RS,8,2>> (K1 encode)")
+        kern["traffic"] = args.traffic or ncu_traffic()
+        kern2 = timed(lambda b: check(lib.gs_apply_device(dec5.handle, S, dslots[b], douts[b], SLICE,
+                                                          ks.cuda_stream), "k2"),
+                      S * (N_SHARDS + 1) * SLICE,
+                      "k_apply_special<DecSpec<RS,8,2,lost{5}>> (K2 rebuild, 7 data + 1 parity -> 1)")
+        ok_parity &= torch.equal(rebuilt[RING_BLOCKS - 1], ring[RING_BLOCKS - 1, :, 5])
+        del par_dev, rebuilt
 
     # --- host link --------------------------------------------------------------
     link = host_link_peaks(torch, dev)
@@ -444,7 +459,7 @@ def run_ours(args):
                                  f"({RING_BLOCKS * data_bytes_step // world >> 20} MiB per GPU)",
                            "parallelism": f"stripes x{world} (peer loads over NVLink)" if world > 1 else
                            "single GPU holds all 8 TP shards"},
-                "roofline": kern or None, "host_link": host_link, "cpu_baseline": cpu, "e2e": e2e,
+                "roofline": kern or None, "roofline_k2": kern2 or None, "host_link": host_link, "cpu_baseline": cpu, "e2e": e2e,
                 "recovery_ms": recovery.get("c2_block_one_worker_ms"), "recovery": recovery,
                 "gpu_launches": launches, "clocks": clk.summary(), "parity_ok": bool(ok_parity)}
         print(json.dumps(line), flush=True)

@@ -110,6 +110,10 @@ int gs_apply_device(const gs_codec* c, int n_stripes, const void* const* slots,
  * A pipeline owns device staging (`staging_bytes`, split into a ring) and
  * events on `device`. Not thread-safe; one per (device, caller thread). */
 int gs_pipeline_create(int device, size_t staging_bytes, gs_pipeline** out);
+/* Resolve every kernel of the library on `device` (CUDA loads modules
+ * lazily at first launch); gs_pipeline_create calls it, so recovery never
+ * pays module loading on its critical path. */
+int gs_prewarm(int device);
 int gs_pipeline_destroy(gs_pipeline* p);
 
 /* Checkpoint offload (PAPER Alg.1 / checkpoint.hpp:143-146 + the host tier of

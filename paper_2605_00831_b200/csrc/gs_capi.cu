@@ -28,8 +28,10 @@ int special_decoders_kxor_4_1(SpecialEntry* out);
 int special_decoders_kxor_8_1(SpecialEntry* out);
 int special_decoders_kreedsolomon_4_1(SpecialEntry* out);
 int special_decoders_kreedsolomon_4_2(SpecialEntry* out);
-int special_decoders_kreedsolomon_6_2(SpecialEntry* out);
-int special_decoders_kreedsolomon_8_2(SpecialEntry* out);
+int special_decoders_kreedsolomon_6_2_e1(SpecialEntry* out);
+int special_decoders_kreedsolomon_6_2_e2(SpecialEntry* out);
+int special_decoders_kreedsolomon_8_2_e1(SpecialEntry* out);
+int special_decoders_kreedsolomon_8_2_e2(SpecialEntry* out);
 }  // namespace gsb
 
 using namespace gsb;
@@ -125,8 +127,10 @@ struct Registry {
     c += special_decoders_kxor_8_1(buf.data() + c);
     c += special_decoders_kreedsolomon_4_1(buf.data() + c);
     c += special_decoders_kreedsolomon_4_2(buf.data() + c);
-    c += special_decoders_kreedsolomon_6_2(buf.data() + c);
-    c += special_decoders_kreedsolomon_8_2(buf.data() + c);
+    c += special_decoders_kreedsolomon_6_2_e1(buf.data() + c);
+    c += special_decoders_kreedsolomon_6_2_e2(buf.data() + c);
+    c += special_decoders_kreedsolomon_8_2_e1(buf.data() + c);
+    c += special_decoders_kreedsolomon_8_2_e2(buf.data() + c);
     entries.assign(buf.begin(), buf.begin() + c);
   }
   const SpecialEntry* find(bool decoder, int kind, int n, int k, uint64_t mask) const {
@@ -286,10 +290,18 @@ int run_codec(const gs_codec* c, int n_stripes, SlotFn slot_ptr, OutFn out_ptr, 
       aligned &= aligned16(p);
     }
   }
-  const uint64_t tps64 = (len + kTile - 1) / kTile;
+  // The generic table is uploaded up front (the specialised path still needs
+  // it for ragged tails), so later calls never synchronise -- graph-safe.
+  const CoefWords* dw = nullptr;
+  if (int s = upload_words(c, dev, &dw)) return s;
   std::vector<const void*> ptrs;
 
-  if (c->special) {
+  // Specialised kernel over the 16-byte-aligned body.
+  uint64_t done = 0;
+  if (c->special && aligned && len >= kVec) {
+    const uint64_t body = len / kVec * kVec;
+    const uint64_t tile = static_cast<uint64_t>(c->special->tile);
+    const uint64_t tps64 = (body + tile - 1) / tile;
     const int stride = c->n_slots + c->n_out;
     const int per = kPtrCap / stride;
     const int occ = blocks_per_sm(dev, c->special->kernel, 0);
@@ -302,18 +314,20 @@ int run_codec(const gs_codec* c, int n_stripes, SlotFn slot_ptr, OutFn out_ptr, 
       }
       const uint64_t total = tps64 * cnt;
       if (total > 0xFFFFFFFFull) return fail(GS_INVALID_ARGUMENT, "apply: too many tiles in one launch");
-      TileGeom g{len, static_cast<uint32_t>(tps64), static_cast<uint32_t>(total), stride, c->n_slots,
-                 aligned ? 1 : 0};
+      TileGeom g{body, static_cast<uint32_t>(tps64), static_cast<uint32_t>(total), stride, c->n_slots, 1};
       const int grid = static_cast<int>(std::min<uint64_t>(total, static_cast<uint64_t>(occ) * sms));
       cudaError_t e = c->special->launch(ptrs.data(), cnt * stride, g, grid, st);
       if (e != cudaSuccess) return fail(GS_CUDA_ERROR, "special kernel launch: %s", cudaGetErrorString(e));
       g_launches.fetch_add(1, std::memory_order_relaxed);
     }
-    return GS_OK;
+    done = body;
+    if (done == len) return GS_OK;
   }
 
-  const CoefWords* dw = nullptr;
-  if (int s = upload_words(c, dev, &dw)) return s;
+  // Generic kernel: everything, or the ragged tail [done, len).
+  const uint64_t glen = len - done;
+  const uint64_t tps64 = (glen + kTile - 1) / kTile;
+  const bool galigned = aligned && (done % kVec == 0);
   const int ns = static_cast<int>(c->used.size());
   const int stride = ns + c->n_out;
   const int per = kPtrCap / stride;
@@ -322,15 +336,17 @@ int run_codec(const gs_codec* c, int n_stripes, SlotFn slot_ptr, OutFn out_ptr, 
     const int cnt = std::min(per, n_stripes - s0);
     ptrs.assign(static_cast<size_t>(cnt) * stride, nullptr);
     for (int s = 0; s < cnt; ++s) {
-      for (int u = 0; u < ns; ++u) ptrs[s * stride + u] = slot_ptr(s0 + s, c->used[u]);
-      for (int i = 0; i < c->n_out; ++i) ptrs[s * stride + ns + i] = out_ptr(s0 + s, i);
+      for (int u = 0; u < ns; ++u)
+        ptrs[s * stride + u] = static_cast<const uint8_t*>(slot_ptr(s0 + s, c->used[u])) + done;
+      for (int i = 0; i < c->n_out; ++i)
+        ptrs[s * stride + ns + i] = static_cast<const uint8_t*>(out_ptr(s0 + s, i)) + done;
     }
     const uint64_t total = tps64 * cnt;
     if (total > 0xFFFFFFFFull) return fail(GS_INVALID_ARGUMENT, "apply: too many tiles in one launch");
     for (int r0 = 0; r0 < c->n_out; r0 += kMaxGenericRows) {
       const int kb = std::min(kMaxGenericRows, c->n_out - r0);
-      TileGeom g{len, static_cast<uint32_t>(tps64), static_cast<uint32_t>(total), stride, ns + r0,
-                 aligned ? 1 : 0};
+      TileGeom g{glen, static_cast<uint32_t>(tps64), static_cast<uint32_t>(total), stride, ns + r0,
+                 galigned ? 1 : 0};
       const size_t smem = static_cast<size_t>(kb) * ns * sizeof(CoefWords);
       const int occ = blocks_per_sm(dev, generic_kernel(kb), smem);
       const int grid = static_cast<int>(std::min<uint64_t>(total, static_cast<uint64_t>(occ) * sms));
@@ -622,6 +638,27 @@ int gs_apply_device(const gs_codec* c, int n_stripes, const void* const* slots, 
 // ============================================================================
 // pipelines
 // ============================================================================
+int gs_prewarm(int device) {
+  // CUDA loads kernels lazily on first launch; a recovery must not pay that
+  // on its critical path, so resolve every kernel (and its occupancy) now.
+  DeviceGuard g(device);
+  const int sms = device_sms(device);
+  (void)sms;
+  for (const auto& e : registry().entries) {
+    cudaFuncAttributes a;
+    GS_CUDA(cudaFuncGetAttributes(&a, e.kernel));
+    blocks_per_sm(device, e.kernel, 0);
+  }
+  for (int kb = 1; kb <= kMaxGenericRows; ++kb) {
+    cudaFuncAttributes a;
+    GS_CUDA(cudaFuncGetAttributes(&a, generic_kernel(kb)));
+  }
+  cudaFuncAttributes a;
+  GS_CUDA(cudaFuncGetAttributes(&a, reinterpret_cast<const void*>(&k_ground_truth)));
+  GS_CUDA(cudaFuncGetAttributes(&a, reinterpret_cast<const void*>(&k_pad_partial)));
+  return GS_OK;
+}
+
 int gs_pipeline_create(int device, size_t staging_bytes, gs_pipeline** out) {
   if (!out) return fail(GS_INVALID_ARGUMENT, "pipeline_create: out is NULL");
   *out = nullptr;
@@ -645,6 +682,10 @@ int gs_pipeline_create(int device, size_t staging_bytes, gs_pipeline** out) {
   cudaStreamCreateWithFlags(&p->s_h2d, cudaStreamNonBlocking);
   cudaStreamCreateWithFlags(&p->s_comp, cudaStreamNonBlocking);
   cudaStreamCreateWithFlags(&p->s_d2h, cudaStreamNonBlocking);
+  if (int st = gs_prewarm(device)) {
+    gs_pipeline_destroy(p);
+    return st;
+  }
   *out = p;
   return GS_OK;
 }

@@ -81,15 +81,20 @@ __device__ __forceinline__ uint32_t& word(uint4& v, int w) {
 
 // Byte-granular load/store of up to 16 bytes (tail of a shard, or shards
 // whose base pointers are not 16-B aligned).
+// Fully unrolled with guards so the words stay in registers.
 __device__ __forceinline__ uint4 ld_partial(const uint8_t* p, int nbytes) {
   uint32_t w[4] = {0, 0, 0, 0};
-  for (int b = 0; b < nbytes; ++b) w[b >> 2] |= static_cast<uint32_t>(p[b]) << (8 * (b & 3));
+#pragma unroll
+  for (int b = 0; b < 16; ++b)
+    if (b < nbytes) w[b >> 2] |= static_cast<uint32_t>(p[b]) << (8 * (b & 3));
   return make_uint4(w[0], w[1], w[2], w[3]);
 }
 
 __device__ __forceinline__ void st_partial(uint8_t* p, const uint4& v, int nbytes) {
   const uint32_t w[4] = {v.x, v.y, v.z, v.w};
-  for (int b = 0; b < nbytes; ++b) p[b] = static_cast<uint8_t>(w[b >> 2] >> (8 * (b & 3)));
+#pragma unroll
+  for (int b = 0; b < 16; ++b)
+    if (b < nbytes) p[b] = static_cast<uint8_t>(w[b >> 2] >> (8 * (b & 3)));
 }
 
 // ---- tile walk shared by both back ends ------------------------------------
@@ -147,34 +152,49 @@ __device__ constexpr bool column_used(int j) {
   return false;
 }
 
-template <class Spec, int CAP>
+// Each CTA tile covers kThreads * 16 * U bytes of every shard; thread t owns
+// the 16-byte groups t, t + kThreads, ... so every warp access is 512
+// contiguous bytes, and all loads of a tile are issued before any
+// arithmetic. The host guarantees 16-B aligned pointers and len % 16 == 0
+// (a ragged tail or misaligned shards go to the generic kernel instead), so
+// this kernel carries no byte-granular code at all.
+template <class Spec, int CAP, int U>
 __global__ void __launch_bounds__(kThreads) k_apply_special(const PtrTable<CAP> tab, const TileGeom g) {
+  constexpr uint64_t kSpan = static_cast<uint64_t>(kThreads) * kVec;
   for (uint32_t t = blockIdx.x; t < g.total; t += gridDim.x) {
     const uint32_t s = t / g.tps;
-    const uint64_t off = static_cast<uint64_t>(t - s * g.tps) * kTile + threadIdx.x * kVec;
-    if (off >= g.len) continue;
+    const uint64_t off0 = static_cast<uint64_t>(t - s * g.tps) * (kSpan * U) + threadIdx.x * kVec;
     const int base = static_cast<int>(s) * g.stride;
-    const bool full = g.aligned && off + kVec <= g.len;
-    const int nb = full ? kVec : static_cast<int>(g.len - off < kVec ? g.len - off : kVec);
-    uint4 src[Spec::NS];
+    if (off0 + (U - 1) * kSpan < g.len) {  // whole tile row in range: no per-group guards
+      uint4 src[U][Spec::NS];
 #pragma unroll
-    for (int j = 0; j < Spec::NS; ++j) {
-      if (column_used<Spec>(j)) {
-        const uint8_t* p = tab.p[base + j] + off;
-        src[j] = full ? ld_stream(p) : ld_partial(p, nb);
-      } else {
-        src[j] = make_uint4(0, 0, 0, 0);
+      for (int j = 0; j < Spec::NS; ++j)
+#pragma unroll
+        for (int u = 0; u < U; ++u)
+          src[u][j] = column_used<Spec>(j) ? ld_stream(tab.p[base + j] + off0 + u * kSpan)
+                                           : make_uint4(0, 0, 0, 0);
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        uint4 out[Spec::NO];
+        horner_apply<Spec>(src[u], out);
+#pragma unroll
+        for (int i = 0; i < Spec::NO; ++i)
+          st_stream(const_cast<uint8_t*>(tab.p[base + g.out0 + i]) + off0 + u * kSpan, out[i]);
       }
-    }
-    uint4 out[Spec::NO];
-    horner_apply<Spec>(src, out);
+    } else {
+#pragma unroll 1
+      for (int u = 0; u < U; ++u) {
+        const uint64_t off = off0 + u * kSpan;
+        if (off >= g.len) break;
+        uint4 src[Spec::NS];
 #pragma unroll
-    for (int i = 0; i < Spec::NO; ++i) {
-      uint8_t* p = const_cast<uint8_t*>(tab.p[base + g.out0 + i]) + off;
-      if (full)
-        st_stream(p, out[i]);
-      else
-        st_partial(p, out[i], nb);
+        for (int j = 0; j < Spec::NS; ++j)
+          src[j] = column_used<Spec>(j) ? ld_stream(tab.p[base + j] + off) : make_uint4(0, 0, 0, 0);
+        uint4 out[Spec::NO];
+        horner_apply<Spec>(src, out);
+#pragma unroll
+        for (int i = 0; i < Spec::NO; ++i) st_stream(const_cast<uint8_t*>(tab.p[base + g.out0 + i]) + off, out[i]);
+      }
     }
   }
 }
@@ -242,7 +262,63 @@ __device__ __forceinline__ void pair_finish(uint32_t accP, uint32_t accQ, uint32
   y = prmt(accP, accQ, 0x7531u);
 }
 
-// coef: rows x ns CoefWords for this launch's row group (row-major).
+// One 16-byte group of every source -> KB outputs. FULL: 16-B vector
+// loads/stores; otherwise byte-granular (ragged tail / misaligned shards).
+template <int KB, int CAP, bool FULL>
+__device__ __forceinline__ void generic_group(const PtrTable<CAP>& tab, int base, int out0, uint64_t off,
+                                              int nb, const CoefWords* sc, int ns) {
+  uint32_t acc[KB][4];
+#pragma unroll
+  for (int r = 0; r < KB; ++r)
+#pragma unroll
+    for (int q = 0; q < 4; ++q) acc[r][q] = 0;
+  int j = 0;
+  for (; j + 4 <= ns; j += 4) {
+    uint4 d[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const uint8_t* p = tab.p[base + j + u] + off;
+      d[u] = FULL ? ld_stream(p) : ld_partial(p, nb);
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const PairSel s0 = pair_setup(d[u].x, d[u].y);
+      const PairSel s1 = pair_setup(d[u].z, d[u].w);
+#pragma unroll
+      for (int r = 0; r < KB; ++r) {
+        const CoefWords c = sc[r * ns + j + u];
+        pair_mac(acc[r][0], acc[r][1], s0, c);
+        pair_mac(acc[r][2], acc[r][3], s1, c);
+      }
+    }
+  }
+  for (; j < ns; ++j) {
+    const uint8_t* p = tab.p[base + j] + off;
+    const uint4 d = FULL ? ld_stream(p) : ld_partial(p, nb);
+    const PairSel s0 = pair_setup(d.x, d.y);
+    const PairSel s1 = pair_setup(d.z, d.w);
+#pragma unroll
+    for (int r = 0; r < KB; ++r) {
+      const CoefWords c = sc[r * ns + j];
+      pair_mac(acc[r][0], acc[r][1], s0, c);
+      pair_mac(acc[r][2], acc[r][3], s1, c);
+    }
+  }
+#pragma unroll
+  for (int r = 0; r < KB; ++r) {
+    uint4 o;
+    pair_finish(acc[r][0], acc[r][1], o.x, o.y);
+    pair_finish(acc[r][2], acc[r][3], o.z, o.w);
+    uint8_t* p = const_cast<uint8_t*>(tab.p[base + out0 + r]) + off;
+    if (FULL)
+      st_stream(p, o);
+    else
+      st_partial(p, o, nb);
+  }
+}
+
+// coef: rows x ns CoefWords for this launch's row group (row-major), staged
+// in shared memory (broadcast reads: every thread uses the same entry).
 template <int KB, int CAP>
 __global__ void __launch_bounds__(kThreads) k_apply_generic(const PtrTable<CAP> tab, const TileGeom g,
                                                             const CoefWords* __restrict__ coef,
@@ -257,57 +333,11 @@ __global__ void __launch_bounds__(kThreads) k_apply_generic(const PtrTable<CAP> 
     const uint64_t off = static_cast<uint64_t>(t - s * g.tps) * kTile + threadIdx.x * kVec;
     if (off >= g.len) continue;
     const int base = static_cast<int>(s) * g.stride;
-    const bool full = g.aligned && off + kVec <= g.len;
-    const int nb = full ? kVec : static_cast<int>(g.len - off < kVec ? g.len - off : kVec);
-
-    uint32_t acc[KB][4];
-#pragma unroll
-    for (int r = 0; r < KB; ++r)
-#pragma unroll
-      for (int q = 0; q < 4; ++q) acc[r][q] = 0;
-
-    int j = 0;
-    for (; j + 4 <= ns; j += 4) {
-      uint4 d[4];
-#pragma unroll
-      for (int u = 0; u < 4; ++u) {
-        const uint8_t* p = tab.p[base + j + u] + off;
-        d[u] = full ? ld_stream(p) : ld_partial(p, nb);
-      }
-#pragma unroll
-      for (int u = 0; u < 4; ++u) {
-        const PairSel s0 = pair_setup(d[u].x, d[u].y);
-        const PairSel s1 = pair_setup(d[u].z, d[u].w);
-#pragma unroll
-        for (int r = 0; r < KB; ++r) {
-          const CoefWords c = sc[r * ns + j + u];
-          pair_mac(acc[r][0], acc[r][1], s0, c);
-          pair_mac(acc[r][2], acc[r][3], s1, c);
-        }
-      }
-    }
-    for (; j < ns; ++j) {
-      const uint8_t* p = tab.p[base + j] + off;
-      const uint4 d = full ? ld_stream(p) : ld_partial(p, nb);
-      const PairSel s0 = pair_setup(d.x, d.y);
-      const PairSel s1 = pair_setup(d.z, d.w);
-#pragma unroll
-      for (int r = 0; r < KB; ++r) {
-        const CoefWords c = sc[r * ns + j];
-        pair_mac(acc[r][0], acc[r][1], s0, c);
-        pair_mac(acc[r][2], acc[r][3], s1, c);
-      }
-    }
-#pragma unroll
-    for (int r = 0; r < KB; ++r) {
-      uint4 o;
-      pair_finish(acc[r][0], acc[r][1], o.x, o.y);
-      pair_finish(acc[r][2], acc[r][3], o.z, o.w);
-      uint8_t* p = const_cast<uint8_t*>(tab.p[base + g.out0 + r]) + off;
-      if (full)
-        st_stream(p, o);
-      else
-        st_partial(p, o, nb);
+    if (g.aligned && off + kVec <= g.len) {
+      generic_group<KB, CAP, true>(tab, base, g.out0, off, kVec, sc, ns);
+    } else {
+      const uint64_t rem = g.len - off;
+      generic_group<KB, CAP, false>(tab, base, g.out0, off, static_cast<int>(rem < kVec ? rem : kVec), sc, ns);
     }
   }
 }

@@ -23,6 +23,8 @@ using KernelAddr = const void*;
 
 // Pointer-table capacity of one launch (kernel parameter space: 4 KiB).
 constexpr int kPtrCap = 508;
+// 16-byte groups per thread per source per tile of the specialised kernels.
+constexpr int kSpecialU = 2;
 
 struct SpecialEntry {
   bool decoder;
@@ -30,6 +32,7 @@ struct SpecialEntry {
   uint64_t mask;
   LaunchFn launch;
   KernelAddr kernel;
+  int tile;  // bytes of every shard per CTA tile
 };
 
 constexpr int popcount64(uint64_t x) {
@@ -77,7 +80,7 @@ cudaError_t launch_special(const void* const* ptrs, int count, const TileGeom& g
                            cudaStream_t st) {
   PtrTable<CAP> tab;
   for (int i = 0; i < count; ++i) tab.p[i] = static_cast<const uint8_t*>(ptrs[i]);
-  k_apply_special<Spec, CAP><<<grid, kThreads, 0, st>>>(tab, g);
+  k_apply_special<Spec, CAP, kSpecialU><<<grid, kThreads, 0, st>>>(tab, g);
   return cudaGetLastError();
 }
 
@@ -90,7 +93,8 @@ SpecialEntry make_entry(bool decoder, int kind, int n, int k, uint64_t mask) {
   e.k = k;
   e.mask = mask;
   e.launch = &launch_special<Spec, kPtrCap>;
-  e.kernel = reinterpret_cast<KernelAddr>(&k_apply_special<Spec, kPtrCap>);
+  e.kernel = reinterpret_cast<KernelAddr>(&k_apply_special<Spec, kPtrCap, kSpecialU>);
+  e.tile = kThreads * kVec * kSpecialU;
   return e;
 }
 
@@ -99,25 +103,27 @@ void add_encoder(SpecialEntry* out, int& cnt) {
   out[cnt++] = make_entry<EncSpec<KIND, N, K>>(false, KIND, N, K, 0);
 }
 
-template <int KIND, int N, int K, uint64_t MASK>
+template <int KIND, int N, int K, int E, uint64_t MASK>
 void add_decoder_if_canonical(SpecialEntry* out, int& cnt) {
   constexpr int tol = KIND == kReedSolomon ? K : 1;
   constexpr uint64_t data_bits = MASK & ((1ull << N) - 1);
-  if constexpr (popcount64(MASK) <= tol && data_bits != 0 &&
+  if constexpr (popcount64(MASK) <= tol && data_bits != 0 && (E == 0 || popcount64(data_bits) == E) &&
                 canonical_mask(KIND, N, K, MASK) == MASK &&
                 decode_plan_mask(KIND, N, K, MASK).ok) {
     out[cnt++] = make_entry<DecSpec<KIND, N, K, MASK>>(true, KIND, N, K, MASK);
   }
 }
 
-template <int KIND, int N, int K, uint64_t... M>
+template <int KIND, int N, int K, int E, uint64_t... M>
 void add_decoders_impl(SpecialEntry* out, int& cnt, std::integer_sequence<uint64_t, M...>) {
-  (add_decoder_if_canonical<KIND, N, K, M>(out, cnt), ...);
+  (add_decoder_if_canonical<KIND, N, K, E, M>(out, cnt), ...);
 }
 
-template <int KIND, int N, int K>
+// All canonical patterns of the scheme (E = 0) or only those losing exactly
+// E data shards (lets one scheme's decoders spread over several TUs).
+template <int KIND, int N, int K, int E = 0>
 void add_decoders(SpecialEntry* out, int& cnt) {
-  add_decoders_impl<KIND, N, K>(out, cnt, std::make_integer_sequence<uint64_t, (1ull << (N + K))>{});
+  add_decoders_impl<KIND, N, K, E>(out, cnt, std::make_integer_sequence<uint64_t, (1ull << (N + K))>{});
 }
 
 // Filled by gs_special.cu.
