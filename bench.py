@@ -357,9 +357,19 @@ def run_ours(args):
                     "timing": f"CUDA graph of {reps * RING_BLOCKS} launches over {RING_BLOCKS} distinct "
                               f"blocks, replayed {n_graph}x, events on the launch stream"}
 
+        variants = {}
+        for v, vname in ((0, "ldg128"), (1, "bulk_smem_pipeline")):
+            check(lib.gs_set_kernel_variant(v), "variant")
+            variants[vname] = timed(
+                lambda b: check(lib.gs_apply_device(enc.handle, S, slots[b], outs[b], SLICE, ks.cuda_stream),
+                                "k1"), S * (N_SHARDS + K_PARITY) * SLICE, f"K1 {vname}")["per_launch_us"]
+        best = min(variants, key=variants.get)
+        check(lib.gs_set_kernel_variant(0 if best == "ldg128" else 1), "variant")
         kern = timed(lambda b: check(lib.gs_apply_device(enc.handle, S, slots[b], outs[b], SLICE,
                                                          ks.cuda_stream), "k1"),
-                     S * (N_SHARDS + K_PARITY) * SLICE, "k_apply_special<EncSpec<RS,8,2>> (K1 encode)")
+                     S * (N_SHARDS + K_PARITY) * SLICE,
+                     f"k_apply_special{'_bulk' if best != 'ldg128' else ''}<EncSpec<RS,8,2>> (K1 encode)")
+        kern["variants_us_per_launch"] = variants
         kern["traffic"] = args.traffic or ncu_traffic()
         kern2 = timed(lambda b: check(lib.gs_apply_device(dec5.handle, S, dslots[b], douts[b], SLICE,
                                                           ks.cuda_stream), "k2"),

@@ -114,6 +114,11 @@ int gs_pipeline_create(int device, size_t staging_bytes, gs_pipeline** out);
  * lazily at first launch); gs_pipeline_create calls it, so recovery never
  * pays module loading on its critical path. */
 int gs_prewarm(int device);
+/* Variant of the specialised kernels for aligned bodies (process-wide):
+ * 0 = register-streaming LDG.128 kernel, 1 = bulk-copy (cp.async.bulk)
+ * shared-memory pipeline with producer/consumer warps (default). Both are
+ * bit-identical; exposed for benchmarking and cross-checking. */
+int gs_set_kernel_variant(int variant);
 int gs_pipeline_destroy(gs_pipeline* p);
 
 /* Checkpoint offload (PAPER Alg.1 / checkpoint.hpp:143-146 + the host tier of

@@ -45,6 +45,7 @@ SIGNATURES = {
     "gs_pipeline_create": (_i, [_i, _sz, _vpp]),
     "gs_pipeline_destroy": (_i, [_vp]),
     "gs_prewarm": (_i, [_i]),
+    "gs_set_kernel_variant": (_i, [_i]),
     "gs_encode_offload": (_i, [_vp, _vp, _i, _vpp, _vpp, _sz, _vp, _vp]),
     "gs_reconstruct_upload": (_i, [_vp, _vp, _i, _vpp, _vpp, _sz, _vp, _vp]),
     "gs_encode_host": (_i, [_vp, _vp, _vpp, _vpp, _sz]),

@@ -103,16 +103,27 @@ int device_sms(int dev) {
   return g_dev[dev].sms;
 }
 
-int blocks_per_sm(int dev, const void* kernel, size_t smem) {
+int blocks_per_sm(int dev, const void* kernel, size_t smem, int threads = kThreads) {
   std::lock_guard<std::mutex> lk(g_dev_mu);
   auto key = std::make_pair(dev, kernel);
   auto it = g_occ.find(key);
   if (it != g_occ.end()) return it->second;
+  if (smem > 48 * 1024)
+    cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
   int b = 0;
-  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, kernel, kThreads, smem) != cudaSuccess || b < 1)
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, kernel, threads, smem) != cudaSuccess || b < 1)
     b = 1;
   g_occ[key] = b;
   return b;
+}
+
+// Which specialised kernel variant serves aligned bodies: 0 = register
+// (LDG.128) streaming, 1 = bulk-copy smem pipeline. gs_set_kernel_variant.
+std::atomic<int> g_variant{1};
+
+int bulk_stages(const SpecialEntry* e) {
+  const size_t per = static_cast<size_t>(e->used_cols) * e->tile_bulk;
+  return per ? static_cast<int>(std::min<size_t>(bulk::kMaxStages, (kBulkSmemMax - kBulkSmemHeader) / per)) : 0;
 }
 
 // Registry of compile-time kernels, built once.
@@ -300,11 +311,17 @@ int run_codec(const gs_codec* c, int n_stripes, SlotFn slot_ptr, OutFn out_ptr, 
   uint64_t done = 0;
   if (c->special && aligned && len >= kVec) {
     const uint64_t body = len / kVec * kVec;
-    const uint64_t tile = static_cast<uint64_t>(c->special->tile);
+    const int stages = bulk_stages(c->special);
+    const bool use_bulk = g_variant.load(std::memory_order_relaxed) == 1 && stages >= 2;
+    const uint64_t tile = static_cast<uint64_t>(use_bulk ? c->special->tile_bulk : c->special->tile);
     const uint64_t tps64 = (body + tile - 1) / tile;
     const int stride = c->n_slots + c->n_out;
     const int per = kPtrCap / stride;
-    const int occ = blocks_per_sm(dev, c->special->kernel, 0);
+    const size_t smem = use_bulk ? kBulkSmemHeader + static_cast<size_t>(stages) * c->special->used_cols *
+                                                         c->special->tile_bulk
+                                 : 0;
+    const int occ = use_bulk ? blocks_per_sm(dev, c->special->kernel_bulk, smem, kBulkThreads)
+                             : blocks_per_sm(dev, c->special->kernel, 0);
     for (int s0 = 0; s0 < n_stripes; s0 += per) {
       const int cnt = std::min(per, n_stripes - s0);
       ptrs.assign(static_cast<size_t>(cnt) * stride, nullptr);
@@ -316,7 +333,8 @@ int run_codec(const gs_codec* c, int n_stripes, SlotFn slot_ptr, OutFn out_ptr, 
       if (total > 0xFFFFFFFFull) return fail(GS_INVALID_ARGUMENT, "apply: too many tiles in one launch");
       TileGeom g{body, static_cast<uint32_t>(tps64), static_cast<uint32_t>(total), stride, c->n_slots, 1};
       const int grid = static_cast<int>(std::min<uint64_t>(total, static_cast<uint64_t>(occ) * sms));
-      cudaError_t e = c->special->launch(ptrs.data(), cnt * stride, g, grid, st);
+      cudaError_t e = use_bulk ? c->special->launch_bulk(ptrs.data(), cnt * stride, g, grid, st, stages, smem)
+                               : c->special->launch(ptrs.data(), cnt * stride, g, grid, st);
       if (e != cudaSuccess) return fail(GS_CUDA_ERROR, "special kernel launch: %s", cudaGetErrorString(e));
       g_launches.fetch_add(1, std::memory_order_relaxed);
     }
@@ -638,6 +656,12 @@ int gs_apply_device(const gs_codec* c, int n_stripes, const void* const* slots, 
 // ============================================================================
 // pipelines
 // ============================================================================
+int gs_set_kernel_variant(int variant) {
+  if (variant != 0 && variant != 1) return fail(GS_INVALID_ARGUMENT, "kernel variant must be 0 or 1");
+  g_variant.store(variant);
+  return GS_OK;
+}
+
 int gs_prewarm(int device) {
   // CUDA loads kernels lazily on first launch; a recovery must not pay that
   // on its critical path, so resolve every kernel (and its occupancy) now.
@@ -648,6 +672,11 @@ int gs_prewarm(int device) {
     cudaFuncAttributes a;
     GS_CUDA(cudaFuncGetAttributes(&a, e.kernel));
     blocks_per_sm(device, e.kernel, 0);
+    GS_CUDA(cudaFuncGetAttributes(&a, e.kernel_bulk));
+    const int stages = bulk_stages(&e);
+    if (stages >= 2)
+      blocks_per_sm(device, e.kernel_bulk,
+                    kBulkSmemHeader + static_cast<size_t>(stages) * e.used_cols * e.tile_bulk, kBulkThreads);
   }
   for (int kb = 1; kb <= kMaxGenericRows; ++kb) {
     cudaFuncAttributes a;

@@ -342,4 +342,168 @@ __global__ void __launch_bounds__(kThreads) k_apply_generic(const PtrTable<CAP> 
   }
 }
 
+// ============================================================================
+// Bulk-copy pipelined specialised kernel (K1/K2 "bulk" variant).
+//
+// One persistent CTA per SM: warp 0 is a producer that streams each tile of
+// every used source into a ring of shared-memory stages with
+// cp.async.bulk (the TMA engine's 1-D bulk path, completion on an mbarrier);
+// CW consumer warps wait on the stage's full barrier, read their 16-byte
+// groups with LDS.128, run the Horner arithmetic and store the outputs with
+// STG.128, then release the stage. Memory-level parallelism is set by the
+// ring depth (stages x sources x tile bytes, ~200 KB per SM), independent of
+// registers and occupancy; the arithmetic of tile i overlaps the loads of
+// tiles i+1..i+S-1.
+// ============================================================================
+namespace bulk {
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n"
+      "WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+      "@!p bra WAIT_%=;\n\t}" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+__device__ __forceinline__ uint4 lds128(const uint8_t* p) {
+  uint4 r;
+  asm volatile("ld.shared.v4.u32 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
+               : "r"(smem_u32(p)));
+  return r;
+}
+
+constexpr int kMaxStages = 8;
+
+template <class Spec>
+struct UsedCols {
+  int n = 0;
+  int col[2 * kMaxSpecial] = {};
+};
+
+template <class Spec>
+__host__ __device__ constexpr UsedCols<Spec> used_cols() {
+  constexpr CoefMatrix m = Spec::matrix();
+  UsedCols<Spec> u{};
+  for (int j = 0; j < Spec::NS; ++j) {
+    bool any = false;
+    for (int i = 0; i < Spec::NO; ++i) any = any || m.c[i][j] != 0;
+    if (any) u.col[u.n++] = j;
+  }
+  return u;
+}
+
+}  // namespace bulk
+
+// CW consumer warps; every consumer thread owns U 16-byte groups per tile,
+// so a tile is CW*32*16*U bytes of every used source.
+template <class Spec, int CAP, int CW, int U>
+__global__ void __launch_bounds__((CW + 1) * 32, 1)
+    k_apply_special_bulk(const PtrTable<CAP> tab, const TileGeom g, int stages) {
+  constexpr bulk::UsedCols<Spec> uc = bulk::used_cols<Spec>();
+  constexpr int NU = uc.n;
+  constexpr uint32_t T = CW * 32 * kVec * U;  // tile bytes per source
+  extern __shared__ __align__(128) uint8_t smem[];
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem);
+  uint64_t* empty = full + bulk::kMaxStages;
+  uint8_t* ring = smem + 2 * bulk::kMaxStages * sizeof(uint64_t) + 112;  // 128-B aligned data
+
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < stages; ++s) {
+      bulk::mbar_init(&full[s], 1);
+      bulk::mbar_init(&empty[s], CW);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+
+  if (warp == CW) {  // ---- producer warp (one elected lane issues) ----
+    if (lane == 0) {
+      int stage = 0;
+      uint32_t phase = 0;
+      for (uint32_t t = blockIdx.x; t < g.total; t += gridDim.x) {
+        const uint32_t s = t / g.tps;
+        const uint64_t off = static_cast<uint64_t>(t - s * g.tps) * T;
+        const uint32_t size = static_cast<uint32_t>(g.len - off < T ? g.len - off : T);
+        const int base = static_cast<int>(s) * g.stride;
+        bulk::mbar_wait(&empty[stage], phase ^ 1u);
+        bulk::mbar_expect_tx(&full[stage], size * NU);
+#pragma unroll
+        for (int u = 0; u < NU; ++u)
+          bulk::bulk_g2s(ring + (static_cast<size_t>(stage) * NU + u) * T, tab.p[base + uc.col[u]] + off, size,
+                         &full[stage]);
+        if (++stage == stages) {
+          stage = 0;
+          phase ^= 1u;
+        }
+      }
+    }
+    return;
+  }
+
+  // ---- consumer warps ----
+  int stage = 0;
+  uint32_t phase = 0;
+  const uint32_t tid = threadIdx.x;  // 0 .. CW*32-1
+  for (uint32_t t = blockIdx.x; t < g.total; t += gridDim.x) {
+    const uint32_t s = t / g.tps;
+    const uint64_t off = static_cast<uint64_t>(t - s * g.tps) * T;
+    const uint32_t size = static_cast<uint32_t>(g.len - off < T ? g.len - off : T);
+    const int base = static_cast<int>(s) * g.stride;
+    bulk::mbar_wait(&full[stage], phase);
+    const uint8_t* st = ring + static_cast<size_t>(stage) * NU * T;
+    uint4 src[U][Spec::NS];
+#pragma unroll
+    for (int v = 0; v < U; ++v) {
+      const uint32_t idx = (v * CW * 32 + tid) * kVec;
+#pragma unroll
+      for (int j = 0; j < Spec::NS; ++j) src[v][j] = make_uint4(0, 0, 0, 0);
+      if (idx < size) {
+#pragma unroll
+        for (int u = 0; u < NU; ++u) src[v][uc.col[u]] = bulk::lds128(st + u * T + idx);
+      }
+    }
+    __syncwarp();
+    if (lane == 0) bulk::mbar_arrive(&empty[stage]);
+#pragma unroll
+    for (int v = 0; v < U; ++v) {
+      const uint32_t idx = (v * CW * 32 + tid) * kVec;
+      if (idx < size) {
+        uint4 out[Spec::NO];
+        horner_apply<Spec>(src[v], out);
+#pragma unroll
+        for (int i = 0; i < Spec::NO; ++i)
+          st_stream(const_cast<uint8_t*>(tab.p[base + g.out0 + i]) + off + idx, out[i]);
+      }
+    }
+    if (++stage == stages) {
+      stage = 0;
+      phase ^= 1u;
+    }
+  }
+}
+
 }  // namespace gsb

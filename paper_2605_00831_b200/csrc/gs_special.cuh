@@ -20,11 +20,20 @@ namespace gsb {
 using LaunchFn = cudaError_t (*)(const void* const* ptrs, int count, const TileGeom& g, int grid,
                                  cudaStream_t st);
 using KernelAddr = const void*;
+using BulkLaunchFn = cudaError_t (*)(const void* const* ptrs, int count, const TileGeom& g, int grid,
+                                     cudaStream_t st, int stages, size_t smem);
 
 // Pointer-table capacity of one launch (kernel parameter space: 4 KiB).
 constexpr int kPtrCap = 508;
 // 16-byte groups per thread per source per tile of the specialised kernels.
 constexpr int kSpecialU = 2;
+// Consumer warps and 16-byte groups per consumer thread of the bulk variant.
+constexpr int kBulkCW = 8;
+constexpr int kBulkU = 1;
+constexpr int kBulkThreads = (kBulkCW + 1) * 32;
+constexpr int kBulkTile = kBulkCW * 32 * kVec * kBulkU;
+constexpr size_t kBulkSmemHeader = 2 * bulk::kMaxStages * sizeof(uint64_t) + 112;
+constexpr size_t kBulkSmemMax = 200 * 1024;
 
 struct SpecialEntry {
   bool decoder;
@@ -33,6 +42,11 @@ struct SpecialEntry {
   LaunchFn launch;
   KernelAddr kernel;
   int tile;  // bytes of every shard per CTA tile
+  // bulk-copy pipelined variant (k_apply_special_bulk)
+  BulkLaunchFn launch_bulk;
+  KernelAddr kernel_bulk;
+  int tile_bulk;
+  int used_cols;  // sources streamed per tile
 };
 
 constexpr int popcount64(uint64_t x) {
@@ -84,6 +98,15 @@ cudaError_t launch_special(const void* const* ptrs, int count, const TileGeom& g
   return cudaGetLastError();
 }
 
+template <class Spec, int CAP>
+cudaError_t launch_special_bulk(const void* const* ptrs, int count, const TileGeom& g, int grid,
+                                cudaStream_t st, int stages, size_t smem) {
+  PtrTable<CAP> tab;
+  for (int i = 0; i < count; ++i) tab.p[i] = static_cast<const uint8_t*>(ptrs[i]);
+  k_apply_special_bulk<Spec, CAP, kBulkCW, kBulkU><<<grid, kBulkThreads, smem, st>>>(tab, g, stages);
+  return cudaGetLastError();
+}
+
 template <class Spec>
 SpecialEntry make_entry(bool decoder, int kind, int n, int k, uint64_t mask) {
   SpecialEntry e;
@@ -95,6 +118,10 @@ SpecialEntry make_entry(bool decoder, int kind, int n, int k, uint64_t mask) {
   e.launch = &launch_special<Spec, kPtrCap>;
   e.kernel = reinterpret_cast<KernelAddr>(&k_apply_special<Spec, kPtrCap, kSpecialU>);
   e.tile = kThreads * kVec * kSpecialU;
+  e.launch_bulk = &launch_special_bulk<Spec, kPtrCap>;
+  e.kernel_bulk = reinterpret_cast<KernelAddr>(&k_apply_special_bulk<Spec, kPtrCap, kBulkCW, kBulkU>);
+  e.tile_bulk = kBulkTile;
+  e.used_cols = bulk::used_cols<Spec>().n;
   return e;
 }
 
