@@ -1,0 +1,95 @@
+"""Kernel-only throughput sweep (not the bench): K1 RS(8,2) encode and K2
+single-loss rebuild over growing shard sizes, both specialised variants,
+next to torch's device copy of the same byte volume (the roofline
+reference). Times CUDA-graph replays with events on the launch stream.
+
+    python tools/kernel_sweep.py [--sizes 1,4,16,64,256] (MiB per shard)
+"""
+import argparse
+import json
+import os
+import sys
+
+import torch
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+from paper_2605_00831_b200 import _lib as L  # noqa: E402
+from paper_2605_00831_b200.coding import CodingScheme, ErasurePattern, check, decoder, encoder  # noqa: E402
+
+
+def graph_time(fn, reps, stream):
+    with torch.cuda.stream(stream):
+        fn()
+    stream.synchronize()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g, stream=stream):
+        for _ in range(reps):
+            fn()
+    with torch.cuda.stream(stream):
+        g.replay()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(3):
+            g.replay()
+        e1.record(stream)
+    e1.synchronize()
+    return e0.elapsed_time(e1) / (3 * reps) * 1e-3
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--sizes", default="0.25,1,4,16,64,256")
+    ap.add_argument("--n", type=int, default=8)
+    ap.add_argument("--k", type=int, default=2)
+    args = ap.parse_args()
+    lib = L.lib()
+    dev = torch.device("cuda:0")
+    st = torch.cuda.Stream()
+    n, k = args.n, args.k
+    scheme = CodingScheme.reed_solomon(n, k)
+    enc = encoder(scheme)
+    dec = decoder(scheme, ErasurePattern([1]))
+    out = []
+    for mib in [float(x) for x in args.sizes.split(",")]:
+        L_ = int(mib * (1 << 20)) // 4096 * 4096
+        nbuf = max(2, min(8, int((1 << 30) // (L_ * (n + k))) ))  # rotate so data > L2
+        data = torch.randint(0, 256, (nbuf, n, L_), dtype=torch.uint8, device=dev)
+        par = torch.empty((nbuf, k, L_), dtype=torch.uint8, device=dev)
+        reb = torch.empty((nbuf, L_), dtype=torch.uint8, device=dev)
+        sl = [L.ptr_array([data[b, j].data_ptr() for j in range(n)]) for b in range(nbuf)]
+        ol = [L.ptr_array([par[b, i].data_ptr() for i in range(k)]) for b in range(nbuf)]
+        dl = [L.ptr_array([None if j == 1 else (data[b, j].data_ptr() if j < n else par[b, j - n].data_ptr())
+                           for j in range(n + k)]) for b in range(nbuf)]
+        rl = [L.ptr_array([reb[b].data_ptr()]) for b in range(nbuf)]
+        row = {"mib_per_shard": mib, "bytes_enc": (n + k) * L_, "bytes_dec": (n + 1) * L_}
+        for v in (0, 1):
+            check(lib.gs_set_kernel_variant(v))
+            cnt = [0]
+
+            def k1():
+                b = cnt[0] % nbuf
+                cnt[0] += 1
+                check(lib.gs_apply_device(enc.handle, 1, sl[b], ol[b], L_, st.cuda_stream))
+
+            def k2():
+                b = cnt[0] % nbuf
+                cnt[0] += 1
+                check(lib.gs_apply_device(dec.handle, 1, dl[b], rl[b], L_, st.cuda_stream))
+            t1 = graph_time(k1, nbuf * 2, st)
+            t2 = graph_time(k2, nbuf * 2, st)
+            row[f"k1_v{v}_gbs"] = round((n + k) * L_ / t1 / 1e9, 1)
+            row[f"k2_v{v}_gbs"] = round((n + 1) * L_ / t2 / 1e9, 1)
+            row[f"k1_v{v}_us"] = round(t1 * 1e6, 2)
+        src = torch.empty(((n + k) * L_ // 2,), dtype=torch.uint8, device=dev)
+        dst = torch.empty_like(src)
+        tc = graph_time(lambda: dst.copy_(src), 4, st)
+        row["torch_copy_gbs"] = round((n + k) * L_ / tc / 1e9, 1)
+        out.append(row)
+        print(json.dumps(row), flush=True)
+        del data, par, reb, src, dst
+    check(lib.gs_set_kernel_variant(1))
+
+
+if __name__ == "__main__":
+    main()
