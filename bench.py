@@ -363,12 +363,11 @@ def run_ours(args):
             variants[vname] = timed(
                 lambda b: check(lib.gs_apply_device(enc.handle, S, slots[b], outs[b], SLICE, ks.cuda_stream),
                                 "k1"), S * (N_SHARDS + K_PARITY) * SLICE, f"K1 {vname}")["per_launch_us"]
-        best = min(variants, key=variants.get)
-        check(lib.gs_set_kernel_variant(0 if best == "ldg128" else 1), "variant")
+        check(lib.gs_set_kernel_variant(2), "variant")  # auto: what the timed step used
         kern = timed(lambda b: check(lib.gs_apply_device(enc.handle, S, slots[b], outs[b], SLICE,
                                                          ks.cuda_stream), "k1"),
                      S * (N_SHARDS + K_PARITY) * SLICE,
-                     f"k_apply_special{'_bulk' if best != 'ldg128' else ''}<EncSpec<RS,8,2>> (K1 encode)")
+                     "k_apply_special<EncSpec<RS,8,2>> (K1 encode, auto variant = ldg128 at this size)")
         kern["variants_us_per_launch"] = variants
         kern["traffic"] = args.traffic or ncu_traffic()
         kern2 = timed(lambda b: check(lib.gs_apply_device(dec5.handle, S, dslots[b], douts[b], SLICE,

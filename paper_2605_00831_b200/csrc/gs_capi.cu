@@ -118,8 +118,11 @@ int blocks_per_sm(int dev, const void* kernel, size_t smem, int threads = kThrea
 }
 
 // Which specialised kernel variant serves aligned bodies: 0 = register
-// (LDG.128) streaming, 1 = bulk-copy smem pipeline. gs_set_kernel_variant.
-std::atomic<int> g_variant{1};
+// (LDG.128) streaming, 1 = bulk-copy smem pipeline, 2 = auto (measured on
+// B200, tools/kernel_sweep.py: the bulk pipeline wins for encoders once a
+// launch moves >= 512 MB; the register kernel everywhere else).
+std::atomic<int> g_variant{2};
+constexpr uint64_t kBulkAutoBytes = 512ull << 20;
 
 int bulk_stages(const SpecialEntry* e) {
   const size_t per = static_cast<size_t>(e->used_cols) * e->tile_bulk;
@@ -312,7 +315,11 @@ int run_codec(const gs_codec* c, int n_stripes, SlotFn slot_ptr, OutFn out_ptr, 
   if (c->special && aligned && len >= kVec) {
     const uint64_t body = len / kVec * kVec;
     const int stages = bulk_stages(c->special);
-    const bool use_bulk = g_variant.load(std::memory_order_relaxed) == 1 && stages >= 2;
+    const int variant = g_variant.load(std::memory_order_relaxed);
+    const uint64_t launch_bytes = body * static_cast<uint64_t>(n_stripes) *
+                                  static_cast<uint64_t>(c->special->used_cols + c->n_out);
+    const bool use_bulk = stages >= 2 && (variant == 1 || (variant == 2 && !c->decoder &&
+                                                           launch_bytes >= kBulkAutoBytes));
     const uint64_t tile = static_cast<uint64_t>(use_bulk ? c->special->tile_bulk : c->special->tile);
     const uint64_t tps64 = (body + tile - 1) / tile;
     const int stride = c->n_slots + c->n_out;
@@ -401,6 +408,8 @@ struct gs_pipeline {
 
 namespace {
 
+constexpr uint64_t kHostPiece = 2ull << 20;
+
 struct DeviceGuard {
   int prev = -1;
   explicit DeviceGuard(int dev) {
@@ -416,33 +425,57 @@ struct DeviceGuard {
 
 // Choose the byte range per piece: as large as the slot allows, at least one
 // 4 KiB tile, rounded to 4 KiB so every piece but the last stays aligned.
-uint64_t piece_len(uint64_t len, size_t slot, int per_byte) {
-  uint64_t r = slot / static_cast<uint64_t>(per_byte);
+uint64_t piece_len(uint64_t len, size_t slot, int per_byte, uint64_t cap = ~0ull) {
+  uint64_t r = std::min<uint64_t>(slot / static_cast<uint64_t>(per_byte), cap);
   r = r / 4096 * 4096;
   if (r == 0) r = 4096;
   return std::min<uint64_t>(r, len);
 }
 
-// Copy a list of (dst, src, bytes) with adjacent runs merged.
+// Host-link copies of one piece. Adjacent (dst, src) runs are merged into
+// one 1-D copy; what remains is grouped by `key` (e.g. parity row) into
+// constant-pitch runs issued as single 2-D copies, so a batch of 32 request
+// slices costs one DMA command per parity row instead of 32.
 struct CopyOp {
   uint8_t* dst;
   const uint8_t* src;
   size_t bytes;
+  int key;
 };
 
 int issue_copies(std::vector<CopyOp>& ops, cudaMemcpyKind kind, cudaStream_t st) {
-  size_t i = 0;
-  while (i < ops.size()) {
+  std::vector<CopyOp> merged;
+  for (size_t i = 0; i < ops.size();) {
     CopyOp cur = ops[i];
     size_t j = i + 1;
     while (j < ops.size() && ops[j].dst == cur.dst + cur.bytes && ops[j].src == cur.src + cur.bytes) {
       cur.bytes += ops[j].bytes;
       ++j;
     }
-    if (cur.bytes) GS_CUDA(cudaMemcpyAsync(cur.dst, cur.src, cur.bytes, kind, st));
+    if (cur.bytes) merged.push_back(cur);
     i = j;
   }
   ops.clear();
+  std::stable_sort(merged.begin(), merged.end(), [](const CopyOp& a, const CopyOp& b) { return a.key < b.key; });
+  for (size_t i = 0; i < merged.size();) {
+    const CopyOp& a = merged[i];
+    size_t j = i + 1;
+    if (j < merged.size() && merged[j].key == a.key && merged[j].bytes == a.bytes && merged[j].dst > a.dst &&
+        merged[j].src > a.src) {
+      const size_t dp = static_cast<size_t>(merged[j].dst - a.dst), sp = static_cast<size_t>(merged[j].src - a.src);
+      constexpr size_t kMaxPitch = (size_t{1} << 31) - 1;
+      if (dp >= a.bytes && sp >= a.bytes && dp <= kMaxPitch && sp <= kMaxPitch) {
+        while (j < merged.size() && merged[j].key == a.key && merged[j].bytes == a.bytes &&
+               merged[j].dst == merged[j - 1].dst + dp && merged[j].src == merged[j - 1].src + sp)
+          ++j;
+        GS_CUDA(cudaMemcpy2DAsync(a.dst, dp, a.src, sp, a.bytes, j - i, kind, st));
+        i = j;
+        continue;
+      }
+    }
+    GS_CUDA(cudaMemcpyAsync(a.dst, a.src, a.bytes, kind, st));
+    i = i + 1;
+  }
   return GS_OK;
 }
 
@@ -657,7 +690,7 @@ int gs_apply_device(const gs_codec* c, int n_stripes, const void* const* slots, 
 // pipelines
 // ============================================================================
 int gs_set_kernel_variant(int variant) {
-  if (variant != 0 && variant != 1) return fail(GS_INVALID_ARGUMENT, "kernel variant must be 0 or 1");
+  if (variant < 0 || variant > 2) return fail(GS_INVALID_ARGUMENT, "kernel variant must be 0, 1 or 2");
   g_variant.store(variant);
   return GS_OK;
 }
@@ -769,7 +802,7 @@ int gs_encode_offload(gs_pipeline* p, const gs_codec* c, int n_stripes, const vo
       for (int s = 0; s < cnt; ++s)
         for (int i = 0; i < K; ++i)
           ops.push_back({static_cast<uint8_t*>(h_parity[static_cast<size_t>(s0 + s) * K + i]) + r0,
-                         base + (static_cast<size_t>(s) * K + i) * rl, rl});
+                         base + (static_cast<size_t>(s) * K + i) * rl, rl, i});
       if (int st = issue_copies(ops, cudaMemcpyDeviceToHost, ks)) return st;
       GS_CUDA(cudaEventRecord(p->drained[sl], ks));
     }
@@ -808,7 +841,8 @@ int gs_reconstruct_upload(gs_pipeline* p, const gs_codec* c, int n_stripes, cons
         for (size_t h = 0; h < host_slots.size(); ++h) {
           const void* hp = slots[static_cast<size_t>(s0 + s) * NS + host_slots[h]];
           if (!hp) return fail(GS_INVALID_ARGUMENT, "reconstruct_upload: parity slot %d is NULL", host_slots[h]);
-          ops.push_back({base + (static_cast<size_t>(s) * H + h) * rl, static_cast<const uint8_t*>(hp) + r0, rl});
+          ops.push_back({base + (static_cast<size_t>(s) * H + h) * rl, static_cast<const uint8_t*>(hp) + r0, rl,
+                         static_cast<int>(h)});
         }
       if (int st = issue_copies(ops, cudaMemcpyHostToDevice, ks)) return st;
       GS_CUDA(cudaEventRecord(p->ready[sl], ks));
@@ -845,7 +879,9 @@ int gs_encode_host(gs_pipeline* p, const gs_codec* c, const void* const* h_data,
   DeviceGuard g(p->device);
   const int N = c->n_slots, K = c->n_out;
   const size_t slot = p->slot_bytes();
-  const uint64_t rl_max = piece_len(len, slot, N + K);
+  // ~2 MiB per shard per piece: deep enough pipelining that the H2D of piece
+  // i+1, the kernel of piece i and the D2H of piece i-1 overlap.
+  const uint64_t rl_max = piece_len(len, slot, N + K, kHostPiece);
   std::vector<CopyOp> ops;
   for (uint64_t r0 = 0; r0 < len; r0 += rl_max) {
     const uint64_t rl = std::min<uint64_t>(rl_max, len - r0);
@@ -855,7 +891,7 @@ int gs_encode_host(gs_pipeline* p, const gs_codec* c, const void* const* h_data,
     uint8_t* outb = in + static_cast<size_t>(N) * rl;
     GS_CUDA(cudaStreamWaitEvent(p->s_h2d, p->drained[sl], 0));
     for (int j = 0; j < N; ++j)
-      ops.push_back({in + static_cast<size_t>(j) * rl, static_cast<const uint8_t*>(h_data[j]) + r0, rl});
+      ops.push_back({in + static_cast<size_t>(j) * rl, static_cast<const uint8_t*>(h_data[j]) + r0, rl, 0});
     if (int st = issue_copies(ops, cudaMemcpyHostToDevice, p->s_h2d)) return st;
     GS_CUDA(cudaEventRecord(p->ready[sl], p->s_h2d));
     GS_CUDA(cudaStreamWaitEvent(p->s_comp, p->ready[sl], 0));
@@ -865,7 +901,7 @@ int gs_encode_host(gs_pipeline* p, const gs_codec* c, const void* const* h_data,
     GS_CUDA(cudaEventRecord(p->done[sl], p->s_comp));
     GS_CUDA(cudaStreamWaitEvent(p->s_d2h, p->done[sl], 0));
     for (int i = 0; i < K; ++i)
-      ops.push_back({static_cast<uint8_t*>(h_parity[i]) + r0, outb + static_cast<size_t>(i) * rl, rl});
+      ops.push_back({static_cast<uint8_t*>(h_parity[i]) + r0, outb + static_cast<size_t>(i) * rl, rl, 0});
     if (int st = issue_copies(ops, cudaMemcpyDeviceToHost, p->s_d2h)) return st;
     GS_CUDA(cudaEventRecord(p->drained[sl], p->s_d2h));
   }
@@ -885,7 +921,7 @@ int gs_reconstruct_host(gs_pipeline* p, const gs_codec* c, const void* const* h_
   DeviceGuard g(p->device);
   const int U = static_cast<int>(c->used.size()), E = c->n_out;
   const size_t slot = p->slot_bytes();
-  const uint64_t rl_max = piece_len(len, slot, U + E);
+  const uint64_t rl_max = piece_len(len, slot, U + E, kHostPiece);
   std::vector<CopyOp> ops;
   for (uint64_t r0 = 0; r0 < len; r0 += rl_max) {
     const uint64_t rl = std::min<uint64_t>(rl_max, len - r0);
@@ -895,7 +931,7 @@ int gs_reconstruct_host(gs_pipeline* p, const gs_codec* c, const void* const* h_
     uint8_t* outb = in + static_cast<size_t>(U) * rl;
     GS_CUDA(cudaStreamWaitEvent(p->s_h2d, p->drained[sl], 0));
     for (int u = 0; u < U; ++u)
-      ops.push_back({in + static_cast<size_t>(u) * rl, static_cast<const uint8_t*>(h_slots[c->used[u]]) + r0, rl});
+      ops.push_back({in + static_cast<size_t>(u) * rl, static_cast<const uint8_t*>(h_slots[c->used[u]]) + r0, rl, 0});
     if (int st = issue_copies(ops, cudaMemcpyHostToDevice, p->s_h2d)) return st;
     GS_CUDA(cudaEventRecord(p->ready[sl], p->s_h2d));
     GS_CUDA(cudaStreamWaitEvent(p->s_comp, p->ready[sl], 0));
@@ -908,7 +944,7 @@ int gs_reconstruct_host(gs_pipeline* p, const gs_codec* c, const void* const* h_
     GS_CUDA(cudaEventRecord(p->done[sl], p->s_comp));
     GS_CUDA(cudaStreamWaitEvent(p->s_d2h, p->done[sl], 0));
     for (int i = 0; i < E; ++i)
-      ops.push_back({static_cast<uint8_t*>(h_out[i]) + r0, outb + static_cast<size_t>(i) * rl, rl});
+      ops.push_back({static_cast<uint8_t*>(h_out[i]) + r0, outb + static_cast<size_t>(i) * rl, rl, 0});
     if (int st = issue_copies(ops, cudaMemcpyDeviceToHost, p->s_d2h)) return st;
     GS_CUDA(cudaEventRecord(p->drained[sl], p->s_d2h));
   }

@@ -26,7 +26,7 @@ using BulkLaunchFn = cudaError_t (*)(const void* const* ptrs, int count, const T
 // Pointer-table capacity of one launch (kernel parameter space: 4 KiB).
 constexpr int kPtrCap = 508;
 // 16-byte groups per thread per source per tile of the specialised kernels.
-constexpr int kSpecialU = 2;
+constexpr int kSpecialU = 1;
 // Consumer warps and 16-byte groups per consumer thread of the bulk variant.
 constexpr int kBulkCW = 8;
 constexpr int kBulkU = 1;

@@ -309,4 +309,4 @@ def test_kernel_variants_bit_identical(golden, variant):
                         for i, t in got.items():
                             assert torch.equal(t, data[:, i]), (n, k, lost, variant)
     finally:
-        L.lib().gs_set_kernel_variant(1)
+        L.lib().gs_set_kernel_variant(2)

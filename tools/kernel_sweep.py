@@ -88,7 +88,7 @@ def main():
         out.append(row)
         print(json.dumps(row), flush=True)
         del data, par, reb, src, dst
-    check(lib.gs_set_kernel_variant(1))
+    check(lib.gs_set_kernel_variant(2))
 
 
 if __name__ == "__main__":
