@@ -113,6 +113,44 @@ class PeerGroup:
         self._opened.clear()
 
 
+class StripedCall:
+    """A prepared striped encode / rebuild: pointer tables built once, so the
+    timed path is a single C-ABI call (re-runnable, e.g. every decode step
+    that reuses the same KV block buffers)."""
+
+    def __init__(self, fn, args, offset: int, length: int, two_streams: bool = True):
+        self.fn, self.args, self.offset, self.length = fn, args, offset, length
+        self.two_streams = two_streams
+
+    def run(self, stream: int, copy_stream: Optional[int] = None) -> None:
+        if self.length == 0 or self.fn is None:
+            return
+        if not self.two_streams:
+            check(self.fn(*self.args, stream), "striped")
+            return
+        check(self.fn(*self.args, stream, copy_stream if copy_stream is not None else stream), "striped")
+
+
+def plan_encode_striped(scheme: CodingScheme, layout: ShardLayout, bases: Sequence[int], rank: int,
+                        parity_out=None, pipeline=None, h_parity=None) -> StripedCall:
+    """K1 over this rank's byte range of all stripes (see encode_striped)."""
+    enc = encoder(scheme)
+    off, ln, slots = striped_slots(layout, bases, rank)
+    if ln == 0:
+        return StripedCall(None, (), off, 0)
+    flat = L.ptr_array([p for row in slots for p in row])
+    lib = L.lib()
+    if pipeline is None:
+        outs = L.ptr_array([parity_out[s, i].data_ptr() for s in range(layout.stripes)
+                            for i in range(scheme.k)])
+        return StripedCall(lib.gs_apply_device, (enc.handle, layout.stripes, flat, outs, ln), off, ln,
+                           two_streams=False)
+    outs = L.ptr_array([h_parity[s, i].data_ptr() + off for s in range(layout.stripes)
+                        for i in range(scheme.k)])
+    return StripedCall(lib.gs_encode_offload, (pipeline.handle, enc.handle, layout.stripes, flat, outs, ln),
+                       off, ln)
+
+
 def encode_striped(scheme: CodingScheme, layout: ShardLayout, bases: Sequence[int], rank: int,
                    parity_out, stream: int, pipeline=None, h_parity=None, copy_stream=None) -> Tuple[int, int]:
     """K1 over this rank's byte range of all stripes.
@@ -120,34 +158,18 @@ def encode_striped(scheme: CodingScheme, layout: ShardLayout, bases: Sequence[in
     Without a pipeline: parity range -> `parity_out` device [S, k, len_r].
     With a pipeline: parity range -> pinned host `h_parity` [S, k, L] at the
     range's offset (encode + D2H overlapped on this rank's host link)."""
-    enc = encoder(scheme)
-    off, ln, slots = striped_slots(layout, bases, rank)
-    if ln == 0:
-        return off, 0
-    flat = L.ptr_array([p for row in slots for p in row])
-    if pipeline is None:
-        outs = L.ptr_array([parity_out[s, i].data_ptr() for s in range(layout.stripes)
-                            for i in range(scheme.k)])
-        check(L.lib().gs_apply_device(enc.handle, layout.stripes, flat, outs, ln, stream), "encode_striped")
-    else:
-        outs = L.ptr_array([h_parity[s, i].data_ptr() + off for s in range(layout.stripes)
-                            for i in range(scheme.k)])
-        check(L.lib().gs_encode_offload(pipeline.handle, enc.handle, layout.stripes, flat, outs, ln, stream,
-                                        copy_stream if copy_stream is not None else stream),
-              "encode_striped")
-    return off, ln
+    call = plan_encode_striped(scheme, layout, bases, rank, parity_out, pipeline, h_parity)
+    call.run(stream, copy_stream)
+    return call.offset, call.length
 
 
-def reconstruct_striped(scheme: CodingScheme, layout: ShardLayout, bases: Sequence[int], rank: int,
-                        lost: ErasurePattern, h_parity, pipeline, stream: int,
-                        copy_stream: Optional[int] = None) -> Tuple[int, int]:
-    """K2 over this rank's byte range: parity range H2D'd from this rank's
-    pinned host slab, survivors pulled from peers, rebuilt bytes stored
-    straight into the lost workers' buffers (on their owners' GPUs)."""
+def plan_reconstruct_striped(scheme: CodingScheme, layout: ShardLayout, bases: Sequence[int], rank: int,
+                             lost: ErasurePattern, h_parity, pipeline) -> StripedCall:
+    """K2 over this rank's byte range (see reconstruct_striped)."""
     dec = decoder(scheme, lost)
     off, ln, slots = striped_slots(layout, bases, rank, lost.lost)
     if ln == 0 or dec.n_out == 0:
-        return off, ln
+        return StripedCall(None, (), off, 0)
     n, k = scheme.n, scheme.k
     full = []
     for s in range(layout.stripes):
@@ -159,8 +181,17 @@ def reconstruct_striped(scheme: CodingScheme, layout: ShardLayout, bases: Sequen
         for w in dec.out_index:
             r, _ = layout.owner(w)
             outs.append(bases[r] + layout.shard_offset(s, w) + off)
-    check(L.lib().gs_reconstruct_upload(pipeline.handle, dec.handle, layout.stripes, L.ptr_array(full),
-                                        L.ptr_array(outs), ln, stream,
-                                        copy_stream if copy_stream is not None else stream),
-          "reconstruct_striped")
-    return off, ln
+    return StripedCall(L.lib().gs_reconstruct_upload,
+                       (pipeline.handle, dec.handle, layout.stripes, L.ptr_array(full), L.ptr_array(outs), ln),
+                       off, ln)
+
+
+def reconstruct_striped(scheme: CodingScheme, layout: ShardLayout, bases: Sequence[int], rank: int,
+                        lost: ErasurePattern, h_parity, pipeline, stream: int,
+                        copy_stream: Optional[int] = None) -> Tuple[int, int]:
+    """K2 over this rank's byte range: parity range H2D'd from this rank's
+    pinned host slab, survivors pulled from peers, rebuilt bytes stored
+    straight into the lost workers' buffers (on their owners' GPUs)."""
+    call = plan_reconstruct_striped(scheme, layout, bases, rank, lost, h_parity, pipeline)
+    call.run(stream, copy_stream)
+    return call.offset, call.length
