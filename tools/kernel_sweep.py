@@ -81,10 +81,20 @@ def main():
             row[f"k1_v{v}_gbs"] = round((n + k) * L_ / t1 / 1e9, 1)
             row[f"k2_v{v}_gbs"] = round((n + 1) * L_ / t2 / 1e9, 1)
             row[f"k1_v{v}_us"] = round(t1 * 1e6, 2)
-        src = torch.empty(((n + k) * L_ // 2,), dtype=torch.uint8, device=dev)
+        # device copy of the same byte volume (read + write), rotating over
+        # buffers so the L2 cannot serve it: the attainable HBM rate at this size
+        half = (n + k) * L_ // 2
+        ncp = max(2, min(8, int((1 << 30) // half)))
+        src = torch.empty((ncp, half), dtype=torch.uint8, device=dev)
         dst = torch.empty_like(src)
-        tc = graph_time(lambda: dst.copy_(src), 4, st)
-        row["torch_copy_gbs"] = round((n + k) * L_ / tc / 1e9, 1)
+        cc = [0]
+
+        def cp():
+            b = cc[0] % ncp
+            cc[0] += 1
+            dst[b].copy_(src[b])
+        tc = graph_time(cp, ncp * 2, st)
+        row["copy_gbs"] = round((n + k) * L_ / tc / 1e9, 1)
         out.append(row)
         print(json.dumps(row), flush=True)
         del data, par, reb, src, dst
