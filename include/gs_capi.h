@@ -40,7 +40,9 @@ typedef enum {
   GS_UNRECOVERABLE = 2,
   GS_DOMAIN_ERROR = 3,
   GS_CUDA_ERROR = 4,
-  GS_UNSUPPORTED = 5
+  GS_UNSUPPORTED = 5,
+  GS_LOGIC_ERROR = 6,   /* std::logic_error (duplicate store entry) */
+  GS_RUNTIME_ERROR = 7  /* std::runtime_error (parity file format / integrity) */
 } gs_status;
 
 /* CodeKind (coding.hpp:19). RDP is out of scope on this path: accepted by
@@ -49,6 +51,7 @@ typedef enum { GS_XOR = 0, GS_RDP = 1, GS_RS = 2 } gs_code_kind;
 
 typedef struct gs_codec gs_codec;       /* immutable coefficient plan + kernel choice */
 typedef struct gs_pipeline gs_pipeline; /* per-device staging ring + events for host-link overlap */
+typedef struct gs_store gs_store;       /* host tier: ParityStore on pinned slabs */
 
 /* ---- diagnostics ------------------------------------------------------- */
 const char* gs_status_string(int status);
@@ -171,6 +174,38 @@ uint64_t gs_parity_checksum(const void* const* parity, int k, size_t len);
  * out[c] = checksum of parity[c*k .. c*k+k-1]. */
 int gs_parity_checksum_batch(const void* const* parity, int n_chunks, int k, size_t len,
                              int threads, uint64_t* out);
+
+/* ---- host tier: ParityStore on pinned slabs (parity_store.hpp:31-263) ----
+ * Entries are keyed (request, chunk). Reserve -> the D2H of K1 writes the k
+ * parity buffers straight into the returned pinned pointers (no try_put
+ * copy, checkpoint.hpp:207) -> commit: the FNV-1a seal runs on host threads
+ * once `stream` reaches that point (cudaLaunchHostFunc), off the GPU path. */
+int gs_store_create(uint64_t capacity_bytes /* ~0 = unlimited */, int seal_threads, gs_store** out);
+int gs_store_destroy(gs_store* s);
+/* try_put accounting (parity_store.hpp:77-90): *accepted = 0 is back-pressure
+ * (store unchanged); a duplicate key is GS_LOGIC_ERROR. parity_out[k]. */
+int gs_store_reserve(gs_store* s, uint64_t request_id, uint32_t chunk, int kind, int n, int k,
+                     uint32_t valid_tokens, uint64_t slice_len, int* accepted, void** parity_out);
+int gs_store_commit(gs_store* s, uint64_t request_id, uint32_t chunk, void* stream);
+int gs_store_wait_sealed(gs_store* s);
+/* Copying put (reference try_put): sealed != 0 keeps `checksum` as given. */
+int gs_store_put(gs_store* s, uint64_t request_id, uint32_t chunk, int kind, int n, int k,
+                 uint32_t valid_tokens, uint64_t slice_len, const void* const* parity, uint64_t checksum,
+                 int sealed, int* accepted);
+/* get (parity_store.hpp:92-101): *status 0 = kOk, 1 = kMissing, 2 = kCorrupt
+ * (FNV re-verified when verify != 0). kind_n_k[3] optional. */
+int gs_store_get(gs_store* s, uint64_t request_id, uint32_t chunk, int verify, int* status, void** parity_out,
+                 uint64_t* slice_len, uint32_t* valid_tokens, uint64_t* checksum, int* kind_n_k);
+int gs_store_contains(gs_store* s, uint64_t request_id, uint32_t chunk);
+int gs_store_erase_request(gs_store* s, uint64_t request_id);
+/* out5 = {used_bytes, capacity_bytes, payload_bytes, peak_payload_bytes, entry_count} */
+int gs_store_stats(gs_store* s, uint64_t* out5);
+int gs_store_audit(gs_store* s);
+int gs_store_corrupt_entry(gs_store* s, uint64_t request_id, uint32_t chunk);
+int gs_store_keys(gs_store* s, uint64_t* keys, uint64_t max_entries, uint64_t* count);
+/* GSRV file image (parity_store.hpp:145-263); out == NULL queries *size. */
+int gs_store_serialize(gs_store* s, void* out, uint64_t cap, uint64_t* size);
+int gs_store_deserialize(const void* bytes, uint64_t size, uint64_t capacity, int seal_threads, gs_store** out);
 
 /* ---- peer memory over NVLink (multi-GPU striping) ---------------------- */
 #define GS_IPC_HANDLE_BYTES 64

@@ -335,3 +335,33 @@ int ghs_encode_and_seal(int kind, int n, int k, const uint8_t* const* data, size
 }
 
 }  // extern "C"
+
+// GSRV image of a ParityStore built by the reference (parity_store.hpp:145-263)
+// from `count` entries: keys req[i]/chunk[i]/valid[i], parity[i*k + j] of
+// slice_len bytes each, sealed with the reference's own seal().
+extern "C" int ghs_gsrv_image(int kind, int n, int k, int count, const uint64_t* req, const uint32_t* chunk,
+                              const uint32_t* valid, uint64_t slice_len, const uint8_t* const* parity,
+                              uint8_t* out, uint64_t cap, uint64_t* size) {
+  try {
+    ParityStore store;
+    for (int i = 0; i < count; ++i) {
+      ParityChunk c;
+      c.request_id = req[i];
+      c.chunk_id = ChunkId{chunk[i]};
+      c.scheme = scheme_of(kind, n, k);
+      c.valid_tokens = valid[i];
+      c.slice_len = slice_len;
+      c.parity.resize(static_cast<size_t>(k));
+      for (int j = 0; j < k; ++j)
+        c.parity[static_cast<size_t>(j)].assign(parity[i * k + j], parity[i * k + j] + slice_len);
+      c.seal();
+      store.try_put(std::move(c));
+    }
+    auto bytes = serialize_parity_store(store);
+    *size = bytes.size();
+    if (out && cap >= bytes.size()) std::memcpy(out, bytes.data(), bytes.size());
+    return 0;
+  } catch (...) {
+    return map_exception();
+  }
+}

@@ -13,7 +13,8 @@ import threading
 HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(HERE, "_lib", "libghostserve_b200.so")
 
-GS_OK, GS_INVALID_ARGUMENT, GS_UNRECOVERABLE, GS_DOMAIN_ERROR, GS_CUDA_ERROR, GS_UNSUPPORTED = range(6)
+(GS_OK, GS_INVALID_ARGUMENT, GS_UNRECOVERABLE, GS_DOMAIN_ERROR, GS_CUDA_ERROR, GS_UNSUPPORTED,
+ GS_LOGIC_ERROR, GS_RUNTIME_ERROR) = range(8)
 GS_XOR, GS_RDP, GS_RS = 0, 1, 2
 IPC_HANDLE_BYTES = 64
 
@@ -56,6 +57,21 @@ SIGNATURES = {
     "gs_fnv1a64": (_u64, [_vp, _sz, _u64]),
     "gs_parity_checksum": (_u64, [_vpp, _i, _sz]),
     "gs_parity_checksum_batch": (_i, [_vpp, _i, _i, _sz, _i, _u64p]),
+    "gs_store_create": (_i, [_u64, _i, _vpp]),
+    "gs_store_destroy": (_i, [_vp]),
+    "gs_store_reserve": (_i, [_vp, _u64, _u32, _i, _i, _i, _u32, _u64, _ip, _vpp]),
+    "gs_store_commit": (_i, [_vp, _u64, _u32, _vp]),
+    "gs_store_wait_sealed": (_i, [_vp]),
+    "gs_store_put": (_i, [_vp, _u64, _u32, _i, _i, _i, _u32, _u64, _vpp, _u64, _i, _ip]),
+    "gs_store_get": (_i, [_vp, _u64, _u32, _i, _ip, _vpp, _u64p, C.POINTER(C.c_uint32), _u64p, _ip]),
+    "gs_store_contains": (_i, [_vp, _u64, _u32]),
+    "gs_store_erase_request": (_i, [_vp, _u64]),
+    "gs_store_stats": (_i, [_vp, _u64p]),
+    "gs_store_audit": (_i, [_vp]),
+    "gs_store_corrupt_entry": (_i, [_vp, _u64, _u32]),
+    "gs_store_keys": (_i, [_vp, _u64p, _u64, _u64p]),
+    "gs_store_serialize": (_i, [_vp, _vp, _u64, _u64p]),
+    "gs_store_deserialize": (_i, [_vp, _u64, _u64, _i, _vpp]),
     "gs_ipc_handle": (_i, [_vp, _vp, _u64p]),
     "gs_ipc_open": (_i, [_vp, _i, _vpp]),
     "gs_ipc_close": (_i, [_vp]),

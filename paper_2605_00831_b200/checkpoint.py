@@ -1,0 +1,464 @@
+"""Checkpoint / recovery orchestration on the GPU byte path.
+
+Mirrors the byte-moving parts of checkpoint.hpp and recovery.hpp:
+
+* ``next_parity_worker`` / ``AssignmentState``      checkpoint.hpp:21-30
+* ``CheckpointConfig``                              checkpoint.hpp:32-47
+* ``Checkpointer.checkpoint_chunk``                 checkpoint.hpp:123-149 (encode + seal -> host tier)
+* ``Checkpointer.run_prefill_with_checkpointing``   checkpoint.hpp:179-222
+* ``DecodeCheckpointer``                            checkpoint.hpp:228-281
+* ``get_recompute_units`` / ``CostModel``           recovery.hpp:58-88, cost_model.hpp:17-68
+* ``Checkpointer.reconstruct_chunk``                recovery.hpp:100-133
+* ``verify_recovery``                               recovery.hpp:135-145
+* ``Checkpointer.recover``                          recovery.hpp:176-298 (plan + byte restore)
+
+The reference computes bytes on one CPU thread and models time with
+cost-model constants. Here the bytes come from K1/K2 with the D2H/H2D
+overlapped by the pipeline, parity lands directly in the pinned host store
+(no try_put copy) and is sealed by host threads, and the outcomes carry
+MEASURED device times (CUDA events) instead of virtual-clock events. The
+cost model survives only as the recompute/reconstruct split planner, and can
+be calibrated from measurements (``CostModel.measured``).
+"""
+from __future__ import annotations
+
+import math
+import time
+from dataclasses import dataclass, field
+from typing import Dict, List, Optional, Sequence, Set
+
+import torch
+
+from . import _lib as L
+from .coding import (CodingScheme, ErasurePattern, InvalidArgument, LogicError, UnrecoverableError, check,
+                     decoder, encoder, max_tolerance)
+from .device import Pipeline
+from .kv_layout import ModelConfig, chunk_count, make_ground_truth_slice, slice_bytes
+from .parity_store import ParityGetStatus, ParityStore
+
+
+# ---------------------------------------------------------------------------
+# cost model + planner (cost_model.hpp:17-68, recovery.hpp:58-88)
+# ---------------------------------------------------------------------------
+@dataclass
+class CostModel:
+    compute_per_token: float = 6.0e-5
+    intra_bw: float = 400e9
+    host_bw: float = 32e9
+    encode_rate: float = 180e9
+    reconstruct_rate: float = 300e9
+    fixed_collective_latency: float = 2.0e-5
+    restart_overhead: float = 2.0
+
+    def validate(self) -> None:
+        if (self.compute_per_token <= 0 or self.intra_bw <= 0 or self.host_bw <= 0 or self.encode_rate <= 0
+                or self.reconstruct_rate <= 0 or self.fixed_collective_latency < 0 or self.restart_overhead < 0):
+            raise InvalidArgument("cost: rates must be positive")
+        if self.host_bw > self.intra_bw:
+            raise InvalidArgument("cost: host link cannot be faster than the intra-node fabric")
+
+    def chunk_compute_time(self, tokens: int) -> float:
+        return tokens * self.compute_per_token
+
+    def gather_time(self, tp: int, slice_: int) -> float:
+        return (tp - 1) * slice_ / self.intra_bw + self.fixed_collective_latency
+
+    def encode_time(self, tp: int, slice_: int) -> float:
+        return tp * slice_ / self.encode_rate
+
+    def offload_time(self, k: int, slice_: int) -> float:
+        return k * slice_ / self.host_bw
+
+    def parity_fetch_time(self, k: int, slice_: int) -> float:
+        return k * slice_ / self.host_bw
+
+    def reconstruct_time(self, tp: int, slice_: int) -> float:
+        return tp * slice_ / self.reconstruct_rate
+
+    def reconstruct_chunk_time(self, scheme: CodingScheme, slice_: int) -> float:
+        return (self.parity_fetch_time(scheme.k, slice_) + self.gather_time(scheme.n, slice_)
+                + self.reconstruct_time(scheme.n, slice_))
+
+    @staticmethod
+    def measured(host_gbs: float, encode_gbs: float, reconstruct_gbs: float, intra_gbs: float = 770.0,
+                 compute_per_token: float = 6.0e-5, restart_overhead: float = 2.0) -> "CostModel":
+        """Cost model calibrated from B200 measurements (bench.py / kernel_sweep):
+        host link, K1 and K2 data rates in GB/s; NVLink peer rate default =
+        the measured 770 GB/s per direction (B200_PROFILING.md)."""
+        return CostModel(compute_per_token, intra_gbs * 1e9, host_gbs * 1e9, encode_gbs * 1e9,
+                         reconstruct_gbs * 1e9, 2.0e-5, restart_overhead)
+
+
+def get_recompute_units(n: int, chunk_size: int, scheme: CodingScheme, slice_: int, cost: CostModel) -> int:
+    """argmin_r max(r*m*c + restart, (n-r)*T_rec); ties -> smaller r (recovery.hpp:58-88)."""
+    if n == 0:
+        return 0
+    a = chunk_size * cost.compute_per_token
+    c = cost.reconstruct_chunk_time(scheme, slice_)
+    restart = cost.restart_overhead
+
+    def objective(r: int) -> float:
+        return max(r * a + restart, (n - r) * c)
+
+    cands = [0, n]
+    if a + c > 0:
+        x = (n * c - restart) / (a + c)
+        fl = math.floor(x)
+        if 0 <= fl <= n:
+            cands.append(int(fl))
+        if 0 <= fl + 1 <= n:
+            cands.append(int(fl + 1))
+    cands.sort()
+    best, best_f = cands[0], objective(cands[0])
+    for r in cands:
+        f = objective(r)
+        if f < best_f:
+            best, best_f = r, f
+    return best
+
+
+# ---------------------------------------------------------------------------
+# assignment + config (checkpoint.hpp:21-47)
+# ---------------------------------------------------------------------------
+@dataclass
+class AssignmentState:
+    next_worker: int = 0
+
+
+def next_parity_worker(state: AssignmentState, tp_degree: int) -> int:
+    if tp_degree < 1:
+        raise InvalidArgument("assignment: worker count must be positive")
+    w = state.next_worker
+    state.next_worker = (state.next_worker + 1) % tp_degree
+    return w
+
+
+@dataclass
+class CheckpointConfig:
+    scheme: CodingScheme = field(default_factory=lambda: CodingScheme.reed_solomon(8, 2))
+    chunk_size: int = 2048
+    model: ModelConfig = field(default_factory=ModelConfig)
+    cost: CostModel = field(default_factory=CostModel)
+    checkpoint_decode: bool = True
+
+    def validate(self) -> None:
+        self.scheme.validate()
+        self.model.validate()
+        self.cost.validate()
+        if self.chunk_size == 0:
+            raise InvalidArgument("checkpoint: chunk size must be positive")
+        if self.scheme.n != self.model.tp_degree:
+            raise InvalidArgument("checkpoint: data shard count must equal tp_degree")
+
+
+@dataclass
+class KvChunkSlice:
+    """kv_layout.hpp:62-68 with the bytes on the device."""
+
+    request_id: int
+    chunk_id: int
+    worker: int
+    bytes: torch.Tensor
+    valid_tokens: int
+
+
+@dataclass
+class ChunkCheckpointOutcome:
+    request_id: int
+    chunk_id: int
+    valid_tokens: int
+    parity_worker: int
+    stored: bool                 # False = back-pressure (store unchanged)
+    enqueue_s: float = 0.0       # host time to plan + enqueue
+
+
+@dataclass
+class PrefillRunResult:
+    completed: bool = False
+    chunks_done: int = 0
+    stalled_at_chunk: Optional[int] = None
+    state: AssignmentState = field(default_factory=AssignmentState)
+    ground_truth: List[List[KvChunkSlice]] = field(default_factory=list)
+    device_ms: float = 0.0
+
+
+class ChunkRepairStatus:
+    kOk = 0
+    kBadParity = 1
+
+
+@dataclass
+class ChunkRepairResult:
+    status: int = ChunkRepairStatus.kOk
+    recovered: Dict[int, KvChunkSlice] = field(default_factory=dict)
+
+
+@dataclass
+class FailureEvent:
+    failed_workers: List[int]
+    at_chunk: int = 0
+    at_time: float = 0.0
+
+
+class RecoveryMode:
+    kPureRecompute = "pure_recompute"
+    kHybrid = "hybrid"
+    kFullRecomputeFallback = "full_recompute_fallback"
+
+
+@dataclass
+class RecoveryPlan:
+    recompute_chunks: int = 0
+    reconstruct_ids: List[int] = field(default_factory=list)
+    mode: str = RecoveryMode.kPureRecompute
+
+
+@dataclass
+class RecoveryResult:
+    plan: RecoveryPlan = field(default_factory=RecoveryPlan)
+    recovered: Dict[int, List[Optional[KvChunkSlice]]] = field(default_factory=dict)
+    verified: bool = True
+    parity_bytes_fetched: int = 0
+    reconstruct_device_ms: float = 0.0
+
+
+def verify_recovery(recovered, ground_truth) -> bool:
+    """recovery.hpp:135-145 (bytes, or slices incl. worker / valid_tokens)."""
+    if isinstance(recovered, KvChunkSlice):
+        return (recovered.worker == ground_truth.worker and recovered.valid_tokens == ground_truth.valid_tokens
+                and verify_recovery(recovered.bytes, ground_truth.bytes))
+    return recovered.numel() == ground_truth.numel() and bool(torch.equal(recovered, ground_truth))
+
+
+# ---------------------------------------------------------------------------
+# the orchestrator
+# ---------------------------------------------------------------------------
+class Checkpointer:
+    """One device's checkpoint engine: pipeline (staging ring + events),
+    compute and copy streams, the host-tier store."""
+
+    def __init__(self, cfg: CheckpointConfig, store: ParityStore, device: int = 0,
+                 staging_bytes: int = 256 << 20):
+        cfg.validate()
+        self.cfg = cfg
+        self.store = store
+        self.device = device
+        self.dev = torch.device("cuda", device)
+        self.pipe = Pipeline(device, staging_bytes)
+        self.compute = torch.cuda.Stream(device=self.dev)
+        self.copy = torch.cuda.Stream(device=self.dev)
+        self.slice = slice_bytes(cfg.model, cfg.chunk_size)
+
+    def close(self) -> None:
+        self.pipe.close()
+
+    def synchronize(self) -> None:
+        self.copy.synchronize()
+        self.compute.synchronize()
+        self.store.wait_sealed()
+
+    # checkpoint.hpp:123-149 (+ the try_put of :207)
+    def checkpoint_chunk(self, slices: Sequence[KvChunkSlice], state: AssignmentState) -> ChunkCheckpointOutcome:
+        cfg = self.cfg
+        if len(slices) != cfg.scheme.n:
+            raise LogicError("checkpoint: expected one slice per worker")
+        s0 = slices[0]
+        for s in slices:
+            if s.bytes.numel() != self.slice:
+                raise LogicError("checkpoint: slice has unexpected length")
+            if (s.chunk_id, s.request_id, s.valid_tokens) != (s0.chunk_id, s0.request_id, s0.valid_tokens):
+                raise LogicError("checkpoint: slices disagree on chunk identity")
+        return self.checkpoint_batch([list(slices)], state)[0]
+
+    def checkpoint_batch(self, batch: Sequence[Sequence[KvChunkSlice]], state: AssignmentState
+                         ) -> List[ChunkCheckpointOutcome]:
+        """Checkpoint several (request, chunk) stripes with ONE K1 launch +
+        overlapped D2H (e.g. the 32 requests of a decode block)."""
+        t0 = time.perf_counter()
+        cfg = self.cfg
+        sch = cfg.scheme
+        outs, slots, dsts, keys = [], [], [], []
+        for slices in batch:
+            s0 = slices[0]
+            worker = next_parity_worker(state, sch.n)
+            ptrs = self.store.reserve(s0.request_id, s0.chunk_id, sch, s0.valid_tokens, self.slice)
+            outs.append(ChunkCheckpointOutcome(s0.request_id, s0.chunk_id, s0.valid_tokens, worker, ptrs is not None))
+            if ptrs is None:
+                continue
+            slots.extend(s.bytes.data_ptr() for s in slices)
+            dsts.extend(ptrs)
+            keys.append((s0.request_id, s0.chunk_id))
+        if keys:
+            self.compute.wait_stream(torch.cuda.current_stream(self.dev))
+            check(L.lib().gs_encode_offload(self.pipe.handle, encoder(sch).handle, len(keys), L.ptr_array(slots),
+                                            L.ptr_array(dsts), self.slice, self.compute.cuda_stream,
+                                            self.copy.cuda_stream), "checkpoint")
+            for k in keys:
+                self.store.commit(k[0], k[1], self.copy)
+        dt = time.perf_counter() - t0
+        for o in outs:
+            o.enqueue_s = dt / max(len(outs), 1)
+        return outs
+
+    def make_slices(self, kv_seed: int, request_id: int, chunk: int, valid: int) -> List[KvChunkSlice]:
+        m = self.cfg.model
+        return [KvChunkSlice(request_id, chunk, w,
+                             make_ground_truth_slice(kv_seed, request_id, chunk, w, m, self.cfg.chunk_size, valid,
+                                                     device=self.dev), valid)
+                for w in range(self.cfg.scheme.n)]
+
+    # checkpoint.hpp:179-222
+    def run_prefill_with_checkpointing(self, request_id: int, input_tokens: int, kv_seed: int = 0,
+                                       keep_ground_truth: bool = True) -> PrefillRunResult:
+        cfg = self.cfg
+        chunks = chunk_count(input_tokens, cfg.chunk_size)
+        run = PrefillRunResult()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(self.compute)
+        for c in range(chunks):
+            valid = input_tokens - c * cfg.chunk_size if c + 1 == chunks else cfg.chunk_size
+            slices = self.make_slices(kv_seed, request_id, c, valid)
+            out = self.checkpoint_chunk(slices, run.state)
+            if not out.stored:
+                run.stalled_at_chunk = c
+                break
+            if keep_ground_truth:
+                run.ground_truth.append(slices)
+            run.chunks_done += 1
+        self.compute.wait_stream(self.copy)
+        e1.record(self.compute)
+        e1.synchronize()
+        run.device_ms = e0.elapsed_time(e1)
+        run.completed = run.stalled_at_chunk is None
+        return run
+
+    # recovery.hpp:100-133
+    def reconstruct_chunk(self, chunk_id: int, surviving: Sequence[KvChunkSlice], request_id: int,
+                          failed: Set[int]) -> ChunkRepairResult:
+        sch = self.cfg.scheme
+        if len(failed) > max_tolerance(sch):
+            raise UnrecoverableError("recovery: failures exceed scheme tolerance")
+        res = ChunkRepairResult()
+        status, entry = self.store.get(request_id, chunk_id, verify=True)
+        if status != ParityGetStatus.kOk or not entry.payload_present():
+            res.status = ChunkRepairStatus.kBadParity
+            return res
+        lost = ErasurePattern(sorted(failed))
+        dec = decoder(sch, lost)
+        slots: List[Optional[int]] = [None] * (sch.n + sch.k)
+        for s in surviving:
+            if s.worker not in failed:
+                slots[s.worker] = s.bytes.data_ptr()
+        for i in range(sch.k):
+            slots[sch.n + i] = entry.parity[i].ctypes.data
+        for j in range(sch.n):
+            if j not in failed and slots[j] is None:
+                raise InvalidArgument(f"coding: surviving shard {j} missing from input")
+        outs = {w: torch.empty(self.slice, dtype=torch.uint8, device=self.dev) for w in dec.out_index}
+        if dec.n_out:
+            self.compute.wait_stream(torch.cuda.current_stream(self.dev))
+            check(L.lib().gs_reconstruct_upload(self.pipe.handle, dec.handle, 1, L.ptr_array(slots),
+                                                L.ptr_array([outs[w].data_ptr() for w in dec.out_index]),
+                                                self.slice, self.compute.cuda_stream, self.copy.cuda_stream),
+                  "reconstruct_chunk")
+            torch.cuda.current_stream(self.dev).wait_stream(self.compute)
+        for w, t in outs.items():
+            res.recovered[w] = KvChunkSlice(request_id, chunk_id, w, t, entry.valid_tokens)
+        return res
+
+    # recovery.hpp:176-298
+    def recover(self, request_id: int, failure: FailureEvent,
+                ground_truth: Optional[List[List[KvChunkSlice]]], chunk_tokens: Sequence[int],
+                buffered_decode_tokens: int = 0) -> RecoveryResult:
+        cfg = self.cfg
+        if not failure.failed_workers:
+            raise InvalidArgument("recovery: no failed workers")
+        n = failure.at_chunk
+        if len(chunk_tokens) < n:
+            raise InvalidArgument("recovery: missing chunk token counts")
+        result = RecoveryResult()
+        plan = result.plan
+        over = len(failure.failed_workers) > max_tolerance(cfg.scheme)
+        r = n if over else get_recompute_units(n, cfg.chunk_size, cfg.scheme, self.slice, cfg.cost)
+        parity_ok = True
+        if not over and r < n:
+            for c in range(r, n):
+                if self.store.get(request_id, c)[0] != ParityGetStatus.kOk:
+                    parity_ok = False
+                    break
+        if over or (not parity_ok and r < n):
+            plan.mode, r = RecoveryMode.kFullRecomputeFallback, n
+        elif r >= n:
+            plan.mode, r = RecoveryMode.kPureRecompute, n
+        else:
+            plan.mode = RecoveryMode.kHybrid
+        plan.recompute_chunks = r
+        plan.reconstruct_ids = list(range(r, n))
+        result.parity_bytes_fetched = len(plan.reconstruct_ids) * cfg.scheme.k * self.slice
+        if ground_truth is None:
+            return result
+        if len(ground_truth) < n:
+            raise RuntimeError("recovery: ground truth missing for completed chunks")
+        failed = set(failure.failed_workers)
+        for w in failure.failed_workers:
+            result.recovered[w] = [None] * n
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(self.compute)
+        for c in range(n):
+            gt = ground_truth[c]
+            if c < r:   # recompute lane stand-in: restore from the oracle slices
+                for w in failure.failed_workers:
+                    result.recovered[w][c] = gt[w]
+                continue
+            rep = self.reconstruct_chunk(c, gt, request_id, failed)
+            if rep.status != ChunkRepairStatus.kOk:
+                raise RuntimeError("recovery: parity failed verification mid-recovery")
+            for w in failure.failed_workers:
+                if w not in rep.recovered:
+                    raise RuntimeError("recovery: codec did not return a failed shard")
+                result.recovered[w][c] = rep.recovered[w]
+        e1.record(self.compute)
+        e1.synchronize()
+        result.reconstruct_device_ms = e0.elapsed_time(e1)
+        for c in range(r, n):
+            for w in failure.failed_workers:
+                if not verify_recovery(result.recovered[w][c], ground_truth[c][w]):
+                    result.verified = False
+        return result
+
+
+class DecodeCheckpointer:
+    """checkpoint.hpp:228-281: buffer decode tokens, emit a chunk checkpoint
+    every m tokens, flush the masked tail at request end."""
+
+    def __init__(self, request_id: int, first_chunk_index: int, ckpt: Checkpointer, kv_seed: int = 0):
+        ckpt.cfg.validate()
+        self.request_id = request_id
+        self.next_chunk = first_chunk_index
+        self.ckpt = ckpt
+        self.kv_seed = kv_seed
+        self.buffered = 0
+        self.ground_truth: List[List[KvChunkSlice]] = []
+
+    def buffered_tokens(self) -> int:
+        return self.buffered
+
+    def step(self, state: AssignmentState) -> Optional[ChunkCheckpointOutcome]:
+        self.buffered += 1
+        if self.buffered < self.ckpt.cfg.chunk_size:
+            return None
+        return self._emit(state)
+
+    def flush(self, state: AssignmentState) -> Optional[ChunkCheckpointOutcome]:
+        if self.buffered == 0:
+            return None
+        return self._emit(state)
+
+    def _emit(self, state: AssignmentState) -> ChunkCheckpointOutcome:
+        valid = self.buffered
+        slices = self.ckpt.make_slices(self.kv_seed, self.request_id, self.next_chunk, valid)
+        out = self.ckpt.checkpoint_chunk(slices, state)
+        self.ground_truth.append(slices)
+        self.next_chunk += 1
+        self.buffered = 0
+        return out

@@ -56,8 +56,18 @@ class Unsupported(NotImplementedError, L.GhostServeError):
     status = L.GS_UNSUPPORTED
 
 
+class LogicError(RuntimeError, L.GhostServeError):
+    """std::logic_error (e.g. duplicate parity-store entry, parity_store.hpp:78-82)."""
+    status = L.GS_LOGIC_ERROR
+
+
+class ParityFileError(RuntimeError, L.GhostServeError):
+    """std::runtime_error of the GSRV reader (parity_store.hpp:301-397)."""
+    status = L.GS_RUNTIME_ERROR
+
+
 _BY_STATUS = {c.status: c for c in (InvalidArgument, UnrecoverableError, DomainError, CudaError,
-                                     Unsupported)}
+                                     Unsupported, LogicError, ParityFileError)}
 
 
 def check(status: int, what: str = "") -> None:

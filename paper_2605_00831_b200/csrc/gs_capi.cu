@@ -36,6 +36,10 @@ int special_decoders_kreedsolomon_8_2_e2(SpecialEntry* out);
 
 using namespace gsb;
 
+namespace gsb {
+void set_last_error(const char* msg);
+}
+
 // ============================================================================
 // errors
 // ============================================================================
@@ -160,6 +164,8 @@ const Registry& registry() {
 }
 
 }  // namespace
+
+void gsb::set_last_error(const char* msg) { g_err = msg; }
 
 // ============================================================================
 // codec
@@ -494,6 +500,8 @@ const char* gs_status_string(int status) {
     case GS_DOMAIN_ERROR: return "domain error";
     case GS_CUDA_ERROR: return "cuda error";
     case GS_UNSUPPORTED: return "unsupported";
+    case GS_LOGIC_ERROR: return "logic error";
+    case GS_RUNTIME_ERROR: return "runtime error";
     default: return "unknown status";
   }
 }

@@ -1,0 +1,519 @@
+// gs_store.cu -- the host tier of the checkpoint: a ParityStore on pinned
+// slabs (parity_store.hpp:31-143, 145-263 restated B200-side).
+//
+// Differences from the reference, all on the byte path's behalf:
+//  * entries are RESERVED first and the encode kernel's D2H lands directly in
+//    the entry's pinned slab (the reference encodes into fresh vectors and
+//    copies them again in try_put, checkpoint.hpp:207);
+//  * the FNV-1a seal (serial per chunk, ~0.5 GB/s per core) runs on a pool
+//    of host threads, triggered from the copy stream by cudaLaunchHostFunc
+//    once the parity bytes have landed -- off the GPU's critical path;
+//  * pinned memory comes from a slab pool (cudaHostAlloc costs ~ms per call).
+// Accounting, back-pressure, duplicate handling, get() verification and the
+// GSRV file format are the reference's.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <atomic>
+#include <condition_variable>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <deque>
+#include <map>
+#include <mutex>
+#include <string>
+#include <thread>
+#include <vector>
+
+#include "../../include/gs_capi.h"
+
+namespace gsb {
+void set_last_error(const char* msg);  // gs_capi.cu: shared gs_last_error() slot
+}
+
+namespace {
+
+int sfail(int status, const char* fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  std::vsnprintf(buf, sizeof buf, fmt, ap);
+  va_end(ap);
+  gsb::set_last_error(buf);
+  return status;
+}
+
+constexpr uint64_t kMetaBytes = 64;  // parity_store.hpp:67 kPerEntryMetadataBytes
+constexpr uint64_t kUnlimited = ~0ull;
+
+// Pinned slabs carved by exact size class; blocks are recycled, slabs are
+// returned when the store dies.
+class SlabPool {
+ public:
+  explicit SlabPool(size_t slab) : slab_(slab) {}
+  ~SlabPool() {
+    for (void* s : slabs_) cudaFreeHost(s);
+  }
+  int alloc(size_t bytes, uint8_t** out) {
+    bytes = std::max<size_t>(4096, (bytes + 4095) / 4096 * 4096);
+    auto& fl = free_[bytes];
+    if (!fl.empty()) {
+      *out = fl.back();
+      fl.pop_back();
+      return GS_OK;
+    }
+    if (bytes > slab_ / 4) {  // large entries get their own allocation
+      void* p = nullptr;
+      cudaError_t e = cudaHostAlloc(&p, bytes, cudaHostAllocPortable);
+      if (e != cudaSuccess) return sfail(GS_CUDA_ERROR, "store: pinned alloc of %zu B: %s", bytes, cudaGetErrorString(e));
+      slabs_.push_back(p);
+      *out = static_cast<uint8_t*>(p);
+      return GS_OK;
+    }
+    if (!cur_ || used_ + bytes > slab_) {
+      void* p = nullptr;
+      cudaError_t e = cudaHostAlloc(&p, slab_, cudaHostAllocPortable);
+      if (e != cudaSuccess) return sfail(GS_CUDA_ERROR, "store: pinned slab alloc: %s", cudaGetErrorString(e));
+      slabs_.push_back(p);
+      cur_ = static_cast<uint8_t*>(p);
+      used_ = 0;
+    }
+    *out = cur_ + used_;
+    used_ += bytes;
+    return GS_OK;
+  }
+  void release(uint8_t* p, size_t bytes) {
+    bytes = std::max<size_t>(4096, (bytes + 4095) / 4096 * 4096);
+    free_[bytes].push_back(p);
+  }
+
+ private:
+  size_t slab_;
+  std::vector<void*> slabs_;
+  uint8_t* cur_ = nullptr;
+  size_t used_ = 0;
+  std::map<size_t, std::vector<uint8_t*>> free_;
+};
+
+uint64_t fnv_chain(const uint8_t* p, size_t n, uint64_t h) { return gs_fnv1a64(p, n, h); }
+
+}  // namespace
+
+struct gs_store {
+  struct Entry {
+    int kind = 0, n = 0, k = 0;
+    uint32_t valid = 0;
+    uint64_t slice_len = 0;
+    uint8_t* buf = nullptr;  // k * slice_len, parity i at buf + i * slice_len
+    uint64_t checksum = 0;
+    bool sealed = false;
+    bool owned = true;
+    uint64_t payload() const { return static_cast<uint64_t>(k) * slice_len; }
+  };
+  using Key = std::pair<uint64_t, uint32_t>;
+
+  uint64_t capacity = kUnlimited;
+  uint64_t used = 0, payload = 0, peak = 0;
+  std::map<Key, Entry> entries;
+  SlabPool pool{size_t{256} << 20};
+  std::mutex mu;
+  std::condition_variable sealed_cv;
+
+  // seal workers
+  std::deque<Key> jobs;
+  std::condition_variable job_cv;
+  std::vector<std::thread> workers;
+  bool stop = false;
+  std::atomic<uint64_t> pending{0};
+
+  void worker() {
+    for (;;) {
+      Key key;
+      uint8_t* buf = nullptr;
+      uint64_t len = 0;
+      {
+        std::unique_lock<std::mutex> lk(mu);
+        job_cv.wait(lk, [&] { return stop || !jobs.empty(); });
+        if (stop && jobs.empty()) return;
+        key = jobs.front();
+        jobs.pop_front();
+        auto it = entries.find(key);
+        if (it == entries.end()) {
+          --pending;
+          lk.unlock();
+          sealed_cv.notify_all();
+          continue;
+        }
+        buf = it->second.buf;
+        len = it->second.payload();
+      }
+      // parity_store.hpp:46-50: FNV chained over the k buffers in order ==
+      // FNV over the contiguous k * slice_len bytes.
+      const uint64_t h = fnv_chain(buf, len, 0xcbf29ce484222325ull);
+      {
+        std::lock_guard<std::mutex> lk(mu);
+        auto it = entries.find(key);
+        if (it != entries.end()) {
+          it->second.checksum = h;
+          it->second.sealed = true;
+        }
+        --pending;
+      }
+      sealed_cv.notify_all();
+    }
+  }
+
+  struct HostJob {
+    gs_store* s;
+    Key key;
+  };
+  static void CUDART_CB on_stream(void* p) {
+    auto* j = static_cast<HostJob*>(p);
+    {
+      std::lock_guard<std::mutex> lk(j->s->mu);
+      j->s->jobs.push_back(j->key);
+    }
+    j->s->job_cv.notify_one();
+    delete j;
+  }
+
+  ~gs_store() {
+    {
+      std::lock_guard<std::mutex> lk(mu);
+      stop = true;
+    }
+    job_cv.notify_all();
+    for (auto& t : workers) t.join();
+  }
+};
+
+extern "C" {
+
+int gs_store_create(uint64_t capacity_bytes, int seal_threads, gs_store** out) {
+  if (!out) return sfail(GS_INVALID_ARGUMENT, "store_create: out is NULL");
+  auto* s = new gs_store;
+  s->capacity = capacity_bytes;
+  const int t = std::max(1, seal_threads);
+  for (int i = 0; i < t; ++i) s->workers.emplace_back([s] { s->worker(); });
+  *out = s;
+  return GS_OK;
+}
+
+int gs_store_destroy(gs_store* s) {
+  if (!s) return GS_OK;
+  gs_store_wait_sealed(s);
+  delete s;
+  return GS_OK;
+}
+
+int gs_store_reserve(gs_store* s, uint64_t request_id, uint32_t chunk, int kind, int n, int k,
+                     uint32_t valid_tokens, uint64_t slice_len, int* accepted, void** parity_out) {
+  if (!s || !accepted) return sfail(GS_INVALID_ARGUMENT, "store_reserve: NULL argument");
+  if (int st = gs_scheme_validate(kind, n, k)) return sfail(st, "%s", gs_last_error());
+  *accepted = 0;
+  std::lock_guard<std::mutex> lk(s->mu);
+  const gs_store::Key key{request_id, chunk};
+  if (s->entries.count(key))  // parity_store.hpp:78-82
+    return sfail(GS_LOGIC_ERROR, "parity store: duplicate entry for request %llu chunk %u",
+                 static_cast<unsigned long long>(request_id), chunk);
+  const uint64_t pay = static_cast<uint64_t>(k) * slice_len;
+  const uint64_t cost = pay + kMetaBytes;
+  if (s->capacity != kUnlimited && s->used + cost > s->capacity) return GS_OK;  // back-pressure (:83)
+  gs_store::Entry e;
+  e.kind = kind;
+  e.n = n;
+  e.k = k;
+  e.valid = valid_tokens;
+  e.slice_len = slice_len;
+  if (pay) {
+    if (int st = s->pool.alloc(pay, &e.buf)) return st;
+  }
+  s->used += cost;
+  s->payload += pay;
+  s->peak = std::max(s->peak, s->payload);
+  if (parity_out)
+    for (int i = 0; i < k; ++i) parity_out[i] = e.buf ? e.buf + static_cast<uint64_t>(i) * slice_len : nullptr;
+  s->entries.emplace(key, e);
+  *accepted = 1;
+  return GS_OK;
+}
+
+int gs_store_commit(gs_store* s, uint64_t request_id, uint32_t chunk, void* stream) {
+  if (!s) return sfail(GS_INVALID_ARGUMENT, "store_commit: NULL store");
+  {
+    std::lock_guard<std::mutex> lk(s->mu);
+    if (!s->entries.count({request_id, chunk}))
+      return sfail(GS_INVALID_ARGUMENT, "store_commit: no reserved entry for request %llu chunk %u",
+                   static_cast<unsigned long long>(request_id), chunk);
+    ++s->pending;
+  }
+  if (stream) {
+    auto* job = new gs_store::HostJob{s, {request_id, chunk}};
+    cudaError_t e = cudaLaunchHostFunc(static_cast<cudaStream_t>(stream), &gs_store::on_stream, job);
+    if (e != cudaSuccess) {
+      delete job;
+      --s->pending;
+      return sfail(GS_CUDA_ERROR, "store_commit: cudaLaunchHostFunc: %s", cudaGetErrorString(e));
+    }
+    return GS_OK;
+  }
+  {
+    std::lock_guard<std::mutex> lk(s->mu);
+    s->jobs.push_back({request_id, chunk});
+  }
+  s->job_cv.notify_one();
+  return GS_OK;
+}
+
+int gs_store_wait_sealed(gs_store* s) {
+  if (!s) return GS_OK;
+  std::unique_lock<std::mutex> lk(s->mu);
+  s->sealed_cv.wait(lk, [&] { return s->pending.load() == 0; });
+  return GS_OK;
+}
+
+// Copying put with the reference's try_put semantics (parity_store.hpp:77-90):
+// parity[k] host buffers are copied into the store and sealed synchronously.
+int gs_store_put(gs_store* s, uint64_t request_id, uint32_t chunk, int kind, int n, int k,
+                 uint32_t valid_tokens, uint64_t slice_len, const void* const* parity, uint64_t checksum,
+                 int sealed, int* accepted) {
+  void* dst[256];
+  if (k > 256) return sfail(GS_INVALID_ARGUMENT, "store_put: k too large");
+  if (int st = gs_store_reserve(s, request_id, chunk, kind, n, k, valid_tokens, slice_len, accepted, dst)) return st;
+  if (!*accepted) return GS_OK;
+  for (int i = 0; i < k; ++i)
+    if (slice_len) std::memcpy(dst[i], parity[i], slice_len);
+  std::lock_guard<std::mutex> lk(s->mu);
+  auto& e = s->entries.at({request_id, chunk});
+  e.checksum = sealed ? checksum : (e.buf ? fnv_chain(e.buf, e.payload(), 0xcbf29ce484222325ull)
+                                          : 0xcbf29ce484222325ull);
+  e.sealed = true;
+  return GS_OK;
+}
+
+// parity_store.hpp:92-101: kOk / kMissing / kCorrupt (status out: 0/1/2).
+int gs_store_get(gs_store* s, uint64_t request_id, uint32_t chunk, int verify, int* status, void** parity_out,
+                 uint64_t* slice_len, uint32_t* valid_tokens, uint64_t* checksum, int* kind_n_k) {
+  if (!s || !status) return sfail(GS_INVALID_ARGUMENT, "store_get: NULL argument");
+  std::unique_lock<std::mutex> lk(s->mu);
+  auto it = s->entries.find({request_id, chunk});
+  if (it == s->entries.end()) {
+    *status = 1;
+    return GS_OK;
+  }
+  s->sealed_cv.wait(lk, [&] {
+    auto jt = s->entries.find({request_id, chunk});
+    return jt == s->entries.end() || jt->second.sealed;
+  });
+  it = s->entries.find({request_id, chunk});
+  if (it == s->entries.end()) {
+    *status = 1;
+    return GS_OK;
+  }
+  const gs_store::Entry e = it->second;
+  lk.unlock();
+  if (verify && e.buf && fnv_chain(e.buf, e.payload(), 0xcbf29ce484222325ull) != e.checksum) {
+    *status = 2;
+    return GS_OK;
+  }
+  *status = 0;
+  if (parity_out)
+    for (int i = 0; i < e.k; ++i) parity_out[i] = e.buf ? e.buf + static_cast<uint64_t>(i) * e.slice_len : nullptr;
+  if (slice_len) *slice_len = e.slice_len;
+  if (valid_tokens) *valid_tokens = e.valid;
+  if (checksum) *checksum = e.checksum;
+  if (kind_n_k) {
+    kind_n_k[0] = e.kind;
+    kind_n_k[1] = e.n;
+    kind_n_k[2] = e.k;
+  }
+  return GS_OK;
+}
+
+int gs_store_contains(gs_store* s, uint64_t request_id, uint32_t chunk) {
+  if (!s) return 0;
+  std::lock_guard<std::mutex> lk(s->mu);
+  return s->entries.count({request_id, chunk}) ? 1 : 0;
+}
+
+// parity_store.hpp:105-112
+int gs_store_erase_request(gs_store* s, uint64_t request_id) {
+  if (!s) return sfail(GS_INVALID_ARGUMENT, "store_erase: NULL store");
+  gs_store_wait_sealed(s);
+  std::lock_guard<std::mutex> lk(s->mu);
+  auto it = s->entries.lower_bound({request_id, 0u});
+  while (it != s->entries.end() && it->first.first == request_id) {
+    s->used -= it->second.payload() + kMetaBytes;
+    s->payload -= it->second.payload();
+    if (it->second.buf && it->second.owned) s->pool.release(it->second.buf, it->second.payload());
+    it = s->entries.erase(it);
+  }
+  return GS_OK;
+}
+
+// used, capacity, payload, peak_payload, entry_count
+int gs_store_stats(gs_store* s, uint64_t* out5) {
+  if (!s || !out5) return sfail(GS_INVALID_ARGUMENT, "store_stats: NULL argument");
+  std::lock_guard<std::mutex> lk(s->mu);
+  out5[0] = s->used;
+  out5[1] = s->capacity;
+  out5[2] = s->payload;
+  out5[3] = s->peak;
+  out5[4] = s->entries.size();
+  return GS_OK;
+}
+
+// parity_store.hpp:115-123
+int gs_store_audit(gs_store* s) {
+  if (!s) return 0;
+  std::lock_guard<std::mutex> lk(s->mu);
+  uint64_t sum = 0;
+  for (const auto& kv : s->entries) sum += kv.second.payload() + kMetaBytes;
+  return sum == s->used ? 1 : 0;
+}
+
+// Test hook (parity_store.hpp:126-131): flip parity[0][0].
+int gs_store_corrupt_entry(gs_store* s, uint64_t request_id, uint32_t chunk) {
+  if (!s) return GS_OK;
+  gs_store_wait_sealed(s);
+  std::lock_guard<std::mutex> lk(s->mu);
+  auto it = s->entries.find({request_id, chunk});
+  if (it == s->entries.end() || !it->second.buf || !it->second.payload()) return GS_OK;
+  it->second.buf[0] ^= 0xFF;
+  return GS_OK;
+}
+
+// Keys in (request, chunk) order: keys[2*i] = request, keys[2*i+1] = chunk.
+int gs_store_keys(gs_store* s, uint64_t* keys, uint64_t max_entries, uint64_t* count) {
+  if (!s || !count) return sfail(GS_INVALID_ARGUMENT, "store_keys: NULL argument");
+  std::lock_guard<std::mutex> lk(s->mu);
+  uint64_t i = 0;
+  for (const auto& kv : s->entries) {
+    if (keys && i < max_entries) {
+      keys[2 * i] = kv.first.first;
+      keys[2 * i + 1] = kv.first.second;
+    }
+    ++i;
+  }
+  *count = i;
+  return GS_OK;
+}
+
+// ---- GSRV persistence (parity_store.hpp:145-263) --------------------------
+// magic "GSRV", u16 version=1, u8 kind, u8 n, u8 k; per entry (key order):
+// u64 request, u32 chunk, u32 valid_tokens, u64 slice_len, k * slice_len
+// parity bytes, u64 checksum. All little-endian.
+int gs_store_serialize(gs_store* s, void* out, uint64_t cap, uint64_t* size) {
+  if (!s || !size) return sfail(GS_INVALID_ARGUMENT, "store_serialize: NULL argument");
+  gs_store_wait_sealed(s);
+  std::lock_guard<std::mutex> lk(s->mu);
+  if (s->entries.empty()) return sfail(GS_INVALID_ARGUMENT, "parity store: nothing to serialize");
+  const auto& first = s->entries.begin()->second;
+  uint64_t need = 4 + 2 + 3;
+  for (const auto& kv : s->entries) {
+    const auto& e = kv.second;
+    if (e.kind != first.kind || e.n != first.n || e.k != first.k)
+      return sfail(GS_INVALID_ARGUMENT, "parity store: mixed schemes cannot be serialized");
+    if (!e.buf && e.payload())
+      return sfail(GS_INVALID_ARGUMENT, "parity store: cannot serialize entries without payloads");
+    need += 8 + 4 + 4 + 8 + e.payload() + 8;
+  }
+  *size = need;
+  if (!out) return GS_OK;
+  if (cap < need) return sfail(GS_INVALID_ARGUMENT, "store_serialize: buffer too small (%llu < %llu)",
+                               static_cast<unsigned long long>(cap), static_cast<unsigned long long>(need));
+  uint8_t* p = static_cast<uint8_t*>(out);
+  auto put = [&](uint64_t v, int bytes) {
+    for (int i = 0; i < bytes; ++i) *p++ = static_cast<uint8_t>(v >> (8 * i));
+  };
+  *p++ = 'G';
+  *p++ = 'S';
+  *p++ = 'R';
+  *p++ = 'V';
+  put(1, 2);
+  put(static_cast<uint64_t>(first.kind), 1);
+  put(static_cast<uint64_t>(first.n), 1);
+  put(static_cast<uint64_t>(first.k), 1);
+  for (const auto& kv : s->entries) {
+    const auto& e = kv.second;
+    put(kv.first.first, 8);
+    put(kv.first.second, 4);
+    put(e.valid, 4);
+    put(e.slice_len, 8);
+    if (e.payload()) std::memcpy(p, e.buf, e.payload());
+    p += e.payload();
+    put(e.checksum, 8);
+  }
+  return GS_OK;
+}
+
+int gs_store_deserialize(const void* bytes, uint64_t size, uint64_t capacity, int seal_threads, gs_store** out) {
+  if (!bytes || !out) return sfail(GS_INVALID_ARGUMENT, "store_deserialize: NULL argument");
+  *out = nullptr;
+  const uint8_t* p = static_cast<const uint8_t*>(bytes);
+  uint64_t pos = 0;
+  auto take = [&](uint64_t n, const uint8_t** q) -> bool {
+    if (pos + n > size) return false;
+    *q = p + pos;
+    pos += n;
+    return true;
+  };
+  auto get = [&](int nbytes, uint64_t* v) -> bool {
+    const uint8_t* q;
+    if (!take(static_cast<uint64_t>(nbytes), &q)) return false;
+    *v = 0;
+    for (int i = 0; i < nbytes; ++i) *v |= static_cast<uint64_t>(q[i]) << (8 * i);
+    return true;
+  };
+  const uint8_t* magic;
+  if (!take(4, &magic)) return sfail(GS_RUNTIME_ERROR, "parity file: truncated");
+  if (std::memcmp(magic, "GSRV", 4) != 0) return sfail(GS_RUNTIME_ERROR, "parity file: bad magic");
+  uint64_t version, kind, n, k;
+  if (!get(2, &version)) return sfail(GS_RUNTIME_ERROR, "parity file: truncated");
+  if (version != 1) return sfail(GS_RUNTIME_ERROR, "parity file: unsupported version");
+  if (!get(1, &kind) || !get(1, &n) || !get(1, &k)) return sfail(GS_RUNTIME_ERROR, "parity file: truncated");
+  if (int st = gs_scheme_validate(static_cast<int>(kind), static_cast<int>(n), static_cast<int>(k)))
+    return sfail(st, "%s", gs_last_error());
+  gs_store* s = nullptr;
+  gs_store_create(capacity, seal_threads, &s);
+  while (pos < size) {
+    uint64_t req, chunk, valid, slice;
+    if (!get(8, &req) || !get(4, &chunk) || !get(4, &valid) || !get(8, &slice)) {
+      gs_store_destroy(s);
+      return sfail(GS_RUNTIME_ERROR, "parity file: truncated");
+    }
+    const uint8_t* payload;
+    if (slice > size || !take(k * slice, &payload)) {
+      gs_store_destroy(s);
+      return sfail(GS_RUNTIME_ERROR, "parity file: truncated");
+    }
+    uint64_t checksum;
+    if (!get(8, &checksum)) {
+      gs_store_destroy(s);
+      return sfail(GS_RUNTIME_ERROR, "parity file: truncated");
+    }
+    if (fnv_chain(payload, k * slice, 0xcbf29ce484222325ull) != checksum) {
+      gs_store_destroy(s);
+      return sfail(GS_RUNTIME_ERROR, "parity file: checksum mismatch for request %llu chunk %llu",
+                   static_cast<unsigned long long>(req), static_cast<unsigned long long>(chunk));
+    }
+    const void* par[256];
+    for (uint64_t i = 0; i < k; ++i) par[i] = payload + i * slice;
+    int accepted = 0;
+    int st = gs_store_put(s, req, static_cast<uint32_t>(chunk), static_cast<int>(kind), static_cast<int>(n),
+                          static_cast<int>(k), static_cast<uint32_t>(valid), slice, par, checksum, 1, &accepted);
+    if (st) {
+      gs_store_destroy(s);
+      return st;
+    }
+    if (!accepted) {
+      gs_store_destroy(s);
+      return sfail(GS_RUNTIME_ERROR, "parity file: contents exceed store capacity");
+    }
+  }
+  *out = s;
+  return GS_OK;
+}
+
+}  // extern "C"

@@ -151,6 +151,21 @@ def main() -> None:
                   "a": fnv(np.frombuffer(b"a", np.uint8)),
                   "foobar": fnv(np.frombuffer(b"foobar", np.uint8))}
 
+    # GSRV image written by the reference's serialize_parity_store
+    import ctypes as C
+    keys = [(7, 2, 16), (3, 0, 16), (3, 1, 5)]  # (request, chunk, valid): out of order on purpose
+    gl, gk = 33, 2
+    pars = [splitmix_bytes(5000 + 10 * i + j, gl) for i in range(len(keys)) for j in range(gk)]
+    req = (C.c_uint64 * 3)(*[x[0] for x in keys])
+    chk = (C.c_uint32 * 3)(*[x[1] for x in keys])
+    val = (C.c_uint32 * 3)(*[x[2] for x in keys])
+    size = C.c_uint64()
+    buf = np.zeros(4096, np.uint8)
+    assert R.fn("gsrv_image")(O.RS, 4, gk, 3, req, chk, val, C.c_uint64(gl), O._ptrs(pars),
+                              buf.ctypes.data_as(C.POINTER(C.c_uint8)), C.c_uint64(4096), C.byref(size)) == 0
+    out["gsrv"] = {"kind": O.RS, "n": 4, "k": gk, "slice_len": gl, "keys": keys, "parity_seed": 5000,
+                   "image_hex": buf[: size.value].tobytes().hex()}
+
     path = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden.json")
     with open(path, "w") as f:
         json.dump(out, f, indent=1, sort_keys=True)

@@ -1,0 +1,165 @@
+"""Checkpoint / recovery orchestration (checkpoint.hpp, recovery.hpp,
+cost_model.hpp): planner + assignment logic on CPU; the byte path on GPU,
+checked against the CPU oracle (checkpoint_test.cpp:151-292,
+recovery_test.cpp:135-317)."""
+import itertools
+import random
+
+import numpy as np
+import pytest
+
+from oracle import oracle as O
+from paper_2605_00831_b200.checkpoint import (AssignmentState, CheckpointConfig, CostModel, FailureEvent,
+                                              RecoveryMode, get_recompute_units, next_parity_worker)
+from paper_2605_00831_b200.coding import CodingScheme, InvalidArgument
+from paper_2605_00831_b200.kv_layout import ModelConfig
+
+
+def sweep(n, m, scheme, slice_, cost):
+    best, best_f = 0, float("inf")
+    for r in range(n + 1):
+        f = max(r * m * cost.compute_per_token + cost.restart_overhead, (n - r) * cost.reconstruct_chunk_time(scheme, slice_))
+        if f < best_f:
+            best, best_f = r, f
+    return best
+
+
+def test_recompute_units_match_sweep_oracle():
+    # recovery_test.cpp:67-89 / acceptance.cpp C6(a)
+    rng = random.Random(99)
+    for _ in range(1000):
+        cost = CostModel(compute_per_token=rng.uniform(1e-7, 1e-3), intra_bw=rng.uniform(50e9, 900e9))
+        cost.host_bw = rng.uniform(0.5e9, cost.intra_bw)
+        cost.encode_rate = rng.uniform(10e9, 500e9)
+        cost.reconstruct_rate = rng.uniform(10e9, 500e9)
+        cost.fixed_collective_latency = rng.uniform(0, 1e-4)
+        cost.restart_overhead = rng.uniform(0, 5.0)
+        n, m = rng.randrange(200), 1 + rng.randrange(4096)
+        slice_ = 1 + rng.randrange(200 << 20)
+        scheme = CodingScheme.reed_solomon(8, 1 + rng.randrange(4))
+        assert get_recompute_units(n, m, scheme, slice_, cost) == sweep(n, m, scheme, slice_, cost)
+    assert get_recompute_units(0, 2048, CodingScheme.reed_solomon(8, 2), 1 << 20, CostModel()) == 0
+    free = CostModel(fixed_collective_latency=0)
+    assert get_recompute_units(32, 2048, CodingScheme.reed_solomon(8, 2), 0, free) == 0
+
+
+def test_round_robin_fairness_and_config_validation():
+    rng = random.Random(777)  # acceptance.cpp C7
+    for _ in range(300):
+        n, c = 1 + rng.randrange(32), 1 + rng.randrange(5000)
+        st = AssignmentState()
+        counts = [0] * n
+        for _ in range(c):
+            counts[next_parity_worker(st, n)] += 1
+        assert max(counts) - min(counts) <= 1
+    with pytest.raises(InvalidArgument):
+        next_parity_worker(AssignmentState(), 0)
+    with pytest.raises(InvalidArgument):
+        CheckpointConfig(CodingScheme.reed_solomon(4, 2), 16, ModelConfig(2, 8, 8, 2, 8)).validate()
+    with pytest.raises(InvalidArgument):
+        CostModel(host_bw=500e9, intra_bw=400e9).validate()
+    m = CostModel.measured(55.2, 5030.0, 5600.0)
+    m.validate()
+    assert m.host_bw == 55.2e9 and m.intra_bw == 770e9
+
+
+# ---------------------------------------------------------------- GPU ------
+def _ck(n, k, tp, chunk=16, capacity=None, layers=2, heads=8, dim=8, restart=1e-4):
+    torch = pytest.importorskip("torch")
+    from paper_2605_00831_b200.checkpoint import Checkpointer
+    from paper_2605_00831_b200.parity_store import ParityStore
+    cfg = CheckpointConfig(CodingScheme.reed_solomon(n, k), chunk, ModelConfig(layers, heads, dim, 2, tp))
+    cfg.cost.restart_overhead = restart
+    store = ParityStore() if capacity is None else ParityStore(capacity)
+    return Checkpointer(cfg, store), store, torch
+
+
+@pytest.mark.gpu
+def test_prefill_stored_parity_equals_encode_of_ground_truth():
+    ck, store, torch = _ck(4, 2, 4)
+    run = ck.run_prefill_with_checkpointing(11, 3 * 16 + 5, kv_seed=13)
+    ck.synchronize()
+    assert run.completed and run.chunks_done == 4
+    port = O.port()
+    for c in range(run.chunks_done):
+        st, entry = store.get(11, c)
+        assert int(st) == 0
+        valid = 16 if c < 3 else 5
+        assert entry.valid_tokens == valid
+        host = [port.make_ground_truth_slice(13, 11, c, w, 2, 8, 8, 4, 16, valid) for w in range(4)]
+        want = port.encode(O.RS, 4, 2, host)
+        for i in range(2):
+            assert np.array_equal(entry.parity[i], want[i]), (c, i)
+        assert entry.checksum == port.parity_checksum(want)
+    assert [s.worker for s in run.ground_truth[0]] == [0, 1, 2, 3]
+
+
+@pytest.mark.gpu
+def test_prefill_back_pressure_stops_at_the_offending_chunk():
+    slice_ = 2 * 2 * 16 * (8 * 8 // 4) * 2
+    ck, store, _ = _ck(4, 2, 4, capacity=2 * (2 * slice_ + 64) + 10)
+    run = ck.run_prefill_with_checkpointing(1, 5 * 16, kv_seed=3)
+    ck.synchronize()
+    assert not run.completed and run.stalled_at_chunk == 2 and run.chunks_done == 2
+    assert store.entry_count() == 2 and store.audit()
+
+
+@pytest.mark.gpu
+def test_decode_checkpointer_emits_every_m_tokens_and_flushes_tail():
+    from paper_2605_00831_b200.checkpoint import DecodeCheckpointer
+    ck, store, _ = _ck(8, 2, 8)
+    dc = DecodeCheckpointer(5, 100, ck, kv_seed=21)
+    st = AssignmentState()
+    emitted = [o for o in (dc.step(st) for _ in range(40)) if o is not None]
+    assert [o.chunk_id for o in emitted] == [100, 101] and dc.buffered_tokens() == 8
+    tail = dc.flush(st)
+    assert tail.chunk_id == 102 and tail.valid_tokens == 8 and dc.flush(st) is None
+    ck.synchronize()
+    port = O.port()
+    for c, valid in ((100, 16), (101, 16), (102, 8)):
+        entry = store.get(5, c)[1]
+        host = [port.make_ground_truth_slice(21, 5, c, w, 2, 8, 8, 8, 16, valid) for w in range(8)]
+        want = port.encode(O.RS, 8, 2, host)
+        assert all(np.array_equal(entry.parity[i], want[i]) for i in range(2))
+
+
+@pytest.mark.gpu
+def test_every_double_failure_rs42_bit_exact():
+    ck, store, _ = _ck(4, 2, 4)   # recovery_test.cpp:180-203
+    run = ck.run_prefill_with_checkpointing(9, 4 * 16, kv_seed=17)
+    ck.synchronize()
+    for pair in itertools.combinations(range(4), 2):
+        res = ck.recover(9, FailureEvent(list(pair), at_chunk=run.chunks_done), run.ground_truth,
+                         [16] * run.chunks_done)
+        assert res.verified
+        for w in pair:
+            for c in range(run.chunks_done):
+                assert res.recovered[w][c] is not None
+
+
+@pytest.mark.gpu
+def test_long_request_single_failure_rs82_bit_exact():
+    # recovery_test.cpp:299-317: 64K tokens, 32 chunks of 2048 through RS(8,2), worker 5 lost
+    ck, store, _ = _ck(8, 2, 8, chunk=2048)
+    run = ck.run_prefill_with_checkpointing(6, 65536, kv_seed=36)
+    assert run.completed and run.chunks_done == 32
+    ck.synchronize()
+    ck.cfg.cost.restart_overhead = 1e9   # force pure reconstruction of all 32 chunks
+    res = ck.recover(6, FailureEvent([5], at_chunk=32), run.ground_truth, [2048] * 32)
+    assert res.plan.mode == RecoveryMode.kHybrid and res.plan.recompute_chunks == 0
+    assert res.verified and len(res.plan.reconstruct_ids) == 32
+
+
+@pytest.mark.gpu
+def test_bad_parity_and_over_tolerance_fallbacks():
+    ck, store, _ = _ck(4, 2, 4)
+    run = ck.run_prefill_with_checkpointing(3, 4 * 16, kv_seed=5)
+    ck.synchronize()
+    store.corrupt_entry(3, 2)
+    rep = ck.reconstruct_chunk(2, run.ground_truth[2], 3, {1})
+    assert rep.status == 1 and not rep.recovered
+    res = ck.recover(3, FailureEvent([0, 1, 2], at_chunk=4), run.ground_truth, [16] * 4)
+    assert res.plan.mode == RecoveryMode.kFullRecomputeFallback and res.plan.recompute_chunks == 4
+    ck.cfg.cost.restart_overhead = 1e9
+    res = ck.recover(3, FailureEvent([1], at_chunk=4), run.ground_truth, [16] * 4)
+    assert res.plan.mode == RecoveryMode.kFullRecomputeFallback   # corrupt chunk 2 -> fallback
