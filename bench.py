@@ -461,6 +461,11 @@ def run_ours(args):
 
     if rank == 0 and world == 1 and not args.no_c3:
         recovery.update(c3_recovery(torch, dev, comp, copy, pipe))
+    if rank == 0 and world == 1 and not args.no_c4:
+        recovery.update(c4_recovery(torch, dev, comp, copy, pipe))
+    overhead = None
+    if rank == 0 and world == 1 and not args.no_overhead:
+        overhead = decode_overhead(torch, dev, pipe, args)
 
     if pg:
         pg.close()
@@ -479,10 +484,136 @@ def run_ours(args):
                            "single GPU holds all 8 TP shards"},
                 "roofline": kern or None, "roofline_k2": kern2 or None, "host_link": host_link, "cpu_baseline": cpu, "e2e": e2e,
                 "recovery_ms": recovery.get("c2_block_one_worker_ms"), "recovery": recovery,
+                "decode_overhead": overhead,
                 "gpu_launches": launches, "clocks": clk.summary(), "parity_ok": bool(ok_parity)}
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()
+
+
+def c4_recovery(torch, dev, comp, copy, pipe):
+    """C4: double-GPU failure, RS(6,2) -- rebuild two lost KV shards (workers 0
+    and 3) from the 4 survivors + BOTH parity rows uploaded from host.
+    Geometry 80 layers x 6 KV heads x 128 dim, TP=6 (6-divisible, SURVEY
+    §7 hard parts), 2K-token chunks (83,886,080 B slices), 8 chunks."""
+    from paper_2605_00831_b200 import _lib as L
+    from paper_2605_00831_b200 import kv_layout as K
+    from paper_2605_00831_b200.coding import CodingScheme, ErasurePattern, check, decoder, encoder
+
+    cfg = K.ModelConfig(80, 6, 128, 2, 6)
+    m, chunks, n, k = 2048, 8, 6, 2
+    sl = K.slice_bytes(cfg, m)
+    scheme = CodingScheme.reed_solomon(n, k)
+    kv = torch.empty((n, chunks, sl), dtype=torch.uint8, device=dev)
+    for w in range(n):
+        for c in range(chunks):
+            K.make_ground_truth_slice(KV_SEED, 4, c, w, cfg, m, m, out=kv[w, c])
+    h_par = torch.empty((chunks, k, sl), dtype=torch.uint8).pin_memory()
+    enc = encoder(scheme)
+    check(L.lib().gs_encode_offload(pipe.handle, enc.handle, chunks,
+                                    L.ptr_array([kv[w, c].data_ptr() for c in range(chunks) for w in range(n)]),
+                                    L.ptr_array([h_par[c, i].data_ptr() for c in range(chunks) for i in range(k)]),
+                                    sl, comp.cuda_stream, copy.cuda_stream), "c4 encode")
+    copy.synchronize()
+    lost = [0, 3]
+    saved = kv[lost].clone()
+    kv[lost].zero_()
+    torch.cuda.synchronize()
+    dec = decoder(scheme, ErasurePattern(lost))
+    slots = []
+    for c in range(chunks):
+        for j in range(n + k):
+            slots.append(None if j in lost else (kv[j, c].data_ptr() if j < n else h_par[c, j - n].data_ptr()))
+    outs = L.ptr_array([kv[w, c].data_ptr() for c in range(chunks) for w in dec.out_index])
+    sp = L.ptr_array(slots)
+    r0, r1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    r0.record(comp)
+    check(L.lib().gs_reconstruct_upload(pipe.handle, dec.handle, chunks, sp, outs, sl, comp.cuda_stream,
+                                        copy.cuda_stream), "c4 rebuild")
+    r1.record(comp)
+    r1.synchronize()
+    ms = r0.elapsed_time(r1)
+    ok = bool(torch.equal(kv[lost], saved))
+    out = {"c4_rs62_two_lost_ms": round(ms, 2), "c4_bytes_rebuilt": 2 * chunks * sl,
+           "c4_h2d_gbs": round(2 * chunks * sl / (ms * 1e-3) / 1e9, 2), "c4_decoder_specialised": dec.specialised,
+           "c4_rebuild_ok": ok}
+    del kv, h_par, saved
+    torch.cuda.empty_cache()
+    return out
+
+
+def decode_overhead(torch, dev, pipe, args):
+    """Per-16-token-block checkpoint overhead vs the decode step (north_star
+    target < 5%), Llama-3-70B KV at TP=8, batch 32, as seen by ONE GPU of the
+    TP group. Decode-step stand-in: stream this GPU's weight
+    shard (70.6e9 x 2 B / 8 = 17.65 GB) plus its KV at the chosen context
+    (32 x ctx x 40,960 B) from HBM. Block checkpoint: K1 over this GPU's 1/8
+    byte range of the 8 workers' block slices (32 x 8 x 81,920 B = 20 MiB in,
+    5 MiB parity) + D2H of the parity, on side streams, once per 16 steps."""
+    from paper_2605_00831_b200 import _lib as L
+    from paper_2605_00831_b200.coding import CodingScheme, check, encoder
+
+    ctx = args.decode_ctx
+    wbytes = int(70.6e9 * 2 / 8)
+    kvbytes = 32 * ctx * 40960
+    free, _ = torch.cuda.mem_get_info(dev)
+    if free < wbytes + kvbytes + (4 << 30):
+        return {"skipped": f"needs {(wbytes + kvbytes) >> 30} GiB"}
+    w = torch.zeros(wbytes // 4, dtype=torch.float32, device=dev)
+    kvc = torch.zeros(kvbytes // 4, dtype=torch.float32, device=dev)
+    rng = 81920                                   # 655,360 B block slice / 8 GPUs
+    data = torch.randint(0, 256, (32, 8, rng), dtype=torch.uint8, device=dev)
+    h_par = torch.empty((32, 2, rng), dtype=torch.uint8).pin_memory()
+    enc = encoder(CodingScheme.reed_solomon(8, 2))
+    slots = L.ptr_array([data[s, j].data_ptr() for s in range(32) for j in range(8)])
+    outs = L.ptr_array([h_par[s, i].data_ptr() for s in range(32) for i in range(2)])
+    main = torch.cuda.Stream(device=dev)
+    side, side_copy = torch.cuda.Stream(device=dev), torch.cuda.Stream(device=dev)
+    sink = torch.empty(2, device=dev)
+
+    def step():
+        torch.amax(w, dim=0, out=sink[0])
+        torch.amax(kvc, dim=0, out=sink[1])
+
+    def ckpt():
+        check(L.lib().gs_encode_offload(pipe.handle, enc.handle, 32, slots, outs, rng, side.cuda_stream,
+                                        side_copy.cuda_stream), "overhead ckpt")
+
+    def run(blocks, with_ckpt):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        with torch.cuda.stream(main):
+            e0.record(main)
+            for _ in range(blocks):
+                if with_ckpt:
+                    side.wait_stream(main)
+                    ckpt()
+                for _ in range(16):
+                    step()
+            main.wait_stream(side_copy)
+            e1.record(main)
+        e1.synchronize()
+        return e0.elapsed_time(e1)
+
+    run(1, True)
+    run(1, False)
+    blocks = 4
+    base = min(run(blocks, False) for _ in range(3))
+    withc = min(run(blocks, True) for _ in range(3))
+    a0, a1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a0.record(side)
+    ckpt()
+    side.wait_stream(side_copy)
+    a1.record(side)
+    a1.synchronize()
+    out = {"model": "Llama-3-70B KV, TP=8, batch 32, one GPU's share", "context_tokens": ctx,
+           "decode_step_ms": round(base / (blocks * 16), 4),
+           "block_ms_without_ckpt": round(base / blocks, 4), "block_ms_with_ckpt": round(withc / blocks, 4),
+           "checkpoint_alone_ms": round(a0.elapsed_time(a1), 4),
+           "overhead_pct_of_block": round((withc - base) / base * 100, 3),
+           "overhead_pct_of_decode_step": round((withc - base) / blocks / (base / (blocks * 16)) * 100, 3)}
+    del w, kvc, data, h_par
+    torch.cuda.empty_cache()
+    return out
 
 
 def c3_recovery(torch, dev, comp, copy, pipe):
@@ -563,6 +694,9 @@ def main():
     ap.add_argument("--cpu-sample-s", type=float, default=3.0)
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-c3", action="store_true")
+    ap.add_argument("--no-c4", action="store_true")
+    ap.add_argument("--no-overhead", action="store_true")
+    ap.add_argument("--decode-ctx", type=int, default=4096)
     ap.add_argument("--traffic", type=float, default=None,
                     help="ncu dram bytes per K1 launch (from profiles/), echoed into roofline.traffic")
     args = ap.parse_args()
