@@ -109,6 +109,28 @@ int gs_codec_coefficients(const gs_codec* c, uint8_t* coef);
 int gs_apply_device(const gs_codec* c, int n_stripes, const void* const* slots,
                     void* const* outs, size_t len, void* stream);
 
+/* ---- paged KV cache ------------------------------------------
+ * A slice in the reference byte order [K,V][layer][token][H*D/tp]
+ * (kv_layout.hpp:59-68) read straight out of a paged KV cache: page (t, l) of
+ * the chunk's block lives at  base + l*layer_stride + t*kv_stride  (the
+ * per-stripe base pointer already includes the block's offset); each page is
+ * page_bytes = block tokens * token_bytes. Tokens >= valid_tokens of a page
+ * read as zero (pad_partial, kv_layout.hpp:73-84) and are never written.
+ * Sizes and strides are multiples of 16. */
+typedef struct {
+  uint32_t page_bytes;
+  uint32_t layers;
+  uint32_t token_bytes;
+  uint32_t valid_tokens;
+  uint64_t layer_stride;
+  uint64_t kv_stride;
+} gs_page_map;
+/* gs_apply_device with slots whose bit is set in paged_slot_mask read through
+ * src_map and (dst_map != NULL) outputs scattered through dst_map. */
+int gs_apply_device_paged(const gs_codec* c, int n_stripes, const void* const* slots, void* const* outs,
+                          size_t len, const gs_page_map* src_map, uint32_t paged_slot_mask,
+                          const gs_page_map* dst_map, void* stream);
+
 /* ---- host-link pipelines ----------------------------------------------------
  * A pipeline owns device staging (`staging_bytes`, split into a ring) and
  * events on `device`. Not thread-safe; one per (device, caller thread). */
@@ -134,6 +156,11 @@ int gs_encode_offload(gs_pipeline* p, const gs_codec* enc, int n_stripes,
                       const void* const* d_data, void* const* h_parity, size_t len,
                       void* compute, void* copy);
 
+/* Same, data slices gathered from a paged KV cache (no staging copy). */
+int gs_encode_offload_paged(gs_pipeline* p, const gs_codec* enc, int n_stripes, const void* const* d_data,
+                            void* const* h_parity, size_t len, const gs_page_map* src_map, void* compute,
+                            void* copy);
+
 /* Recovery upload (recovery.hpp:100-133 byte path): parity slots of `slots`
  * are HOST pointers (pinned), data slots DEVICE pointers (local or peer).
  * Used parity rows are H2D'd piecewise on `copy` into staging; the rebuild
@@ -142,6 +169,13 @@ int gs_encode_offload(gs_pipeline* p, const gs_codec* enc, int n_stripes,
 int gs_reconstruct_upload(gs_pipeline* p, const gs_codec* dec, int n_stripes,
                           const void* const* slots, void* const* outs, size_t len,
                           void* compute, void* copy);
+
+/* Same with the surviving data slots read from paged caches (src_map) and
+ * the rebuilt slices scattered into the replacement's paged cache (dst_map);
+ * either map may be NULL (contiguous). */
+int gs_reconstruct_upload_paged(gs_pipeline* p, const gs_codec* dec, int n_stripes, const void* const* slots,
+                                void* const* outs, size_t len, const gs_page_map* src_map,
+                                const gs_page_map* dst_map, void* compute, void* copy);
 
 /* Drop-in host-buffer calls (synchronous): the byte semantics of
  * ghostserve::encode (coding.hpp:313) and ghostserve::reconstruct (:458) with

@@ -43,6 +43,9 @@ SIGNATURES = {
     "gs_codec_info": (_i, [_vp, _ip, _ip, _ip, _ip]),
     "gs_codec_coefficients": (_i, [_vp, _u8p]),
     "gs_apply_device": (_i, [_vp, _i, _vpp, _vpp, _sz, _vp]),
+    "gs_apply_device_paged": (_i, [_vp, _i, _vpp, _vpp, _sz, _vp, _u32, _vp, _vp]),
+    "gs_encode_offload_paged": (_i, [_vp, _vp, _i, _vpp, _vpp, _sz, _vp, _vp, _vp]),
+    "gs_reconstruct_upload_paged": (_i, [_vp, _vp, _i, _vpp, _vpp, _sz, _vp, _vp, _vp, _vp]),
     "gs_pipeline_create": (_i, [_i, _sz, _vpp]),
     "gs_pipeline_destroy": (_i, [_vp]),
     "gs_prewarm": (_i, [_i]),
@@ -109,6 +112,13 @@ def lib() -> C.CDLL:
                 fn.argtypes = args
             _lib = handle
     return _lib
+
+
+class PageMap(C.Structure):
+    """gs_page_map (include/gs_capi.h)."""
+
+    _fields_ = [("page_bytes", C.c_uint32), ("layers", C.c_uint32), ("token_bytes", C.c_uint32),
+                ("valid_tokens", C.c_uint32), ("layer_stride", C.c_uint64), ("kv_stride", C.c_uint64)]
 
 
 def last_error() -> str:

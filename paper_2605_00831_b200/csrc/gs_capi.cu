@@ -8,6 +8,7 @@
 #include <atomic>
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <map>
 #include <mutex>
@@ -126,6 +127,11 @@ int blocks_per_sm(int dev, const void* kernel, size_t smem, int threads = kThrea
 // B200, tools/kernel_sweep.py: the bulk pipeline wins for encoders once a
 // launch moves >= 512 MB; the register kernel everywhere else).
 std::atomic<int> g_variant{2};
+// Tuning override for the register kernel's resident CTAs per SM (0 = max).
+int g_ctas_per_sm = [] {
+  const char* e = std::getenv("GS_CTAS_PER_SM");
+  return e ? std::atoi(e) : 0;
+}();
 constexpr uint64_t kBulkAutoBytes = 512ull << 20;
 
 int bulk_stages(const SpecialEntry* e) {
@@ -288,13 +294,55 @@ const void* generic_kernel(int kb) {
 
 // Launch the codec over stripes. slot_ptr(s, j) / out_ptr(s, i) give the
 // (already offset) pointers; every stripe has `len` bytes.
+// Paging (optional): slots whose bit is set in pg.paged_slots are paged-cache
+// bases mapped with pg.src (NOT pre-offset: the kernel maps logical0 + off);
+// outputs are mapped with pg.dst when pg.dst.page_bytes != 0.
+struct Paging {
+  uint32_t paged_slots = 0;
+  uint64_t logical0 = 0;
+  PageMap src{};
+  PageMap dst{};
+  bool any() const { return paged_slots != 0 || dst.page_bytes != 0; }
+};
+
+PageMap to_map(const gs_page_map* m) {
+  PageMap r{};
+  if (m) {
+    r.page_bytes = m->page_bytes;
+    r.layers = m->layers;
+    r.token_bytes = m->token_bytes;
+    r.valid_tokens = m->valid_tokens;
+    r.layer_stride = m->layer_stride;
+    r.kv_stride = m->kv_stride;
+  }
+  return r;
+}
+
+int check_page_map(const PageMap& m, const char* what) {
+  if (m.page_bytes == 0) return GS_OK;
+  if (m.page_bytes % kVec || m.token_bytes == 0 || m.token_bytes % kVec || m.layers == 0 ||
+      m.layer_stride % kVec || m.kv_stride % kVec || m.page_bytes % m.token_bytes)
+    return fail(GS_INVALID_ARGUMENT, "%s page map: page/token bytes and strides must be multiples of 16", what);
+  if (static_cast<uint64_t>(m.valid_tokens) * m.token_bytes > m.page_bytes)
+    return fail(GS_INVALID_ARGUMENT, "kv: valid_tokens exceeds chunk size");
+  return GS_OK;
+}
+
 template <class SlotFn, class OutFn>
 int run_codec(const gs_codec* c, int n_stripes, SlotFn slot_ptr, OutFn out_ptr, uint64_t len,
-              cudaStream_t st) {
+              cudaStream_t st, const Paging& pg = Paging{}) {
   if (len == 0 || n_stripes == 0 || c->n_out == 0) return GS_OK;
   int dev = 0;
   if (int s = current_device(&dev)) return s;
   const int sms = device_sms(dev);
+  if (pg.any()) {
+    if (c->n_slots > 32) return fail(GS_INVALID_ARGUMENT, "paged apply: at most 32 shard slots");
+    if (len % kVec) return fail(GS_INVALID_ARGUMENT, "paged apply: slice length must be a multiple of 16");
+    if (pg.paged_slots && pg.src.page_bytes == 0)
+      return fail(GS_INVALID_ARGUMENT, "paged apply: paged slots need a source page map");
+    if (int s = check_page_map(pg.src, "source")) return s;
+    if (int s = check_page_map(pg.dst, "output")) return s;
+  }
 
   bool aligned = true;
   for (int s = 0; s < n_stripes; ++s) {
@@ -318,14 +366,15 @@ int run_codec(const gs_codec* c, int n_stripes, SlotFn slot_ptr, OutFn out_ptr, 
 
   // Specialised kernel over the 16-byte-aligned body.
   uint64_t done = 0;
+  if (pg.any() && !aligned) return fail(GS_INVALID_ARGUMENT, "paged apply: pointers must be 16-B aligned");
   if (c->special && aligned && len >= kVec) {
     const uint64_t body = len / kVec * kVec;
     const int stages = bulk_stages(c->special);
     const int variant = g_variant.load(std::memory_order_relaxed);
     const uint64_t launch_bytes = body * static_cast<uint64_t>(n_stripes) *
                                   static_cast<uint64_t>(c->special->used_cols + c->n_out);
-    const bool use_bulk = stages >= 2 && (variant == 1 || (variant == 2 && !c->decoder &&
-                                                           launch_bytes >= kBulkAutoBytes));
+    const bool use_bulk = !pg.any() && stages >= 2 &&
+                          (variant == 1 || (variant == 2 && !c->decoder && launch_bytes >= kBulkAutoBytes));
     const uint64_t tile = static_cast<uint64_t>(use_bulk ? c->special->tile_bulk : c->special->tile);
     const uint64_t tps64 = (body + tile - 1) / tile;
     const int stride = c->n_slots + c->n_out;
@@ -333,8 +382,9 @@ int run_codec(const gs_codec* c, int n_stripes, SlotFn slot_ptr, OutFn out_ptr, 
     const size_t smem = use_bulk ? kBulkSmemHeader + static_cast<size_t>(stages) * c->special->used_cols *
                                                          c->special->tile_bulk
                                  : 0;
-    const int occ = use_bulk ? blocks_per_sm(dev, c->special->kernel_bulk, smem, kBulkThreads)
-                             : blocks_per_sm(dev, c->special->kernel, 0);
+    int occ = use_bulk ? blocks_per_sm(dev, c->special->kernel_bulk, smem, kBulkThreads)
+                       : blocks_per_sm(dev, c->special->kernel, 0);
+    if (!use_bulk && g_ctas_per_sm > 0) occ = std::min(occ, g_ctas_per_sm);
     for (int s0 = 0; s0 < n_stripes; s0 += per) {
       const int cnt = std::min(per, n_stripes - s0);
       ptrs.assign(static_cast<size_t>(cnt) * stride, nullptr);
@@ -344,7 +394,8 @@ int run_codec(const gs_codec* c, int n_stripes, SlotFn slot_ptr, OutFn out_ptr, 
       }
       const uint64_t total = tps64 * cnt;
       if (total > 0xFFFFFFFFull) return fail(GS_INVALID_ARGUMENT, "apply: too many tiles in one launch");
-      TileGeom g{body, static_cast<uint32_t>(tps64), static_cast<uint32_t>(total), stride, c->n_slots, 1};
+      TileGeom g{body, static_cast<uint32_t>(tps64), static_cast<uint32_t>(total), stride, c->n_slots, 1,
+                 pg.paged_slots, pg.logical0, pg.src, pg.dst};
       const int grid = static_cast<int>(std::min<uint64_t>(total, static_cast<uint64_t>(occ) * sms));
       cudaError_t e = use_bulk ? c->special->launch_bulk(ptrs.data(), cnt * stride, g, grid, st, stages, smem)
                                : c->special->launch(ptrs.data(), cnt * stride, g, grid, st);
@@ -363,21 +414,26 @@ int run_codec(const gs_codec* c, int n_stripes, SlotFn slot_ptr, OutFn out_ptr, 
   const int stride = ns + c->n_out;
   const int per = kPtrCap / stride;
   if (per < 1) return fail(GS_INVALID_ARGUMENT, "apply: stripe needs %d pointers (> %d)", stride, kPtrCap);
+  uint32_t gpaged = 0;  // paged bits in compacted (used-slot) order
+  for (int u = 0; u < ns; ++u)
+    if ((pg.paged_slots >> c->used[u]) & 1u) gpaged |= 1u << u;
   for (int s0 = 0; s0 < n_stripes; s0 += per) {
     const int cnt = std::min(per, n_stripes - s0);
     ptrs.assign(static_cast<size_t>(cnt) * stride, nullptr);
     for (int s = 0; s < cnt; ++s) {
       for (int u = 0; u < ns; ++u)
-        ptrs[s * stride + u] = static_cast<const uint8_t*>(slot_ptr(s0 + s, c->used[u])) + done;
+        ptrs[s * stride + u] = static_cast<const uint8_t*>(slot_ptr(s0 + s, c->used[u])) +
+                               (((gpaged >> u) & 1u) ? 0 : done);
       for (int i = 0; i < c->n_out; ++i)
-        ptrs[s * stride + ns + i] = static_cast<const uint8_t*>(out_ptr(s0 + s, i)) + done;
+        ptrs[s * stride + ns + i] = static_cast<const uint8_t*>(out_ptr(s0 + s, i)) +
+                                    (pg.dst.page_bytes ? 0 : done);
     }
     const uint64_t total = tps64 * cnt;
     if (total > 0xFFFFFFFFull) return fail(GS_INVALID_ARGUMENT, "apply: too many tiles in one launch");
     for (int r0 = 0; r0 < c->n_out; r0 += kMaxGenericRows) {
       const int kb = std::min(kMaxGenericRows, c->n_out - r0);
       TileGeom g{glen, static_cast<uint32_t>(tps64), static_cast<uint32_t>(total), stride, ns + r0,
-                 galigned ? 1 : 0};
+                 galigned ? 1 : 0, gpaged, pg.logical0 + done, pg.src, pg.dst};
       const size_t smem = static_cast<size_t>(kb) * ns * sizeof(CoefWords);
       const int occ = blocks_per_sm(dev, generic_kernel(kb), smem);
       const int grid = static_cast<int>(std::min<uint64_t>(total, static_cast<uint64_t>(occ) * sms));
@@ -694,6 +750,22 @@ int gs_apply_device(const gs_codec* c, int n_stripes, const void* const* slots, 
   return run_codec(c, n_stripes, slot, out, len, static_cast<cudaStream_t>(stream));
 }
 
+int gs_apply_device_paged(const gs_codec* c, int n_stripes, const void* const* slots, void* const* outs,
+                          size_t len, const gs_page_map* src_map, uint32_t paged_slot_mask,
+                          const gs_page_map* dst_map, void* stream) {
+  if (!c) return fail(GS_INVALID_ARGUMENT, "apply: NULL codec");
+  if (n_stripes < 0) return fail(GS_INVALID_ARGUMENT, "apply: negative stripe count");
+  if (len == 0 || n_stripes == 0 || c->n_out == 0) return GS_OK;
+  if (!slots || !outs) return fail(GS_INVALID_ARGUMENT, "apply: NULL pointer array");
+  Paging pg;
+  pg.src = to_map(src_map);
+  pg.dst = to_map(dst_map);
+  pg.paged_slots = src_map ? paged_slot_mask : 0;
+  auto slot = [&](int s, int j) -> const void* { return slots[static_cast<size_t>(s) * c->n_slots + j]; };
+  auto out = [&](int s, int i) -> const void* { return outs[static_cast<size_t>(s) * c->n_out + i]; };
+  return run_codec(c, n_stripes, slot, out, len, static_cast<cudaStream_t>(stream), pg);
+}
+
 // ============================================================================
 // pipelines
 // ============================================================================
@@ -777,9 +849,23 @@ int gs_pipeline_destroy(gs_pipeline* p) {
   return GS_OK;
 }
 
+static int encode_offload(gs_pipeline* p, const gs_codec* c, int n_stripes, const void* const* d_data,
+                          void* const* h_parity, size_t len, void* compute, void* copy, const gs_page_map* src_map);
+
 // Encode device data, stage parity, D2H it piecewise (checkpoint offload).
 int gs_encode_offload(gs_pipeline* p, const gs_codec* c, int n_stripes, const void* const* d_data,
                       void* const* h_parity, size_t len, void* compute, void* copy) {
+  return encode_offload(p, c, n_stripes, d_data, h_parity, len, compute, copy, nullptr);
+}
+
+int gs_encode_offload_paged(gs_pipeline* p, const gs_codec* c, int n_stripes, const void* const* d_data,
+                            void* const* h_parity, size_t len, const gs_page_map* src_map, void* compute,
+                            void* copy) {
+  return encode_offload(p, c, n_stripes, d_data, h_parity, len, compute, copy, src_map);
+}
+
+static int encode_offload(gs_pipeline* p, const gs_codec* c, int n_stripes, const void* const* d_data,
+                          void* const* h_parity, size_t len, void* compute, void* copy, const gs_page_map* src_map) {
   if (!p || !c) return fail(GS_INVALID_ARGUMENT, "encode_offload: NULL pipeline/codec");
   if (c->decoder) return fail(GS_INVALID_ARGUMENT, "encode_offload: codec is a decoder");
   if (len == 0 || n_stripes == 0) return GS_OK;
@@ -801,10 +887,16 @@ int gs_encode_offload(gs_pipeline* p, const gs_codec* c, int n_stripes, const vo
       uint8_t* base = p->staging + static_cast<size_t>(sl) * slot;
       GS_CUDA(cudaStreamWaitEvent(cs, p->drained[sl], 0));  // slot's previous D2H finished
       auto src = [&](int s, int j) -> const void* {
-        return static_cast<const uint8_t*>(d_data[static_cast<size_t>(s0 + s) * N + j]) + r0;
+        return static_cast<const uint8_t*>(d_data[static_cast<size_t>(s0 + s) * N + j]) + (src_map ? 0 : r0);
       };
       auto dst = [&](int s, int i) -> const void* { return base + (static_cast<size_t>(s) * K + i) * rl; };
-      if (int st = run_codec(c, cnt, src, dst, rl, cs)) return st;
+      Paging pg;
+      if (src_map) {
+        pg.src = to_map(src_map);
+        pg.paged_slots = N >= 32 ? ~0u : (1u << N) - 1;
+        pg.logical0 = r0;
+      }
+      if (int st = run_codec(c, cnt, src, dst, rl, cs, pg)) return st;
       GS_CUDA(cudaEventRecord(p->done[sl], cs));
       GS_CUDA(cudaStreamWaitEvent(ks, p->done[sl], 0));
       for (int s = 0; s < cnt; ++s)
@@ -818,9 +910,25 @@ int gs_encode_offload(gs_pipeline* p, const gs_codec* c, int n_stripes, const vo
   return GS_OK;
 }
 
+static int reconstruct_upload(gs_pipeline* p, const gs_codec* c, int n_stripes, const void* const* slots,
+                              void* const* outs, size_t len, void* compute, void* copy, const gs_page_map* src_map,
+                              const gs_page_map* dst_map);
+
 // Rebuild lost shards: H2D used parity rows piecewise, rebuild per piece.
 int gs_reconstruct_upload(gs_pipeline* p, const gs_codec* c, int n_stripes, const void* const* slots,
                           void* const* outs, size_t len, void* compute, void* copy) {
+  return reconstruct_upload(p, c, n_stripes, slots, outs, len, compute, copy, nullptr, nullptr);
+}
+
+int gs_reconstruct_upload_paged(gs_pipeline* p, const gs_codec* c, int n_stripes, const void* const* slots,
+                                void* const* outs, size_t len, const gs_page_map* src_map,
+                                const gs_page_map* dst_map, void* compute, void* copy) {
+  return reconstruct_upload(p, c, n_stripes, slots, outs, len, compute, copy, src_map, dst_map);
+}
+
+static int reconstruct_upload(gs_pipeline* p, const gs_codec* c, int n_stripes, const void* const* slots,
+                              void* const* outs, size_t len, void* compute, void* copy, const gs_page_map* src_map,
+                              const gs_page_map* dst_map) {
   if (!p || !c) return fail(GS_INVALID_ARGUMENT, "reconstruct_upload: NULL pipeline/codec");
   if (!c->decoder) return fail(GS_INVALID_ARGUMENT, "reconstruct_upload: codec is an encoder");
   if (len == 0 || n_stripes == 0 || c->n_out == 0) return GS_OK;
@@ -862,12 +970,19 @@ int gs_reconstruct_upload(gs_pipeline* p, const gs_codec* c, int n_stripes, cons
           return base + (static_cast<size_t>(s) * H + (it - host_slots.begin())) * rl;
         }
         const void* d = slots[static_cast<size_t>(s0 + s) * NS + j];
-        return d ? static_cast<const uint8_t*>(d) + r0 : nullptr;
+        return d ? static_cast<const uint8_t*>(d) + (src_map ? 0 : r0) : nullptr;
       };
       auto dst = [&](int s, int i) -> const void* {
-        return static_cast<const uint8_t*>(outs[static_cast<size_t>(s0 + s) * NO + i]) + r0;
+        return static_cast<const uint8_t*>(outs[static_cast<size_t>(s0 + s) * NO + i]) + (dst_map ? 0 : r0);
       };
-      if (int st = run_codec(c, cnt, src, dst, rl, cs)) return st;
+      Paging pg;
+      pg.logical0 = r0;
+      if (src_map) {
+        pg.src = to_map(src_map);
+        pg.paged_slots = n >= 32 ? ~0u : (1u << n) - 1;  // data slots; parity comes from staging
+      }
+      if (dst_map) pg.dst = to_map(dst_map);
+      if (int st = run_codec(c, cnt, src, dst, rl, cs, pg)) return st;
       GS_CUDA(cudaEventRecord(p->done[sl], cs));
     }
   }

@@ -102,14 +102,46 @@ __device__ __forceinline__ void st_partial(uint8_t* p, const uint4& v, int nbyte
 // Work = n_stripes x ceil(len / 4 KiB) tiles, walked grid-stride so that
 // consecutive CTAs stream consecutive 4 KiB pieces of the same shards.
 
+// Paged KV addressing. A slice in the reference byte order
+// [K,V][layer][token][elems] (kv_layout.hpp:59-68) lives in a paged KV cache
+// as 2*layers pages of page_bytes (= block_size tokens x token_bytes): page
+// (t, l) of a block sits at  base + l*layer_stride + t*kv_stride, where the
+// per-stripe base already includes the block's offset. Tokens >= valid_tokens
+// of each page read as zero (pad_partial, kv_layout.hpp:73-84) and are not
+// written back. page_bytes == 0 means contiguous slices.
+struct PageMap {
+  uint32_t page_bytes;
+  uint32_t layers;
+  uint32_t token_bytes;
+  uint32_t valid_tokens;
+  uint64_t layer_stride;
+  uint64_t kv_stride;
+};
+
 struct TileGeom {
-  uint64_t len;        // bytes per shard
+  uint64_t len;        // bytes per shard (this launch's range)
   uint32_t tps;        // tiles per stripe
   uint32_t total;      // tiles overall
   int stride;          // pointers per stripe in the table
   int out0;            // first output pointer within a stripe's entries
   int aligned;         // all pointers 16-B aligned -> vector path allowed
+  uint32_t paged_slots;  // bit j: source pointer j is a paged base (mapped with src)
+  uint64_t logical0;     // slice offset of this launch's byte 0 (for the page mapping)
+  PageMap src;           // mapping of paged source slots
+  PageMap dst;           // mapping of the outputs (dst.page_bytes == 0: contiguous)
 };
+
+// Offset of logical slice byte `o` inside a paged slot; `masked` = beyond
+// the valid tokens of its page.
+__device__ __forceinline__ uint64_t paged_offset(const PageMap& m, uint64_t logical, bool& masked) {
+  const uint32_t o = static_cast<uint32_t>(logical);
+  const uint32_t q = o / m.page_bytes;
+  const uint32_t in = o - q * m.page_bytes;
+  const uint32_t t = q / m.layers;
+  const uint32_t l = q - t * m.layers;
+  masked = in >= m.valid_tokens * m.token_bytes;
+  return static_cast<uint64_t>(l) * m.layer_stride + static_cast<uint64_t>(t) * m.kv_stride + in;
+}
 
 // ---- specialised back end --------------------------------------------------
 
@@ -160,41 +192,30 @@ __device__ constexpr bool column_used(int j) {
 // this kernel carries no byte-granular code at all.
 template <class Spec, int CAP, int U>
 __global__ void __launch_bounds__(kThreads) k_apply_special(const PtrTable<CAP> tab, const TileGeom g) {
-  constexpr uint64_t kSpan = static_cast<uint64_t>(kThreads) * kVec;
+  static_assert(U == 1, "one 16-byte group per thread per tile");
   for (uint32_t t = blockIdx.x; t < g.total; t += gridDim.x) {
     const uint32_t s = t / g.tps;
-    const uint64_t off0 = static_cast<uint64_t>(t - s * g.tps) * (kSpan * U) + threadIdx.x * kVec;
+    const uint64_t off = static_cast<uint64_t>(t - s * g.tps) * kTile + threadIdx.x * kVec;
+    if (off >= g.len) continue;
     const int base = static_cast<int>(s) * g.stride;
-    if (off0 + (U - 1) * kSpan < g.len) {  // whole tile row in range: no per-group guards
-      uint4 src[U][Spec::NS];
+    bool smask = false, dmask = false;
+    uint64_t soff = off, doff = off;
+    if (g.paged_slots) soff = paged_offset(g.src, g.logical0 + off, smask);
+    if (g.dst.page_bytes) doff = paged_offset(g.dst, g.logical0 + off, dmask);
+    uint4 src[Spec::NS];
 #pragma unroll
-      for (int j = 0; j < Spec::NS; ++j)
-#pragma unroll
-        for (int u = 0; u < U; ++u)
-          src[u][j] = column_used<Spec>(j) ? ld_stream(tab.p[base + j] + off0 + u * kSpan)
-                                           : make_uint4(0, 0, 0, 0);
-#pragma unroll
-      for (int u = 0; u < U; ++u) {
-        uint4 out[Spec::NO];
-        horner_apply<Spec>(src[u], out);
-#pragma unroll
-        for (int i = 0; i < Spec::NO; ++i)
-          st_stream(const_cast<uint8_t*>(tab.p[base + g.out0 + i]) + off0 + u * kSpan, out[i]);
+    for (int j = 0; j < Spec::NS; ++j) {
+      src[j] = make_uint4(0, 0, 0, 0);
+      if (column_used<Spec>(j)) {
+        const bool paged = (g.paged_slots >> j) & 1u;
+        if (!(paged && smask)) src[j] = ld_stream(tab.p[base + j] + (paged ? soff : off));
       }
-    } else {
-#pragma unroll 1
-      for (int u = 0; u < U; ++u) {
-        const uint64_t off = off0 + u * kSpan;
-        if (off >= g.len) break;
-        uint4 src[Spec::NS];
+    }
+    uint4 out[Spec::NO];
+    horner_apply<Spec>(src, out);
+    if (!dmask) {
 #pragma unroll
-        for (int j = 0; j < Spec::NS; ++j)
-          src[j] = column_used<Spec>(j) ? ld_stream(tab.p[base + j] + off) : make_uint4(0, 0, 0, 0);
-        uint4 out[Spec::NO];
-        horner_apply<Spec>(src, out);
-#pragma unroll
-        for (int i = 0; i < Spec::NO; ++i) st_stream(const_cast<uint8_t*>(tab.p[base + g.out0 + i]) + off, out[i]);
-      }
+      for (int i = 0; i < Spec::NO; ++i) st_stream(const_cast<uint8_t*>(tab.p[base + g.out0 + i]) + doff, out[i]);
     }
   }
 }
@@ -266,7 +287,11 @@ __device__ __forceinline__ void pair_finish(uint32_t accP, uint32_t accQ, uint32
 // loads/stores; otherwise byte-granular (ragged tail / misaligned shards).
 template <int KB, int CAP, bool FULL>
 __device__ __forceinline__ void generic_group(const PtrTable<CAP>& tab, int base, int out0, uint64_t off,
-                                              int nb, const CoefWords* sc, int ns) {
+                                              int nb, const CoefWords* sc, int ns, const TileGeom& g) {
+  bool smask = false, dmask = false;
+  uint64_t soff = off, doff = off;
+  if (FULL && g.paged_slots) soff = paged_offset(g.src, g.logical0 + off, smask);
+  if (FULL && g.dst.page_bytes) doff = paged_offset(g.dst, g.logical0 + off, dmask);
   uint32_t acc[KB][4];
 #pragma unroll
   for (int r = 0; r < KB; ++r)
@@ -277,8 +302,9 @@ __device__ __forceinline__ void generic_group(const PtrTable<CAP>& tab, int base
     uint4 d[4];
 #pragma unroll
     for (int u = 0; u < 4; ++u) {
-      const uint8_t* p = tab.p[base + j + u] + off;
-      d[u] = FULL ? ld_stream(p) : ld_partial(p, nb);
+      const bool paged = FULL && ((g.paged_slots >> (j + u)) & 1u);
+      const uint8_t* p = tab.p[base + j + u] + (paged ? soff : off);
+      d[u] = (paged && smask) ? make_uint4(0, 0, 0, 0) : (FULL ? ld_stream(p) : ld_partial(p, nb));
     }
 #pragma unroll
     for (int u = 0; u < 4; ++u) {
@@ -293,8 +319,9 @@ __device__ __forceinline__ void generic_group(const PtrTable<CAP>& tab, int base
     }
   }
   for (; j < ns; ++j) {
-    const uint8_t* p = tab.p[base + j] + off;
-    const uint4 d = FULL ? ld_stream(p) : ld_partial(p, nb);
+    const bool paged = FULL && ((g.paged_slots >> j) & 1u);
+    const uint8_t* p = tab.p[base + j] + (paged ? soff : off);
+    const uint4 d = (paged && smask) ? make_uint4(0, 0, 0, 0) : (FULL ? ld_stream(p) : ld_partial(p, nb));
     const PairSel s0 = pair_setup(d.x, d.y);
     const PairSel s1 = pair_setup(d.z, d.w);
 #pragma unroll
@@ -309,11 +336,12 @@ __device__ __forceinline__ void generic_group(const PtrTable<CAP>& tab, int base
     uint4 o;
     pair_finish(acc[r][0], acc[r][1], o.x, o.y);
     pair_finish(acc[r][2], acc[r][3], o.z, o.w);
-    uint8_t* p = const_cast<uint8_t*>(tab.p[base + out0 + r]) + off;
-    if (FULL)
-      st_stream(p, o);
-    else
+    uint8_t* p = const_cast<uint8_t*>(tab.p[base + out0 + r]) + doff;
+    if (FULL) {
+      if (!dmask) st_stream(p, o);
+    } else {
       st_partial(p, o, nb);
+    }
   }
 }
 
@@ -334,10 +362,10 @@ __global__ void __launch_bounds__(kThreads) k_apply_generic(const PtrTable<CAP> 
     if (off >= g.len) continue;
     const int base = static_cast<int>(s) * g.stride;
     if (g.aligned && off + kVec <= g.len) {
-      generic_group<KB, CAP, true>(tab, base, g.out0, off, kVec, sc, ns);
+      generic_group<KB, CAP, true>(tab, base, g.out0, off, kVec, sc, ns, g);
     } else {
       const uint64_t rem = g.len - off;
-      generic_group<KB, CAP, false>(tab, base, g.out0, off, static_cast<int>(rem < kVec ? rem : kVec), sc, ns);
+      generic_group<KB, CAP, false>(tab, base, g.out0, off, static_cast<int>(rem < kVec ? rem : kVec), sc, ns, g);
     }
   }
 }

@@ -23,8 +23,9 @@ using KernelAddr = const void*;
 using BulkLaunchFn = cudaError_t (*)(const void* const* ptrs, int count, const TileGeom& g, int grid,
                                      cudaStream_t st, int stages, size_t smem);
 
-// Pointer-table capacity of one launch (kernel parameter space: 4 KiB).
-constexpr int kPtrCap = 508;
+// Pointer-table capacity of one launch (pointers + TileGeom fit the classic
+// 4 KiB kernel-parameter space).
+constexpr int kPtrCap = 496;
 // 16-byte groups per thread per source per tile of the specialised kernels.
 constexpr int kSpecialU = 1;
 // Consumer warps and 16-byte groups per consumer thread of the bulk variant.

@@ -1,0 +1,97 @@
+"""K1/K2 on a paged KV cache: pages read / written in place,
+partial blocks masked exactly like pad_partial; bytes checked against the
+oracle on the gathered reference-layout slices."""
+import numpy as np
+import pytest
+
+from oracle import oracle as O
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+from paper_2605_00831_b200 import device as D  # noqa: E402
+from paper_2605_00831_b200.coding import CodingScheme, ErasurePattern, InvalidArgument  # noqa: E402
+from paper_2605_00831_b200.kv_layout import ModelConfig, make_ground_truth_slice  # noqa: E402
+from paper_2605_00831_b200.paged import (PagedKVCache, checkpoint_blocks, encode_blocks,  # noqa: E402
+                                         rebuild_blocks)
+
+
+def build(model, n, S, block, valid, nblocks=64, seed=0):
+    g = torch.Generator(device="cuda").manual_seed(seed)
+    caches = []
+    for j in range(n):
+        c = PagedKVCache(model, nblocks, block)
+        c.buf.copy_(torch.randint(0, 256, c.buf.shape, dtype=torch.uint8, device="cuda", generator=g))
+        caches.append(c)  # garbage everywhere, incl. past `valid`
+    rng = np.random.default_rng(seed)
+    tables = [[int(b) for b in rng.permutation(nblocks)[:n]] for _ in range(S)]
+    truth = []
+    for s in range(S):
+        row = []
+        for j in range(n):
+            sl = make_ground_truth_slice(3, s, 9, j, model, block, valid, device="cuda")
+            caches[j].write_slice(tables[s][j], sl, valid)
+            row.append(sl)
+        truth.append(row)
+    return caches, tables, truth
+
+
+@pytest.mark.parametrize("valid", [16, 5, 0])
+def test_paged_encode_equals_oracle_on_reference_slices(valid):
+    model = ModelConfig(32, 8, 128, 2, 8)              # Llama-3-8B TP8: 4 KiB pages at block 16
+    n, k, S = 8, 2, 6
+    caches, tables, truth = build(model, n, S, 16, valid)
+    scheme = CodingScheme.reed_solomon(n, k)
+    par = torch.empty((S, k, caches[0].slice_bytes), dtype=torch.uint8, device="cuda")
+    encode_blocks(scheme, caches, tables, valid, par)
+    hp = par.cpu().numpy()
+    for s in range(S):
+        host = [t.cpu().numpy() for t in truth[s]]
+        for j in range(n):
+            assert np.array_equal(caches[j].read_slice(tables[s][j], valid).cpu().numpy(), host[j])
+        want = O.port().encode(O.RS, n, k, host)
+        for i in range(k):
+            assert np.array_equal(hp[s, i], want[i]), (valid, s, i)
+
+
+def test_paged_checkpoint_and_rebuild_into_replacement_cache():
+    model = ModelConfig(2, 6, 64, 2, 6)                # 6-divisible geometry, RS(6,2)
+    n, k, S, valid = 6, 2, 5, 11
+    caches, tables, truth = build(model, n, S, 16, valid, nblocks=40, seed=3)
+    scheme = CodingScheme.reed_solomon(n, k)
+    pipe = D.Pipeline(0, 64 << 10)                     # tiny ring: many pieces across page boundaries
+    h_par = torch.zeros((S, k, caches[0].slice_bytes), dtype=torch.uint8).pin_memory()
+    comp, copy = torch.cuda.Stream(), torch.cuda.Stream()
+    comp.wait_stream(torch.cuda.current_stream())
+    checkpoint_blocks(pipe, scheme, caches, tables, valid, h_par, comp, copy)
+    copy.synchronize()
+    for s in range(S):
+        want = O.port().encode(O.RS, n, k, [t.cpu().numpy() for t in truth[s]])
+        for i in range(k):
+            assert np.array_equal(h_par[s, i].numpy(), want[i])
+    for lost in ([2], [0, 4], [5, 7]):
+        pat = ErasurePattern(lost)
+        reps = {}
+        for w in lost:
+            if w < n:
+                reps[w] = PagedKVCache(model, 40, 16, fill=0xEE)
+        rebuild_blocks(pipe, scheme, pat, [None if j in lost else caches[j] for j in range(n)], reps, tables,
+                       valid, h_par, comp, copy)
+        comp.synchronize()
+        for w, rep in reps.items():
+            for s in range(S):
+                assert torch.equal(rep.read_slice(tables[s][w], valid), truth[s][w]), (lost, w, s)
+                # tokens past `valid` of the page are never written
+                assert bool((rep.buf[:, :, tables[s][w], valid:] == 0xEE).all())
+    pipe.close()
+
+
+def test_paged_rejects_bad_geometry():
+    model = ModelConfig(2, 8, 8, 2, 8)                 # 16 B/token: fine
+    c = PagedKVCache(model, 4, 16)
+    with pytest.raises(InvalidArgument):
+        c.page_map(17)
+    bad = ModelConfig(2, 4, 2, 2, 1)                  # 16 B tokens but check odd strides via apply
+    cb = PagedKVCache(bad, 4, 3)                       # 3-token pages of 16 B -> 48 B pages: ok (multiple of 16)
+    par = torch.empty((1, 1, cb.slice_bytes), dtype=torch.uint8, device="cuda")
+    encode_blocks(CodingScheme.xor_code(2), [cb, cb], [[0, 1]], 3, par)
