@@ -378,7 +378,28 @@ def run_ours(args):
                       S * (N_SHARDS + 1) * SLICE,
                       "k_apply_special<DecSpec<RS,8,2,lost{5}>> (K2 rebuild, 7 data + 1 parity -> 1)")
         ok_parity &= torch.equal(rebuilt[RING_BLOCKS - 1], ring[RING_BLOCKS - 1, :, 5])
-        del par_dev, rebuilt
+
+        # the same C2 blocks living in per-worker PAGED KV caches (vLLM-style
+        # [layer][K/V][block][16 tok][256 B]): K1 gathers the 64 pages of every
+        # slice in place instead of reading contiguous slices.
+        from paper_2605_00831_b200.paged import PagedKVCache
+        caches = [PagedKVCache(cfg, RING_BLOCKS * S, BLOCK_TOKENS, device=dev) for _ in range(N_SHARDS)]
+        for b in range(RING_BLOCKS):
+            for s_ in range(S):
+                for j in range(N_SHARDS):
+                    caches[j].write_slice(b * S + s_, ring[b, s_, j])
+        pm = caches[0].page_map(BLOCK_TOKENS)
+        pslots = [L.ptr_array([caches[j].block_base(b * S + s_) for s_ in range(S) for j in range(N_SHARDS)])
+                  for b in range(RING_BLOCKS)]
+        kern_paged = timed(lambda b: check(lib.gs_apply_device_paged(enc.handle, S, pslots[b], outs[b], SLICE,
+                                                                     C.byref(pm), (1 << N_SHARDS) - 1, None,
+                                                                     ks.cuda_stream), "k1 paged"),
+                           S * (N_SHARDS + K_PARITY) * SLICE, "K1 encode reading a paged KV cache in place")
+        ok_parity &= torch.equal(par_dev[RING_BLOCKS - 1, :2].cpu(),
+                                 D.encode(scheme, ring[RING_BLOCKS - 1, :2]).cpu())
+        kern["paged_kv_cache_us_per_launch"] = kern_paged["per_launch_us"]
+        kern["paged_kv_cache_frac"] = kern_paged["frac"]
+        del par_dev, rebuilt, caches
 
     # --- host link --------------------------------------------------------------
     link = host_link_peaks(torch, dev)

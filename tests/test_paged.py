@@ -24,7 +24,8 @@ def build(model, n, S, block, valid, nblocks=64, seed=0):
         c.buf.copy_(torch.randint(0, 256, c.buf.shape, dtype=torch.uint8, device="cuda", generator=g))
         caches.append(c)  # garbage everywhere, incl. past `valid`
     rng = np.random.default_rng(seed)
-    tables = [[int(b) for b in rng.permutation(nblocks)[:n]] for _ in range(S)]
+    perms = [rng.permutation(nblocks) for _ in range(n)]     # distinct blocks per worker across stripes
+    tables = [[int(perms[j][s]) for j in range(n)] for s in range(S)]
     truth = []
     for s in range(S):
         row = []
