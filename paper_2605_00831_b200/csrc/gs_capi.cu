@@ -382,8 +382,9 @@ int run_codec(const gs_codec* c, int n_stripes, SlotFn slot_ptr, OutFn out_ptr, 
     const size_t smem = use_bulk ? kBulkSmemHeader + static_cast<size_t>(stages) * c->special->used_cols *
                                                          c->special->tile_bulk
                                  : 0;
+    const bool paged = pg.any();
     int occ = use_bulk ? blocks_per_sm(dev, c->special->kernel_bulk, smem, kBulkThreads)
-                       : blocks_per_sm(dev, c->special->kernel, 0);
+                       : blocks_per_sm(dev, paged ? c->special->kernel_paged : c->special->kernel, 0);
     if (!use_bulk && g_ctas_per_sm > 0) occ = std::min(occ, g_ctas_per_sm);
     for (int s0 = 0; s0 < n_stripes; s0 += per) {
       const int cnt = std::min(per, n_stripes - s0);
@@ -398,6 +399,7 @@ int run_codec(const gs_codec* c, int n_stripes, SlotFn slot_ptr, OutFn out_ptr, 
                  pg.paged_slots, pg.logical0, pg.src, pg.dst};
       const int grid = static_cast<int>(std::min<uint64_t>(total, static_cast<uint64_t>(occ) * sms));
       cudaError_t e = use_bulk ? c->special->launch_bulk(ptrs.data(), cnt * stride, g, grid, st, stages, smem)
+                      : paged  ? c->special->launch_paged(ptrs.data(), cnt * stride, g, grid, st)
                                : c->special->launch(ptrs.data(), cnt * stride, g, grid, st);
       if (e != cudaSuccess) return fail(GS_CUDA_ERROR, "special kernel launch: %s", cudaGetErrorString(e));
       g_launches.fetch_add(1, std::memory_order_relaxed);
@@ -785,6 +787,8 @@ int gs_prewarm(int device) {
     cudaFuncAttributes a;
     GS_CUDA(cudaFuncGetAttributes(&a, e.kernel));
     blocks_per_sm(device, e.kernel, 0);
+    GS_CUDA(cudaFuncGetAttributes(&a, e.kernel_paged));
+    blocks_per_sm(device, e.kernel_paged, 0);
     GS_CUDA(cudaFuncGetAttributes(&a, e.kernel_bulk));
     const int stages = bulk_stages(&e);
     if (stages >= 2)

@@ -190,7 +190,7 @@ __device__ constexpr bool column_used(int j) {
 // arithmetic. The host guarantees 16-B aligned pointers and len % 16 == 0
 // (a ragged tail or misaligned shards go to the generic kernel instead), so
 // this kernel carries no byte-granular code at all.
-template <class Spec, int CAP, int U>
+template <class Spec, int CAP, int U, bool PAGED>
 __global__ void __launch_bounds__(kThreads) k_apply_special(const PtrTable<CAP> tab, const TileGeom g) {
   static_assert(U == 1, "one 16-byte group per thread per tile");
   for (uint32_t t = blockIdx.x; t < g.total; t += gridDim.x) {
@@ -198,24 +198,34 @@ __global__ void __launch_bounds__(kThreads) k_apply_special(const PtrTable<CAP> 
     const uint64_t off = static_cast<uint64_t>(t - s * g.tps) * kTile + threadIdx.x * kVec;
     if (off >= g.len) continue;
     const int base = static_cast<int>(s) * g.stride;
-    bool smask = false, dmask = false;
-    uint64_t soff = off, doff = off;
-    if (g.paged_slots) soff = paged_offset(g.src, g.logical0 + off, smask);
-    if (g.dst.page_bytes) doff = paged_offset(g.dst, g.logical0 + off, dmask);
     uint4 src[Spec::NS];
-#pragma unroll
-    for (int j = 0; j < Spec::NS; ++j) {
-      src[j] = make_uint4(0, 0, 0, 0);
-      if (column_used<Spec>(j)) {
-        const bool paged = (g.paged_slots >> j) & 1u;
-        if (!(paged && smask)) src[j] = ld_stream(tab.p[base + j] + (paged ? soff : off));
-      }
-    }
     uint4 out[Spec::NO];
-    horner_apply<Spec>(src, out);
-    if (!dmask) {
+    if constexpr (!PAGED) {
 #pragma unroll
-      for (int i = 0; i < Spec::NO; ++i) st_stream(const_cast<uint8_t*>(tab.p[base + g.out0 + i]) + doff, out[i]);
+      for (int j = 0; j < Spec::NS; ++j)
+        src[j] = column_used<Spec>(j) ? ld_stream(tab.p[base + j] + off) : make_uint4(0, 0, 0, 0);
+      horner_apply<Spec>(src, out);
+#pragma unroll
+      for (int i = 0; i < Spec::NO; ++i) st_stream(const_cast<uint8_t*>(tab.p[base + g.out0 + i]) + off, out[i]);
+    } else {
+      bool smask = false, dmask = false;
+      uint64_t soff = off, doff = off;
+      if (g.paged_slots) soff = paged_offset(g.src, g.logical0 + off, smask);
+      if (g.dst.page_bytes) doff = paged_offset(g.dst, g.logical0 + off, dmask);
+#pragma unroll
+      for (int j = 0; j < Spec::NS; ++j) {
+        src[j] = make_uint4(0, 0, 0, 0);
+        if (column_used<Spec>(j)) {
+          const bool paged = (g.paged_slots >> j) & 1u;
+          if (!(paged && smask)) src[j] = ld_stream(tab.p[base + j] + (paged ? soff : off));
+        }
+      }
+      horner_apply<Spec>(src, out);
+      if (!dmask) {
+#pragma unroll
+        for (int i = 0; i < Spec::NO; ++i)
+          st_stream(const_cast<uint8_t*>(tab.p[base + g.out0 + i]) + doff, out[i]);
+      }
     }
   }
 }

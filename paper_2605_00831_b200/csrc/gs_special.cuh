@@ -42,6 +42,8 @@ struct SpecialEntry {
   uint64_t mask;
   LaunchFn launch;
   KernelAddr kernel;
+  LaunchFn launch_paged;    // same arithmetic, paged-KV address mapping
+  KernelAddr kernel_paged;
   int tile;  // bytes of every shard per CTA tile
   // bulk-copy pipelined variant (k_apply_special_bulk)
   BulkLaunchFn launch_bulk;
@@ -90,12 +92,12 @@ struct DecSpec {
   GS_HD static constexpr CoefMatrix matrix() { return decode_plan_mask(KIND, N, K, MASK).m; }
 };
 
-template <class Spec, int CAP>
+template <class Spec, int CAP, bool PAGED>
 cudaError_t launch_special(const void* const* ptrs, int count, const TileGeom& g, int grid,
                            cudaStream_t st) {
   PtrTable<CAP> tab;
   for (int i = 0; i < count; ++i) tab.p[i] = static_cast<const uint8_t*>(ptrs[i]);
-  k_apply_special<Spec, CAP, kSpecialU><<<grid, kThreads, 0, st>>>(tab, g);
+  k_apply_special<Spec, CAP, kSpecialU, PAGED><<<grid, kThreads, 0, st>>>(tab, g);
   return cudaGetLastError();
 }
 
@@ -116,8 +118,10 @@ SpecialEntry make_entry(bool decoder, int kind, int n, int k, uint64_t mask) {
   e.n = n;
   e.k = k;
   e.mask = mask;
-  e.launch = &launch_special<Spec, kPtrCap>;
-  e.kernel = reinterpret_cast<KernelAddr>(&k_apply_special<Spec, kPtrCap, kSpecialU>);
+  e.launch = &launch_special<Spec, kPtrCap, false>;
+  e.kernel = reinterpret_cast<KernelAddr>(&k_apply_special<Spec, kPtrCap, kSpecialU, false>);
+  e.launch_paged = &launch_special<Spec, kPtrCap, true>;
+  e.kernel_paged = reinterpret_cast<KernelAddr>(&k_apply_special<Spec, kPtrCap, kSpecialU, true>);
   e.tile = kThreads * kVec * kSpecialU;
   e.launch_bulk = &launch_special_bulk<Spec, kPtrCap>;
   e.kernel_bulk = reinterpret_cast<KernelAddr>(&k_apply_special_bulk<Spec, kPtrCap, kBulkCW, kBulkU>);
