@@ -133,6 +133,27 @@ struct TileGeom {
 
 // Offset of logical slice byte `o` inside a paged slot; `masked` = beyond
 // the valid tokens of its page.
+__device__ __forceinline__ uint64_t paged_offset(const PageMap& m, uint64_t logical, bool& masked);
+
+// Same for the byte `tile_logical + lane_off` of a CTA tile: when the tile
+// sits inside one page (pages are multiples of the 4 KiB tile -- every
+// paged cache geometry of the configs), the page arithmetic is CTA-uniform
+// and only an add + compare remain per thread.
+__device__ __forceinline__ uint64_t paged_offset_tile(const PageMap& m, uint64_t tile_logical, uint32_t lane_off,
+                                                      bool& masked) {
+  const uint32_t u = static_cast<uint32_t>(tile_logical);
+  const uint32_t q = u / m.page_bytes;
+  const uint32_t in0 = u - q * m.page_bytes;
+  if (in0 + static_cast<uint32_t>(kTile) <= m.page_bytes) {
+    const uint32_t t = q / m.layers;
+    const uint32_t l = q - t * m.layers;
+    const uint32_t in = in0 + lane_off;
+    masked = in >= m.valid_tokens * m.token_bytes;
+    return static_cast<uint64_t>(l) * m.layer_stride + static_cast<uint64_t>(t) * m.kv_stride + in;
+  }
+  return paged_offset(m, tile_logical + lane_off, masked);
+}
+
 __device__ __forceinline__ uint64_t paged_offset(const PageMap& m, uint64_t logical, bool& masked) {
   const uint32_t o = static_cast<uint32_t>(logical);
   const uint32_t q = o / m.page_bytes;
@@ -210,8 +231,10 @@ __global__ void __launch_bounds__(kThreads) k_apply_special(const PtrTable<CAP> 
     } else {
       bool smask = false, dmask = false;
       uint64_t soff = off, doff = off;
-      if (g.paged_slots) soff = paged_offset(g.src, g.logical0 + off, smask);
-      if (g.dst.page_bytes) doff = paged_offset(g.dst, g.logical0 + off, dmask);
+      const uint64_t tile_logical = g.logical0 + static_cast<uint64_t>(t - s * g.tps) * kTile;
+      const uint32_t lane_off = threadIdx.x * kVec;
+      if (g.paged_slots) soff = paged_offset_tile(g.src, tile_logical, lane_off, smask);
+      if (g.dst.page_bytes) doff = paged_offset_tile(g.dst, tile_logical, lane_off, dmask);
 #pragma unroll
       for (int j = 0; j < Spec::NS; ++j) {
         src[j] = make_uint4(0, 0, 0, 0);
