@@ -238,10 +238,18 @@ def run_ours(args):
                                             plan_reconstruct_striped)
 
     rank, world, local = env_rank()
+    # GS_BENCH_SHARED_GPU=1: functional check of the multi-rank path with all
+    # ranks on cuda:0 (gloo plumbing; timings are not meaningful then).
+    shared = os.environ.get("GS_BENCH_SHARED_GPU") == "1"
+    if shared:
+        local = 0
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        if shared:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=dev)
     scheme = CodingScheme.reed_solomon(N_SHARDS, K_PARITY)
     cfg = K.LLAMA3_8B
     assert K.slice_bytes(cfg, BLOCK_TOKENS) == SLICE
@@ -298,7 +306,7 @@ def run_ours(args):
     barrier()
     ms = e0.elapsed_time(e1)
     if world > 1:
-        t = torch.tensor([ms], device=dev)
+        t = torch.tensor([ms], device="cpu" if shared else dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms = float(t.item())
     data_bytes_step = S * N_SHARDS * SLICE          # whole job
@@ -462,7 +470,7 @@ def run_ours(args):
     barrier()
     rec_ms = r0.elapsed_time(r1)
     if world > 1:
-        t = torch.tensor([rec_ms], device=dev)
+        t = torch.tensor([rec_ms], device="cpu" if shared else dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         rec_ms = float(t.item())
     if rank == owner:
