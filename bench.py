@@ -475,6 +475,10 @@ def run_ours(args):
         rec_ms = float(t.item())
     if rank == owner:
         ok_parity &= torch.equal(ring[b, :, jl], saved)
+    if world > 1:  # every rank's verdict (the rebuilt shard lives on its owner)
+        t = torch.tensor([1 if ok_parity else 0], device="cpu" if shared else dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MIN)
+        ok_parity = bool(t.item())
     recovery["c2_block_one_worker_ms"] = round(rec_ms, 4)
     recovery["c2_plan_host_ms"] = round(plan_ms, 3)
     recovery["c2_block_bytes_rebuilt"] = S * SLICE

@@ -1,0 +1,91 @@
+"""Small workload for compute-sanitizer (memcheck / racecheck / synccheck):
+every kernel family once -- specialised (register + bulk-copy pipeline),
+generic (aligned, ragged tail, misaligned), paged gather/scatter, the
+offload / upload pipelines -- at sizes that finish quickly under
+instrumentation. Exits non-zero on any byte mismatch vs the oracle.
+
+    compute-sanitizer --tool memcheck python tools/sanitize_smoke.py
+"""
+import os
+import sys
+
+import numpy as np
+import torch
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+from oracle import oracle as O  # noqa: E402
+from paper_2605_00831_b200 import _lib as L  # noqa: E402
+from paper_2605_00831_b200 import device as D  # noqa: E402
+from paper_2605_00831_b200.coding import CodingScheme, ErasurePattern, codec_ex  # noqa: E402
+from paper_2605_00831_b200.kv_layout import ModelConfig, make_ground_truth_slice  # noqa: E402
+from paper_2605_00831_b200.paged import PagedKVCache, encode_blocks, rebuild_blocks  # noqa: E402
+
+
+def main():
+    torch.cuda.set_device(0)
+    g = torch.Generator(device="cuda").manual_seed(1)
+    bad = 0
+    for variant in (0, 1):
+        L.lib().gs_set_kernel_variant(variant)
+        for n, k, ln in ((8, 2, 3 * 4096 + 32), (4, 2, 4096 + 5), (9, 3, 1000)):
+            sch = CodingScheme.reed_solomon(n, k)
+            data = torch.randint(0, 256, (n, ln), dtype=torch.uint8, device="cuda", generator=g)
+            par = D.encode(sch, data)
+            want = O.port().encode(O.RS, n, k, list(data.cpu().numpy()))
+            bad += sum(not np.array_equal(par[i].cpu().numpy(), want[i]) for i in range(k))
+            lost = ErasurePattern([0, n])
+            sh = {j: data[j] for j in range(1, n)}
+            sh.update({n + i: par[i] for i in range(1, k)})
+            got = D.reconstruct(sch, sh, lost)
+            bad += not torch.equal(got[0], data[0])
+    L.lib().gs_set_kernel_variant(2)
+    # generic on misaligned pointers
+    sch = CodingScheme.reed_solomon(8, 2)
+    buf = torch.randint(0, 256, (8, 4096 + 64), dtype=torch.uint8, device="cuda", generator=g)
+    out = torch.zeros((2, 4096 + 64), dtype=torch.uint8, device="cuda")
+    c = codec_ex(sch, generic=True)
+    D.apply(c, [[buf[j, 3:].data_ptr() for j in range(8)]], [[out[i, 3:].data_ptr() for i in range(2)]], 4096 + 17)
+    want = O.port().encode(O.RS, 8, 2, [buf[j, 3:3 + 4096 + 17].cpu().numpy() for j in range(8)])
+    bad += sum(not np.array_equal(out[i, 3:3 + 4096 + 17].cpu().numpy(), want[i]) for i in range(2))
+    # pipelines
+    pipe = D.Pipeline(0, 64 << 10)
+    data = torch.randint(0, 256, (3, 8, 3 * 4096 + 16), dtype=torch.uint8, device="cuda", generator=g)
+    h = torch.zeros((3, 2, data.shape[-1]), dtype=torch.uint8).pin_memory()
+    st = torch.cuda.current_stream()
+    pipe.encode_offload(sch, data, h, st, st)
+    st.synchronize()
+    bad += not torch.equal(h, D.encode(sch, data).cpu())
+    outs = {2: torch.zeros((3, data.shape[-1]), dtype=torch.uint8, device="cuda")}
+    pipe.reconstruct_upload(sch, ErasurePattern([2]), {j: data[:, j].contiguous() for j in range(8) if j != 2}, h,
+                            outs, st, st)
+    st.synchronize()
+    bad += not torch.equal(outs[2], data[:, 2])
+    # paged
+    model = ModelConfig(2, 8, 8, 2, 8)
+    caches = [PagedKVCache(model, 6, 16) for _ in range(8)]
+    truth = []
+    for j in range(8):
+        caches[j].buf.zero_()
+        sl = make_ground_truth_slice(3, 0, 0, j, model, 16, 9, device="cuda")
+        caches[j].write_slice(j % 6, sl, 9)
+        truth.append(sl)
+    tables = [[j % 6 for j in range(8)]]
+    par = torch.empty((1, 2, caches[0].slice_bytes), dtype=torch.uint8, device="cuda")
+    encode_blocks(sch, caches, tables, 9, par)
+    want = O.port().encode(O.RS, 8, 2, [t.cpu().numpy() for t in truth])
+    bad += sum(not np.array_equal(par[0, i].cpu().numpy(), want[i]) for i in range(2))
+    hp = par.cpu().pin_memory()
+    rep = {4: PagedKVCache(model, 6, 16, fill=0)}
+    rebuild_blocks(pipe, sch, ErasurePattern([4]), [None if j == 4 else caches[j] for j in range(8)], rep, tables,
+                   9, hp, st, st)
+    st.synchronize()
+    bad += not torch.equal(rep[4].read_slice(4, 9), truth[4])
+    pipe.close()
+    torch.cuda.synchronize()
+    print("sanitize_smoke: mismatches =", bad, "kernels =", D.launches())
+    sys.exit(1 if bad else 0)
+
+
+if __name__ == "__main__":
+    main()
