@@ -118,13 +118,136 @@ static void mul_xor(uint8_t* dst, const uint8_t* src, size_t len, uint8_t c) {
   for (size_t b = 0; b < len; ++b) dst[b] ^= row[src[b]];
 }
 
-/* coding.hpp:313-336 (+ encode_xor :263-267, encode_rs :269-275).
- * RDP is out of scope for this path. */
+/* ---- RDP (coding.hpp:225-251 layout, :277-307 encode, :343-449 recover) -- */
+
+/* coding.hpp:174-184 */
+static int smallest_prime_ge(int x) {
+  int v = x < 2 ? 2 : x;
+  for (;; ++v) {
+    int prime = v >= 2;
+    for (int d = 2; d * d <= v; ++d)
+      if (v % d == 0) prime = 0;
+    if (prime) return v;
+  }
+}
+
+static int pmod(int a, int p) { return ((a % p) + p) % p; }
+
+/* Array of (p-1) rows x (p+1) columns over the smallest prime p >= n+1:
+ * data columns 0..n-1 (n..p-2 virtual zeros), row parity = column p-1,
+ * diagonal d = (r + c) mod p stored at row d of the diagonal buffer for
+ * d <= p-2. Bytes past the last whole stripe are protected by P (row parity)
+ * and Q = sum_c 2^c * data_c. */
+static int rdp_encode(int n, const uint8_t* const* data, size_t len, uint8_t* const* parity) {
+  const int p = smallest_prime_ge(n + 1), rows = p - 1;
+  const size_t full = len / (size_t)rows * (size_t)rows;
+  uint8_t* rp = parity[0];
+  uint8_t* dp = parity[1];
+  memset(rp, 0, len);
+  memset(dp, 0, len);
+  for (int c = 0; c < n; ++c)
+    for (size_t b = 0; b < len; ++b) rp[b] ^= data[c][b];
+  for (size_t base = 0; base < full; base += (size_t)rows) {
+    for (int c = 0; c < n; ++c)
+      for (int r = 0; r < rows; ++r) {
+        const int d = (r + c) % p;
+        if (d != p - 1) dp[base + (size_t)d] ^= data[c][base + (size_t)r];
+      }
+    for (int r = 0; r < rows; ++r) {
+      const int d = (r + p - 1) % p;
+      if (d != p - 1) dp[base + (size_t)d] ^= rp[base + (size_t)r];
+    }
+  }
+  for (int c = 0; c < n; ++c) mul_xor(dp + full, data[c] + full, len - full, gso_gf_exp2((unsigned)c));
+  return GSO_OK;
+}
+
+/* coding.hpp:343-449: lost_cols are array columns (data c, row parity p-1);
+ * col[] holds present columns (NULL otherwise); outputs into outc[c]. */
+static void rdp_recover(int n, int p, size_t len, const uint8_t* const* col, const int* lost_cols, int nl,
+                        const uint8_t* diag, uint8_t** outc) {
+  const int rows = p - 1;
+  const size_t full = len / (size_t)rows * (size_t)rows;
+  for (int a = 0; a < nl; ++a) memset(outc[lost_cols[a]], 0, len);
+  if (nl == 1) { /* :356-371 single column: XOR of the present columns */
+    uint8_t* dst = outc[lost_cols[0]];
+    for (int c = 0; c < p; ++c)
+      if (col[c] && (lost_cols[0] != p - 1 || c != p - 1))
+        for (size_t b = 0; b < len; ++b) dst[b] ^= col[c][b];
+    return;
+  }
+  const int i = lost_cols[0] < lost_cols[1] ? lost_cols[0] : lost_cols[1];
+  const int j = lost_cols[0] < lost_cols[1] ? lost_cols[1] : lost_cols[0];
+  uint8_t* oi = outc[i];
+  uint8_t* oj = outc[j];
+  for (size_t base = 0; base < full; base += (size_t)rows) {
+    /* :384-413: two diagonal-walk chains, each solving its primary column from
+     * a stored diagonal, then the partner's cell in that row from the row sum. */
+    for (int pass = 0; pass < 2; ++pass) {
+      const int prim = pass == 0 ? i : j, part = pass == 0 ? j : i;
+      uint8_t* po = pass == 0 ? oi : oj;
+      uint8_t* qo = pass == 0 ? oj : oi;
+      int d = pmod(part - 1, p);
+      const int step = pmod(part - prim, p);
+      while (d != p - 1) {
+        const int r = pmod(d - prim, p);
+        uint8_t v = diag[base + (size_t)d];
+        for (int c = 0; c < p; ++c) {
+          if (c == prim) continue;
+          const int rc = pmod(d - c, p);
+          if (rc == p - 1) continue;
+          v ^= c == i ? oi[base + (size_t)rc] : c == j ? oj[base + (size_t)rc] : col[c] ? col[c][base + (size_t)rc] : 0;
+        }
+        po[base + (size_t)r] = v;
+        uint8_t w = 0;
+        for (int c = 0; c < p; ++c) {
+          if (c == part) continue;
+          w ^= c == i ? oi[base + (size_t)r] : c == j ? oj[base + (size_t)r] : col[c] ? col[c][base + (size_t)r] : 0;
+        }
+        qo[base + (size_t)r] = w;
+        d = (d + step) % p;
+      }
+    }
+  }
+  const size_t tail = len - full; /* :415-448 P/Q algebra on the tail */
+  if (!tail) return;
+  uint8_t* ps = (uint8_t*)calloc(tail, 1);
+  uint8_t* qs = (uint8_t*)calloc(tail, 1);
+  for (int c = 0; c < n; ++c) {
+    if (c == i || c == j || !col[c]) continue;
+    for (size_t b = 0; b < tail; ++b) ps[b] ^= col[c][full + b];
+    mul_xor(qs, col[c] + full, tail, gso_gf_exp2((unsigned)c));
+  }
+  for (size_t b = 0; b < tail; ++b) qs[b] ^= diag[full + b];
+  if (j == p - 1) {
+    uint8_t ci;
+    gso_gf_inv(gso_gf_exp2((unsigned)i), &ci);
+    for (size_t b = 0; b < tail; ++b) {
+      oi[full + b] = gso_gf_mul(qs[b], ci);
+      oj[full + b] = (uint8_t)(ps[b] ^ oi[full + b]);
+    }
+  } else {
+    for (size_t b = 0; b < tail; ++b) ps[b] ^= col[p - 1][full + b];
+    const uint8_t gi = gso_gf_exp2((unsigned)i), gj = gso_gf_exp2((unsigned)j);
+    uint8_t den;
+    gso_gf_inv((uint8_t)(gi ^ gj), &den);
+    for (size_t b = 0; b < tail; ++b) {
+      const uint8_t di = gso_gf_mul((uint8_t)(qs[b] ^ gso_gf_mul(gj, ps[b])), den);
+      oi[full + b] = di;
+      oj[full + b] = (uint8_t)(ps[b] ^ di);
+    }
+  }
+  free(ps);
+  free(qs);
+}
+
+/* coding.hpp:313-336 (+ encode_xor :263-267, encode_rs :269-275, encode_rdp
+ * :277-307). */
 int gso_encode(int kind, int n, int k, const uint8_t* const* data, size_t len,
                uint8_t* const* parity) {
   int st = gso_validate(kind, n, k);
   if (st) return st;
-  if (kind == GSO_RDP) return GSO_INVALID_ARGUMENT;
+  if (kind == GSO_RDP) return rdp_encode(n, data, len, parity);
   uint8_t* coef = (uint8_t*)malloc((size_t)k * (size_t)n);
   st = gso_encoding_matrix(kind, n, k, coef);
   if (st) {
@@ -270,12 +393,11 @@ int gso_decode_matrix(int kind, int n, int k, const int* lost_in, int n_lost_in,
   return GSO_OK;
 }
 
-/* coding.hpp:458-571 (XOR and RS branches). */
+/* coding.hpp:458-571 (XOR, RDP and RS branches). */
 int gso_reconstruct(int kind, int n, int k, const uint8_t* const* shards, const int* lost_in,
                     int n_lost, size_t len, uint8_t* const* out, int* n_out) {
   int st = gso_validate(kind, n, k);
   if (st) return st;
-  if (kind == GSO_RDP) return GSO_INVALID_ARGUMENT;
   int lost[255];
   if (n_lost > 255) return GSO_INVALID_ARGUMENT;
   int m = normalise_lost(lost_in, n_lost, lost);
@@ -284,6 +406,30 @@ int gso_reconstruct(int kind, int n, int k, const uint8_t* const* shards, const 
   if (m > gso_max_tolerance(kind, k)) return GSO_UNRECOVERABLE;       /* :466-470 */
   for (int idx = 0; idx < n + k; ++idx)                               /* :474-486 */
     if (!contains(lost, m, idx) && shards[idx] == NULL) return GSO_INVALID_ARGUMENT;
+  if (kind == GSO_RDP) { /* coding.hpp:503-534 */
+    int ld[2], e = 0;
+    for (int a = 0; a < m; ++a)
+      if (lost[a] < n) ld[e++] = lost[a];
+    *n_out = e;
+    if (e == 0) return GSO_OK;
+    const int p = smallest_prime_ge(n + 1);
+    const uint8_t** col = (const uint8_t**)calloc((size_t)p, sizeof(uint8_t*));
+    uint8_t** outc = (uint8_t**)calloc((size_t)p, sizeof(uint8_t*));
+    for (int c = 0; c < n; ++c)
+      if (!contains(lost, m, c)) col[c] = shards[c];
+    if (!contains(lost, m, n)) col[p - 1] = shards[n];
+    int lc[3], nl = 0;
+    for (int a = 0; a < e; ++a) lc[nl++] = ld[a];
+    if (contains(lost, m, n)) lc[nl++] = p - 1;
+    uint8_t* scratch = NULL;
+    for (int a = 0; a < e; ++a) outc[ld[a]] = out[a];
+    if (contains(lost, m, n)) outc[p - 1] = scratch = (uint8_t*)malloc(len ? len : 1);
+    rdp_recover(n, p, len, col, lc, nl, contains(lost, m, n + 1) ? NULL : shards[n + 1], outc);
+    free(scratch);
+    free(col);
+    free(outc);
+    return GSO_OK;
+  }
   uint8_t* cd = (uint8_t*)malloc((size_t)255 * (size_t)n);
   uint8_t* cp = (uint8_t*)malloc((size_t)255 * (size_t)k);
   int e = 0;

@@ -42,7 +42,8 @@ int gso_validate(int kind, int n, int k);
 int gso_max_tolerance(int kind, int k);
 int gso_encoding_matrix(int kind, int n, int k, uint8_t* coef /* k*n row-major */);
 
-/* encode (coding.hpp:313-336): n data buffers of len bytes -> k parity buffers. */
+/* encode (coding.hpp:313-336): n data buffers of len bytes -> k parity buffers
+ * (XOR, RS and the shortened RDP of coding.hpp:225-307). */
 int gso_encode(int kind, int n, int k, const uint8_t* const* data, size_t len,
                uint8_t* const* parity);
 

@@ -14,12 +14,14 @@
 #include <mutex>
 #include <string>
 #include <thread>
+#include <tuple>
 #include <vector>
 
 #include "../../include/gs_capi.h"
 #include "gs_field.hpp"
 #include "gs_kernels.cuh"
 #include "gs_kv.cuh"
+#include "gs_rdp.cuh"
 #include "gs_special.cuh"
 
 namespace gsb {
@@ -96,7 +98,7 @@ struct DeviceInfo {
 };
 std::mutex g_dev_mu;
 std::map<int, DeviceInfo> g_dev;
-std::map<std::pair<int, const void*>, int> g_occ;  // (device, kernel) -> blocks per SM
+std::map<std::tuple<int, const void*, size_t>, int> g_occ;  // (device, kernel, smem) -> blocks per SM
 
 int device_sms(int dev) {
   std::lock_guard<std::mutex> lk(g_dev_mu);
@@ -110,7 +112,7 @@ int device_sms(int dev) {
 
 int blocks_per_sm(int dev, const void* kernel, size_t smem, int threads = kThreads) {
   std::lock_guard<std::mutex> lk(g_dev_mu);
-  auto key = std::make_pair(dev, kernel);
+  auto key = std::make_tuple(dev, kernel, smem);
   auto it = g_occ.find(key);
   if (it != g_occ.end()) return it->second;
   if (smem > 48 * 1024)
@@ -186,10 +188,16 @@ struct gs_codec {
   std::vector<int> used;         // slots with a nonzero coefficient (generic path)
   const SpecialEntry* special = nullptr;
   std::vector<CoefWords> words;  // n_out x used.size(), generic path table
+  // RDP (position-dependent): p of the array, the two lost array columns of
+  // a chain recovery, or an XOR decoder for single-column recoveries.
+  int rdp_p = 0;
+  int rdp_li = -1, rdp_lj = -1;
+  gs_codec* xor_helper = nullptr;
   mutable std::mutex mu;
   mutable std::map<int, CoefWords*> dev_words;  // device -> uploaded table
 
   ~gs_codec() {
+    delete xor_helper;
     for (auto& kv : dev_words) {
       int prev = 0;
       cudaGetDevice(&prev);
@@ -300,6 +308,7 @@ const void* generic_kernel(int kb) {
 struct Paging {
   uint32_t paged_slots = 0;
   uint64_t logical0 = 0;
+  uint64_t total_len = 0;  // RDP: absolute column length (0 = this launch's len)
   PageMap src{};
   PageMap dst{};
   bool any() const { return paged_slots != 0 || dst.page_bytes != 0; }
@@ -329,9 +338,14 @@ int check_page_map(const PageMap& m, const char* what) {
 }
 
 template <class SlotFn, class OutFn>
+int run_rdp(const gs_codec* c, int n_stripes, SlotFn slot_ptr, OutFn out_ptr, uint64_t len, cudaStream_t st,
+            const Paging& pg);
+
+template <class SlotFn, class OutFn>
 int run_codec(const gs_codec* c, int n_stripes, SlotFn slot_ptr, OutFn out_ptr, uint64_t len,
               cudaStream_t st, const Paging& pg = Paging{}) {
   if (len == 0 || n_stripes == 0 || c->n_out == 0) return GS_OK;
+  if (c->kind == GS_RDP) return run_rdp(c, n_stripes, slot_ptr, out_ptr, len, st, pg);
   int dev = 0;
   if (int s = current_device(&dev)) return s;
   const int sms = device_sms(dev);
@@ -454,6 +468,72 @@ int run_codec(const gs_codec* c, int n_stripes, SlotFn slot_ptr, OutFn out_ptr, 
   return GS_OK;
 }
 
+// RDP (position-dependent, coding.hpp:225-534): tile kernels of gs_rdp.cuh
+// for encode and two-column recovery; single-column recovery through the
+// XOR helper codec. `pg.logical0` / `pg.total_len` place this launch's range
+// inside the column (pipelines split on dstripe boundaries).
+template <class SlotFn, class OutFn>
+int run_rdp(const gs_codec* c, int n_stripes, SlotFn slot_ptr, OutFn out_ptr, uint64_t len, cudaStream_t st,
+            const Paging& pg) {
+  if (pg.paged_slots || pg.dst.page_bytes) return fail(GS_UNSUPPORTED, "rdp: paged KV caches are not supported");
+  if (c->xor_helper) return run_codec(c->xor_helper, n_stripes, slot_ptr, out_ptr, len, st);
+  const int n = c->n, p = c->rdp_p, rows = p - 1;
+  const uint64_t total = pg.total_len ? pg.total_len : len;
+  if (pg.logical0 % static_cast<uint64_t>(rows))
+    return fail(GS_INVALID_ARGUMENT, "rdp: range must start on a dstripe boundary");
+  int dev = 0;
+  if (int s = current_device(&dev)) return s;
+  const int sms = device_sms(dev);
+  bool aligned = true;
+  const bool encode = !c->decoder;
+  for (int s = 0; s < n_stripes; ++s) {
+    for (int j = 0; j < c->n_slots; ++j) {
+      const void* q = slot_ptr(s, j);
+      const bool needed = encode || std::find(c->used.begin(), c->used.end(), j) != c->used.end();
+      if (needed && !q) return fail(GS_INVALID_ARGUMENT, "apply: shard slot %d of stripe %d is NULL but required", j, s);
+      if (q) aligned &= aligned16(q);
+    }
+    for (int i = 0; i < c->n_out; ++i) {
+      const void* q = out_ptr(s, i);
+      if (!q) return fail(GS_INVALID_ARGUMENT, "apply: output %d of stripe %d is NULL", i, s);
+      aligned &= aligned16(q);
+    }
+  }
+  const uint32_t T = static_cast<uint32_t>(rows) * kRdpThreads;
+  const uint64_t tps64 = (len + T - 1) / T;
+  const int in_slots = encode ? n : n + 2;
+  const int stride = in_slots + c->n_out;
+  const int per = kPtrCap / stride;
+  if (per < 1) return fail(GS_INVALID_ARGUMENT, "rdp: stripe needs %d pointers (> %d)", stride, kPtrCap);
+  const size_t smem = static_cast<size_t>(encode ? n + 2 : p + 1) * T;
+  const void* kern = encode ? reinterpret_cast<const void*>(&k_rdp_encode<kPtrCap>)
+                            : reinterpret_cast<const void*>(&k_rdp_recover<kPtrCap>);
+  const int occ = blocks_per_sm(dev, kern, smem, kRdpThreads);
+  std::vector<const void*> ptrs;
+  for (int s0 = 0; s0 < n_stripes; s0 += per) {
+    const int cnt = std::min(per, n_stripes - s0);
+    ptrs.assign(static_cast<size_t>(cnt) * stride, nullptr);
+    for (int s = 0; s < cnt; ++s) {
+      for (int j = 0; j < in_slots; ++j) ptrs[s * stride + j] = slot_ptr(s0 + s, j);
+      for (int i = 0; i < c->n_out; ++i) ptrs[s * stride + in_slots + i] = out_ptr(s0 + s, i);
+    }
+    const uint64_t ntiles = tps64 * cnt;
+    RdpGeom g{n, p, rows, len, pg.logical0, total / rows * rows, total, static_cast<uint32_t>(tps64),
+              static_cast<uint32_t>(ntiles), stride, aligned ? 1 : 0, c->rdp_li, c->rdp_lj};
+    PtrTable<kPtrCap> tab;
+    for (int i = 0; i < cnt * stride; ++i) tab.p[i] = static_cast<const uint8_t*>(ptrs[i]);
+    const int grid = static_cast<int>(std::min<uint64_t>(ntiles, static_cast<uint64_t>(occ) * sms));
+    if (encode)
+      k_rdp_encode<kPtrCap><<<grid, kRdpThreads, smem, st>>>(tab, g);
+    else
+      k_rdp_recover<kPtrCap><<<grid, kRdpThreads, smem, st>>>(tab, g, c->n_out, in_slots);
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return fail(GS_CUDA_ERROR, "rdp kernel launch: %s", cudaGetErrorString(e));
+    g_launches.fetch_add(1, std::memory_order_relaxed);
+  }
+  return GS_OK;
+}
+
 }  // namespace
 
 // ============================================================================
@@ -493,6 +573,17 @@ uint64_t piece_len(uint64_t len, size_t slot, int per_byte, uint64_t cap = ~0ull
   uint64_t r = std::min<uint64_t>(slot / static_cast<uint64_t>(per_byte), cap);
   r = r / 4096 * 4096;
   if (r == 0) r = 4096;
+  return std::min<uint64_t>(r, len);
+}
+
+// RDP pieces must cover whole dstripes (p-1 bytes) and stay 4 KiB aligned.
+uint64_t align_piece(const gs_codec* c, uint64_t rl, uint64_t len) {
+  if (c->kind != GS_RDP || c->xor_helper) return rl;
+  const uint64_t rows = static_cast<uint64_t>(c->rdp_p - 1);
+  uint64_t a = 4096;
+  while (a % rows) a += 4096;
+  uint64_t r = rl / a * a;
+  if (r == 0) r = a;
   return std::min<uint64_t>(r, len);
 }
 
@@ -611,18 +702,19 @@ static int encoder_create(int kind, int n, int k, bool generic, gs_codec** out) 
   if (!out) return fail(GS_INVALID_ARGUMENT, "encoder_create: out is NULL");
   *out = nullptr;
   if (int s = validate_scheme(kind, n, k)) return s;
-  if (kind == GS_RDP)
-    return fail(GS_UNSUPPORTED, "coding: rdp is not implemented on the GPU path (out of scope)");
+  if (kind == GS_RDP && smallest_prime_ge(n + 1) > kRdpMaxCols)
+    return fail(GS_UNSUPPORTED, "coding: rdp on the GPU path supports n <= %d", kRdpMaxCols - 2);
   auto* c = new gs_codec;
   c->kind = kind;
   c->n = n;
   c->k = k;
   c->n_out = k;
   c->n_slots = n;
+  if (kind == GS_RDP) c->rdp_p = smallest_prime_ge(n + 1);
   c->coef.resize(static_cast<size_t>(k) * n);
   gs_encoding_matrix(kind, n, k, c->coef.data());
   for (int i = 0; i < k; ++i) c->out_index.push_back(n + i);
-  c->special = generic ? nullptr : registry().find(false, kind, n, k, 0);
+  c->special = (generic || kind == GS_RDP) ? nullptr : registry().find(false, kind, n, k, 0);
   finish_codec(c);
   *out = c;
   return GS_OK;
@@ -633,8 +725,8 @@ static int decoder_create(int kind, int n, int k, const int* lost_in, int n_lost
   if (!out) return fail(GS_INVALID_ARGUMENT, "decoder_create: out is NULL");
   *out = nullptr;
   if (int s = validate_scheme(kind, n, k)) return s;
-  if (kind == GS_RDP)
-    return fail(GS_UNSUPPORTED, "coding: rdp is not implemented on the GPU path (out of scope)");
+  if (kind == GS_RDP && smallest_prime_ge(n + 1) > kRdpMaxCols)
+    return fail(GS_UNSUPPORTED, "coding: rdp on the GPU path supports n <= %d", kRdpMaxCols - 2);
   if (n_lost < 0 || (n_lost > 0 && lost_in == nullptr))
     return fail(GS_INVALID_ARGUMENT, "decoder_create: bad lost list");
   // ErasurePattern: sort + dedup (coding.hpp:131-134)
@@ -646,7 +738,7 @@ static int decoder_create(int kind, int n, int k, const int* lost_in, int n_lost
     if (idx < 0 || idx >= total) return fail(GS_INVALID_ARGUMENT, "coding: lost shard index out of range");
   if (static_cast<int>(lost.size()) > tolerance(kind, k))  // :466-470
     return fail(GS_UNRECOVERABLE, "coding: %zu erasures exceed tolerance %d for scheme %s", lost.size(),
-                tolerance(kind, k), kind == GS_XOR ? "xor" : "rs");
+                tolerance(kind, k), kind == GS_XOR ? "xor" : kind == GS_RDP ? "rdp" : "rs");
   auto is_lost = [&](int idx) { return std::binary_search(lost.begin(), lost.end(), idx); };
   std::vector<int> ld;
   for (int idx : lost)
@@ -662,6 +754,34 @@ static int decoder_create(int kind, int n, int k, const int* lost_in, int n_lost
   c->n_slots = total;
   c->out_index = ld;
   c->coef.assign(static_cast<size_t>(e) * total, 0);
+  if (e > 0 && kind == GS_RDP) {  // coding.hpp:503-534
+    const int p = smallest_prime_ge(n + 1);
+    c->rdp_p = p;
+    const bool row_lost = is_lost(n), diag_lost = is_lost(n + 1);
+    if (e == 1 && !row_lost) {
+      // single data column, row parity present: XOR of every present column
+      // (diagonal parity unused) -- served by the XOR(n) decoder, whose
+      // slots 0..n coincide with RDP's data + row parity.
+      const int lo = ld[0];
+      if (int st = decoder_create(GS_XOR, n, 1, &lo, 1, generic, &c->xor_helper)) {
+        delete c;
+        return st;
+      }
+      for (int s2 = 0; s2 <= n; ++s2)
+        if (s2 != lo) c->coef[s2] = 1;
+    } else {
+      (void)diag_lost;  // two lost columns imply a surviving diagonal parity
+      c->rdp_li = ld[0];
+      c->rdp_lj = e == 2 ? ld[1] : p - 1;
+      for (int b = 0; b < e; ++b)
+        for (int s2 = 0; s2 < total; ++s2)
+          if (!is_lost(s2)) c->coef[static_cast<size_t>(b) * total + s2] = 1;
+    }
+    c->out_index = ld;
+    finish_codec(c);
+    *out = c;
+    return GS_OK;
+  }
   if (e > 0) {
     if (kind == GS_XOR) {  // coding.hpp:496-502
       for (int s = 0; s < total; ++s)
@@ -879,7 +999,7 @@ static int encode_offload(gs_pipeline* p, const gs_codec* c, int n_stripes, cons
   auto ks = static_cast<cudaStream_t>(copy);
   const int K = c->n_out, N = c->n_slots;
   const size_t slot = p->slot_bytes();
-  const uint64_t rl_max = piece_len(len, slot, K);
+  const uint64_t rl_max = align_piece(c, piece_len(len, slot, K), len);
   std::vector<CopyOp> ops;
   for (uint64_t r0 = 0; r0 < len; r0 += rl_max) {
     const uint64_t rl = std::min<uint64_t>(rl_max, len - r0);
@@ -895,10 +1015,11 @@ static int encode_offload(gs_pipeline* p, const gs_codec* c, int n_stripes, cons
       };
       auto dst = [&](int s, int i) -> const void* { return base + (static_cast<size_t>(s) * K + i) * rl; };
       Paging pg;
+      pg.logical0 = r0;
+      pg.total_len = len;
       if (src_map) {
         pg.src = to_map(src_map);
         pg.paged_slots = N >= 32 ? ~0u : (1u << N) - 1;
-        pg.logical0 = r0;
       }
       if (int st = run_codec(c, cnt, src, dst, rl, cs, pg)) return st;
       GS_CUDA(cudaEventRecord(p->done[sl], cs));
@@ -946,7 +1067,7 @@ static int reconstruct_upload(gs_pipeline* p, const gs_codec* c, int n_stripes, 
     if (j >= n) host_slots.push_back(j);
   const int H = std::max<int>(1, static_cast<int>(host_slots.size()));
   const size_t slot = p->slot_bytes();
-  const uint64_t rl_max = piece_len(len, slot, H);
+  const uint64_t rl_max = align_piece(c, piece_len(len, slot, H), len);
   std::vector<CopyOp> ops;
   for (uint64_t r0 = 0; r0 < len; r0 += rl_max) {
     const uint64_t rl = std::min<uint64_t>(rl_max, len - r0);
@@ -981,6 +1102,7 @@ static int reconstruct_upload(gs_pipeline* p, const gs_codec* c, int n_stripes, 
       };
       Paging pg;
       pg.logical0 = r0;
+      pg.total_len = len;
       if (src_map) {
         pg.src = to_map(src_map);
         pg.paged_slots = n >= 32 ? ~0u : (1u << n) - 1;  // data slots; parity comes from staging
@@ -1008,7 +1130,7 @@ int gs_encode_host(gs_pipeline* p, const gs_codec* c, const void* const* h_data,
   const size_t slot = p->slot_bytes();
   // ~2 MiB per shard per piece: deep enough pipelining that the H2D of piece
   // i+1, the kernel of piece i and the D2H of piece i-1 overlap.
-  const uint64_t rl_max = piece_len(len, slot, N + K, kHostPiece);
+  const uint64_t rl_max = align_piece(c, piece_len(len, slot, N + K, kHostPiece), len);
   std::vector<CopyOp> ops;
   for (uint64_t r0 = 0; r0 < len; r0 += rl_max) {
     const uint64_t rl = std::min<uint64_t>(rl_max, len - r0);
@@ -1024,7 +1146,10 @@ int gs_encode_host(gs_pipeline* p, const gs_codec* c, const void* const* h_data,
     GS_CUDA(cudaStreamWaitEvent(p->s_comp, p->ready[sl], 0));
     auto src = [&](int, int j) -> const void* { return in + static_cast<size_t>(j) * rl; };
     auto dst = [&](int, int i) -> const void* { return outb + static_cast<size_t>(i) * rl; };
-    if (int st = run_codec(c, 1, src, dst, rl, p->s_comp)) return st;
+    Paging pg;
+    pg.logical0 = r0;
+    pg.total_len = len;
+    if (int st = run_codec(c, 1, src, dst, rl, p->s_comp, pg)) return st;
     GS_CUDA(cudaEventRecord(p->done[sl], p->s_comp));
     GS_CUDA(cudaStreamWaitEvent(p->s_d2h, p->done[sl], 0));
     for (int i = 0; i < K; ++i)
@@ -1048,7 +1173,7 @@ int gs_reconstruct_host(gs_pipeline* p, const gs_codec* c, const void* const* h_
   DeviceGuard g(p->device);
   const int U = static_cast<int>(c->used.size()), E = c->n_out;
   const size_t slot = p->slot_bytes();
-  const uint64_t rl_max = piece_len(len, slot, U + E, kHostPiece);
+  const uint64_t rl_max = align_piece(c, piece_len(len, slot, U + E, kHostPiece), len);
   std::vector<CopyOp> ops;
   for (uint64_t r0 = 0; r0 < len; r0 += rl_max) {
     const uint64_t rl = std::min<uint64_t>(rl_max, len - r0);
@@ -1067,7 +1192,10 @@ int gs_reconstruct_host(gs_pipeline* p, const gs_codec* c, const void* const* h_
       return it == c->used.end() ? nullptr : in + static_cast<size_t>(it - c->used.begin()) * rl;
     };
     auto dst = [&](int, int i) -> const void* { return outb + static_cast<size_t>(i) * rl; };
-    if (int st = run_codec(c, 1, src, dst, rl, p->s_comp)) return st;
+    Paging pg;
+    pg.logical0 = r0;
+    pg.total_len = len;
+    if (int st = run_codec(c, 1, src, dst, rl, p->s_comp, pg)) return st;
     GS_CUDA(cudaEventRecord(p->done[sl], p->s_comp));
     GS_CUDA(cudaStreamWaitEvent(p->s_d2h, p->done[sl], 0));
     for (int i = 0; i < E; ++i)

@@ -65,6 +65,25 @@ GS_HD constexpr uint8_t gf_inv(uint8_t a) {
   return a ? r : 0;
 }
 
+// 2^e in the field (gf256.hpp:59-61), e >= 0.
+GS_HD constexpr uint8_t exp2_of(int e) {
+  uint8_t r = 1;
+  for (int i = 0; i < e % 255; ++i) r = gf_mul(r, 2);
+  return r;
+}
+
+// Smallest prime >= x (coding.hpp:174-184): the RDP array's p for n data
+// columns is smallest_prime_ge(n + 1).
+GS_HD constexpr int smallest_prime_ge(int x) {
+  int v = x < 2 ? 2 : x;
+  for (;; ++v) {
+    bool prime = true;
+    for (int d = 2; d * d <= v; ++d)
+      if (v % d == 0) prime = false;
+    if (prime) return v;
+  }
+}
+
 // Systematic Cauchy coefficient of parity row i, data column j for RS(n, k):
 // 1 / (x_i ^ y_j) with x_i = i, y_j = k + j (coding.hpp:108-114).
 GS_HD constexpr uint8_t cauchy(int k, int i, int j) {

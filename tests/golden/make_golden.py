@@ -23,13 +23,14 @@ sys.path.insert(0, ROOT)
 from oracle import oracle as O  # noqa: E402
 from tests.golden.vectors import splitmix_bytes  # noqa: E402
 
-# Scheme set of the reference acceptance C1 (tests/acceptance.cpp:101-107)
-# minus RDP (out of scope), plus the configs' RS(6,2)
-# and a few wider / taller shapes for the generic kernel.
+# Scheme set of the reference acceptance C1 (tests/acceptance.cpp:101-107),
+# plus the configs' RS(6,2), a few wider / taller RS shapes for the generic
+# kernel, and RDP at primes p = 3, 5, 7, 11, 13.
 SCHEMES = [
     (O.XOR, 2, 1), (O.XOR, 4, 1), (O.XOR, 8, 1),
     (O.RS, 4, 1), (O.RS, 4, 2), (O.RS, 8, 2), (O.RS, 8, 3), (O.RS, 6, 2),
     (O.RS, 2, 2), (O.RS, 10, 4), (O.RS, 16, 4), (O.RS, 12, 3),
+    (O.RDP, 2, 2), (O.RDP, 3, 2), (O.RDP, 4, 2), (O.RDP, 6, 2), (O.RDP, 8, 2), (O.RDP, 12, 2),
 ]
 MATRIX_ONLY = [(O.RS, 200, 55), (O.RS, 127, 127), (O.RS, 1, 1), (O.RS, 32, 8)]
 HEX_LENGTHS = [1, 17, 64]

@@ -120,11 +120,16 @@ def test_decoder_errors_match_reference(golden):
             assert sorted(c.out_index) == rec["rebuilt"]
 
 
-def test_rdp_is_rejected_not_faked():
+def test_rdp_codecs_and_limits():
+    # RDP runs on the GPU path for p <= 23 (n <= 22); wider arrays are refused, not faked
+    enc = G.encoder(G.CodingScheme.rdp(8))
+    assert enc.n_out == 2 and enc.out_index == [8, 9] and not enc.specialised
     h = C.c_void_p()
-    assert L.lib().gs_encoder_create(1, 4, 2, C.byref(h)) == L.GS_UNSUPPORTED
-    with pytest.raises(G.Unsupported):
-        G.encoder(G.CodingScheme.rdp(4))
+    assert L.lib().gs_encoder_create(1, 30, 2, C.byref(h)) == L.GS_UNSUPPORTED
+    for lost, outs in (([3], [3]), ([3, 8], [3]), ([3, 9], [3]), ([1, 5], [1, 5]), ([8, 9], [])):
+        assert G.decoder(G.CodingScheme.rdp(6 if max(lost) < 8 else 8), G.ErasurePattern(lost)).out_index == outs
+    with pytest.raises(G.UnrecoverableError):
+        G.decoder(G.CodingScheme.rdp(4), G.ErasurePattern([0, 1, 2]))
 
 
 def test_slice_bytes_and_seal(golden, port):

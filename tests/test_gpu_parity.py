@@ -310,3 +310,65 @@ def test_kernel_variants_bit_identical(golden, variant):
                             assert torch.equal(t, data[:, i]), (n, k, lost, variant)
     finally:
         L.lib().gs_set_kernel_variant(2)
+
+
+@pytest.mark.parametrize("n", [1, 2, 3, 4, 5, 6, 8, 10, 12])
+def test_rdp_every_pattern_many_lengths(n):
+    """Shortened RDP (coding.hpp:225-534) on the GPU tile kernels: encode and
+    every single / double erasure at lengths with and without a P/Q tail,
+    multi-tile and multi-stripe launches; bit-exact vs the oracle."""
+    scheme = G.CodingScheme.rdp(n)
+    p = next(q for q in range(n + 1, 64) if all(q % d for d in range(2, q)))
+    rows = p - 1
+    for ln in (1, rows - 1, rows, 2 * rows + 1, 256 * rows, 256 * rows + 3, 3 * 256 * rows + 7, 70001):
+        S = 3
+        host = [[splitmix_bytes(7 * n + 100 * s + j + ln, ln) for j in range(n)] for s in range(S)]
+        data = torch.stack([to_dev(h) for h in host])
+        par = D.encode(scheme, data)
+        hp = par.cpu().numpy()
+        for s in range(S):
+            want = O.port().encode(O.RDP, n, 2, host[s])
+            for i in range(2):
+                assert np.array_equal(hp[s, i], want[i]), (n, ln, s, i)
+        for e in (1, 2):
+            for lost in itertools.combinations(range(n + 2), e):
+                sh = {j: data[:, j].contiguous() for j in range(n) if j not in lost}
+                sh.update({n + i: par[:, i].contiguous() for i in range(2) if n + i not in lost})
+                got = D.reconstruct(scheme, sh, G.ErasurePattern(lost))
+                assert sorted(got) == [j for j in lost if j < n]
+                for i, t in got.items():
+                    assert torch.equal(t, data[:, i]), (n, ln, lost)
+
+
+def test_rdp_pipelines_split_on_dstripes():
+    """offload / upload / host calls cut RDP columns into pieces: pieces must
+    respect dstripe boundaries and the tail (tiny staging ring forces many)."""
+    for n in (4, 8):
+        scheme = G.CodingScheme.rdp(n)
+        ln = 3 * 81920 + 13
+        host = [splitmix_bytes(500 + j, ln) for j in range(n)]
+        want = O.port().encode(O.RDP, n, 2, host)
+        got = G.encode(scheme, host)
+        assert all(np.array_equal(got[i], want[i]) for i in range(2))
+        pipe = D.Pipeline(0, 256 << 10)
+        data = to_dev(host).unsqueeze(0)
+        h = torch.zeros((1, 2, ln), dtype=torch.uint8).pin_memory()
+        st = torch.cuda.current_stream()
+        pipe.encode_offload(scheme, data, h, st, st)
+        st.synchronize()
+        assert all(np.array_equal(h[0, i].numpy(), want[i]) for i in range(2))
+        for lost in ([1], [0, 2], [3, n], [2, n + 1]):
+            pat = G.ErasurePattern(lost)
+            dec = G.decoder(scheme, pat)
+            outs = {i: torch.zeros((1, ln), dtype=torch.uint8, device="cuda") for i in dec.out_index}
+            pipe.reconstruct_upload(scheme, pat, {j: data[:, j].contiguous() for j in range(n) if j not in lost},
+                                    h, outs, st, st)
+            st.synchronize()
+            for i in dec.out_index:
+                assert np.array_equal(outs[i][0].cpu().numpy(), host[i]), (n, lost)
+            surv = {j: host[j] for j in range(n) if j not in lost}
+            surv.update({n + i: want[i] for i in range(2) if n + i not in lost})
+            rb = G.reconstruct(scheme, surv, pat)
+            for i, b in rb.items():
+                assert np.array_equal(b, host[i])
+        pipe.close()
