@@ -42,7 +42,8 @@ static std::vector<std::vector<uint8_t>> shards(int n, size_t len, uint64_t seed
 
 int main() {
   const std::vector<gs::CodingScheme> schemes = {
-      gs::CodingScheme::xor_code(2), gs::CodingScheme::xor_code(8), gs::CodingScheme::reed_solomon(4, 1),
+      gs::CodingScheme::xor_code(2), gs::CodingScheme::xor_code(8), gs::CodingScheme::rdp(4), gs::CodingScheme::rdp(6),
+      gs::CodingScheme::reed_solomon(4, 1),
       gs::CodingScheme::reed_solomon(4, 2), gs::CodingScheme::reed_solomon(8, 2),
       gs::CodingScheme::reed_solomon(8, 3), gs::CodingScheme::reed_solomon(6, 2)};
   uint64_t seed = 1;
