@@ -42,27 +42,33 @@ def main():
     ap.add_argument("--sizes", default="0.25,1,4,16,64,256")
     ap.add_argument("--n", type=int, default=8)
     ap.add_argument("--k", type=int, default=2)
+    ap.add_argument("--kind", choices=["rs", "rdp", "xor"], default="rs")
+    ap.add_argument("--lost", default="1", help="comma-separated lost shard indices for K2")
     args = ap.parse_args()
     lib = L.lib()
     dev = torch.device("cuda:0")
     st = torch.cuda.Stream()
     n, k = args.n, args.k
-    scheme = CodingScheme.reed_solomon(n, k)
+    scheme = {"rs": lambda: CodingScheme.reed_solomon(n, k), "rdp": lambda: CodingScheme.rdp(n),
+              "xor": lambda: CodingScheme.xor_code(n)}[args.kind]()
+    k = scheme.k
+    lost = [int(x) for x in args.lost.split(",")]
     enc = encoder(scheme)
-    dec = decoder(scheme, ErasurePattern([1]))
+    dec = decoder(scheme, ErasurePattern(lost))
     out = []
     for mib in [float(x) for x in args.sizes.split(",")]:
         L_ = int(mib * (1 << 20)) // 4096 * 4096
         nbuf = max(2, min(8, int((1 << 30) // (L_ * (n + k))) ))  # rotate so data > L2
         data = torch.randint(0, 256, (nbuf, n, L_), dtype=torch.uint8, device=dev)
         par = torch.empty((nbuf, k, L_), dtype=torch.uint8, device=dev)
-        reb = torch.empty((nbuf, L_), dtype=torch.uint8, device=dev)
+        reb = torch.empty((nbuf, max(dec.n_out, 1), L_), dtype=torch.uint8, device=dev)
         sl = [L.ptr_array([data[b, j].data_ptr() for j in range(n)]) for b in range(nbuf)]
         ol = [L.ptr_array([par[b, i].data_ptr() for i in range(k)]) for b in range(nbuf)]
-        dl = [L.ptr_array([None if j == 1 else (data[b, j].data_ptr() if j < n else par[b, j - n].data_ptr())
+        dl = [L.ptr_array([None if j in lost else (data[b, j].data_ptr() if j < n else par[b, j - n].data_ptr())
                            for j in range(n + k)]) for b in range(nbuf)]
-        rl = [L.ptr_array([reb[b].data_ptr()]) for b in range(nbuf)]
-        row = {"mib_per_shard": mib, "bytes_enc": (n + k) * L_, "bytes_dec": (n + 1) * L_}
+        rl = [L.ptr_array([reb[b, i].data_ptr() for i in range(dec.n_out)]) for b in range(nbuf)]
+        dec_bytes = (len(dec.coefficients().any(axis=0).nonzero()[0]) + dec.n_out) * L_
+        row = {"kind": args.kind, "mib_per_shard": mib, "bytes_enc": (n + k) * L_, "bytes_dec": dec_bytes}
         for v in (0, 1):
             check(lib.gs_set_kernel_variant(v))
             cnt = [0]
@@ -79,7 +85,7 @@ def main():
             t1 = graph_time(k1, nbuf * 2, st)
             t2 = graph_time(k2, nbuf * 2, st)
             row[f"k1_v{v}_gbs"] = round((n + k) * L_ / t1 / 1e9, 1)
-            row[f"k2_v{v}_gbs"] = round((n + 1) * L_ / t2 / 1e9, 1)
+            row[f"k2_v{v}_gbs"] = round(dec_bytes / t2 / 1e9, 1)
             row[f"k1_v{v}_us"] = round(t1 * 1e6, 2)
         # device copy of the same byte volume (read + write), rotating over
         # buffers so the L2 cannot serve it: the attainable HBM rate at this size
