@@ -42,9 +42,11 @@ struct RdpGeom {
 
 __device__ __forceinline__ uint8_t gf_mul_dev(uint8_t a, uint8_t b) { return gf_mul(a, b); }
 
+// (a mod p) for a in (-p, 2p): one compare-and-add instead of an integer
+// division (all the array index arithmetic stays in that range).
 __device__ __forceinline__ int pmod(int a, int p) {
-  a %= p;
-  return a < 0 ? a + p : a;
+  a = a < 0 ? a + p : a;
+  return a >= p ? a - p : a;
 }
 
 // Cooperative tile load of `bytes` bytes at src into smem (16-B vectors when
@@ -90,10 +92,16 @@ __global__ void __launch_bounds__(kRdpThreads) k_rdp_encode(const PtrTable<CAP> 
     __syncthreads();  // previous tile's smem fully consumed
     for (int c = 0; c < n; ++c) rdp_load(data + static_cast<size_t>(c) * T, tab.p[base + c] + off, bytes, T, g.aligned);
     __syncthreads();
-    for (uint32_t b = threadIdx.x; b < T; b += blockDim.x) {
-      uint8_t v = 0;
-      for (int c = 0; c < n; ++c) v ^= data[static_cast<size_t>(c) * T + b];
-      rowp[b] = v;
+    for (uint32_t v16 = threadIdx.x; v16 < T / 16; v16 += blockDim.x) {  // T = rows * 256: 16-B multiple
+      uint4 v = make_uint4(0, 0, 0, 0);
+      for (int c = 0; c < n; ++c) {
+        const uint4 x = reinterpret_cast<const uint4*>(data + static_cast<size_t>(c) * T)[v16];
+        v.x ^= x.x;
+        v.y ^= x.y;
+        v.z ^= x.z;
+        v.w ^= x.w;
+      }
+      reinterpret_cast<uint4*>(rowp)[v16] = v;
     }
     __syncthreads();
     // one dstripe per thread
@@ -182,7 +190,7 @@ __global__ void __launch_bounds__(kRdpThreads) k_rdp_recover(const PtrTable<CAP>
             for (int c = 0; c < p; ++c)
               if (c != part) w ^= col[static_cast<size_t>(c) * T + sb + r];
             qo[r] = w;
-            d = (d + step) % p;
+            d = pmod(d + step, p);
           }
         }
       } else {
