@@ -505,9 +505,15 @@ int run_rdp(const gs_codec* c, int n_stripes, SlotFn slot_ptr, OutFn out_ptr, ui
   const int stride = in_slots + c->n_out;
   const int per = kPtrCap / stride;
   if (per < 1) return fail(GS_INVALID_ARGUMENT, "rdp: stripe needs %d pointers (> %d)", stride, kPtrCap);
-  const size_t smem = static_cast<size_t>(encode ? n + 2 : p + 1) * T;
-  const void* kern = encode ? reinterpret_cast<const void*>(&k_rdp_encode<kPtrCap>)
-                            : reinterpret_cast<const void*>(&k_rdp_recover<kPtrCap>);
+  const size_t smem = static_cast<size_t>(encode ? rows + 2 : p + 1) * T;
+  const void* kern = nullptr;
+#define GS_RDP_PICK(P_)                                                                        \
+  if (p == P_)                                                                                 \
+    kern = encode ? reinterpret_cast<const void*>(&k_rdp_encode<kPtrCap, P_>)                  \
+                  : reinterpret_cast<const void*>(&k_rdp_recover<kPtrCap, P_>);
+  GS_RDP_PRIMES(GS_RDP_PICK)
+#undef GS_RDP_PICK
+  if (!kern) return fail(GS_UNSUPPORTED, "rdp: no kernel for p = %d", p);
   const int occ = blocks_per_sm(dev, kern, smem, kRdpThreads);
   std::vector<const void*> ptrs;
   for (int s0 = 0; s0 < n_stripes; s0 += per) {
@@ -523,10 +529,15 @@ int run_rdp(const gs_codec* c, int n_stripes, SlotFn slot_ptr, OutFn out_ptr, ui
     PtrTable<kPtrCap> tab;
     for (int i = 0; i < cnt * stride; ++i) tab.p[i] = static_cast<const uint8_t*>(ptrs[i]);
     const int grid = static_cast<int>(std::min<uint64_t>(ntiles, static_cast<uint64_t>(occ) * sms));
-    if (encode)
-      k_rdp_encode<kPtrCap><<<grid, kRdpThreads, smem, st>>>(tab, g);
-    else
-      k_rdp_recover<kPtrCap><<<grid, kRdpThreads, smem, st>>>(tab, g, c->n_out, in_slots);
+#define GS_RDP_LAUNCH(P_)                                                                      \
+  if (p == P_) {                                                                               \
+    if (encode)                                                                                \
+      k_rdp_encode<kPtrCap, P_><<<grid, kRdpThreads, smem, st>>>(tab, g);                      \
+    else                                                                                       \
+      k_rdp_recover<kPtrCap, P_><<<grid, kRdpThreads, smem, st>>>(tab, g, c->n_out, in_slots); \
+  }
+    GS_RDP_PRIMES(GS_RDP_LAUNCH)
+#undef GS_RDP_LAUNCH
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return fail(GS_CUDA_ERROR, "rdp kernel launch: %s", cudaGetErrorString(e));
     g_launches.fetch_add(1, std::memory_order_relaxed);

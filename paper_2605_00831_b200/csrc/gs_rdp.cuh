@@ -27,6 +27,9 @@ namespace gsb {
 constexpr int kRdpThreads = 256;  // one dstripe per thread per tile
 constexpr int kRdpMaxCols = 24;   // p <= 23 -> n <= 22 on this path
 
+// Primes with kernels (p = smallest prime >= n+1 for n = 1..22).
+#define GS_RDP_PRIMES(X) X(3) X(5) X(7) X(11) X(13) X(17) X(19) X(23)
+
 struct RdpGeom {
   int n, p, rows;
   uint64_t len;       // bytes of this launch's range (per column)
@@ -75,14 +78,18 @@ __device__ __forceinline__ void rdp_store(uint8_t* dst, const uint8_t* src, uint
 }
 
 // Encode: out0 = row parity (whole range), out1 = diagonal parity (whole
-// dstripes) + Q (tail). smem: n data tiles + row tile + diag tile.
-template <int CAP>
+// dstripes) + Q (tail). smem: p-1 column tiles (virtual columns n..p-2 are
+// zero, so the diagonal loop is the same for every n) + row + diag tiles.
+// P is a template parameter: every index in the diagonal loop is a
+// compile-time constant and the 90-odd byte XORs per dstripe fully unroll.
+template <int CAP, int P>
 __global__ void __launch_bounds__(kRdpThreads) k_rdp_encode(const PtrTable<CAP> tab, const RdpGeom g) {
   extern __shared__ __align__(16) uint8_t sm[];
-  const int rows = g.rows, p = g.p, n = g.n;
-  const uint32_t T = static_cast<uint32_t>(rows) * kRdpThreads;
+  constexpr int R = P - 1;
+  constexpr uint32_t T = static_cast<uint32_t>(R) * kRdpThreads;
+  const int n = g.n;
   uint8_t* data = sm;
-  uint8_t* rowp = sm + static_cast<size_t>(n) * T;
+  uint8_t* rowp = sm + static_cast<size_t>(R) * T;
   uint8_t* diag = rowp + T;
   for (uint32_t t = blockIdx.x; t < g.ntiles; t += gridDim.x) {
     const uint32_t s = t / g.tps;
@@ -91,6 +98,9 @@ __global__ void __launch_bounds__(kRdpThreads) k_rdp_encode(const PtrTable<CAP> 
     const int base = static_cast<int>(s) * g.stride;
     __syncthreads();  // previous tile's smem fully consumed
     for (int c = 0; c < n; ++c) rdp_load(data + static_cast<size_t>(c) * T, tab.p[base + c] + off, bytes, T, g.aligned);
+    for (int c = n; c < R; ++c)
+      for (uint32_t v = threadIdx.x; v < T / 16; v += blockDim.x)
+        reinterpret_cast<uint4*>(data + static_cast<size_t>(c) * T)[v] = make_uint4(0, 0, 0, 0);
     __syncthreads();
     for (uint32_t v16 = threadIdx.x; v16 < T / 16; v16 += blockDim.x) {  // T = rows * 256: 16-B multiple
       uint4 v = make_uint4(0, 0, 0, 0);
@@ -106,22 +116,26 @@ __global__ void __launch_bounds__(kRdpThreads) k_rdp_encode(const PtrTable<CAP> 
     __syncthreads();
     // one dstripe per thread
     const uint64_t abs0 = g.logical0 + off;
-    const uint32_t q = threadIdx.x;
-    const uint32_t sb = q * rows;
+    const uint32_t sb = threadIdx.x * R;
     if (sb < bytes) {
-      if (abs0 + sb + rows <= g.full) {
-        for (int d = 0; d < rows; ++d) {
+      if (abs0 + sb + R <= g.full) {
+        uint8_t dv[R];
+#pragma unroll
+        for (int d = 0; d < R; ++d) {
           uint8_t v = 0;
-          for (int c = 0; c < n; ++c) {
-            const int r = pmod(d - c, p);
-            if (r != p - 1) v ^= data[static_cast<size_t>(c) * T + sb + r];
+#pragma unroll
+          for (int c = 0; c < R; ++c) {
+            const int r = (d - c + P) % P;
+            if (r != P - 1) v ^= data[static_cast<size_t>(c) * T + sb + r];
           }
-          const int r = pmod(d + 1, p);  // row-parity column p-1
-          if (r != p - 1) v ^= rowp[sb + r];
-          diag[sb + d] = v;
+          const int r = (d + 1) % P;  // row-parity column p-1
+          if (r != P - 1) v ^= rowp[sb + r];
+          dv[d] = v;
         }
+#pragma unroll
+        for (int d = 0; d < R; ++d) diag[sb + d] = dv[d];
       } else {  // tail bytes (only in the range's last tile): Q parity
-        for (uint32_t x = sb; x < bytes && x < sb + rows; ++x) {
+        for (uint32_t x = sb; x < bytes && x < sb + R; ++x) {
           uint8_t v = 0;
           for (int c = 0; c < n; ++c) v ^= gf_mul_dev(exp2_of(c), data[static_cast<size_t>(c) * T + x]);
           diag[x] = v;
@@ -138,12 +152,13 @@ __global__ void __launch_bounds__(kRdpThreads) k_rdp_encode(const PtrTable<CAP> 
 // stripe: data 0..n-1 (NULL if lost), row parity (NULL if lost), diagonal;
 // outputs: the lost data columns (ascending). smem: p column tiles (array
 // order, lost ones are the outputs being built, virtual ones zero) + diag.
-template <int CAP>
+template <int CAP, int P>
 __global__ void __launch_bounds__(kRdpThreads) k_rdp_recover(const PtrTable<CAP> tab, const RdpGeom g, int n_out,
                                                              int out0) {
   extern __shared__ __align__(16) uint8_t sm[];
-  const int rows = g.rows, p = g.p, n = g.n;
-  const uint32_t T = static_cast<uint32_t>(rows) * kRdpThreads;
+  constexpr int p = P, rows = P - 1;
+  constexpr uint32_t T = static_cast<uint32_t>(rows) * kRdpThreads;
+  const int n = g.n;
   uint8_t* col = sm;                                   // p tiles
   uint8_t* diag = sm + static_cast<size_t>(p) * T;
   const int i = g.li, j = g.lj;
@@ -157,7 +172,8 @@ __global__ void __launch_bounds__(kRdpThreads) k_rdp_recover(const PtrTable<CAP>
       uint8_t* dst = col + static_cast<size_t>(c) * T;
       const uint8_t* src = c < n ? tab.p[base + c] : (c == p - 1 ? tab.p[base + n] : nullptr);
       if (c == i || c == j || src == nullptr) {
-        for (uint32_t b = threadIdx.x; b < T; b += blockDim.x) dst[b] = 0;
+        for (uint32_t v = threadIdx.x; v < T / 16; v += blockDim.x)
+          reinterpret_cast<uint4*>(dst)[v] = make_uint4(0, 0, 0, 0);
       } else {
         rdp_load(dst, src + off, bytes, T, g.aligned);
       }
@@ -180,6 +196,7 @@ __global__ void __launch_bounds__(kRdpThreads) k_rdp_recover(const PtrTable<CAP>
           while (d != p - 1) {
             const int r = pmod(d - prim, p);
             uint8_t v = diag[sb + d];
+#pragma unroll
             for (int c = 0; c < p; ++c) {
               if (c == prim) continue;
               const int rc = pmod(d - c, p);
@@ -187,6 +204,7 @@ __global__ void __launch_bounds__(kRdpThreads) k_rdp_recover(const PtrTable<CAP>
             }
             po[r] = v;
             uint8_t w = 0;
+#pragma unroll
             for (int c = 0; c < p; ++c)
               if (c != part) w ^= col[static_cast<size_t>(c) * T + sb + r];
             qo[r] = w;
