@@ -28,7 +28,7 @@ constexpr int kRdpThreads = 256;  // one dstripe per thread per tile
 constexpr int kRdpMaxCols = 24;   // p <= 23 -> n <= 22 on this path
 
 // Primes with kernels (p = smallest prime >= n+1 for n = 1..22).
-#define GS_RDP_PRIMES(X) X(3) X(5) X(7) X(11) X(13) X(17) X(19) X(23)
+#define GS_RDP_PRIMES(X) X(2) X(3) X(5) X(7) X(11) X(13) X(17) X(19) X(23)
 
 struct RdpGeom {
   int n, p, rows;
