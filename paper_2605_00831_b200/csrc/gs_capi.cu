@@ -634,7 +634,17 @@ int issue_copies(std::vector<CopyOp>& ops, cudaMemcpyKind kind, cudaStream_t st)
         while (j < merged.size() && merged[j].key == a.key && merged[j].bytes == a.bytes &&
                merged[j].dst == merged[j - 1].dst + dp && merged[j].src == merged[j - 1].src + sp)
           ++j;
-        GS_CUDA(cudaMemcpy2DAsync(a.dst, dp, a.src, sp, a.bytes, j - i, kind, st));
+        // A constant-pitch run can still straddle two allocations (e.g. pinned
+        // slabs that happen to be adjacent in VA space); the driver rejects
+        // that up front, and the rows then go as 1-D copies.
+        cudaError_t e2 = cudaMemcpy2DAsync(a.dst, dp, a.src, sp, a.bytes, j - i, kind, st);
+        if (e2 == cudaErrorInvalidValue) {
+          cudaGetLastError();
+          for (size_t r = i; r < j; ++r)
+            GS_CUDA(cudaMemcpyAsync(merged[r].dst, merged[r].src, merged[r].bytes, kind, st));
+        } else {
+          GS_CUDA(e2);
+        }
         i = j;
         continue;
       }
