@@ -548,14 +548,12 @@ def host_tier_checkpoint(torch, dev, ring, scheme, pipe, comp, copy, args):
              for b in range(RING_BLOCKS)]
 
     def one(b):
-        dst = []
-        for s in range(S):
-            ptrs = store.reserve(s, b, scheme, BLOCK_TOKENS, SLICE)
-            dst.extend(ptrs)
+        keys = [(s, b) for s in range(S)]
+        acc, dst = store.reserve_batch(keys, scheme, BLOCK_TOKENS, SLICE)
+        assert acc == S
         check(L.lib().gs_encode_offload(pipe.handle, enc.handle, S, slots[b % RING_BLOCKS], L.ptr_array(dst), SLICE,
                                         comp.cuda_stream, copy.cuda_stream), "host tier")
-        for s in range(S):
-            store.commit(s, b, copy)
+        store.commit_batch(keys, copy)
 
     # warm pass: pinned slabs are allocated once (cudaHostAlloc ~ms per call),
     # then recycled through the store's free lists

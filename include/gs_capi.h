@@ -221,6 +221,14 @@ int gs_store_destroy(gs_store* s);
 int gs_store_reserve(gs_store* s, uint64_t request_id, uint32_t chunk, int kind, int n, int k,
                      uint32_t valid_tokens, uint64_t slice_len, int* accepted, void** parity_out);
 int gs_store_commit(gs_store* s, uint64_t request_id, uint32_t chunk, void* stream);
+/* Batched forms for a decode block's S requests: one host callback seals
+ * the whole batch; reserve_batch stops at the first back-pressure refusal
+ * (*accepted = entries reserved). parity_out[i*k + j]. */
+int gs_store_reserve_batch(gs_store* s, int count, const uint64_t* request_ids, const uint32_t* chunks, int kind,
+                           int n, int k, uint32_t valid_tokens, uint64_t slice_len, int* accepted,
+                           void** parity_out);
+int gs_store_commit_batch(gs_store* s, int count, const uint64_t* request_ids, const uint32_t* chunks,
+                          void* stream);
 int gs_store_wait_sealed(gs_store* s);
 /* Copying put (reference try_put): sealed != 0 keeps `checksum` as given. */
 int gs_store_put(gs_store* s, uint64_t request_id, uint32_t chunk, int kind, int n, int k,

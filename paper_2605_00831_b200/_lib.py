@@ -64,6 +64,8 @@ SIGNATURES = {
     "gs_store_destroy": (_i, [_vp]),
     "gs_store_reserve": (_i, [_vp, _u64, _u32, _i, _i, _i, _u32, _u64, _ip, _vpp]),
     "gs_store_commit": (_i, [_vp, _u64, _u32, _vp]),
+    "gs_store_reserve_batch": (_i, [_vp, _i, _u64p, C.POINTER(C.c_uint32), _i, _i, _i, _u32, _u64, _ip, _vpp]),
+    "gs_store_commit_batch": (_i, [_vp, _i, _u64p, C.POINTER(C.c_uint32), _vp]),
     "gs_store_wait_sealed": (_i, [_vp]),
     "gs_store_put": (_i, [_vp, _u64, _u32, _i, _i, _i, _u32, _u64, _vpp, _u64, _i, _ip]),
     "gs_store_get": (_i, [_vp, _u64, _u32, _i, _ip, _vpp, _u64p, C.POINTER(C.c_uint32), _u64p, _ip]),

@@ -293,8 +293,7 @@ class Checkpointer:
             check(L.lib().gs_encode_offload(self.pipe.handle, encoder(sch).handle, len(keys), L.ptr_array(slots),
                                             L.ptr_array(dsts), self.slice, self.compute.cuda_stream,
                                             self.copy.cuda_stream), "checkpoint")
-            for k in keys:
-                self.store.commit(k[0], k[1], self.copy)
+            self.store.commit_batch(keys, self.copy)   # one host callback seals the batch
         dt = time.perf_counter() - t0
         for o in outs:
             o.enqueue_s = dt / max(len(outs), 1)

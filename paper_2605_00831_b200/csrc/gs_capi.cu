@@ -19,6 +19,7 @@
 
 #include "../../include/gs_capi.h"
 #include "gs_field.hpp"
+#include "gs_fnv.hpp"
 #include "gs_kernels.cuh"
 #include "gs_kv.cuh"
 #include "gs_rdp.cuh"
@@ -1318,11 +1319,20 @@ int gs_parity_checksum_batch(const void* const* parity, int n_chunks, int k, siz
   if (n_chunks < 0 || k < 1 || !out || (n_chunks > 0 && !parity))
     return fail(GS_INVALID_ARGUMENT, "checksum_batch: bad arguments");
   if (threads < 1) threads = 1;
-  threads = std::min(threads, std::max(1, n_chunks));
+  const int groups = (n_chunks + 3) / 4;  // four chunks advanced in lockstep per thread
+  threads = std::min(threads, std::max(1, groups));
   std::atomic<int> next{0};
   auto work = [&] {
-    for (int c = next.fetch_add(1); c < n_chunks; c = next.fetch_add(1))
-      out[c] = gs_parity_checksum(parity + static_cast<size_t>(c) * k, k, len);
+    for (int g = next.fetch_add(1); g < groups; g = next.fetch_add(1)) {
+      const int c0 = 4 * g, m = std::min(4, n_chunks - c0);
+      uint64_t h[4] = {kFnvOffset, kFnvOffset, kFnvOffset, kFnvOffset};
+      for (int i = 0; i < k; ++i) {  // chained over the k buffers in order
+        const uint8_t* ps[4];
+        for (int q = 0; q < m; ++q) ps[q] = static_cast<const uint8_t*>(parity[static_cast<size_t>(c0 + q) * k + i]);
+        fnv1a64_x4(ps, m, len, h);
+      }
+      for (int q = 0; q < m; ++q) out[c0 + q] = h[q];
+    }
   };
   std::vector<std::thread> pool;
   for (int t = 1; t < threads; ++t) pool.emplace_back(work);

@@ -1,0 +1,43 @@
+// gs_fnv.hpp -- FNV-1a 64 (parity_store.hpp:19-25), bit-exact, for the
+// host-side parity seal. One chain is a serial xor -> 64-bit multiply per
+// byte (latency-bound, ~0.7 GB/s per core); independent chunks are advanced
+// in lockstep, four per thread, so the multiplier pipelines across chains.
+#pragma once
+
+#include <cstddef>
+#include <cstdint>
+
+namespace gsb {
+
+constexpr uint64_t kFnvOffset = 0xcbf29ce484222325ull;
+constexpr uint64_t kFnvPrime = 0x100000001b3ull;
+
+inline uint64_t fnv1a64_one(const uint8_t* p, size_t len, uint64_t h) {
+  for (size_t i = 0; i < len; ++i) h = (h ^ p[i]) * kFnvPrime;
+  return h;
+}
+
+// h[q] = FNV-1a of p[q][0..len) continued from h[q], for q < m (m <= 4).
+inline void fnv1a64_x4(const uint8_t* const* p, int m, size_t len, uint64_t* h) {
+  if (m == 1) {
+    h[0] = fnv1a64_one(p[0], len, h[0]);
+    return;
+  }
+  const uint8_t* p0 = p[0];
+  const uint8_t* p1 = m > 1 ? p[1] : p[0];
+  const uint8_t* p2 = m > 2 ? p[2] : p[0];
+  const uint8_t* p3 = m > 3 ? p[3] : p[0];
+  uint64_t a = h[0], b = m > 1 ? h[1] : 0, c = m > 2 ? h[2] : 0, d = m > 3 ? h[3] : 0;
+  for (size_t i = 0; i < len; ++i) {
+    a = (a ^ p0[i]) * kFnvPrime;
+    b = (b ^ p1[i]) * kFnvPrime;
+    c = (c ^ p2[i]) * kFnvPrime;
+    d = (d ^ p3[i]) * kFnvPrime;
+  }
+  h[0] = a;
+  if (m > 1) h[1] = b;
+  if (m > 2) h[2] = c;
+  if (m > 3) h[3] = d;
+}
+
+}  // namespace gsb

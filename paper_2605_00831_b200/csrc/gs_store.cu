@@ -27,6 +27,7 @@
 #include <vector>
 
 #include "../../include/gs_capi.h"
+#include "gs_fnv.hpp"
 
 namespace gsb {
 void set_last_error(const char* msg);  // gs_capi.cu: shared gs_last_error() slot
@@ -127,38 +128,53 @@ struct gs_store {
   bool stop = false;
   std::atomic<uint64_t> pending{0};
 
+  // Seal workers take up to four pending entries of equal size at a time and
+  // hash them in lockstep (gs_fnv.hpp): FNV-1a chained over the k buffers in
+  // order == FNV over the entry's contiguous k * slice_len bytes
+  // (parity_store.hpp:46-50).
   void worker() {
     for (;;) {
-      Key key;
-      uint8_t* buf = nullptr;
+      Key keys[4];
+      const uint8_t* bufs[4];
       uint64_t len = 0;
+      int m = 0, dropped = 0;
       {
         std::unique_lock<std::mutex> lk(mu);
         job_cv.wait(lk, [&] { return stop || !jobs.empty(); });
         if (stop && jobs.empty()) return;
-        key = jobs.front();
-        jobs.pop_front();
-        auto it = entries.find(key);
-        if (it == entries.end()) {
-          --pending;
-          lk.unlock();
-          sealed_cv.notify_all();
-          continue;
+        while (!jobs.empty() && m < 4) {
+          const Key key = jobs.front();
+          auto it = entries.find(key);
+          if (it == entries.end()) {
+            jobs.pop_front();
+            ++dropped;
+            continue;
+          }
+          if (m > 0 && it->second.payload() != len) break;
+          jobs.pop_front();
+          len = it->second.payload();
+          keys[m] = key;
+          bufs[m] = it->second.buf;
+          ++m;
         }
-        buf = it->second.buf;
-        len = it->second.payload();
+        pending -= static_cast<uint64_t>(dropped);
       }
-      // parity_store.hpp:46-50: FNV chained over the k buffers in order ==
-      // FNV over the contiguous k * slice_len bytes.
-      const uint64_t h = fnv_chain(buf, len, 0xcbf29ce484222325ull);
+      if (m == 0) {
+        sealed_cv.notify_all();
+        continue;
+      }
+      uint64_t h[4] = {gsb::kFnvOffset, gsb::kFnvOffset, gsb::kFnvOffset, gsb::kFnvOffset};
+      if (len) gsb::fnv1a64_x4(bufs, m, len, h);
       {
         std::lock_guard<std::mutex> lk(mu);
-        auto it = entries.find(key);
-        if (it != entries.end()) {
-          it->second.checksum = h;
-          it->second.sealed = true;
+        for (int q = 0; q < m; ++q) {
+          auto it = entries.find(keys[q]);
+          if (it != entries.end()) {
+            it->second.checksum = h[q];
+            it->second.sealed = true;
+          }
         }
-        --pending;
+        pending -= static_cast<uint64_t>(m);
       }
       sealed_cv.notify_all();
     }
@@ -166,15 +182,15 @@ struct gs_store {
 
   struct HostJob {
     gs_store* s;
-    Key key;
+    std::vector<Key> keys;
   };
   static void CUDART_CB on_stream(void* p) {
     auto* j = static_cast<HostJob*>(p);
     {
       std::lock_guard<std::mutex> lk(j->s->mu);
-      j->s->jobs.push_back(j->key);
+      for (const auto& k : j->keys) j->s->jobs.push_back(k);
     }
-    j->s->job_cv.notify_one();
+    j->s->job_cv.notify_all();
     delete j;
   }
 
@@ -239,30 +255,57 @@ int gs_store_reserve(gs_store* s, uint64_t request_id, uint32_t chunk, int kind,
   return GS_OK;
 }
 
-int gs_store_commit(gs_store* s, uint64_t request_id, uint32_t chunk, void* stream) {
-  if (!s) return sfail(GS_INVALID_ARGUMENT, "store_commit: NULL store");
+int gs_store_commit_batch(gs_store* s, int count, const uint64_t* request_ids, const uint32_t* chunks,
+                          void* stream) {
+  if (!s || count < 0 || (count > 0 && (!request_ids || !chunks)))
+    return sfail(GS_INVALID_ARGUMENT, "store_commit: bad arguments");
+  if (count == 0) return GS_OK;
+  auto* job = new gs_store::HostJob{s, {}};
+  job->keys.reserve(static_cast<size_t>(count));
   {
     std::lock_guard<std::mutex> lk(s->mu);
-    if (!s->entries.count({request_id, chunk}))
-      return sfail(GS_INVALID_ARGUMENT, "store_commit: no reserved entry for request %llu chunk %u",
-                   static_cast<unsigned long long>(request_id), chunk);
-    ++s->pending;
+    for (int i = 0; i < count; ++i) {
+      if (!s->entries.count({request_ids[i], chunks[i]})) {
+        delete job;
+        return sfail(GS_INVALID_ARGUMENT, "store_commit: no reserved entry for request %llu chunk %u",
+                     static_cast<unsigned long long>(request_ids[i]), chunks[i]);
+      }
+      job->keys.push_back({request_ids[i], chunks[i]});
+    }
+    s->pending += static_cast<uint64_t>(count);
   }
-  if (stream) {
-    auto* job = new gs_store::HostJob{s, {request_id, chunk}};
+  if (stream) {  // seal once the D2H on `stream` has landed; one host callback per batch
     cudaError_t e = cudaLaunchHostFunc(static_cast<cudaStream_t>(stream), &gs_store::on_stream, job);
     if (e != cudaSuccess) {
+      s->pending -= static_cast<uint64_t>(count);
       delete job;
-      --s->pending;
       return sfail(GS_CUDA_ERROR, "store_commit: cudaLaunchHostFunc: %s", cudaGetErrorString(e));
     }
     return GS_OK;
   }
-  {
-    std::lock_guard<std::mutex> lk(s->mu);
-    s->jobs.push_back({request_id, chunk});
+  gs_store::on_stream(job);
+  return GS_OK;
+}
+
+int gs_store_commit(gs_store* s, uint64_t request_id, uint32_t chunk, void* stream) {
+  return gs_store_commit_batch(s, 1, &request_id, &chunk, stream);
+}
+
+// Reserve `count` entries of one scheme / length at once (all-or-nothing on
+// back-pressure: *accepted = number reserved before the first refusal).
+int gs_store_reserve_batch(gs_store* s, int count, const uint64_t* request_ids, const uint32_t* chunks, int kind,
+                           int n, int k, uint32_t valid_tokens, uint64_t slice_len, int* accepted,
+                           void** parity_out) {
+  if (!s || !accepted || count < 0) return sfail(GS_INVALID_ARGUMENT, "store_reserve: bad arguments");
+  *accepted = 0;
+  for (int i = 0; i < count; ++i) {
+    int acc = 0;
+    if (int st = gs_store_reserve(s, request_ids[i], chunks[i], kind, n, k, valid_tokens, slice_len, &acc,
+                                  parity_out ? parity_out + static_cast<size_t>(i) * k : nullptr))
+      return st;
+    if (!acc) return GS_OK;
+    ++*accepted;
   }
-  s->job_cv.notify_one();
   return GS_OK;
 }
 

@@ -147,6 +147,26 @@ class ParityStore:
             return None
         return [ptrs[i] for i in range(scheme.k)]
 
+    def reserve_batch(self, keys, scheme: CodingScheme, valid_tokens: int, slice_len: int):
+        """Reserve [(request, chunk), ...] at once; returns (accepted count,
+        flat list of pinned parity pointers, k per accepted entry)."""
+        n = len(keys)
+        req = (C.c_uint64 * max(n, 1))(*[r for r, _ in keys])
+        chk = (C.c_uint32 * max(n, 1))(*[c for _, c in keys])
+        acc = C.c_int()
+        ptrs = (C.c_void_p * max(n * scheme.k, 1))()
+        check(L.lib().gs_store_reserve_batch(self.handle, n, req, chk, int(scheme.kind), scheme.n, scheme.k,
+                                             valid_tokens, slice_len, C.byref(acc), ptrs), "parity store")
+        return acc.value, [ptrs[i] for i in range(acc.value * scheme.k)]
+
+    def commit_batch(self, keys, stream=None) -> None:
+        """Seal many entries once `stream` reaches this point (one callback)."""
+        n = len(keys)
+        req = (C.c_uint64 * max(n, 1))(*[r for r, _ in keys])
+        chk = (C.c_uint32 * max(n, 1))(*[c for _, c in keys])
+        st = None if stream is None else int(getattr(stream, "cuda_stream", stream))
+        check(L.lib().gs_store_commit_batch(self.handle, n, req, chk, st), "parity store")
+
     def commit(self, request_id: int, chunk_id: int, stream=None) -> None:
         """Seal once `stream` (the copy stream of the D2H) reaches this point."""
         st = None if stream is None else int(getattr(stream, "cuda_stream", stream))
