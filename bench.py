@@ -539,7 +539,8 @@ def host_tier_checkpoint(torch, dev, ring, scheme, pipe, comp, copy, args):
     from paper_2605_00831_b200.coding import check, encoder
     from paper_2605_00831_b200.parity_store import ParityStore
 
-    threads = os.cpu_count() or 1
+    # leave two cores for the CUDA callback thread and the submitting thread
+    threads = max(1, (os.cpu_count() or 1) - 2)
     S = ring.shape[1]
     store = ParityStore(seal_threads=threads)
     enc = encoder(scheme)
