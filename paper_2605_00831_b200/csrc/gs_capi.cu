@@ -564,7 +564,7 @@ struct gs_pipeline {
 
 namespace {
 
-constexpr uint64_t kHostPiece = 2ull << 20;
+constexpr uint64_t kHostPiece = 1ull << 20;
 
 struct DeviceGuard {
   int prev = -1;
