@@ -111,12 +111,19 @@ int gs_apply_device(const gs_codec* c, int n_stripes, const void* const* slots,
 
 /* ---- paged KV cache ------------------------------------------
  * A slice in the reference byte order [K,V][layer][token][H*D/tp]
- * (kv_layout.hpp:59-68) read straight out of a paged KV cache: page (t, l) of
- * the chunk's block lives at  base + l*layer_stride + t*kv_stride  (the
- * per-stripe base pointer already includes the block's offset); each page is
- * page_bytes = block tokens * token_bytes. Tokens >= valid_tokens of a page
- * read as zero (pad_partial, kv_layout.hpp:73-84) and are never written.
- * Sizes and strides are multiples of 16. */
+ * (kv_layout.hpp:59-68) read straight out of a paged KV cache. The slice is
+ * 2*layers segments of page_bytes = chunk tokens * token_bytes; segment
+ * (t, l) lives at  base + l*layer_stride + t*kv_stride  plus the block:
+ *  - block_table == NULL: the chunk is one cache block and each per-stripe
+ *    base pointer already includes the block's offset;
+ *  - block_table != NULL (device int32 [stripes][table_stride]): the chunk
+ *    spans page_bytes / block_bytes blocks; block i of stripe s is
+ *    block_table[s*table_stride + i] at offset block * block_bytes (the same
+ *    ids for every layer and for K and V, as in vLLM-style caches), and the
+ *    per-stripe base pointers are the worker's cache base.
+ * Tokens >= valid_tokens of a segment read as zero (pad_partial,
+ * kv_layout.hpp:73-84) and are never written. Sizes and strides are
+ * multiples of 16. */
 typedef struct {
   uint32_t page_bytes;
   uint32_t layers;
@@ -124,6 +131,9 @@ typedef struct {
   uint32_t valid_tokens;
   uint64_t layer_stride;
   uint64_t kv_stride;
+  const int32_t* block_table;
+  uint32_t block_bytes;
+  uint32_t table_stride;
 } gs_page_map;
 /* gs_apply_device with slots whose bit is set in paged_slot_mask read through
  * src_map and (dst_map != NULL) outputs scattered through dst_map. */

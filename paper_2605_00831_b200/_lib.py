@@ -120,7 +120,8 @@ class PageMap(C.Structure):
     """gs_page_map (include/gs_capi.h)."""
 
     _fields_ = [("page_bytes", C.c_uint32), ("layers", C.c_uint32), ("token_bytes", C.c_uint32),
-                ("valid_tokens", C.c_uint32), ("layer_stride", C.c_uint64), ("kv_stride", C.c_uint64)]
+                ("valid_tokens", C.c_uint32), ("layer_stride", C.c_uint64), ("kv_stride", C.c_uint64),
+                ("block_table", C.c_void_p), ("block_bytes", C.c_uint32), ("table_stride", C.c_uint32)]
 
 
 def last_error() -> str:

@@ -310,6 +310,7 @@ struct Paging {
   uint32_t paged_slots = 0;
   uint64_t logical0 = 0;
   uint64_t total_len = 0;  // RDP: absolute column length (0 = this launch's len)
+  uint64_t stripe0 = 0;    // absolute index of stripe 0 of this call (block-table rows)
   PageMap src{};
   PageMap dst{};
   bool any() const { return paged_slots != 0 || dst.page_bytes != 0; }
@@ -324,6 +325,9 @@ PageMap to_map(const gs_page_map* m) {
     r.valid_tokens = m->valid_tokens;
     r.layer_stride = m->layer_stride;
     r.kv_stride = m->kv_stride;
+    r.table = m->block_table;
+    r.block_bytes = m->block_table ? m->block_bytes : m->page_bytes;
+    r.table_stride = m->table_stride;
   }
   return r;
 }
@@ -335,6 +339,9 @@ int check_page_map(const PageMap& m, const char* what) {
     return fail(GS_INVALID_ARGUMENT, "%s page map: page/token bytes and strides must be multiples of 16", what);
   if (static_cast<uint64_t>(m.valid_tokens) * m.token_bytes > m.page_bytes)
     return fail(GS_INVALID_ARGUMENT, "kv: valid_tokens exceeds chunk size");
+  if (m.table && (m.block_bytes == 0 || m.block_bytes % kVec || m.page_bytes % m.block_bytes ||
+                  m.block_bytes % m.token_bytes || m.table_stride < m.page_bytes / m.block_bytes))
+    return fail(GS_INVALID_ARGUMENT, "%s page map: block_bytes must divide the segment and the table must cover it", what);
   return GS_OK;
 }
 
@@ -412,6 +419,8 @@ int run_codec(const gs_codec* c, int n_stripes, SlotFn slot_ptr, OutFn out_ptr, 
       if (total > 0xFFFFFFFFull) return fail(GS_INVALID_ARGUMENT, "apply: too many tiles in one launch");
       TileGeom g{body, static_cast<uint32_t>(tps64), static_cast<uint32_t>(total), stride, c->n_slots, 1,
                  pg.paged_slots, pg.logical0, pg.src, pg.dst};
+      if (g.src.table) g.src.table += (pg.stripe0 + s0) * g.src.table_stride;
+      if (g.dst.table) g.dst.table += (pg.stripe0 + s0) * g.dst.table_stride;
       const int grid = static_cast<int>(std::min<uint64_t>(total, static_cast<uint64_t>(occ) * sms));
       cudaError_t e = use_bulk ? c->special->launch_bulk(ptrs.data(), cnt * stride, g, grid, st, stages, smem)
                       : paged  ? c->special->launch_paged(ptrs.data(), cnt * stride, g, grid, st)
@@ -451,6 +460,8 @@ int run_codec(const gs_codec* c, int n_stripes, SlotFn slot_ptr, OutFn out_ptr, 
       const int kb = std::min(kMaxGenericRows, c->n_out - r0);
       TileGeom g{glen, static_cast<uint32_t>(tps64), static_cast<uint32_t>(total), stride, ns + r0,
                  galigned ? 1 : 0, gpaged, pg.logical0 + done, pg.src, pg.dst};
+      if (g.src.table) g.src.table += (pg.stripe0 + s0) * g.src.table_stride;
+      if (g.dst.table) g.dst.table += (pg.stripe0 + s0) * g.dst.table_stride;
       const size_t smem = static_cast<size_t>(kb) * ns * sizeof(CoefWords);
       const int occ = blocks_per_sm(dev, generic_kernel(kb), smem);
       const int grid = static_cast<int>(std::min<uint64_t>(total, static_cast<uint64_t>(occ) * sms));
@@ -1039,6 +1050,7 @@ static int encode_offload(gs_pipeline* p, const gs_codec* c, int n_stripes, cons
       Paging pg;
       pg.logical0 = r0;
       pg.total_len = len;
+      pg.stripe0 = static_cast<uint64_t>(s0);
       if (src_map) {
         pg.src = to_map(src_map);
         pg.paged_slots = N >= 32 ? ~0u : (1u << N) - 1;
@@ -1125,6 +1137,7 @@ static int reconstruct_upload(gs_pipeline* p, const gs_codec* c, int n_stripes, 
       Paging pg;
       pg.logical0 = r0;
       pg.total_len = len;
+      pg.stripe0 = static_cast<uint64_t>(s0);
       if (src_map) {
         pg.src = to_map(src_map);
         pg.paged_slots = n >= 32 ? ~0u : (1u << n) - 1;  // data slots; parity comes from staging

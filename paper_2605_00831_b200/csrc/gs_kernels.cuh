@@ -103,12 +103,16 @@ __device__ __forceinline__ void st_partial(uint8_t* p, const uint4& v, int nbyte
 // consecutive CTAs stream consecutive 4 KiB pieces of the same shards.
 
 // Paged KV addressing. A slice in the reference byte order
-// [K,V][layer][token][elems] (kv_layout.hpp:59-68) lives in a paged KV cache
-// as 2*layers pages of page_bytes (= block_size tokens x token_bytes): page
-// (t, l) of a block sits at  base + l*layer_stride + t*kv_stride, where the
-// per-stripe base already includes the block's offset. Tokens >= valid_tokens
-// of each page read as zero (pad_partial, kv_layout.hpp:73-84) and are not
-// written back. page_bytes == 0 means contiguous slices.
+// [K,V][layer][token][elems] (kv_layout.hpp:59-68) is 2*layers segments of
+// page_bytes = chunk tokens x token_bytes; segment (t, l) lives in a paged KV
+// cache at  base + l*layer_stride + t*kv_stride  (+ the block). Two modes:
+//  * single block (table == nullptr): the chunk is one cache block and the
+//    per-stripe base already includes the block's offset;
+//  * block table: the chunk spans page_bytes / block_bytes cache blocks;
+//    block i of stripe s is table[s * table_stride + i] (the same ids in every
+//    layer and for K and V, as in vLLM-style caches), at block * block_bytes.
+// Tokens >= valid_tokens of each segment read as zero (pad_partial,
+// kv_layout.hpp:73-84) and are never written. page_bytes == 0: contiguous.
 struct PageMap {
   uint32_t page_bytes;
   uint32_t layers;
@@ -116,6 +120,9 @@ struct PageMap {
   uint32_t valid_tokens;
   uint64_t layer_stride;
   uint64_t kv_stride;
+  const int32_t* table;
+  uint32_t block_bytes;
+  uint32_t table_stride;
 };
 
 struct TileGeom {
@@ -131,37 +138,52 @@ struct TileGeom {
   PageMap dst;           // mapping of the outputs (dst.page_bytes == 0: contiguous)
 };
 
-// Offset of logical slice byte `o` inside a paged slot; `masked` = beyond
-// the valid tokens of its page.
-__device__ __forceinline__ uint64_t paged_offset(const PageMap& m, uint64_t logical, bool& masked);
-
-// Same for the byte `tile_logical + lane_off` of a CTA tile: when the tile
-// sits inside one page (pages are multiples of the 4 KiB tile -- every
-// paged cache geometry of the configs), the page arithmetic is CTA-uniform
-// and only an add + compare remain per thread.
-__device__ __forceinline__ uint64_t paged_offset_tile(const PageMap& m, uint64_t tile_logical, uint32_t lane_off,
-                                                      bool& masked) {
-  const uint32_t u = static_cast<uint32_t>(tile_logical);
-  const uint32_t q = u / m.page_bytes;
-  const uint32_t in0 = u - q * m.page_bytes;
-  if (in0 + static_cast<uint32_t>(kTile) <= m.page_bytes) {
-    const uint32_t t = q / m.layers;
-    const uint32_t l = q - t * m.layers;
-    const uint32_t in = in0 + lane_off;
-    masked = in >= m.valid_tokens * m.token_bytes;
-    return static_cast<uint64_t>(l) * m.layer_stride + static_cast<uint64_t>(t) * m.kv_stride + in;
-  }
-  return paged_offset(m, tile_logical + lane_off, masked);
-}
-
-__device__ __forceinline__ uint64_t paged_offset(const PageMap& m, uint64_t logical, bool& masked) {
+// Offset of logical slice byte `logical` of stripe `s` inside a paged slot;
+// `masked` = beyond the valid tokens of its segment.
+__device__ __forceinline__ uint64_t paged_offset(const PageMap& m, uint32_t s, uint64_t logical, bool& masked) {
   const uint32_t o = static_cast<uint32_t>(logical);
   const uint32_t q = o / m.page_bytes;
   const uint32_t in = o - q * m.page_bytes;
   const uint32_t t = q / m.layers;
   const uint32_t l = q - t * m.layers;
   masked = in >= m.valid_tokens * m.token_bytes;
-  return static_cast<uint64_t>(l) * m.layer_stride + static_cast<uint64_t>(t) * m.kv_stride + in;
+  uint64_t r = static_cast<uint64_t>(l) * m.layer_stride + static_cast<uint64_t>(t) * m.kv_stride;
+  if (m.table) {
+    const uint32_t pi = in / m.block_bytes;
+    const int32_t blk = masked ? 0 : m.table[static_cast<uint64_t>(s) * m.table_stride + pi];
+    r += static_cast<uint64_t>(blk) * m.block_bytes + (in - pi * m.block_bytes);
+  } else {
+    r += in;
+  }
+  return r;
+}
+
+// Same for byte `tile_logical + lane_off` of a CTA tile: when the whole 4 KiB
+// tile sits inside one segment (and one cache block), the page arithmetic and
+// the block-table lookup are CTA-uniform; only an add + compare remain per
+// thread. Every paged geometry of the configs (4 KiB blocks) takes this path.
+__device__ __forceinline__ uint64_t paged_offset_tile(const PageMap& m, uint32_t s, uint64_t tile_logical,
+                                                      uint32_t lane_off, bool& masked) {
+  const uint32_t u = static_cast<uint32_t>(tile_logical);
+  const uint32_t q = u / m.page_bytes;
+  const uint32_t in0 = u - q * m.page_bytes;
+  const uint32_t bb = m.table ? m.block_bytes : m.page_bytes;
+  const uint32_t pi = m.table ? in0 / bb : 0;
+  const uint32_t ib0 = in0 - pi * bb;
+  if (in0 + static_cast<uint32_t>(kTile) <= m.page_bytes && ib0 + static_cast<uint32_t>(kTile) <= bb) {
+    const uint32_t t = q / m.layers;
+    const uint32_t l = q - t * m.layers;
+    const uint32_t in = in0 + lane_off;
+    masked = in >= m.valid_tokens * m.token_bytes;
+    uint64_t r = static_cast<uint64_t>(l) * m.layer_stride + static_cast<uint64_t>(t) * m.kv_stride + ib0 + lane_off;
+    if (m.table) {
+      const bool tile_masked = in0 >= m.valid_tokens * m.token_bytes;  // whole tile beyond valid
+      const int32_t blk = tile_masked ? 0 : m.table[static_cast<uint64_t>(s) * m.table_stride + pi];
+      r += static_cast<uint64_t>(blk) * m.block_bytes;
+    }
+    return r;
+  }
+  return paged_offset(m, s, tile_logical + lane_off, masked);
 }
 
 // ---- specialised back end --------------------------------------------------
@@ -233,8 +255,8 @@ __global__ void __launch_bounds__(kThreads) k_apply_special(const PtrTable<CAP> 
       uint64_t soff = off, doff = off;
       const uint64_t tile_logical = g.logical0 + static_cast<uint64_t>(t - s * g.tps) * kTile;
       const uint32_t lane_off = threadIdx.x * kVec;
-      if (g.paged_slots) soff = paged_offset_tile(g.src, tile_logical, lane_off, smask);
-      if (g.dst.page_bytes) doff = paged_offset_tile(g.dst, tile_logical, lane_off, dmask);
+      if (g.paged_slots) soff = paged_offset_tile(g.src, s, tile_logical, lane_off, smask);
+      if (g.dst.page_bytes) doff = paged_offset_tile(g.dst, s, tile_logical, lane_off, dmask);
 #pragma unroll
       for (int j = 0; j < Spec::NS; ++j) {
         src[j] = make_uint4(0, 0, 0, 0);
@@ -320,11 +342,12 @@ __device__ __forceinline__ void pair_finish(uint32_t accP, uint32_t accQ, uint32
 // loads/stores; otherwise byte-granular (ragged tail / misaligned shards).
 template <int KB, int CAP, bool FULL>
 __device__ __forceinline__ void generic_group(const PtrTable<CAP>& tab, int base, int out0, uint64_t off,
-                                              int nb, const CoefWords* sc, int ns, const TileGeom& g) {
+                                              int nb, const CoefWords* sc, int ns, const TileGeom& g,
+                                              uint32_t stripe) {
   bool smask = false, dmask = false;
   uint64_t soff = off, doff = off;
-  if (FULL && g.paged_slots) soff = paged_offset(g.src, g.logical0 + off, smask);
-  if (FULL && g.dst.page_bytes) doff = paged_offset(g.dst, g.logical0 + off, dmask);
+  if (FULL && g.paged_slots) soff = paged_offset(g.src, stripe, g.logical0 + off, smask);
+  if (FULL && g.dst.page_bytes) doff = paged_offset(g.dst, stripe, g.logical0 + off, dmask);
   uint32_t acc[KB][4];
 #pragma unroll
   for (int r = 0; r < KB; ++r)
@@ -395,10 +418,11 @@ __global__ void __launch_bounds__(kThreads) k_apply_generic(const PtrTable<CAP> 
     if (off >= g.len) continue;
     const int base = static_cast<int>(s) * g.stride;
     if (g.aligned && off + kVec <= g.len) {
-      generic_group<KB, CAP, true>(tab, base, g.out0, off, kVec, sc, ns, g);
+      generic_group<KB, CAP, true>(tab, base, g.out0, off, kVec, sc, ns, g, s);
     } else {
       const uint64_t rem = g.len - off;
-      generic_group<KB, CAP, false>(tab, base, g.out0, off, static_cast<int>(rem < kVec ? rem : kVec), sc, ns, g);
+      generic_group<KB, CAP, false>(tab, base, g.out0, off, static_cast<int>(rem < kVec ? rem : kVec), sc, ns, g,
+                                    s);
     }
   }
 }

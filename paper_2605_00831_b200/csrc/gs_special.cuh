@@ -25,7 +25,7 @@ using BulkLaunchFn = cudaError_t (*)(const void* const* ptrs, int count, const T
 
 // Pointer-table capacity of one launch (pointers + TileGeom fit the classic
 // 4 KiB kernel-parameter space).
-constexpr int kPtrCap = 496;
+constexpr int kPtrCap = 488;
 // 16-byte groups per thread per source per tile of the specialised kernels.
 constexpr int kSpecialU = 1;
 // Consumer warps and 16-byte groups per consumer thread of the bulk variant.

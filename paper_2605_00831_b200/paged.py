@@ -12,8 +12,9 @@ the replacement worker's cache. No staging copy of the KV.
 
 Cache layout per worker: ``[layers, 2 (K,V), num_blocks, block_size, H*D/tp * 2 B]``
 (vLLM's per-layer [2, num_blocks, block_size, heads, dim] stacked over layers).
-One checkpoint chunk = one block (m = block_size, e.g. the 16-token decode
-block of config C2).
+A checkpoint chunk is either one block (``*_blocks``: the 16-token decode
+block of config C2) or several blocks listed in a device block table
+(``*_chunks``: e.g. 2048-token prefill chunks of 16-token blocks).
 """
 from __future__ import annotations
 
@@ -52,11 +53,53 @@ class PagedKVCache:
             raise InvalidArgument("paged: block id out of range")
         return self.buf.data_ptr() + block_id * self.page_bytes
 
-    def page_map(self, valid_tokens: int) -> L.PageMap:
-        if valid_tokens > self.block_size:
-            raise InvalidArgument("kv: valid_tokens exceeds chunk size")
-        return L.PageMap(self.page_bytes, self.model.layers, self.token_bytes, valid_tokens,
-                         self.layer_stride, self.kv_stride)
+    def page_map(self, valid_tokens: int, chunk_tokens: Optional[int] = None,
+                 block_table: Optional[torch.Tensor] = None) -> L.PageMap:
+        """Single-block chunks (chunk == one block), or chunks of
+        `chunk_tokens` spanning several blocks listed per stripe in the device
+        int32 `block_table` [stripes, chunk_tokens // block_size]."""
+        if block_table is None:
+            if valid_tokens > self.block_size:
+                raise InvalidArgument("kv: valid_tokens exceeds chunk size")
+            return L.PageMap(self.page_bytes, self.model.layers, self.token_bytes, valid_tokens,
+                             self.layer_stride, self.kv_stride, None, self.page_bytes, 0)
+        m = chunk_tokens
+        if m is None or m % self.block_size or valid_tokens > m:
+            raise InvalidArgument("paged: chunk must be a whole number of blocks >= valid tokens")
+        if block_table.dtype != torch.int32 or not block_table.is_cuda or block_table.dim() != 2:
+            raise InvalidArgument("paged: block_table must be a CUDA int32 [stripes, blocks] tensor")
+        if block_table.shape[1] < m // self.block_size or block_table.stride(1) != 1:
+            raise InvalidArgument("paged: block_table rows must list every block of the chunk")
+        return L.PageMap(m * self.token_bytes, self.model.layers, self.token_bytes, valid_tokens,
+                         self.layer_stride, self.kv_stride, block_table.data_ptr(), self.page_bytes,
+                         block_table.stride(0))
+
+    def chunk_slice_bytes(self, chunk_tokens: int) -> int:
+        return 2 * self.model.layers * chunk_tokens * self.token_bytes
+
+    def write_chunk(self, blocks: Sequence[int], slice_: torch.Tensor, chunk_tokens: int,
+                    valid_tokens: Optional[int] = None) -> None:
+        """Scatter a reference-layout slice of a multi-block chunk (tests)."""
+        v = chunk_tokens if valid_tokens is None else valid_tokens
+        src = slice_.view(2, self.model.layers, chunk_tokens, self.token_bytes)
+        for i, b in enumerate(blocks):
+            lo = i * self.block_size
+            hi = min(lo + self.block_size, v)
+            if hi > lo:
+                self.buf[:, :, b, :hi - lo] = src.permute(1, 0, 2, 3)[:, :, lo:hi]
+
+    def read_chunk(self, blocks: Sequence[int], chunk_tokens: int, valid_tokens: Optional[int] = None
+                   ) -> torch.Tensor:
+        """Gather a multi-block chunk as a reference-layout slice, zero past `valid`."""
+        v = chunk_tokens if valid_tokens is None else valid_tokens
+        out = torch.zeros((2, self.model.layers, chunk_tokens, self.token_bytes), dtype=torch.uint8,
+                          device=self.buf.device)
+        for i, b in enumerate(blocks):
+            lo = i * self.block_size
+            hi = min(lo + self.block_size, v)
+            if hi > lo:
+                out[:, :, lo:hi] = self.buf[:, :, b, :hi - lo].permute(1, 0, 2, 3)
+        return out.view(-1)
 
     # test / ingest helpers (torch copies, not on the checkpoint path)
     def write_slice(self, block_id: int, slice_: torch.Tensor, valid_tokens: Optional[int] = None) -> None:
@@ -121,6 +164,48 @@ def checkpoint_blocks(pipeline, scheme: CodingScheme, caches: Sequence[PagedKVCa
     check(L.lib().gs_encode_offload_paged(pipeline.handle, encoder(scheme).handle, S, L.ptr_array(slots),
                                           L.ptr_array(dst), caches[0].slice_bytes, C.byref(pm), cs,
                                           _stream(copy) if copy is not None else cs), "checkpoint_blocks")
+
+
+def checkpoint_chunks(pipeline, scheme: CodingScheme, caches: Sequence[PagedKVCache], block_table: torch.Tensor,
+                      chunk_tokens: int, valid_tokens: int, h_parity, compute=None, copy=None) -> None:
+    """Prefill-chunk checkpoint from the paged caches: S chunks of
+    `chunk_tokens`, stripe s made of the blocks block_table[s] (the same ids
+    in every worker's cache, as TP workers allocate in lockstep). K1 gathers
+    the pages in place; parity -> pinned `h_parity` [S, k, slice]."""
+    _check_caches(caches)
+    S = block_table.shape[0]
+    pm = caches[0].page_map(valid_tokens, chunk_tokens, block_table)
+    slots = [caches[j].buf.data_ptr() for s in range(S) for j in range(scheme.n)]
+    dst = [h_parity[s, i].data_ptr() for s in range(S) for i in range(scheme.k)]
+    cs = _stream(compute)
+    check(L.lib().gs_encode_offload_paged(pipeline.handle, encoder(scheme).handle, S, L.ptr_array(slots),
+                                          L.ptr_array(dst), caches[0].chunk_slice_bytes(chunk_tokens), C.byref(pm),
+                                          cs, _stream(copy) if copy is not None else cs), "checkpoint_chunks")
+
+
+def rebuild_chunks(pipeline, scheme: CodingScheme, lost: ErasurePattern, caches: Sequence[Optional[PagedKVCache]],
+                   replacements: Dict[int, PagedKVCache], block_table: torch.Tensor, chunk_tokens: int,
+                   valid_tokens: int, h_parity: torch.Tensor, compute=None, copy=None) -> None:
+    """Recovery of multi-block chunks into the replacement workers' caches
+    (same block ids), survivors read in place, parity H2D'd from pinned."""
+    dec = decoder(scheme, lost)
+    live = [c for j, c in enumerate(caches) if c is not None and not lost.contains(j)]
+    _check_caches(live + list(replacements.values()))
+    S = block_table.shape[0]
+    n, k = scheme.n, scheme.k
+    slots: List[Optional[int]] = []
+    for s in range(S):
+        for j in range(n):
+            slots.append(None if lost.contains(j) else caches[j].buf.data_ptr())
+        for i in range(k):
+            slots.append(None if lost.contains(n + i) else h_parity[s, i].data_ptr())
+    outs = [replacements[w].buf.data_ptr() for s in range(S) for w in dec.out_index]
+    ref = live[0]
+    pm = ref.page_map(valid_tokens, chunk_tokens, block_table)
+    cs = _stream(compute)
+    check(L.lib().gs_reconstruct_upload_paged(pipeline.handle, dec.handle, S, L.ptr_array(slots), L.ptr_array(outs),
+                                              ref.chunk_slice_bytes(chunk_tokens), C.byref(pm), C.byref(pm), cs,
+                                              _stream(copy) if copy is not None else cs), "rebuild_chunks")
 
 
 def rebuild_blocks(pipeline, scheme: CodingScheme, lost: ErasurePattern, caches: Sequence[Optional[PagedKVCache]],

@@ -96,3 +96,52 @@ def test_paged_rejects_bad_geometry():
     cb = PagedKVCache(bad, 4, 3)                       # 3-token pages of 16 B -> 48 B pages: ok (multiple of 16)
     par = torch.empty((1, 1, cb.slice_bytes), dtype=torch.uint8, device="cuda")
     encode_blocks(CodingScheme.xor_code(2), [cb, cb], [[0, 1]], 3, par)
+
+
+@pytest.mark.parametrize("model,block,chunk", [
+    (ModelConfig(32, 8, 128, 2, 8), 16, 64),     # 4 KiB blocks: CTA-uniform table lookups
+    (ModelConfig(2, 8, 8, 2, 8), 16, 128),       # 256 B blocks: per-thread mapping path
+])
+@pytest.mark.parametrize("valid", [None, 37])
+def test_paged_multi_block_chunks_with_block_table(model, block, chunk, valid):
+    from paper_2605_00831_b200.paged import checkpoint_chunks, rebuild_chunks
+    n, k, S = 8, 2, 3
+    v = chunk if valid is None else valid
+    nblk = chunk // block
+    nblocks = S * nblk + 5
+    g = torch.Generator(device="cuda").manual_seed(7)
+    caches = []
+    for j in range(n):
+        c = PagedKVCache(model, nblocks, block)
+        c.buf.copy_(torch.randint(0, 256, c.buf.shape, dtype=torch.uint8, device="cuda", generator=g))
+        caches.append(c)
+    perm = np.random.default_rng(5).permutation(nblocks)[: S * nblk].reshape(S, nblk)
+    table = torch.from_numpy(perm.astype(np.int32)).cuda()
+    truth = []
+    for s in range(S):
+        row = []
+        for j in range(n):
+            sl = make_ground_truth_slice(3, s, 2, j, model, chunk, v, device="cuda")
+            caches[j].write_chunk(perm[s], sl, chunk, v)
+            row.append(sl)
+        truth.append(row)
+    scheme = CodingScheme.reed_solomon(n, k)
+    pipe = D.Pipeline(0, 256 << 10)
+    slice_bytes = caches[0].chunk_slice_bytes(chunk)
+    h_par = torch.zeros((S, k, slice_bytes), dtype=torch.uint8).pin_memory()
+    st = torch.cuda.current_stream()
+    checkpoint_chunks(pipe, scheme, caches, table, chunk, v, h_par, st, st)
+    st.synchronize()
+    for s in range(S):
+        want = O.port().encode(O.RS, n, k, [t.cpu().numpy() for t in truth[s]])
+        for i in range(k):
+            assert np.array_equal(h_par[s, i].numpy(), want[i]), (s, i)
+    lost = ErasurePattern([1, 6])
+    reps = {w: PagedKVCache(model, nblocks, block, fill=0x5A) for w in (1, 6)}
+    rebuild_chunks(pipe, scheme, lost, [None if j in (1, 6) else caches[j] for j in range(n)], reps, table, chunk, v,
+                   h_par, st, st)
+    st.synchronize()
+    for w in (1, 6):
+        for s in range(S):
+            assert torch.equal(reps[w].read_chunk(perm[s], chunk, v), truth[s][w]), (w, s)
+    pipe.close()
