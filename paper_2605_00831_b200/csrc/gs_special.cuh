@@ -29,12 +29,12 @@ constexpr int kPtrCap = 488;
 // 16-byte groups per thread per source per tile of the specialised kernels.
 constexpr int kSpecialU = 1;
 // Consumer warps and 16-byte groups per consumer thread of the bulk variant.
-constexpr int kBulkCW = 8;
+constexpr int kBulkCW = 16;
 constexpr int kBulkU = 1;
 constexpr int kBulkThreads = (kBulkCW + 1) * 32;
 constexpr int kBulkTile = kBulkCW * 32 * kVec * kBulkU;
 constexpr size_t kBulkSmemHeader = 2 * bulk::kMaxStages * sizeof(uint64_t) + 112;
-constexpr size_t kBulkSmemMax = 200 * 1024;
+constexpr size_t kBulkSmemMax = 224 * 1024;
 
 struct SpecialEntry {
   bool decoder;
