@@ -152,7 +152,7 @@ int gs_prewarm(int device);
 /* Variant of the specialised kernels for aligned bodies (process-wide):
  * 0 = register-streaming LDG.128 kernel, 1 = bulk-copy (cp.async.bulk)
  * shared-memory pipeline with producer/consumer warps, 2 = auto (default:
- * bulk for encode launches >= 512 MB, register kernel otherwise). All are
+ * bulk for encode launches >= 128 MB, register kernel otherwise). All are
  * bit-identical; exposed for benchmarking and cross-checking. */
 int gs_set_kernel_variant(int variant);
 int gs_pipeline_destroy(gs_pipeline* p);

@@ -128,14 +128,14 @@ int blocks_per_sm(int dev, const void* kernel, size_t smem, int threads = kThrea
 // Which specialised kernel variant serves aligned bodies: 0 = register
 // (LDG.128) streaming, 1 = bulk-copy smem pipeline, 2 = auto (measured on
 // B200, tools/kernel_sweep.py: the bulk pipeline wins for encoders once a
-// launch moves >= 512 MB; the register kernel everywhere else).
+// launch moves >= 128 MB; the register kernel everywhere else).
 std::atomic<int> g_variant{2};
 // Tuning override for the register kernel's resident CTAs per SM (0 = max).
 int g_ctas_per_sm = [] {
   const char* e = std::getenv("GS_CTAS_PER_SM");
   return e ? std::atoi(e) : 0;
 }();
-constexpr uint64_t kBulkAutoBytes = 512ull << 20;
+constexpr uint64_t kBulkAutoBytes = 128ull << 20;
 
 int bulk_stages(const SpecialEntry* e) {
   const size_t per = static_cast<size_t>(e->used_cols) * e->tile_bulk;
