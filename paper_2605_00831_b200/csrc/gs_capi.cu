@@ -568,9 +568,52 @@ struct gs_pipeline {
   uint8_t* staging = nullptr;
   static constexpr int kSlots = 4;
   cudaEvent_t ready[kSlots]{}, done[kSlots]{}, drained[kSlots]{};
+  cudaEvent_t fork = nullptr, join = nullptr;
   cudaStream_t s_h2d = nullptr, s_comp = nullptr, s_d2h = nullptr;  // for the *_host calls
   int next = 0;
   size_t slot_bytes() const { return bytes / kSlots / 4096 * 4096; }
+
+  // CUDA-graph capture: while `compute` is being captured,
+  // only events recorded inside the same capture may be waited on; slot
+  // hazards across replays are ordered by the graph launches themselves.
+  unsigned long long capture_id = 0;
+  bool capturing = false;
+  bool in_capture[3][kSlots] = {};  // ready / done / drained recorded in this capture
+
+  // Called with the compute and copy streams of a call; under capture the
+  // copy stream is forked from the compute stream so it joins the graph.
+  cudaError_t begin(cudaStream_t st, cudaStream_t copy) {
+    cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+    unsigned long long id = 0;
+    cudaStreamGetCaptureInfo(st, &cs, &id);
+    capturing = cs == cudaStreamCaptureStatusActive;
+    if (capturing && id != capture_id) {
+      capture_id = id;
+      for (auto& row : in_capture)
+        for (bool& b : row) b = false;
+    }
+    if (capturing && copy != st) {
+      if (cudaError_t e = cudaEventRecord(fork, st)) return e;
+      return cudaStreamWaitEvent(copy, fork, 0);
+    }
+    return cudaSuccess;
+  }
+  // Under capture, join the copy stream back into the compute stream.
+  cudaError_t end(cudaStream_t st, cudaStream_t copy) {
+    if (!capturing || copy == st) return cudaSuccess;
+    if (cudaError_t e = cudaEventRecord(join, copy)) return e;
+    return cudaStreamWaitEvent(st, join, 0);
+  }
+  cudaError_t wait(cudaStream_t st, int kind, int slot) {
+    cudaEvent_t* evs = kind == 0 ? ready : kind == 1 ? done : drained;
+    if (capturing && !in_capture[kind][slot]) return cudaSuccess;
+    return cudaStreamWaitEvent(st, evs[slot], 0);
+  }
+  cudaError_t record(cudaStream_t st, int kind, int slot) {
+    cudaEvent_t* evs = kind == 0 ? ready : kind == 1 ? done : drained;
+    if (capturing) in_capture[kind][slot] = true;
+    return cudaEventRecord(evs[slot], st);
+  }
 };
 
 namespace {
@@ -978,6 +1021,8 @@ int gs_pipeline_create(int device, size_t staging_bytes, gs_pipeline** out) {
     cudaEventCreateWithFlags(&p->done[i], cudaEventDisableTiming);
     cudaEventCreateWithFlags(&p->drained[i], cudaEventDisableTiming);
   }
+  cudaEventCreateWithFlags(&p->fork, cudaEventDisableTiming);
+  cudaEventCreateWithFlags(&p->join, cudaEventDisableTiming);
   cudaStreamCreateWithFlags(&p->s_h2d, cudaStreamNonBlocking);
   cudaStreamCreateWithFlags(&p->s_comp, cudaStreamNonBlocking);
   cudaStreamCreateWithFlags(&p->s_d2h, cudaStreamNonBlocking);
@@ -998,6 +1043,8 @@ int gs_pipeline_destroy(gs_pipeline* p) {
     cudaEventDestroy(p->done[i]);
     cudaEventDestroy(p->drained[i]);
   }
+  cudaEventDestroy(p->fork);
+  cudaEventDestroy(p->join);
   cudaStreamDestroy(p->s_h2d);
   cudaStreamDestroy(p->s_comp);
   cudaStreamDestroy(p->s_d2h);
@@ -1030,6 +1077,7 @@ static int encode_offload(gs_pipeline* p, const gs_codec* c, int n_stripes, cons
   DeviceGuard g(p->device);
   auto cs = static_cast<cudaStream_t>(compute);
   auto ks = static_cast<cudaStream_t>(copy);
+  GS_CUDA(p->begin(cs, ks));
   const int K = c->n_out, N = c->n_slots;
   const size_t slot = p->slot_bytes();
   const uint64_t rl_max = align_piece(c, piece_len(len, slot, K), len);
@@ -1042,7 +1090,7 @@ static int encode_offload(gs_pipeline* p, const gs_codec* c, int n_stripes, cons
       const int sl = p->next;
       p->next = (p->next + 1) % gs_pipeline::kSlots;
       uint8_t* base = p->staging + static_cast<size_t>(sl) * slot;
-      GS_CUDA(cudaStreamWaitEvent(cs, p->drained[sl], 0));  // slot's previous D2H finished
+      GS_CUDA(p->wait(cs, 2, sl));  // slot's previous D2H finished
       auto src = [&](int s, int j) -> const void* {
         return static_cast<const uint8_t*>(d_data[static_cast<size_t>(s0 + s) * N + j]) + (src_map ? 0 : r0);
       };
@@ -1056,16 +1104,17 @@ static int encode_offload(gs_pipeline* p, const gs_codec* c, int n_stripes, cons
         pg.paged_slots = N >= 32 ? ~0u : (1u << N) - 1;
       }
       if (int st = run_codec(c, cnt, src, dst, rl, cs, pg)) return st;
-      GS_CUDA(cudaEventRecord(p->done[sl], cs));
-      GS_CUDA(cudaStreamWaitEvent(ks, p->done[sl], 0));
+      GS_CUDA(p->record(cs, 1, sl));
+      GS_CUDA(p->wait(ks, 1, sl));
       for (int s = 0; s < cnt; ++s)
         for (int i = 0; i < K; ++i)
           ops.push_back({static_cast<uint8_t*>(h_parity[static_cast<size_t>(s0 + s) * K + i]) + r0,
                          base + (static_cast<size_t>(s) * K + i) * rl, rl, i});
       if (int st = issue_copies(ops, cudaMemcpyDeviceToHost, ks)) return st;
-      GS_CUDA(cudaEventRecord(p->drained[sl], ks));
+      GS_CUDA(p->record(ks, 2, sl));
     }
   }
+  GS_CUDA(p->end(cs, ks));
   return GS_OK;
 }
 
@@ -1095,6 +1144,7 @@ static int reconstruct_upload(gs_pipeline* p, const gs_codec* c, int n_stripes, 
   DeviceGuard g(p->device);
   auto cs = static_cast<cudaStream_t>(compute);
   auto ks = static_cast<cudaStream_t>(copy);
+  GS_CUDA(p->begin(cs, ks));
   const int NS = c->n_slots, NO = c->n_out, n = c->n;
   std::vector<int> host_slots;  // parity slots actually used
   for (int j : c->used)
@@ -1111,7 +1161,7 @@ static int reconstruct_upload(gs_pipeline* p, const gs_codec* c, int n_stripes, 
       const int sl = p->next;
       p->next = (p->next + 1) % gs_pipeline::kSlots;
       uint8_t* base = p->staging + static_cast<size_t>(sl) * slot;
-      GS_CUDA(cudaStreamWaitEvent(ks, p->done[sl], 0));  // slot's previous kernel consumed it
+      GS_CUDA(p->wait(ks, 1, sl));  // slot's previous kernel consumed it
       for (int s = 0; s < cnt; ++s)
         for (size_t h = 0; h < host_slots.size(); ++h) {
           const void* hp = slots[static_cast<size_t>(s0 + s) * NS + host_slots[h]];
@@ -1120,8 +1170,8 @@ static int reconstruct_upload(gs_pipeline* p, const gs_codec* c, int n_stripes, 
                          static_cast<int>(h)});
         }
       if (int st = issue_copies(ops, cudaMemcpyHostToDevice, ks)) return st;
-      GS_CUDA(cudaEventRecord(p->ready[sl], ks));
-      GS_CUDA(cudaStreamWaitEvent(cs, p->ready[sl], 0));
+      GS_CUDA(p->record(ks, 0, sl));
+      GS_CUDA(p->wait(cs, 0, sl));
       auto src = [&](int s, int j) -> const void* {
         if (j >= n) {
           const auto it = std::find(host_slots.begin(), host_slots.end(), j);
@@ -1144,9 +1194,10 @@ static int reconstruct_upload(gs_pipeline* p, const gs_codec* c, int n_stripes, 
       }
       if (dst_map) pg.dst = to_map(dst_map);
       if (int st = run_codec(c, cnt, src, dst, rl, cs, pg)) return st;
-      GS_CUDA(cudaEventRecord(p->done[sl], cs));
+      GS_CUDA(p->record(cs, 1, sl));
     }
   }
+  GS_CUDA(p->end(cs, ks));
   return GS_OK;
 }
 

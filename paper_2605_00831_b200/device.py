@@ -43,6 +43,22 @@ def _check_u8(t: Tensor, what: str) -> None:
         raise InvalidArgument(f"{what}: last dimension must be contiguous")
 
 
+def row_ptrs(t: Tensor) -> List[int]:
+    """Addresses of the rows of a [R, L] or [S, R, L] tensor, stripe-major,
+    by stride arithmetic (indexing each row costs ~1 us of Python per row)."""
+    base, es = t.data_ptr(), t.element_size()
+    if t.dim() == 1:
+        return [base]
+    if t.dim() == 2:
+        s1 = t.stride(0) * es
+        return [base + r * s1 for r in range(t.shape[0])]
+    if t.dim() != 3:
+        raise InvalidArgument(f"expected a 2-D or 3-D tensor, got shape {tuple(t.shape)}")
+    s0, s1 = t.stride(0) * es, t.stride(1) * es
+    R = t.shape[1]
+    return [base + s * s0 + r * s1 for s in range(t.shape[0]) for r in range(R)]
+
+
 def as_bytes(t: Tensor) -> Tensor:
     """Bit-for-bit byte view of an fp16/bf16 (or any) tensor: fp16.hpp:20-21."""
     return t.contiguous().view(torch.uint8)
@@ -87,8 +103,10 @@ def encode(scheme: CodingScheme, data: Union[Tensor, Sequence[Tensor]], out: Opt
                           device=data.device)
     o3 = out.unsqueeze(0) if single else out
     _check_u8(o3, "encode(out)")
-    slots = [[d3[s, j].data_ptr() for j in range(scheme.n)] for s in range(S)]
-    outs = [[o3[s, i].data_ptr() for i in range(scheme.k)] for s in range(S)]
+    dp, op = row_ptrs(d3), row_ptrs(o3)
+    n, k = scheme.n, scheme.k
+    slots = [dp[s * n:(s + 1) * n] for s in range(S)]
+    outs = [op[s * k:(s + 1) * k] for s in range(S)]
     apply(encoder(scheme), slots, outs, ln, stream)
     return out
 
@@ -126,11 +144,10 @@ def reconstruct(scheme: CodingScheme, shards: Mapping[int, Tensor], lost: Erasur
     S = shape[0] if batched else 1
     ln = shape[-1]
 
-    def ptr(t: Tensor, s: int) -> int:
-        return (t[s] if batched else t).data_ptr()
-
-    slots = [[None if lost.contains(j) else ptr(shards[j], s) for j in range(total)] for s in range(S)]
-    outs = [[ptr(res[i], s) for i in dec.out_index] for s in range(S)]
+    rows = {j: row_ptrs(shards[j]) for j in range(total) if not lost.contains(j)}
+    rows.update({i: row_ptrs(res[i]) for i in dec.out_index})
+    slots = [[None if lost.contains(j) else rows[j][s] for j in range(total)] for s in range(S)]
+    outs = [[rows[i][s] for i in dec.out_index] for s in range(S)]
     apply(dec, slots, outs, ln, stream)
     return res
 
@@ -174,8 +191,8 @@ class Pipeline:
         if h_parity.is_cuda or not h_parity.is_pinned():
             raise InvalidArgument("encode_offload: parity must be a pinned host tensor")
         enc = encoder(scheme)
-        d = L.ptr_array([data[s, j].data_ptr() for s in range(S) for j in range(n)])
-        h = L.ptr_array([h_parity[s, i].data_ptr() for s in range(S) for i in range(scheme.k)])
+        d = L.ptr_array(row_ptrs(data))
+        h = L.ptr_array(row_ptrs(h_parity))
         cs = _stream(compute)
         ks = _stream(copy) if copy is not None else cs
         check(L.lib().gs_encode_offload(self.handle, enc.handle, S, d, h, ln, cs, ks), "encode_offload")
@@ -193,22 +210,64 @@ class Pipeline:
         if not h_parity.is_pinned():
             raise InvalidArgument("reconstruct_upload: parity must be a pinned host tensor")
         total = scheme.n + scheme.k
-        slots = []
-        for s in range(S):
-            for j in range(total):
-                if lost.contains(j):
-                    slots.append(None)
-                elif j < scheme.n:
-                    t = data[j]
-                    slots.append((t[s] if t.dim() == 2 else t).data_ptr())
-                else:
-                    slots.append(h_parity[s, j - scheme.n].data_ptr())
-        outs = [(out[i][s] if out[i].dim() == 2 else out[i]).data_ptr()
-                for s in range(S) for i in dec.out_index]
+        rows = {j: row_ptrs(data[j]) for j in range(scheme.n) if not lost.contains(j)}
+        hp = row_ptrs(h_parity)
+        rows.update({scheme.n + i: hp[i::scheme.k] for i in range(scheme.k)})
+        orows = {i: row_ptrs(out[i]) for i in dec.out_index}
+        slots = [None if lost.contains(j) else rows[j][s] for s in range(S) for j in range(total)]
+        outs = [orows[i][s] for s in range(S) for i in dec.out_index]
         cs = _stream(compute)
         ks = _stream(copy) if copy is not None else cs
         check(L.lib().gs_reconstruct_upload(self.handle, dec.handle, S, L.ptr_array(slots),
                                             L.ptr_array(outs), ln, cs, ks), "reconstruct_upload")
+
+
+class CapturedCall:
+    """One pipeline call (encode_offload or reconstruct_upload) recorded
+    into a CUDA graph, replayed with one launch per decode block.
+
+    The paper runs the checkpoint path under CUDA graphs:
+    a block's encode kernels, ring waits and D2H pieces become one graph
+    launch instead of ~2 API calls per piece. The graph owns a private
+    Pipeline (its staging ring is baked into the graph), so eager calls on
+    other pipelines never race it. Buffers are fixed at capture time; the
+    caller refreshes their CONTENTS between replays (e.g. the serving
+    engine's per-block KV slices and a fixed pinned parity buffer).
+    """
+
+    def __init__(self, method: str, *args, staging_bytes: int = 64 << 20, device: Optional[int] = None):
+        dev = torch.cuda.current_device() if device is None else device
+        self.pipe = Pipeline(dev, staging_bytes)
+        self.stream = torch.cuda.Stream(dev)
+        self.copy = torch.cuda.Stream(dev)
+        call = getattr(self.pipe, method)
+        self.stream.wait_stream(torch.cuda.current_stream(dev))
+        call(*args, compute=self.stream, copy=self.copy)        # eager warm-up: resolves kernels and occupancy
+        self.stream.wait_stream(self.copy)
+        self.stream.synchronize()
+        self.graph = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(self.graph, stream=self.stream):
+            call(*args, compute=self.stream, copy=self.copy)    # copy stream is forked/joined inside the call
+
+    def replay(self, stream=None) -> None:
+        """Enqueue the recorded call; complete when `stream` (default: the
+        current stream) reaches this point."""
+        st = torch.cuda.current_stream() if stream is None else stream
+        self.stream.wait_stream(st)
+        with torch.cuda.stream(self.stream):
+            self.graph.replay()
+        st.wait_stream(self.stream)
+
+
+def capture_offload(scheme: CodingScheme, data: Tensor, h_parity: Tensor, **kw) -> CapturedCall:
+    """Graph of Pipeline.encode_offload(scheme, data, h_parity)."""
+    return CapturedCall("encode_offload", scheme, data, h_parity, **kw)
+
+
+def capture_upload(scheme: CodingScheme, lost: ErasurePattern, data: Mapping[int, Tensor], h_parity: Tensor,
+                   out: Mapping[int, Tensor], **kw) -> CapturedCall:
+    """Graph of Pipeline.reconstruct_upload(scheme, lost, data, h_parity, out)."""
+    return CapturedCall("reconstruct_upload", scheme, lost, data, h_parity, out, **kw)
 
 
 def launches() -> int:

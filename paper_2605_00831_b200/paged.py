@@ -25,6 +25,7 @@ import torch
 
 from . import _lib as L
 from .coding import CodingScheme, ErasurePattern, InvalidArgument, check, decoder, encoder
+from .device import row_ptrs
 from .kv_layout import ModelConfig, token_stride_bytes
 
 
@@ -139,7 +140,7 @@ def encode_blocks(scheme: CodingScheme, caches: Sequence[PagedKVCache], block_id
     _check_caches(caches)
     S = len(block_ids)
     slots = [caches[j].block_base(block_ids[s][j]) for s in range(S) for j in range(scheme.n)]
-    outs = [parity_out[s, i].data_ptr() for s in range(S) for i in range(scheme.k)]
+    outs = row_ptrs(parity_out)
     pm = caches[0].page_map(valid_tokens)
     check(L.lib().gs_apply_device_paged(encoder(scheme).handle, S, L.ptr_array(slots), L.ptr_array(outs),
                                         caches[0].slice_bytes, C.byref(pm), (1 << scheme.n) - 1, None,
@@ -156,7 +157,7 @@ def checkpoint_blocks(pipeline, scheme: CodingScheme, caches: Sequence[PagedKVCa
     S = len(block_ids)
     slots = [caches[j].block_base(block_ids[s][j]) for s in range(S) for j in range(scheme.n)]
     if isinstance(h_parity, torch.Tensor):
-        dst = [h_parity[s, i].data_ptr() for s in range(S) for i in range(scheme.k)]
+        dst = row_ptrs(h_parity)
     else:
         dst = list(h_parity)
     pm = caches[0].page_map(valid_tokens)
@@ -176,7 +177,7 @@ def checkpoint_chunks(pipeline, scheme: CodingScheme, caches: Sequence[PagedKVCa
     S = block_table.shape[0]
     pm = caches[0].page_map(valid_tokens, chunk_tokens, block_table)
     slots = [caches[j].buf.data_ptr() for s in range(S) for j in range(scheme.n)]
-    dst = [h_parity[s, i].data_ptr() for s in range(S) for i in range(scheme.k)]
+    dst = row_ptrs(h_parity)
     cs = _stream(compute)
     check(L.lib().gs_encode_offload_paged(pipeline.handle, encoder(scheme).handle, S, L.ptr_array(slots),
                                           L.ptr_array(dst), caches[0].chunk_slice_bytes(chunk_tokens), C.byref(pm),
@@ -193,12 +194,13 @@ def rebuild_chunks(pipeline, scheme: CodingScheme, lost: ErasurePattern, caches:
     _check_caches(live + list(replacements.values()))
     S = block_table.shape[0]
     n, k = scheme.n, scheme.k
+    hp = row_ptrs(h_parity)
     slots: List[Optional[int]] = []
     for s in range(S):
         for j in range(n):
             slots.append(None if lost.contains(j) else caches[j].buf.data_ptr())
         for i in range(k):
-            slots.append(None if lost.contains(n + i) else h_parity[s, i].data_ptr())
+            slots.append(None if lost.contains(n + i) else hp[s * k + i])
     outs = [replacements[w].buf.data_ptr() for s in range(S) for w in dec.out_index]
     ref = live[0]
     pm = ref.page_map(valid_tokens, chunk_tokens, block_table)
@@ -219,12 +221,13 @@ def rebuild_blocks(pipeline, scheme: CodingScheme, lost: ErasurePattern, caches:
     _check_caches(live + list(replacements.values()))
     S = len(block_ids)
     n, k = scheme.n, scheme.k
+    hp = row_ptrs(h_parity)
     slots: List[Optional[int]] = []
     for s in range(S):
         for j in range(n):
             slots.append(None if lost.contains(j) else caches[j].block_base(block_ids[s][j]))
         for i in range(k):
-            slots.append(None if lost.contains(n + i) else h_parity[s, i].data_ptr())
+            slots.append(None if lost.contains(n + i) else hp[s * k + i])
     outs = [replacements[w].block_base(block_ids[s][w]) for s in range(S) for w in dec.out_index]
     ref = live[0]
     pm = ref.page_map(valid_tokens)

@@ -22,6 +22,7 @@ from typing import Dict, List, Optional, Sequence, Tuple
 
 from . import _lib as L
 from .coding import CodingScheme, ErasurePattern, InvalidArgument, check, decoder, encoder
+from .device import row_ptrs
 
 
 def stripe_range(total: int, rank: int, world: int) -> Tuple[int, int]:
@@ -141,12 +142,10 @@ def plan_encode_striped(scheme: CodingScheme, layout: ShardLayout, bases: Sequen
     flat = L.ptr_array([p for row in slots for p in row])
     lib = L.lib()
     if pipeline is None:
-        outs = L.ptr_array([parity_out[s, i].data_ptr() for s in range(layout.stripes)
-                            for i in range(scheme.k)])
+        outs = L.ptr_array(row_ptrs(parity_out))
         return StripedCall(lib.gs_apply_device, (enc.handle, layout.stripes, flat, outs, ln), off, ln,
                            two_streams=False)
-    outs = L.ptr_array([h_parity[s, i].data_ptr() + off for s in range(layout.stripes)
-                        for i in range(scheme.k)])
+    outs = L.ptr_array([p + off for p in row_ptrs(h_parity)])
     return StripedCall(lib.gs_encode_offload, (pipeline.handle, enc.handle, layout.stripes, flat, outs, ln),
                        off, ln)
 
@@ -171,11 +170,12 @@ def plan_reconstruct_striped(scheme: CodingScheme, layout: ShardLayout, bases: S
     if ln == 0 or dec.n_out == 0:
         return StripedCall(None, (), off, 0)
     n, k = scheme.n, scheme.k
+    hp = row_ptrs(h_parity)
     full = []
     for s in range(layout.stripes):
         full.extend(slots[s])
         for i in range(k):
-            full.append(None if lost.contains(n + i) else h_parity[s, i].data_ptr() + off)
+            full.append(None if lost.contains(n + i) else hp[s * k + i] + off)
     outs = []
     for s in range(layout.stripes):
         for w in dec.out_index:

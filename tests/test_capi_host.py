@@ -167,3 +167,15 @@ def test_stripe_ranges_partition_exactly():
                     assert off % 4096 == 0
                 pos = max(pos, off + ln)
             assert sum(ln for _, ln in spans) == total
+
+
+def test_row_ptrs_match_indexing():
+    """row_ptrs (stride arithmetic) == per-row data_ptr() for contiguous,
+    sliced and transposed-stripe views."""
+    import torch
+    from paper_2605_00831_b200.device import row_ptrs
+    base = torch.zeros((6, 5, 64), dtype=torch.uint8)
+    for t in (base, base[1:5], base[:, 1:4], base[:, :, 8:40], base.transpose(0, 1), base[2]):
+        want = ([t[s, r].data_ptr() for s in range(t.shape[0]) for r in range(t.shape[1])] if t.dim() == 3
+                else [t[r].data_ptr() for r in range(t.shape[0])])
+        assert row_ptrs(t) == want

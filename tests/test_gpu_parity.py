@@ -372,3 +372,31 @@ def test_rdp_pipelines_split_on_dstripes():
             for i, b in rb.items():
                 assert np.array_equal(b, host[i])
         pipe.close()
+
+
+@pytest.mark.parametrize("staging", [64 << 10, 64 << 20])
+def test_captured_offload_and_upload_graphs(staging):
+    """encode_offload / reconstruct_upload recorded into CUDA graphs: replays
+    after the inputs' contents change give the fresh parity / rebuilt shards
+    (small rings reuse every staging slot several times inside one graph)."""
+    scheme = G.CodingScheme.reed_solomon(8, 2)
+    S, n, ln = 4, 8, 2 * 65536 + 4096 + 3
+    gen = torch.Generator(device="cuda").manual_seed(1)
+    data = torch.empty((S, n, ln), dtype=torch.uint8, device="cuda")
+    h_par = torch.zeros((S, 2, ln), dtype=torch.uint8).pin_memory()
+    enc = D.capture_offload(scheme, data, h_par, staging_bytes=staging)
+    lost = G.ErasurePattern([2, 8])
+    data_map = {j: torch.empty((S, ln), dtype=torch.uint8, device="cuda") for j in range(n) if j not in (2,)}
+    out = {2: torch.empty((S, ln), dtype=torch.uint8, device="cuda")}
+    dec = D.capture_upload(scheme, lost, data_map, h_par, out, staging_bytes=staging)
+    for rnd in range(3):
+        data.copy_(torch.randint(0, 256, data.shape, dtype=torch.uint8, device="cuda", generator=gen))
+        enc.replay()
+        torch.cuda.synchronize()
+        assert torch.equal(h_par, D.encode(scheme, data).cpu()), rnd
+        for j, t in data_map.items():
+            t.copy_(data[:, j])
+        out[2].zero_()
+        dec.replay()
+        torch.cuda.synchronize()
+        assert torch.equal(out[2], data[:, 2]), rnd
