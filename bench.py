@@ -23,6 +23,7 @@ prefill), clocks sampled through NVML during the timed region, and the
 reference CPU codec timed on this host.
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+  python bench.py --sweep [--sweep-sizes 64K,...,1G]     # C5: one JSON line per (code, L)
 """
 from __future__ import annotations
 
@@ -789,6 +790,168 @@ def c3_recovery(torch, dev, comp, copy, pipe):
     return out
 
 
+# ---------------------------------------------------------------------------
+# C5: parity throughput sweep over block sizes (BASELINE.json configs[4])
+# ---------------------------------------------------------------------------
+def _parse_size(x: str) -> int:
+    x = x.strip().upper()
+    mult = {"K": 1 << 10, "M": 1 << 20, "G": 1 << 30}
+    return int(float(x[:-1]) * mult[x[-1]]) if x[-1] in mult else int(x)
+
+
+def run_sweep(args):
+    """C5: for each shard length L and code (RS(8,2), XOR(8)),
+    encode + D2H offload and K1 alone, weak-scaled (one stripe of n x L per
+    GPU, striped over the ranks like the C2 step), with the roofline fraction
+    t*/t (t* = the slowest of HBM bytes at peak, parity over the host link,
+    peer bytes over NVLink) and the reference CPU encoder on this host."""
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+
+    from paper_2605_00831_b200 import device as D
+    from paper_2605_00831_b200.coding import CodingScheme
+    from paper_2605_00831_b200.peer import PeerGroup, ShardLayout, plan_encode_striped, stripe_range
+
+    rank, world, local = env_rank()
+    shared = os.environ.get("GS_BENCH_SHARED_GPU") == "1"
+    if shared:
+        local = 0
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("gloo" if shared else "nccl", **({} if shared else {"device_id": dev}))
+    hbm_peak, hbm_src = load_peaks()
+    link = host_link_peaks(torch, dev)
+    pipe = D.Pipeline(local, 256 << 20)
+    comp, copy = torch.cuda.Stream(device=dev), torch.cuda.Stream(device=dev)
+    pg = PeerGroup() if world > 1 else None
+    cpu_ref = None
+    if rank == 0 and not args.no_cpu:
+        from oracle import oracle as O
+        cpu_ref = (O, O.ref() if O.have_ref() else O.port(), "reference" if O.have_ref() else "port")
+    threads = os.cpu_count() or 1
+
+    def tmax(ms):
+        if world == 1:
+            return ms
+        t = torch.tensor([ms], device="cpu" if shared else dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    def timed(plans, two, iters):
+        for i in range(2):
+            plans[i % len(plans)].run(comp.cuda_stream, copy.cuda_stream if two else None)
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(comp)
+        for i in range(iters):
+            plans[i % len(plans)].run(comp.cuda_stream, copy.cuda_stream if two else None)
+        comp.wait_stream(copy)
+        e1.record(comp)
+        e1.synchronize()
+        return tmax(e0.elapsed_time(e1)) / iters * 1e-3
+
+    def graph_timed(plans, two, iters):
+        """The same steps replayed from one CUDA graph holding all buffers'
+        calls (the serving engine's launch mode, device.CapturedCall): host
+        launch overhead out of the small-L numbers."""
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g, stream=comp):
+            for p in plans:
+                p.run(comp.cuda_stream, copy.cuda_stream if two else None)
+            if two:
+                comp.wait_stream(copy)
+        reps = max(2, -(-iters // len(plans)))
+        with torch.cuda.stream(comp):
+            g.replay()
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        with torch.cuda.stream(comp):
+            e0.record(comp)
+            for _ in range(reps):
+                g.replay()
+            e1.record(comp)
+        e1.synchronize()
+        del g
+        return tmax(e0.elapsed_time(e1)) / (reps * len(plans)) * 1e-3
+
+    codes = [("RS(8,2)", CodingScheme.reed_solomon(8, 2)), ("XOR(8)", CodingScheme.xor_code(8))]
+    for name, scheme in codes:
+        n, k = scheme.n, scheme.k
+        for L_ in [_parse_size(x) for x in args.sweep_sizes.split(",")]:
+            S = world
+            layout = ShardLayout(n, world, S, L_)
+            nl = layout.n_local
+            iters = max(3, min(args.steps, int((4 << 30) // (S * n * L_))))
+            nbuf = max(1, min(16, -(-(256 << 20) // (S * nl * L_))))   # rotate so each step misses L2
+            data = torch.randint(0, 256, (nbuf, S, nl, L_), dtype=torch.uint8, device=dev)
+            bases = [pg.share(data[b]) if pg else [data[b].data_ptr()] for b in range(nbuf)]
+            h_par = torch.empty((S, k, L_), dtype=torch.uint8).pin_memory()
+            _, ln = stripe_range(L_, rank, world)
+            par_dev = torch.empty((S, k, max(ln, 1)), dtype=torch.uint8, device=dev)
+            off_plans = [plan_encode_striped(scheme, layout, bases[b], rank, pipeline=pipe, h_parity=h_par)
+                         for b in range(nbuf)]
+            k_plans = [plan_encode_striped(scheme, layout, bases[b], rank, parity_out=par_dev)
+                       for b in range(nbuf)]
+            t_off = timed(off_plans, True, iters)
+            last = (iters - 1) % nbuf
+            ok = True
+            if world == 1:
+                ok = torch.equal(h_par.to(dev), D.encode(scheme, data[last].view(S, n, L_)))
+            t_k1 = timed(k_plans, False, iters)
+            t_off_g = graph_timed(off_plans, True, iters)
+            t_k1_g = graph_timed(k_plans, False, iters)
+            if pg:
+                pg.close()
+            per_gpu = S * L_ // world
+            t_star = max((n + k) * per_gpu / (hbm_peak * 1e9), k * per_gpu / (link["d2h"] * 1e9),
+                         (world - 1) / world * n * per_gpu / 900e9)
+            row = {"sweep": "C5", "code": name, "shard_bytes": L_, "n_gpus": world, "stripes": S,
+                   "data_bytes_per_step": S * n * L_,
+                   "offload_gbs": round(S * n * L_ / t_off / 1e9, 2), "offload_ms": round(t_off * 1e3, 4),
+                   "k1_gbs_hbm": round((n + k) * S * L_ / world / t_k1 / 1e9, 1),
+                   "k1_us": round(t_k1 * 1e6, 2), "roofline_frac": round(t_star / t_off, 4),
+                   "graph": {"offload_gbs": round(S * n * L_ / t_off_g / 1e9, 2),
+                             "offload_ms": round(t_off_g * 1e3, 4), "k1_us": round(t_k1_g * 1e6, 2),
+                             "k1_gbs_hbm": round((n + k) * S * L_ / world / t_k1_g / 1e9, 1),
+                             "roofline_frac": round(t_star / t_off_g, 4)},
+                   "roofline_bound": "host_link" if k * per_gpu / link["d2h"] > (n + k) * per_gpu / hbm_peak
+                   else "hbm", "hbm_peak_gbs": hbm_peak, "d2h_peak_gbs": link["d2h"], "parity_ok": ok}
+            if cpu_ref is not None:
+                O, lib, kind = cpu_ref
+                Lc = min(L_, 64 << 20)
+                rng = np.random.default_rng(42)
+                d = [rng.integers(0, 256, Lc, dtype=np.uint8) for _ in range(n)]
+                pp = [np.zeros(Lc, np.uint8) for _ in range(k)]
+                okind = O.RS if name.startswith("RS") else O.XOR
+                busy, reps = 0.0, 0
+                while busy < args.sweep_cpu_s or reps == 0:
+                    if kind == "reference":
+                        busy += lib.encode_timed(okind, n, k, d, pp, threads)
+                    else:
+                        t1 = time.perf_counter()
+                        lib.encode(okind, n, k, d)
+                        busy += time.perf_counter() - t1
+                    reps += 1
+                row["cpu_baseline"] = {"value": round(reps * n * Lc / busy / 1e9, 3), "unit": "GB/s",
+                                       "cores": threads if kind == "reference" else 1, "kind": kind,
+                                       "sample": f"{reps} encode(s) of {n} x {Lc} B"}
+            if rank == 0:
+                print(json.dumps(row), flush=True)
+            del data, h_par, par_dev, off_plans, k_plans
+            torch.cuda.empty_cache()
+            if world > 1:
+                dist.barrier()
+    pipe.close()
+    if world > 1:
+        dist.destroy_process_group()
+
+
 def main():
     ap = argparse.ArgumentParser(description=__doc__, formatter_class=argparse.RawDescriptionHelpFormatter)
     ap.add_argument("--gpus", type=int, default=1)
@@ -803,7 +966,16 @@ def main():
     ap.add_argument("--decode-ctx", type=int, default=4096)
     ap.add_argument("--traffic", type=float, default=None,
                     help="ncu dram bytes per K1 launch (from profiles/), echoed into roofline.traffic")
+    ap.add_argument("--sweep", action="store_true", help="C5 block-size sweep instead of the C2 step")
+    ap.add_argument("--sweep-sizes", default="64K,256K,1M,4M,16M,64M,256M,1G")
+    ap.add_argument("--sweep-cpu-s", type=float, default=0.5)
     args = ap.parse_args()
+    if args.sweep:
+        if args.impl == "reference":
+            print(json.dumps({"impl": "reference", "unavailable": "--sweep is our arm only"}))
+            return
+        run_sweep(args)
+        return
     if args.warmup < 3:
         args.warmup = 3
     if args.impl == "reference":

@@ -161,7 +161,12 @@ int gs_pipeline_destroy(gs_pipeline* p);
  * parity_store.hpp:77-90): encode device-resident data into staging on
  * `compute`, D2H each finished piece to `h_parity` (pinned host; k per
  * stripe) on `copy`, pieces overlapped. Returns once work is ENQUEUED;
- * completion = `copy` stream. */
+ * completion = `copy` stream.
+ * CUDA graphs: both pipeline calls may be stream-captured (capture on
+ * `compute`; `copy` is forked off it inside the call). Completion rules are
+ * unchanged, so an offload's capturer joins `copy` back into its origin
+ * stream before ending the capture. A graph bakes in the staging ring:
+ * order its launches against eager calls on the same pipeline. */
 int gs_encode_offload(gs_pipeline* p, const gs_codec* enc, int n_stripes,
                       const void* const* d_data, void* const* h_parity, size_t len,
                       void* compute, void* copy);

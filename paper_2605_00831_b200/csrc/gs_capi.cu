@@ -578,6 +578,7 @@ struct gs_pipeline {
   // hazards across replays are ordered by the graph launches themselves.
   unsigned long long capture_id = 0;
   bool capturing = false;
+  bool captured = false;            // a capture used the events since the last eager call
   bool in_capture[3][kSlots] = {};  // ready / done / drained recorded in this capture
 
   // Called with the compute and copy streams of a call; under capture the
@@ -592,13 +593,26 @@ struct gs_pipeline {
       for (auto& row : in_capture)
         for (bool& b : row) b = false;
     }
+    if (capturing) {
+      captured = true;
+    } else if (captured) {
+      // Events last recorded inside a capture cannot be waited on eagerly:
+      // re-arm them on this stream (ordered after any graph launched on it).
+      captured = false;
+      for (int i = 0; i < kSlots; ++i)
+        for (cudaEvent_t e : {ready[i], done[i], drained[i]})
+          if (cudaError_t err = cudaEventRecord(e, st)) return err;
+    }
     if (capturing && copy != st) {
       if (cudaError_t e = cudaEventRecord(fork, st)) return e;
       return cudaStreamWaitEvent(copy, fork, 0);
     }
     return cudaSuccess;
   }
-  // Under capture, join the copy stream back into the compute stream.
+  // Under capture, join the copy stream back into the compute stream. The
+  // offload does not call it: its completion is the copy stream, in a graph
+  // as eagerly, so the next block's kernels overlap this block's D2H; the
+  // capturer joins `copy` into its origin stream before ending the capture.
   cudaError_t end(cudaStream_t st, cudaStream_t copy) {
     if (!capturing || copy == st) return cudaSuccess;
     if (cudaError_t e = cudaEventRecord(join, copy)) return e;
@@ -618,7 +632,12 @@ struct gs_pipeline {
 
 namespace {
 
-constexpr uint64_t kHostPiece = 1ull << 20;
+// Host-buffer pipelines: bytes per shard per piece (GS_HOST_PIECE overrides).
+const uint64_t kHostPiece = [] {
+  const char* e = std::getenv("GS_HOST_PIECE");
+  const uint64_t v = e ? std::strtoull(e, nullptr, 0) : 0;
+  return v >= 4096 ? v / 4096 * 4096 : (1ull << 20);
+}();
 
 struct DeviceGuard {
   int prev = -1;
@@ -1114,7 +1133,6 @@ static int encode_offload(gs_pipeline* p, const gs_codec* c, int n_stripes, cons
       GS_CUDA(p->record(ks, 2, sl));
     }
   }
-  GS_CUDA(p->end(cs, ks));
   return GS_OK;
 }
 
@@ -1212,6 +1230,7 @@ int gs_encode_host(gs_pipeline* p, const gs_codec* c, const void* const* h_data,
   for (int j = 0; j < c->n_slots; ++j)
     if (!h_data[j]) return fail(GS_INVALID_ARGUMENT, "encode_host: data shard %d is NULL", j);
   DeviceGuard g(p->device);
+  GS_CUDA(p->begin(p->s_h2d, p->s_h2d));
   const int N = c->n_slots, K = c->n_out;
   const size_t slot = p->slot_bytes();
   // ~2 MiB per shard per piece: deep enough pipelining that the H2D of piece
@@ -1257,6 +1276,7 @@ int gs_reconstruct_host(gs_pipeline* p, const gs_codec* c, const void* const* h_
   for (int j : c->used)
     if (!h_slots[j]) return fail(GS_INVALID_ARGUMENT, "coding: surviving shard %d missing from input", j);
   DeviceGuard g(p->device);
+  GS_CUDA(p->begin(p->s_h2d, p->s_h2d));
   const int U = static_cast<int>(c->used.size()), E = c->n_out;
   const size_t slot = p->slot_bytes();
   const uint64_t rl_max = align_piece(c, piece_len(len, slot, U + E, kHostPiece), len);

@@ -247,7 +247,8 @@ class CapturedCall:
         self.stream.synchronize()
         self.graph = torch.cuda.CUDAGraph()
         with torch.cuda.graph(self.graph, stream=self.stream):
-            call(*args, compute=self.stream, copy=self.copy)    # copy stream is forked/joined inside the call
+            call(*args, compute=self.stream, copy=self.copy)    # the call forks `copy` off the capture
+            self.stream.wait_stream(self.copy)                  # completion (offload: the copy stream) joins it
 
     def replay(self, stream=None) -> None:
         """Enqueue the recorded call; complete when `stream` (default: the

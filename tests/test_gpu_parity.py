@@ -400,3 +400,21 @@ def test_captured_offload_and_upload_graphs(staging):
         dec.replay()
         torch.cuda.synchronize()
         assert torch.equal(out[2], data[:, 2]), rnd
+
+
+def test_pipeline_eager_after_capture():
+    """A pipeline whose events were used inside a graph capture still works
+    for eager calls afterwards (events re-armed outside the capture)."""
+    scheme = G.CodingScheme.reed_solomon(8, 2)
+    S, ln = 3, 5 * 65536
+    data = torch.randint(0, 256, (S, 8, ln), dtype=torch.uint8, device="cuda")
+    h_par = torch.zeros((S, 2, ln), dtype=torch.uint8).pin_memory()
+    g = D.capture_offload(scheme, data, h_par, staging_bytes=256 << 10)
+    g.replay()
+    torch.cuda.synchronize()
+    data.copy_(torch.randint(0, 256, data.shape, dtype=torch.uint8, device="cuda"))
+    h_par.zero_()
+    st = torch.cuda.current_stream()
+    g.pipe.encode_offload(scheme, data, h_par, st, st)
+    torch.cuda.synchronize()
+    assert torch.equal(h_par, D.encode(scheme, data).cpu())
