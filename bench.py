@@ -381,6 +381,15 @@ def run_ours(args):
                      S * (N_SHARDS + K_PARITY) * SLICE,
                      "k_apply_special<EncSpec<RS,8,2>> (K1 encode, auto variant = ldg128 at this size)")
         kern["variants_us_per_launch"] = variants
+        # attainable at this launch size: a device copy moving the same bytes
+        # (half read, half written), same rotation and graph timing
+        half = S * (N_SHARDS + K_PARITY) * SLICE // 2
+        cdst = torch.empty((RING_BLOCKS, half), dtype=torch.uint8, device=dev)
+        flat = ring.view(RING_BLOCKS, -1)
+        cp = timed(lambda b: cdst[b].copy_(flat[b, :half]), 2 * half, "copy")
+        kern["copy_same_bytes"] = {"per_launch_us": cp["per_launch_us"], "achieved": cp["achieved"],
+                                   "kernel_vs_copy": round(cp["per_launch_us"] / kern["per_launch_us"], 4)}
+        del cdst
         kern["traffic"] = args.traffic or ncu_traffic()
         kern2 = timed(lambda b: check(lib.gs_apply_device(dec5.handle, S, dslots[b], douts[b], SLICE,
                                                           ks.cuda_stream), "k2"),

@@ -135,6 +135,11 @@ int g_ctas_per_sm = [] {
   const char* e = std::getenv("GS_CTAS_PER_SM");
   return e ? std::atoi(e) : 0;
 }();
+// Tuning override: grid = every tile (non-persistent) when set.
+int g_full_grid = [] {
+  const char* e = std::getenv("GS_FULL_GRID");
+  return e ? std::atoi(e) : 0;
+}();
 constexpr uint64_t kBulkAutoBytes = 128ull << 20;
 
 int bulk_stages(const SpecialEntry* e) {
@@ -328,6 +333,9 @@ PageMap to_map(const gs_page_map* m) {
     r.table = m->block_table;
     r.block_bytes = m->block_table ? m->block_bytes : m->page_bytes;
     r.table_stride = m->table_stride;
+    r.page_m = fastdiv_magic(r.page_bytes);
+    r.layers_m = fastdiv_magic(r.layers);
+    r.block_m = fastdiv_magic(r.block_bytes);
   }
   return r;
 }
@@ -419,9 +427,10 @@ int run_codec(const gs_codec* c, int n_stripes, SlotFn slot_ptr, OutFn out_ptr, 
       if (total > 0xFFFFFFFFull) return fail(GS_INVALID_ARGUMENT, "apply: too many tiles in one launch");
       TileGeom g{body, static_cast<uint32_t>(tps64), static_cast<uint32_t>(total), stride, c->n_slots, 1,
                  pg.paged_slots, pg.logical0, pg.src, pg.dst};
+      g.tps_m = fastdiv_magic(g.tps);
       if (g.src.table) g.src.table += (pg.stripe0 + s0) * g.src.table_stride;
       if (g.dst.table) g.dst.table += (pg.stripe0 + s0) * g.dst.table_stride;
-      const int grid = static_cast<int>(std::min<uint64_t>(total, static_cast<uint64_t>(occ) * sms));
+      const int grid = static_cast<int>(std::min<uint64_t>(total, g_full_grid && !use_bulk ? total : static_cast<uint64_t>(occ) * sms));
       cudaError_t e = use_bulk ? c->special->launch_bulk(ptrs.data(), cnt * stride, g, grid, st, stages, smem)
                       : paged  ? c->special->launch_paged(ptrs.data(), cnt * stride, g, grid, st)
                                : c->special->launch(ptrs.data(), cnt * stride, g, grid, st);
@@ -460,6 +469,7 @@ int run_codec(const gs_codec* c, int n_stripes, SlotFn slot_ptr, OutFn out_ptr, 
       const int kb = std::min(kMaxGenericRows, c->n_out - r0);
       TileGeom g{glen, static_cast<uint32_t>(tps64), static_cast<uint32_t>(total), stride, ns + r0,
                  galigned ? 1 : 0, gpaged, pg.logical0 + done, pg.src, pg.dst};
+      g.tps_m = fastdiv_magic(g.tps);
       if (g.src.table) g.src.table += (pg.stripe0 + s0) * g.src.table_stride;
       if (g.dst.table) g.dst.table += (pg.stripe0 + s0) * g.dst.table_stride;
       const size_t smem = static_cast<size_t>(kb) * ns * sizeof(CoefWords);

@@ -123,7 +123,22 @@ struct PageMap {
   const int32_t* table;
   uint32_t block_bytes;
   uint32_t table_stride;
+  // fastdiv_magic() of page_bytes / layers / block_bytes (0: divide)
+  uint64_t page_m, layers_m, block_m;
 };
+
+// Division by a launch-invariant divisor without the ~20-instruction integer
+// divide: q = floor(n * M / 2^64) with M = floor(2^64 / d) + 1 (or 2^64 / d
+// for powers of two) is exact for every 32-bit n when 2 <= d < 2^32 (the
+// rounding error n * (M - 2^64/d) / 2^64 < 2^-32 < 1/d never crosses an
+// integer). M = 0 means "no magic": plain division (d == 1 returns n).
+__host__ __device__ constexpr uint64_t fastdiv_magic(uint32_t d) { return d > 1 ? ~0ull / d + 1 : 0; }
+
+__device__ __forceinline__ uint32_t fdiv(uint32_t n, uint32_t d, uint64_t m) {
+  if (m == 0) return d == 1 ? n : n / d;
+  const uint64_t r = static_cast<uint64_t>(n) * static_cast<uint32_t>(m >> 32) + __umulhi(n, static_cast<uint32_t>(m));
+  return static_cast<uint32_t>(r >> 32);
+}
 
 struct TileGeom {
   uint64_t len;        // bytes per shard (this launch's range)
@@ -136,20 +151,23 @@ struct TileGeom {
   uint64_t logical0;     // slice offset of this launch's byte 0 (for the page mapping)
   PageMap src;           // mapping of paged source slots
   PageMap dst;           // mapping of the outputs (dst.page_bytes == 0: contiguous)
+  uint64_t tps_m;        // fastdiv_magic(tps)
 };
+
+__device__ __forceinline__ uint32_t tile_stripe(uint32_t t, const TileGeom& g) { return fdiv(t, g.tps, g.tps_m); }
 
 // Offset of logical slice byte `logical` of stripe `s` inside a paged slot;
 // `masked` = beyond the valid tokens of its segment.
 __device__ __forceinline__ uint64_t paged_offset(const PageMap& m, uint32_t s, uint64_t logical, bool& masked) {
   const uint32_t o = static_cast<uint32_t>(logical);
-  const uint32_t q = o / m.page_bytes;
+  const uint32_t q = fdiv(o, m.page_bytes, m.page_m);
   const uint32_t in = o - q * m.page_bytes;
-  const uint32_t t = q / m.layers;
+  const uint32_t t = fdiv(q, m.layers, m.layers_m);
   const uint32_t l = q - t * m.layers;
   masked = in >= m.valid_tokens * m.token_bytes;
   uint64_t r = static_cast<uint64_t>(l) * m.layer_stride + static_cast<uint64_t>(t) * m.kv_stride;
   if (m.table) {
-    const uint32_t pi = in / m.block_bytes;
+    const uint32_t pi = fdiv(in, m.block_bytes, m.block_m);
     const int32_t blk = masked ? 0 : m.table[static_cast<uint64_t>(s) * m.table_stride + pi];
     r += static_cast<uint64_t>(blk) * m.block_bytes + (in - pi * m.block_bytes);
   } else {
@@ -165,13 +183,13 @@ __device__ __forceinline__ uint64_t paged_offset(const PageMap& m, uint32_t s, u
 __device__ __forceinline__ uint64_t paged_offset_tile(const PageMap& m, uint32_t s, uint64_t tile_logical,
                                                       uint32_t lane_off, bool& masked) {
   const uint32_t u = static_cast<uint32_t>(tile_logical);
-  const uint32_t q = u / m.page_bytes;
+  const uint32_t q = fdiv(u, m.page_bytes, m.page_m);
   const uint32_t in0 = u - q * m.page_bytes;
   const uint32_t bb = m.table ? m.block_bytes : m.page_bytes;
-  const uint32_t pi = m.table ? in0 / bb : 0;
+  const uint32_t pi = m.table ? fdiv(in0, m.block_bytes, m.block_m) : 0;
   const uint32_t ib0 = in0 - pi * bb;
   if (in0 + static_cast<uint32_t>(kTile) <= m.page_bytes && ib0 + static_cast<uint32_t>(kTile) <= bb) {
-    const uint32_t t = q / m.layers;
+    const uint32_t t = fdiv(q, m.layers, m.layers_m);
     const uint32_t l = q - t * m.layers;
     const uint32_t in = in0 + lane_off;
     masked = in >= m.valid_tokens * m.token_bytes;
@@ -237,7 +255,7 @@ template <class Spec, int CAP, int U, bool PAGED>
 __global__ void __launch_bounds__(kThreads) k_apply_special(const PtrTable<CAP> tab, const TileGeom g) {
   static_assert(U == 1, "one 16-byte group per thread per tile");
   for (uint32_t t = blockIdx.x; t < g.total; t += gridDim.x) {
-    const uint32_t s = t / g.tps;
+    const uint32_t s = tile_stripe(t, g);
     const uint64_t off = static_cast<uint64_t>(t - s * g.tps) * kTile + threadIdx.x * kVec;
     if (off >= g.len) continue;
     const int base = static_cast<int>(s) * g.stride;
@@ -413,7 +431,7 @@ __global__ void __launch_bounds__(kThreads) k_apply_generic(const PtrTable<CAP> 
   __syncthreads();
 
   for (uint32_t t = blockIdx.x; t < g.total; t += gridDim.x) {
-    const uint32_t s = t / g.tps;
+    const uint32_t s = tile_stripe(t, g);
     const uint64_t off = static_cast<uint64_t>(t - s * g.tps) * kTile + threadIdx.x * kVec;
     if (off >= g.len) continue;
     const int base = static_cast<int>(s) * g.stride;
@@ -530,7 +548,7 @@ __global__ void __launch_bounds__((CW + 1) * 32, 1)
       int stage = 0;
       uint32_t phase = 0;
       for (uint32_t t = blockIdx.x; t < g.total; t += gridDim.x) {
-        const uint32_t s = t / g.tps;
+        const uint32_t s = tile_stripe(t, g);
         const uint64_t off = static_cast<uint64_t>(t - s * g.tps) * T;
         const uint32_t size = static_cast<uint32_t>(g.len - off < T ? g.len - off : T);
         const int base = static_cast<int>(s) * g.stride;
@@ -554,7 +572,7 @@ __global__ void __launch_bounds__((CW + 1) * 32, 1)
   uint32_t phase = 0;
   const uint32_t tid = threadIdx.x;  // 0 .. CW*32-1
   for (uint32_t t = blockIdx.x; t < g.total; t += gridDim.x) {
-    const uint32_t s = t / g.tps;
+    const uint32_t s = tile_stripe(t, g);
     const uint64_t off = static_cast<uint64_t>(t - s * g.tps) * T;
     const uint32_t size = static_cast<uint32_t>(g.len - off < T ? g.len - off : T);
     const int base = static_cast<int>(s) * g.stride;

@@ -179,3 +179,21 @@ def test_row_ptrs_match_indexing():
         want = ([t[s, r].data_ptr() for s in range(t.shape[0]) for r in range(t.shape[1])] if t.dim() == 3
                 else [t[r].data_ptr() for r in range(t.shape[0])])
         assert row_ptrs(t) == want
+
+
+def test_fastdiv_magic_is_exact():
+    """The kernels' invariant-divisor division (gs_kernels.cuh fdiv): exact
+    for 32-bit numerators at the edges and at random, divisors 2 .. 2^32-1."""
+    import random
+    rnd = random.Random(7)
+    divs = [2, 3, 5, 7, 16, 80, 4096, 65536, 16 * 256, 1 << 31, (1 << 32) - 1, 641, 6700417]
+    divs += [rnd.randrange(2, 1 << 32) for _ in range(200)]
+    for d in divs:
+        m = ((1 << 64) - 1) // d + 1
+        nums = [0, 1, d - 1, d, d + 1, (1 << 32) - 1, ((1 << 32) - 1) // d * d, ((1 << 32) - 1) // d * d - 1]
+        nums += [rnd.randrange(0, 1 << 32) for _ in range(200)]
+        for n in nums:
+            if n < 0:
+                continue
+            r = n * (m >> 32) + ((n * (m & 0xFFFFFFFF)) >> 32)
+            assert (r >> 32) == n // d, (n, d)
