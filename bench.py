@@ -235,7 +235,7 @@ def run_ours(args):
     from paper_2605_00831_b200 import device as D
     from paper_2605_00831_b200 import kv_layout as K
     from paper_2605_00831_b200.coding import CodingScheme, ErasurePattern, check, decoder, encoder
-    from paper_2605_00831_b200.peer import (PeerGroup, ShardLayout, plan_encode_striped,
+    from paper_2605_00831_b200.peer import (PeerGroup, ShardLayout, plan_encode_rotating, plan_encode_striped,
                                             plan_reconstruct_striped)
 
     rank, world, local = env_rank()
@@ -277,8 +277,12 @@ def run_ours(args):
     enc = encoder(scheme)
     launches0 = D.launches()
 
-    plans = [plan_encode_striped(scheme, layout, bases[b], rank, pipeline=pipe, h_parity=h_parity)
-             for b in range(RING_BLOCKS)]
+    if args.encoder == "rotate":     # comparison mode: whole stripes, round-robin parity worker
+        plans = [plan_encode_rotating(scheme, layout, bases[b], rank, pipe, h_parity, first_worker=b)
+                 for b in range(RING_BLOCKS)]
+    else:
+        plans = [plan_encode_striped(scheme, layout, bases[b], rank, pipeline=pipe, h_parity=h_parity)
+                 for b in range(RING_BLOCKS)]
 
     def step(i):
         plans[i % RING_BLOCKS].run(comp.cuda_stream, copy.cuda_stream)
@@ -526,7 +530,10 @@ def run_ours(args):
                            "data_bytes_per_step": data_bytes_step, "parity_d2h_bytes_per_step": d2h_step,
                            "l2": f"inputs > L2: steps rotate over {RING_BLOCKS} distinct decode blocks "
                                  f"({RING_BLOCKS * data_bytes_step // world >> 20} MiB per GPU)",
-                           "parallelism": f"stripes x{world} (peer loads over NVLink)" if world > 1 else
+                           "parallelism": (f"byte-range striping x{world} (peer loads over NVLink)"
+                                           if args.encoder == "stripe" else
+                                           f"rotating whole-stripe encoder x{world} (paper's temporal "
+                                           "balancing; peer loads over NVLink)") if world > 1 else
                            "single GPU holds all 8 TP shards"},
                 "roofline": kern or None, "roofline_k2": kern2 or None, "host_link": host_link, "cpu_baseline": cpu, "e2e": e2e,
                 "recovery_ms": recovery.get("c2_block_one_worker_ms"), "recovery": recovery,
@@ -975,6 +982,8 @@ def main():
     ap.add_argument("--decode-ctx", type=int, default=4096)
     ap.add_argument("--traffic", type=float, default=None,
                     help="ncu dram bytes per K1 launch (from profiles/), echoed into roofline.traffic")
+    ap.add_argument("--encoder", choices=["stripe", "rotate"], default="stripe",
+                    help="N>1: byte-range striping (default) or the paper's rotating per-chunk encoder")
     ap.add_argument("--sweep", action="store_true", help="C5 block-size sweep instead of the C2 step")
     ap.add_argument("--sweep-sizes", default="64K,256K,1M,4M,16M,64M,256M,1G")
     ap.add_argument("--sweep-cpu-s", type=float, default=0.5)

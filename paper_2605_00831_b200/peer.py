@@ -150,6 +150,36 @@ def plan_encode_striped(scheme: CodingScheme, layout: ShardLayout, bases: Sequen
                        off, ln)
 
 
+def rotating_stripes(layout: ShardLayout, rank: int, first_worker: int = 0) -> List[int]:
+    """The paper's temporal balancing: stripe s is encoded
+    whole by the GPU owning parity worker (first_worker + s) mod n, the
+    reference's round-robin next_parity_worker (checkpoint.hpp:21-30)."""
+    return [s for s in range(layout.stripes)
+            if layout.owner((first_worker + s) % layout.n)[0] == rank]
+
+
+def plan_encode_rotating(scheme: CodingScheme, layout: ShardLayout, bases: Sequence[int], rank: int,
+                         pipeline, h_parity, first_worker: int = 0) -> StripedCall:
+    """Comparison mode for the striped encoder: this rank
+    gathers ALL n shards of its rotating stripes over NVLink (peer loads
+    inside K1) and D2H's their whole parity through its own host link, so
+    each stripe's parity crosses one link instead of W."""
+    mine = rotating_stripes(layout, rank, first_worker)
+    if not mine or layout.length == 0:
+        return StripedCall(None, (), 0, 0)
+    enc = encoder(scheme)
+    slots = []
+    for s in mine:
+        for j in range(layout.n):
+            r, _ = layout.owner(j)
+            slots.append(bases[r] + layout.shard_offset(s, j))
+    hp = row_ptrs(h_parity)
+    k = scheme.k
+    outs = [hp[s * k + i] for s in mine for i in range(k)]
+    return StripedCall(L.lib().gs_encode_offload, (pipeline.handle, enc.handle, len(mine), L.ptr_array(slots),
+                                                   L.ptr_array(outs), layout.length), 0, layout.length)
+
+
 def encode_striped(scheme: CodingScheme, layout: ShardLayout, bases: Sequence[int], rank: int,
                    parity_out, stream: int, pipeline=None, h_parity=None, copy_stream=None) -> Tuple[int, int]:
     """K1 over this rank's byte range of all stripes.

@@ -168,3 +168,62 @@ def test_ipc_striped_encode_and_rebuild_two_processes_one_gpu():
     if not torch.cuda.is_available():
         pytest.fail("GPU test collected without a CUDA device")
     _run(_gpu_worker)
+
+
+def test_rotating_assignment_covers_every_stripe_once():
+    """Rotating mode: every stripe is encoded by exactly one rank, the owner
+    of the round-robin parity worker (checkpoint.hpp:21-30)."""
+    from paper_2605_00831_b200.peer import ShardLayout, rotating_stripes
+    for world in (1, 2, 4, 8):
+        for first in (0, 3, 7):
+            lay = ShardLayout(8, world, 37, 4096)
+            got = sorted(s for r in range(world) for s in rotating_stripes(lay, r, first))
+            assert got == list(range(37))
+            for r in range(world):
+                for s in rotating_stripes(lay, r, first):
+                    assert lay.owner((first + s) % 8)[0] == r
+
+
+def _gpu_rotating_worker(rank, world, port, q):
+    import sys
+    sys.path.insert(0, ROOT)
+    try:
+        torch.cuda.set_device(0)
+        from paper_2605_00831_b200 import device as D
+        from paper_2605_00831_b200.coding import CodingScheme
+        from paper_2605_00831_b200.peer import PeerGroup, ShardLayout, plan_encode_rotating, rotating_stripes
+        _init(rank, world, port)
+        scheme = CodingScheme.reed_solomon(N, K)
+        lay = ShardLayout(N, world, S, LEN)
+        nl = lay.n_local
+        mine = torch.stack([torch.from_numpy(np.stack(_shards(s)[rank * nl:(rank + 1) * nl])) for s in range(S)]).cuda()
+        pg = PeerGroup()
+        bases = pg.share(mine)
+        h_par = torch.zeros((S, K, LEN), dtype=torch.uint8).pin_memory()
+        pipe = D.Pipeline(0, 1 << 20)
+        comp, copy = torch.cuda.Stream(), torch.cuda.Stream()
+        torch.cuda.synchronize()
+        dist.barrier()
+        plan_encode_rotating(scheme, lay, bases, rank, pipe, h_par, first_worker=1).run(comp.cuda_stream,
+                                                                                         copy.cuda_stream)
+        copy.synchronize()
+        torch.cuda.synchronize()
+        for s in rotating_stripes(lay, rank, 1):
+            want = O.port().encode(O.RS, N, K, _shards(s))
+            for i in range(K):
+                assert np.array_equal(h_par[s, i].numpy(), want[i]), (rank, s, i)
+        dist.barrier()
+        pg.close()
+        pipe.close()
+        dist.destroy_process_group()
+        q.put((rank, "ok"))
+    except Exception:  # pragma: no cover
+        import traceback
+        q.put((rank, traceback.format_exc()))
+
+
+@pytest.mark.gpu
+def test_ipc_rotating_encode_two_processes_one_gpu():
+    if not torch.cuda.is_available():
+        pytest.fail("GPU test collected without a CUDA device")
+    _run(_gpu_rotating_worker)
