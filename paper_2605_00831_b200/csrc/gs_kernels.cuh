@@ -13,9 +13,10 @@
 //
 //  * Specialised (compile-time coefficients, `k_apply_special`): Horner over
 //    the coefficient bits,  p = (((S7)*2 ^ S6)*2 ^ ...)*2 ^ S0,  where S_b is
-//    the XOR of the sources whose coefficient has bit b set. Multiply-by-2 on
-//    four packed bytes is 2 ALU + 2 FMA-pipe ops (xtime4). Cost per source
-//    word ~ rows*(28/ns + 2) ops -- about 11 for RS(8,2) encode.
+//    the XOR of the sources whose coefficient has bit b set. A Horner step
+//    (x * acc ^ S_b on four packed bytes, xtime4_xor) is 2 ALU + 3 FMA-pipe
+//    ops, the ALU merge absorbing one XOR term. Cost per source word ~
+//    rows*(35/ns + 2) ops -- about 13 for RS(8,2) encode, ~7 of them ALU.
 //
 //  * Generic (runtime coefficients, `k_apply_generic`): split-table lookups
 //    with PRMT. Byte b = lo3 | bit3 | hi3<<4 | bit7, so
@@ -59,6 +60,20 @@ __device__ __forceinline__ uint32_t prmt(uint32_t a, uint32_t b, uint32_t sel) {
 __device__ __forceinline__ uint32_t xtime4(uint32_t a) {
   const uint32_t fold = __umulhi(a & 0x80808080u, 0x3A000000u);
   return ((a + a) & 0xFEFEFEFEu) ^ fold;
+}
+
+// x * a ^ s, the Horner step, balanced across the integer pipes: the ALU
+// (LOP3) does the low-bit mask and one 3-input merge that also absorbs the
+// next XOR term s; the FMA pipe (IMAD) does the top-bit split (a - t, exact:
+// t = a & 0x7F7F7F7F is a submask of a), the shift and the fold. 2 ALU + 3
+// FMA ops instead of 3 ALU + 2 FMA with a separate XOR.
+__device__ __forceinline__ uint32_t xtime4_xor(uint32_t a, uint32_t s) {
+  const uint32_t t = a & 0x7F7F7F7Fu;
+  uint32_t h, t2;
+  asm("mad.lo.u32 %0, %1, %2, %3;" : "=r"(h) : "r"(t), "r"(0xFFFFFFFFu), "r"(a));  // a - t = a & 0x80808080
+  asm("mul.lo.u32 %0, %1, 2;" : "=r"(t2) : "r"(t));
+  const uint32_t fold = __umulhi(h, 0x3A000000u);
+  return t2 ^ fold ^ s;
 }
 
 __device__ __forceinline__ uint4 ld_stream(const uint8_t* p) {
@@ -218,7 +233,6 @@ __device__ __forceinline__ void horner_apply(const uint4 (&src)[Spec::NS], uint4
       bool live = false;
 #pragma unroll
       for (int b = 7; b >= 0; --b) {
-        if (live) acc = xtime4(acc);
         uint32_t s = 0;
         bool any = false;
 #pragma unroll
@@ -227,8 +241,10 @@ __device__ __forceinline__ void horner_apply(const uint4 (&src)[Spec::NS], uint4
             s ^= word(const_cast<uint4&>(src[j]), w);
             any = true;
           }
-        if (any) {
-          acc ^= s;
+        if (live) {
+          acc = xtime4_xor(acc, s);
+        } else if (any) {
+          acc = s;
           live = true;
         }
       }
