@@ -1,5 +1,5 @@
 """K1 at the C2 launch (32 stripes x RS(8,2) x 256 KiB) under tuning env
-overrides (GS_CTAS_PER_SM, GS_FULL_GRID); CUDA-graph timed, 8 rotating
+overrides (GS_CTAS_PER_SM, GS_FULL_GRID, GS_PDL); CUDA-graph timed, 8 rotating
 blocks. Prints us/launch and GB/s per configuration (child processes)."""
 import json
 import os
@@ -37,6 +37,8 @@ if __name__ == "__main__":
         print(json.dumps(child()))
         sys.exit(0)
     confs = [{}, {"GS_FULL_GRID": "1"}] + [{"GS_CTAS_PER_SM": str(c)} for c in (2, 3, 4, 5)]
+    if "--confs" in sys.argv:  # e.g. --confs '[{"GS_PDL": "0"}, {}]'
+        confs = json.loads(sys.argv[sys.argv.index("--confs") + 1])
     for c in confs:
         out = subprocess.check_output([sys.executable, __file__, "--child"], cwd=ROOT,
                                       env=dict(os.environ, **c)).decode().strip().splitlines()[-1]
