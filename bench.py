@@ -46,6 +46,7 @@ BLOCK_TOKENS, BATCH = 16, 32
 SLICE = 262_144                    # slice_bytes(Llama-3-8B, tp 8, m 16)
 RING_BLOCKS = 8                    # distinct decode blocks the steps rotate over (> L2)
 KV_SEED = 3
+NVLINK_GBS = 900.0                 # NVLink 5 per direction per GPU (spec)
 
 
 def env_rank():
@@ -236,7 +237,7 @@ def run_ours(args):
     from paper_2605_00831_b200 import kv_layout as K
     from paper_2605_00831_b200.coding import CodingScheme, ErasurePattern, check, decoder, encoder
     from paper_2605_00831_b200.peer import (PeerGroup, ShardLayout, plan_encode_rotating, plan_encode_striped,
-                                            plan_reconstruct_striped)
+                                            plan_reconstruct_striped, stripe_range)
 
     rank, world, local = env_rank()
     # GS_BENCH_SHARED_GPU=1: functional check of the multi-rank path with all
@@ -328,6 +329,38 @@ def run_ours(args):
 
     # --- kernel-only rooflines: K1 encode and K2 single-loss rebuild ---------
     kern, kern2 = {}, {}
+    peak, peak_src = load_peaks()
+    ks = torch.cuda.Stream(device=dev)
+
+    def timed(launch, alg_bytes, name):
+        with torch.cuda.stream(ks):
+            for b in range(RING_BLOCKS):
+                launch(b)
+        ks.synchronize()
+        reps = 4
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g, stream=ks):
+            for _ in range(reps):
+                for b in range(RING_BLOCKS):
+                    launch(b)
+        n_graph = max(3, args.steps // (reps * RING_BLOCKS))
+        with torch.cuda.stream(ks):
+            g.replay()
+            ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            ev0.record(ks)
+            for _ in range(n_graph):
+                g.replay()
+            ev1.record(ks)
+        ev1.synchronize()
+        per_ms = ev0.elapsed_time(ev1) / (n_graph * reps * RING_BLOCKS)
+        achieved = alg_bytes / (per_ms * 1e-3) / 1e9
+        return {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
+                "frac": round(achieved / peak, 4), "kernel": name,
+                "per_launch_us": round(per_ms * 1e3, 2), "algorithmic_bytes_per_launch": alg_bytes,
+                "peak_source": peak_src,
+                "timing": f"CUDA graph of {reps * RING_BLOCKS} launches over {RING_BLOCKS} distinct "
+                          f"blocks, replayed {n_graph}x, events on the launch stream"}
+
     if world == 1:
         par_dev = torch.empty((RING_BLOCKS, S, K_PARITY, SLICE), dtype=torch.uint8, device=dev)
         rebuilt = torch.empty((RING_BLOCKS, S, SLICE), dtype=torch.uint8, device=dev)
@@ -341,38 +374,6 @@ def run_ours(args):
                                for s in range(S) for j in range(N_SHARDS + K_PARITY)])
                   for b in range(RING_BLOCKS)]
         douts = [L.ptr_array([rebuilt[b, s].data_ptr() for s in range(S)]) for b in range(RING_BLOCKS)]
-        peak, peak_src = load_peaks()
-        ks = torch.cuda.Stream(device=dev)
-
-        def timed(launch, alg_bytes, name):
-            with torch.cuda.stream(ks):
-                for b in range(RING_BLOCKS):
-                    launch(b)
-            ks.synchronize()
-            reps = 4
-            g = torch.cuda.CUDAGraph()
-            with torch.cuda.graph(g, stream=ks):
-                for _ in range(reps):
-                    for b in range(RING_BLOCKS):
-                        launch(b)
-            n_graph = max(3, args.steps // (reps * RING_BLOCKS))
-            with torch.cuda.stream(ks):
-                g.replay()
-                ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-                ev0.record(ks)
-                for _ in range(n_graph):
-                    g.replay()
-                ev1.record(ks)
-            ev1.synchronize()
-            per_ms = ev0.elapsed_time(ev1) / (n_graph * reps * RING_BLOCKS)
-            achieved = alg_bytes / (per_ms * 1e-3) / 1e9
-            return {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
-                    "frac": round(achieved / peak, 4), "kernel": name,
-                    "per_launch_us": round(per_ms * 1e3, 2), "algorithmic_bytes_per_launch": alg_bytes,
-                    "peak_source": peak_src,
-                    "timing": f"CUDA graph of {reps * RING_BLOCKS} launches over {RING_BLOCKS} distinct "
-                              f"blocks, replayed {n_graph}x, events on the launch stream"}
-
         variants = {}
         for v, vname in ((0, "ldg128"), (1, "bulk_smem_pipeline")):
             check(lib.gs_set_kernel_variant(v), "variant")
@@ -423,6 +424,37 @@ def run_ours(args):
         kern["paged_kv_cache_frac"] = kern_paged["frac"]
         del par_dev, rebuilt, caches
 
+    else:
+        # N > 1: the step's own kernel -- K1 over this rank's byte range of all
+        # S stripes, ranges it does not own read from peers over NVLink -- timed
+        # per rank, max over ranks. Roofline t* = max(HBM bytes / HBM peak,
+        # NVLink bytes pulled / NVLink peak).
+        off_r, ln_r = stripe_range(SLICE, rank, world)
+        par_dev = torch.empty((RING_BLOCKS, S, K_PARITY, max(ln_r, 16)), dtype=torch.uint8, device=dev)
+        kplans = [plan_encode_striped(scheme, layout, bases[b], rank, parity_out=par_dev[b])
+                  for b in range(RING_BLOCKS)]
+        alg = S * (N_SHARDS + K_PARITY) * ln_r
+        k = timed(lambda b: kplans[b].run(ks.cuda_stream), alg, "striped K1")
+        t = torch.tensor([k["per_launch_us"]], device="cpu" if shared else dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        per_us = float(t.item())
+        nvl_bytes = S * N_SHARDS * ln_r * (world - 1) // world
+        t_hbm, t_nvl = alg / (peak * 1e3), nvl_bytes / (NVLINK_GBS * 1e3)  # us
+        bound = "nvlink" if t_nvl > t_hbm else "hbm"
+        achieved = alg / per_us / 1e3
+        kern = {"bound": bound, "achieved": round(achieved, 1),
+                "peak": NVLINK_GBS if bound == "nvlink" else peak, "unit": "GB/s",
+                "frac": round(max(t_hbm, t_nvl) / per_us, 4),
+                "kernel": "k_apply_special<EncSpec<RS,8,2>> striped: this rank's byte range of all stripes, "
+                          "peer ranges loaded over NVLink inside the kernel",
+                "per_launch_us": round(per_us, 2), "algorithmic_bytes_per_launch": alg,
+                "nvlink_bytes_per_launch": nvl_bytes,
+                "roofline_us": {"hbm": round(t_hbm, 2), "nvlink": round(t_nvl, 2)},
+                "peak_source": (f"NVLink 5 spec {NVLINK_GBS:.0f} GB/s per direction (not measured)"
+                                if bound == "nvlink" else peak_src),
+                "timing": k["timing"] + ", max over ranks", "traffic": None}
+        del par_dev
+
     # --- host link --------------------------------------------------------------
     link = host_link_peaks(torch, dev)
     d2h_step = S * K_PARITY * SLICE
@@ -432,32 +464,46 @@ def run_ours(args):
                  "peak_h2d_gbs": link["h2d"], "frac": round(link_achieved / link["d2h"], 4)}
 
     # --- e2e through the reference-facing C ABI with host buffers -------------
-    e2e = None
-    if world == 1:
-        per_worker = BATCH * SLICE   # request slices of a worker are contiguous: one stripe
-        h_in = torch.empty((N_SHARDS, per_worker), dtype=torch.uint8).pin_memory()
-        h_out = torch.empty((K_PARITY, per_worker), dtype=torch.uint8).pin_memory()
-        h_in.copy_(ring[0].permute(1, 0, 2).reshape(N_SHARDS, per_worker).cpu())
-        hp_in = L.ptr_array([h_in[j].data_ptr() for j in range(N_SHARDS)])
-        hp_out = L.ptr_array([h_out[i].data_ptr() for i in range(K_PARITY)])
-        epipe = D.Pipeline(local, 256 << 20)
-        for _ in range(max(3, args.warmup)):
-            check(lib.gs_encode_host(epipe.handle, enc.handle, hp_in, hp_out, per_worker), "e2e")
-        torch.cuda.synchronize()
-        t0 = time.perf_counter()
-        for _ in range(args.steps):
-            check(lib.gs_encode_host(epipe.handle, enc.handle, hp_in, hp_out, per_worker), "e2e")
-        torch.cuda.synchronize()
-        dt = time.perf_counter() - t0
-        got = h_out.view(K_PARITY, BATCH, SLICE).permute(1, 0, 2)
-        ok_parity &= torch.equal(got[:2], D.encode(scheme, ring[0, :2]).cpu())
-        e2e = {"value": round(data_bytes_step * args.steps / dt / 1e9, 3), "unit": "GB/s",
-               "h2d_bytes_per_step": N_SHARDS * per_worker, "d2h_bytes_per_step": K_PARITY * per_worker,
-               "ms_per_step": round(dt / args.steps * 1e3, 3),
-               "api": "gs_encode_host (C ABI; drop-in byte semantics of ghostserve::encode), pinned host "
-                      "buffers, wall clock around synchronous calls"}
-        epipe.close()
-        del h_in, h_out
+    # Every rank encodes its own 32 requests (all 8 worker slices each) from
+    # pinned host memory through gs_encode_host on its own host link: H2D of
+    # the data, K1, D2H of the parity, synchronous per call. Wall clock per
+    # rank between barriers, max over ranks.
+    per_worker = BATCH * SLICE   # request slices of a worker are contiguous: one stripe
+    h_in = torch.empty((N_SHARDS, per_worker), dtype=torch.uint8).pin_memory()
+    h_out = torch.empty((K_PARITY, per_worker), dtype=torch.uint8).pin_memory()
+    src = torch.empty((N_SHARDS, BATCH, SLICE), dtype=torch.uint8, device=dev)
+    for j in range(N_SHARDS):
+        for s_ in range(BATCH):
+            K.make_ground_truth_slice(KV_SEED, rank * BATCH + s_, 0, j, cfg, BLOCK_TOKENS, BLOCK_TOKENS,
+                                      out=src[j, s_])
+    h_in.copy_(src.view(N_SHARDS, per_worker).cpu())
+    hp_in = L.ptr_array([h_in[j].data_ptr() for j in range(N_SHARDS)])
+    hp_out = L.ptr_array([h_out[i].data_ptr() for i in range(K_PARITY)])
+    epipe = D.Pipeline(local, 256 << 20)
+    for _ in range(max(3, args.warmup)):
+        check(lib.gs_encode_host(epipe.handle, enc.handle, hp_in, hp_out, per_worker), "e2e")
+    torch.cuda.synchronize()
+    barrier()
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        check(lib.gs_encode_host(epipe.handle, enc.handle, hp_in, hp_out, per_worker), "e2e")
+    torch.cuda.synchronize()
+    dt = time.perf_counter() - t0
+    barrier()
+    if world > 1:
+        t = torch.tensor([dt], dtype=torch.float64, device="cpu" if shared else dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        dt = float(t.item())
+    got = h_out.view(K_PARITY, BATCH, SLICE).permute(1, 0, 2)
+    ok_parity &= torch.equal(got[:2], D.encode(scheme, src[:, :2].permute(1, 0, 2).contiguous()).cpu())
+    e2e = {"value": round(world * BATCH * N_SHARDS * SLICE * args.steps / dt / 1e9, 3), "unit": "GB/s",
+           "h2d_bytes_per_step": world * N_SHARDS * per_worker, "d2h_bytes_per_step": world * K_PARITY * per_worker,
+           "ms_per_step": round(dt / args.steps * 1e3, 3),
+           "api": "gs_encode_host (C ABI; drop-in byte semantics of ghostserve::encode), pinned host "
+                  "buffers, wall clock around synchronous calls" + (", one call per rank, max over ranks"
+                                                                   if world > 1 else "")}
+    epipe.close()
+    del h_in, h_out, src
 
     # --- recovery: one lost worker of the C2 block ----------------------------
     recovery = {}
