@@ -24,6 +24,7 @@ reference CPU codec timed on this host.
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
   python bench.py --sweep [--sweep-sizes 64K,...,1G]     # C5: one JSON line per (code, L)
+  python bench.py --configs [--configs-only C1,C3]       # C1-C4 table incl. reference CPU + bit-exact
 """
 from __future__ import annotations
 
@@ -155,7 +156,8 @@ def cpu_encode_baseline(target_s: float, threads: int):
         busy += blk.run(BATCH, threads)
         done += 1
     gbs = done * BATCH * N_SHARDS * SLICE / busy / 1e9
-    return {"value": round(gbs, 4), "unit": "GB/s", "cores": threads, "kind": blk.kind,
+    from tools.config_table import cpu_model
+    return {"value": round(gbs, 4), "unit": "GB/s", "cores": threads, "kind": blk.kind, "cpu_model": cpu_model(),
             "sample": f"{done} C2 decode blocks (32 requests x RS(8,2) over 8 x 256 KiB), {busy:.2f} s "
                       f"of encode time, {threads} thread(s) taking whole requests"}
 
@@ -1033,7 +1035,17 @@ def main():
     ap.add_argument("--sweep", action="store_true", help="C5 block-size sweep instead of the C2 step")
     ap.add_argument("--sweep-sizes", default="64K,256K,1M,4M,16M,64M,256M,1G")
     ap.add_argument("--sweep-cpu-s", type=float, default=0.5)
+    ap.add_argument("--configs", action="store_true",
+                    help="per-config table C1-C4 (encode+D2H, K1, recovery, rooflines, reference CPU, bit-exact)")
+    ap.add_argument("--configs-only", default="", help="subset for --configs, e.g. C1,C4")
     args = ap.parse_args()
+    if args.configs:
+        if args.impl == "reference":
+            print(json.dumps({"impl": "reference", "unavailable": "--configs is our arm only"}))
+            return
+        from tools.config_table import run_configs
+        run_configs(args)
+        return
     if args.sweep:
         if args.impl == "reference":
             print(json.dumps({"impl": "reference", "unavailable": "--sweep is our arm only"}))

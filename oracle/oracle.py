@@ -207,6 +207,27 @@ class _Ref(_Lib):
         _check(st, "reconstruct")
         return secs.value
 
+    def checkpoint_chunk_timed(self, kind, n, k, model, chunk_size, req, chunk, valid, data, parity):
+        """The reference checkpoint_chunk (encode + seal) on one chunk's n
+        slices; model = (layers, kv_heads, head_dim). Returns (checksum, s)."""
+        secs, cs = C.c_double(0), C.c_uint64(0)
+        st = self.fn("checkpoint_chunk_timed")(kind, n, k, *model, C.c_uint32(chunk_size), C.c_uint64(req),
+                                                C.c_uint32(chunk), C.c_uint32(valid), _ptrs(data), _ptrs(parity),
+                                                C.byref(cs), C.byref(secs))
+        _check(st, "checkpoint_chunk")
+        return cs.value, secs.value
+
+    def reconstruct_chunk_timed(self, kind, n, k, slots: List[Optional[np.ndarray]], outs, sealed: int = 0) -> float:
+        """The reference reconstruct_chunk (FNV verify + reconstruct): slots =
+        n data + k parity arrays, None = lost; rebuilt data -> outs; sealed =
+        the checkpoint-time checksum (0: seal the given parity)."""
+        secs, n_out = C.c_double(0), C.c_int(0)
+        ln = int(next(s for s in slots if s is not None).size)
+        st = self.fn("reconstruct_chunk_timed")(kind, n, k, C.c_uint64(ln), _ptrs(slots),
+                                                 C.c_uint64(sealed), _ptrs(outs), C.byref(n_out), C.byref(secs))
+        _check(st, "reconstruct_chunk")
+        return secs.value
+
 
 _port = None
 _ref = None

@@ -18,6 +18,7 @@
 #include <cstdint>
 #include <cstring>
 #include <map>
+#include <set>
 #include <span>
 #include <stdexcept>
 #include <thread>
@@ -28,6 +29,8 @@
 #include "ghostserve/coding.hpp"
 #include "ghostserve/gf256.hpp"
 #include "ghostserve/parity_store.hpp"
+#include "ghostserve/checkpoint.hpp"
+#include "ghostserve/recovery.hpp"
 
 using namespace ghostserve;
 
@@ -360,6 +363,97 @@ extern "C" int ghs_gsrv_image(int kind, int n, int k, int count, const uint64_t*
     auto bytes = serialize_parity_store(store);
     *size = bytes.size();
     if (out && cap >= bytes.size()) std::memcpy(out, bytes.data(), bytes.size());
+    return 0;
+  } catch (...) {
+    return map_exception();
+  }
+}
+
+// The reference's own per-chunk entry points, timed as the reference bench
+// does (steady_clock around the call): checkpoint_chunk (checkpoint.hpp:123-149:
+// validate, encode, seal) and reconstruct_chunk (recovery.hpp:100-133: FNV
+// verify, reconstruct, wrap). Slices are materialised as KvChunkSlice copies
+// and the ParityChunk is sealed OUTSIDE the timed region.
+namespace {
+ModelConfig model_of(int layers, int kv_heads, int head_dim, int tp) {
+  ModelConfig m;
+  m.layers = layers;
+  m.kv_heads = kv_heads;
+  m.head_dim = head_dim;
+  m.tp_degree = tp;
+  return m;
+}
+}  // namespace
+
+extern "C" int ghs_checkpoint_chunk_timed(int kind, int n, int k, int layers, int kv_heads, int head_dim,
+                                          uint32_t chunk_size, uint64_t req, uint32_t chunk, uint32_t valid,
+                                          const uint8_t* const* data, uint8_t* const* parity,
+                                          uint64_t* checksum, double* secs) {
+  try {
+    CheckpointConfig cfg;
+    cfg.scheme = scheme_of(kind, n, k);
+    cfg.chunk_size = chunk_size;
+    cfg.model = model_of(layers, kv_heads, head_dim, n);
+    const uint64_t len = slice_bytes(cfg.model, chunk_size);
+    std::vector<KvChunkSlice> slices(static_cast<size_t>(n));
+    for (int w = 0; w < n; ++w) {
+      auto& sl = slices[static_cast<size_t>(w)];
+      sl.request_id = req;
+      sl.chunk_id = ChunkId{chunk};
+      sl.worker = w;
+      sl.valid_tokens = valid;
+      sl.bytes.assign(data[w], data[w] + len);
+    }
+    AssignmentState state;
+    const auto t0 = std::chrono::steady_clock::now();
+    auto out = checkpoint_chunk(slices, cfg, state, ChunkTiming{});
+    if (secs) *secs = seconds_since(t0);
+    *checksum = out.parity.checksum;
+    for (int i = 0; i < k; ++i)
+      if (len) std::memcpy(parity[i], out.parity.parity[static_cast<size_t>(i)].data(), len);
+    return 0;
+  } catch (...) {
+    return map_exception();
+  }
+}
+
+// slots[0..n+k): data workers then parity rows; NULL = lost. Rebuilt data
+// workers (ascending) -> out. `sealed` = the checksum stored at checkpoint
+// time (0: seal the given parity here). Returns 4 for kBadParity.
+extern "C" int ghs_reconstruct_chunk_timed(int kind, int n, int k, uint64_t len, const uint8_t* const* slots,
+                                           uint64_t sealed, uint8_t* const* out, int* n_out, double* secs) {
+  try {
+    ParityChunk pc;
+    pc.scheme = scheme_of(kind, n, k);
+    pc.slice_len = len;
+    pc.parity.resize(static_cast<size_t>(k));
+    for (int i = 0; i < k; ++i)
+      if (slots[n + i]) pc.parity[static_cast<size_t>(i)].assign(slots[n + i], slots[n + i] + len);
+    pc.seal();
+    if (sealed) pc.checksum = sealed;
+    std::vector<KvChunkSlice> surviving;
+    std::set<int> failed;
+    for (int w = 0; w < n; ++w) {
+      if (!slots[w]) {
+        failed.insert(w);
+        continue;
+      }
+      KvChunkSlice sl;
+      sl.worker = w;
+      sl.bytes.assign(slots[w], slots[w] + len);
+      surviving.push_back(std::move(sl));
+    }
+    const auto t0 = std::chrono::steady_clock::now();
+    auto res = reconstruct_chunk(ChunkId{0}, surviving, pc, failed);
+    if (secs) *secs = seconds_since(t0);
+    if (res.status != ChunkRepairStatus::kOk) return 4;
+    int b = 0;
+    for (auto& [w, sl] : res.recovered) {
+      (void)w;
+      if (len) std::memcpy(out[b], sl.bytes.data(), len);
+      ++b;
+    }
+    *n_out = b;
     return 0;
   } catch (...) {
     return map_exception();

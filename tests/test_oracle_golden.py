@@ -140,3 +140,35 @@ def test_rs_mds_all_patterns(port):
                 got = port.reconstruct(O.RS, n, k, sh, list(lost))
                 for i, b in got.items():
                     assert np.array_equal(b, data[i])
+
+
+@pytest.mark.skipif(not O.have_ref(), reason="reference not compiled here (oracle/_ref)")
+def test_reference_chunk_entry_points_agree_with_port(port):
+    """The reference's own checkpoint_chunk / reconstruct_chunk (through the
+    oracle/_ref shim; the bench times them as the CPU baseline) produce the
+    same parity, seal and rebuilt bytes as the port: 2 L / 6 H / 64 D, tp 6,
+    RS(6,2), m = 16 (SURVEY §8c fingerprint case), valid = 16 and 5."""
+    ref = O.ref()
+    for valid in (16, 5):
+        data = [port.make_ground_truth_slice(3, 0, 0, w, 2, 6, 64, 6, 16, valid) for w in range(6)]
+        ln = data[0].size
+        par = [np.zeros(ln, np.uint8) for _ in range(2)]
+        cs, secs = ref.checkpoint_chunk_timed(O.RS, 6, 2, (2, 6, 64), 16, 0, 0, valid, data, par)
+        want = port.encode(O.RS, 6, 2, data)
+        assert all(np.array_equal(a, b) for a, b in zip(par, want))
+        assert cs == port.parity_checksum(want) and secs >= 0
+        if valid == 16:
+            assert f"{port.fnv1a64(par[0]):016x}" == "fd24dd05670ae3ce"
+            assert f"{port.fnv1a64(par[1]):016x}" == "d34a1b7a95bdf4e4"
+        slots = list(data) + list(par)
+        slots[1] = slots[4] = None
+        outs = [np.zeros(ln, np.uint8) for _ in range(2)]
+        ref.reconstruct_chunk_timed(O.RS, 6, 2, slots, outs)
+        assert np.array_equal(outs[0], data[1]) and np.array_equal(outs[1], data[4])
+        # corrupted parity -> kBadParity (recovery.hpp:109-112), status 4
+        bad = list(slots)
+        bad[6] = par[0].copy()
+        bad[6][7] ^= 1
+        with pytest.raises(O.OracleError) as ex:
+            ref.reconstruct_chunk_timed(O.RS, 6, 2, bad, outs, sealed=cs)
+        assert ex.value.status == 4
