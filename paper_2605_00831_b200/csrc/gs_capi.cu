@@ -141,6 +141,11 @@ int g_full_grid = [] {
   return e ? std::atoi(e) : 0;
 }();
 constexpr uint64_t kBulkAutoBytes = 128ull << 20;
+// RDP whole-dstripe body on the pipelined kernels (GS_RDP_FAST=0: tile kernels only, for A/B).
+const bool g_rdp_fast = [] {
+  const char* e = std::getenv("GS_RDP_FAST");
+  return !(e && std::atoi(e) == 0);
+}();
 
 int bulk_stages(const SpecialEntry* e) {
   const size_t per = static_cast<size_t>(e->used_cols) * e->tile_bulk;
@@ -521,12 +526,44 @@ int run_rdp(const gs_codec* c, int n_stripes, SlotFn slot_ptr, OutFn out_ptr, ui
       aligned &= aligned16(q);
     }
   }
-  const uint32_t T = static_cast<uint32_t>(rows) * kRdpThreads;
-  const uint64_t tps64 = (len + T - 1) / T;
   const int in_slots = encode ? n : n + 2;
   const int stride = in_slots + c->n_out;
   const int per = kPtrCap / stride;
   if (per < 1) return fail(GS_INVALID_ARGUMENT, "rdp: stripe needs %d pointers (> %d)", stride, kPtrCap);
+  // Whole-dstripe body -> pipelined kernels (16-B aligned columns, whole
+  // 1024-dstripe tiles, >= 2 ring stages); the rest of the range (its last
+  // partial tile and the P/Q tail past the last whole dstripe) -> tile kernels.
+  const uint64_t full_abs = total / rows * rows;
+  const uint32_t TB = rdpb::tile_bytes(p);
+  const size_t fixed = rdpb::kHeader + rdpb::out_bytes(p) + (encode ? 0 : rdpb::chain_bytes(p));
+  const int fast_stages = fixed < rdpb::kSmemBudget
+                              ? static_cast<int>(std::min<size_t>(rdpb::kMaxStages, (rdpb::kSmemBudget - fixed) / TB))
+                              : 0;
+  uint64_t body = 0;
+  if (aligned && fast_stages >= 2 && g_rdp_fast && full_abs > pg.logical0)
+    body = std::min<uint64_t>(len, full_abs - pg.logical0) / TB * TB;
+  const void* kfast = nullptr;
+#define GS_RDP_PICK_FAST(P_)                                                                  \
+  if (p == P_)                                                                                \
+    kfast = encode ? reinterpret_cast<const void*>(&k_rdp_encode_bulk<kPtrCap, P_>)           \
+                   : reinterpret_cast<const void*>(&k_rdp_recover_bulk<kPtrCap, P_>);
+  GS_RDP_PRIMES(GS_RDP_PICK_FAST)
+#undef GS_RDP_PICK_FAST
+  const size_t fast_smem = fixed + static_cast<size_t>(fast_stages) * TB;
+  if (body && kfast) {
+    static std::mutex mu;
+    std::lock_guard<std::mutex> lk(mu);
+    if (cudaFuncSetAttribute(kfast, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(fast_smem)) !=
+        cudaSuccess) {
+      cudaGetLastError();
+      body = 0;
+    }
+  } else {
+    body = 0;
+  }
+  const uint64_t rest = len - body;
+  const uint32_t T = static_cast<uint32_t>(rows) * kRdpThreads;
+  const uint64_t tps64 = (rest + T - 1) / T;
   const size_t smem = static_cast<size_t>(encode ? rows + 2 : p + 1) * T;
   const void* kern = nullptr;
 #define GS_RDP_PICK(P_)                                                                        \
@@ -536,7 +573,7 @@ int run_rdp(const gs_codec* c, int n_stripes, SlotFn slot_ptr, OutFn out_ptr, ui
   GS_RDP_PRIMES(GS_RDP_PICK)
 #undef GS_RDP_PICK
   if (!kern) return fail(GS_UNSUPPORTED, "rdp: no kernel for p = %d", p);
-  const int occ = blocks_per_sm(dev, kern, smem, kRdpThreads);
+  const int occ = rest ? blocks_per_sm(dev, kern, smem, kRdpThreads) : 1;
   std::vector<const void*> ptrs;
   for (int s0 = 0; s0 < n_stripes; s0 += per) {
     const int cnt = std::min(per, n_stripes - s0);
@@ -545,11 +582,43 @@ int run_rdp(const gs_codec* c, int n_stripes, SlotFn slot_ptr, OutFn out_ptr, ui
       for (int j = 0; j < in_slots; ++j) ptrs[s * stride + j] = slot_ptr(s0 + s, j);
       for (int i = 0; i < c->n_out; ++i) ptrs[s * stride + in_slots + i] = out_ptr(s0 + s, i);
     }
-    const uint64_t ntiles = tps64 * cnt;
-    RdpGeom g{n, p, rows, len, pg.logical0, total / rows * rows, total, static_cast<uint32_t>(tps64),
-              static_cast<uint32_t>(ntiles), stride, aligned ? 1 : 0, c->rdp_li, c->rdp_lj};
     PtrTable<kPtrCap> tab;
-    for (int i = 0; i < cnt * stride; ++i) tab.p[i] = static_cast<const uint8_t*>(ptrs[i]);
+    if (body) {
+      const uint64_t ftps = body / TB, fntiles = ftps * cnt;
+      for (int i = 0; i < cnt * stride; ++i) tab.p[i] = static_cast<const uint8_t*>(ptrs[i]);
+      RdpGeom g{n, p, rows, body, pg.logical0, full_abs, total, static_cast<uint32_t>(ftps),
+                static_cast<uint32_t>(fntiles), stride, 1, c->rdp_li, c->rdp_lj, 0, 0};
+      const int grid = static_cast<int>(std::min<uint64_t>(fntiles, static_cast<uint64_t>(sms)));
+      const int threads = (rdpb::kCW + 1) * 32;
+#define GS_RDP_LAUNCH_FAST(P_)                                                                               \
+  if (p == P_) {                                                                                             \
+    if (encode)                                                                                              \
+      k_rdp_encode_bulk<kPtrCap, P_><<<grid, threads, fast_smem, st>>>(tab, g, fast_stages);                 \
+    else                                                                                                     \
+      k_rdp_recover_bulk<kPtrCap, P_><<<grid, threads, fast_smem, st>>>(tab, g, fast_stages, c->n_out,       \
+                                                                        in_slots);                           \
+  }
+      GS_RDP_PRIMES(GS_RDP_LAUNCH_FAST)
+#undef GS_RDP_LAUNCH_FAST
+      cudaError_t e = cudaGetLastError();
+      if (e != cudaSuccess) return fail(GS_CUDA_ERROR, "rdp kernel launch: %s", cudaGetErrorString(e));
+      g_launches.fetch_add(1, std::memory_order_relaxed);
+    }
+    if (!rest) continue;
+    const uint64_t ntiles = tps64 * cnt;
+    RdpGeom g{n, p, rows, rest, pg.logical0 + body, full_abs, total, static_cast<uint32_t>(tps64),
+              static_cast<uint32_t>(ntiles), stride, aligned ? 1 : 0, c->rdp_li, c->rdp_lj, 0, 0};
+    if (!encode && c->rdp_li >= 0) {  // tail coefficients (coding.hpp:415-448)
+      const uint8_t gi = exp2_of(c->rdp_li);
+      if (c->rdp_lj == p - 1) {
+        g.inv = gf_inv(gi);
+      } else {
+        g.gj = exp2_of(c->rdp_lj);
+        g.inv = gf_inv(static_cast<uint8_t>(gi ^ g.gj));
+      }
+    }
+    for (int i = 0; i < cnt * stride; ++i)
+      tab.p[i] = ptrs[i] ? static_cast<const uint8_t*>(ptrs[i]) + body : nullptr;
     const int grid = static_cast<int>(std::min<uint64_t>(ntiles, static_cast<uint64_t>(occ) * sms));
 #define GS_RDP_LAUNCH(P_)                                                                      \
   if (p == P_) {                                                                               \

@@ -41,9 +41,18 @@ struct RdpGeom {
   int aligned;
   // recovery: the two lost array columns (i < j; j == p-1 => row parity lost)
   int li, lj;
+  // recovery tail (coding.hpp:415-448): gj = 2^j, inv = 1 / 2^i (j == p-1)
+  // or 1 / (2^i ^ 2^j)
+  uint8_t gj, inv;
 };
 
-__device__ __forceinline__ uint8_t gf_mul_dev(uint8_t a, uint8_t b) { return gf_mul(a, b); }
+// P/Q tail arithmetic: Q = sum_c 2^c d_c is evaluated by Horner (one
+// multiply-by-x per column); the two remaining general products of the
+// recovery use launch-uniform coefficients computed on the host (RdpGeom
+// gj, inv), so no tail byte runs an inversion.
+__device__ __forceinline__ uint8_t xtime1(uint8_t a) {
+  return static_cast<uint8_t>((a << 1) ^ ((a & 0x80u) ? 0x1Du : 0u));
+}
 
 // (a mod p) for a in (-p, 2p): one compare-and-add instead of an integer
 // division (all the array index arithmetic stays in that range).
@@ -114,33 +123,33 @@ __global__ void __launch_bounds__(kRdpThreads) k_rdp_encode(const PtrTable<CAP> 
       reinterpret_cast<uint4*>(rowp)[v16] = v;
     }
     __syncthreads();
-    // one dstripe per thread
+    // one whole dstripe per thread
     const uint64_t abs0 = g.logical0 + off;
     const uint32_t sb = threadIdx.x * R;
-    if (sb < bytes) {
-      if (abs0 + sb + R <= g.full) {
-        uint8_t dv[R];
+    if (sb < bytes && abs0 + sb + R <= g.full) {
+      uint8_t dv[R];
 #pragma unroll
-        for (int d = 0; d < R; ++d) {
-          uint8_t v = 0;
+      for (int d = 0; d < R; ++d) {
+        uint8_t v = 0;
 #pragma unroll
-          for (int c = 0; c < R; ++c) {
-            const int r = (d - c + P) % P;
-            if (r != P - 1) v ^= data[static_cast<size_t>(c) * T + sb + r];
-          }
-          const int r = (d + 1) % P;  // row-parity column p-1
-          if (r != P - 1) v ^= rowp[sb + r];
-          dv[d] = v;
+        for (int c = 0; c < R; ++c) {
+          const int r = (d - c + P) % P;
+          if (r != P - 1) v ^= data[static_cast<size_t>(c) * T + sb + r];
         }
-#pragma unroll
-        for (int d = 0; d < R; ++d) diag[sb + d] = dv[d];
-      } else {  // tail bytes (only in the range's last tile): Q parity
-        for (uint32_t x = sb; x < bytes && x < sb + R; ++x) {
-          uint8_t v = 0;
-          for (int c = 0; c < n; ++c) v ^= gf_mul_dev(exp2_of(c), data[static_cast<size_t>(c) * T + x]);
-          diag[x] = v;
-        }
+        const int r = (d + 1) % P;  // row-parity column p-1
+        if (r != P - 1) v ^= rowp[sb + r];
+        dv[d] = v;
       }
+#pragma unroll
+      for (int d = 0; d < R; ++d) diag[sb + d] = dv[d];
+    }
+    // tail bytes past the last whole dstripe (only in a column's last tile):
+    // Q = sum_c 2^c * data_c, one byte per thread
+    const uint64_t tail0 = g.full > abs0 ? g.full - abs0 : 0;
+    for (uint64_t x = tail0 + threadIdx.x; x < bytes; x += blockDim.x) {
+      uint8_t v = 0;
+      for (int c = n - 1; c >= 0; --c) v = xtime1(v) ^ data[static_cast<size_t>(c) * T + x];
+      diag[x] = v;
     }
     __syncthreads();
     rdp_store(const_cast<uint8_t*>(tab.p[base + n]) + off, rowp, bytes, g.aligned);
@@ -182,57 +191,56 @@ __global__ void __launch_bounds__(kRdpThreads) k_rdp_recover(const PtrTable<CAP>
     __syncthreads();
     const uint64_t abs0 = g.logical0 + off;
     const uint32_t sb = threadIdx.x * rows;
-    if (sb < bytes) {
+    if (sb < bytes && abs0 + sb + rows <= g.full) {
       uint8_t* ci = col + static_cast<size_t>(i) * T + sb;
       uint8_t* cj = col + static_cast<size_t>(j) * T + sb;
-      if (abs0 + sb + rows <= g.full) {
-        // coding.hpp:384-413: chain (primary i, partner j) then (j, i).
-        for (int pass = 0; pass < 2; ++pass) {
-          const int prim = pass == 0 ? i : j, part = pass == 0 ? j : i;
-          uint8_t* po = pass == 0 ? ci : cj;
-          uint8_t* qo = pass == 0 ? cj : ci;
-          int d = pmod(part - 1, p);
-          const int step = pmod(part - prim, p);
-          while (d != p - 1) {
-            const int r = pmod(d - prim, p);
-            uint8_t v = diag[sb + d];
+      // coding.hpp:384-413: chain (primary i, partner j) then (j, i).
+      for (int pass = 0; pass < 2; ++pass) {
+        const int prim = pass == 0 ? i : j, part = pass == 0 ? j : i;
+        uint8_t* po = pass == 0 ? ci : cj;
+        uint8_t* qo = pass == 0 ? cj : ci;
+        int d = pmod(part - 1, p);
+        const int step = pmod(part - prim, p);
+        while (d != p - 1) {
+          const int r = pmod(d - prim, p);
+          uint8_t v = diag[sb + d];
 #pragma unroll
-            for (int c = 0; c < p; ++c) {
-              if (c == prim) continue;
-              const int rc = pmod(d - c, p);
-              if (rc != p - 1) v ^= col[static_cast<size_t>(c) * T + sb + rc];
-            }
-            po[r] = v;
-            uint8_t w = 0;
-#pragma unroll
-            for (int c = 0; c < p; ++c)
-              if (c != part) w ^= col[static_cast<size_t>(c) * T + sb + r];
-            qo[r] = w;
-            d = pmod(d + step, p);
+          for (int c = 0; c < p; ++c) {
+            if (c == prim) continue;
+            const int rc = pmod(d - c, p);
+            if (rc != p - 1) v ^= col[static_cast<size_t>(c) * T + sb + rc];
           }
+          po[r] = v;
+          uint8_t w = 0;
+#pragma unroll
+          for (int c = 0; c < p; ++c)
+            if (c != part) w ^= col[static_cast<size_t>(c) * T + sb + r];
+          qo[r] = w;
+          d = pmod(d + step, p);
         }
+      }
+    }
+    // coding.hpp:415-448: P/Q algebra on the tail bytes, one byte per thread.
+    const uint64_t tail0 = g.full > abs0 ? g.full - abs0 : 0;
+    for (uint64_t x = tail0 + threadIdx.x; x < bytes; x += blockDim.x) {
+      uint8_t ps = 0, h = 0;
+      for (int c = n - 1; c >= 0; --c) {
+        const uint8_t v = (c == i || c == j) ? 0 : col[static_cast<size_t>(c) * T + x];
+        ps ^= v;
+        h = xtime1(h) ^ v;
+      }
+      const uint8_t qs = diag[x] ^ h;
+      uint8_t* ci = col + static_cast<size_t>(i) * T;
+      uint8_t* cj = col + static_cast<size_t>(j) * T;
+      if (j == p - 1) {
+        const uint8_t di = gf_mul(qs, g.inv);
+        ci[x] = di;
+        cj[x] = static_cast<uint8_t>(ps ^ di);
       } else {
-        // coding.hpp:415-448: P/Q algebra on the tail bytes.
-        for (uint32_t x = sb; x < bytes && x < sb + rows; ++x) {
-          uint8_t ps = 0, qs = diag[x];
-          for (int c = 0; c < n; ++c) {
-            if (c == i || c == j) continue;
-            const uint8_t v = col[static_cast<size_t>(c) * T + x];
-            ps ^= v;
-            qs ^= gf_mul_dev(exp2_of(c), v);
-          }
-          if (j == p - 1) {
-            const uint8_t di = gf_mul_dev(qs, gf_inv(exp2_of(i)));
-            ci[x - sb] = di;
-            cj[x - sb] = static_cast<uint8_t>(ps ^ di);
-          } else {
-            ps ^= col[static_cast<size_t>(p - 1) * T + x];
-            const uint8_t gi = exp2_of(i), gj = exp2_of(j);
-            const uint8_t di = gf_mul_dev(static_cast<uint8_t>(qs ^ gf_mul_dev(gj, ps)), gf_inv(gi ^ gj));
-            ci[x - sb] = di;
-            cj[x - sb] = static_cast<uint8_t>(ps ^ di);
-          }
-        }
+        ps ^= col[static_cast<size_t>(p - 1) * T + x];
+        const uint8_t di = gf_mul(static_cast<uint8_t>(qs ^ gf_mul(g.gj, ps)), g.inv);
+        ci[x] = di;
+        cj[x] = static_cast<uint8_t>(ps ^ di);
       }
     }
     __syncthreads();
@@ -243,6 +251,356 @@ __global__ void __launch_bounds__(kRdpThreads) k_rdp_recover(const PtrTable<CAP>
       rdp_store(const_cast<uint8_t*>(tab.p[base + out0 + o]) + off, col + static_cast<size_t>(j) * T, bytes,
                 g.aligned);
   }
+}
+
+
+// ============================================================================
+// Pipelined RDP kernels (whole-dstripe body of a launch range).
+//
+// Same producer/consumer shape as k_apply_special_bulk: one persistent CTA
+// per SM, a producer warp streams COLUMN tiles (1024 dstripes = 1024*(p-1)
+// bytes of one column) into a shared-memory ring with cp.async.bulk, CW
+// consumer warps take them in column order. Each consumer thread owns 4
+// consecutive dstripes: it loads their 4*(p-1) bytes of a column (LDS.64) and
+// transposes them in registers into p-1 "row words" -- word r = byte r of
+// each of the 4 dstripes (3 PRMT per word). In that domain a diagonal
+// (r + c) mod p is a compile-time register index for every (r, c), so the
+// row parity and all diagonals are plain 32-bit XORs over 4 dstripes at once
+// (the column loop is unrolled over 0..p-2; columns >= n are the virtual
+// zero columns and are skipped). Results are transposed back, staged in
+// shared memory and written with cp.async.bulk (TMA bulk store).
+// ============================================================================
+namespace rdpb {
+
+constexpr int kCW = 8;                                  // consumer warps
+constexpr int kNT = kCW * 32;                           // consumer threads
+constexpr int kDsPerThread = 4;                         // dstripes per thread per tile
+constexpr int kTileDs = kNT * kDsPerThread;             // dstripes per tile (1024)
+constexpr int kMaxStages = 16;
+constexpr size_t kSmemBudget = 220 * 1024;
+constexpr size_t kHeader = 1024;                        // barriers, 128-B aligned data after
+
+__host__ __device__ constexpr uint32_t tile_bytes(int p) { return static_cast<uint32_t>(p - 1) * kTileDs; }
+// chain scratch of the recovery kernel: sr[R], sd[R], ai[R+1], aj[R+1] words per thread
+__host__ __device__ constexpr size_t chain_bytes(int p) { return static_cast<size_t>(4 * (p - 1) + 2) * kNT * 4; }
+__host__ __device__ constexpr size_t out_bytes(int p) { return 2u * 2u * tile_bytes(p); }  // 2 buffers x 2 outputs
+
+// byte q of the thread's 4*R-byte natural block (words w[q >> 2])
+template <int R>
+__device__ __forceinline__ uint32_t nat_byte_sel(int q) { return static_cast<uint32_t>(q & 3); }
+
+// rows[r] = {byte r of dstripe 0, of dstripe 1, of dstripe 2, of dstripe 3}
+template <int R>
+__device__ __forceinline__ void to_rows(const uint32_t (&w)[R], uint32_t (&rows)[R]) {
+#pragma unroll
+  for (int r = 0; r < R; ++r) {
+    const int q0 = r, q1 = R + r, q2 = 2 * R + r, q3 = 3 * R + r;
+    const uint32_t lo = __byte_perm(w[q0 >> 2], w[q1 >> 2], (q0 & 3) | ((4 + (q1 & 3)) << 4));
+    const uint32_t hi = __byte_perm(w[q2 >> 2], w[q3 >> 2], (q2 & 3) | ((4 + (q3 & 3)) << 4));
+    rows[r] = __byte_perm(lo, hi, 0x5410);
+  }
+}
+
+// inverse: natural word v = bytes q = 4v..4v+3, byte q = byte (q / R) of rows[q % R]
+template <int R>
+__device__ __forceinline__ void from_rows(const uint32_t (&rows)[R], uint32_t (&w)[R]) {
+#pragma unroll
+  for (int v = 0; v < R; ++v) {
+    const int q0 = 4 * v, q1 = q0 + 1, q2 = q0 + 2, q3 = q0 + 3;
+    const uint32_t lo = __byte_perm(rows[q0 % R], rows[q1 % R], (q0 / R) | ((4 + q1 / R) << 4));
+    const uint32_t hi = __byte_perm(rows[q2 % R], rows[q3 % R], (q2 / R) | ((4 + q3 / R) << 4));
+    w[v] = __byte_perm(lo, hi, 0x5410);
+  }
+}
+
+template <int R>
+__device__ __forceinline__ void lds_block(const uint8_t* p, uint32_t (&w)[R]) {
+  if constexpr (R % 2 == 0) {
+#pragma unroll
+    for (int v = 0; v < R / 2; ++v) {
+      uint32_t a, b;
+      asm volatile("ld.shared.v2.u32 {%0,%1}, [%2];" : "=r"(a), "=r"(b) : "r"(bulk::smem_u32(p + 8 * v)));
+      w[2 * v] = a;
+      w[2 * v + 1] = b;
+    }
+  } else {
+#pragma unroll
+    for (int v = 0; v < R; ++v)
+      asm volatile("ld.shared.u32 %0, [%1];" : "=r"(w[v]) : "r"(bulk::smem_u32(p + 4 * v)));
+  }
+}
+
+template <int R>
+__device__ __forceinline__ void sts_block(uint8_t* p, const uint32_t (&w)[R]) {
+  if constexpr (R % 2 == 0) {
+#pragma unroll
+    for (int v = 0; v < R / 2; ++v)
+      asm volatile("st.shared.v2.u32 [%0], {%1,%2};" ::"r"(bulk::smem_u32(p + 8 * v)), "r"(w[2 * v]),
+                   "r"(w[2 * v + 1])
+                   : "memory");
+  } else {
+#pragma unroll
+    for (int v = 0; v < R; ++v)
+      asm volatile("st.shared.u32 [%0], %1;" ::"r"(bulk::smem_u32(p + 4 * v)), "r"(w[v]) : "memory");
+  }
+}
+
+__device__ __forceinline__ void bulk_s2g(void* gdst, const void* ssrc, uint32_t bytes) {
+  asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(gdst),
+               "r"(bulk::smem_u32(ssrc)), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void bulk_wait_read() {
+  asm volatile("cp.async.bulk.wait_group.read %0;" ::"n"(N) : "memory");
+}
+__device__ __forceinline__ void bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
+__device__ __forceinline__ void fence_async_smem() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+__device__ __forceinline__ void consumers_sync() { asm volatile("bar.sync 1, %0;" ::"n"(kNT) : "memory"); }
+
+struct Ring {
+  uint64_t* full;
+  uint64_t* empty;
+  uint8_t* data;
+  int stages;
+  uint32_t tb;
+  int stage = 0;
+  uint32_t phase = 0;
+  __device__ __forceinline__ void advance() {
+    if (++stage == stages) {
+      stage = 0;
+      phase ^= 1u;
+    }
+  }
+};
+
+// Producer: for every tile, stream the listed column slots in order.
+template <int CAP>
+__device__ __forceinline__ void rdp_produce(const PtrTable<CAP>& tab, const RdpGeom& g, Ring ring,
+                                            const int* cols, int ncols) {
+  for (uint32_t t = blockIdx.x; t < g.ntiles; t += gridDim.x) {
+    const uint32_t s = t / g.tps;
+    const uint64_t off = static_cast<uint64_t>(t - s * g.tps) * ring.tb;
+    const int base = static_cast<int>(s) * g.stride;
+    for (int u = 0; u < ncols; ++u) {
+      bulk::mbar_wait(&ring.empty[ring.stage], ring.phase ^ 1u);
+      bulk::mbar_expect_tx(&ring.full[ring.stage], ring.tb);
+      bulk::bulk_g2s(ring.data + static_cast<size_t>(ring.stage) * ring.tb, tab.p[base + cols[u]] + off, ring.tb,
+                     &ring.full[ring.stage]);
+      ring.advance();
+    }
+  }
+}
+
+// Consumer: take the next column stage, return the thread's row words.
+template <int R>
+__device__ __forceinline__ void take_rows(Ring& ring, uint32_t (&rows)[R]) {
+  bulk::mbar_wait(&ring.full[ring.stage], ring.phase);
+  uint32_t w[R];
+  lds_block<R>(ring.data + static_cast<size_t>(ring.stage) * ring.tb + threadIdx.x * (4 * R), w);
+  __syncwarp();
+  if ((threadIdx.x & 31) == 0) bulk::mbar_arrive(&ring.empty[ring.stage]);
+  ring.advance();
+  to_rows<R>(w, rows);
+}
+
+__device__ __forceinline__ void init_ring(uint8_t* smem, int stages, Ring& ring, uint32_t tb) {
+  ring.full = reinterpret_cast<uint64_t*>(smem);
+  ring.empty = ring.full + kMaxStages;
+  ring.data = smem + kHeader;
+  ring.stages = stages;
+  ring.tb = tb;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < stages; ++s) {
+      bulk::mbar_init(&ring.full[s], 1);
+      bulk::mbar_init(&ring.empty[s], kCW);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+}
+
+// Stage the thread's natural words of output `o` of buffer `buf`, then (one
+// thread) bulk-store the tile. Buffer reuse is guarded by wait_group.read 1.
+template <int R>
+__device__ __forceinline__ void out_stage(uint8_t* outbuf, int buf, int o, uint32_t tb, const uint32_t (&rows)[R]) {
+  uint32_t w[R];
+  from_rows<R>(rows, w);
+  sts_block<R>(outbuf + (static_cast<size_t>(buf) * 2 + o) * tb + threadIdx.x * (4 * R), w);
+}
+
+}  // namespace rdpb
+
+template <int CAP, int P>
+__global__ void __launch_bounds__((rdpb::kCW + 1) * 32, 1)
+    k_rdp_encode_bulk(const PtrTable<CAP> tab, const RdpGeom g, int stages) {
+  using namespace rdpb;
+  constexpr int R = P - 1;
+  constexpr uint32_t TB = tile_bytes(P);
+  extern __shared__ __align__(128) uint8_t smem[];
+  Ring ring;
+  init_ring(smem, stages, ring, TB);
+  uint8_t* outbuf = ring.data + static_cast<size_t>(stages) * TB;
+  const int n = g.n;
+  if (threadIdx.x >= kNT) {  // producer warp
+    if ((threadIdx.x & 31) == 0) {
+      int cols[kRdpMaxCols];
+      for (int c = 0; c < n; ++c) cols[c] = c;
+      rdp_produce(tab, g, ring, cols, n);
+    }
+    return;
+  }
+  int buf = 0;
+  for (uint32_t t = blockIdx.x; t < g.ntiles; t += gridDim.x) {
+    const uint32_t s = t / g.tps;
+    const uint64_t off = static_cast<uint64_t>(t - s * g.tps) * TB;
+    const int base = static_cast<int>(s) * g.stride;
+    uint32_t rowp[R], diag[R];
+#pragma unroll
+    for (int r = 0; r < R; ++r) rowp[r] = diag[r] = 0;
+#pragma unroll
+    for (int c = 0; c < R; ++c) {  // data columns 0..n-1 of the p-1 array columns
+      if (c < n) {
+        uint32_t a[R];
+        take_rows<R>(ring, a);
+#pragma unroll
+        for (int r = 0; r < R; ++r) {
+          rowp[r] ^= a[r];
+          if ((r + c) % P != P - 1) diag[(r + c) % P] ^= a[r];
+        }
+      }
+    }
+    // row-parity column p-1 on diagonal (r + p - 1) mod p = r - 1
+#pragma unroll
+    for (int r = 1; r < R; ++r) diag[r - 1] ^= rowp[r];
+    // outputs: row parity -> slot n, diagonal parity -> slot n + 1
+    if (threadIdx.x == 0) bulk_wait_read<1>();  // buffer `buf` (two tiles ago) drained
+    consumers_sync();
+    out_stage<R>(outbuf, buf, 0, TB, rowp);
+    out_stage<R>(outbuf, buf, 1, TB, diag);
+    fence_async_smem();
+    consumers_sync();
+    if (threadIdx.x == 0) {
+      bulk_s2g(const_cast<uint8_t*>(tab.p[base + n]) + off, outbuf + (static_cast<size_t>(buf) * 2) * TB, TB);
+      bulk_s2g(const_cast<uint8_t*>(tab.p[base + n + 1]) + off, outbuf + (static_cast<size_t>(buf) * 2 + 1) * TB,
+               TB);
+      bulk_commit();
+    }
+    buf ^= 1;
+  }
+  if (threadIdx.x == 0) bulk_wait_all();
+}
+
+// Two-column recovery (coding.hpp:384-413) on the whole-dstripe body. Lost
+// array columns i < j (j == p-1: row parity lost). Syndromes are accumulated
+// in row words while the surviving columns stream past:
+//   sr[r] = XOR_{c != i,j} A_c[r]            (= A_i[r] ^ A_j[r])
+//   sd[d] = Q[d] ^ XOR_{c != i,j} A_c[(d-c) mod p]
+// then the reference's two zig-zag chains run on the syndromes out of shared
+// memory (their indices depend on the launch-uniform i, j).
+template <int CAP, int P>
+__global__ void __launch_bounds__((rdpb::kCW + 1) * 32, 1)
+    k_rdp_recover_bulk(const PtrTable<CAP> tab, const RdpGeom g, int stages, int n_out, int out0) {
+  using namespace rdpb;
+  constexpr int R = P - 1;
+  constexpr uint32_t TB = tile_bytes(P);
+  extern __shared__ __align__(128) uint8_t smem[];
+  Ring ring;
+  init_ring(smem, stages, ring, TB);
+  uint8_t* outbuf = ring.data + static_cast<size_t>(stages) * TB;
+  uint32_t* chain = reinterpret_cast<uint32_t*>(outbuf + out_bytes(P));
+  const int n = g.n, i = g.li, j = g.lj;
+  if (threadIdx.x >= kNT) {  // producer: surviving array columns ascending, then the diagonal
+    if ((threadIdx.x & 31) == 0) {
+      int cols[kRdpMaxCols + 1];
+      int nc = 0;
+      for (int c = 0; c < n; ++c)
+        if (c != i && c != j) cols[nc++] = c;
+      if (j != P - 1) cols[nc++] = n;  // row parity slot
+      cols[nc++] = n + 1;              // diagonal slot
+      rdp_produce(tab, g, ring, cols, nc);
+    }
+    return;
+  }
+  const int tid = threadIdx.x;
+  uint32_t* sr = chain;
+  uint32_t* sd = chain + R * kNT;
+  uint32_t* ai = chain + 2 * R * kNT;
+  uint32_t* aj = chain + (3 * R + 1) * kNT;
+  auto at = [tid](uint32_t* a, int idx) -> uint32_t& { return a[idx * kNT + tid]; };
+  int buf = 0;
+  for (uint32_t t = blockIdx.x; t < g.ntiles; t += gridDim.x) {
+    const uint32_t s = t / g.tps;
+    const uint64_t off = static_cast<uint64_t>(t - s * g.tps) * TB;
+    const int base = static_cast<int>(s) * g.stride;
+    uint32_t rsyn[R], dsyn[R];
+#pragma unroll
+    for (int r = 0; r < R; ++r) rsyn[r] = dsyn[r] = 0;
+#pragma unroll
+    for (int c = 0; c < P; ++c) {  // array columns; virtual ones (n <= c < p-1) are zero
+      const bool present = (c < n || c == P - 1) && c != i && c != j;
+      if (present) {
+        uint32_t a[R];
+        take_rows<R>(ring, a);
+#pragma unroll
+        for (int r = 0; r < R; ++r) {
+          rsyn[r] ^= a[r];
+          if ((r + c) % P != P - 1) dsyn[(r + c) % P] ^= a[r];
+        }
+      }
+    }
+    {
+      uint32_t q[R];
+      take_rows<R>(ring, q);
+#pragma unroll
+      for (int d = 0; d < R; ++d) dsyn[d] ^= q[d];
+    }
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+      at(sr, r) = rsyn[r];
+      at(sd, r) = dsyn[r];
+      at(ai, r) = 0;
+      at(aj, r) = 0;
+    }
+    at(ai, R) = 0;
+    at(aj, R) = 0;
+    for (int pass = 0; pass < 2; ++pass) {
+      const int prim = pass == 0 ? i : j, part = pass == 0 ? j : i;
+      uint32_t* ap = pass == 0 ? ai : aj;
+      uint32_t* aq = pass == 0 ? aj : ai;
+      int d = pmod(part - 1, P);
+      const int step = pmod(part - prim, P);
+      while (d != P - 1) {
+        const int r = pmod(d - prim, P);
+        const uint32_t v = at(sd, d) ^ at(aq, pmod(d - part, P));
+        at(ap, r) = v;
+        at(aq, r) = at(sr, r) ^ v;
+        d = pmod(d + step, P);
+      }
+    }
+    uint32_t ri[R], rj[R];
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+      ri[r] = at(ai, r);
+      rj[r] = at(aj, r);
+    }
+    if (threadIdx.x == 0) bulk_wait_read<1>();
+    consumers_sync();
+    out_stage<R>(outbuf, buf, 0, TB, ri);
+    if (n_out > 1) out_stage<R>(outbuf, buf, 1, TB, rj);
+    fence_async_smem();
+    consumers_sync();
+    if (threadIdx.x == 0) {
+      bulk_s2g(const_cast<uint8_t*>(tab.p[base + out0]) + off, outbuf + (static_cast<size_t>(buf) * 2) * TB, TB);
+      if (n_out > 1)
+        bulk_s2g(const_cast<uint8_t*>(tab.p[base + out0 + 1]) + off,
+                 outbuf + (static_cast<size_t>(buf) * 2 + 1) * TB, TB);
+      bulk_commit();
+    }
+    buf ^= 1;
+  }
+  if (threadIdx.x == 0) bulk_wait_all();
 }
 
 }  // namespace gsb

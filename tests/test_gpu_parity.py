@@ -320,7 +320,8 @@ def test_rdp_every_pattern_many_lengths(n):
     scheme = G.CodingScheme.rdp(n)
     p = next(q for q in range(n + 1, 64) if all(q % d for d in range(2, q)))
     rows = p - 1
-    for ln in (1, rows - 1, rows, 2 * rows + 1, 256 * rows, 256 * rows + 3, 3 * 256 * rows + 7, 70001):
+    for ln in (1, rows - 1, rows, 2 * rows + 1, 256 * rows, 256 * rows + 3, 3 * 256 * rows + 7, 70001,
+               5 * 1024 * rows + 3):
         S = 3
         host = [[splitmix_bytes(7 * n + 100 * s + j + ln, ln) for j in range(n)] for s in range(S)]
         data = torch.stack([to_dev(h) for h in host])
