@@ -200,6 +200,17 @@ int gs_encode_host(gs_pipeline* p, const gs_codec* enc, const void* const* h_dat
                    void* const* h_parity, size_t len);
 int gs_reconstruct_host(gs_pipeline* p, const gs_codec* dec, const void* const* h_slots,
                         void* const* h_out, size_t len);
+/* Stream-ordered forms for callers that keep several calls in flight (a
+ * serving loop checkpointing block after block from host buffers): return
+ * once enqueued on the pipeline's own streams; host buffers must stay valid
+ * and unmodified until gs_pipeline_sync(p) returns. Successive calls on one
+ * pipeline overlap (the H2D of call i+1 runs under the D2H of call i). */
+int gs_encode_host_async(gs_pipeline* p, const gs_codec* enc, const void* const* h_data,
+                         void* const* h_parity, size_t len);
+int gs_reconstruct_host_async(gs_pipeline* p, const gs_codec* dec, const void* const* h_slots,
+                              void* const* h_out, size_t len);
+/* Wait for everything enqueued on the pipeline. */
+int gs_pipeline_sync(gs_pipeline* p);
 
 /* ---- KV data model (kv_layout.hpp) ------------------------------------- */
 /* slice_bytes (kv_layout.hpp:40-45), validate (:21-28) */

@@ -740,6 +740,15 @@ uint64_t piece_len(uint64_t len, size_t slot, int per_byte, uint64_t cap = ~0ull
   return std::min<uint64_t>(r, len);
 }
 
+// Tapered piece schedule of the host-buffer pipelines: full pieces, then the
+// last full piece's worth split into quarters, so the drain after the final
+// H2D (last kernel + last D2H) is a quarter piece instead of a whole one.
+uint64_t taper(uint64_t r0, uint64_t len, uint64_t rl_max, uint64_t quarter) {
+  const uint64_t left = len - r0;
+  if (left > rl_max || quarter == 0) return std::min<uint64_t>(rl_max, left);
+  return std::min<uint64_t>(quarter, left);
+}
+
 // RDP pieces must cover whole dstripes (p-1 bytes) and stay 4 KiB aligned.
 uint64_t align_piece(const gs_codec* c, uint64_t rl, uint64_t len) {
   if (c->kind != GS_RDP || c->xor_helper) return rl;
@@ -1300,8 +1309,8 @@ static int reconstruct_upload(gs_pipeline* p, const gs_codec* c, int n_stripes, 
 
 // Host buffers in, host buffers out: H2D data -> kernel -> D2H parity, per
 // piece, three streams so both copy directions and the kernel overlap.
-int gs_encode_host(gs_pipeline* p, const gs_codec* c, const void* const* h_data, void* const* h_parity,
-                   size_t len) {
+int gs_encode_host_async(gs_pipeline* p, const gs_codec* c, const void* const* h_data, void* const* h_parity,
+                         size_t len) {
   if (!p || !c) return fail(GS_INVALID_ARGUMENT, "encode_host: NULL pipeline/codec");
   if (c->decoder) return fail(GS_INVALID_ARGUMENT, "encode_host: codec is a decoder");
   if (len == 0) return GS_OK;
@@ -1316,8 +1325,9 @@ int gs_encode_host(gs_pipeline* p, const gs_codec* c, const void* const* h_data,
   // i+1, the kernel of piece i and the D2H of piece i-1 overlap.
   const uint64_t rl_max = align_piece(c, piece_len(len, slot, N + K, kHostPiece), len);
   std::vector<CopyOp> ops;
-  for (uint64_t r0 = 0; r0 < len; r0 += rl_max) {
-    const uint64_t rl = std::min<uint64_t>(rl_max, len - r0);
+  const uint64_t quarter = rl_max >= 4 * 4096 ? align_piece(c, rl_max / 4 / 4096 * 4096, len) : 0;
+  for (uint64_t r0 = 0, rl = 0; r0 < len; r0 += rl) {
+    rl = taper(r0, len, rl_max, quarter);
     const int sl = p->next;
     p->next = (p->next + 1) % gs_pipeline::kSlots;
     uint8_t* in = p->staging + static_cast<size_t>(sl) * slot;
@@ -1341,13 +1351,26 @@ int gs_encode_host(gs_pipeline* p, const gs_codec* c, const void* const* h_data,
     if (int st = issue_copies(ops, cudaMemcpyDeviceToHost, p->s_d2h)) return st;
     GS_CUDA(cudaEventRecord(p->drained[sl], p->s_d2h));
   }
-  GS_CUDA(cudaStreamSynchronize(p->s_d2h));
-  GS_CUDA(cudaStreamSynchronize(p->s_comp));
   return GS_OK;
 }
 
-int gs_reconstruct_host(gs_pipeline* p, const gs_codec* c, const void* const* h_slots, void* const* h_out,
-                        size_t len) {
+int gs_pipeline_sync(gs_pipeline* p) {
+  if (!p) return fail(GS_INVALID_ARGUMENT, "pipeline_sync: NULL pipeline");
+  DeviceGuard g(p->device);
+  GS_CUDA(cudaStreamSynchronize(p->s_h2d));
+  GS_CUDA(cudaStreamSynchronize(p->s_comp));
+  GS_CUDA(cudaStreamSynchronize(p->s_d2h));
+  return GS_OK;
+}
+
+int gs_encode_host(gs_pipeline* p, const gs_codec* c, const void* const* h_data, void* const* h_parity,
+                   size_t len) {
+  if (int st = gs_encode_host_async(p, c, h_data, h_parity, len)) return st;
+  return p ? gs_pipeline_sync(p) : GS_OK;
+}
+
+int gs_reconstruct_host_async(gs_pipeline* p, const gs_codec* c, const void* const* h_slots,
+                              void* const* h_out, size_t len) {
   if (!p || !c) return fail(GS_INVALID_ARGUMENT, "reconstruct_host: NULL pipeline/codec");
   if (!c->decoder) return fail(GS_INVALID_ARGUMENT, "reconstruct_host: codec is an encoder");
   if (len == 0 || c->n_out == 0) return GS_OK;
@@ -1360,8 +1383,9 @@ int gs_reconstruct_host(gs_pipeline* p, const gs_codec* c, const void* const* h_
   const size_t slot = p->slot_bytes();
   const uint64_t rl_max = align_piece(c, piece_len(len, slot, U + E, kHostPiece), len);
   std::vector<CopyOp> ops;
-  for (uint64_t r0 = 0; r0 < len; r0 += rl_max) {
-    const uint64_t rl = std::min<uint64_t>(rl_max, len - r0);
+  const uint64_t quarter = rl_max >= 4 * 4096 ? align_piece(c, rl_max / 4 / 4096 * 4096, len) : 0;
+  for (uint64_t r0 = 0, rl = 0; r0 < len; r0 += rl) {
+    rl = taper(r0, len, rl_max, quarter);
     const int sl = p->next;
     p->next = (p->next + 1) % gs_pipeline::kSlots;
     uint8_t* in = p->staging + static_cast<size_t>(sl) * slot;
@@ -1388,9 +1412,13 @@ int gs_reconstruct_host(gs_pipeline* p, const gs_codec* c, const void* const* h_
     if (int st = issue_copies(ops, cudaMemcpyDeviceToHost, p->s_d2h)) return st;
     GS_CUDA(cudaEventRecord(p->drained[sl], p->s_d2h));
   }
-  GS_CUDA(cudaStreamSynchronize(p->s_d2h));
-  GS_CUDA(cudaStreamSynchronize(p->s_comp));
   return GS_OK;
+}
+
+int gs_reconstruct_host(gs_pipeline* p, const gs_codec* c, const void* const* h_slots, void* const* h_out,
+                        size_t len) {
+  if (int st = gs_reconstruct_host_async(p, c, h_slots, h_out, len)) return st;
+  return p ? gs_pipeline_sync(p) : GS_OK;
 }
 
 // ============================================================================

@@ -123,6 +123,47 @@ def test_host_api_errors():
     assert all(p.size == 0 for p in empty)
 
 
+def test_host_async_calls_in_flight():
+    """gs_encode_host_async / gs_reconstruct_host_async: several calls in
+    flight on one pipeline (distinct host buffers, ragged and tapered piece
+    schedules), one gs_pipeline_sync; every result bit-exact vs the oracle."""
+    from paper_2605_00831_b200 import _lib as L
+    lib = L.lib()
+    pipe = D.Pipeline(0, 1 << 20)  # small ring: many pieces, slot reuse across calls
+    for scheme in (G.CodingScheme.reed_solomon(8, 2), G.CodingScheme.rdp(6)):
+        n, k = scheme.n, scheme.k
+        enc = G.encoder(scheme)
+        calls = []
+        for c, ln in enumerate((300_000, 1 << 18, 4096 * 37 + 5, 1 << 20)):
+            h_in = torch.from_numpy(np.stack([splitmix_bytes(900 + 31 * c + j, ln) for j in range(n)])).pin_memory()
+            h_out = torch.zeros((k, ln), dtype=torch.uint8).pin_memory()
+            pi = L.ptr_array([h_in[j].data_ptr() for j in range(n)])
+            po = L.ptr_array([h_out[i].data_ptr() for i in range(k)])
+            G.check(lib.gs_encode_host_async(pipe.handle, enc.handle, pi, po, ln), "async")
+            calls.append((h_in, h_out, ln))
+        G.check(lib.gs_pipeline_sync(pipe.handle), "sync")
+        for h_in, h_out, ln in calls:
+            want = O.port().encode(int(scheme.kind), n, k, [h_in[j].numpy() for j in range(n)])
+            for i in range(k):
+                assert np.array_equal(h_out[i].numpy(), want[i]), (scheme, ln, i)
+        lost = [1, 3]
+        dec = G.decoder(scheme, G.ErasurePattern(lost))
+        outs = []
+        for h_in, h_out, ln in calls:
+            slots = [None if j in lost else h_in[j].data_ptr() for j in range(n)] + \
+                    [h_out[i].data_ptr() for i in range(k)]
+            o = torch.zeros((len(lost), ln), dtype=torch.uint8).pin_memory()
+            G.check(lib.gs_reconstruct_host_async(pipe.handle, dec.handle, L.ptr_array(slots),
+                                                  L.ptr_array([o[b].data_ptr() for b in range(len(lost))]), ln),
+                    "async rec")
+            outs.append(o)
+        G.check(lib.gs_pipeline_sync(pipe.handle), "sync")
+        for (h_in, _, ln), o in zip(calls, outs):
+            for b, j in enumerate(lost):
+                assert torch.equal(o[b], h_in[j]), (scheme, ln, j)
+    pipe.close()
+
+
 @pytest.mark.parametrize("offset", [0, 1, 3, 8, 15])
 @pytest.mark.parametrize("ln", [1, 15, 16, 17, 4095, 4097, (1 << 20) + 3])
 def test_misaligned_and_ragged_tails(offset, ln):
