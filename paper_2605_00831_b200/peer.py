@@ -132,9 +132,18 @@ class StripedCall:
         check(self.fn(*self.args, stream, copy_stream if copy_stream is not None else stream), "striped")
 
 
+def _host_rows(h_parity, off: int, local: bool) -> List[int]:
+    """Row pointers p such that p + off is where byte `off` of each (stripe,
+    parity row) lands: a full-width [S, k, L] host slab, or (local=True) a
+    range-local [S, k, len_r] slab holding only this rank's byte range."""
+    rows = row_ptrs(h_parity)
+    return [r - off for r in rows] if local else rows
+
+
 def plan_encode_striped(scheme: CodingScheme, layout: ShardLayout, bases: Sequence[int], rank: int,
-                        parity_out=None, pipeline=None, h_parity=None) -> StripedCall:
-    """K1 over this rank's byte range of all stripes (see encode_striped)."""
+                        parity_out=None, pipeline=None, h_parity=None, local_parity: bool = False) -> StripedCall:
+    """K1 over this rank's byte range of all stripes (see encode_striped).
+    local_parity: h_parity is [S, k, len_r] (this rank's range only)."""
     enc = encoder(scheme)
     off, ln, slots = striped_slots(layout, bases, rank)
     if ln == 0:
@@ -145,7 +154,7 @@ def plan_encode_striped(scheme: CodingScheme, layout: ShardLayout, bases: Sequen
         outs = L.ptr_array(row_ptrs(parity_out))
         return StripedCall(lib.gs_apply_device, (enc.handle, layout.stripes, flat, outs, ln), off, ln,
                            two_streams=False)
-    outs = L.ptr_array([p + off for p in row_ptrs(h_parity)])
+    outs = L.ptr_array([p + off for p in _host_rows(h_parity, off, local_parity)])
     return StripedCall(lib.gs_encode_offload, (pipeline.handle, enc.handle, layout.stripes, flat, outs, ln),
                        off, ln)
 
@@ -193,14 +202,15 @@ def encode_striped(scheme: CodingScheme, layout: ShardLayout, bases: Sequence[in
 
 
 def plan_reconstruct_striped(scheme: CodingScheme, layout: ShardLayout, bases: Sequence[int], rank: int,
-                             lost: ErasurePattern, h_parity, pipeline) -> StripedCall:
-    """K2 over this rank's byte range (see reconstruct_striped)."""
+                             lost: ErasurePattern, h_parity, pipeline, local_parity: bool = False) -> StripedCall:
+    """K2 over this rank's byte range (see reconstruct_striped).
+    local_parity: h_parity is [S, k, len_r] (this rank's range only)."""
     dec = decoder(scheme, lost)
     off, ln, slots = striped_slots(layout, bases, rank, lost.lost)
     if ln == 0 or dec.n_out == 0:
         return StripedCall(None, (), off, 0)
     n, k = scheme.n, scheme.k
-    hp = row_ptrs(h_parity)
+    hp = _host_rows(h_parity, off, local_parity)
     full = []
     for s in range(layout.stripes):
         full.extend(slots[s])

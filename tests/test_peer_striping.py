@@ -170,6 +170,73 @@ def test_ipc_striped_encode_and_rebuild_two_processes_one_gpu():
     _run(_gpu_worker)
 
 
+def _gpu_worker_local(rank, world, port, q):
+    """The C3 flow at N ranks: each rank keeps ONLY its byte range of the
+    parity in a range-local pinned slab ([S, K, len_r]), and rebuilds from it."""
+    import sys
+    sys.path.insert(0, ROOT)
+    try:
+        torch.cuda.set_device(0)
+        from paper_2605_00831_b200 import device as D
+        from paper_2605_00831_b200.coding import CodingScheme, ErasurePattern
+        from paper_2605_00831_b200.peer import (PeerGroup, ShardLayout, plan_encode_striped,
+                                                plan_reconstruct_striped)
+        _init(rank, world, port)
+        scheme = CodingScheme.reed_solomon(N, K)
+        lay = ShardLayout(N, world, S, LEN)
+        nl = lay.n_local
+        mine = torch.stack([torch.from_numpy(np.stack(_shards(s)[rank * nl:(rank + 1) * nl])) for s in range(S)]).cuda()
+        pg = PeerGroup()
+        bases = pg.share(mine)
+        pipe = D.Pipeline(0, 1 << 20)
+        comp, copy = torch.cuda.Stream(), torch.cuda.Stream()
+        from paper_2605_00831_b200.peer import stripe_range
+        off, ln = stripe_range(LEN, rank, world)
+        h_loc = torch.zeros((S, K, max(ln, 16)), dtype=torch.uint8).pin_memory()
+        torch.cuda.synchronize()
+        dist.barrier()
+        enc = plan_encode_striped(scheme, lay, bases, rank, pipeline=pipe, h_parity=h_loc, local_parity=True)
+        enc.run(comp.cuda_stream, copy.cuda_stream)
+        copy.synchronize()
+        torch.cuda.synchronize()
+        for s in range(S):
+            want = O.port().encode(O.RS, N, K, _shards(s))
+            for i in range(K):
+                assert np.array_equal(h_loc[s, i, :ln].numpy(), want[i][off:off + ln]), (rank, s, i)
+        lost = 2
+        owner, jl = lay.owner(lost)
+        dist.barrier()
+        if rank == owner:
+            mine[:, jl].zero_()
+        torch.cuda.synchronize()
+        dist.barrier()
+        rec = plan_reconstruct_striped(scheme, lay, bases, rank, ErasurePattern([lost]), h_loc, pipe,
+                                       local_parity=True)
+        rec.run(comp.cuda_stream, copy.cuda_stream)
+        comp.synchronize()
+        torch.cuda.synchronize()
+        dist.barrier()
+        if rank == owner:
+            got = mine[:, jl].cpu().numpy()
+            for s in range(S):
+                assert np.array_equal(got[s], _shards(s)[lost]), s
+        dist.barrier()
+        pg.close()
+        pipe.close()
+        dist.destroy_process_group()
+        q.put((rank, "ok"))
+    except Exception:  # pragma: no cover
+        import traceback
+        q.put((rank, traceback.format_exc()))
+
+
+@pytest.mark.gpu
+def test_ipc_striped_range_local_parity_two_processes_one_gpu():
+    if not torch.cuda.is_available():
+        pytest.fail("GPU test collected without a CUDA device")
+    _run(_gpu_worker_local)
+
+
 def test_rotating_assignment_covers_every_stripe_once():
     """Rotating mode: every stripe is encoded by exactly one rank, the owner
     of the round-robin parity worker (checkpoint.hpp:21-30)."""
