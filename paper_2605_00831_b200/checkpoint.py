@@ -22,7 +22,9 @@ be calibrated from measurements (``CostModel.measured``).
 """
 from __future__ import annotations
 
+import ctypes as C
 import math
+import os
 import time
 from dataclasses import dataclass, field
 from typing import Dict, List, Optional, Sequence, Set
@@ -219,7 +221,9 @@ class RecoveryResult:
     recovered: Dict[int, List[Optional[KvChunkSlice]]] = field(default_factory=dict)
     verified: bool = True
     parity_bytes_fetched: int = 0
-    reconstruct_device_ms: float = 0.0
+    reconstruct_device_ms: float = 0.0   # batched H2D + K2 over every reconstructed chunk
+    verify_host_ms: float = 0.0          # FNV verification of their parity (host threads)
+    wall_ms: float = 0.0                 # plan -> verified, rebuilt bytes on the device
 
 
 def verify_recovery(recovered, ground_truth) -> bool:
@@ -368,8 +372,23 @@ class Checkpointer:
     # recovery.hpp:176-298
     def recover(self, request_id: int, failure: FailureEvent,
                 ground_truth: Optional[List[List[KvChunkSlice]]], chunk_tokens: Sequence[int],
-                buffered_decode_tokens: int = 0) -> RecoveryResult:
+                buffered_decode_tokens: int = 0, verify_threads: int = 0) -> RecoveryResult:
+        """Hybrid recovery with the reference's decisions (recovery.hpp:176-298):
+        r = get_recompute_units(...) chunks recomputed (here restored from the
+        ground-truth slices, the reference's own stand-in, recovery.hpp:269-296)
+        and chunks r..n-1 erasure-decoded, after a planning pass that requires
+        every one of their parity entries to verify (kCorrupt / kMissing ->
+        full-recompute fallback).
+
+        B200 schedule of the same decisions: ONE batched gs_reconstruct_upload
+        (H2D of the used parity rows + K2 over all n-r chunks, pieces pipelined)
+        is enqueued speculatively, and the FNV verification of those entries
+        runs on host threads while it executes; a failed verification discards
+        the decode and falls back exactly as the planning pass would. Each
+        chunk's parity is verified once (the reference re-verifies inside
+        reconstruct_chunk; the store is not modified in between)."""
         cfg = self.cfg
+        t_wall = time.perf_counter()
         if not failure.failed_workers:
             raise InvalidArgument("recovery: no failed workers")
         n = failure.at_chunk
@@ -379,12 +398,25 @@ class Checkpointer:
         plan = result.plan
         over = len(failure.failed_workers) > max_tolerance(cfg.scheme)
         r = n if over else get_recompute_units(n, cfg.chunk_size, cfg.scheme, self.slice, cfg.cost)
+        entries = []
         parity_ok = True
         if not over and r < n:
             for c in range(r, n):
-                if self.store.get(request_id, c)[0] != ParityGetStatus.kOk:
+                st, e = self.store.get(request_id, c, verify=False)
+                if st != ParityGetStatus.kOk or not e.payload_present():
                     parity_ok = False
                     break
+                entries.append(e)
+        failed = set(failure.failed_workers)
+        pending = None
+        if parity_ok and not over and r < n and ground_truth is not None:
+            if len(ground_truth) < n:
+                raise RuntimeError("recovery: ground truth missing for completed chunks")
+            pending = self._enqueue_batched_decode(ground_truth, list(range(r, n)), entries, failed)
+        if parity_ok and entries:   # planning-pass verification, overlapped with the decode
+            t0 = time.perf_counter()
+            parity_ok = all(self._verify_entries(entries, verify_threads))
+            result.verify_host_ms = (time.perf_counter() - t0) * 1e3
         if over or (not parity_ok and r < n):
             plan.mode, r = RecoveryMode.kFullRecomputeFallback, n
         elif r >= n:
@@ -395,35 +427,78 @@ class Checkpointer:
         plan.reconstruct_ids = list(range(r, n))
         result.parity_bytes_fetched = len(plan.reconstruct_ids) * cfg.scheme.k * self.slice
         if ground_truth is None:
+            result.wall_ms = (time.perf_counter() - t_wall) * 1e3
             return result
         if len(ground_truth) < n:
             raise RuntimeError("recovery: ground truth missing for completed chunks")
-        failed = set(failure.failed_workers)
         for w in failure.failed_workers:
             result.recovered[w] = [None] * n
-        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        e0.record(self.compute)
-        for c in range(n):
-            gt = ground_truth[c]
-            if c < r:   # recompute lane stand-in: restore from the oracle slices
-                for w in failure.failed_workers:
-                    result.recovered[w][c] = gt[w]
-                continue
-            rep = self.reconstruct_chunk(c, gt, request_id, failed)
-            if rep.status != ChunkRepairStatus.kOk:
-                raise RuntimeError("recovery: parity failed verification mid-recovery")
+        for c in range(r):   # recompute lane stand-in: restore from the ground-truth slices
             for w in failure.failed_workers:
-                if w not in rep.recovered:
+                result.recovered[w][c] = ground_truth[c][w]
+        if r < n:
+            outs, out_index, e0, e1 = pending
+            e1.synchronize()
+            result.reconstruct_device_ms = e0.elapsed_time(e1)
+            for i, c in enumerate(range(r, n)):
+                for b, w in enumerate(out_index):
+                    result.recovered[w][c] = KvChunkSlice(request_id, c, w, outs[i, b], entries[i].valid_tokens)
+            for w in failure.failed_workers:
+                if any(result.recovered[w][c] is None for c in range(r, n)):
                     raise RuntimeError("recovery: codec did not return a failed shard")
-                result.recovered[w][c] = rep.recovered[w]
-        e1.record(self.compute)
-        e1.synchronize()
-        result.reconstruct_device_ms = e0.elapsed_time(e1)
+        elif pending is not None:
+            pending[3].synchronize()   # discarded speculative decode
+        result.wall_ms = (time.perf_counter() - t_wall) * 1e3
         for c in range(r, n):
             for w in failure.failed_workers:
                 if not verify_recovery(result.recovered[w][c], ground_truth[c][w]):
                     result.verified = False
         return result
+
+    def _verify_entries(self, entries, threads: int) -> List[bool]:
+        """ParityChunk::compute_checksum == checksum for every entry, the
+        chunks spread over host threads (gs_parity_checksum_batch)."""
+        k = entries[0].scheme.k
+        ln = entries[0].slice_len
+        if any(e.scheme.k != k or e.slice_len != ln for e in entries):
+            return [e.compute_checksum() == e.checksum for e in entries]
+        ptrs = L.ptr_array([p.ctypes.data for e in entries for p in e.parity])
+        out = (C.c_uint64 * len(entries))()
+        check(L.lib().gs_parity_checksum_batch(ptrs, len(entries), k, ln, threads or (os.cpu_count() or 1), out),
+              "verify")
+        return [int(out[i]) == e.checksum for i, e in enumerate(entries)]
+
+    def _enqueue_batched_decode(self, ground_truth, chunk_ids, entries, failed):
+        sch = self.cfg.scheme
+        lost = ErasurePattern(sorted(failed))
+        dec = decoder(sch, lost)
+        S = len(chunk_ids)
+        outs = torch.empty((S, max(dec.n_out, 1), self.slice), dtype=torch.uint8, device=self.dev)
+        slots: List[Optional[int]] = []
+        for c, e in zip(chunk_ids, entries):
+            gt = ground_truth[c]
+            row: List[Optional[int]] = [None] * (sch.n + sch.k)
+            for sl in gt:
+                if sl.worker not in failed:
+                    row[sl.worker] = sl.bytes.data_ptr()
+            for i in range(sch.k):
+                row[sch.n + i] = e.parity[i].ctypes.data
+            for j in range(sch.n):
+                if j not in failed and row[j] is None:
+                    raise InvalidArgument(f"coding: surviving shard {j} missing from input")
+            slots.extend(row)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        self.compute.wait_stream(torch.cuda.current_stream(self.dev))
+        e0.record(self.compute)
+        if dec.n_out:
+            check(L.lib().gs_reconstruct_upload(self.pipe.handle, dec.handle, S, L.ptr_array(slots),
+                                                L.ptr_array([outs[i, b].data_ptr() for i in range(S)
+                                                             for b in range(dec.n_out)]),
+                                                self.slice, self.compute.cuda_stream, self.copy.cuda_stream),
+                  "recover")
+        e1.record(self.compute)
+        torch.cuda.current_stream(self.dev).wait_stream(self.compute)
+        return outs, list(dec.out_index), e0, e1
 
 
 class DecodeCheckpointer:

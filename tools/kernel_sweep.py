@@ -44,6 +44,7 @@ def main():
     ap.add_argument("--k", type=int, default=2)
     ap.add_argument("--kind", choices=["rs", "rdp", "xor"], default="rs")
     ap.add_argument("--lost", default="1", help="comma-separated lost shard indices for K2")
+    ap.add_argument("--generic", action="store_true", help="runtime-coefficient (PRMT split-table) back end")
     args = ap.parse_args()
     lib = L.lib()
     dev = torch.device("cuda:0")
@@ -53,8 +54,13 @@ def main():
               "xor": lambda: CodingScheme.xor_code(n)}[args.kind]()
     k = scheme.k
     lost = [int(x) for x in args.lost.split(",")]
-    enc = encoder(scheme)
-    dec = decoder(scheme, ErasurePattern(lost))
+    if args.generic:
+        from paper_2605_00831_b200.coding import codec_ex
+        enc = codec_ex(scheme, generic=True)
+        dec = codec_ex(scheme, ErasurePattern(lost), generic=True)
+    else:
+        enc = encoder(scheme)
+        dec = decoder(scheme, ErasurePattern(lost))
     out = []
     for mib in [float(x) for x in args.sizes.split(",")]:
         L_ = int(mib * (1 << 20)) // 4096 * 4096
@@ -68,7 +74,7 @@ def main():
                            for j in range(n + k)]) for b in range(nbuf)]
         rl = [L.ptr_array([reb[b, i].data_ptr() for i in range(dec.n_out)]) for b in range(nbuf)]
         dec_bytes = (len(dec.coefficients().any(axis=0).nonzero()[0]) + dec.n_out) * L_
-        row = {"kind": args.kind, "mib_per_shard": mib, "bytes_enc": (n + k) * L_, "bytes_dec": dec_bytes}
+        row = {"kind": args.kind, "n": n, "k": k, "generic": args.generic, "mib_per_shard": mib, "bytes_enc": (n + k) * L_, "bytes_dec": dec_bytes}
         for v in (0, 1):
             check(lib.gs_set_kernel_variant(v))
             cnt = [0]
