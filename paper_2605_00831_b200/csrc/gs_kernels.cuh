@@ -261,6 +261,14 @@ __device__ constexpr bool column_used(int j) {
   return false;
 }
 
+template <class Spec>
+__device__ constexpr uint32_t used_mask() {
+  uint32_t m = 0;
+  for (int j = 0; j < Spec::NS && j < 32; ++j)
+    if (column_used<Spec>(j)) m |= 1u << j;
+  return m;
+}
+
 // Each CTA tile covers kThreads * 16 * U bytes of every shard; thread t owns
 // the 16-byte groups t, t + kThreads, ... so every warp access is 512
 // contiguous bytes, and all loads of a tile are issued before any
@@ -291,15 +299,32 @@ __global__ void __launch_bounds__(kThreads) k_apply_special(const PtrTable<CAP> 
       const uint32_t lane_off = threadIdx.x * kVec;
       if (g.paged_slots) soff = paged_offset_tile(g.src, s, tile_logical, lane_off, smask);
       if (g.dst.page_bytes) doff = paged_offset_tile(g.dst, s, tile_logical, lane_off, dmask);
+      constexpr uint32_t used = used_mask<Spec>();
+      if ((g.paged_slots & used) == used) {
+        // every used source is a paged cache with the same geometry (K1 over
+        // a paged KV cache): one address for all of them, and a masked token
+        // (>= valid) is zero in every source, so its parity is zero -- no
+        // loads, no per-source selects.
+        if (!smask) {
 #pragma unroll
-      for (int j = 0; j < Spec::NS; ++j) {
-        src[j] = make_uint4(0, 0, 0, 0);
-        if (column_used<Spec>(j)) {
-          const bool paged = (g.paged_slots >> j) & 1u;
-          if (!(paged && smask)) src[j] = ld_stream(tab.p[base + j] + (paged ? soff : off));
+          for (int j = 0; j < Spec::NS; ++j)
+            src[j] = column_used<Spec>(j) ? ld_stream(tab.p[base + j] + soff) : make_uint4(0, 0, 0, 0);
+          horner_apply<Spec>(src, out);
+        } else {
+#pragma unroll
+          for (int i = 0; i < Spec::NO; ++i) out[i] = make_uint4(0, 0, 0, 0);
         }
+      } else {
+#pragma unroll
+        for (int j = 0; j < Spec::NS; ++j) {
+          src[j] = make_uint4(0, 0, 0, 0);
+          if (column_used<Spec>(j)) {
+            const bool paged = (g.paged_slots >> j) & 1u;
+            if (!(paged && smask)) src[j] = ld_stream(tab.p[base + j] + (paged ? soff : off));
+          }
+        }
+        horner_apply<Spec>(src, out);
       }
-      horner_apply<Spec>(src, out);
       if (!dmask) {
 #pragma unroll
         for (int i = 0; i < Spec::NO; ++i)
