@@ -464,6 +464,18 @@ def run_ours(args):
     host_link = {"d2h_bytes_per_step_per_gpu": d2h_step // world,
                  "achieved_gbs_per_gpu": round(link_achieved, 2), "peak_d2h_gbs": link["d2h"],
                  "peak_h2d_gbs": link["h2d"], "frac": round(link_achieved / link["d2h"], 4)}
+    # roofline of the whole step: t* = the slowest of HBM bytes at
+    # peak, parity over this GPU's host link, peer bytes over NVLink; per GPU
+    hbm_b = S * (N_SHARDS + K_PARITY) * SLICE // world
+    nvl_b = S * N_SHARDS * SLICE * (world - 1) // world // world
+    legs = {"hbm": hbm_b / (load_peaks()[0] * 1e9), "host_link": (d2h_step // world) / (link["d2h"] * 1e9),
+            "nvlink": nvl_b / (NVLINK_GBS * 1e9)}
+    t_star = max(legs.values())
+    step_roofline = {"bound": max(legs, key=legs.get), "t_star_ms": round(t_star * 1e3, 4),
+                     "legs_ms": {k_: round(v * 1e3, 4) for k_, v in legs.items()},
+                     "frac": round(t_star / (ms_step * 1e-3), 4),
+                     "note": "per GPU: HBM (n+k)*L*S/N at the measured copy peak, parity D2H at this GPU's measured "
+                             "link peak, peer reads (N-1)/N of the data over NVLink 5 (900 GB/s spec)"}
 
     # --- e2e through the reference-facing C ABI with host buffers -------------
     # Every rank encodes its own 32 requests (all 8 worker slices each) from
@@ -607,7 +619,8 @@ def run_ours(args):
                                            f"rotating whole-stripe encoder x{world} (paper's temporal "
                                            "balancing; peer loads over NVLink)") if world > 1 else
                            "single GPU holds all 8 TP shards"},
-                "roofline": kern or None, "roofline_k2": kern2 or None, "host_link": host_link, "cpu_baseline": cpu, "e2e": e2e,
+                "roofline": kern or None, "roofline_k2": kern2 or None, "step_roofline": step_roofline,
+                "host_link": host_link, "cpu_baseline": cpu, "e2e": e2e,
                 "recovery_ms": recovery.get("c2_block_one_worker_ms"), "recovery": recovery,
                 "decode_overhead": overhead, "host_tier": host_tier,
                 "gpu_launches": launches, "clocks": clk.summary(), "parity_ok": bool(ok_parity)}
