@@ -156,6 +156,18 @@ int gs_prewarm(int device);
  * bit-identical; exposed for benchmarking and cross-checking. */
 int gs_set_kernel_variant(int variant);
 int gs_pipeline_destroy(gs_pipeline* p);
+/* Live kernel timing of the pipelined calls (encode_offload /
+ * reconstruct_upload): while on, each codec launch group is measured two
+ * ways inside the caller's real schedule: (1) timing events on the compute
+ * stream around the group, after the slot waits; (2) kernel-internal
+ * %globaltimer stamps (first CTA start, last warp's stores performed),
+ * which unlike (1) carry no front-end latency when copy engines are busy on
+ * other streams. kernel_time synchronises and returns both summed times
+ * (device_ms may be NULL), the number of launch groups and of kernel
+ * launches since set_timing / the previous kernel_time, then resets.
+ * Ignored under stream capture. */
+int gs_pipeline_set_timing(gs_pipeline* p, int on);
+int gs_pipeline_kernel_time(gs_pipeline* p, double* event_ms, double* device_ms, int* groups, uint64_t* launches);
 
 /* Checkpoint offload (PAPER Alg.1 / checkpoint.hpp:143-146 + the host tier of
  * parity_store.hpp:77-90): encode device-resident data into staging on

@@ -57,6 +57,8 @@ SIGNATURES = {
     "gs_encode_host_async": (_i, [_vp, _vp, _vpp, _vpp, _sz]),
     "gs_reconstruct_host_async": (_i, [_vp, _vp, _vpp, _vpp, _sz]),
     "gs_pipeline_sync": (_i, [_vp]),
+    "gs_pipeline_set_timing": (_i, [_vp, _i]),
+    "gs_pipeline_kernel_time": (_i, [_vp, C.POINTER(C.c_double), C.POINTER(C.c_double), _ip, _u64p]),
     "gs_slice_bytes": (_i, [_i, _i, _i, _i, _u32, _u64p]),
     "gs_ground_truth_slice_device": (_i, [_u64, _u64, _u32, _i, _i, _i, _i, _i, _u32, _u32, _vp, _vp]),
     "gs_pad_partial_device": (_i, [_vp, _i, _i, _i, _i, _u32, _u32, _vp]),

@@ -323,6 +323,7 @@ struct Paging {
   uint64_t stripe0 = 0;    // absolute index of stripe 0 of this call (block-table rows)
   PageMap src{};
   PageMap dst{};
+  unsigned long long* tstamp = nullptr;  // kernel-internal timing slot (gs_pipeline_set_timing)
   bool any() const { return paged_slots != 0 || dst.page_bytes != 0; }
 };
 
@@ -433,6 +434,7 @@ int run_codec(const gs_codec* c, int n_stripes, SlotFn slot_ptr, OutFn out_ptr, 
       TileGeom g{body, static_cast<uint32_t>(tps64), static_cast<uint32_t>(total), stride, c->n_slots, 1,
                  pg.paged_slots, pg.logical0, pg.src, pg.dst};
       g.tps_m = fastdiv_magic(g.tps);
+      g.tstamp = pg.tstamp;
       if (g.src.table) g.src.table += (pg.stripe0 + s0) * g.src.table_stride;
       if (g.dst.table) g.dst.table += (pg.stripe0 + s0) * g.dst.table_stride;
       const int grid = static_cast<int>(std::min<uint64_t>(total, g_full_grid && !use_bulk ? total : static_cast<uint64_t>(occ) * sms));
@@ -475,6 +477,7 @@ int run_codec(const gs_codec* c, int n_stripes, SlotFn slot_ptr, OutFn out_ptr, 
       TileGeom g{glen, static_cast<uint32_t>(tps64), static_cast<uint32_t>(total), stride, ns + r0,
                  galigned ? 1 : 0, gpaged, pg.logical0 + done, pg.src, pg.dst};
       g.tps_m = fastdiv_magic(g.tps);
+      g.tstamp = pg.tstamp;
       if (g.src.table) g.src.table += (pg.stripe0 + s0) * g.src.table_stride;
       if (g.dst.table) g.dst.table += (pg.stripe0 + s0) * g.dst.table_stride;
       const size_t smem = static_cast<size_t>(kb) * ns * sizeof(CoefWords);
@@ -651,6 +654,48 @@ struct gs_pipeline {
   cudaStream_t s_h2d = nullptr, s_comp = nullptr, s_d2h = nullptr;  // for the *_host calls
   int next = 0;
   size_t slot_bytes() const { return bytes / kSlots / 4096 * 4096; }
+
+  // Optional live kernel timing (gs_pipeline_set_timing): a pair of timing
+  // events on the compute stream brackets each codec launch group of the
+  // pipelined calls -- recorded after the slot waits, so a pair measures the
+  // kernels alone, inside the caller's real schedule. Not under capture.
+  bool timing = false;
+  std::vector<cudaEvent_t> tev;  // 2 per timed launch group
+  size_t tused = 0;
+  uint64_t tlaunch0 = 0;
+  // and a {start, end} %globaltimer pair per group written by the kernels
+  static constexpr size_t kStampSlots = 4096;
+  unsigned long long* d_stamps = nullptr;
+  cudaError_t reset_stamps() {
+    if (!d_stamps) {
+      if (cudaError_t e = cudaMalloc(&d_stamps, kStampSlots * 2 * sizeof(unsigned long long))) return e;
+    }
+    std::vector<unsigned long long> init(kStampSlots * 2);
+    for (size_t i = 0; i < kStampSlots; ++i) {
+      init[2 * i] = ~0ull;
+      init[2 * i + 1] = 0;
+    }
+    return cudaMemcpy(d_stamps, init.data(), init.size() * sizeof(unsigned long long), cudaMemcpyHostToDevice);
+  }
+  unsigned long long* stamp_slot() const {
+    const size_t g = tused / 2;  // group index after timed_begin
+    return (timing && d_stamps && g >= 1 && g <= kStampSlots) ? d_stamps + 2 * (g - 1) : nullptr;
+  }
+  cudaError_t timed_begin(cudaStream_t st, cudaEvent_t* e0, cudaEvent_t* e1) {
+    *e0 = *e1 = nullptr;
+    if (!timing || capturing) return cudaSuccess;
+    if (tused + 2 > tev.size()) {
+      for (int i = 0; i < 512; ++i) {
+        cudaEvent_t e;
+        if (cudaError_t err = cudaEventCreate(&e)) return err;
+        tev.push_back(e);
+      }
+    }
+    *e0 = tev[tused];
+    *e1 = tev[tused + 1];
+    tused += 2;
+    return cudaEventRecord(*e0, st);
+  }
 
   // CUDA-graph capture: while `compute` is being captured,
   // only events recorded inside the same capture may be waited on; slot
@@ -1141,10 +1186,52 @@ int gs_pipeline_create(int device, size_t staging_bytes, gs_pipeline** out) {
   return GS_OK;
 }
 
+int gs_pipeline_set_timing(gs_pipeline* p, int on) {
+  if (!p) return fail(GS_INVALID_ARGUMENT, "pipeline_set_timing: NULL pipeline");
+  DeviceGuard g(p->device);
+  p->timing = on != 0;
+  p->tused = 0;
+  p->tlaunch0 = g_launches.load();
+  if (p->timing) GS_CUDA(p->reset_stamps());
+  return GS_OK;
+}
+
+int gs_pipeline_kernel_time(gs_pipeline* p, double* event_ms, double* device_ms, int* groups, uint64_t* launches) {
+  if (!p || !event_ms || !groups) return fail(GS_INVALID_ARGUMENT, "pipeline_kernel_time: NULL argument");
+  DeviceGuard g(p->device);
+  double sum = 0;
+  for (size_t i = 0; i + 1 < p->tused; i += 2) {
+    GS_CUDA(cudaEventSynchronize(p->tev[i + 1]));
+    float ms = 0;
+    GS_CUDA(cudaEventElapsedTime(&ms, p->tev[i], p->tev[i + 1]));
+    sum += ms;
+  }
+  const size_t n = std::min(p->tused / 2, gs_pipeline::kStampSlots);
+  if (device_ms) {
+    double dsum = 0;
+    if (n && p->d_stamps) {
+      std::vector<unsigned long long> h(2 * n);
+      GS_CUDA(cudaMemcpy(h.data(), p->d_stamps, h.size() * sizeof(unsigned long long), cudaMemcpyDeviceToHost));
+      for (size_t i = 0; i < n; ++i)
+        if (h[2 * i + 1] > h[2 * i] && h[2 * i] != ~0ull) dsum += static_cast<double>(h[2 * i + 1] - h[2 * i]) * 1e-6;
+    }
+    *device_ms = dsum;
+  }
+  *event_ms = sum;
+  *groups = static_cast<int>(p->tused / 2);
+  if (launches) *launches = g_launches.load() - p->tlaunch0;
+  p->tused = 0;
+  p->tlaunch0 = g_launches.load();
+  if (p->timing) GS_CUDA(p->reset_stamps());
+  return GS_OK;
+}
+
 int gs_pipeline_destroy(gs_pipeline* p) {
   if (!p) return GS_OK;
   DeviceGuard g(p->device);
   cudaDeviceSynchronize();
+  for (cudaEvent_t e : p->tev) cudaEventDestroy(e);
+  cudaFree(p->d_stamps);
   for (int i = 0; i < gs_pipeline::kSlots; ++i) {
     cudaEventDestroy(p->ready[i]);
     cudaEventDestroy(p->done[i]);
@@ -1210,7 +1297,11 @@ static int encode_offload(gs_pipeline* p, const gs_codec* c, int n_stripes, cons
         pg.src = to_map(src_map);
         pg.paged_slots = N >= 32 ? ~0u : (1u << N) - 1;
       }
+      cudaEvent_t t0, t1;
+      GS_CUDA(p->timed_begin(cs, &t0, &t1));
+      if (t0) pg.tstamp = p->stamp_slot();
       if (int st = run_codec(c, cnt, src, dst, rl, cs, pg)) return st;
+      if (t1) GS_CUDA(cudaEventRecord(t1, cs));
       GS_CUDA(p->record(cs, 1, sl));
       GS_CUDA(p->wait(ks, 1, sl));
       for (int s = 0; s < cnt; ++s)
@@ -1299,7 +1390,11 @@ static int reconstruct_upload(gs_pipeline* p, const gs_codec* c, int n_stripes, 
         pg.paged_slots = n >= 32 ? ~0u : (1u << n) - 1;  // data slots; parity comes from staging
       }
       if (dst_map) pg.dst = to_map(dst_map);
+      cudaEvent_t t0, t1;
+      GS_CUDA(p->timed_begin(cs, &t0, &t1));
+      if (t0) pg.tstamp = p->stamp_slot();
       if (int st = run_codec(c, cnt, src, dst, rl, cs, pg)) return st;
+      if (t1) GS_CUDA(cudaEventRecord(t1, cs));
       GS_CUDA(p->record(cs, 1, sl));
     }
   }

@@ -167,7 +167,27 @@ struct TileGeom {
   PageMap src;           // mapping of paged source slots
   PageMap dst;           // mapping of the outputs (dst.page_bytes == 0: contiguous)
   uint64_t tps_m;        // fastdiv_magic(tps)
+  // Optional kernel-internal timing (gs_pipeline_set_timing): {first CTA
+  // start, last warp end} in %globaltimer ns, combined with atomics across
+  // every launch of one codec call. nullptr = off.
+  unsigned long long* tstamp;
 };
+
+__device__ __forceinline__ unsigned long long globaltimer_ns() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+__device__ __forceinline__ void stamp_start(const TileGeom& g) {
+  if (g.tstamp && threadIdx.x == 0) atomicMin(&g.tstamp[0], globaltimer_ns());
+}
+// Called by every warp when it has issued its last store.
+__device__ __forceinline__ void stamp_end(const TileGeom& g) {
+  if (g.tstamp) {
+    __threadfence();  // this warp's stores performed
+    if ((threadIdx.x & 31) == 0) atomicMax(&g.tstamp[1], globaltimer_ns());
+  }
+}
 
 __device__ __forceinline__ uint32_t tile_stripe(uint32_t t, const TileGeom& g) { return fdiv(t, g.tps, g.tps_m); }
 
@@ -278,6 +298,7 @@ __device__ constexpr uint32_t used_mask() {
 template <class Spec, int CAP, int U, bool PAGED>
 __global__ void __launch_bounds__(kThreads) k_apply_special(const PtrTable<CAP> tab, const TileGeom g) {
   static_assert(U == 1, "one 16-byte group per thread per tile");
+  stamp_start(g);
   for (uint32_t t = blockIdx.x; t < g.total; t += gridDim.x) {
     const uint32_t s = tile_stripe(t, g);
     const uint64_t off = static_cast<uint64_t>(t - s * g.tps) * kTile + threadIdx.x * kVec;
@@ -332,6 +353,7 @@ __global__ void __launch_bounds__(kThreads) k_apply_special(const PtrTable<CAP> 
       }
     }
   }
+  stamp_end(g);
 }
 
 // ---- generic back end ------------------------------------------------------
@@ -468,6 +490,7 @@ __global__ void __launch_bounds__(kThreads) k_apply_generic(const PtrTable<CAP> 
                                                             int ns) {
   extern __shared__ uint4 smem_coef[];
   CoefWords* sc = reinterpret_cast<CoefWords*>(smem_coef);
+  stamp_start(g);
   for (int i = threadIdx.x; i < KB * ns; i += blockDim.x) sc[i] = coef[i];
   __syncthreads();
 
@@ -484,6 +507,7 @@ __global__ void __launch_bounds__(kThreads) k_apply_generic(const PtrTable<CAP> 
                                     s);
     }
   }
+  stamp_end(g);
 }
 
 // ============================================================================
@@ -583,6 +607,7 @@ __global__ void __launch_bounds__((CW + 1) * 32, 1)
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   __syncthreads();
+  stamp_start(g);
 
   if (warp == CW) {  // ---- producer warp (one elected lane issues) ----
     if (lane == 0) {
@@ -648,6 +673,7 @@ __global__ void __launch_bounds__((CW + 1) * 32, 1)
       phase ^= 1u;
     }
   }
+  stamp_end(g);
 }
 
 }  // namespace gsb
