@@ -224,6 +224,29 @@ int gs_reconstruct_host_async(gs_pipeline* p, const gs_codec* dec, const void* c
 /* Wait for everything enqueued on the pipeline. */
 int gs_pipeline_sync(gs_pipeline* p);
 
+/* ---- one-call forms (the boundary as SURVEY §8b words it) ----------------
+ * Same kernels and pipelines as above, with the staging pipeline implicit: a
+ * per-(calling thread, device) default pipeline (256 MiB staging) is created
+ * on first use and reused.
+ *  gs_codec_create      = gs_encoder_create (coding.hpp:96-118 + :44-60).
+ *  gs_encode_async      : one stripe, n device shards (local or peer-mapped)
+ *                         -> k pinned host parity buffers (checkpoint.hpp:
+ *                         143-146); K1 on `compute`, D2H on `copy`.
+ *  gs_reconstruct_async : lost shard indices (coding.hpp:458-571), index-
+ *                         aligned DEVICE data shards (NULL for lost), the k
+ *                         pinned HOST parity rows (NULL for lost), outputs =
+ *                         the lost data shards ascending (device). The
+ *                         decoder (host Gauss-Jordan) is cached per pattern.
+ *                         Only the parity rows the decode uses are H2D'd.
+ *  gs_sync              : wait for `stream` and the calling thread's default
+ *                         pipelines. */
+int gs_codec_create(int kind, int n, int k, gs_codec** out);
+int gs_encode_async(const gs_codec* enc, const void* const* d_shards, size_t len, void* const* h_parity,
+                    void* compute, void* copy);
+int gs_reconstruct_async(const gs_codec* enc, const int* lost, int n_lost, const void* const* d_survivors,
+                         const void* const* h_parity, void* const* d_out, size_t len, void* stream);
+int gs_sync(void* stream);
+
 /* ---- KV data model (kv_layout.hpp) ------------------------------------- */
 /* slice_bytes (kv_layout.hpp:40-45), validate (:21-28) */
 int gs_slice_bytes(int layers, int kv_heads, int head_dim, int tp, uint32_t chunk_size,

@@ -57,6 +57,10 @@ SIGNATURES = {
     "gs_encode_host_async": (_i, [_vp, _vp, _vpp, _vpp, _sz]),
     "gs_reconstruct_host_async": (_i, [_vp, _vp, _vpp, _vpp, _sz]),
     "gs_pipeline_sync": (_i, [_vp]),
+    "gs_codec_create": (_i, [_i, _i, _i, _vpp]),
+    "gs_encode_async": (_i, [_vp, _vpp, _sz, _vpp, _vp, _vp]),
+    "gs_reconstruct_async": (_i, [_vp, _ip, _i, _vpp, _vpp, _vpp, _sz, _vp]),
+    "gs_sync": (_i, [_vp]),
     "gs_pipeline_set_timing": (_i, [_vp, _i]),
     "gs_pipeline_kernel_time": (_i, [_vp, C.POINTER(C.c_double), C.POINTER(C.c_double), _ip, _u64p]),
     "gs_slice_bytes": (_i, [_i, _i, _i, _i, _u32, _u64p]),

@@ -1402,6 +1402,86 @@ static int reconstruct_upload(gs_pipeline* p, const gs_codec* c, int n_stripes, 
   return GS_OK;
 }
 
+// ---- one-call forms ------------------------------------------
+namespace {
+// Default pipelines live until process exit: they are not destroyed from
+// thread-exit destructors, which may run after the CUDA runtime unloads.
+struct DefaultPipelines {
+  std::map<int, gs_pipeline*> by_dev;
+};
+thread_local DefaultPipelines t_pipes;
+
+int default_pipeline(gs_pipeline** out) {
+  int dev = 0;
+  GS_CUDA(cudaGetDevice(&dev));
+  auto it = t_pipes.by_dev.find(dev);
+  if (it != t_pipes.by_dev.end()) {
+    *out = it->second;
+    return GS_OK;
+  }
+  gs_pipeline* p = nullptr;
+  if (int st = gs_pipeline_create(dev, 256ull << 20, &p)) return st;
+  t_pipes.by_dev[dev] = p;
+  *out = p;
+  return GS_OK;
+}
+
+// decoders cached per (encoder scheme, canonical lost set); process-wide
+std::mutex g_dec_mu;
+std::map<std::tuple<int, int, int, std::vector<int>>, gs_codec*> g_dec_cache;
+}  // namespace
+
+int gs_codec_create(int kind, int n, int k, gs_codec** out) { return gs_encoder_create(kind, n, k, out); }
+
+int gs_encode_async(const gs_codec* enc, const void* const* d_shards, size_t len, void* const* h_parity,
+                    void* compute, void* copy) {
+  if (!enc) return fail(GS_INVALID_ARGUMENT, "encode_async: NULL codec");
+  gs_pipeline* p = nullptr;
+  if (int st = default_pipeline(&p)) return st;
+  return gs_encode_offload(p, enc, 1, d_shards, h_parity, len, compute, copy);
+}
+
+int gs_reconstruct_async(const gs_codec* enc, const int* lost, int n_lost, const void* const* d_survivors,
+                         const void* const* h_parity, void* const* d_out, size_t len, void* stream) {
+  if (!enc) return fail(GS_INVALID_ARGUMENT, "reconstruct_async: NULL codec");
+  if (enc->decoder) return fail(GS_INVALID_ARGUMENT, "reconstruct_async: pass the scheme's encoder codec");
+  if (n_lost < 0 || (n_lost > 0 && !lost)) return fail(GS_INVALID_ARGUMENT, "reconstruct_async: bad lost list");
+  std::vector<int> key_lost(lost, lost + n_lost);
+  std::sort(key_lost.begin(), key_lost.end());
+  key_lost.erase(std::unique(key_lost.begin(), key_lost.end()), key_lost.end());
+  gs_codec* dec = nullptr;
+  {
+    std::lock_guard<std::mutex> lk(g_dec_mu);
+    auto key = std::make_tuple(enc->kind, enc->n, enc->k, key_lost);
+    auto it = g_dec_cache.find(key);
+    if (it != g_dec_cache.end()) {
+      dec = it->second;
+    } else {
+      if (int st = gs_decoder_create(enc->kind, enc->n, enc->k, key_lost.data(),
+                                     static_cast<int>(key_lost.size()), &dec))
+        return st;
+      g_dec_cache[key] = dec;
+    }
+  }
+  if (dec->n_out == 0) return GS_OK;
+  if (!d_survivors || !h_parity || !d_out) return fail(GS_INVALID_ARGUMENT, "reconstruct_async: NULL pointer array");
+  std::vector<const void*> slots(static_cast<size_t>(enc->n + enc->k), nullptr);
+  for (int j = 0; j < enc->n; ++j) slots[j] = d_survivors[j];
+  for (int i = 0; i < enc->k; ++i) slots[enc->n + i] = h_parity[i];
+  for (int idx : key_lost)
+    if (idx >= 0 && idx < enc->n + enc->k) slots[idx] = nullptr;
+  gs_pipeline* p = nullptr;
+  if (int st = default_pipeline(&p)) return st;
+  return gs_reconstruct_upload(p, dec, 1, slots.data(), d_out, len, stream, stream);
+}
+
+int gs_sync(void* stream) {
+  if (stream) GS_CUDA(cudaStreamSynchronize(static_cast<cudaStream_t>(stream)));
+  for (auto& kv : t_pipes.by_dev)
+    if (int st = gs_pipeline_sync(kv.second)) return st;
+  return GS_OK;
+}
+
 // Host buffers in, host buffers out: H2D data -> kernel -> D2H parity, per
 // piece, three streams so both copy directions and the kernel overlap.
 int gs_encode_host_async(gs_pipeline* p, const gs_codec* c, const void* const* h_data, void* const* h_parity,

@@ -164,6 +164,49 @@ def test_host_async_calls_in_flight():
     pipe.close()
 
 
+def test_one_call_abi_forms():
+    """gs_codec_create / gs_encode_async / gs_reconstruct_async / gs_sync (the
+    boundary as SURVEY §8b words it): device shards -> pinned host parity ->
+    rebuilt device shards, every single and double loss of RS(8,2) and RS(6,2),
+    bit-exact vs the oracle."""
+    import ctypes as C
+    from paper_2605_00831_b200 import _lib as L
+    lib = L.lib()
+    st = torch.cuda.current_stream()
+    for (n, k) in ((8, 2), (6, 2)):
+        enc = C.c_void_p()
+        G.check(lib.gs_codec_create(2, n, k, C.byref(enc)), "codec_create")
+        ln = 4096 * 9 + 48
+        host = [splitmix_bytes(700 + 13 * n + j, ln) for j in range(n)]
+        want = O.port().encode(O.RS, n, k, host)
+        data = to_dev(host)
+        hp = torch.zeros((k, ln), dtype=torch.uint8).pin_memory()
+        G.check(lib.gs_encode_async(enc, L.ptr_array([data[j].data_ptr() for j in range(n)]), ln,
+                                    L.ptr_array([hp[i].data_ptr() for i in range(k)]), st.cuda_stream,
+                                    st.cuda_stream), "encode_async")
+        G.check(lib.gs_sync(st.cuda_stream), "sync")
+        for i in range(k):
+            assert np.array_equal(hp[i].numpy(), want[i]), (n, k, i)
+        for e in (1, 2):
+            for lost in itertools.combinations(range(n + k), e):
+                data_lost = [j for j in lost if j < n]
+                out = torch.zeros((max(len(data_lost), 1), ln), dtype=torch.uint8, device="cuda")
+                surv = L.ptr_array([None if j in lost else data[j].data_ptr() for j in range(n)])
+                par = L.ptr_array([None if n + i in lost else hp[i].data_ptr() for i in range(k)])
+                arr = (C.c_int * len(lost))(*lost)
+                G.check(lib.gs_reconstruct_async(enc, arr, len(lost), surv, par,
+                                                 L.ptr_array([out[b].data_ptr() for b in range(len(data_lost))]),
+                                                 ln, st.cuda_stream), "reconstruct_async")
+                G.check(lib.gs_sync(st.cuda_stream), "sync")
+                for b, j in enumerate(data_lost):
+                    assert torch.equal(out[b], data[j]), (n, k, lost)
+        # three losses exceed RS(n,2): the reference's UnrecoverableError
+        arr = (C.c_int * 3)(0, 1, 2)
+        assert lib.gs_reconstruct_async(enc, arr, 3, L.ptr_array([None] * n), L.ptr_array([None] * k),
+                                        L.ptr_array([None] * 3), ln, st.cuda_stream) == L.GS_UNRECOVERABLE
+        lib.gs_codec_destroy(enc)
+
+
 @pytest.mark.parametrize("offset", [0, 1, 3, 8, 15])
 @pytest.mark.parametrize("ln", [1, 15, 16, 17, 4095, 4097, (1 << 20) + 3])
 def test_misaligned_and_ragged_tails(offset, ln):
