@@ -221,4 +221,55 @@ inline std::map<int, std::vector<std::uint8_t>> reconstruct(const CodingScheme& 
   return out;
 }
 
+// ---- device-pointer overloads (the serving engine's calls) -----------------
+// KV already lives in HBM: K1 over n device shards (local or peer-mapped over
+// NVLink), parity D2H'd into k PINNED host buffers (the host tier) on the
+// caller's streams; returns once enqueued (completion = `copy`). The byte
+// work of checkpoint_chunk (checkpoint.hpp:143-146). Streams are
+// cudaStream_t passed as void*.
+inline void encode_device(const CodingScheme& scheme, std::span<const void* const> d_shards, std::size_t len,
+                          std::span<void* const> h_parity, void* compute, void* copy) {
+  scheme.validate();
+  if (static_cast<int>(d_shards.size()) != scheme.n)
+    throw std::invalid_argument("coding: expected " + std::to_string(scheme.n) + " data shards, got " +
+                                std::to_string(d_shards.size()));
+  if (static_cast<int>(h_parity.size()) != scheme.k)
+    throw std::invalid_argument("coding: expected " + std::to_string(scheme.k) + " parity buffers");
+  if (len == 0) return;
+  std::lock_guard<std::mutex> lk(detail::handles().mu);
+  gs_codec* c = detail::codec(scheme, nullptr);
+  detail::check(gs_encode_async(c, d_shards.data(), len, h_parity.data(), compute, copy), "encode");
+}
+
+// Rebuild the lost DATA shards into d_out (ascending shard index) from the
+// index-aligned device survivors (NULL for lost) and the k pinned host parity
+// rows (NULL for lost): decode matrix inverted on the host (coding.hpp:
+// 540-566), only the used parity rows H2D'd, K2 on `stream`; returns once
+// enqueued. reconstruct()'s errors: invalid_argument, UnrecoverableError.
+inline void reconstruct_device(const CodingScheme& scheme, const ErasurePattern& lost,
+                               std::span<const void* const> d_survivors, std::span<const void* const> h_parity,
+                               std::span<void* const> d_out, std::size_t len, void* stream) {
+  scheme.validate();
+  const int total = scheme.n + scheme.k;
+  for (int idx : lost.lost)
+    if (idx < 0 || idx >= total) throw std::invalid_argument("coding: lost shard index out of range");
+  if (static_cast<int>(lost.lost.size()) > max_tolerance(scheme))
+    throw UnrecoverableError("coding: " + std::to_string(lost.lost.size()) + " erasures exceed tolerance " +
+                             std::to_string(max_tolerance(scheme)) + " for scheme " + to_string(scheme.kind));
+  if (static_cast<int>(d_survivors.size()) != scheme.n || static_cast<int>(h_parity.size()) != scheme.k)
+    throw std::invalid_argument("coding: expected n device shards and k parity buffers");
+  int data_lost = 0;
+  for (int idx : lost.lost) data_lost += idx < scheme.n;
+  if (static_cast<int>(d_out.size()) < data_lost) throw std::invalid_argument("coding: too few output buffers");
+  if (len == 0 || data_lost == 0) return;
+  std::lock_guard<std::mutex> lk(detail::handles().mu);
+  gs_codec* c = detail::codec(scheme, nullptr);
+  detail::check(gs_reconstruct_async(c, lost.lost.data(), static_cast<int>(lost.lost.size()), d_survivors.data(),
+                                     h_parity.data(), d_out.data(), len, stream),
+                "reconstruct");
+}
+
+// Wait for `stream` and the calling thread's implicit staging pipelines.
+inline void sync(void* stream) { detail::check(gs_sync(stream), "sync"); }
+
 }  // namespace ghostserve_gpu

@@ -5,9 +5,12 @@
 // infrastructure). Exit code = number of failed checks. Needs a GPU.
 #include <cstdio>
 #include <cstdint>
+#include <cstring>
 #include <map>
 #include <stdexcept>
 #include <vector>
+
+#include <cuda_runtime.h>
 
 #include "ghostserve_gpu/coding.hpp"
 #include "../../oracle/gs_oracle.h"
@@ -112,6 +115,63 @@ int main() {
     gs::CodingScheme{gs::CodeKind::kReedSolomon, 4, 5}.validate();
     CHECK(false, "k>n did not throw");
   } catch (const std::invalid_argument&) {
+  }
+  // device-pointer overloads: KV in HBM -> pinned host parity -> rebuilt in HBM
+  {
+    const size_t len = (size_t{1} << 20) + 48;
+    const auto host = shards(8, len, 4242);
+    std::vector<void*> dptr(8);
+    for (int j = 0; j < 8; ++j) {
+      cudaMalloc(&dptr[static_cast<size_t>(j)], len);
+      cudaMemcpy(dptr[static_cast<size_t>(j)], host[static_cast<size_t>(j)].data(), len, cudaMemcpyHostToDevice);
+    }
+    std::vector<void*> hpar(2);
+    for (auto& h : hpar) cudaMallocHost(&h, len);
+    cudaStream_t st;
+    cudaStreamCreate(&st);
+    std::vector<const void*> din(dptr.begin(), dptr.end());
+    gs::encode_device(rs, din, len, hpar, st, st);
+    gs::sync(st);
+    const auto want = gs::encode(rs, host);
+    for (int i = 0; i < 2; ++i)
+      CHECK(std::memcmp(hpar[static_cast<size_t>(i)], want[static_cast<size_t>(i)].data(), len) == 0,
+            "encode_device parity %d mismatch", i);
+    for (const std::vector<int>& lv : {std::vector<int>{3}, std::vector<int>{2, 7}, std::vector<int>{5, 8}}) {
+      gs::ErasurePattern pat(lv);
+      std::vector<const void*> surv(din);
+      std::vector<const void*> par(hpar.begin(), hpar.end());
+      std::vector<void*> outs;
+      for (int idx : pat.lost) {
+        if (idx < 8) {
+          surv[static_cast<size_t>(idx)] = nullptr;
+          void* o;
+          cudaMalloc(&o, len);
+          outs.push_back(o);
+        } else {
+          par[static_cast<size_t>(idx - 8)] = nullptr;
+        }
+      }
+      gs::reconstruct_device(rs, pat, surv, par, outs, len, st);
+      gs::sync(st);
+      size_t b = 0;
+      std::vector<uint8_t> got(len);
+      for (int idx : pat.lost) {
+        if (idx >= 8) continue;
+        cudaMemcpy(got.data(), outs[b++], len, cudaMemcpyDeviceToHost);
+        CHECK(got == host[static_cast<size_t>(idx)], "reconstruct_device shard %d mismatch", idx);
+      }
+      for (void* o : outs) cudaFree(o);
+    }
+    try {
+      gs::ErasurePattern pat({0, 1, 2});
+      std::vector<void*> outs(3, nullptr);
+      gs::reconstruct_device(rs, pat, din, std::vector<const void*>(hpar.begin(), hpar.end()), outs, len, st);
+      CHECK(false, "device over-tolerance did not throw");
+    } catch (const gs::UnrecoverableError&) {
+    }
+    for (void* d : dptr) cudaFree(d);
+    for (void* h : hpar) cudaFreeHost(h);
+    cudaStreamDestroy(st);
   }
   std::printf("facade_test: %d failure(s), %llu kernels launched\n", failures,
               static_cast<unsigned long long>(gs_kernel_launches()));
