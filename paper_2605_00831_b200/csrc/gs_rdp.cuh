@@ -61,17 +61,39 @@ __device__ __forceinline__ int pmod(int a, int p) {
   return a >= p ? a - p : a;
 }
 
-// Cooperative tile load of `bytes` bytes at src into smem (16-B vectors when
-// aligned, bytes otherwise; zero-fill to `span`).
-__device__ __forceinline__ void rdp_load(uint8_t* dst, const uint8_t* src, uint32_t bytes, uint32_t span,
-                                         bool aligned) {
-  if (aligned) {
-    const uint32_t vec = bytes / 16;
-    for (uint32_t v = threadIdx.x; v < vec; v += blockDim.x)
-      reinterpret_cast<uint4*>(dst)[v] = ld_stream(src + v * 16);
-    for (uint32_t b = vec * 16 + threadIdx.x; b < span; b += blockDim.x) dst[b] = b < bytes ? src[b] : 0;
-  } else {
-    for (uint32_t b = threadIdx.x; b < span; b += blockDim.x) dst[b] = b < bytes ? src[b] : 0;
+// All columns of a tile at once: `cols` sources (nullptr = a zero column)
+// into smem tiles dst + c*T. On the aligned path each thread issues its
+// 16-byte loads of EVERY column before storing any, so the column loads
+// overlap instead of paying one memory latency per column.
+template <int MAXC>
+__device__ __forceinline__ void rdp_load_cols(uint8_t* dst, uint32_t T, const uint8_t* const* src, int cols,
+                                              uint32_t bytes, bool aligned) {
+  if (!aligned) {
+    for (int c = 0; c < cols; ++c) {
+      uint8_t* d = dst + static_cast<size_t>(c) * T;
+      for (uint32_t b = threadIdx.x; b < T; b += blockDim.x) d[b] = (src[c] && b < bytes) ? src[c][b] : 0;
+    }
+    return;
+  }
+  const uint32_t vec = bytes / 16, rem = bytes % 16, nv = T / 16;
+  for (uint32_t v0 = 0; v0 < nv; v0 += blockDim.x) {
+    const uint32_t v = v0 + threadIdx.x;
+    uint4 r[MAXC];
+#pragma unroll
+    for (int c = 0; c < MAXC; ++c) {
+      r[c] = make_uint4(0, 0, 0, 0);
+      if (c < cols && src[c] && v < nv) {
+        if (v < vec)
+          r[c] = ld_stream(src[c] + static_cast<size_t>(v) * 16);
+        else if (v == vec && rem)
+          r[c] = ld_partial(src[c] + static_cast<size_t>(v) * 16, static_cast<int>(rem));
+      }
+    }
+    if (v < nv) {
+#pragma unroll
+      for (int c = 0; c < MAXC; ++c)
+        if (c < cols) reinterpret_cast<uint4*>(dst + static_cast<size_t>(c) * T)[v] = r[c];
+    }
   }
 }
 
@@ -106,10 +128,12 @@ __global__ void __launch_bounds__(kRdpThreads) k_rdp_encode(const PtrTable<CAP> 
     const uint32_t bytes = static_cast<uint32_t>(g.len - off < T ? g.len - off : T);
     const int base = static_cast<int>(s) * g.stride;
     __syncthreads();  // previous tile's smem fully consumed
-    for (int c = 0; c < n; ++c) rdp_load(data + static_cast<size_t>(c) * T, tab.p[base + c] + off, bytes, T, g.aligned);
-    for (int c = n; c < R; ++c)
-      for (uint32_t v = threadIdx.x; v < T / 16; v += blockDim.x)
-        reinterpret_cast<uint4*>(data + static_cast<size_t>(c) * T)[v] = make_uint4(0, 0, 0, 0);
+    {
+      const uint8_t* srcs[R];
+#pragma unroll
+      for (int c = 0; c < R; ++c) srcs[c] = c < n ? tab.p[base + c] + off : nullptr;  // n..p-2: virtual zero
+      rdp_load_cols<R>(data, T, srcs, R, bytes, g.aligned);
+    }
     __syncthreads();
     for (uint32_t v16 = threadIdx.x; v16 < T / 16; v16 += blockDim.x) {  // T = rows * 256: 16-B multiple
       uint4 v = make_uint4(0, 0, 0, 0);
@@ -177,17 +201,18 @@ __global__ void __launch_bounds__(kRdpThreads) k_rdp_recover(const PtrTable<CAP>
     const uint32_t bytes = static_cast<uint32_t>(g.len - off < T ? g.len - off : T);
     const int base = static_cast<int>(s) * g.stride;
     __syncthreads();
-    for (int c = 0; c < p; ++c) {
-      uint8_t* dst = col + static_cast<size_t>(c) * T;
-      const uint8_t* src = c < n ? tab.p[base + c] : (c == p - 1 ? tab.p[base + n] : nullptr);
-      if (c == i || c == j || src == nullptr) {
-        for (uint32_t v = threadIdx.x; v < T / 16; v += blockDim.x)
-          reinterpret_cast<uint4*>(dst)[v] = make_uint4(0, 0, 0, 0);
-      } else {
-        rdp_load(dst, src + off, bytes, T, g.aligned);
+    {
+      // p array columns (lost ones are the outputs being built, virtual ones
+      // zero) followed by the diagonal buffer: p + 1 consecutive smem tiles
+      const uint8_t* srcs[P + 1];
+#pragma unroll
+      for (int c = 0; c < P; ++c) {
+        const uint8_t* src = c < n ? tab.p[base + c] : (c == P - 1 ? tab.p[base + n] : nullptr);
+        srcs[c] = (c == i || c == j || src == nullptr) ? nullptr : src + off;
       }
+      srcs[P] = tab.p[base + n + 1] + off;
+      rdp_load_cols<P + 1>(col, T, srcs, P + 1, bytes, g.aligned);
     }
-    rdp_load(diag, tab.p[base + n + 1] + off, bytes, T, g.aligned);
     __syncthreads();
     const uint64_t abs0 = g.logical0 + off;
     const uint32_t sb = threadIdx.x * rows;
