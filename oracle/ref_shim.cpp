@@ -459,3 +459,26 @@ extern "C" int ghs_reconstruct_chunk_timed(int kind, int n, int k, uint64_t len,
     return map_exception();
   }
 }
+
+// The reference's hybrid recovery planner (recovery.hpp:58-88) on a given
+// cost model (cost_model.hpp:18-24); the orchestration mirror is checked
+// against it.
+extern "C" int ghs_get_recompute_units(uint32_t n, uint32_t chunk_size, int kind, int sn, int sk, uint64_t slice,
+                                       double compute_per_token, double intra_bw, double host_bw,
+                                       double encode_rate, double reconstruct_rate, double fixed_latency,
+                                       double restart, uint32_t* out) {
+  try {
+    CostModel c;
+    c.compute_per_token = compute_per_token;
+    c.intra_bw = intra_bw;
+    c.host_bw = host_bw;
+    c.encode_rate = encode_rate;
+    c.reconstruct_rate = reconstruct_rate;
+    c.fixed_collective_latency = fixed_latency;
+    c.restart_overhead = restart;
+    *out = get_recompute_units(n, chunk_size, scheme_of(kind, sn, sk), slice, c);
+    return 0;
+  } catch (...) {
+    return map_exception();
+  }
+}

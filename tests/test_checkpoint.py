@@ -43,6 +43,32 @@ def test_recompute_units_match_sweep_oracle():
     assert get_recompute_units(32, 2048, CodingScheme.reed_solomon(8, 2), 0, free) == 0
 
 
+@pytest.mark.skipif(not O.have_ref(), reason="reference not compiled here (oracle/_ref)")
+def test_recompute_units_match_the_reference_planner():
+    """Same decisions as the reference's own get_recompute_units (recovery.hpp:
+    58-88, compiled in place) on random cost models, incl. exact ties."""
+    import ctypes as C
+    fn = O.ref().fn("get_recompute_units")
+    fn.argtypes = [C.c_uint32, C.c_uint32, C.c_int, C.c_int, C.c_int, C.c_uint64] + [C.c_double] * 7 + \
+        [C.POINTER(C.c_uint32)]
+    rng = random.Random(7)
+    out = C.c_uint32()
+    for i in range(2000):
+        cost = CostModel(compute_per_token=rng.uniform(1e-7, 1e-3), intra_bw=rng.uniform(50e9, 900e9))
+        cost.host_bw = rng.uniform(0.5e9, cost.intra_bw)
+        cost.encode_rate = rng.uniform(10e9, 500e9)
+        cost.reconstruct_rate = rng.uniform(10e9, 500e9)
+        cost.fixed_collective_latency = rng.uniform(0, 1e-4) if i % 5 else 0.0
+        cost.restart_overhead = rng.uniform(0, 5.0) if i % 7 else 0.0
+        n, m = rng.randrange(300), 1 + rng.randrange(4096)
+        slice_ = rng.randrange(200 << 20) if i % 11 else 0
+        k = 1 + rng.randrange(4)
+        scheme = CodingScheme.reed_solomon(8, k)
+        assert fn(n, m, 2, 8, k, slice_, cost.compute_per_token, cost.intra_bw, cost.host_bw, cost.encode_rate,
+                  cost.reconstruct_rate, cost.fixed_collective_latency, cost.restart_overhead, C.byref(out)) == 0
+        assert get_recompute_units(n, m, scheme, slice_, cost) == out.value, (i, n, m, k, slice_)
+
+
 def test_round_robin_fairness_and_config_validation():
     rng = random.Random(777)  # acceptance.cpp C7
     for _ in range(300):
