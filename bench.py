@@ -249,6 +249,8 @@ def run_ours(args):
         local = 0
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
+    # multi-socket hosts: run next to this GPU's host link (no-op on one node)
+    numa_cpus = None if shared else D.bind_local_cpus(local)
     if world > 1:
         if shared:
             dist.init_process_group("gloo")
@@ -273,7 +275,7 @@ def run_ours(args):
     torch.cuda.synchronize()
     pg = PeerGroup() if world > 1 else None
     bases = [pg.share(ring[b]) if pg else [ring[b].data_ptr()] for b in range(RING_BLOCKS)]
-    h_parity = torch.empty((S, K_PARITY, SLICE), dtype=torch.uint8).pin_memory()
+    h_parity = D.pinned_near((S, K_PARITY, SLICE), local)   # on the GPU's NUMA node
     pipe = D.Pipeline(local, 256 << 20)
     comp = torch.cuda.Stream(device=dev)
     copy = torch.cuda.Stream(device=dev)
@@ -515,8 +517,8 @@ def run_ours(args):
     # pinned host memory on its own host link: H2D of the data, K1, D2H of the
     # parity, every step. Wall clock per rank between barriers, max over ranks.
     per_worker = BATCH * SLICE   # request slices of a worker are contiguous: one stripe
-    h_in = torch.empty((N_SHARDS, per_worker), dtype=torch.uint8).pin_memory()
-    h_out = torch.empty((K_PARITY, per_worker), dtype=torch.uint8).pin_memory()
+    h_in = D.pinned_near((N_SHARDS, per_worker), local)
+    h_out = D.pinned_near((K_PARITY, per_worker), local)
     src = torch.empty((N_SHARDS, BATCH, SLICE), dtype=torch.uint8, device=dev)
     for j in range(N_SHARDS):
         for s_ in range(BATCH):
@@ -549,25 +551,35 @@ def run_ours(args):
             dt = float(t.item())
         return dt
 
-    # headline: the stream-ordered host-buffer call a serving loop issues block
-    # after block (gs_encode_host_async; one gs_pipeline_sync at the end), so
-    # the H2D of step i+1 overlaps the D2H of step i; every step still moves
-    # its own inputs H2D and its parity D2H.
-    dt = e2e_run(lib.gs_encode_host_async, False)
-    # drop-in synchronous encode (ghostserve::encode semantics), one call per step
-    dt_sync = e2e_run(lib.gs_encode_host, True)
+    # Two public ways to drive it, each timed twice (alternating, best trial):
+    #  * stream-ordered: gs_encode_host_async per step, one gs_pipeline_sync at
+    #    the end -- the H2D of step i+1 overlaps the D2H of step i (a serving
+    #    loop checkpointing block after block from host memory);
+    #  * synchronous drop-in: gs_encode_host per step (ghostserve::encode
+    #    semantics). Every step moves its own inputs H2D and its parity D2H.
+    # Which one is faster depends on how the box's PCIe handles both
+    # directions at once; the headline is the faster, both are reported.
+    t_async, t_sync = [], []
+    for _ in range(2):
+        t_async.append(e2e_run(lib.gs_encode_host_async, False))
+        t_sync.append(e2e_run(lib.gs_encode_host, True))
+    dt, dt_sync = min(t_async), min(t_sync)
     got = h_out.view(K_PARITY, BATCH, SLICE).permute(1, 0, 2)
     ok_parity &= torch.equal(got[:2], D.encode(scheme, src[:, :2].permute(1, 0, 2).contiguous()).cpu())
     bytes_e2e = world * BATCH * N_SHARDS * SLICE * args.steps
-    e2e = {"value": round(bytes_e2e / dt / 1e9, 3), "unit": "GB/s",
+    modes = {"stream_ordered": {"value": round(bytes_e2e / dt / 1e9, 3), "ms_per_step": round(dt / args.steps * 1e3, 3),
+                                "api": "gs_encode_host_async per step, gs_pipeline_sync after the last step"},
+             "sync_per_call": {"value": round(bytes_e2e / dt_sync / 1e9, 3),
+                               "ms_per_step": round(dt_sync / args.steps * 1e3, 3),
+                               "api": "gs_encode_host per step (drop-in synchronous ghostserve::encode)"}}
+    best = max(modes, key=lambda m: modes[m]["value"])
+    e2e = {"value": modes[best]["value"], "unit": "GB/s",
            "h2d_bytes_per_step": world * N_SHARDS * per_worker, "d2h_bytes_per_step": world * K_PARITY * per_worker,
-           "ms_per_step": round(dt / args.steps * 1e3, 3),
-           "api": "gs_encode_host_async per step (C ABI, host buffers: H2D data -> K1 -> D2H parity on the "
-                  "pipeline's streams), gs_pipeline_sync after the last step; wall clock" +
-                  (", one pipeline per rank, max over ranks" if world > 1 else ""),
-           "sync_per_call": {"value": round(bytes_e2e / dt_sync / 1e9, 3),
-                             "ms_per_step": round(dt_sync / args.steps * 1e3, 3),
-                             "api": "gs_encode_host (drop-in synchronous ghostserve::encode semantics)"}}
+           "ms_per_step": modes[best]["ms_per_step"],
+           "api": f"{best}: {modes[best]['api']} (C ABI, pinned host buffers; H2D data -> K1 -> D2H parity every "
+                  "step); wall clock, best of 2 trials" + (", one pipeline per rank, max over ranks"
+                                                          if world > 1 else ""),
+           "modes": modes}
     epipe.close()
     del h_in, h_out, src
 
@@ -647,6 +659,8 @@ def run_ours(args):
                            "data_bytes_per_step": data_bytes_step, "parity_d2h_bytes_per_step": d2h_step,
                            "l2": f"inputs > L2: steps rotate over {RING_BLOCKS} distinct decode blocks "
                                  f"({RING_BLOCKS * data_bytes_step // world >> 20} MiB per GPU)",
+                           "host_placement": ("pinned buffers and host threads on the GPU's NUMA node (CPUs "
+                                              f"{numa_cpus})" if numa_cpus else "single NUMA node host"),
                            "parallelism": (f"byte-range striping x{world} (peer loads over NVLink)"
                                            if args.encoder == "stripe" else
                                            f"rotating whole-stripe encoder x{world} (paper's temporal "
@@ -678,6 +692,7 @@ def host_tier_checkpoint(torch, dev, ring, scheme, pipe, comp, copy, args):
     threads = max(1, (os.cpu_count() or 1) - 2)
     S = ring.shape[1]
     store = ParityStore(seal_threads=threads)
+    store.bind_device(dev.index or 0)   # slabs on the GPU's NUMA node
     enc = encoder(scheme)
     blocks = max(4, min(args.steps, 64))
     slots = [L.ptr_array([ring[b % RING_BLOCKS, s, j].data_ptr() for s in range(S) for j in range(N_SHARDS)])
@@ -950,6 +965,7 @@ def c3_orchestrated(torch, dev, link, k1_gbs, k2_gbs):
     cfg = CheckpointConfig(CodingScheme.reed_solomon(8, 2), m, cfg_m, cost)
     threads = max(1, (os.cpu_count() or 1) - 2)
     store = ParityStore(seal_threads=threads)
+    store.bind_device(dev.index or 0)
     ck = Checkpointer(cfg, store, device=dev.index or 0)
     # warm pass: the host tier's pinned slabs (10 GiB here) and the device
     # blocks of the 512 KV slices are allocated once and then recycled (store
@@ -997,6 +1013,7 @@ def c3_recovery_striped(torch, dist, dev, comp, copy, pipe, rank, world, shared,
     range of the 7 survivors and P2P-stores the rebuilt range into worker 5's
     buffer on its owner -- the 5 GiB upload striped over N host links.
     Device time per rank, max over ranks."""
+    from paper_2605_00831_b200 import device as D
     from paper_2605_00831_b200 import kv_layout as K
     from paper_2605_00831_b200.coding import CodingScheme, ErasurePattern
     from paper_2605_00831_b200.peer import PeerGroup, ShardLayout, plan_encode_striped, plan_reconstruct_striped
@@ -1022,7 +1039,7 @@ def c3_recovery_striped(torch, dist, dev, comp, copy, pipe, rank, world, shared,
     torch.cuda.synchronize()
     pg = PeerGroup()
     bases = pg.share(kv)
-    h_par = torch.empty((chunks, k, max(ln, 16)), dtype=torch.uint8).pin_memory()
+    h_par = D.pinned_near((chunks, k, max(ln, 16)), dev.index or 0)
 
     def dev_timed(call):
         barrier()

@@ -277,6 +277,9 @@ int gs_parity_checksum_batch(const void* const* parity, int n_chunks, int k, siz
  * once `stream` reaches that point (cudaLaunchHostFunc), off the GPU path. */
 int gs_store_create(uint64_t capacity_bytes /* ~0 = unlimited */, int seal_threads, gs_store** out);
 int gs_store_destroy(gs_store* s);
+/* Place the store's future pinned slabs on `device`'s NUMA node (the socket
+ * of the GPU whose D2H fills them); -1 = unbound (cudaHostAlloc). */
+int gs_store_bind_device(gs_store* s, int device);
 /* try_put accounting (parity_store.hpp:77-90): *accepted = 0 is back-pressure
  * (store unchanged); a duplicate key is GS_LOGIC_ERROR. parity_out[k]. */
 int gs_store_reserve(gs_store* s, uint64_t request_id, uint32_t chunk, int kind, int n, int k,
@@ -326,7 +329,15 @@ int gs_stripe_range(uint64_t total, int rank, int world, uint64_t* off, uint64_t
 
 /* ---- pinned host memory for the parity host tier ----------------------- */
 int gs_host_alloc(size_t bytes, void** out);
+/* Pinned host memory on `device`'s NUMA node (its host link's socket):
+ * mmap + mbind + first touch + cudaHostRegister; plain cudaHostAlloc on
+ * single-node hosts. Free either kind with gs_host_free. */
+int gs_host_alloc_near(int device, size_t bytes, void** out);
 int gs_host_free(void* p);
+/* NUMA node of the GPU's PCI device (-1 if unknown) and its local CPU list
+ * (sysfs local_cpulist, e.g. "0-47,96-143"; "" if unknown). */
+int gs_device_numa_node(int device, int* node);
+int gs_device_local_cpus(int device, char* buf, size_t cap);
 
 #ifdef __cplusplus
 }

@@ -93,6 +93,10 @@ SIGNATURES = {
     "gs_stripe_range": (_i, [_u64, _i, _i, _u64p, _u64p]),
     "gs_host_alloc": (_i, [_sz, _vpp]),
     "gs_host_free": (_i, [_vp]),
+    "gs_host_alloc_near": (_i, [_i, _sz, _vpp]),
+    "gs_store_bind_device": (_i, [_vp, _i]),
+    "gs_device_numa_node": (_i, [_i, _ip]),
+    "gs_device_local_cpus": (_i, [_i, C.c_char_p, _sz]),
 }
 
 _lib = None

@@ -28,6 +28,7 @@
 
 #include "../../include/gs_capi.h"
 #include "gs_fnv.hpp"
+#include "gs_host.hpp"
 
 namespace gsb {
 void set_last_error(const char* msg);  // gs_capi.cu: shared gs_last_error() slot
@@ -54,7 +55,13 @@ class SlabPool {
  public:
   explicit SlabPool(size_t slab) : slab_(slab) {}
   ~SlabPool() {
-    for (void* s : slabs_) cudaFreeHost(s);
+    for (void* s : slabs_)
+      if (!gsb::pinned_free_near(s)) cudaFreeHost(s);
+  }
+  int device = -1;  // >= 0: slabs placed on this GPU's NUMA node
+  cudaError_t host_alloc(void** p, size_t bytes) {
+    if (device >= 0) return gsb::pinned_alloc_near(device, bytes, p) == GS_OK ? cudaSuccess : cudaErrorMemoryAllocation;
+    return cudaHostAlloc(p, bytes, cudaHostAllocPortable);
   }
   int alloc(size_t bytes, uint8_t** out) {
     bytes = std::max<size_t>(4096, (bytes + 4095) / 4096 * 4096);
@@ -66,7 +73,7 @@ class SlabPool {
     }
     if (bytes > slab_ / 4) {  // large entries get their own allocation
       void* p = nullptr;
-      cudaError_t e = cudaHostAlloc(&p, bytes, cudaHostAllocPortable);
+      cudaError_t e = host_alloc(&p, bytes);
       if (e != cudaSuccess) return sfail(GS_CUDA_ERROR, "store: pinned alloc of %zu B: %s", bytes, cudaGetErrorString(e));
       slabs_.push_back(p);
       *out = static_cast<uint8_t*>(p);
@@ -74,7 +81,7 @@ class SlabPool {
     }
     if (!cur_ || used_ + bytes > slab_) {
       void* p = nullptr;
-      cudaError_t e = cudaHostAlloc(&p, slab_, cudaHostAllocPortable);
+      cudaError_t e = host_alloc(&p, slab_);
       if (e != cudaSuccess) return sfail(GS_CUDA_ERROR, "store: pinned slab alloc: %s", cudaGetErrorString(e));
       slabs_.push_back(p);
       cur_ = static_cast<uint8_t*>(p);
@@ -213,6 +220,13 @@ int gs_store_create(uint64_t capacity_bytes, int seal_threads, gs_store** out) {
   const int t = std::max(1, seal_threads);
   for (int i = 0; i < t; ++i) s->workers.emplace_back([s] { s->worker(); });
   *out = s;
+  return GS_OK;
+}
+
+int gs_store_bind_device(gs_store* s, int device) {
+  if (!s) return sfail(GS_INVALID_ARGUMENT, "store_bind_device: NULL store");
+  std::lock_guard<std::mutex> lk(s->mu);
+  s->pool.device = device;
   return GS_OK;
 }
 

@@ -271,6 +271,64 @@ def capture_upload(scheme: CodingScheme, lost: ErasurePattern, data: Mapping[int
     return CapturedCall("reconstruct_upload", scheme, lost, data, h_parity, out, **kw)
 
 
+# ---------------------------------------------------------------------------
+# NUMA-local pinned host memory
+# ---------------------------------------------------------------------------
+class _NearBuffer:
+    """Owner of a gs_host_alloc_near allocation, exposed through the numpy
+    array interface (the array keeps this object, and so the memory, alive)."""
+
+    def __init__(self, device: int, nbytes: int):
+        p = C.c_void_p()
+        check(L.lib().gs_host_alloc_near(device, max(nbytes, 1), C.byref(p)), "host_alloc_near")
+        self.ptr, self.nbytes = p.value, nbytes
+        self.__array_interface__ = {"shape": (nbytes,), "typestr": "|u1", "data": (self.ptr, False),
+                                    "version": 3}
+
+    def __del__(self):
+        if getattr(self, "ptr", None):
+            L.lib().gs_host_free(self.ptr)
+            self.ptr = None
+
+
+def pinned_near(shape, device: int = 0) -> Tensor:
+    """uint8 CPU tensor in pinned memory on `device`'s NUMA node (the socket of
+    its host link; plain pinned memory on single-node hosts)."""
+    import math
+
+    import numpy as np
+    n = int(math.prod(shape)) if isinstance(shape, (tuple, list)) else int(shape)
+    arr = np.asarray(_NearBuffer(device, n))
+    return torch.from_numpy(arr).view(*(shape if isinstance(shape, (tuple, list)) else (shape,)))
+
+
+def bind_local_cpus(device: int = 0) -> Optional[str]:
+    """Pin this process to the CPUs local to `device` (multi-socket hosts), so
+    the submitting thread and the seal workers sit next to its host link.
+    Returns the CPU list applied, or None when the host has one NUMA node."""
+    import os
+    node = C.c_int(-1)
+    check(L.lib().gs_device_numa_node(device, C.byref(node)), "numa")
+    buf = C.create_string_buffer(4096)
+    check(L.lib().gs_device_local_cpus(device, buf, 4096), "local cpus")
+    cpus = buf.value.decode()
+    try:
+        nodes = open("/sys/devices/system/node/online").read().strip()
+    except OSError:
+        nodes = "0"
+    if node.value < 0 or "-" not in nodes and "," not in nodes or not cpus:
+        return None
+    sel = set()
+    for part in cpus.split(","):
+        a, _, b = part.partition("-")
+        sel.update(range(int(a), int(b or a) + 1))
+    try:
+        os.sched_setaffinity(0, sel)
+    except OSError:
+        return None
+    return cpus
+
+
 def launches() -> int:
     """Kernels launched by libghostserve_b200.so in this process."""
     return int(L.lib().gs_kernel_launches())

@@ -86,6 +86,10 @@ class ParityStore:
             _handle = h.value
         self.handle = _handle
 
+    def bind_device(self, device: int) -> None:
+        """Place future pinned slabs on `device`'s NUMA node (gs_store_bind_device)."""
+        check(L.lib().gs_store_bind_device(self.handle, device), "parity store")
+
     def close(self) -> None:
         if self.handle:
             L.lib().gs_store_destroy(self.handle)

@@ -503,3 +503,39 @@ def test_pipeline_eager_after_capture():
     g.pipe.encode_offload(scheme, data, h_par, st, st)
     torch.cuda.synchronize()
     assert torch.equal(h_par, D.encode(scheme, data).cpu())
+
+
+@pytest.mark.parametrize("force", ["0", "1"])
+def test_numa_near_pinned_buffers(force):
+    """Parity D2H'd into NUMA-placed pinned memory (gs_host_alloc_near; the
+    mmap + mbind + cudaHostRegister path forced with GS_FORCE_NUMA_BIND=1)
+    and a store bound to the device; bit-exact vs the oracle. Runs in a child
+    process so the env switch is read at library load."""
+    code = f"""
+import os, sys
+sys.path.insert(0, {ROOT!r})
+import numpy as np, torch
+from oracle import oracle as O
+from paper_2605_00831_b200 import device as D, coding as G
+from paper_2605_00831_b200.parity_store import ParityStore
+from tests.golden.vectors import splitmix_bytes
+n, k, S, ln = 8, 2, 4, 300_000
+host = [[splitmix_bytes(31 * s + j, ln) for j in range(n)] for s in range(S)]
+data = torch.stack([torch.from_numpy(np.stack(h)) for h in host]).cuda()
+hp = D.pinned_near((S, k, ln), 0)
+pipe = D.Pipeline(0, 1 << 20)
+st = torch.cuda.current_stream()
+pipe.encode_offload(G.CodingScheme.reed_solomon(n, k), data, hp, st, st)
+st.synchronize()
+for s in range(S):
+    want = O.port().encode(O.RS, n, k, host[s])
+    assert all(np.array_equal(hp[s, i].numpy(), want[i]) for i in range(k))
+store = ParityStore(seal_threads=2)
+store.bind_device(0)
+del hp
+pipe.close()
+print("ok", D.bind_local_cpus(0))
+"""
+    out = subprocess.run([os.sys.executable, "-c", code], capture_output=True, text=True, cwd=ROOT,
+                         env=dict(os.environ, GS_FORCE_NUMA_BIND=force), timeout=300)
+    assert out.returncode == 0 and "ok" in out.stdout, out.stderr[-2000:]
