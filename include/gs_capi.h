@@ -155,6 +155,17 @@ int gs_prewarm(int device);
  * bulk for encode launches >= 128 MB, register kernel otherwise). All are
  * bit-identical; exposed for benchmarking and cross-checking. */
 int gs_set_kernel_variant(int variant);
+/* Runtime-specialised kernels: a codec with no compiled specialisation
+ * (e.g. RS(10,4) decode, RS(9,2)) starts on the runtime-coefficient kernel
+ * and, on its first GPU launch, queues an NVRTC build of the specialised
+ * Horner kernel for its matrix (background thread, cubin cached on disk in
+ * _lib/jit or $GS_JIT_CACHE); later launches use it. Bytes are identical.
+ * gs_set_jit(0) / GS_JIT=0 disables. jit_status: -2 not applicable
+ * (compiled kernel, RDP, disabled, matrix too large), 0 building, 1 ready,
+ * -1 failed (GS_RUNTIME_ERROR with the compiler log); wait != 0 blocks
+ * until the build is done (and requests it if not yet requested). */
+int gs_set_jit(int on);
+int gs_codec_jit_status(const gs_codec* c, int wait, int* status);
 int gs_pipeline_destroy(gs_pipeline* p);
 /* Live kernel timing of the pipelined calls (encode_offload /
  * reconstruct_upload): while on, each codec launch group is measured two

@@ -57,6 +57,8 @@ SIGNATURES = {
     "gs_encode_host_async": (_i, [_vp, _vp, _vpp, _vpp, _sz]),
     "gs_reconstruct_host_async": (_i, [_vp, _vp, _vpp, _vpp, _sz]),
     "gs_pipeline_sync": (_i, [_vp]),
+    "gs_set_jit": (_i, [_i]),
+    "gs_codec_jit_status": (_i, [_vp, _i, _ip]),
     "gs_codec_create": (_i, [_i, _i, _i, _vpp]),
     "gs_encode_async": (_i, [_vp, _vpp, _sz, _vpp, _vp, _vp]),
     "gs_reconstruct_async": (_i, [_vp, _ip, _i, _vpp, _vpp, _vpp, _sz, _vp]),

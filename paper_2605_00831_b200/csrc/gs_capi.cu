@@ -25,6 +25,7 @@
 #include "gs_field.hpp"
 #include "gs_fnv.hpp"
 #include "gs_host.hpp"
+#include "gs_jit.hpp"
 #include "gs_kernels.cuh"
 #include "gs_kv.cuh"
 #include "gs_rdp.cuh"
@@ -306,6 +307,10 @@ struct gs_codec {
   gs_codec* xor_helper = nullptr;
   mutable std::mutex mu;
   mutable std::map<int, CoefWords*> dev_words;  // device -> uploaded table
+  // runtime-specialised kernel (gs_jit.hpp), requested on the first GPU run
+  // when no compiled specialisation exists
+  mutable JitKernel* jit = nullptr;
+  mutable bool jit_tried = false;
 
   ~gs_codec() {
     delete xor_helper;
@@ -411,6 +416,15 @@ const void* generic_kernel(int kb) {
   }
 }
 
+JitKernel* codec_jit(const gs_codec* c) {
+  std::lock_guard<std::mutex> lk(c->mu);
+  if (!c->jit_tried) {
+    c->jit_tried = true;
+    c->jit = jit_request(c->n_out, c->n_slots, c->coef.data());
+  }
+  return c->jit;
+}
+
 // Launch the codec over stripes. slot_ptr(s, j) / out_ptr(s, i) give the
 // (already offset) pointers; every stripe has `len` bytes.
 // Paging (optional): slots whose bit is set in pg.paged_slots are paged-cache
@@ -500,18 +514,26 @@ int run_codec(const gs_codec* c, int n_stripes, SlotFn slot_ptr, OutFn out_ptr, 
   if (int s = upload_words(c, dev, &dw)) return s;
   std::vector<const void*> ptrs;
 
-  // Specialised kernel over the 16-byte-aligned body.
+  // Specialised kernel over the 16-byte-aligned body: compiled registry, or
+  // a runtime-specialised (JIT) build of this codec's matrix once it is ready.
   uint64_t done = 0;
   if (pg.any() && !aligned) return fail(GS_INVALID_ARGUMENT, "paged apply: pointers must be 16-B aligned");
-  if (c->special && aligned && len >= kVec) {
+  JitKernel* jit = nullptr;
+  if (!c->special && aligned && len >= kVec && !pg.any()) {
+    jit = codec_jit(c);
+    if (jit && jit_status(jit, false) != 1) jit = nullptr;
+    if (jit && jit_occupancy(jit) < 1) jit = nullptr;
+  }
+  if ((c->special || jit) && aligned && len >= kVec) {
     const uint64_t body = len / kVec * kVec;
-    const int stages = bulk_stages(c->special);
+    const int stages = c->special ? bulk_stages(c->special) : 0;
     const int variant = g_variant.load(std::memory_order_relaxed);
-    const uint64_t launch_bytes = body * static_cast<uint64_t>(n_stripes) *
-                                  static_cast<uint64_t>(c->special->used_cols + c->n_out);
-    const bool use_bulk = !pg.any() && stages >= 2 &&
+    const uint64_t launch_bytes = c->special ? body * static_cast<uint64_t>(n_stripes) *
+                                                   static_cast<uint64_t>(c->special->used_cols + c->n_out)
+                                             : 0;
+    const bool use_bulk = c->special && !pg.any() && stages >= 2 &&
                           (variant == 1 || (variant == 2 && !c->decoder && launch_bytes >= kBulkAutoBytes));
-    const uint64_t tile = static_cast<uint64_t>(use_bulk ? c->special->tile_bulk : c->special->tile);
+    const uint64_t tile = static_cast<uint64_t>(use_bulk ? c->special->tile_bulk : c->special ? c->special->tile : kTile);
     const uint64_t tps64 = (body + tile - 1) / tile;
     const int stride = c->n_slots + c->n_out;
     const int per = kPtrCap / stride;
@@ -519,8 +541,9 @@ int run_codec(const gs_codec* c, int n_stripes, SlotFn slot_ptr, OutFn out_ptr, 
                                                          c->special->tile_bulk
                                  : 0;
     const bool paged = pg.any();
-    int occ = use_bulk ? blocks_per_sm(dev, c->special->kernel_bulk, smem, kBulkThreads)
-                       : blocks_per_sm(dev, paged ? c->special->kernel_paged : c->special->kernel, 0);
+    int occ = jit        ? jit_occupancy(jit)
+              : use_bulk ? blocks_per_sm(dev, c->special->kernel_bulk, smem, kBulkThreads)
+                         : blocks_per_sm(dev, paged ? c->special->kernel_paged : c->special->kernel, 0);
     if (!use_bulk && g_ctas_per_sm > 0) occ = std::min(occ, g_ctas_per_sm);
     for (int s0 = 0; s0 < n_stripes; s0 += per) {
       const int cnt = std::min(per, n_stripes - s0);
@@ -538,9 +561,10 @@ int run_codec(const gs_codec* c, int n_stripes, SlotFn slot_ptr, OutFn out_ptr, 
       if (g.src.table) g.src.table += (pg.stripe0 + s0) * g.src.table_stride;
       if (g.dst.table) g.dst.table += (pg.stripe0 + s0) * g.dst.table_stride;
       const int grid = static_cast<int>(std::min<uint64_t>(total, g_full_grid && !use_bulk ? total : static_cast<uint64_t>(occ) * sms));
-      cudaError_t e = use_bulk ? c->special->launch_bulk(ptrs.data(), cnt * stride, g, grid, st, stages, smem)
-                      : paged  ? c->special->launch_paged(ptrs.data(), cnt * stride, g, grid, st)
-                               : c->special->launch(ptrs.data(), cnt * stride, g, grid, st);
+      cudaError_t e = jit        ? jit_launch(jit, ptrs.data(), cnt * stride, g, sms, st)
+                      : use_bulk ? c->special->launch_bulk(ptrs.data(), cnt * stride, g, grid, st, stages, smem)
+                      : paged    ? c->special->launch_paged(ptrs.data(), cnt * stride, g, grid, st)
+                                 : c->special->launch(ptrs.data(), cnt * stride, g, grid, st);
       if (e != cudaSuccess) return fail(GS_CUDA_ERROR, "special kernel launch: %s", cudaGetErrorString(e));
       g_launches.fetch_add(1, std::memory_order_relaxed);
     }
@@ -1219,6 +1243,22 @@ int gs_apply_device_paged(const gs_codec* c, int n_stripes, const void* const* s
 // ============================================================================
 // pipelines
 // ============================================================================
+int gs_set_jit(int on) {
+  jit_set_enabled(on != 0);
+  return GS_OK;
+}
+
+int gs_codec_jit_status(const gs_codec* c, int wait, int* status) {
+  if (!c || !status) return fail(GS_INVALID_ARGUMENT, "codec_jit_status: NULL argument");
+  *status = -2;  // compiled registry kernel, RDP, disabled or not eligible
+  if (c->special || c->kind == GS_RDP) return GS_OK;
+  JitKernel* k = codec_jit(c);
+  if (!k) return GS_OK;
+  *status = jit_status(k, wait != 0);
+  if (*status == -1) return fail(GS_RUNTIME_ERROR, "jit: %s", jit_last_log(k));
+  return GS_OK;
+}
+
 int gs_set_kernel_variant(int variant) {
   if (variant < 0 || variant > 2) return fail(GS_INVALID_ARGUMENT, "kernel variant must be 0, 1 or 2");
   g_variant.store(variant);

@@ -7,8 +7,19 @@
 // Cauchy coefficient is identical byte for byte.
 #pragma once
 
+#if defined(__CUDACC_RTC__)
+// runtime (NVRTC) compilation of specialised kernels: no host headers
+typedef unsigned char uint8_t;
+typedef unsigned short uint16_t;
+typedef unsigned int uint32_t;
+typedef unsigned long long uint64_t;
+typedef int int32_t;
+typedef long long int64_t;
+typedef unsigned long long uintptr_t;
+#else
 #include <cstddef>
 #include <cstdint>
+#endif
 
 #ifdef __CUDACC__
 #define GS_HD __host__ __device__

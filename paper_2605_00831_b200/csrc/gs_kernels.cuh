@@ -27,7 +27,9 @@
 //    undone once per output word.
 #pragma once
 
+#if !defined(__CUDACC_RTC__)
 #include <cstdint>
+#endif
 
 #include "gs_field.hpp"
 

@@ -61,6 +61,11 @@ def main():
     else:
         enc = encoder(scheme)
         dec = decoder(scheme, ErasurePattern(lost))
+        # codecs outside the compiled registry: wait for their runtime-specialised build
+        import ctypes as C
+        for c in (enc, dec):
+            js = C.c_int()
+            lib.gs_codec_jit_status(c.handle, 1, C.byref(js))
     out = []
     for mib in [float(x) for x in args.sizes.split(",")]:
         L_ = int(mib * (1 << 20)) // 4096 * 4096
