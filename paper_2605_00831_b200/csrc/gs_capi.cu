@@ -1185,8 +1185,12 @@ int gs_decoder_create(int kind, int n, int k, const int* lost, int n_lost, gs_co
 
 int gs_codec_create_ex(int kind, int n, int k, const int* lost, int n_lost, int flags, gs_codec** out) {
   const bool generic = (flags & GS_FLAG_GENERIC) != 0;
-  if (flags & GS_FLAG_DECODER) return decoder_create(kind, n, k, lost, n_lost, generic, out);
-  return encoder_create(kind, n, k, generic, out);
+  const int st = (flags & GS_FLAG_DECODER) ? decoder_create(kind, n, k, lost, n_lost, generic, out)
+                                           : encoder_create(kind, n, k, generic, out);
+  // a forced-generic codec stays on the runtime-coefficient kernel (no JIT):
+  // it is how the tests cross-check the two back ends
+  if (st == GS_OK && generic) (*out)->jit_tried = true;
+  return st;
 }
 
 int gs_codec_destroy(gs_codec* c) {
