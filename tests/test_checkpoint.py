@@ -189,3 +189,18 @@ def test_bad_parity_and_over_tolerance_fallbacks():
     ck.cfg.cost.restart_overhead = 1e9
     res = ck.recover(3, FailureEvent([1], at_chunk=4), run.ground_truth, [16] * 4)
     assert res.plan.mode == RecoveryMode.kFullRecomputeFallback   # corrupt chunk 2 -> fallback
+
+
+@pytest.mark.gpu
+def test_serving_loop_example_runs_bit_exact():
+    """examples/serving_loop.py end to end: prefill + decode checkpoints
+    (incl. a masked tail), worker failure, planned recovery, bit-exact."""
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    out = subprocess.run([sys.executable, os.path.join(root, "examples", "serving_loop.py"), "--tokens", "256",
+                          "--decode", "40", "--chunk", "16", "--lost", "3"], capture_output=True, text=True,
+                         timeout=600, cwd=root)
+    assert out.returncode == 0, out.stderr[-2000:]
+    assert "bit-exact: True" in out.stdout and "masked tail of 8 tokens" in out.stdout, out.stdout
