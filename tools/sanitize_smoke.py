@@ -1,7 +1,9 @@
 """Small workload for compute-sanitizer (memcheck / racecheck / synccheck):
 every kernel family once -- specialised (register + bulk-copy pipeline),
 generic (aligned, ragged tail, misaligned), paged gather/scatter, the
-offload / upload pipelines -- at sizes that finish quickly under
+offload / upload pipelines (with live kernel timing stamps), RDP (pipelined
+body + tile remainder + P/Q tail, two-column and single-column recovery) and
+a runtime-specialised (NVRTC) kernel -- at sizes that finish quickly under
 instrumentation. Exits non-zero on any byte mismatch vs the oracle.
 
     compute-sanitizer --tool memcheck python tools/sanitize_smoke.py
@@ -81,9 +83,42 @@ def main():
                    9, hp, st, st)
     st.synchronize()
     bad += not torch.equal(rep[4].read_slice(4, 9), truth[4])
+    # pipelines with live kernel timing (globaltimer stamps)
+    import ctypes as C
+    L.lib().gs_pipeline_set_timing(pipe.handle, 1)
+    pipe.encode_offload(sch, data, h, st, st)
+    st.synchronize()
+    ev, dv, grp, nl = C.c_double(), C.c_double(), C.c_int(), C.c_uint64()
+    L.lib().gs_pipeline_kernel_time(pipe.handle, C.byref(ev), C.byref(dv), C.byref(grp), C.byref(nl))
+    L.lib().gs_pipeline_set_timing(pipe.handle, 0)
+    bad += grp.value < 1 or dv.value <= 0
+    bad += not torch.equal(h, D.encode(sch, data).cpu())
+    # RDP(8): p = 11, two pipelined tiles + tile-kernel remainder + P/Q tail
+    rdp = CodingScheme.rdp(8)
+    ln = 2 * 1024 * 10 + 37 * 10 + 3
+    data = torch.randint(0, 256, (2, 8, ln), dtype=torch.uint8, device="cuda", generator=g)
+    par = D.encode(rdp, data)
+    for s_ in range(2):
+        want = O.port().encode(O.RDP, 8, 2, list(data[s_].cpu().numpy()))
+        bad += sum(not np.array_equal(par[s_, i].cpu().numpy(), want[i]) for i in range(2))
+    for lost in ([1, 6], [3, 8], [5]):
+        sh = {j: data[:, j].contiguous() for j in range(8) if j not in lost}
+        sh.update({8 + i: par[:, i].contiguous() for i in range(2) if 8 + i not in lost})
+        got = D.reconstruct(rdp, sh, ErasurePattern(lost))
+        bad += sum(not torch.equal(t, data[:, j]) for j, t in got.items())
+    # runtime-specialised kernel (NVRTC), RS(9,2) is outside the compiled set
+    from paper_2605_00831_b200.coding import encoder
+    sch9 = CodingScheme.reed_solomon(9, 2)
+    enc9 = encoder(sch9)
+    js = C.c_int()
+    L.lib().gs_codec_jit_status(enc9.handle, 1, C.byref(js))
+    data = torch.randint(0, 256, (9, 3 * 4096), dtype=torch.uint8, device="cuda", generator=g)
+    par = D.encode(sch9, data)
+    want = O.port().encode(O.RS, 9, 2, list(data.cpu().numpy()))
+    bad += sum(not np.array_equal(par[i].cpu().numpy(), want[i]) for i in range(2))
     pipe.close()
     torch.cuda.synchronize()
-    print("sanitize_smoke: mismatches =", bad, "kernels =", D.launches())
+    print("sanitize_smoke: mismatches =", bad, "kernels =", D.launches(), "jit status =", js.value)
     sys.exit(1 if bad else 0)
 
 
