@@ -562,18 +562,19 @@ int run_rdp(const gs_codec* c, int n_stripes, SlotFn slot_ptr, OutFn out_ptr, ui
   const int stride = in_slots + c->n_out;
   const int per = kPtrCap / stride;
   if (per < 1) return fail(GS_INVALID_ARGUMENT, "rdp: stripe needs %d pointers (> %d)", stride, kPtrCap);
-  // Whole-dstripe body -> pipelined kernels (16-B aligned columns, whole
-  // 1024-dstripe tiles, >= 2 ring stages); the rest of the range (its last
-  // partial tile and the P/Q tail past the last whole dstripe) -> tile kernels.
+  // Pipelined kernels take the whole range when the columns are 16-B aligned
+  // and it holds at least one whole dstripe: every whole dstripe (the last
+  // tile may be partial) plus the P/Q tail past the last one. Otherwise the
+  // shared-memory tile kernels run the lot.
   const uint64_t full_abs = total / rows * rows;
   const uint32_t TB = rdpb::tile_bytes(p);
   const size_t fixed = rdpb::kHeader + rdpb::out_bytes(p) + (encode ? 0 : rdpb::chain_bytes(p));
   const int fast_stages = fixed < rdpb::kSmemBudget
                               ? static_cast<int>(std::min<size_t>(rdpb::kMaxStages, (rdpb::kSmemBudget - fixed) / TB))
                               : 0;
-  uint64_t body = 0;
+  uint64_t body = 0;  // whole-dstripe bytes handled by the pipelined kernel
   if (aligned && fast_stages >= 2 && g_rdp_fast && full_abs > pg.logical0)
-    body = std::min<uint64_t>(len, full_abs - pg.logical0) / TB * TB;
+    body = std::min<uint64_t>(len, full_abs - pg.logical0);
   const void* kfast = nullptr;
 #define GS_RDP_PICK_FAST(P_)                                                                  \
   if (p == P_)                                                                                \
@@ -592,6 +593,19 @@ int run_rdp(const gs_codec* c, int n_stripes, SlotFn slot_ptr, OutFn out_ptr, ui
     }
   } else {
     body = 0;
+  }
+  const uint32_t fast_tail = body ? static_cast<uint32_t>(len - body) : 0;  // < rows bytes
+  if (body) body = len;  // the pipelined kernel covers the tail too
+  // tail coefficients of the two-column recovery (coding.hpp:415-448)
+  uint8_t tail_gj = 0, tail_inv = 0;
+  if (!encode && c->rdp_li >= 0) {
+    const uint8_t gi = exp2_of(c->rdp_li);
+    if (c->rdp_lj == p - 1) {
+      tail_inv = gf_inv(gi);
+    } else {
+      tail_gj = exp2_of(c->rdp_lj);
+      tail_inv = gf_inv(static_cast<uint8_t>(gi ^ tail_gj));
+    }
   }
   const uint64_t rest = len - body;
   const uint32_t T = static_cast<uint32_t>(rows) * kRdpThreads;
@@ -616,10 +630,11 @@ int run_rdp(const gs_codec* c, int n_stripes, SlotFn slot_ptr, OutFn out_ptr, ui
     }
     PtrTable<kPtrCap> tab;
     if (body) {
-      const uint64_t ftps = body / TB, fntiles = ftps * cnt;
+      const uint64_t whole = len - fast_tail;
+      const uint64_t ftps = (whole + TB - 1) / TB, fntiles = ftps * cnt;
       for (int i = 0; i < cnt * stride; ++i) tab.p[i] = static_cast<const uint8_t*>(ptrs[i]);
-      RdpGeom g{n, p, rows, body, pg.logical0, full_abs, total, static_cast<uint32_t>(ftps),
-                static_cast<uint32_t>(fntiles), stride, 1, c->rdp_li, c->rdp_lj, 0, 0};
+      RdpGeom g{n, p, rows, whole, pg.logical0, full_abs, total, static_cast<uint32_t>(ftps),
+                static_cast<uint32_t>(fntiles), stride, 1, c->rdp_li, c->rdp_lj, tail_gj, tail_inv, fast_tail};
       const int grid = static_cast<int>(std::min<uint64_t>(fntiles, static_cast<uint64_t>(sms)));
       const int threads = (rdpb::kCW + 1) * 32;
 #define GS_RDP_LAUNCH_FAST(P_)                                                                               \
@@ -639,16 +654,7 @@ int run_rdp(const gs_codec* c, int n_stripes, SlotFn slot_ptr, OutFn out_ptr, ui
     if (!rest) continue;
     const uint64_t ntiles = tps64 * cnt;
     RdpGeom g{n, p, rows, rest, pg.logical0 + body, full_abs, total, static_cast<uint32_t>(tps64),
-              static_cast<uint32_t>(ntiles), stride, aligned ? 1 : 0, c->rdp_li, c->rdp_lj, 0, 0};
-    if (!encode && c->rdp_li >= 0) {  // tail coefficients (coding.hpp:415-448)
-      const uint8_t gi = exp2_of(c->rdp_li);
-      if (c->rdp_lj == p - 1) {
-        g.inv = gf_inv(gi);
-      } else {
-        g.gj = exp2_of(c->rdp_lj);
-        g.inv = gf_inv(static_cast<uint8_t>(gi ^ g.gj));
-      }
-    }
+              static_cast<uint32_t>(ntiles), stride, aligned ? 1 : 0, c->rdp_li, c->rdp_lj, tail_gj, tail_inv, 0};
     for (int i = 0; i < cnt * stride; ++i)
       tab.p[i] = ptrs[i] ? static_cast<const uint8_t*>(ptrs[i]) + body : nullptr;
     const int grid = static_cast<int>(std::min<uint64_t>(ntiles, static_cast<uint64_t>(occ) * sms));

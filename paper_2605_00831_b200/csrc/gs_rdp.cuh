@@ -44,6 +44,9 @@ struct RdpGeom {
   // recovery tail (coding.hpp:415-448): gj = 2^j, inv = 1 / 2^i (j == p-1)
   // or 1 / (2^i ^ 2^j)
   uint8_t gj, inv;
+  // pipelined kernels: P/Q tail bytes after the whole-dstripe body `len`
+  // (only in a column's last range), handled by the last tile's CTA
+  uint32_t tail;
 };
 
 // P/Q tail arithmetic: Q = sum_c 2^c d_c is evaluated by Horner (one
@@ -408,11 +411,18 @@ __device__ __forceinline__ void rdp_produce(const PtrTable<CAP>& tab, const RdpG
     const uint32_t s = t / g.tps;
     const uint64_t off = static_cast<uint64_t>(t - s * g.tps) * ring.tb;
     const int base = static_cast<int>(s) * g.stride;
+    // the last tile of a range may be partial (whole dstripes, any count):
+    // the 16-byte-multiple part goes through the bulk engine, the < 16-byte
+    // rest is copied by this lane before the arrive that publishes it
+    const uint32_t size = static_cast<uint32_t>(g.len - off < ring.tb ? g.len - off : ring.tb);
+    const uint32_t bsz = size & ~15u;
     for (int u = 0; u < ncols; ++u) {
       bulk::mbar_wait(&ring.empty[ring.stage], ring.phase ^ 1u);
-      bulk::mbar_expect_tx(&ring.full[ring.stage], ring.tb);
-      bulk::bulk_g2s(ring.data + static_cast<size_t>(ring.stage) * ring.tb, tab.p[base + cols[u]] + off, ring.tb,
-                     &ring.full[ring.stage]);
+      uint8_t* dst = ring.data + static_cast<size_t>(ring.stage) * ring.tb;
+      const uint8_t* src = tab.p[base + cols[u]] + off;
+      for (uint32_t b = bsz; b < size; ++b) dst[b] = src[b];
+      bulk::mbar_expect_tx(&ring.full[ring.stage], bsz);
+      if (bsz) bulk::bulk_g2s(dst, src, bsz, &ring.full[ring.stage]);
       ring.advance();
     }
   }
@@ -455,7 +465,62 @@ __device__ __forceinline__ void out_stage(uint8_t* outbuf, int buf, int o, uint3
   sts_block<R>(outbuf + (static_cast<size_t>(buf) * 2 + o) * tb + threadIdx.x * (4 * R), w);
 }
 
+// One thread: write `size` bytes of a staged output tile (bulk engine for the
+// 16-byte multiple, plain stores for the rest).
+__device__ __forceinline__ void store_tile(uint8_t* gdst, const uint8_t* ssrc, uint32_t size) {
+  const uint32_t bsz = size & ~15u;
+  if (bsz) bulk_s2g(gdst, ssrc, bsz);
+  for (uint32_t b = bsz; b < size; ++b) gdst[b] = ssrc[b];
+}
+
 }  // namespace rdpb
+
+// P/Q tail of a column (coding.hpp:237-241, 300-306): bytes [x0, x0 + cnt) past
+// the last whole dstripe, one byte per lane, straight from global memory.
+template <int CAP>
+__device__ __forceinline__ void rdp_encode_tail(const PtrTable<CAP>& tab, int base, int n, uint64_t x0,
+                                                uint32_t cnt) {
+  const uint32_t lane = threadIdx.x & 31;
+  if (lane >= cnt) return;
+  const uint64_t x = x0 + lane;
+  uint8_t pp = 0, h = 0;
+  for (int c = n - 1; c >= 0; --c) {
+    const uint8_t v = tab.p[base + c][x];
+    pp ^= v;
+    h = xtime1(h) ^ v;
+  }
+  const_cast<uint8_t*>(tab.p[base + n])[x] = pp;
+  const_cast<uint8_t*>(tab.p[base + n + 1])[x] = h;
+}
+
+// coding.hpp:415-448 on the tail bytes (slots: data 0..n-1, row parity n,
+// diagonal n+1; outputs out0.. = lost data columns ascending).
+template <int CAP, int P>
+__device__ __forceinline__ void rdp_recover_tail(const PtrTable<CAP>& tab, const RdpGeom& g, int base, int out0,
+                                                 int n_out, uint64_t x0, uint32_t cnt) {
+  const uint32_t lane = threadIdx.x & 31;
+  if (lane >= cnt) return;
+  const uint64_t x = x0 + lane;
+  const int n = g.n, i = g.li, j = g.lj;
+  uint8_t ps = 0, h = 0;
+  for (int c = n - 1; c >= 0; --c) {
+    const uint8_t v = (c == i || c == j) ? 0 : tab.p[base + c][x];
+    ps ^= v;
+    h = xtime1(h) ^ v;
+  }
+  const uint8_t qs = tab.p[base + n + 1][x] ^ h;
+  uint8_t di, dj;
+  if (j == P - 1) {
+    di = gf_mul(qs, g.inv);
+    dj = 0;
+  } else {
+    ps ^= tab.p[base + n][x];
+    di = gf_mul(static_cast<uint8_t>(qs ^ gf_mul(g.gj, ps)), g.inv);
+    dj = static_cast<uint8_t>(ps ^ di);
+  }
+  const_cast<uint8_t*>(tab.p[base + out0])[x] = di;
+  if (n_out > 1 && j < n) const_cast<uint8_t*>(tab.p[base + out0 + 1])[x] = dj;
+}
 
 template <int CAP, int P>
 __global__ void __launch_bounds__((rdpb::kCW + 1) * 32, 1)
@@ -506,12 +571,14 @@ __global__ void __launch_bounds__((rdpb::kCW + 1) * 32, 1)
     out_stage<R>(outbuf, buf, 1, TB, diag);
     fence_async_smem();
     consumers_sync();
+    const uint32_t size = static_cast<uint32_t>(g.len - off < TB ? g.len - off : TB);
     if (threadIdx.x == 0) {
-      bulk_s2g(const_cast<uint8_t*>(tab.p[base + n]) + off, outbuf + (static_cast<size_t>(buf) * 2) * TB, TB);
-      bulk_s2g(const_cast<uint8_t*>(tab.p[base + n + 1]) + off, outbuf + (static_cast<size_t>(buf) * 2 + 1) * TB,
-               TB);
+      store_tile(const_cast<uint8_t*>(tab.p[base + n]) + off, outbuf + (static_cast<size_t>(buf) * 2) * TB, size);
+      store_tile(const_cast<uint8_t*>(tab.p[base + n + 1]) + off, outbuf + (static_cast<size_t>(buf) * 2 + 1) * TB,
+                 size);
       bulk_commit();
     }
+    if (g.tail && threadIdx.x < 32 && t - s * g.tps == g.tps - 1) rdp_encode_tail(tab, base, n, g.len, g.tail);
     buf ^= 1;
   }
   if (threadIdx.x == 0) bulk_wait_all();
@@ -616,13 +683,16 @@ __global__ void __launch_bounds__((rdpb::kCW + 1) * 32, 1)
     if (n_out > 1) out_stage<R>(outbuf, buf, 1, TB, rj);
     fence_async_smem();
     consumers_sync();
+    const uint32_t size = static_cast<uint32_t>(g.len - off < TB ? g.len - off : TB);
     if (threadIdx.x == 0) {
-      bulk_s2g(const_cast<uint8_t*>(tab.p[base + out0]) + off, outbuf + (static_cast<size_t>(buf) * 2) * TB, TB);
+      store_tile(const_cast<uint8_t*>(tab.p[base + out0]) + off, outbuf + (static_cast<size_t>(buf) * 2) * TB, size);
       if (n_out > 1)
-        bulk_s2g(const_cast<uint8_t*>(tab.p[base + out0 + 1]) + off,
-                 outbuf + (static_cast<size_t>(buf) * 2 + 1) * TB, TB);
+        store_tile(const_cast<uint8_t*>(tab.p[base + out0 + 1]) + off,
+                   outbuf + (static_cast<size_t>(buf) * 2 + 1) * TB, size);
       bulk_commit();
     }
+    if (g.tail && threadIdx.x < 32 && t - s * g.tps == g.tps - 1)
+      rdp_recover_tail<CAP, P>(tab, g, base, out0, n_out, g.len, g.tail);
     buf ^= 1;
   }
   if (threadIdx.x == 0) bulk_wait_all();
