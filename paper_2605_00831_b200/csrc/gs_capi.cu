@@ -1403,11 +1403,17 @@ static int reconstruct_upload(gs_pipeline* p, const gs_codec* c, int n_stripes, 
     if (j >= n) host_slots.push_back(j);
   const int H = std::max<int>(1, static_cast<int>(host_slots.size()));
   const size_t slot = p->slot_bytes();
-  const uint64_t rl_max = align_piece(c, piece_len(len, slot, H), len);
+  // Recovery is latency-bound on the H2D: cut the upload into >= 4 pieces
+  // (>= 1 MiB each) so the rebuild of piece i runs under the H2D of piece
+  // i+1 instead of after the whole upload.
+  const uint64_t total_h2d = static_cast<uint64_t>(n_stripes) * H * len;
+  const uint64_t piece_cap = std::max<uint64_t>(1ull << 20, total_h2d / 4);
+  const uint64_t rl_max = align_piece(c, piece_len(len, slot, H, std::max<uint64_t>(4096, piece_cap / H)), len);
   std::vector<CopyOp> ops;
   for (uint64_t r0 = 0; r0 < len; r0 += rl_max) {
     const uint64_t rl = std::min<uint64_t>(rl_max, len - r0);
-    const int spp = static_cast<int>(std::max<uint64_t>(1, slot / (H * rl)));
+    const int spp = static_cast<int>(
+        std::max<uint64_t>(1, std::min<uint64_t>(slot / (H * rl), piece_cap / (H * rl))));
     for (int s0 = 0; s0 < n_stripes; s0 += spp) {
       const int cnt = std::min(spp, n_stripes - s0);
       const int sl = p->next;
