@@ -811,13 +811,37 @@ struct DeviceGuard {
   }
 };
 
-// Choose the byte range per piece: as large as the slot allows, at least one
-// 4 KiB tile, rounded to 4 KiB so every piece but the last stays aligned.
-uint64_t piece_len(uint64_t len, size_t slot, int per_byte, uint64_t cap = ~0ull) {
-  uint64_t r = std::min<uint64_t>(slot / static_cast<uint64_t>(per_byte), cap);
-  r = r / 4096 * 4096;
-  if (r == 0) r = 4096;
-  return std::min<uint64_t>(r, len);
+// Piece geometry of the pipelines. Every piece start stays 16-B aligned (the
+// vector kernels' requirement) and, for RDP, on a dstripe boundary (p-1
+// bytes); pieces are 4 KiB multiples whenever that fits in the staging slot.
+uint64_t gcd_u64(uint64_t a, uint64_t b) {
+  while (b) {
+    const uint64_t t = a % b;
+    a = b;
+    b = t;
+  }
+  return a;
+}
+
+uint64_t piece_unit(const gs_codec* c, uint64_t base) {
+  if (c->kind != GS_RDP || c->xor_helper) return base;
+  const uint64_t rows = static_cast<uint64_t>(c->rdp_p - 1);
+  return base / gcd_u64(base, rows) * rows;  // lcm(base, rows)
+}
+
+uint64_t align_down_piece(const gs_codec* c, uint64_t x) {
+  const uint64_t big = piece_unit(c, 4096);
+  if (x >= big) return x / big * big;
+  const uint64_t u = piece_unit(c, 16);
+  return x / u * u;
+}
+
+// Bytes per shard per piece: as large as the slot (and `cap`) allows.
+// 0 = the slot cannot hold one aligned piece (the caller reports it).
+uint64_t piece_len(const gs_codec* c, uint64_t len, size_t slot, int per_byte, uint64_t cap = ~0ull) {
+  const uint64_t room = std::min<uint64_t>(slot / static_cast<uint64_t>(std::max(per_byte, 1)), cap);
+  const uint64_t r = align_down_piece(c, room);
+  return r ? std::min<uint64_t>(r, len) : 0;
 }
 
 // Tapered piece schedule of the host-buffer pipelines: full pieces, then the
@@ -827,17 +851,6 @@ uint64_t taper(uint64_t r0, uint64_t len, uint64_t rl_max, uint64_t quarter) {
   const uint64_t left = len - r0;
   if (left > rl_max || quarter == 0) return std::min<uint64_t>(rl_max, left);
   return std::min<uint64_t>(quarter, left);
-}
-
-// RDP pieces must cover whole dstripes (p-1 bytes) and stay 4 KiB aligned.
-uint64_t align_piece(const gs_codec* c, uint64_t rl, uint64_t len) {
-  if (c->kind != GS_RDP || c->xor_helper) return rl;
-  const uint64_t rows = static_cast<uint64_t>(c->rdp_p - 1);
-  uint64_t a = 4096;
-  while (a % rows) a += 4096;
-  uint64_t r = rl / a * a;
-  if (r == 0) r = a;
-  return std::min<uint64_t>(r, len);
 }
 
 // Host-link copies of one piece. Adjacent (dst, src) runs are merged into
@@ -1329,7 +1342,8 @@ static int encode_offload(gs_pipeline* p, const gs_codec* c, int n_stripes, cons
   GS_CUDA(p->begin(cs, ks));
   const int K = c->n_out, N = c->n_slots;
   const size_t slot = p->slot_bytes();
-  const uint64_t rl_max = align_piece(c, piece_len(len, slot, K), len);
+  const uint64_t rl_max = piece_len(c, len, slot, K);
+  if (!rl_max) return fail(GS_INVALID_ARGUMENT, "encode_offload: staging slot of %zu B cannot hold one piece", slot);
   std::vector<CopyOp> ops;
   for (uint64_t r0 = 0; r0 < len; r0 += rl_max) {
     const uint64_t rl = std::min<uint64_t>(rl_max, len - r0);
@@ -1408,7 +1422,8 @@ static int reconstruct_upload(gs_pipeline* p, const gs_codec* c, int n_stripes, 
   // i+1 instead of after the whole upload.
   const uint64_t total_h2d = static_cast<uint64_t>(n_stripes) * H * len;
   const uint64_t piece_cap = std::max<uint64_t>(1ull << 20, total_h2d / 4);
-  const uint64_t rl_max = align_piece(c, piece_len(len, slot, H, std::max<uint64_t>(4096, piece_cap / H)), len);
+  const uint64_t rl_max = piece_len(c, len, slot, H, std::max<uint64_t>(4096, piece_cap / H));
+  if (!rl_max) return fail(GS_INVALID_ARGUMENT, "reconstruct_upload: staging slot of %zu B cannot hold one piece", slot);
   std::vector<CopyOp> ops;
   for (uint64_t r0 = 0; r0 < len; r0 += rl_max) {
     const uint64_t rl = std::min<uint64_t>(rl_max, len - r0);
@@ -1559,9 +1574,10 @@ int gs_encode_host_async(gs_pipeline* p, const gs_codec* c, const void* const* h
   const size_t slot = p->slot_bytes();
   // ~2 MiB per shard per piece: deep enough pipelining that the H2D of piece
   // i+1, the kernel of piece i and the D2H of piece i-1 overlap.
-  const uint64_t rl_max = align_piece(c, piece_len(len, slot, N + K, kHostPiece), len);
+  const uint64_t rl_max = piece_len(c, len, slot, N + K, kHostPiece);
+  if (!rl_max) return fail(GS_INVALID_ARGUMENT, "encode_host: staging slot of %zu B cannot hold one piece", slot);
   std::vector<CopyOp> ops;
-  const uint64_t quarter = rl_max >= 4 * 4096 ? align_piece(c, rl_max / 4 / 4096 * 4096, len) : 0;
+  const uint64_t quarter = rl_max >= 4 * 4096 ? std::min<uint64_t>(align_down_piece(c, rl_max / 4), len) : 0;
   for (uint64_t r0 = 0, rl = 0; r0 < len; r0 += rl) {
     rl = taper(r0, len, rl_max, quarter);
     const int sl = p->next;
@@ -1617,9 +1633,10 @@ int gs_reconstruct_host_async(gs_pipeline* p, const gs_codec* c, const void* con
   GS_CUDA(p->begin(p->s_h2d, p->s_h2d));
   const int U = static_cast<int>(c->used.size()), E = c->n_out;
   const size_t slot = p->slot_bytes();
-  const uint64_t rl_max = align_piece(c, piece_len(len, slot, U + E, kHostPiece), len);
+  const uint64_t rl_max = piece_len(c, len, slot, U + E, kHostPiece);
+  if (!rl_max) return fail(GS_INVALID_ARGUMENT, "reconstruct_host: staging slot of %zu B cannot hold one piece", slot);
   std::vector<CopyOp> ops;
-  const uint64_t quarter = rl_max >= 4 * 4096 ? align_piece(c, rl_max / 4 / 4096 * 4096, len) : 0;
+  const uint64_t quarter = rl_max >= 4 * 4096 ? std::min<uint64_t>(align_down_piece(c, rl_max / 4), len) : 0;
   for (uint64_t r0 = 0, rl = 0; r0 < len; r0 += rl) {
     rl = taper(r0, len, rl_max, quarter);
     const int sl = p->next;
