@@ -622,11 +622,11 @@ def test_pipeline_fuzz():
     shards bit-exact vs the oracle, several calls in flight on one ring."""
     import random
     rng = random.Random(4242)
-    for trial in range(16):
+    for trial in range(40):
         kind = rng.choice(["rs", "rs", "xor", "rdp"])
         if kind == "rs":
-            k = rng.randint(1, 3)
-            n = rng.randint(max(k, 2), 10)
+            k = rng.randint(1, 4)
+            n = rng.randint(max(k, 2), 16)
             scheme = G.CodingScheme.reed_solomon(n, k)
         elif kind == "xor":
             n, k = rng.randint(2, 8), 1
@@ -635,8 +635,8 @@ def test_pipeline_fuzz():
             n, k = rng.randint(2, 10), 2
             scheme = G.CodingScheme.rdp(n)
         S = rng.randint(1, 6)
-        ln = rng.choice([4096, 65536 + 48, 300_001, 1 << 20, 3 * (1 << 20) + 5])
-        ring = rng.choice([64 << 10, 256 << 10, 1 << 20, 16 << 20])
+        ln = rng.choice([1, 17, 4096, 65536 + 48, 300_001, 1 << 20, 3 * (1 << 20) + 5])
+        ring = rng.choice([16 << 10, 64 << 10, 256 << 10, 1 << 20, 16 << 20])
         pipe = D.Pipeline(0, ring)
         host = [[splitmix_bytes(90_000 + 1000 * trial + 37 * s + j, ln) for j in range(n)] for s in range(S)]
         data = torch.stack([to_dev(h) for h in host])
