@@ -145,3 +145,62 @@ def test_paged_multi_block_chunks_with_block_table(model, block, chunk, valid):
         for s in range(S):
             assert torch.equal(reps[w].read_chunk(perm[s], chunk, v), truth[s][w]), (w, s)
     pipe.close()
+
+
+def test_paged_fuzz_geometries():
+    """Random model geometries (layers, heads, head dim, tp), block sizes,
+    chunk sizes (one or several blocks per chunk), valid-token counts, schemes
+    and staging rings through checkpoint_chunks / rebuild_chunks: parity and
+    rebuilt pages bit-exact vs the oracle on the reference-layout slices."""
+    import random
+    from paper_2605_00831_b200.paged import checkpoint_chunks, rebuild_chunks
+    rng = random.Random(31337)
+    for trial in range(30):
+        tp = rng.choice([2, 4, 6, 8])
+        heads = tp * rng.choice([1, 2])
+        model = ModelConfig(rng.choice([1, 2, 3, 5]), heads, rng.choice([8, 16, 64, 128]), 2, tp)
+        block = rng.choice([1, 2, 8, 16])
+        chunk = block * rng.choice([1, 2, 4])
+        n = tp
+        k = rng.randint(1, min(3, n))
+        valid = rng.randint(0, chunk)
+        S = rng.randint(1, 4)
+        nblk = chunk // block
+        nblocks = S * nblk + rng.randint(0, 4)
+        g = torch.Generator(device="cuda").manual_seed(trial)
+        caches = []
+        for j in range(n):
+            c = PagedKVCache(model, nblocks, block)
+            c.buf.copy_(torch.randint(0, 256, c.buf.shape, dtype=torch.uint8, device="cuda", generator=g))
+            caches.append(c)
+        perm = np.random.default_rng(trial).permutation(nblocks)[: S * nblk].reshape(S, nblk)
+        table = torch.from_numpy(perm.astype(np.int32)).cuda()
+        truth = []
+        for s in range(S):
+            row = []
+            for j in range(n):
+                sl = make_ground_truth_slice(3, s, trial, j, model, chunk, valid, device="cuda")
+                caches[j].write_chunk(perm[s], sl, chunk, valid)
+                row.append(sl)
+            truth.append(row)
+        scheme = CodingScheme.reed_solomon(n, k)
+        pipe = D.Pipeline(0, rng.choice([16 << 10, 64 << 10, 1 << 20]))
+        slice_bytes = caches[0].chunk_slice_bytes(chunk)
+        h_par = torch.zeros((S, k, slice_bytes), dtype=torch.uint8).pin_memory()
+        st = torch.cuda.current_stream()
+        ctx = (trial, model, block, chunk, valid, n, k, S)
+        checkpoint_chunks(pipe, scheme, caches, table, chunk, valid, h_par, st, st)
+        st.synchronize()
+        for s in range(S):
+            want = O.port().encode(O.RS, n, k, [t.cpu().numpy() for t in truth[s]])
+            for i in range(k):
+                assert np.array_equal(h_par[s, i].numpy(), want[i]), ctx
+        lost_w = sorted(rng.sample(range(n), rng.randint(1, k)))
+        reps = {w: PagedKVCache(model, nblocks, block, fill=0xA5) for w in lost_w}
+        rebuild_chunks(pipe, scheme, ErasurePattern(lost_w), [None if j in lost_w else caches[j] for j in range(n)],
+                       reps, table, chunk, valid, h_par, st, st)
+        st.synchronize()
+        for w in lost_w:
+            for s in range(S):
+                assert torch.equal(reps[w].read_chunk(perm[s], chunk, valid), truth[s][w]), ctx + (w, s)
+        pipe.close()
