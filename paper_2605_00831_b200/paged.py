@@ -202,7 +202,9 @@ def rebuild_chunks(pipeline, scheme: CodingScheme, lost: ErasurePattern, caches:
         for i in range(k):
             slots.append(None if lost.contains(n + i) else hp[s * k + i])
     outs = [replacements[w].buf.data_ptr() for s in range(S) for w in dec.out_index]
-    ref = live[0]
+    # geometry reference: a surviving cache, or a replacement when every data
+    # worker was lost (the rebuild then reads parity only)
+    ref = live[0] if live else next(iter(replacements.values()))
     pm = ref.page_map(valid_tokens, chunk_tokens, block_table)
     cs = _stream(compute)
     check(L.lib().gs_reconstruct_upload_paged(pipeline.handle, dec.handle, S, L.ptr_array(slots), L.ptr_array(outs),
@@ -229,7 +231,9 @@ def rebuild_blocks(pipeline, scheme: CodingScheme, lost: ErasurePattern, caches:
         for i in range(k):
             slots.append(None if lost.contains(n + i) else hp[s * k + i])
     outs = [replacements[w].block_base(block_ids[s][w]) for s in range(S) for w in dec.out_index]
-    ref = live[0]
+    # geometry reference: a surviving cache, or a replacement when every data
+    # worker was lost (the rebuild then reads parity only)
+    ref = live[0] if live else next(iter(replacements.values()))
     pm = ref.page_map(valid_tokens)
     cs = _stream(compute)
     check(L.lib().gs_reconstruct_upload_paged(pipeline.handle, dec.handle, S, L.ptr_array(slots), L.ptr_array(outs),
