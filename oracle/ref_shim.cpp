@@ -482,3 +482,46 @@ extern "C" int ghs_get_recompute_units(uint32_t n, uint32_t chunk_size, int kind
     return map_exception();
   }
 }
+
+// A reference ParityStore driven op by op (parity_store.hpp:62-143), so the
+// host-tier mirror can be checked against it on random operation sequences.
+extern "C" void* ghs_store_new(uint64_t capacity) { return new ParityStore(capacity); }
+extern "C" void ghs_store_free(void* s) { delete static_cast<ParityStore*>(s); }
+extern "C" int ghs_store_try_put(void* s, uint64_t req, uint32_t chunk, int kind, int n, int k, uint32_t valid,
+                                 uint64_t slice_len, const uint8_t* const* parity, int* accepted) {
+  try {
+    ParityChunk c;
+    c.request_id = req;
+    c.chunk_id = ChunkId{chunk};
+    c.scheme = scheme_of(kind, n, k);
+    c.valid_tokens = valid;
+    c.slice_len = slice_len;
+    if (parity) {
+      c.parity.resize(static_cast<size_t>(k));
+      for (int i = 0; i < k; ++i) c.parity[static_cast<size_t>(i)].assign(parity[i], parity[i] + slice_len);
+    }
+    c.seal();
+    *accepted = static_cast<ParityStore*>(s)->try_put(std::move(c)) ? 1 : 0;
+    return 0;
+  } catch (...) {
+    return map_exception();
+  }
+}
+extern "C" int ghs_store_get(void* s, uint64_t req, uint32_t chunk) {
+  return static_cast<int>(static_cast<ParityStore*>(s)->get(req, chunk, nullptr));
+}
+extern "C" int ghs_store_contains(void* s, uint64_t req, uint32_t chunk) {
+  return static_cast<ParityStore*>(s)->contains(req, chunk) ? 1 : 0;
+}
+extern "C" void ghs_store_erase(void* s, uint64_t req) { static_cast<ParityStore*>(s)->erase_request(req); }
+extern "C" void ghs_store_corrupt(void* s, uint64_t req, uint32_t chunk) {
+  static_cast<ParityStore*>(s)->corrupt_entry(req, chunk);
+}
+extern "C" void ghs_store_stats(void* s, uint64_t* out5) {
+  auto* st = static_cast<ParityStore*>(s);
+  out5[0] = st->used_bytes();
+  out5[1] = st->payload_bytes();
+  out5[2] = st->peak_payload_bytes();
+  out5[3] = st->entry_count();
+  out5[4] = st->audit() ? 1 : 0;
+}

@@ -89,3 +89,69 @@ def test_gsrv_round_trip_matches_reference_bytes(golden):
         deserialize_parity_store(b"XSRV" + bytes.fromhex(g["image_hex"])[4:])
     with pytest.raises(ParityFileError):
         deserialize_parity_store(bytes.fromhex(g["image_hex"]), capacity_bytes=100)
+
+
+@needs_pinned
+@pytest.mark.gpu
+def test_store_matches_reference_on_random_operations():
+    """Random try_put / get / contains / erase_request / corrupt sequences
+    with capacity back-pressure and duplicates: the native host tier answers
+    exactly like the reference's ParityStore (compiled in place) after every
+    operation, accounting and peak included."""
+    import ctypes as C
+    import random
+    from oracle import oracle as O
+    if not O.have_ref():
+        pytest.skip("reference not compiled here")
+    ref = O.ref()
+    f = lambda name: ref.fn(name)  # noqa: E731
+    f("store_new").restype = C.c_void_p
+    f("store_new").argtypes = [C.c_uint64]
+    for nm in ("store_free",):
+        f(nm).argtypes = [C.c_void_p]
+    f("store_try_put").argtypes = [C.c_void_p, C.c_uint64, C.c_uint32, C.c_int, C.c_int, C.c_int, C.c_uint32,
+                                   C.c_uint64, C.c_void_p, C.POINTER(C.c_int)]
+    f("store_get").argtypes = [C.c_void_p, C.c_uint64, C.c_uint32]
+    f("store_contains").argtypes = [C.c_void_p, C.c_uint64, C.c_uint32]
+    f("store_erase").argtypes = [C.c_void_p, C.c_uint64]
+    f("store_corrupt").argtypes = [C.c_void_p, C.c_uint64, C.c_uint32]
+    f("store_stats").argtypes = [C.c_void_p, C.POINTER(C.c_uint64)]
+    rng = random.Random(99)
+    for cap in (ParityStore.UNLIMITED if hasattr(ParityStore, "UNLIMITED") else (1 << 64) - 1, 50_000, 9_000):
+        mine = ParityStore(cap)
+        theirs = f("store_new")(cap)
+        try:
+            for step in range(400):
+                op = rng.random()
+                req, ch = rng.randrange(6), rng.randrange(8)
+                if op < 0.45:
+                    k = rng.randint(1, 3)
+                    ln = rng.choice([0, 16, 1000, 4096])
+                    par = [splitmix_bytes(rng.randrange(1 << 30), ln) for _ in range(k)] if ln else []
+                    c = ParityChunk(req, ch, CodingScheme.reed_solomon(4, k), par, rng.randrange(17), ln)
+                    c.seal()
+                    acc = C.c_int(-1)
+                    arr = (C.c_void_p * k)(*[p.ctypes.data for p in par]) if par else None
+                    rst = f("store_try_put")(theirs, req, ch, 2, 4, k, c.valid_tokens, ln, arr, C.byref(acc))
+                    try:
+                        got = mine.try_put(c)
+                        assert rst == 0 and int(got) == acc.value, (step, cap)
+                    except LogicError:
+                        assert rst == 1, (step, cap)   # duplicate -> logic_error on both sides
+                elif op < 0.75:
+                    st, _ = mine.get(req, ch)
+                    assert int(st) == f("store_get")(theirs, req, ch), (step, cap)
+                    assert mine.contains(req, ch) == bool(f("store_contains")(theirs, req, ch))
+                elif op < 0.85:
+                    mine.erase_request(req)
+                    f("store_erase")(theirs, req)
+                else:
+                    mine.corrupt_entry(req, ch)
+                    f("store_corrupt")(theirs, req, ch)
+                out = (C.c_uint64 * 5)()
+                f("store_stats")(theirs, out)
+                assert (mine.used_bytes(), mine.payload_bytes(), mine.peak_payload_bytes(), mine.entry_count(),
+                        int(mine.audit())) == tuple(out), (step, cap)
+        finally:
+            f("store_free")(theirs)
+            mine.close()
