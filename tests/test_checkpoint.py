@@ -204,3 +204,37 @@ def test_serving_loop_example_runs_bit_exact():
                          timeout=600, cwd=root)
     assert out.returncode == 0, out.stderr[-2000:]
     assert "bit-exact: True" in out.stdout and "masked tail of 8 tokens" in out.stdout, out.stdout
+
+
+@pytest.mark.gpu
+def test_orchestration_fuzz():
+    """Random schemes (RS(tp, k)), geometries, chunk sizes, prompt and decode
+    lengths and 1..k failed workers: prefill + decode checkpointing, then
+    recover() -- every recovered slice bit-exact (recovery.hpp:135-145)."""
+    import random
+    from paper_2605_00831_b200.checkpoint import DecodeCheckpointer
+    rng = random.Random(5150)
+    for trial in range(10):
+        tp = rng.choice([2, 4, 6, 8])
+        k = rng.randint(1, min(3, tp))
+        chunk = rng.choice([4, 16, 32])
+        ck, store, torch = _ck(tp, k, tp, chunk=chunk, layers=rng.choice([1, 2, 3]), heads=tp,
+                               dim=rng.choice([8, 16]), restart=1e9)
+        req = 100 + trial
+        tokens = rng.randint(1, 5 * chunk)
+        run = ck.run_prefill_with_checkpointing(req, tokens, kv_seed=trial)
+        ground, counts = list(run.ground_truth), [min(chunk, tokens - c * chunk) for c in range(run.chunks_done)]
+        if tokens % chunk == 0:
+            dec = DecodeCheckpointer(req, run.chunks_done, ck, kv_seed=trial)
+            steps = rng.randint(0, 3 * chunk)
+            for _ in range(steps):
+                dec.step(run.state)
+            dec.flush(run.state)
+            ground += dec.ground_truth
+            counts += [s[0].valid_tokens for s in dec.ground_truth]
+        ck.synchronize()
+        failed = sorted(rng.sample(range(tp), rng.randint(1, k)))
+        res = ck.recover(req, FailureEvent(failed, at_chunk=len(ground)), ground, counts)
+        assert res.verified, (trial, tp, k, chunk, tokens, failed, res.plan.mode)
+        assert res.plan.recompute_chunks == 0 and len(res.plan.reconstruct_ids) == len(ground)
+        ck.close()
