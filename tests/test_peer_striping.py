@@ -294,3 +294,44 @@ def test_ipc_rotating_encode_two_processes_one_gpu():
     if not torch.cuda.is_available():
         pytest.fail("GPU test collected without a CUDA device")
     _run(_gpu_rotating_worker)
+
+
+def test_striped_partition_fuzz_single_process():
+    """Random TP widths, world sizes (dividing n), stripe counts and lengths:
+    every rank's byte range of every shard, resolved through the owners' base
+    addresses (all ranks simulated in one process), reassembles exactly the
+    full parity (no GPU: the pointer arithmetic of peer.striped_slots)."""
+    import random
+    import sys
+    sys.path.insert(0, ROOT)
+    from paper_2605_00831_b200.peer import ShardLayout, striped_slots
+    rng = random.Random(808)
+    port_lib = O.port()
+    for trial in range(25):
+        n = rng.choice([2, 4, 6, 8, 12, 16])
+        world = rng.choice([w for w in (1, 2, 3, 4, 6, 8) if n % w == 0])
+        k = rng.randint(1, min(4, n))
+        S = rng.randint(1, 4)
+        L = rng.choice([1, 17, 4095, 4096, 4097, 3 * 4096 + 80, 65536 + 3])
+        lay = ShardLayout(n, world, S, L)
+        shards = [[splitmix_bytes(50_000 + 1000 * trial + 31 * s + j, L) for j in range(n)] for s in range(S)]
+        mem = [np.stack([np.stack(shards[s][r * lay.n_local:(r + 1) * lay.n_local]) for s in range(S)])
+               for r in range(world)]
+        bases = [m.ctypes.data for m in mem]
+        got = [[np.zeros(L, np.uint8) for _ in range(k)] for _ in range(S)]
+        covered = 0
+        for rank in range(world):
+            off, ln, slots = striped_slots(lay, bases, rank)
+            covered += ln
+            if not ln:
+                continue
+            for s in range(S):
+                data = [np.ctypeslib.as_array(C.cast(p, C.POINTER(C.c_uint8)), (ln,)).copy() for p in slots[s]]
+                part = port_lib.encode(O.RS, n, k, data)
+                for i in range(k):
+                    got[s][i][off:off + ln] = part[i]
+        assert covered == L, (trial, n, world, L)
+        for s in range(S):
+            want = port_lib.encode(O.RS, n, k, shards[s])
+            for i in range(k):
+                assert np.array_equal(got[s][i], want[i]), (trial, n, world, k, S, L, s, i)
