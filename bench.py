@@ -972,6 +972,10 @@ def c3_orchestrated(torch, dev, link, k1_gbs, k2_gbs):
     # free lists, torch caching allocator), as in a serving process
     warm = ck.run_prefill_with_checkpointing(10, tokens, kv_seed=KV_SEED, keep_ground_truth=True)
     ck.synchronize()
+    # ... and the recovery's device buffers (uploaded parity rows, rebuilt
+    # shards, GPU checksum scratch) likewise
+    ck.recover(10, FailureEvent([5], at_chunk=warm.chunks_done), warm.ground_truth, [m] * warm.chunks_done,
+               verify_threads=max(1, (os.cpu_count() or 1) - 2))
     del warm
     store.erase_request(10)
     t0 = time.perf_counter()
@@ -992,11 +996,15 @@ def c3_orchestrated(torch, dev, link, k1_gbs, k2_gbs):
            "plan": {"mode": res.plan.mode, "recompute_chunks": res.plan.recompute_chunks,
                     "reconstruct_chunks": len(res.plan.reconstruct_ids),
                     "recompute_chunks_with_reference_constants": r_ref},
+           "plan_ms": round(res.plan_ms, 1), "enqueue_ms": round(res.enqueue_ms, 1),
            "verify_host_ms": round(res.verify_host_ms, 1), "verify_threads": threads,
+           "verify_gpu_chunks": res.verify_gpu_chunks,
            "decode_device_ms": round(res.reconstruct_device_ms, 2), "recover_wall_ms": round(res.wall_ms, 1),
            "parity_bytes_verified": len(res.plan.reconstruct_ids) * 2 * sl, "verified": res.verified,
-           "note": "wall = plan + speculative batched H2D/K2 overlapped with the FNV verification of the "
-                   "64 entries (reference semantics: corrupt parity -> full-recompute fallback)"}
+           "note": "wall = plan + speculative H2D/K2 overlapped with the FNV verification of the 64 entries "
+                   "(reference semantics: corrupt parity -> full-recompute fallback); verify_gpu_chunks of them "
+                   "upload both parity rows and are checksummed in HBM (bit-sliced GPU FNV-1a), the rest on "
+                   "host threads, split so the host link and the host cores finish together"}
     ck.close()
     del run, res
     torch.cuda.empty_cache()

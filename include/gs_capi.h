@@ -280,6 +280,22 @@ uint64_t gs_parity_checksum(const void* const* parity, int k, size_t len);
  * out[c] = checksum of parity[c*k .. c*k+k-1]. */
 int gs_parity_checksum_batch(const void* const* parity, int n_chunks, int k, size_t len,
                              int threads, uint64_t* out);
+/* The same FNV-1a on the GPU, bit-exact (gs_fnv_gpu.cu): chain c is the k
+ * device buffers bufs[c*k .. c*k+k-1] of `len` bytes each, concatenated in
+ * order and hashed from h0 (0xcbf29ce484222325 = ParityChunk checksum);
+ * d_out[c] (device memory) receives the hash, stream-ordered on `stream`.
+ * len % 16 == 0 and 16-B aligned buffers (GS_INVALID_ARGUMENT otherwise).
+ * Replaces the serial parity_store.hpp:19-25 loop for parity that is already
+ * in HBM: bit-sliced low-byte recovery + a linear reduction, no serial chain. */
+int gs_fnv1a64_device(const void* const* bufs, int n_chains, int k, uint64_t len, uint64_t h0,
+                      uint64_t* d_out, void* stream);
+/* Upload chunks' pinned host parity rows (h_parity[c*k + i]) into device rows
+ * (d_parity[c*k + i]) on `copy` and checksum them on the GPU on `compute` as
+ * groups land: d_sums[c] = ParityChunk::compute_checksum of chunk c as it sits
+ * in HBM (the verification of reconstruct_chunk, recovery.hpp:108-113, moved
+ * off the host; the uploaded rows then feed K2 directly). */
+int gs_parity_upload_checksum(const void* const* h_parity, int n_chunks, int k, uint64_t len,
+                              void* const* d_parity, uint64_t* d_sums, void* compute, void* copy);
 
 /* ---- host tier: ParityStore on pinned slabs (parity_store.hpp:31-263) ----
  * Entries are keyed (request, chunk). Reserve -> the D2H of K1 writes the k

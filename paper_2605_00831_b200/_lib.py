@@ -71,6 +71,8 @@ SIGNATURES = {
     "gs_fnv1a64": (_u64, [_vp, _sz, _u64]),
     "gs_parity_checksum": (_u64, [_vpp, _i, _sz]),
     "gs_parity_checksum_batch": (_i, [_vpp, _i, _i, _sz, _i, _u64p]),
+    "gs_fnv1a64_device": (_i, [_vpp, _i, _i, _u64, _u64, _vp, _vp]),
+    "gs_parity_upload_checksum": (_i, [_vpp, _i, _i, _u64, _vpp, _vp, _vp, _vp]),
     "gs_store_create": (_i, [_u64, _i, _vpp]),
     "gs_store_destroy": (_i, [_vp]),
     "gs_store_reserve": (_i, [_vp, _u64, _u32, _i, _i, _i, _u32, _u64, _ip, _vpp]),

@@ -223,6 +223,9 @@ class RecoveryResult:
     parity_bytes_fetched: int = 0
     reconstruct_device_ms: float = 0.0   # batched H2D + K2 over every reconstructed chunk
     verify_host_ms: float = 0.0          # FNV verification of their parity (host threads)
+    plan_ms: float = 0.0                 # get_recompute_units + store lookups
+    enqueue_ms: float = 0.0              # host time to enqueue the batched H2D + K2
+    verify_gpu_chunks: int = 0           # entries whose checksum was verified on the GPU
     wall_ms: float = 0.0                 # plan -> verified, rebuilt bytes on the device
 
 
@@ -232,6 +235,35 @@ def verify_recovery(recovered, ground_truth) -> bool:
         return (recovered.worker == ground_truth.worker and recovered.valid_tokens == ground_truth.valid_tokens
                 and verify_recovery(recovered.bytes, ground_truth.bytes))
     return recovered.numel() == ground_truth.numel() and bool(torch.equal(recovered, ground_truth))
+
+
+class _HostVerify:
+    """FNV verification of parity entries on host threads, run from a Python
+    thread (the C call releases the GIL) so it overlaps the enqueue of the
+    speculative decode instead of following it."""
+
+    def __init__(self, ck: "Checkpointer", entries, threads: int):
+        import threading
+        self._ok = True
+        self._ms = 0.0
+        self._err: Optional[BaseException] = None
+
+        def run():
+            t0 = time.perf_counter()
+            try:
+                self._ok = all(ck._verify_entries(entries, threads))
+            except BaseException as e:   # re-raised in result()
+                self._err = e
+            self._ms = (time.perf_counter() - t0) * 1e3
+
+        self._t = threading.Thread(target=run, daemon=True)
+        self._t.start()
+
+    def result(self):
+        self._t.join()
+        if self._err is not None:
+            raise self._err
+        return self._ok, self._ms
 
 
 # ---------------------------------------------------------------------------
@@ -251,7 +283,15 @@ class Checkpointer:
         self.pipe = Pipeline(device, staging_bytes)
         self.compute = torch.cuda.Stream(device=self.dev)
         self.copy = torch.cuda.Stream(device=self.dev)
+        self.verify = torch.cuda.Stream(device=self.dev)   # GPU parity checksums (recover)
         self.slice = slice_bytes(cfg.model, cfg.chunk_size)
+        # Aggregate host FNV-1a rate (bytes/s) used to split recovery's parity
+        # verification between host threads and the GPU (recover()): ~1.6 GB/s
+        # per hardware thread while the parity upload streams over the same
+        # host memory (measured on the B200 hosts, bench recovery.c3_orchestrated).
+        self.host_fnv_rate = 1.6e9 * max(1, (os.cpu_count() or 1) - 2)
+        # False: verify every entry on host threads (the reference's placement)
+        self.gpu_verify = True
 
     def close(self) -> None:
         self.pipe.close()
@@ -380,11 +420,15 @@ class Checkpointer:
         every one of their parity entries to verify (kCorrupt / kMissing ->
         full-recompute fallback).
 
-        B200 schedule of the same decisions: ONE batched gs_reconstruct_upload
-        (H2D of the used parity rows + K2 over all n-r chunks, pieces pipelined)
-        is enqueued speculatively, and the FNV verification of those entries
-        runs on host threads while it executes; a failed verification discards
-        the decode and falls back exactly as the planning pass would. Each
+        B200 schedule of the same decisions: the decode of all n-r chunks is
+        enqueued speculatively while their parity is verified, and a failed
+        verification discards it and falls back exactly as the planning pass
+        would. The verification is split (_gpu_verify_count) so the host link
+        and the host cores finish together: g entries upload ALL their parity
+        rows and are checksummed in HBM as they land (gs_parity_upload_checksum,
+        the bit-sliced GPU FNV-1a), then K2 reads the uploaded rows; the other
+        n-r-g go through one gs_reconstruct_upload (H2D of only the used rows +
+        K2, pieces pipelined) while host threads run their serial FNV. Each
         chunk's parity is verified once (the reference re-verifies inside
         reconstruct_chunk; the store is not modified in between)."""
         cfg = self.cfg
@@ -408,15 +452,46 @@ class Checkpointer:
                     break
                 entries.append(e)
         failed = set(failure.failed_workers)
-        pending = None
-        if parity_ok and not over and r < n and ground_truth is not None:
+        pending = []            # (first chunk id, outs, out_index, keep-alive)
+        gpu_sums = None
+        n_gpu = 0
+        e0 = e1 = None
+        result.plan_ms = (time.perf_counter() - t_wall) * 1e3
+        decode = parity_ok and not over and r < n and ground_truth is not None
+        host_verify = None
+        if parity_ok and entries:
+            if decode and self.gpu_verify:
+                n_gpu = self._gpu_verify_count(len(entries), failed)
+            if entries[n_gpu:]:   # host threads verify the rest, overlapped with the enqueue and decode
+                host_verify = _HostVerify(self, entries[n_gpu:], verify_threads)
+        if decode:
             if len(ground_truth) < n:
                 raise RuntimeError("recovery: ground truth missing for completed chunks")
-            pending = self._enqueue_batched_decode(ground_truth, list(range(r, n)), entries, failed)
-        if parity_ok and entries:   # planning-pass verification, overlapped with the decode
             t0 = time.perf_counter()
-            parity_ok = all(self._verify_entries(entries, verify_threads))
-            result.verify_host_ms = (time.perf_counter() - t0) * 1e3
+            ids = list(range(r, n))
+            cur = torch.cuda.current_stream(self.dev)
+            for st in (self.compute, self.copy, self.verify):
+                st.wait_stream(cur)
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(self.compute)
+            if n_gpu:   # uploads of every parity row first: the GPU hashes them as they land
+                outs, oi, gpu_sums, par = self._enqueue_gpu_verified_decode(ground_truth, ids[:n_gpu],
+                                                                             entries[:n_gpu], failed)
+                pending.append((r, outs, oi, par))
+            if n_gpu < len(ids):
+                outs, oi = self._enqueue_batched_decode(ground_truth, ids[n_gpu:], entries[n_gpu:], failed)
+                pending.append((r + n_gpu, outs, oi, None))
+            self.compute.wait_stream(self.verify)
+            e1.record(self.compute)
+            cur.wait_stream(self.compute)
+            result.enqueue_ms = (time.perf_counter() - t0) * 1e3
+        if parity_ok and entries:
+            if host_verify is not None:
+                parity_ok, result.verify_host_ms = host_verify.result()
+            if n_gpu:
+                sums = [int(v) & 0xFFFFFFFFFFFFFFFF for v in gpu_sums.cpu().tolist()]
+                parity_ok = parity_ok and all(sums[i] == entries[i].checksum for i in range(n_gpu))
+                result.verify_gpu_chunks = n_gpu
         if over or (not parity_ok and r < n):
             plan.mode, r = RecoveryMode.kFullRecomputeFallback, n
         elif r >= n:
@@ -436,18 +511,18 @@ class Checkpointer:
         for c in range(r):   # recompute lane stand-in: restore from the ground-truth slices
             for w in failure.failed_workers:
                 result.recovered[w][c] = ground_truth[c][w]
-        if r < n:
-            outs, out_index, e0, e1 = pending
+        if e1 is not None:
             e1.synchronize()
+        if r < n:
             result.reconstruct_device_ms = e0.elapsed_time(e1)
-            for i, c in enumerate(range(r, n)):
-                for b, w in enumerate(out_index):
-                    result.recovered[w][c] = KvChunkSlice(request_id, c, w, outs[i, b], entries[i].valid_tokens)
+            for c_first, outs, out_index, _ in pending:
+                for i in range(outs.shape[0]):
+                    for b, w in enumerate(out_index):
+                        result.recovered[w][c_first + i] = KvChunkSlice(request_id, c_first + i, w, outs[i, b],
+                                                                        entries[c_first + i - r].valid_tokens)
             for w in failure.failed_workers:
                 if any(result.recovered[w][c] is None for c in range(r, n)):
                     raise RuntimeError("recovery: codec did not return a failed shard")
-        elif pending is not None:
-            pending[3].synchronize()   # discarded speculative decode
         result.wall_ms = (time.perf_counter() - t_wall) * 1e3
         for c in range(r, n):
             for w in failure.failed_workers:
@@ -468,37 +543,84 @@ class Checkpointer:
               "verify")
         return [int(out[i]) == e.checksum for i, e in enumerate(entries)]
 
-    def _enqueue_batched_decode(self, ground_truth, chunk_ids, entries, failed):
+    def _gpu_verify_count(self, n: int, failed: Set[int]) -> int:
+        """How many of the n entries to verify on the GPU. A GPU-verified
+        entry uploads all k parity rows (the checksum chains over every row)
+        instead of the u rows the decode uses; a host-verified one costs k
+        rows of serial FNV on host threads. Pick g minimising
+        max(link time, host FNV time):  link = (n*u + g*(k-u)) L / B_link,
+        host = (n-g) k L / B_fnv."""
+        k = self.cfg.scheme.k
+        u = min(k, len(failed))
+        if self.slice % 16 or n == 0:
+            return 0
+        if u >= k:
+            return n   # no extra upload: verify everything on the GPU
+        bl, bf = self.cfg.cost.host_bw, self.host_fnv_rate
+        g = n * (k / bf - u / bl) / ((k - u) / bl + k / bf)
+        return max(0, min(n, int(math.ceil(g))))
+
+    def _survivor_row(self, gt, failed) -> List[Optional[int]]:
         sch = self.cfg.scheme
-        lost = ErasurePattern(sorted(failed))
-        dec = decoder(sch, lost)
+        row: List[Optional[int]] = [None] * (sch.n + sch.k)
+        for sl in gt:
+            if sl.worker not in failed:
+                row[sl.worker] = sl.bytes.data_ptr()
+        for j in range(sch.n):
+            if j not in failed and row[j] is None:
+                raise InvalidArgument(f"coding: surviving shard {j} missing from input")
+        return row
+
+    def _enqueue_gpu_verified_decode(self, ground_truth, chunk_ids, entries, failed):
+        """Upload every parity row of these entries into HBM (copy stream),
+        checksum them there as they land (gs_parity_upload_checksum, compute
+        stream) and rebuild the lost shards from the uploaded rows with K2."""
+        sch = self.cfg.scheme
+        dec = decoder(sch, ErasurePattern(sorted(failed)))
+        S, k = len(chunk_ids), sch.k
+        lib = L.lib()
+        par = torch.empty((S, k, self.slice), dtype=torch.uint8, device=self.dev)
+        sums = torch.empty(S, dtype=torch.int64, device=self.dev)
+        check(lib.gs_parity_upload_checksum(L.ptr_array([e.parity[i].ctypes.data for e in entries for i in range(k)]),
+                                            S, k, self.slice,
+                                            L.ptr_array([par[s, i].data_ptr() for s in range(S) for i in range(k)]),
+                                            sums.data_ptr(), self.verify.cuda_stream, self.copy.cuda_stream),
+              "recover verify")
+        self.compute.wait_stream(self.copy)   # K2 needs the uploaded rows, not their checksums
+        outs = torch.empty((S, max(dec.n_out, 1), self.slice), dtype=torch.uint8, device=self.dev)
+        if dec.n_out:
+            slots: List[Optional[int]] = []
+            for s, c in enumerate(chunk_ids):
+                row = self._survivor_row(ground_truth[c], failed)
+                for i in range(k):
+                    row[sch.n + i] = par[s, i].data_ptr()
+                slots.extend(row)
+            check(lib.gs_apply_device(dec.handle, S, L.ptr_array(slots),
+                                      L.ptr_array([outs[s, b].data_ptr() for s in range(S)
+                                                   for b in range(dec.n_out)]),
+                                      self.slice, self.compute.cuda_stream), "recover")
+        return outs, list(dec.out_index), sums, par
+
+    def _enqueue_batched_decode(self, ground_truth, chunk_ids, entries, failed):
+        """One gs_reconstruct_upload over the chunks: H2D of the used parity
+        rows from the host entries + K2, pieces pipelined."""
+        sch = self.cfg.scheme
+        dec = decoder(sch, ErasurePattern(sorted(failed)))
         S = len(chunk_ids)
         outs = torch.empty((S, max(dec.n_out, 1), self.slice), dtype=torch.uint8, device=self.dev)
         slots: List[Optional[int]] = []
         for c, e in zip(chunk_ids, entries):
-            gt = ground_truth[c]
-            row: List[Optional[int]] = [None] * (sch.n + sch.k)
-            for sl in gt:
-                if sl.worker not in failed:
-                    row[sl.worker] = sl.bytes.data_ptr()
+            row = self._survivor_row(ground_truth[c], failed)
             for i in range(sch.k):
                 row[sch.n + i] = e.parity[i].ctypes.data
-            for j in range(sch.n):
-                if j not in failed and row[j] is None:
-                    raise InvalidArgument(f"coding: surviving shard {j} missing from input")
             slots.extend(row)
-        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        self.compute.wait_stream(torch.cuda.current_stream(self.dev))
-        e0.record(self.compute)
         if dec.n_out:
             check(L.lib().gs_reconstruct_upload(self.pipe.handle, dec.handle, S, L.ptr_array(slots),
                                                 L.ptr_array([outs[i, b].data_ptr() for i in range(S)
                                                              for b in range(dec.n_out)]),
                                                 self.slice, self.compute.cuda_stream, self.copy.cuda_stream),
                   "recover")
-        e1.record(self.compute)
-        torch.cuda.current_stream(self.dev).wait_stream(self.compute)
-        return outs, list(dec.out_index), e0, e1
+        return outs, list(dec.out_index)
 
 
 class DecodeCheckpointer:

@@ -1763,17 +1763,23 @@ int gs_parity_checksum_batch(const void* const* parity, int n_chunks, int k, siz
   if (n_chunks < 0 || k < 1 || !out || (n_chunks > 0 && !parity))
     return fail(GS_INVALID_ARGUMENT, "checksum_batch: bad arguments");
   if (threads < 1) threads = 1;
-  const int groups = (n_chunks + 3) / 4;  // four chunks advanced in lockstep per thread
+  // Every chain is serial (one multiply per byte), so the wall time is the
+  // number of chains one thread advances one after another times a chain's
+  // length: give each thread ONE lockstep group of ceil(chunks / threads)
+  // chains (4..8) rather than several groups of four.
+  const int per = std::max(4, std::min(8, (n_chunks + threads - 1) / std::max(threads, 1)));
+  const int groups = (n_chunks + per - 1) / per;
   threads = std::min(threads, std::max(1, groups));
   std::atomic<int> next{0};
   auto work = [&] {
     for (int g = next.fetch_add(1); g < groups; g = next.fetch_add(1)) {
-      const int c0 = 4 * g, m = std::min(4, n_chunks - c0);
-      uint64_t h[4] = {kFnvOffset, kFnvOffset, kFnvOffset, kFnvOffset};
+      const int c0 = per * g, m = std::min(per, n_chunks - c0);
+      uint64_t h[8];
+      for (int q = 0; q < 8; ++q) h[q] = kFnvOffset;
       for (int i = 0; i < k; ++i) {  // chained over the k buffers in order
-        const uint8_t* ps[4];
+        const uint8_t* ps[8];
         for (int q = 0; q < m; ++q) ps[q] = static_cast<const uint8_t*>(parity[static_cast<size_t>(c0 + q) * k + i]);
-        fnv1a64_x4(ps, m, len, h);
+        fnv1a64_x8(ps, m, len, h);
       }
       for (int q = 0; q < m; ++q) out[c0 + q] = h[q];
     }

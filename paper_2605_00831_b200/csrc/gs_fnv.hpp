@@ -1,7 +1,8 @@
 // gs_fnv.hpp -- FNV-1a 64 (parity_store.hpp:19-25), bit-exact, for the
 // host-side parity seal. One chain is a serial xor -> 64-bit multiply per
 // byte (latency-bound, ~0.7 GB/s per core); independent chunks are advanced
-// in lockstep, four per thread, so the multiplier pipelines across chains.
+// in lockstep (four, or up to eight when there are few chains per thread), so
+// the multiplier pipelines across chains.
 #pragma once
 
 #include <cstddef>
@@ -38,6 +39,34 @@ inline void fnv1a64_x4(const uint8_t* const* p, int m, size_t len, uint64_t* h) 
   if (m > 1) h[1] = b;
   if (m > 2) h[2] = c;
   if (m > 3) h[3] = d;
+}
+
+// Same for up to eight chains (m <= 8, exactly m multiplies per byte): used
+// when the chains outnumber the threads by a non-multiple of four, so every
+// thread takes ONE group and the wall time is one chain's length, not two.
+template <int M>
+inline void fnv1a64_lanes(const uint8_t* const* p, size_t len, uint64_t* h) {
+  const uint8_t* q[M];
+  uint64_t v[M];
+  for (int c = 0; c < M; ++c) {
+    q[c] = p[c];
+    v[c] = h[c];
+  }
+  for (size_t i = 0; i < len; ++i) {
+#pragma GCC unroll 8
+    for (int c = 0; c < M; ++c) v[c] = (v[c] ^ q[c][i]) * kFnvPrime;
+  }
+  for (int c = 0; c < M; ++c) h[c] = v[c];
+}
+
+inline void fnv1a64_x8(const uint8_t* const* p, int m, size_t len, uint64_t* h) {
+  switch (m) {
+    case 5: return fnv1a64_lanes<5>(p, len, h);
+    case 6: return fnv1a64_lanes<6>(p, len, h);
+    case 7: return fnv1a64_lanes<7>(p, len, h);
+    case 8: return fnv1a64_lanes<8>(p, len, h);
+    default: return fnv1a64_x4(p, m, len, h);
+  }
 }
 
 }  // namespace gsb

@@ -1,0 +1,383 @@
+// gs_fnv_gpu.cu -- FNV-1a 64 (parity_store.hpp:19-25) of long byte chains on
+// the GPU, bit-exact with the serial definition
+//
+//     h_{i+1} = (h_i ^ b_i) * P  (mod 2^64),  P = 0x100000001b3.
+//
+// One chain is inherently serial on a CPU (a multiply per byte, ~1 GB/s per
+// core); the GPU splits it with two observations.
+//
+// 1. XOR with a byte only touches the low byte of h, so h ^ b = h + d with
+//    d = (s ^ b) - s, s = h mod 256. Given the sequence of low bytes s_i the
+//    recurrence is LINEAR:  h_N = h_0 * P^N + sum_i d_i * P^(N - i).
+//    That sum is an ordinary parallel reduction (k_fnv_final).
+//
+// 2. The low bytes follow an 8-bit machine  s' = ((s ^ b) * 0xB3) mod 256
+//    (P mod 256 = 0xB3), and bit k of s' depends only on bits <= k:
+//        s'_k = s_k ^ b_k ^ bit_k(((s ^ b) mod 2^k) * 0xB3)
+//    (0xB3 is odd, so x_k * 2^k * 0xB3 adds exactly x_k at bit k). Once bits
+//    < k of every s_i are known, bit k is an XOR prefix scan of
+//    e_i = b_k ^ bit_k(...). Eight rounds (k = 0..7) of "map + XOR scan"
+//    recover every s_i without a serial chain (k_fnv_round + k_fnv_scan).
+//
+// Layout: a chain is the concatenation of k buffers of `len` bytes (the
+// parity buffers of one chunk, chained in order as ParityChunk::
+// compute_checksum does, parity_store.hpp:46-50). Blocks of 16 KiB (256
+// threads x 64 contiguous bytes). Between rounds the low bytes are kept in a
+// scratch byte array, RELATIVE to each block's entry state (so a round never
+// waits for the global scan of its own bit); the per-block entry bytes come
+// from k_fnv_scan, one CTA per chain.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdarg>
+#include <cstdint>
+#include <cstdio>
+#include <mutex>
+#include <set>
+
+#include "../../include/gs_capi.h"
+
+namespace gsb {
+void set_last_error(const char* msg);  // gs_capi.cu
+}
+
+namespace {
+
+constexpr int kFT = 256;                       // threads per CTA
+constexpr int kFPer = 64;                      // contiguous bytes per thread
+constexpr uint32_t kFB = kFT * kFPer;          // 16 KiB per block
+constexpr int kFCap = 480;                     // buffer pointers per job
+constexpr uint64_t kFnvP = 0x100000001b3ull;
+constexpr uint64_t kScratchBudget = 2ull << 30;  // bytes of low-byte scratch per job
+
+int ffail(int status, const char* fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  std::vsnprintf(buf, sizeof buf, fmt, ap);
+  va_end(ap);
+  gsb::set_last_error(buf);
+  return status;
+}
+
+struct FnvJob {
+  const uint8_t* p[kFCap];  // chain c, buffer i -> p[c * k + i]
+  int k;
+  uint64_t len;             // bytes per buffer (multiple of 16)
+  uint64_t n;               // bytes per chain = k * len
+  uint32_t bpc;             // blocks per chain
+  uint32_t nblocks;         // chains * bpc
+};
+
+__device__ __forceinline__ uint64_t pow64(uint64_t b, uint64_t e) {
+  uint64_t r = 1;
+  while (e) {
+    if (e & 1) r *= b;
+    b *= b;
+    e >>= 1;
+  }
+  return r;
+}
+
+// The thread's four 16-byte groups of block `blk`; groups at or past the end
+// of the chain are zero and not `valid`.
+__device__ __forceinline__ int load_groups(const FnvJob& j, uint32_t c, uint64_t pos0, uint4 (&d)[4]) {
+  int nvalid = 0;
+  if (pos0 >= j.n) {
+#pragma unroll
+    for (int q = 0; q < 4; ++q) d[q] = make_uint4(0, 0, 0, 0);
+    return 0;
+  }
+  uint64_t bi = pos0 / j.len;
+  uint64_t off = pos0 - bi * j.len;
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    const uint64_t p = pos0 + 16u * q;
+    if (p < j.n) {
+      while (off >= j.len) {
+        off -= j.len;
+        ++bi;
+      }
+      d[q] = __ldcs(reinterpret_cast<const uint4*>(j.p[c * j.k + bi] + off));
+      ++nvalid;
+    } else {
+      d[q] = make_uint4(0, 0, 0, 0);
+    }
+    off += 16;
+  }
+  return nvalid;
+}
+
+__device__ __forceinline__ uint32_t& wd(uint4& v, int w) { return w == 0 ? v.x : w == 1 ? v.y : w == 2 ? v.z : v.w; }
+
+// Round K: bit K of every low byte, relative to the block's entry bit K.
+template <int K>
+__global__ void __launch_bounds__(kFT) k_fnv_round(const FnvJob j, uint8_t* __restrict__ scratch,
+                                                   uint8_t* __restrict__ agg, const uint8_t* __restrict__ entry) {
+  __shared__ uint32_t wpar[kFT / 32];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  constexpr uint32_t kMask = ((1u << K) - 1u) * 0x01010101u;
+  for (uint32_t blk = blockIdx.x; blk < j.nblocks; blk += gridDim.x) {
+    const uint32_t c = blk / j.bpc, b = blk - c * j.bpc;
+    const uint64_t pos0 = static_cast<uint64_t>(b) * kFB + static_cast<uint64_t>(tid) * kFPer;
+    uint4 d[4];
+    const int nvalid = load_groups(j, c, pos0, d);
+    uint4 s[4];
+    uint4* sp = reinterpret_cast<uint4*>(scratch + static_cast<uint64_t>(blk) * kFB + tid * kFPer);
+#pragma unroll
+    for (int q = 0; q < 4; ++q) s[q] = K > 0 ? sp[q] : make_uint4(0, 0, 0, 0);
+    const uint32_t rep = K > 0 ? entry[blk] * 0x01010101u : 0u;
+    uint64_t e64 = 0;
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+#pragma unroll
+      for (int w = 0; w < 4; ++w) {
+        const uint32_t bw = wd(d[q], w);
+        const uint32_t x = ((wd(s[q], w) ^ rep) ^ bw) & kMask;  // (s ^ b) mod 2^K, true bits
+        const uint32_t lo = (x & 0x00FF00FFu) * 0xB3u;           // bytes 0, 2 in 16-bit lanes
+        const uint32_t hi = ((x >> 8) & 0x00FF00FFu) * 0xB3u;    // bytes 1, 3
+        const uint32_t t = ((lo >> K) & 0x00010001u) | (((hi >> K) & 0x00010001u) << 8);
+        const uint32_t e = t ^ ((bw >> K) & 0x01010101u);
+        const uint32_t nib = ((e * 0x01020408u) >> 24) & 0xFu;  // byte j -> bit j
+        if (q < nvalid) e64 |= static_cast<uint64_t>(nib) << (16 * q + 4 * w);
+      }
+    }
+    // exclusive XOR prefix: within the thread, then across the block
+    uint64_t inc = e64;
+    inc ^= inc << 1;
+    inc ^= inc << 2;
+    inc ^= inc << 4;
+    inc ^= inc << 8;
+    inc ^= inc << 16;
+    inc ^= inc << 32;
+    const uint32_t par = static_cast<uint32_t>(inc >> 63);
+    uint64_t exc = inc << 1;
+    const uint32_t bal = __ballot_sync(0xFFFFFFFFu, par);
+    uint32_t carry = __popc(bal & ((1u << lane) - 1u)) & 1u;
+    if (lane == 0) wpar[warp] = __popc(bal) & 1u;
+    __syncthreads();
+    uint32_t tot = 0;
+#pragma unroll
+    for (int w = 0; w < kFT / 32; ++w) {
+      if (w < warp) carry ^= wpar[w];
+      tot ^= wpar[w];
+    }
+    if (carry) exc = ~exc;
+    if (tid == 0) agg[blk] = static_cast<uint8_t>(tot);
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+#pragma unroll
+      for (int w = 0; w < 4; ++w) {
+        const uint32_t nib = static_cast<uint32_t>(exc >> (16 * q + 4 * w)) & 0xFu;
+        wd(s[q], w) |= ((nib * 0x00204081u) & 0x01010101u) << K;  // bit j -> byte j
+      }
+      sp[q] = s[q];
+    }
+    __syncthreads();  // wpar reuse
+  }
+}
+
+// entry bit K of every block of chain blockIdx.x: bit K of h0 ^ XOR of the
+// aggregates of the chain's earlier blocks.
+template <int K>
+__global__ void __launch_bounds__(1024) k_fnv_scan(const uint8_t* __restrict__ agg, uint8_t* __restrict__ entry,
+                                                   uint32_t bpc, uint64_t h0) {
+  __shared__ uint32_t wpar[32];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const uint64_t base = static_cast<uint64_t>(blockIdx.x) * bpc;
+  const uint32_t per = (bpc + blockDim.x - 1) / blockDim.x;
+  const uint32_t b0 = std::min<uint32_t>(bpc, tid * per), b1 = std::min<uint32_t>(bpc, b0 + per);
+  uint32_t par = 0;
+  for (uint32_t b = b0; b < b1; ++b) par ^= agg[base + b];
+  const uint32_t bal = __ballot_sync(0xFFFFFFFFu, par);
+  uint32_t pre = __popc(bal & ((1u << lane) - 1u)) & 1u;
+  if (lane == 0) wpar[warp] = __popc(bal) & 1u;
+  __syncthreads();
+  for (int w = 0; w < warp; ++w) pre ^= wpar[w];
+  pre ^= static_cast<uint32_t>(h0 >> K) & 1u;
+  for (uint32_t b = b0; b < b1; ++b) {
+    if (K == 0)
+      entry[base + b] = static_cast<uint8_t>(pre);
+    else
+      entry[base + b] |= static_cast<uint8_t>(pre << K);
+    pre ^= agg[base + b];
+  }
+}
+
+__global__ void k_fnv_init(uint64_t* out, int n_chains, uint64_t h0, uint64_t n) {
+  const int c = blockIdx.x * blockDim.x + threadIdx.x;
+  if (c < n_chains) out[c] = h0 * pow64(kFnvP, n);
+}
+
+// out[c] += sum over the chain's bytes of d_i * P^(N - i), d_i = (s_i ^ b_i) - s_i.
+__global__ void __launch_bounds__(kFT) k_fnv_final(const FnvJob j, const uint8_t* __restrict__ scratch,
+                                                   const uint8_t* __restrict__ entry,
+                                                   unsigned long long* __restrict__ out) {
+  __shared__ uint64_t pw[kFT];  // P^(64 t)
+  __shared__ uint64_t pblk;
+  __shared__ uint64_t wsum[kFT / 32];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  pw[tid] = pow64(kFnvP, static_cast<uint64_t>(kFPer) * tid);
+  __syncthreads();
+  for (uint32_t blk = blockIdx.x; blk < j.nblocks; blk += gridDim.x) {
+    const uint32_t c = blk / j.bpc, b = blk - c * j.bpc;
+    const uint64_t bstart = static_cast<uint64_t>(b) * kFB;
+    const uint64_t bend = bstart + kFB;
+    const uint64_t pos0 = bstart + static_cast<uint64_t>(tid) * kFPer;
+    if (tid == 0) pblk = bend <= j.n ? pow64(kFnvP, j.n - bend) : 0;
+    uint4 d[4];
+    const int nvalid = load_groups(j, c, pos0, d);
+    const uint4* sp = reinterpret_cast<const uint4*>(scratch + static_cast<uint64_t>(blk) * kFB + tid * kFPer);
+    const uint32_t rep = entry[blk] * 0x01010101u;
+    uint64_t acc = 0;
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      if (q < nvalid) {
+        uint4 s = sp[q];
+#pragma unroll
+        for (int w = 0; w < 4; ++w) {
+          const uint32_t sw = wd(s, w) ^ rep, xw = sw ^ wd(d[q], w);
+#pragma unroll
+          for (int by = 0; by < 4; ++by) {
+            const int64_t dd = static_cast<int64_t>((xw >> (8 * by)) & 0xFFu) -
+                               static_cast<int64_t>((sw >> (8 * by)) & 0xFFu);
+            acc = (acc + static_cast<uint64_t>(dd)) * kFnvP;
+          }
+        }
+      }
+    }
+    __syncthreads();  // pblk visible
+    uint64_t contrib = 0;
+    if (nvalid > 0) {
+      const uint64_t tend = pos0 + 16u * nvalid;
+      contrib = acc * (bend <= j.n ? pblk * pw[kFT - 1 - tid] : pow64(kFnvP, j.n - tend));
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) contrib += __shfl_xor_sync(0xFFFFFFFFu, contrib, o);
+    if (lane == 0) wsum[warp] = contrib;
+    __syncthreads();
+    if (tid == 0) {
+      uint64_t sum = 0;
+#pragma unroll
+      for (int w = 0; w < kFT / 32; ++w) sum += wsum[w];
+      atomicAdd(out + c, static_cast<unsigned long long>(sum));
+    }
+    __syncthreads();  // pblk / wsum reuse
+  }
+}
+
+template <int K>
+cudaError_t round_and_scan(const FnvJob& j, int grid, int n_chains, uint8_t* scratch, uint8_t* agg, uint8_t* entry,
+                           uint64_t h0, cudaStream_t st) {
+  k_fnv_round<K><<<grid, kFT, 0, st>>>(j, scratch, agg, entry);
+  k_fnv_scan<K><<<n_chains, 1024, 0, st>>>(agg, entry, j.bpc, h0);
+  return cudaGetLastError();
+}
+
+int g_sms = 0;
+std::mutex g_pool_mu;
+std::set<int> g_pool_tuned;
+
+}  // namespace
+
+extern "C" int gs_fnv1a64_device(const void* const* bufs, int n_chains, int k, uint64_t len, uint64_t h0,
+                                 uint64_t* d_out, void* stream) {
+  if (n_chains < 0 || k < 1 || k > kFCap || (n_chains > 0 && (!bufs || !d_out)))
+    return ffail(GS_INVALID_ARGUMENT, "fnv1a64_device: bad arguments");
+  if (len % 16) return ffail(GS_INVALID_ARGUMENT, "fnv1a64_device: buffer length must be a multiple of 16");
+  for (int i = 0; i < n_chains * k; ++i)
+    if (!bufs[i] || (reinterpret_cast<uintptr_t>(bufs[i]) & 15u))
+      return ffail(GS_INVALID_ARGUMENT, "fnv1a64_device: buffer %d is NULL or not 16-B aligned", i);
+  if (reinterpret_cast<uintptr_t>(d_out) & 7u)
+    return ffail(GS_INVALID_ARGUMENT, "fnv1a64_device: output must be 8-B aligned");
+  if (n_chains == 0) return GS_OK;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return ffail(GS_CUDA_ERROR, "fnv1a64_device: %s", cudaGetErrorString(e));
+  {
+    std::lock_guard<std::mutex> lk(g_pool_mu);
+    if (!g_sms) cudaDeviceGetAttribute(&g_sms, cudaDevAttrMultiProcessorCount, dev);
+    if (!g_pool_tuned.count(dev)) {  // keep the stream-ordered scratch mapped between calls
+      cudaMemPool_t pool;
+      if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+        uint64_t keep = ~0ull;
+        cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+      }
+      g_pool_tuned.insert(dev);
+    }
+  }
+  const uint64_t n = static_cast<uint64_t>(k) * len;
+  const uint64_t bpc64 = (n + kFB - 1) / kFB;
+  if (bpc64 > 0xFFFFFFFFull) return ffail(GS_INVALID_ARGUMENT, "fnv1a64_device: chain too long");
+  const uint32_t bpc = static_cast<uint32_t>(bpc64);
+  k_fnv_init<<<(n_chains + 255) / 256, 256, 0, st>>>(d_out, n_chains, h0, n);
+  if ((e = cudaGetLastError()) != cudaSuccess) return ffail(GS_CUDA_ERROR, "fnv init: %s", cudaGetErrorString(e));
+  if (n == 0) return GS_OK;
+  const uint64_t chain_scratch = bpc64 * kFB;
+  int per_job = static_cast<int>(std::max<uint64_t>(1, std::min<uint64_t>(kScratchBudget / chain_scratch, kFCap / k)));
+  per_job = std::min(per_job, n_chains);
+  const size_t scratch_bytes = static_cast<size_t>(per_job) * chain_scratch;
+  const size_t meta = static_cast<size_t>(per_job) * bpc;
+  uint8_t* mem = nullptr;
+  if ((e = cudaMallocAsync(reinterpret_cast<void**>(&mem), scratch_bytes + 2 * meta, st)) != cudaSuccess)
+    return ffail(GS_CUDA_ERROR, "fnv scratch (%zu bytes): %s", scratch_bytes + 2 * meta, cudaGetErrorString(e));
+  uint8_t* agg = mem + scratch_bytes;
+  uint8_t* entry = agg + meta;
+  int status = GS_OK;
+  for (int c0 = 0; c0 < n_chains && status == GS_OK; c0 += per_job) {
+    const int cnt = std::min(per_job, n_chains - c0);
+    FnvJob j{};
+    for (int i = 0; i < cnt * k; ++i) j.p[i] = static_cast<const uint8_t*>(bufs[static_cast<size_t>(c0) * k + i]);
+    j.k = k;
+    j.len = len;
+    j.n = n;
+    j.bpc = bpc;
+    j.nblocks = static_cast<uint32_t>(static_cast<uint64_t>(cnt) * bpc);
+    const int grid = static_cast<int>(std::min<uint64_t>(j.nblocks, static_cast<uint64_t>(g_sms > 0 ? g_sms : 148) * 4));
+    cudaError_t r = round_and_scan<0>(j, grid, cnt, mem, agg, entry, h0, st);
+    if (r == cudaSuccess) r = round_and_scan<1>(j, grid, cnt, mem, agg, entry, h0, st);
+    if (r == cudaSuccess) r = round_and_scan<2>(j, grid, cnt, mem, agg, entry, h0, st);
+    if (r == cudaSuccess) r = round_and_scan<3>(j, grid, cnt, mem, agg, entry, h0, st);
+    if (r == cudaSuccess) r = round_and_scan<4>(j, grid, cnt, mem, agg, entry, h0, st);
+    if (r == cudaSuccess) r = round_and_scan<5>(j, grid, cnt, mem, agg, entry, h0, st);
+    if (r == cudaSuccess) r = round_and_scan<6>(j, grid, cnt, mem, agg, entry, h0, st);
+    if (r == cudaSuccess) r = round_and_scan<7>(j, grid, cnt, mem, agg, entry, h0, st);
+    if (r == cudaSuccess) {
+      k_fnv_final<<<grid, kFT, 0, st>>>(j, mem, entry, reinterpret_cast<unsigned long long*>(d_out) + c0);
+      r = cudaGetLastError();
+    }
+    if (r != cudaSuccess) status = ffail(GS_CUDA_ERROR, "fnv kernels: %s", cudaGetErrorString(r));
+  }
+  cudaFreeAsync(mem, st);
+  return status;
+}
+
+// Upload chunks' host parity rows into HBM on `copy` and checksum them on
+// `compute` as they land (groups of kUpGroup chunks, one event per group), so
+// the hashing of group g overlaps the upload of group g + 1.
+extern "C" int gs_parity_upload_checksum(const void* const* h_parity, int n_chunks, int k, uint64_t len,
+                                         void* const* d_parity, uint64_t* d_sums, void* compute, void* copy) {
+  constexpr int kUpGroup = 4;
+  constexpr uint64_t kOffset = 0xcbf29ce484222325ull;
+  if (n_chunks < 0 || k < 1 || (n_chunks > 0 && (!h_parity || !d_parity || !d_sums)))
+    return ffail(GS_INVALID_ARGUMENT, "parity_upload_checksum: bad arguments");
+  cudaStream_t cs = static_cast<cudaStream_t>(compute), ys = static_cast<cudaStream_t>(copy);
+  for (int g0 = 0; g0 < n_chunks; g0 += kUpGroup) {
+    const int cnt = std::min(kUpGroup, n_chunks - g0);
+    for (int i = g0 * k; i < (g0 + cnt) * k; ++i) {
+      if (!h_parity[i] || !d_parity[i]) return ffail(GS_INVALID_ARGUMENT, "parity_upload_checksum: NULL row %d", i);
+      cudaError_t e = cudaMemcpyAsync(d_parity[i], h_parity[i], len, cudaMemcpyHostToDevice, ys);
+      if (e != cudaSuccess) return ffail(GS_CUDA_ERROR, "parity upload: %s", cudaGetErrorString(e));
+    }
+    cudaEvent_t ev;
+    cudaError_t e = cudaEventCreateWithFlags(&ev, cudaEventDisableTiming);
+    if (e == cudaSuccess) e = cudaEventRecord(ev, ys);
+    if (e == cudaSuccess) e = cudaStreamWaitEvent(cs, ev, 0);
+    cudaEventDestroy(ev);  // released once the recorded work completes
+    if (e != cudaSuccess) return ffail(GS_CUDA_ERROR, "parity upload event: %s", cudaGetErrorString(e));
+    if (int s = gs_fnv1a64_device(d_parity + static_cast<size_t>(g0) * k, cnt, k, len, kOffset, d_sums + g0, cs))
+      return s;
+  }
+  return GS_OK;
+}

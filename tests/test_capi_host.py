@@ -149,6 +149,16 @@ def test_slice_bytes_and_seal(golden, port):
                                         out) == 0
     for c in range(4):
         assert out[c] == port.parity_checksum(parity[3 * c: 3 * c + 3])
+    # lockstep groups of 4..8 chains per thread (chunk counts that are not a
+    # multiple of the group, one thread, more threads than chunks)
+    rng = np.random.default_rng(5)
+    for n_chunks, threads, ln in [(13, 2, 301), (9, 1, 64), (64, 14, 33), (7, 3, 1), (5, 16, 100)]:
+        parity = [rng.integers(0, 256, ln, dtype=np.uint8) for _ in range(2 * n_chunks)]
+        out = (C.c_uint64 * n_chunks)()
+        assert lib.gs_parity_checksum_batch(L.ptr_array([p.ctypes.data for p in parity]), n_chunks, 2, ln,
+                                            threads, out) == 0
+        for c in range(n_chunks):
+            assert out[c] == port.parity_checksum(parity[2 * c: 2 * c + 2]), (n_chunks, threads, c)
 
 
 def test_stripe_ranges_partition_exactly():

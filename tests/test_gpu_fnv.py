@@ -1,0 +1,103 @@
+"""GPU FNV-1a (gs_fnv1a64_device, gs_fnv_gpu.cu) against the oracle's serial
+FNV-1a (parity_store.hpp:19-25) and ParityChunk::compute_checksum
+(parity_store.hpp:46-50): bit-exact on random chains, chain lengths around
+the 16 KiB block and 64-byte thread boundaries, several buffers per chain,
+arbitrary seeds h0, the golden "foobar"-style KAT extended to 16-B multiples,
+and a full-size C3 chunk (2 x 80 MiB) against the reference checksum."""
+import ctypes as C
+
+import numpy as np
+import pytest
+
+from oracle import oracle as O
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+from paper_2605_00831_b200 import _lib as L  # noqa: E402
+
+OFFSET = 0xCBF29CE484222325
+
+
+@pytest.fixture(scope="module", autouse=True)
+def cuda0():
+    if not torch.cuda.is_available():
+        pytest.fail("GPU test collected without a CUDA device")
+    torch.cuda.set_device(0)
+    yield
+
+
+def device_fnv(bufs, n_chains, k, ln, h0=OFFSET):
+    out = torch.full((max(n_chains, 1),), 7, dtype=torch.int64, device="cuda")
+    st = torch.cuda.current_stream()
+    rc = L.lib().gs_fnv1a64_device(L.ptr_array([b.data_ptr() for b in bufs]), n_chains, k, ln, h0,
+                                   out.data_ptr(), st.cuda_stream)
+    assert rc == 0, L.lib().gs_last_error()
+    st.synchronize()
+    return [int(v) & (2**64 - 1) for v in out.cpu().tolist()[:n_chains]]
+
+
+@pytest.mark.parametrize("ln", [16, 48, 64, 1008, 16368, 16384, 16400, 32768 + 48, 3 * 16384 + 4096 + 16,
+                                262144, 1 << 20])
+@pytest.mark.parametrize("k", [1, 2, 3])
+def test_chains_match_serial_fnv(ln, k):
+    rng = np.random.default_rng(ln * 7 + k)
+    n_chains = 3
+    host = [rng.integers(0, 256, ln, dtype=np.uint8) for _ in range(n_chains * k)]
+    dev = [torch.from_numpy(h).cuda() for h in host]
+    got = device_fnv(dev, n_chains, k, ln)
+    port = O.port()
+    for c in range(n_chains):
+        assert got[c] == port.parity_checksum(host[c * k:(c + 1) * k]), (ln, k, c)
+
+
+def test_seeds_and_special_bytes():
+    port = O.port()
+    rng = np.random.default_rng(3)
+    for h0 in [0, 1, 0xFF, 0x100, OFFSET, 2**64 - 1, int(rng.integers(0, 2**63)) * 2 + 1]:
+        for fill in [None, 0, 0xFF, 0x80]:
+            ln = 16384 * 2 + 32
+            h = rng.integers(0, 256, ln, dtype=np.uint8) if fill is None else np.full(ln, fill, np.uint8)
+            got = device_fnv([torch.from_numpy(h).cuda()], 1, 1, ln, h0)
+            assert got[0] == port.fnv1a64(h, h0), (h0, fill)
+
+
+def test_many_chains_and_jobs():
+    """More chains than one job's pointer table (480 / k) and zero-length
+    chains (hash = h0)."""
+    port = O.port()
+    rng = np.random.default_rng(11)
+    k, ln, n_chains = 2, 4096, 300
+    host = [rng.integers(0, 256, ln, dtype=np.uint8) for _ in range(n_chains * k)]
+    flat = torch.from_numpy(np.concatenate(host)).cuda()
+    dev = [flat[i * ln:(i + 1) * ln] for i in range(n_chains * k)]
+    got = device_fnv(dev, n_chains, k, ln)
+    for c in range(0, n_chains, 37):
+        assert got[c] == port.parity_checksum(host[c * k:(c + 1) * k]), c
+    assert got[-1] == port.parity_checksum(host[-k:])
+    z = torch.zeros(16, dtype=torch.uint8, device="cuda")
+    assert device_fnv([z, z], 2, 1, 0, 12345) == [12345, 12345]
+
+
+def test_rejects_bad_arguments():
+    lib = L.lib()
+    x = torch.zeros(64, dtype=torch.uint8, device="cuda")
+    out = torch.zeros(1, dtype=torch.int64, device="cuda")
+    assert lib.gs_fnv1a64_device(L.ptr_array([x.data_ptr()]), 1, 1, 17, OFFSET, out.data_ptr(), None) == \
+        L.GS_INVALID_ARGUMENT
+    assert lib.gs_fnv1a64_device(L.ptr_array([x.data_ptr() + 1]), 1, 1, 16, OFFSET, out.data_ptr(), None) == \
+        L.GS_INVALID_ARGUMENT
+    assert lib.gs_fnv1a64_device(L.ptr_array([None]), 1, 1, 16, OFFSET, out.data_ptr(), None) == \
+        L.GS_INVALID_ARGUMENT
+
+
+def test_full_size_c3_chunk_checksum():
+    """One C3 chunk's parity (RS(8,2), 2 x 83,886,080 B) sealed on the GPU
+    equals the host seal (the reference's compute_checksum)."""
+    ln = 83886080
+    g = torch.Generator(device="cuda").manual_seed(5)
+    par = torch.randint(0, 256, (2, ln), dtype=torch.uint8, device="cuda", generator=g)
+    got = device_fnv([par[0], par[1]], 1, 2, ln)
+    hp = par.cpu().numpy()
+    want = L.lib().gs_parity_checksum(L.ptr_array([hp[0].ctypes.data, hp[1].ctypes.data]), 2, ln)
+    assert got[0] == want
