@@ -296,6 +296,12 @@ int gs_fnv1a64_device(const void* const* bufs, int n_chains, int k, uint64_t len
  * off the host; the uploaded rows then feed K2 directly). */
 int gs_parity_upload_checksum(const void* const* h_parity, int n_chunks, int k, uint64_t len,
                               void* const* d_parity, uint64_t* d_sums, void* compute, void* copy);
+/* The checkpoint-side mirror: K1's parity rows in HBM (written on `compute`)
+ * are copied to pinned host rows on `copy` while the GPU computes their chunk
+ * checksums; h_sums[c] (pinned) receives them behind the rows. Pair with
+ * gs_store_commit_sealed_batch on `copy`. */
+int gs_parity_offload_sealed(const void* const* d_parity, int n_chunks, int k, uint64_t len,
+                             void* const* h_parity, uint64_t* h_sums, void* compute, void* copy);
 
 /* ---- host tier: ParityStore on pinned slabs (parity_store.hpp:31-263) ----
  * Entries are keyed (request, chunk). Reserve -> the D2H of K1 writes the k
@@ -320,6 +326,12 @@ int gs_store_reserve_batch(gs_store* s, int count, const uint64_t* request_ids, 
                            void** parity_out);
 int gs_store_commit_batch(gs_store* s, int count, const uint64_t* request_ids, const uint32_t* chunks,
                           void* stream);
+/* Commit entries whose checksums were computed on the GPU (gs_parity_offload_
+ * sealed): once `stream` reaches this point the entries are sealed with
+ * checksums[i] (pinned host memory, read at that time; keep it alive until
+ * then) -- no host FNV pass. */
+int gs_store_commit_sealed_batch(gs_store* s, int count, const uint64_t* request_ids, const uint32_t* chunks,
+                                 const uint64_t* checksums, void* stream);
 int gs_store_wait_sealed(gs_store* s);
 /* Copying put (reference try_put): sealed != 0 keeps `checksum` as given. */
 int gs_store_put(gs_store* s, uint64_t request_id, uint32_t chunk, int kind, int n, int k,

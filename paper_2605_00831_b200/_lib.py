@@ -73,12 +73,14 @@ SIGNATURES = {
     "gs_parity_checksum_batch": (_i, [_vpp, _i, _i, _sz, _i, _u64p]),
     "gs_fnv1a64_device": (_i, [_vpp, _i, _i, _u64, _u64, _vp, _vp]),
     "gs_parity_upload_checksum": (_i, [_vpp, _i, _i, _u64, _vpp, _vp, _vp, _vp]),
+    "gs_parity_offload_sealed": (_i, [_vpp, _i, _i, _u64, _vpp, _vp, _vp, _vp]),
     "gs_store_create": (_i, [_u64, _i, _vpp]),
     "gs_store_destroy": (_i, [_vp]),
     "gs_store_reserve": (_i, [_vp, _u64, _u32, _i, _i, _i, _u32, _u64, _ip, _vpp]),
     "gs_store_commit": (_i, [_vp, _u64, _u32, _vp]),
     "gs_store_reserve_batch": (_i, [_vp, _i, _u64p, C.POINTER(C.c_uint32), _i, _i, _i, _u32, _u64, _ip, _vpp]),
     "gs_store_commit_batch": (_i, [_vp, _i, _u64p, C.POINTER(C.c_uint32), _vp]),
+    "gs_store_commit_sealed_batch": (_i, [_vp, _i, _u64p, C.POINTER(C.c_uint32), _vp, _vp]),
     "gs_store_wait_sealed": (_i, [_vp]),
     "gs_store_put": (_i, [_vp, _u64, _u32, _i, _i, _i, _u32, _u64, _vpp, _u64, _i, _ip]),
     "gs_store_get": (_i, [_vp, _u64, _u32, _i, _ip, _vpp, _u64p, C.POINTER(C.c_uint32), _u64p, _ip]),

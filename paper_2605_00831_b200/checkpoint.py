@@ -292,6 +292,14 @@ class Checkpointer:
         self.host_fnv_rate = 1.6e9 * max(1, (os.cpu_count() or 1) - 2)
         # False: verify every entry on host threads (the reference's placement)
         self.gpu_verify = True
+        # Where checkpoint_batch seals parity (ParityChunk::seal): "host" = FNV
+        # on the store's host threads after the D2H (the reference's order);
+        # "device" = K1 into HBM, checksum on the GPU, D2H of rows + checksum;
+        # "auto" = device when one chunk's parity is >= 16 MiB, where a serial
+        # host FNV chain (~1 GB/s) would trail the host link by > 15 ms.
+        self.seal = "auto"
+        self.seal_inflight_bytes = 2 << 30   # device parity buffers awaiting their D2H
+        self._inflight: List[tuple] = []      # (event on copy, keep-alive tensors, bytes)
 
     def close(self) -> None:
         self.pipe.close()
@@ -300,6 +308,7 @@ class Checkpointer:
         self.copy.synchronize()
         self.compute.synchronize()
         self.store.wait_sealed()
+        self._inflight.clear()
 
     # checkpoint.hpp:123-149 (+ the try_put of :207)
     def checkpoint_chunk(self, slices: Sequence[KvChunkSlice], state: AssignmentState) -> ChunkCheckpointOutcome:
@@ -332,7 +341,9 @@ class Checkpointer:
             slots.extend(s.bytes.data_ptr() for s in slices)
             dsts.extend(ptrs)
             keys.append((s0.request_id, s0.chunk_id))
-        if keys:
+        if keys and self._device_seal():
+            self._checkpoint_device_sealed(keys, slots, dsts)
+        elif keys:
             self.compute.wait_stream(torch.cuda.current_stream(self.dev))
             check(L.lib().gs_encode_offload(self.pipe.handle, encoder(sch).handle, len(keys), L.ptr_array(slots),
                                             L.ptr_array(dsts), self.slice, self.compute.cuda_stream,
@@ -351,6 +362,40 @@ class Checkpointer:
                 for w in range(self.cfg.scheme.n)]
 
     # checkpoint.hpp:179-222
+    def _device_seal(self) -> bool:
+        if self.seal == "device":
+            return True
+        if self.seal == "auto":
+            return self.slice % 16 == 0 and self.cfg.scheme.k * self.slice >= (16 << 20)
+        return False
+
+    def _checkpoint_device_sealed(self, keys, slots, dsts) -> None:
+        """K1 over the batch into HBM, the chunks' checksums on the GPU
+        (gs_parity_offload_sealed), D2H of the rows and the checksums into the
+        reserved store entries, sealed by one host callback with no FNV pass.
+        At most seal_inflight_bytes of device parity await their D2H."""
+        sch = self.cfg.scheme
+        S, k = len(keys), sch.k
+        need = S * k * self.slice
+        self._inflight = [f for f in self._inflight if not f[0].query()]
+        while self._inflight and sum(f[2] for f in self._inflight) + need > self.seal_inflight_bytes:
+            self._inflight.pop(0)[0].synchronize()
+        cur = torch.cuda.current_stream(self.dev)
+        self.compute.wait_stream(cur)
+        self.copy.wait_stream(cur)
+        par = torch.empty((S, k, self.slice), dtype=torch.uint8, device=self.dev)
+        sums = torch.empty(S, dtype=torch.int64).pin_memory()
+        rows = L.ptr_array([par[s, i].data_ptr() for s in range(S) for i in range(k)])
+        lib = L.lib()
+        check(lib.gs_apply_device(encoder(sch).handle, S, L.ptr_array(slots), rows, self.slice,
+                                  self.compute.cuda_stream), "checkpoint")
+        check(lib.gs_parity_offload_sealed(rows, S, k, self.slice, L.ptr_array(dsts), sums.data_ptr(),
+                                           self.compute.cuda_stream, self.copy.cuda_stream), "checkpoint seal")
+        self.store.commit_sealed_batch(keys, sums.data_ptr(), self.copy)
+        done = torch.cuda.Event()
+        done.record(self.copy)
+        self._inflight.append((done, (par, sums), need))
+
     def run_prefill_with_checkpointing(self, request_id: int, input_tokens: int, kv_seed: int = 0,
                                        keep_ground_truth: bool = True) -> PrefillRunResult:
         cfg = self.cfg

@@ -381,3 +381,49 @@ extern "C" int gs_parity_upload_checksum(const void* const* h_parity, int n_chun
   }
   return GS_OK;
 }
+
+// K1's parity rows already in HBM (d_parity, written on `compute` before this
+// call) -> pinned host rows on `copy`, and their chunk checksums computed on
+// the GPU (`compute`) and copied to h_sums (pinned) behind them: the seal of
+// ParityChunk (parity_store.hpp:46-53) without a host FNV pass. Stream order:
+// rows D2H after K1; sums D2H after the FNV; a store commit enqueued on `copy`
+// after this call sees both.
+extern "C" int gs_parity_offload_sealed(const void* const* d_parity, int n_chunks, int k, uint64_t len,
+                                        void* const* h_parity, uint64_t* h_sums, void* compute, void* copy) {
+  constexpr uint64_t kOffset = 0xcbf29ce484222325ull;
+  if (n_chunks < 0 || k < 1 || (n_chunks > 0 && (!d_parity || !h_parity || !h_sums)))
+    return ffail(GS_INVALID_ARGUMENT, "parity_offload_sealed: bad arguments");
+  if (n_chunks == 0) return GS_OK;
+  cudaStream_t cs = static_cast<cudaStream_t>(compute), ys = static_cast<cudaStream_t>(copy);
+  cudaEvent_t ev;
+  cudaError_t e = cudaEventCreateWithFlags(&ev, cudaEventDisableTiming);
+  if (e == cudaSuccess) e = cudaEventRecord(ev, cs);  // K1 done
+  if (e == cudaSuccess) e = cudaStreamWaitEvent(ys, ev, 0);
+  for (int i = 0; e == cudaSuccess && i < n_chunks * k; ++i) {
+    if (!d_parity[i] || !h_parity[i]) {
+      cudaEventDestroy(ev);
+      return ffail(GS_INVALID_ARGUMENT, "parity_offload_sealed: NULL row %d", i);
+    }
+    e = cudaMemcpyAsync(h_parity[i], d_parity[i], len, cudaMemcpyDeviceToHost, ys);
+  }
+  if (e != cudaSuccess) {
+    cudaEventDestroy(ev);
+    return ffail(GS_CUDA_ERROR, "parity offload: %s", cudaGetErrorString(e));
+  }
+  uint64_t* d_sums = nullptr;
+  e = cudaMallocAsync(reinterpret_cast<void**>(&d_sums), sizeof(uint64_t) * n_chunks, cs);
+  if (e != cudaSuccess) {
+    cudaEventDestroy(ev);
+    return ffail(GS_CUDA_ERROR, "parity offload sums: %s", cudaGetErrorString(e));
+  }
+  int st = gs_fnv1a64_device(d_parity, n_chunks, k, len, kOffset, d_sums, cs);
+  if (st == GS_OK) {
+    e = cudaEventRecord(ev, cs);  // checksums done
+    if (e == cudaSuccess) e = cudaStreamWaitEvent(ys, ev, 0);
+    if (e == cudaSuccess) e = cudaMemcpyAsync(h_sums, d_sums, sizeof(uint64_t) * n_chunks, cudaMemcpyDeviceToHost, ys);
+    if (e != cudaSuccess) st = ffail(GS_CUDA_ERROR, "parity offload sums: %s", cudaGetErrorString(e));
+  }
+  cudaFreeAsync(d_sums, ys);
+  cudaEventDestroy(ev);
+  return st;
+}

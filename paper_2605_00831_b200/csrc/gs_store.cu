@@ -190,9 +190,26 @@ struct gs_store {
   struct HostJob {
     gs_store* s;
     std::vector<Key> keys;
+    const uint64_t* sums = nullptr;  // checksums already computed (GPU seal), read at callback time
   };
   static void CUDART_CB on_stream(void* p) {
     auto* j = static_cast<HostJob*>(p);
+    if (j->sums) {  // sealed on the device: record the checksums, no host FNV
+      {
+        std::lock_guard<std::mutex> lk(j->s->mu);
+        for (size_t i = 0; i < j->keys.size(); ++i) {
+          auto it = j->s->entries.find(j->keys[i]);
+          if (it != j->s->entries.end()) {
+            it->second.checksum = j->sums[i];
+            it->second.sealed = true;
+          }
+        }
+        j->s->pending -= static_cast<uint64_t>(j->keys.size());
+      }
+      j->s->sealed_cv.notify_all();
+      delete j;
+      return;
+    }
     {
       std::lock_guard<std::mutex> lk(j->s->mu);
       for (const auto& k : j->keys) j->s->jobs.push_back(k);
@@ -269,12 +286,12 @@ int gs_store_reserve(gs_store* s, uint64_t request_id, uint32_t chunk, int kind,
   return GS_OK;
 }
 
-int gs_store_commit_batch(gs_store* s, int count, const uint64_t* request_ids, const uint32_t* chunks,
-                          void* stream) {
+static int commit_batch(gs_store* s, int count, const uint64_t* request_ids, const uint32_t* chunks,
+                        const uint64_t* sums, void* stream) {
   if (!s || count < 0 || (count > 0 && (!request_ids || !chunks)))
     return sfail(GS_INVALID_ARGUMENT, "store_commit: bad arguments");
   if (count == 0) return GS_OK;
-  auto* job = new gs_store::HostJob{s, {}};
+  auto* job = new gs_store::HostJob{s, {}, sums};
   job->keys.reserve(static_cast<size_t>(count));
   {
     std::lock_guard<std::mutex> lk(s->mu);
@@ -299,6 +316,17 @@ int gs_store_commit_batch(gs_store* s, int count, const uint64_t* request_ids, c
   }
   gs_store::on_stream(job);
   return GS_OK;
+}
+
+int gs_store_commit_batch(gs_store* s, int count, const uint64_t* request_ids, const uint32_t* chunks,
+                          void* stream) {
+  return commit_batch(s, count, request_ids, chunks, nullptr, stream);
+}
+
+int gs_store_commit_sealed_batch(gs_store* s, int count, const uint64_t* request_ids, const uint32_t* chunks,
+                                 const uint64_t* checksums, void* stream) {
+  if (count > 0 && !checksums) return sfail(GS_INVALID_ARGUMENT, "store_commit_sealed: NULL checksums");
+  return commit_batch(s, count, request_ids, chunks, checksums, stream);
 }
 
 int gs_store_commit(gs_store* s, uint64_t request_id, uint32_t chunk, void* stream) {

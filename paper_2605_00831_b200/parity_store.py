@@ -171,6 +171,15 @@ class ParityStore:
         st = None if stream is None else int(getattr(stream, "cuda_stream", stream))
         check(L.lib().gs_store_commit_batch(self.handle, n, req, chk, st), "parity store")
 
+    def commit_sealed_batch(self, keys, checksums_ptr: int, stream=None) -> None:
+        """Seal entries with checksums computed on the GPU (pinned uint64
+        array at `checksums_ptr`, read when `stream` reaches this point)."""
+        n = len(keys)
+        req = (C.c_uint64 * max(n, 1))(*[r for r, _ in keys])
+        chk = (C.c_uint32 * max(n, 1))(*[c for _, c in keys])
+        st = None if stream is None else int(getattr(stream, "cuda_stream", stream))
+        check(L.lib().gs_store_commit_sealed_batch(self.handle, n, req, chk, checksums_ptr, st), "parity store")
+
     def commit(self, request_id: int, chunk_id: int, stream=None) -> None:
         """Seal once `stream` (the copy stream of the D2H) reaches this point."""
         st = None if stream is None else int(getattr(stream, "cuda_stream", stream))

@@ -101,8 +101,14 @@ def _ck(n, k, tp, chunk=16, capacity=None, layers=2, heads=8, dim=8, restart=1e-
 
 
 @pytest.mark.gpu
-def test_prefill_stored_parity_equals_encode_of_ground_truth():
+@pytest.mark.parametrize("seal", ["host", "device"])
+def test_prefill_stored_parity_equals_encode_of_ground_truth(seal):
+    """Stored parity == encode of the ground truth and the seal == the
+    reference checksum (checkpoint_test.cpp:207-219), with the seal computed
+    by the store's host threads or by the GPU (gs_parity_offload_sealed)."""
     ck, store, torch = _ck(4, 2, 4)
+    ck.seal = seal
+    ck.seal_inflight_bytes = 1   # device seal: every batch waits for the previous D2H (bound exercised)
     run = ck.run_prefill_with_checkpointing(11, 3 * 16 + 5, kv_seed=13)
     ck.synchronize()
     assert run.completed and run.chunks_done == 4
@@ -118,6 +124,25 @@ def test_prefill_stored_parity_equals_encode_of_ground_truth():
             assert np.array_equal(entry.parity[i], want[i]), (c, i)
         assert entry.checksum == port.parity_checksum(want)
     assert [s.worker for s in run.ground_truth[0]] == [0, 1, 2, 3]
+    store.corrupt_entry(11, 1)   # a GPU-computed seal still catches host-tier corruption
+    assert int(store.get(11, 1)[0]) != 0 and int(store.get(11, 2)[0]) == 0
+
+
+@pytest.mark.gpu
+def test_large_chunks_seal_on_device_and_recover():
+    """auto seal policy: >= 16 MiB of parity per chunk is sealed on the GPU;
+    the host re-verification (get) and a recovery from those entries agree."""
+    ck, store, torch = _ck(8, 2, 8, chunk=2048, layers=32, heads=8, dim=128)   # 32 MiB slices
+    assert ck._device_seal()
+    run = ck.run_prefill_with_checkpointing(21, 4 * 2048, kv_seed=8)
+    ck.synchronize()
+    assert run.completed and run.chunks_done == 4
+    for c in range(4):
+        st, e = store.get(21, c, verify=True)
+        assert int(st) == 0 and e.checksum == O.port().parity_checksum(e.parity)
+    ck.cfg.cost.restart_overhead = 1e9
+    res = ck.recover(21, FailureEvent([2], at_chunk=4), run.ground_truth, [2048] * 4)
+    assert res.verified and len(res.plan.reconstruct_ids) == 4
 
 
 @pytest.mark.gpu
