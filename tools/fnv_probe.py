@@ -21,10 +21,16 @@ OFFSET = 0xCBF29CE484222325
 
 
 def main():
+    import argparse
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--configs", default="C2,C3")
+    want = ap.parse_args().configs.split(",")
     lib = L.lib()
     st = torch.cuda.Stream()
     res = []
     for name, chunks, ln, reps in [("C2", 32, 262144, 20), ("C3", 64, 83886080, 5)]:
+        if name not in want:
+            continue
         par = torch.randint(0, 256, (chunks, 2, ln), dtype=torch.uint8, device="cuda")
         ptrs = L.ptr_array([par[c, i].data_ptr() for c in range(chunks) for i in range(2)])
         out = torch.zeros(chunks, dtype=torch.int64, device="cuda")
