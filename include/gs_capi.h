@@ -52,6 +52,7 @@ typedef enum { GS_XOR = 0, GS_RDP = 1, GS_RS = 2 } gs_code_kind;
 typedef struct gs_codec gs_codec;       /* immutable coefficient plan + kernel choice */
 typedef struct gs_pipeline gs_pipeline; /* per-device staging ring + events for host-link overlap */
 typedef struct gs_store gs_store;       /* host tier: ParityStore on pinned slabs */
+typedef struct gs_verify gs_verify;     /* an in-flight split parity verification (recovery) */
 
 /* ---- diagnostics ------------------------------------------------------- */
 const char* gs_status_string(int status);
@@ -302,6 +303,17 @@ int gs_parity_upload_checksum(const void* const* h_parity, int n_chunks, int k, 
  * gs_store_commit_sealed_batch on `copy`. */
 int gs_parity_offload_sealed(const void* const* d_parity, int n_chunks, int k, uint64_t len,
                              void* const* h_parity, uint64_t* h_sums, void* compute, void* copy);
+/* Recovery's parity verification split between the GPU and host threads.
+ * enqueue: chunks [0, n_full) upload all k rows (h_parity[c*k+i] -> d_parity[c*k+i])
+ * and are checksummed on the GPU; chunks [n_full, n_chunks) upload only rows
+ * 0..u-1 (the rows the decode uses), the GPU hashes them and host threads
+ * continue the serial FNV chain over rows u..k-1 from the host copy. Uploads
+ * on `copy`, hashing on `compute`; rows not uploaded may be NULL in d_parity.
+ * finish: blocks, sums[c] = ParityChunk::compute_checksum of chunk c (bit-exact),
+ * frees the handle. */
+int gs_verify_enqueue(const void* const* h_parity, int n_chunks, int k, uint64_t len, int n_full, int u,
+                      void* const* d_parity, void* compute, void* copy, gs_verify** out);
+int gs_verify_finish(gs_verify* v, int threads, uint64_t* sums);
 
 /* ---- host tier: ParityStore on pinned slabs (parity_store.hpp:31-263) ----
  * Entries are keyed (request, chunk). Reserve -> the D2H of K1 writes the k

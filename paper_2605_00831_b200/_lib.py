@@ -74,6 +74,8 @@ SIGNATURES = {
     "gs_fnv1a64_device": (_i, [_vpp, _i, _i, _u64, _u64, _vp, _vp]),
     "gs_parity_upload_checksum": (_i, [_vpp, _i, _i, _u64, _vpp, _vp, _vp, _vp]),
     "gs_parity_offload_sealed": (_i, [_vpp, _i, _i, _u64, _vpp, _vp, _vp, _vp]),
+    "gs_verify_enqueue": (_i, [_vpp, _i, _i, _u64, _i, _i, _vpp, _vp, _vp, _vpp]),
+    "gs_verify_finish": (_i, [_vp, _i, _u64p]),
     "gs_store_create": (_i, [_u64, _i, _vpp]),
     "gs_store_destroy": (_i, [_vp]),
     "gs_store_reserve": (_i, [_vp, _u64, _u32, _i, _i, _i, _u32, _u64, _ip, _vpp]),

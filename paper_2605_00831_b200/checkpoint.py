@@ -237,6 +237,32 @@ def verify_recovery(recovered, ground_truth) -> bool:
     return recovered.numel() == ground_truth.numel() and bool(torch.equal(recovered, ground_truth))
 
 
+class _VerifyFinish:
+    """gs_verify_finish on a Python thread (the C call drops the GIL): host
+    threads continue the split entries' FNV chains as the GPU's chain states
+    arrive; result() -> (checksums, host ms)."""
+
+    def __init__(self, handle, n: int, threads: int):
+        import threading
+        self._out = (C.c_uint64 * max(n, 1))()
+        self._n = n
+        self._rc = 0
+        self._ms = 0.0
+
+        def run():
+            t0 = time.perf_counter()
+            self._rc = L.lib().gs_verify_finish(handle, threads, self._out)
+            self._ms = (time.perf_counter() - t0) * 1e3
+
+        self._t = threading.Thread(target=run, daemon=True)
+        self._t.start()
+
+    def result(self):
+        self._t.join()
+        check(self._rc, "recover verify")
+        return [int(self._out[i]) for i in range(self._n)], self._ms
+
+
 class _HostVerify:
     """FNV verification of parity entries on host threads, run from a Python
     thread (the C call releases the GIL) so it overlaps the enqueue of the
@@ -290,6 +316,7 @@ class Checkpointer:
         # per hardware thread while the parity upload streams over the same
         # host memory (measured on the B200 hosts, bench recovery.c3_orchestrated).
         self.host_fnv_rate = 1.6e9 * max(1, (os.cpu_count() or 1) - 2)
+        self.host_chain_rate = 0.9e9   # ONE serial FNV chain on one host thread (bytes/s)
         # False: verify every entry on host threads (the reference's placement)
         self.gpu_verify = True
         # Where checkpoint_batch seals parity (ParityChunk::seal): "host" = FNV
@@ -468,13 +495,16 @@ class Checkpointer:
         B200 schedule of the same decisions: the decode of all n-r chunks is
         enqueued speculatively while their parity is verified, and a failed
         verification discards it and falls back exactly as the planning pass
-        would. The verification is split (_gpu_verify_count) so the host link
-        and the host cores finish together: g entries upload ALL their parity
-        rows and are checksummed in HBM as they land (gs_parity_upload_checksum,
-        the bit-sliced GPU FNV-1a), then K2 reads the uploaded rows; the other
-        n-r-g go through one gs_reconstruct_upload (H2D of only the used rows +
-        K2, pieces pipelined) while host threads run their serial FNV. Each
-        chunk's parity is verified once (the reference re-verifies inside
+        would. Verification (gpu_verify=True) is split so the host link and
+        the host cores finish together (_split_plan): n_full entries upload
+        ALL their parity rows and are checksummed in HBM by the bit-sliced GPU
+        FNV-1a; the others upload only the rows K2 uses, the GPU hashes those
+        and host threads continue the serial chain over the remaining rows
+        (gs_verify_enqueue / gs_verify_finish, finished on a Python thread).
+        K2 then reads the uploaded rows. gpu_verify=False keeps the
+        reference's placement: one gs_reconstruct_upload + FNV of every entry
+        on host threads. Each chunk's parity is verified once (the reference
+        re-verifies inside
         reconstruct_chunk; the store is not modified in between)."""
         cfg = self.cfg
         t_wall = time.perf_counter()
@@ -504,11 +534,11 @@ class Checkpointer:
         result.plan_ms = (time.perf_counter() - t_wall) * 1e3
         decode = parity_ok and not over and r < n and ground_truth is not None
         host_verify = None
-        if parity_ok and entries:
-            if decode and self.gpu_verify:
-                n_gpu = self._gpu_verify_count(len(entries), failed)
-            if entries[n_gpu:]:   # host threads verify the rest, overlapped with the enqueue and decode
-                host_verify = _HostVerify(self, entries[n_gpu:], verify_threads)
+        split = None            # (n_full, in-flight gs_verify finished on a host thread)
+        if parity_ok and entries and not (decode and self.gpu_verify):
+            # the reference's placement: every entry verified on host threads,
+            # overlapped with the enqueue and the decode
+            host_verify = _HostVerify(self, entries, verify_threads)
         if decode:
             if len(ground_truth) < n:
                 raise RuntimeError("recovery: ground truth missing for completed chunks")
@@ -519,13 +549,14 @@ class Checkpointer:
                 st.wait_stream(cur)
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             e0.record(self.compute)
-            if n_gpu:   # uploads of every parity row first: the GPU hashes them as they land
-                outs, oi, gpu_sums, par = self._enqueue_gpu_verified_decode(ground_truth, ids[:n_gpu],
-                                                                             entries[:n_gpu], failed)
-                pending.append((r, outs, oi, par))
-            if n_gpu < len(ids):
-                outs, oi = self._enqueue_batched_decode(ground_truth, ids[n_gpu:], entries[n_gpu:], failed)
-                pending.append((r + n_gpu, outs, oi, None))
+            if self.gpu_verify:
+                outs, oi, n_full, split_h, keep = self._enqueue_split_verified_decode(ground_truth, ids, entries,
+                                                                                     failed, verify_threads)
+                pending.append((r, outs, oi, keep))
+                split = (n_full, split_h)
+            else:
+                outs, oi = self._enqueue_batched_decode(ground_truth, ids, entries, failed)
+                pending.append((r, outs, oi, None))
             self.compute.wait_stream(self.verify)
             e1.record(self.compute)
             cur.wait_stream(self.compute)
@@ -533,10 +564,10 @@ class Checkpointer:
         if parity_ok and entries:
             if host_verify is not None:
                 parity_ok, result.verify_host_ms = host_verify.result()
-            if n_gpu:
-                sums = [int(v) & 0xFFFFFFFFFFFFFFFF for v in gpu_sums.cpu().tolist()]
-                parity_ok = parity_ok and all(sums[i] == entries[i].checksum for i in range(n_gpu))
-                result.verify_gpu_chunks = n_gpu
+            if split is not None:
+                sums, result.verify_host_ms = split[1].result()
+                parity_ok = all(sums[i] == e.checksum for i, e in enumerate(entries))
+                result.verify_gpu_chunks = split[0]
         if over or (not parity_ok and r < n):
             plan.mode, r = RecoveryMode.kFullRecomputeFallback, n
         elif r >= n:
@@ -588,22 +619,72 @@ class Checkpointer:
               "verify")
         return [int(out[i]) == e.checksum for i, e in enumerate(entries)]
 
-    def _gpu_verify_count(self, n: int, failed: Set[int]) -> int:
-        """How many of the n entries to verify on the GPU. A GPU-verified
-        entry uploads all k parity rows (the checksum chains over every row)
-        instead of the u rows the decode uses; a host-verified one costs k
-        rows of serial FNV on host threads. Pick g minimising
-        max(link time, host FNV time):  link = (n*u + g*(k-u)) L / B_link,
-        host = (n-g) k L / B_fnv."""
+    def _split_plan(self, n: int, failed: Set[int], threads: int):
+        """(n_full, u): how many of the n entries to verify entirely on the GPU
+        and how many parity rows the decode uses. A GPU-verified ("full")
+        entry uploads all k rows; a split entry uploads only the u rows K2
+        needs, the GPU hashes them and a host thread continues the serial
+        chain over the other k-u rows. n_full minimises
+        max(link time, host time) with
+          link = (n*u + n_full*(k-u)) L / B_link
+          host = max(h*u*L / B_link + (k-u) L / chain_rate, h (k-u) L / fnv_rate),
+        h = n - n_full (the last split chunk's rows land, then one serial chain)."""
         k = self.cfg.scheme.k
-        u = min(k, len(failed))
-        if self.slice % 16 or n == 0:
-            return 0
-        if u >= k:
-            return n   # no extra upload: verify everything on the GPU
-        bl, bf = self.cfg.cost.host_bw, self.host_fnv_rate
-        g = n * (k / bf - u / bl) / ((k - u) / bl + k / bf)
-        return max(0, min(n, int(math.ceil(g))))
+        u = max(1, min(k, len(failed)))
+        if u >= k or n == 0:
+            return n, u
+        L_, bl = float(self.slice), self.cfg.cost.host_bw
+        chain = (k - u) * L_ / self.host_chain_rate
+        best, best_t = n, float("inf")
+        for n_full in range(n + 1):
+            h = n - n_full
+            t_link = (n * u + n_full * (k - u)) * L_ / bl
+            t_host = 0.0 if h == 0 else max(h * u * L_ / bl + chain, h * (k - u) * L_ / self.host_fnv_rate)
+            t = max(t_link, t_host)
+            if t < best_t - 1e-9:
+                best, best_t = n_full, t
+        return best, u
+
+    def _enqueue_split_verified_decode(self, ground_truth, chunk_ids, entries, failed, threads: int):
+        """Upload parity rows into HBM and verify every entry's checksum
+        (gs_verify_enqueue: the first n_full entries entirely on the GPU, the
+        rest GPU-hashed over the decode's rows and finished on host threads in
+        a Python thread), then rebuild the lost shards with K2 from the
+        uploaded rows."""
+        sch = self.cfg.scheme
+        dec = decoder(sch, ErasurePattern(sorted(failed)))
+        S, k = len(chunk_ids), sch.k
+        threads = threads or max(1, (os.cpu_count() or 1) - 2)
+        n_full, u = self._split_plan(S, failed, threads) if self.slice % 16 == 0 else (0, k)
+        lib = L.lib()
+        full = torch.empty((n_full, k, self.slice), dtype=torch.uint8, device=self.dev)
+        part = torch.empty((S - n_full, u, self.slice), dtype=torch.uint8, device=self.dev)
+        drows: List[Optional[int]] = []
+        for s in range(S):
+            for i in range(k):
+                if s < n_full:
+                    drows.append(full[s, i].data_ptr())
+                else:
+                    drows.append(part[s - n_full, i].data_ptr() if i < u else None)
+        handle = C.c_void_p()
+        check(lib.gs_verify_enqueue(L.ptr_array([e.parity[i].ctypes.data for e in entries for i in range(k)]),
+                                    S, k, self.slice, n_full, u, L.ptr_array(drows), self.verify.cuda_stream,
+                                    self.copy.cuda_stream, C.byref(handle)), "recover verify")
+        finish = _VerifyFinish(handle, S, threads)
+        self.compute.wait_stream(self.copy)   # K2 needs the uploaded rows, not their checksums
+        outs = torch.empty((S, max(dec.n_out, 1), self.slice), dtype=torch.uint8, device=self.dev)
+        if dec.n_out:
+            slots: List[Optional[int]] = []
+            for s, c in enumerate(chunk_ids):
+                row = self._survivor_row(ground_truth[c], failed)
+                for i in range(k):
+                    row[sch.n + i] = drows[s * k + i]
+                slots.extend(row)
+            check(lib.gs_apply_device(dec.handle, S, L.ptr_array(slots),
+                                      L.ptr_array([outs[s, b].data_ptr() for s in range(S)
+                                                   for b in range(dec.n_out)]),
+                                      self.slice, self.compute.cuda_stream), "recover")
+        return outs, list(dec.out_index), n_full, finish, (full, part)
 
     def _survivor_row(self, gt, failed) -> List[Optional[int]]:
         sch = self.cfg.scheme
@@ -615,36 +696,6 @@ class Checkpointer:
             if j not in failed and row[j] is None:
                 raise InvalidArgument(f"coding: surviving shard {j} missing from input")
         return row
-
-    def _enqueue_gpu_verified_decode(self, ground_truth, chunk_ids, entries, failed):
-        """Upload every parity row of these entries into HBM (copy stream),
-        checksum them there as they land (gs_parity_upload_checksum, compute
-        stream) and rebuild the lost shards from the uploaded rows with K2."""
-        sch = self.cfg.scheme
-        dec = decoder(sch, ErasurePattern(sorted(failed)))
-        S, k = len(chunk_ids), sch.k
-        lib = L.lib()
-        par = torch.empty((S, k, self.slice), dtype=torch.uint8, device=self.dev)
-        sums = torch.empty(S, dtype=torch.int64, device=self.dev)
-        check(lib.gs_parity_upload_checksum(L.ptr_array([e.parity[i].ctypes.data for e in entries for i in range(k)]),
-                                            S, k, self.slice,
-                                            L.ptr_array([par[s, i].data_ptr() for s in range(S) for i in range(k)]),
-                                            sums.data_ptr(), self.verify.cuda_stream, self.copy.cuda_stream),
-              "recover verify")
-        self.compute.wait_stream(self.copy)   # K2 needs the uploaded rows, not their checksums
-        outs = torch.empty((S, max(dec.n_out, 1), self.slice), dtype=torch.uint8, device=self.dev)
-        if dec.n_out:
-            slots: List[Optional[int]] = []
-            for s, c in enumerate(chunk_ids):
-                row = self._survivor_row(ground_truth[c], failed)
-                for i in range(k):
-                    row[sch.n + i] = par[s, i].data_ptr()
-                slots.extend(row)
-            check(lib.gs_apply_device(dec.handle, S, L.ptr_array(slots),
-                                      L.ptr_array([outs[s, b].data_ptr() for s in range(S)
-                                                   for b in range(dec.n_out)]),
-                                      self.slice, self.compute.cuda_stream), "recover")
-        return outs, list(dec.out_index), sums, par
 
     def _enqueue_batched_decode(self, ground_truth, chunk_ids, entries, failed):
         """One gs_reconstruct_upload over the chunks: H2D of the used parity

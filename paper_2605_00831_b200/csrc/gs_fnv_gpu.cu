@@ -427,3 +427,181 @@ extern "C" int gs_parity_offload_sealed(const void* const* d_parity, int n_chunk
   cudaEventDestroy(ev);
   return st;
 }
+
+// ---------------------------------------------------------------------------
+// Recovery-side verification split between the GPU and host threads.
+//
+// Chunks [0, n_full) upload all k parity rows and are hashed entirely on the
+// GPU. Chunks [n_full, n) upload only their first u rows (the rows K2 uses);
+// the GPU hashes those rows, giving the chain state after row u-1, and host
+// threads continue the serial chain over rows u..k-1 from the host copy. A
+// host-verified chunk therefore costs one serial chain over (k-u) rows
+// instead of k, and its u rows cross the link once (for the decode AND the
+// hash). Host chunks go first on the copy stream so their threads start early.
+// ---------------------------------------------------------------------------
+#include <atomic>
+#include <thread>
+#include <vector>
+
+#include "gs_fnv.hpp"
+
+struct gs_verify {
+  int n = 0, n_full = 0, k = 0, u = 0;
+  uint64_t len = 0;
+  std::vector<const uint8_t*> host_rows;  // n * k
+  uint64_t* pinned = nullptr;             // [0, n): GPU sums (full) / chain states after row u-1 (split)
+  std::vector<cudaEvent_t> group_ev;      // per split group: its states are in `pinned`
+  std::vector<int> group_of;              // chunk -> group index (split chunks)
+  cudaEvent_t full_ev = nullptr;          // full chunks' sums are in `pinned`
+};
+
+namespace {
+constexpr int kSplitGroup = 4;  // chunks per GPU hash launch / host lockstep group
+}
+
+extern "C" int gs_verify_enqueue(const void* const* h_parity, int n_chunks, int k, uint64_t len, int n_full, int u,
+                                 void* const* d_parity, void* compute, void* copy, gs_verify** out) {
+  constexpr uint64_t kOffset = 0xcbf29ce484222325ull;
+  if (!out || n_chunks < 0 || k < 1 || u < 1 || u > k || n_full < 0 || n_full > n_chunks ||
+      (n_chunks > 0 && (!h_parity || !d_parity)))
+    return ffail(GS_INVALID_ARGUMENT, "verify_enqueue: bad arguments");
+  *out = nullptr;
+  cudaStream_t cs = static_cast<cudaStream_t>(compute), ys = static_cast<cudaStream_t>(copy);
+  auto* v = new gs_verify;
+  v->n = n_chunks;
+  v->n_full = n_full;
+  v->k = k;
+  v->u = u;
+  v->len = len;
+  v->host_rows.resize(static_cast<size_t>(n_chunks) * k);
+  for (size_t i = 0; i < v->host_rows.size(); ++i) v->host_rows[i] = static_cast<const uint8_t*>(h_parity[i]);
+  v->group_of.assign(n_chunks, -1);
+  auto bail = [&](int st) {
+    cudaStreamSynchronize(cs);  // nothing may still write `pinned`
+    for (auto e : v->group_ev) cudaEventDestroy(e);
+    if (v->full_ev) cudaEventDestroy(v->full_ev);
+    if (v->pinned) cudaFreeHost(v->pinned);
+    delete v;
+    return st;
+  };
+  cudaError_t e = cudaMallocHost(reinterpret_cast<void**>(&v->pinned), sizeof(uint64_t) * std::max(1, n_chunks));
+  uint64_t* d_state = nullptr;
+  if (e == cudaSuccess) e = cudaMallocAsync(reinterpret_cast<void**>(&d_state), sizeof(uint64_t) * std::max(1, n_chunks), cs);
+  if (e != cudaSuccess) return bail(ffail(GS_CUDA_ERROR, "verify_enqueue: %s", cudaGetErrorString(e)));
+  cudaEvent_t up;
+  if ((e = cudaEventCreateWithFlags(&up, cudaEventDisableTiming)) != cudaSuccess)
+    return bail(ffail(GS_CUDA_ERROR, "verify_enqueue: %s", cudaGetErrorString(e)));
+  auto upload_rows = [&](int c, int rows) -> cudaError_t {
+    for (int i = 0; i < rows; ++i) {
+      const size_t r = static_cast<size_t>(c) * k + i;
+      if (!h_parity[r] || !d_parity[r]) return cudaErrorInvalidValue;
+      cudaError_t x = cudaMemcpyAsync(d_parity[r], h_parity[r], len, cudaMemcpyHostToDevice, ys);
+      if (x != cudaSuccess) return x;
+    }
+    return cudaSuccess;
+  };
+  int st = GS_OK;
+  // split chunks first: rows 0..u-1, hashed per group, states D2H'd per group
+  for (int g0 = n_full; g0 < n_chunks && st == GS_OK; g0 += kSplitGroup) {
+    const int cnt = std::min(kSplitGroup, n_chunks - g0);
+    for (int c = g0; c < g0 + cnt && e == cudaSuccess; ++c) e = upload_rows(c, u);
+    if (e == cudaSuccess) e = cudaEventRecord(up, ys);
+    if (e == cudaSuccess) e = cudaStreamWaitEvent(cs, up, 0);
+    if (e != cudaSuccess) {
+      st = ffail(GS_CUDA_ERROR, "verify_enqueue upload: %s", cudaGetErrorString(e));
+      break;
+    }
+    std::vector<const void*> rows(static_cast<size_t>(cnt) * u);
+    for (int c = 0; c < cnt; ++c)
+      for (int i = 0; i < u; ++i) rows[static_cast<size_t>(c) * u + i] = d_parity[static_cast<size_t>(g0 + c) * k + i];
+    if ((st = gs_fnv1a64_device(rows.data(), cnt, u, len, kOffset, d_state + g0, cs)) != GS_OK) break;
+    cudaEvent_t ge;
+    e = cudaEventCreateWithFlags(&ge, cudaEventDisableTiming | cudaEventBlockingSync);
+    if (e == cudaSuccess) {
+      v->group_ev.push_back(ge);
+      e = cudaMemcpyAsync(v->pinned + g0, d_state + g0, sizeof(uint64_t) * cnt, cudaMemcpyDeviceToHost, cs);
+    }
+    if (e == cudaSuccess) e = cudaEventRecord(ge, cs);
+    if (e != cudaSuccess) st = ffail(GS_CUDA_ERROR, "verify_enqueue: %s", cudaGetErrorString(e));
+    for (int c = g0; c < g0 + cnt; ++c) v->group_of[c] = static_cast<int>(v->group_ev.size()) - 1;
+  }
+  // full chunks: every row, hashed on the GPU as groups land
+  for (int g0 = 0; g0 < n_full && st == GS_OK; g0 += kSplitGroup) {
+    const int cnt = std::min(kSplitGroup, n_full - g0);
+    for (int c = g0; c < g0 + cnt && e == cudaSuccess; ++c) e = upload_rows(c, k);
+    if (e == cudaSuccess) e = cudaEventRecord(up, ys);
+    if (e == cudaSuccess) e = cudaStreamWaitEvent(cs, up, 0);
+    if (e != cudaSuccess) {
+      st = ffail(GS_CUDA_ERROR, "verify_enqueue upload: %s", cudaGetErrorString(e));
+      break;
+    }
+    st = gs_fnv1a64_device(d_parity + static_cast<size_t>(g0) * k, cnt, k, len, kOffset, d_state + g0, cs);
+  }
+  if (st == GS_OK && n_full > 0) {
+    e = cudaEventCreateWithFlags(&v->full_ev, cudaEventDisableTiming | cudaEventBlockingSync);
+    if (e == cudaSuccess)
+      e = cudaMemcpyAsync(v->pinned, d_state, sizeof(uint64_t) * n_full, cudaMemcpyDeviceToHost, cs);
+    if (e == cudaSuccess) e = cudaEventRecord(v->full_ev, cs);
+    if (e != cudaSuccess) st = ffail(GS_CUDA_ERROR, "verify_enqueue: %s", cudaGetErrorString(e));
+  }
+  cudaEventDestroy(up);
+  cudaFreeAsync(d_state, cs);
+  if (st != GS_OK) return bail(st);
+  *out = v;
+  return GS_OK;
+}
+
+// Blocks: host threads continue the split chunks' chains over rows u..k-1 as
+// their GPU states arrive; sums[c] = chunk c's checksum. Frees `v`.
+extern "C" int gs_verify_finish(gs_verify* v, int threads, uint64_t* sums) {
+  if (!v) return ffail(GS_INVALID_ARGUMENT, "verify_finish: NULL handle");
+  int st = GS_OK;
+  if (v->n > 0 && !sums) st = ffail(GS_INVALID_ARGUMENT, "verify_finish: NULL output");
+  const int ns = v->n - v->n_full;
+  if (st == GS_OK && ns > 0) {
+    const int per = std::max(1, std::min(8, (ns + std::max(threads, 1) - 1) / std::max(threads, 1)));
+    const int groups = (ns + per - 1) / per;
+    std::atomic<int> next{0};
+    std::atomic<int> err{0};
+    auto work = [&] {
+      for (int g = next.fetch_add(1); g < groups; g = next.fetch_add(1)) {
+        const int c0 = v->n_full + g * per, m = std::min(per, v->n - c0);
+        for (int c = c0; c < c0 + m; ++c) {
+          const int ge = v->group_of[c];
+          if (ge < 0 || cudaEventSynchronize(v->group_ev[ge]) != cudaSuccess) err = 1;
+        }
+        if (err) return;
+        uint64_t h[8];
+        for (int q = 0; q < m; ++q) h[q] = v->pinned[c0 + q];
+        for (int i = v->u; i < v->k; ++i) {
+          const uint8_t* ps[8];
+          for (int q = 0; q < m; ++q) ps[q] = v->host_rows[static_cast<size_t>(c0 + q) * v->k + i];
+          gsb::fnv1a64_x8(ps, m, v->len, h);
+        }
+        for (int q = 0; q < m; ++q) sums[c0 + q] = h[q];
+      }
+    };
+    std::vector<std::thread> pool;
+    for (int t = 1; t < std::min(std::max(threads, 1), groups); ++t) pool.emplace_back(work);
+    work();
+    for (auto& t : pool) t.join();
+    if (err) st = ffail(GS_CUDA_ERROR, "verify_finish: GPU chain state unavailable");
+  }
+  if (st == GS_OK && v->n_full > 0) {
+    if (cudaEventSynchronize(v->full_ev) != cudaSuccess)
+      st = ffail(GS_CUDA_ERROR, "verify_finish: GPU checksums unavailable");
+    else
+      for (int c = 0; c < v->n_full; ++c) sums[c] = v->pinned[c];
+  }
+  for (auto e : v->group_ev) {  // every D2H into `pinned` has landed before it is freed
+    cudaEventSynchronize(e);
+    cudaEventDestroy(e);
+  }
+  if (v->full_ev) {
+    cudaEventSynchronize(v->full_ev);
+    cudaEventDestroy(v->full_ev);
+  }
+  cudaFreeHost(v->pinned);
+  delete v;
+  return st;
+}

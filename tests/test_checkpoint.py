@@ -199,12 +199,13 @@ def test_long_request_single_failure_rs82_bit_exact():
     res = ck.recover(6, FailureEvent([5], at_chunk=32), run.ground_truth, [2048] * 32)
     assert res.plan.mode == RecoveryMode.kHybrid and res.plan.recompute_chunks == 0
     assert res.verified and len(res.plan.reconstruct_ids) == 32
-    # verification split: some entries checksummed in HBM, the rest on host threads
+    # verification split: some entries checksummed entirely in HBM, the rest
+    # GPU-hashed over the decode's row and finished on host threads
     assert 0 < res.verify_gpu_chunks < 32
-    for gpu, rate, want in [(True, 1.0, 32), (False, None, 0)]:   # all on the GPU / all on the host
+    for gpu, rate, want in [(True, 1.0, 32), (True, 1e30, 0), (False, None, 0)]:
         ck.gpu_verify = gpu
         if rate:
-            ck.host_fnv_rate = rate
+            ck.host_fnv_rate = ck.host_chain_rate = rate
         res = ck.recover(6, FailureEvent([5], at_chunk=32), run.ground_truth, [2048] * 32)
         assert res.verified and res.verify_gpu_chunks == want and len(res.plan.reconstruct_ids) == 32
 
@@ -226,8 +227,8 @@ def test_bad_parity_and_over_tolerance_fallbacks():
     # and by the host threads alone
     for gpu, rate in [(True, 1.0), (True, 1e30), (False, None)]:
         ck.gpu_verify = gpu
-        if rate:
-            ck.host_fnv_rate = rate
+        if rate:   # 1.0: host FNV "slow" -> every entry on the GPU; 1e30: host "fast" -> all split
+            ck.host_fnv_rate = ck.host_chain_rate = rate
         res = ck.recover(3, FailureEvent([1], at_chunk=4), run.ground_truth, [16] * 4)
         assert res.plan.mode == RecoveryMode.kFullRecomputeFallback, (gpu, rate)
         assert res.verify_gpu_chunks == (4 if rate == 1.0 else 0)

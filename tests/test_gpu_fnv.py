@@ -101,3 +101,51 @@ def test_full_size_c3_chunk_checksum():
     hp = par.cpu().numpy()
     want = L.lib().gs_parity_checksum(L.ptr_array([hp[0].ctypes.data, hp[1].ctypes.data]), 2, ln)
     assert got[0] == want
+
+
+@pytest.mark.parametrize("n_full,u", [(0, 1), (2, 1), (5, 1), (1, 2), (0, 3)])
+def test_split_verification_matches_reference_checksum(n_full, u):
+    """gs_verify_enqueue / gs_verify_finish: entries verified entirely on the
+    GPU, or GPU-hashed over rows < u and finished by host threads over the
+    rest -- every checksum equals ParityChunk::compute_checksum; the uploaded
+    rows equal the host rows."""
+    port = O.port()
+    rng = np.random.default_rng(100 + 10 * n_full + u)
+    n, k, ln = 5, 3, 16384 * 3 + 48
+    host = [torch.from_numpy(rng.integers(0, 256, ln, dtype=np.uint8)).pin_memory() for _ in range(n * k)]
+    dev = torch.zeros((n, k, ln), dtype=torch.uint8, device="cuda")
+    drows = [dev[c, i].data_ptr() if (c < n_full or i < u) else None for c in range(n) for i in range(k)]
+    lib = L.lib()
+    comp, copy = torch.cuda.Stream(), torch.cuda.Stream()
+    torch.cuda.synchronize()   # dev zeroed before the side streams write it
+    h = C.c_void_p()
+    assert lib.gs_verify_enqueue(L.ptr_array([t.data_ptr() for t in host]), n, k, ln, n_full, u,
+                                 L.ptr_array(drows), comp.cuda_stream, copy.cuda_stream, C.byref(h)) == 0
+    out = (C.c_uint64 * n)()
+    assert lib.gs_verify_finish(h, 3, out) == 0, lib.gs_last_error()
+    torch.cuda.synchronize()
+    for c in range(n):
+        rows = [host[c * k + i].numpy() for i in range(k)]
+        assert out[c] == port.parity_checksum(rows), (c, n_full, u)
+        for i in range(k):
+            if c < n_full or i < u:
+                assert torch.equal(dev[c, i].cpu(), host[c * k + i])
+
+
+def test_upload_checksum_entry_point():
+    """gs_parity_upload_checksum: rows land in HBM and every chunk's checksum
+    equals the reference's."""
+    port = O.port()
+    rng = np.random.default_rng(77)
+    n, k, ln = 6, 2, 16384 + 32
+    host = [torch.from_numpy(rng.integers(0, 256, ln, dtype=np.uint8)).pin_memory() for _ in range(n * k)]
+    dev = torch.zeros((n, k, ln), dtype=torch.uint8, device="cuda")
+    sums = torch.zeros(n, dtype=torch.int64, device="cuda")
+    st = torch.cuda.current_stream()
+    assert L.lib().gs_parity_upload_checksum(L.ptr_array([t.data_ptr() for t in host]), n, k, ln,
+                                             L.ptr_array([dev[c, i].data_ptr() for c in range(n) for i in range(k)]),
+                                             sums.data_ptr(), st.cuda_stream, st.cuda_stream) == 0
+    st.synchronize()
+    got = [int(v) & (2**64 - 1) for v in sums.cpu().tolist()]
+    for c in range(n):
+        assert got[c] == port.parity_checksum([host[c * k + i].numpy() for i in range(k)])
