@@ -742,6 +742,65 @@ def host_tier_checkpoint(torch, dev, ring, scheme, pipe, comp, copy, args):
            "entries": store.entry_count(), "get_verified_ok": ok,
            "note": "FNV-1a seal is serial per chunk (reference checksum); the GPU path is not waiting on it"}
     store.close()
+    out["device_seal"] = host_tier_device_sealed(torch, dev, ring, scheme, comp, copy, blocks, slots, threads)
+    return out
+
+
+def host_tier_device_sealed(torch, dev, ring, scheme, comp, copy, blocks, slots, threads):
+    """The same sealed C2 block checkpoints with the seal computed on the GPU:
+    K1 into a device parity ring, gs_parity_offload_sealed (D2H of the rows
+    into the reserved entries + the chunks' checksums by the bit-sliced GPU
+    FNV-1a), gs_store_commit_sealed_batch (no host FNV pass)."""
+    from paper_2605_00831_b200 import _lib as L
+    from paper_2605_00831_b200.coding import check, encoder
+    from paper_2605_00831_b200.parity_store import ParityStore
+
+    S = ring.shape[1]
+    store = ParityStore(seal_threads=threads)
+    store.bind_device(dev.index or 0)
+    enc, lib = encoder(scheme), L.lib()
+    R = 4   # device parity buffers / pinned checksum arrays in flight
+    par = torch.empty((R, S, K_PARITY, SLICE), dtype=torch.uint8, device=dev)
+    sums = [torch.zeros(S, dtype=torch.int64).pin_memory() for _ in range(R)]
+    rows = [L.ptr_array([par[i, s, r].data_ptr() for s in range(S) for r in range(K_PARITY)]) for i in range(R)]
+    free = [None] * R
+    torch.cuda.synchronize()
+
+    def one(b):
+        i = b % R
+        if free[i] is not None:
+            comp.wait_event(free[i])      # the buffer's previous D2H is done
+            free[i].synchronize()         # ... and its checksums were consumed by the store callback
+        keys = [(s, b) for s in range(S)]
+        acc, dst = store.reserve_batch(keys, scheme, BLOCK_TOKENS, SLICE)
+        assert acc == S
+        check(lib.gs_apply_device(enc.handle, S, slots[b % RING_BLOCKS], rows[i], SLICE, comp.cuda_stream), "k1")
+        check(lib.gs_parity_offload_sealed(rows[i], S, K_PARITY, SLICE, L.ptr_array(dst), sums[i].data_ptr(),
+                                           comp.cuda_stream, copy.cuda_stream), "device seal")
+        store.commit_sealed_batch(keys, sums[i].data_ptr(), copy)
+        free[i] = torch.cuda.Event()
+        free[i].record(copy)
+
+    for b in range(blocks):   # warm: slabs, scratch pool
+        one(b)
+    copy.synchronize()
+    store.wait_sealed()
+    for s in range(S):
+        store.erase_request(s)
+    t0 = time.perf_counter()
+    for b in range(blocks):
+        one(b)
+    copy.synchronize()
+    store.wait_sealed()
+    t_all = time.perf_counter() - t0
+    ok = all(int(store.get(s, b)[0]) == 0 for s in range(0, S, 7) for b in (0, blocks - 1))
+    data = blocks * S * N_SHARDS * SLICE
+    out = {"checkpoint_gbs_sealed": round(data / t_all / 1e9, 2),
+           "seal_parity_gbs": round(blocks * S * K_PARITY * SLICE / t_all / 1e9, 2),
+           "get_verified_ok": ok,
+           "note": "seal on the GPU (gs_parity_offload_sealed + gs_store_commit_sealed_batch); get() re-verifies "
+                   "on the host with the reference's serial FNV"}
+    store.close()
     return out
 
 

@@ -319,7 +319,9 @@ int gs_verify_finish(gs_verify* v, int threads, uint64_t* sums);
  * Entries are keyed (request, chunk). Reserve -> the D2H of K1 writes the k
  * parity buffers straight into the returned pinned pointers (no try_put
  * copy, checkpoint.hpp:207) -> commit: the FNV-1a seal runs on host threads
- * once `stream` reaches that point (cudaLaunchHostFunc), off the GPU path. */
+ * once `stream` reaches that point (an event waited on by the store's landing
+ * thread; the stream never blocks on the host), off the GPU path. Commits
+ * cannot be captured into CUDA graphs (GS_INVALID_ARGUMENT). */
 int gs_store_create(uint64_t capacity_bytes /* ~0 = unlimited */, int seal_threads, gs_store** out);
 int gs_store_destroy(gs_store* s);
 /* Place the store's future pinned slabs on `device`'s NUMA node (the socket
