@@ -42,6 +42,7 @@ int special_decoders_kreedsolomon_6_2_e1(SpecialEntry* out);
 int special_decoders_kreedsolomon_6_2_e2(SpecialEntry* out);
 int special_decoders_kreedsolomon_8_2_e1(SpecialEntry* out);
 int special_decoders_kreedsolomon_8_2_e2(SpecialEntry* out);
+int batch_copies(void* const* dst, const void* const* src, int n, size_t bytes, int kind_d2h, cudaStream_t st);
 }  // namespace gsb
 
 using namespace gsb;
@@ -911,6 +912,16 @@ int issue_copies(std::vector<CopyOp>& ops, cudaMemcpyKind kind, cudaStream_t st)
 }
 
 }  // namespace
+
+// Batched host-link copies for other translation units (gs_fnv_gpu.cu):
+// same merging into 1-D runs / constant-pitch 2-D copies as the pipelines.
+int gsb::batch_copies(void* const* dst, const void* const* src, int n, size_t bytes, int kind_d2h, cudaStream_t st) {
+  std::vector<CopyOp> ops;
+  ops.reserve(static_cast<size_t>(n));
+  for (int i = 0; i < n; ++i)
+    ops.push_back({static_cast<uint8_t*>(dst[i]), static_cast<const uint8_t*>(src[i]), bytes, 0});
+  return issue_copies(ops, kind_d2h ? cudaMemcpyDeviceToHost : cudaMemcpyHostToDevice, st);
+}
 
 extern "C" {
 

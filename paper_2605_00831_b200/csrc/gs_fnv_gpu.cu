@@ -39,6 +39,8 @@
 
 namespace gsb {
 void set_last_error(const char* msg);  // gs_capi.cu
+// gs_capi.cu: host-link copies merged into 1-D runs / constant-pitch 2-D copies
+int batch_copies(void* const* dst, const void* const* src, int n, size_t bytes, int kind_d2h, cudaStream_t st);
 }
 
 namespace {
@@ -404,11 +406,15 @@ extern "C" int gs_parity_offload_sealed(const void* const* d_parity, int n_chunk
       cudaEventDestroy(ev);
       return ffail(GS_INVALID_ARGUMENT, "parity_offload_sealed: NULL row %d", i);
     }
-    e = cudaMemcpyAsync(h_parity[i], d_parity[i], len, cudaMemcpyDeviceToHost, ys);
   }
   if (e != cudaSuccess) {
     cudaEventDestroy(ev);
     return ffail(GS_CUDA_ERROR, "parity offload: %s", cudaGetErrorString(e));
+  }
+  // rows of consecutive store entries merge into one copy (or one 2-D copy per row)
+  if (int s = gsb::batch_copies(h_parity, d_parity, n_chunks * k, len, 1, ys)) {
+    cudaEventDestroy(ev);
+    return s;
   }
   uint64_t* d_sums = nullptr;
   e = cudaMallocAsync(reinterpret_cast<void**>(&d_sums), sizeof(uint64_t) * n_chunks, cs);
