@@ -600,13 +600,20 @@ def run_ours(args):
     t_plan = time.perf_counter()
     rplan = plan_reconstruct_striped(scheme, layout, bases[b], rank, ErasurePattern([lost_w]), h_parity, pipe)
     plan_ms = (time.perf_counter() - t_plan) * 1e3
-    r0, r1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    r0.record(comp)
-    rplan.run(comp.cuda_stream, copy.cuda_stream)
-    r1.record(comp)
-    r1.synchronize()
-    barrier()
-    rec_ms = r0.elapsed_time(r1)
+    reps = []
+    for rep in range(5):   # the same failure recovered 5 times (buffer re-flushed each time); median
+        if rep and rank == owner:
+            ring[b, :, jl].zero_()
+        torch.cuda.synchronize()
+        barrier()
+        r0, r1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        r0.record(comp)
+        rplan.run(comp.cuda_stream, copy.cuda_stream)
+        r1.record(comp)
+        r1.synchronize()
+        barrier()
+        reps.append(r0.elapsed_time(r1))
+    rec_ms = sorted(reps)[len(reps) // 2]
     if world > 1:
         t = torch.tensor([rec_ms], device="cpu" if shared else dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
@@ -618,6 +625,8 @@ def run_ours(args):
         dist.all_reduce(t, op=dist.ReduceOp.MIN)
         ok_parity = bool(t.item())
     recovery["c2_block_one_worker_ms"] = round(rec_ms, 4)
+    recovery["c2_block_reps_ms"] = [round(x, 4) for x in reps]
+    recovery["c2_block_roofline_ms"] = round(S * SLICE / (link["h2d"] * 1e9) * 1e3 / world, 4)
     recovery["c2_plan_host_ms"] = round(plan_ms, 3)
     recovery["c2_block_bytes_rebuilt"] = S * SLICE
     recovery["c2_h2d_bytes"] = S * SLICE

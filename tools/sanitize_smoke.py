@@ -3,7 +3,8 @@ every kernel family once -- specialised (register + bulk-copy pipeline),
 generic (aligned, ragged tail, misaligned), paged gather/scatter, the
 offload / upload pipelines (with live kernel timing stamps), RDP (pipelined
 body + tile remainder + P/Q tail, two-column and single-column recovery) and
-a runtime-specialised (NVRTC) kernel -- at sizes that finish quickly under
+a runtime-specialised (NVRTC) kernel, the GPU FNV-1a seal and the split
+parity verification -- at sizes that finish quickly under
 instrumentation. Exits non-zero on any byte mismatch vs the oracle.
 
     compute-sanitizer --tool memcheck python tools/sanitize_smoke.py
@@ -116,6 +117,28 @@ def main():
     par = D.encode(sch9, data)
     want = O.port().encode(O.RS, 9, 2, list(data.cpu().numpy()))
     bad += sum(not np.array_equal(par[i].cpu().numpy(), want[i]) for i in range(2))
+    # GPU FNV-1a seal (all 18 kernels: partial last block, several chains) and
+    # the split verification (GPU-hashed rows continued by host threads)
+    port = O.port()
+    ln = 16384 * 2 + 4096 + 48
+    rows = torch.randint(0, 256, (3, 2, ln), dtype=torch.uint8, device="cuda", generator=g)
+    sums = torch.zeros(3, dtype=torch.int64, device="cuda")
+    st = torch.cuda.current_stream()
+    ptrs = L.ptr_array([rows[c, i].data_ptr() for c in range(3) for i in range(2)])
+    assert L.lib().gs_fnv1a64_device(ptrs, 3, 2, ln, 0xCBF29CE484222325, sums.data_ptr(), st.cuda_stream) == 0
+    host = rows.cpu()
+    want = [port.parity_checksum([host[c, 0].numpy(), host[c, 1].numpy()]) for c in range(3)]
+    bad += sum((int(v) & (2**64 - 1)) != w for v, w in zip(sums.cpu().tolist(), want))
+    hp = host.pin_memory()
+    dev = torch.zeros_like(rows)
+    torch.cuda.synchronize()
+    h = C.c_void_p()
+    drows = [dev[c, i].data_ptr() if (c < 1 or i < 1) else None for c in range(3) for i in range(2)]
+    assert L.lib().gs_verify_enqueue(L.ptr_array([hp[c, i].data_ptr() for c in range(3) for i in range(2)]), 3, 2,
+                                     ln, 1, 1, L.ptr_array(drows), st.cuda_stream, st.cuda_stream, C.byref(h)) == 0
+    out = (C.c_uint64 * 3)()
+    assert L.lib().gs_verify_finish(h, 2, out) == 0
+    bad += sum(out[c] != want[c] for c in range(3))
     pipe.close()
     torch.cuda.synchronize()
     print("sanitize_smoke: mismatches =", bad, "kernels =", D.launches(), "jit status =", js.value)
