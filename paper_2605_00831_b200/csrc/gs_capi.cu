@@ -148,6 +148,11 @@ int g_full_grid = [] {
   return e ? std::atoi(e) : 0;
 }();
 constexpr uint64_t kBulkAutoBytes = 128ull << 20;
+// Paged K1/K2 walk tiles page-major (GS_PAGE_MAJOR=0: stripe-major, for A/B).
+const bool g_page_major = [] {
+  const char* e = std::getenv("GS_PAGE_MAJOR");
+  return !(e && std::atoi(e) == 0);
+}();
 // RDP whole-dstripe body on the pipelined kernels (GS_RDP_FAST=0: tile kernels only, for A/B).
 const bool g_rdp_fast = [] {
   const char* e = std::getenv("GS_RDP_FAST");
@@ -464,6 +469,10 @@ int run_codec(const gs_codec* c, int n_stripes, SlotFn slot_ptr, OutFn out_ptr, 
                  pg.paged_slots, pg.logical0, pg.src, pg.dst};
       g.tps_m = fastdiv_magic(g.tps);
       g.tstamp = pg.tstamp;
+      if (paged && !jit && !use_bulk && g_page_major) {  // page-major walk (gs_kernels.cuh TileGeom)
+        g.nstripes = static_cast<uint32_t>(cnt);
+        g.nstripes_m = fastdiv_magic(g.nstripes);
+      }
       if (g.src.table) g.src.table += (pg.stripe0 + s0) * g.src.table_stride;
       if (g.dst.table) g.dst.table += (pg.stripe0 + s0) * g.dst.table_stride;
       const int grid = static_cast<int>(std::min<uint64_t>(total, g_full_grid && !use_bulk ? total : static_cast<uint64_t>(occ) * sms));

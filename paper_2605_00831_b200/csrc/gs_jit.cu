@@ -33,7 +33,7 @@ namespace gsb {
 
 // bumped whenever the kernel template or TileGeom layout changes, so stale
 // on-disk cubins are never reused
-constexpr const char* kJitVersion = "gsjit-3";
+constexpr const char* kJitVersion = "gsjit-4";
 constexpr int kJitMaxRows = 8;
 constexpr int kJitMaxUsed = 24;
 

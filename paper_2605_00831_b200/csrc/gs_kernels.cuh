@@ -173,6 +173,12 @@ struct TileGeom {
   // start, last warp end} in %globaltimer ns, combined with atomics across
   // every launch of one codec call. nullptr = off.
   unsigned long long* tstamp;
+  // Paged launches walk tiles page-major (tile t -> stripe t % nstripes,
+  // page-tile t / nstripes): consecutive CTAs then read the same (layer, K/V)
+  // page of consecutive cache blocks, i.e. contiguous cache memory, instead
+  // of 64 pages 2 MiB apart. 0 = stripe-major (contiguous slices).
+  uint32_t nstripes;
+  uint64_t nstripes_m;  // fastdiv_magic(nstripes)
 };
 
 __device__ __forceinline__ unsigned long long globaltimer_ns() {
@@ -302,8 +308,15 @@ __global__ void __launch_bounds__(kThreads) k_apply_special(const PtrTable<CAP> 
   static_assert(U == 1, "one 16-byte group per thread per tile");
   stamp_start(g);
   for (uint32_t t = blockIdx.x; t < g.total; t += gridDim.x) {
-    const uint32_t s = tile_stripe(t, g);
-    const uint64_t off = static_cast<uint64_t>(t - s * g.tps) * kTile + threadIdx.x * kVec;
+    uint32_t s, tin;
+    if (PAGED && g.nstripes) {
+      tin = fdiv(t, g.nstripes, g.nstripes_m);
+      s = t - tin * g.nstripes;
+    } else {
+      s = tile_stripe(t, g);
+      tin = t - s * g.tps;
+    }
+    const uint64_t off = static_cast<uint64_t>(tin) * kTile + threadIdx.x * kVec;
     if (off >= g.len) continue;
     const int base = static_cast<int>(s) * g.stride;
     uint4 src[Spec::NS];
@@ -318,7 +331,7 @@ __global__ void __launch_bounds__(kThreads) k_apply_special(const PtrTable<CAP> 
     } else {
       bool smask = false, dmask = false;
       uint64_t soff = off, doff = off;
-      const uint64_t tile_logical = g.logical0 + static_cast<uint64_t>(t - s * g.tps) * kTile;
+      const uint64_t tile_logical = g.logical0 + static_cast<uint64_t>(tin) * kTile;
       const uint32_t lane_off = threadIdx.x * kVec;
       if (g.paged_slots) soff = paged_offset_tile(g.src, s, tile_logical, lane_off, smask);
       if (g.dst.page_bytes) doff = paged_offset_tile(g.dst, s, tile_logical, lane_off, dmask);
