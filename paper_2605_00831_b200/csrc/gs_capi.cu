@@ -29,6 +29,7 @@
 #include "gs_kernels.cuh"
 #include "gs_kv.cuh"
 #include "gs_rdp.cuh"
+#include "gs_rdp_pairs.cuh"
 #include "gs_special.cuh"
 
 namespace gsb {
@@ -541,6 +542,32 @@ int run_codec(const gs_codec* c, int n_stripes, SlotFn slot_ptr, OutFn out_ptr, 
 // for encode and two-column recovery; single-column recovery through the
 // XOR helper codec. `pg.logical0` / `pg.total_len` place this launch's range
 // inside the column (pipelines split on dstripe boundaries).
+// Compiled lost-pair RDP recovery kernels (gs_rdp_pairs.cuh); nullptr when
+// the prime has none or GS_RDP_PAIRS=0.
+const RdpPair* rdp_pair(int p, int li, int lj) {
+  static const bool on = [] {
+    const char* e = std::getenv("GS_RDP_PAIRS");
+    return !(e && std::atoi(e) == 0);
+  }();
+  static const std::vector<RdpPair> table = [] {
+    std::vector<RdpPair> t(kRdpPairP * kRdpPairP);
+    rdp_pairs_p11_i0(t.data());
+    rdp_pairs_p11_i1(t.data());
+    rdp_pairs_p11_i2(t.data());
+    rdp_pairs_p11_i3(t.data());
+    rdp_pairs_p11_i4(t.data());
+    rdp_pairs_p11_i5(t.data());
+    rdp_pairs_p11_i6(t.data());
+    rdp_pairs_p11_i7(t.data());
+    rdp_pairs_p11_i8(t.data());
+    rdp_pairs_p11_i9(t.data());
+    return t;
+  }();
+  if (!on || p != kRdpPairP || li < 0 || lj <= li || lj >= p) return nullptr;
+  const RdpPair& r = table[static_cast<size_t>(li) * p + lj];
+  return r.kernel ? &r : nullptr;
+}
+
 template <class SlotFn, class OutFn>
 int run_rdp(const gs_codec* c, int n_stripes, SlotFn slot_ptr, OutFn out_ptr, uint64_t len, cudaStream_t st,
             const Paging& pg) {
@@ -578,7 +605,9 @@ int run_rdp(const gs_codec* c, int n_stripes, SlotFn slot_ptr, OutFn out_ptr, ui
   // shared-memory tile kernels run the lot.
   const uint64_t full_abs = total / rows * rows;
   const uint32_t TB = rdpb::tile_bytes(p);
-  const size_t fixed = rdpb::kHeader + rdpb::out_bytes(p) + (encode ? 0 : rdpb::chain_bytes(p));
+  // two-column recovery with a compiled pair kernel: chains in registers, no chain scratch
+  const RdpPair* pair = !encode && c->rdp_li >= 0 ? rdp_pair(p, c->rdp_li, c->rdp_lj) : nullptr;
+  const size_t fixed = rdpb::kHeader + rdpb::out_bytes(p) + (encode || pair ? 0 : rdpb::chain_bytes(p));
   const int fast_stages = fixed < rdpb::kSmemBudget
                               ? static_cast<int>(std::min<size_t>(rdpb::kMaxStages, (rdpb::kSmemBudget - fixed) / TB))
                               : 0;
@@ -592,6 +621,7 @@ int run_rdp(const gs_codec* c, int n_stripes, SlotFn slot_ptr, OutFn out_ptr, ui
                    : reinterpret_cast<const void*>(&k_rdp_recover_bulk<kPtrCap, P_>);
   GS_RDP_PRIMES(GS_RDP_PICK_FAST)
 #undef GS_RDP_PICK_FAST
+  if (pair) kfast = pair->kernel;
   const size_t fast_smem = fixed + static_cast<size_t>(fast_stages) * TB;
   if (body && kfast) {
     static std::mutex mu;
@@ -655,9 +685,14 @@ int run_rdp(const gs_codec* c, int n_stripes, SlotFn slot_ptr, OutFn out_ptr, ui
       k_rdp_recover_bulk<kPtrCap, P_><<<grid, threads, fast_smem, st>>>(tab, g, fast_stages, c->n_out,       \
                                                                         in_slots);                           \
   }
-      GS_RDP_PRIMES(GS_RDP_LAUNCH_FAST)
+      cudaError_t e = cudaSuccess;
+      if (pair) {
+        e = pair->launch(grid, threads, fast_smem, st, tab, g, fast_stages, c->n_out, in_slots);
+      } else {
+        GS_RDP_PRIMES(GS_RDP_LAUNCH_FAST)
+        e = cudaGetLastError();
+      }
 #undef GS_RDP_LAUNCH_FAST
-      cudaError_t e = cudaGetLastError();
       if (e != cudaSuccess) return fail(GS_CUDA_ERROR, "rdp kernel launch: %s", cudaGetErrorString(e));
       g_launches.fetch_add(1, std::memory_order_relaxed);
     }

@@ -591,18 +591,44 @@ __global__ void __launch_bounds__((rdpb::kCW + 1) * 32, 1)
 //   sd[d] = Q[d] ^ XOR_{c != i,j} A_c[(d-c) mod p]
 // then the reference's two zig-zag chains run on the syndromes out of shared
 // memory (their indices depend on the launch-uniform i, j).
-template <int CAP, int P>
+// Compile-time form of one chain pass (LI/LJ template arguments): with the
+// loop fully unrolled every d and r constant-folds, so the syndromes and both
+// recovered columns stay in registers (no shared-memory chain scratch).
+__host__ __device__ constexpr int pmod_c(int a, int p) { return ((a % p) + p) % p; }
+
+template <int P, int PRIM, int PART>
+__device__ __forceinline__ void rdp_chain_pass(const uint32_t (&rsyn)[P - 1], const uint32_t (&dsyn)[P - 1],
+                                               uint32_t (&ap)[P], uint32_t (&aq)[P]) {
+  constexpr int step = pmod_c(PART - PRIM, P);
+  int d = pmod_c(PART - 1, P);
+#pragma unroll
+  for (int it = 0; it < P - 1; ++it) {
+    if (d != P - 1) {
+      const int r = pmod_c(d - PRIM, P);
+      const uint32_t v = dsyn[d] ^ aq[pmod_c(d - PART, P)];
+      ap[r] = v;
+      aq[r] = rsyn[r] ^ v;
+      d = pmod_c(d + step, P);
+    }
+  }
+}
+
+// LI/LJ >= 0: the lost pair is a compile-time constant (compiled for the
+// primes in GS_RDP_PAIR_PRIMES, gs_rdp_pairs.cu); -1: runtime pair, chain
+// walked in shared memory.
+template <int CAP, int P, int LI = -1, int LJ = -1>
 __global__ void __launch_bounds__((rdpb::kCW + 1) * 32, 1)
     k_rdp_recover_bulk(const PtrTable<CAP> tab, const RdpGeom g, int stages, int n_out, int out0) {
   using namespace rdpb;
   constexpr int R = P - 1;
   constexpr uint32_t TB = tile_bytes(P);
+  constexpr bool kPair = LI >= 0;
   extern __shared__ __align__(128) uint8_t smem[];
   Ring ring;
   init_ring(smem, stages, ring, TB);
   uint8_t* outbuf = ring.data + static_cast<size_t>(stages) * TB;
   uint32_t* chain = reinterpret_cast<uint32_t*>(outbuf + out_bytes(P));
-  const int n = g.n, i = g.li, j = g.lj;
+  const int n = g.n, i = kPair ? LI : g.li, j = kPair ? LJ : g.lj;
   if (threadIdx.x >= kNT) {  // producer: surviving array columns ascending, then the diagonal
     if ((threadIdx.x & 31) == 0) {
       int cols[kRdpMaxCols + 1];
@@ -648,6 +674,19 @@ __global__ void __launch_bounds__((rdpb::kCW + 1) * 32, 1)
 #pragma unroll
       for (int d = 0; d < R; ++d) dsyn[d] ^= q[d];
     }
+    uint32_t ri[R], rj[R];
+    if constexpr (kPair) {
+      uint32_t ai[P], aj[P];
+#pragma unroll
+      for (int r = 0; r < P; ++r) ai[r] = aj[r] = 0;
+      rdp_chain_pass<P, LI, LJ>(rsyn, dsyn, ai, aj);
+      rdp_chain_pass<P, LJ, LI>(rsyn, dsyn, aj, ai);
+#pragma unroll
+      for (int r = 0; r < R; ++r) {
+        ri[r] = ai[r];
+        rj[r] = aj[r];
+      }
+    } else {
 #pragma unroll
     for (int r = 0; r < R; ++r) {
       at(sr, r) = rsyn[r];
@@ -671,11 +710,11 @@ __global__ void __launch_bounds__((rdpb::kCW + 1) * 32, 1)
         d = pmod(d + step, P);
       }
     }
-    uint32_t ri[R], rj[R];
 #pragma unroll
     for (int r = 0; r < R; ++r) {
       ri[r] = at(ai, r);
       rj[r] = at(aj, r);
+    }
     }
     if (threadIdx.x == 0) bulk_wait_read<1>();
     consumers_sync();
