@@ -391,10 +391,12 @@ class Checkpointer:
 
     # checkpoint.hpp:179-222
     def _device_seal(self, stripes: int = 1) -> bool:
+        if self.slice % 16:   # the GPU FNV takes 16-B multiples: host seal
+            return False
         if self.seal == "device":
             return True
         if self.seal == "auto":
-            return self.slice % 16 == 0 and stripes * self.cfg.scheme.k * self.slice >= (4 << 20)
+            return stripes * self.cfg.scheme.k * self.slice >= (4 << 20)
         return False
 
     def _checkpoint_device_sealed(self, keys, slots, dsts) -> None:
@@ -534,9 +536,10 @@ class Checkpointer:
         e0 = e1 = None
         result.plan_ms = (time.perf_counter() - t_wall) * 1e3
         decode = parity_ok and not over and r < n and ground_truth is not None
+        gpu_verify = self.gpu_verify and self.slice % 16 == 0   # the GPU FNV takes 16-B multiples
         host_verify = None
         split = None            # (n_full, in-flight gs_verify finished on a host thread)
-        if parity_ok and entries and not (decode and self.gpu_verify):
+        if parity_ok and entries and not (decode and gpu_verify):
             # the reference's placement: every entry verified on host threads,
             # overlapped with the enqueue and the decode
             host_verify = _HostVerify(self, entries, verify_threads)
@@ -550,7 +553,7 @@ class Checkpointer:
                 st.wait_stream(cur)
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             e0.record(self.compute)
-            if self.gpu_verify:
+            if gpu_verify:
                 outs, oi, n_full, split_h, keep = self._enqueue_split_verified_decode(ground_truth, ids, entries,
                                                                                      failed, verify_threads)
                 pending.append((r, outs, oi, keep))
@@ -656,7 +659,7 @@ class Checkpointer:
         dec = decoder(sch, ErasurePattern(sorted(failed)))
         S, k = len(chunk_ids), sch.k
         threads = threads or max(1, (os.cpu_count() or 1) - 2)
-        n_full, u = self._split_plan(S, failed, threads) if self.slice % 16 == 0 else (0, k)
+        n_full, u = self._split_plan(S, failed, threads)
         lib = L.lib()
         full = torch.empty((n_full, k, self.slice), dtype=torch.uint8, device=self.dev)
         part = torch.empty((S - n_full, u, self.slice), dtype=torch.uint8, device=self.dev)

@@ -1476,7 +1476,11 @@ static int reconstruct_upload(gs_pipeline* p, const gs_codec* c, int n_stripes, 
   // (>= 1 MiB each) so the rebuild of piece i runs under the H2D of piece
   // i+1 instead of after the whole upload.
   const uint64_t total_h2d = static_cast<uint64_t>(n_stripes) * H * len;
-  const uint64_t piece_cap = std::max<uint64_t>(1ull << 20, total_h2d / 4);
+  static const uint64_t min_pieces = [] {
+    const char* e = std::getenv("GS_UPLOAD_PIECES");
+    return static_cast<uint64_t>(e && std::atoi(e) > 0 ? std::atoi(e) : 4);
+  }();
+  const uint64_t piece_cap = std::max<uint64_t>(1ull << 20, total_h2d / min_pieces);
   const uint64_t rl_max = piece_len(c, len, slot, H, std::max<uint64_t>(4096, piece_cap / H));
   if (!rl_max) return fail(GS_INVALID_ARGUMENT, "reconstruct_upload: staging slot of %zu B cannot hold one piece", slot);
   std::vector<CopyOp> ops;
