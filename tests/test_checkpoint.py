@@ -281,3 +281,19 @@ def test_orchestration_fuzz():
         assert res.verified, (trial, tp, k, chunk, tokens, failed, res.plan.mode)
         assert res.plan.recompute_chunks == 0 and len(res.plan.reconstruct_ids) == len(ground)
         ck.close()
+
+
+@pytest.mark.gpu
+def test_odd_slice_sizes_fall_back_to_host_fnv():
+    """Slices that are not 16-B multiples (24 B here) cannot use the GPU FNV:
+    seal="device" and gpu_verify fall back to the host chain, bit-exact."""
+    ck, store, torch = _ck(4, 2, 4, chunk=3, layers=1, heads=4, dim=2, restart=1e9)
+    assert ck.slice == 24 and not ck._device_seal(64)
+    ck.seal = "device"
+    run = ck.run_prefill_with_checkpointing(5, 4 * 3, kv_seed=2)
+    ck.synchronize()
+    for c in range(run.chunks_done):
+        st, e = store.get(5, c, verify=True)
+        assert int(st) == 0 and e.checksum == O.port().parity_checksum(e.parity)
+    res = ck.recover(5, FailureEvent([1], at_chunk=run.chunks_done), run.ground_truth, [3] * run.chunks_done)
+    assert res.verified and res.verify_gpu_chunks == 0 and len(res.plan.reconstruct_ids) == run.chunks_done
