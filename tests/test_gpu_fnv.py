@@ -149,3 +149,24 @@ def test_upload_checksum_entry_point():
     got = [int(v) & (2**64 - 1) for v in sums.cpu().tolist()]
     for c in range(n):
         assert got[c] == port.parity_checksum([host[c * k + i].numpy() for i in range(k)])
+
+
+def test_fnv_fuzz_random_chains():
+    """Random chain counts, buffer counts, lengths (16-B multiples around the
+    64-B thread and 16 KiB block grains) and seeds: bit-exact every time."""
+    port = O.port()
+    rng = np.random.default_rng(2026)
+    for trial in range(30):
+        n_chains = int(rng.integers(1, 9))
+        k = int(rng.integers(1, 5))
+        ln = 16 * int(rng.choice([1, 3, 4, 63, 64, 65, 1023, 1024, 1025, int(rng.integers(1, 12000))]))
+        h0 = int(rng.integers(0, 2**63)) * 2 + int(rng.integers(0, 2))
+        host = [rng.integers(0, 256, ln, dtype=np.uint8) for _ in range(n_chains * k)]
+        flat = torch.from_numpy(np.concatenate(host)).cuda()
+        dev = [flat[i * ln:(i + 1) * ln] for i in range(n_chains * k)]
+        got = device_fnv(dev, n_chains, k, ln, h0)
+        for c in range(n_chains):
+            h = h0
+            for i in range(k):
+                h = port.fnv1a64(host[c * k + i], h)
+            assert got[c] == h, (trial, n_chains, k, ln, c)
