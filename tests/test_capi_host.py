@@ -246,3 +246,18 @@ def test_random_schemes_decode_like_the_reference(port):
                     acc ^= mul[coef[b, s]][slots[s]]
             assert np.array_equal(acc, outs[b]), (trial, n, k, lost, j)
             assert np.array_equal(acc, data[j])
+
+
+def test_reference_gf256_suite_runs_against_the_library():
+    """The reference's own proj/tests/gf256_test.cpp (8 cases: known values,
+    exhaustive schoolbook oracle, inverses, field laws, mul_row), compiled
+    unmodified against the B200 library's GF(2^8) (tests/cpp/refsuite shims;
+    built by build() into oracle/_ref when the reference is mounted)."""
+    import subprocess
+    exe = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "oracle", "_ref",
+                       "ref_gf256_test_b200")
+    if not os.path.exists(exe):
+        pytest.skip("reference suites not built (no /root/reference at build time)")
+    out = subprocess.run([exe], capture_output=True, text=True, timeout=300)
+    assert out.returncode == 0, out.stdout[-2000:] + out.stderr[-2000:]
+    assert "8 tests, 0 failed" in out.stdout

@@ -673,3 +673,17 @@ def test_pipeline_fuzz():
         for j, t in outs.items():
             assert torch.equal(t, data[:, j]), (trial, kind, n, k, S, ln, ring, lost, j)
         pipe.close()
+
+
+def test_reference_coding_suite_runs_against_the_gpu_library():
+    """The reference's own proj/tests/coding_test.cpp (16 cases: validation,
+    tolerance, matrices, MDS, XOR literal vectors, every erasure pattern of
+    XOR / RDP / RS round trips at 1 B / 17 B / 4 KiB, linearity, determinism,
+    error classes), compiled unmodified with ghostserve:: bound to the drop-in
+    facade: every encode / reconstruct it makes runs the sm_100a kernels."""
+    exe = os.path.join(ROOT, "oracle", "_ref", "ref_coding_test_b200")
+    if not os.path.exists(exe):
+        pytest.skip("reference suites not built (no /root/reference at build time)")
+    out = subprocess.run([exe], capture_output=True, text=True, timeout=600)
+    assert out.returncode == 0, out.stdout[-3000:] + out.stderr[-3000:]
+    assert "16 tests, 0 failed" in out.stdout
