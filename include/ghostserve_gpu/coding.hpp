@@ -11,7 +11,8 @@
 //
 // Status codes map back to the reference exception types:
 //   GS_INVALID_ARGUMENT -> std::invalid_argument, GS_UNRECOVERABLE ->
-//   UnrecoverableError, GS_DOMAIN_ERROR -> std::domain_error, others ->
+//   UnrecoverableError, GS_DOMAIN_ERROR -> std::domain_error, GS_LOGIC_ERROR ->
+//   std::logic_error, others ->
 //   std::runtime_error. A consumer switches by changing the namespace (or a
 //   `namespace ghostserve = ghostserve_gpu;` alias) and linking
 //   libghostserve_b200.so; every byte is computed by the sm_100a kernels.
@@ -55,6 +56,7 @@ inline void check(int status, const char* what) {
     case GS_INVALID_ARGUMENT: throw std::invalid_argument(msg);
     case GS_UNRECOVERABLE: throw UnrecoverableError(msg);
     case GS_DOMAIN_ERROR: throw std::domain_error(msg);
+    case GS_LOGIC_ERROR: throw std::logic_error(msg);
     default: throw std::runtime_error(msg);
   }
 }

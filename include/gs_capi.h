@@ -269,6 +269,10 @@ int gs_ground_truth_slice_device(uint64_t kv_seed, uint64_t request_id, uint32_t
                                  int worker, int layers, int kv_heads, int head_dim, int tp,
                                  uint32_t chunk_size, uint32_t valid_tokens, void* d_out,
                                  void* stream);
+/* The same into host memory (device generation + copy back; synchronous). */
+int gs_ground_truth_slice(uint64_t kv_seed, uint64_t request_id, uint32_t chunk, int worker, int layers,
+                          int kv_heads, int head_dim, int tp, uint32_t chunk_size, uint32_t valid_tokens,
+                          void* h_out);
 /* pad_partial (kv_layout.hpp:73-84) on a device slice */
 int gs_pad_partial_device(void* d_slice, int layers, int kv_heads, int head_dim, int tp,
                           uint32_t chunk_size, uint32_t valid_tokens, void* stream);

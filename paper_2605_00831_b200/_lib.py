@@ -67,6 +67,7 @@ SIGNATURES = {
     "gs_pipeline_kernel_time": (_i, [_vp, C.POINTER(C.c_double), C.POINTER(C.c_double), _ip, _u64p]),
     "gs_slice_bytes": (_i, [_i, _i, _i, _i, _u32, _u64p]),
     "gs_ground_truth_slice_device": (_i, [_u64, _u64, _u32, _i, _i, _i, _i, _i, _u32, _u32, _vp, _vp]),
+    "gs_ground_truth_slice": (_i, [_u64, _u64, _u32, _i, _i, _i, _i, _i, _u32, _u32, _vp]),
     "gs_pad_partial_device": (_i, [_vp, _i, _i, _i, _i, _u32, _u32, _vp]),
     "gs_fnv1a64": (_u64, [_vp, _sz, _u64]),
     "gs_parity_checksum": (_u64, [_vpp, _i, _sz]),

@@ -1782,6 +1782,29 @@ int gs_ground_truth_slice_device(uint64_t kv_seed, uint64_t request_id, uint32_t
   return GS_OK;
 }
 
+// Host-buffer form (the reference's make_ground_truth_slice returns host
+// bytes): generated by k_ground_truth into a temporary device buffer, copied
+// back; synchronous.
+int gs_ground_truth_slice(uint64_t kv_seed, uint64_t request_id, uint32_t chunk, int worker, int layers,
+                          int kv_heads, int head_dim, int tp, uint32_t chunk_size, uint32_t valid_tokens,
+                          void* h_out) {
+  uint64_t len = 0;
+  if (int s = gs_slice_bytes(layers, kv_heads, head_dim, tp, chunk_size, &len)) return s;
+  if (valid_tokens > chunk_size) return fail(GS_INVALID_ARGUMENT, "kv: valid_tokens exceeds chunk size");
+  if (len == 0) return GS_OK;
+  if (!h_out) return fail(GS_INVALID_ARGUMENT, "ground_truth: NULL output");
+  void* d = nullptr;
+  GS_CUDA(cudaMalloc(&d, len));
+  int st = gs_ground_truth_slice_device(kv_seed, request_id, chunk, worker, layers, kv_heads, head_dim, tp,
+                                        chunk_size, valid_tokens, d, nullptr);
+  if (st == GS_OK) {
+    const cudaError_t e = cudaMemcpy(h_out, d, len, cudaMemcpyDeviceToHost);
+    if (e != cudaSuccess) st = fail(GS_CUDA_ERROR, "ground_truth copy: %s", cudaGetErrorString(e));
+  }
+  cudaFree(d);
+  return st;
+}
+
 int gs_pad_partial_device(void* d_slice, int layers, int kv_heads, int head_dim, int tp, uint32_t chunk_size,
                           uint32_t valid_tokens, void* stream) {
   uint64_t len = 0;

@@ -687,3 +687,19 @@ def test_reference_coding_suite_runs_against_the_gpu_library():
     out = subprocess.run([exe], capture_output=True, text=True, timeout=600)
     assert out.returncode == 0, out.stdout[-3000:] + out.stderr[-3000:]
     assert "16 tests, 0 failed" in out.stdout
+
+
+def test_reference_kv_model_suite_runs_against_the_library():
+    """The reference's own proj/tests/kv_model_test.cpp (17 cases: chunk
+    counts, slice sizes, pad_partial incl. parity of padded slices vs a masked
+    oracle and pad-length neutrality across schemes, ground-truth determinism,
+    ParityStore put/get/missing/corrupt/capacity/duplicate/audit/peak, GSRV
+    persistence round trip and corruption detection), compiled unmodified
+    against the ghostserve_gpu facades: slices generated by the device kernel,
+    parity by the GPU codec, entries in the pinned-slab store."""
+    exe = os.path.join(ROOT, "oracle", "_ref", "ref_kv_model_test_b200")
+    if not os.path.exists(exe):
+        pytest.skip("reference suites not built (no /root/reference at build time)")
+    out = subprocess.run([exe], capture_output=True, text=True, timeout=600)
+    assert out.returncode == 0, out.stdout[-3000:] + out.stderr[-3000:]
+    assert "17 tests, 0 failed" in out.stdout
