@@ -53,12 +53,14 @@ class ParityStore {  // :62-143
     detail::check(gs_store_create(capacity_bytes, 2, &s_), "parity store");
   }
   explicit ParityStore(gs_store* adopted) : s_(adopted) {}
-  ParityStore(ParityStore&& o) noexcept : s_(std::exchange(o.s_, nullptr)), view_(std::move(o.view_)) {}
+  ParityStore(ParityStore&& o) noexcept
+      : s_(std::exchange(o.s_, nullptr)), view_(std::move(o.view_)), all_(std::move(o.all_)) {}
   ParityStore& operator=(ParityStore&& o) noexcept {
     if (this != &o) {
       if (s_) gs_store_destroy(s_);
       s_ = std::exchange(o.s_, nullptr);
       view_ = std::move(o.view_);
+      all_ = std::move(o.all_);
     }
     return *this;
   }
@@ -78,40 +80,27 @@ class ParityStore {  // :62-143
   bool try_put(ParityChunk chunk) {
     std::vector<const void*> ptrs;
     for (const auto& b : chunk.parity) ptrs.push_back(b.data());
-    if (!chunk.payload_present() || static_cast<int>(ptrs.size()) != chunk.scheme.k)
+    if (chunk.payload_present() && static_cast<int>(ptrs.size()) != chunk.scheme.k)
       throw std::invalid_argument("parity store: entries carry k parity buffers");
     int accepted = 0;
+    // no payload: a cost-only entry (KvPolicy::materialize = false)
     detail::check(gs_store_put(s_, chunk.request_id, chunk.chunk_id.index, static_cast<int>(chunk.scheme.kind),
-                               chunk.scheme.n, chunk.scheme.k, chunk.valid_tokens, chunk.slice_len, ptrs.data(),
-                               chunk.checksum, 1, &accepted),
+                               chunk.scheme.n, chunk.scheme.k, chunk.valid_tokens, chunk.slice_len,
+                               chunk.payload_present() ? ptrs.data() : nullptr, chunk.checksum, 1, &accepted),
                   "parity store");
     return accepted != 0;
   }
 
   // :92-101 -- kMissing / kCorrupt (FNV re-verified) / kOk with *out.
   ParityGetStatus get(std::uint64_t request_id, std::uint32_t chunk_index, const ParityChunk** out) const {
-    int status = 0, knk[3] = {0, 0, 0};
-    void* rows[256];
-    std::uint64_t slice_len = 0, checksum = 0;
-    std::uint32_t valid = 0;
-    detail::check(gs_store_get(s_, request_id, chunk_index, 1, &status, rows, &slice_len, &valid, &checksum, knk),
-                  "parity store");
+    ParityChunk c;
+    const int status = materialize(request_id, chunk_index, /*verify=*/1, c);
     if (status == 1) return ParityGetStatus::kMissing;
     if (status == 2) return ParityGetStatus::kCorrupt;
     if (out) {
-      ParityChunk& c = view_[{request_id, chunk_index}];
-      c = ParityChunk{};
-      c.request_id = request_id;
-      c.chunk_id = ChunkId{chunk_index};
-      c.scheme = CodingScheme{static_cast<CodeKind>(knk[0]), knk[1], knk[2]};
-      c.valid_tokens = valid;
-      c.slice_len = slice_len;
-      c.checksum = checksum;
-      for (int i = 0; i < knk[2]; ++i) {
-        const auto* p = static_cast<const std::uint8_t*>(rows[i]);
-        c.parity.emplace_back(p, p + slice_len);
-      }
-      *out = &c;
+      ParityChunk& slot = view_[{request_id, chunk_index}];
+      slot = std::move(c);
+      *out = &slot;
     }
     return ParityGetStatus::kOk;
   }
@@ -129,7 +118,48 @@ class ParityStore {  // :62-143
   }
   gs_store* handle() const { return s_; }
 
+  // :133-135 -- every entry as stored (no verification: a corrupted entry's
+  // bytes and recorded checksum), rebuilt from the store on each call; the
+  // map stays valid until the next entries() call.
+  const std::map<std::pair<std::uint64_t, std::uint32_t>, ParityChunk>& entries() const {
+    std::uint64_t cnt = 0;
+    detail::check(gs_store_keys(s_, nullptr, 0, &cnt), "parity store");
+    std::vector<std::uint64_t> keys(2 * cnt + 2);
+    detail::check(gs_store_keys(s_, keys.data(), cnt, &cnt), "parity store");
+    all_.clear();
+    for (std::uint64_t e = 0; e < cnt; ++e) {
+      const auto req = keys[2 * e];
+      const auto idx = static_cast<std::uint32_t>(keys[2 * e + 1]);
+      materialize(req, idx, /*verify=*/0, all_[{req, idx}]);
+    }
+    return all_;
+  }
+
  private:
+  // copy of entry (req, idx) into c; returns the store status (0 ok, 1 missing, 2 corrupt)
+  int materialize(std::uint64_t request_id, std::uint32_t chunk_index, int verify, ParityChunk& c) const {
+    int status = 0, knk[3] = {0, 0, 0};
+    void* rows[256];
+    std::uint64_t slice_len = 0, checksum = 0;
+    std::uint32_t valid = 0;
+    detail::check(gs_store_get(s_, request_id, chunk_index, verify, &status, rows, &slice_len, &valid, &checksum,
+                               knk),
+                  "parity store");
+    if (status != 0) return status;
+    c = ParityChunk{};
+    c.request_id = request_id;
+    c.chunk_id = ChunkId{chunk_index};
+    c.scheme = CodingScheme{static_cast<CodeKind>(knk[0]), knk[1], knk[2]};
+    c.valid_tokens = valid;
+    c.slice_len = slice_len;
+    c.checksum = checksum;
+    for (int i = 0; i < knk[2] && rows[0]; ++i) {  // rows NULL: cost-only entry, no payload
+      const auto* p = static_cast<const std::uint8_t*>(rows[i]);
+      c.parity.emplace_back(p, p + slice_len);
+    }
+    return 0;
+  }
+
   std::uint64_t stat(int i) const {
     std::uint64_t v[5] = {0, 0, 0, 0, 0};
     detail::check(gs_store_stats(s_, v), "parity store");
@@ -137,6 +167,7 @@ class ParityStore {  // :62-143
   }
   gs_store* s_ = nullptr;
   mutable std::map<std::pair<std::uint64_t, std::uint32_t>, ParityChunk> view_;
+  mutable std::map<std::pair<std::uint64_t, std::uint32_t>, ParityChunk> all_;
 };
 
 // :201-263 -- the GSRV image, byte-identical to the reference's writer.

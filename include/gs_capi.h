@@ -351,7 +351,8 @@ int gs_store_commit_batch(gs_store* s, int count, const uint64_t* request_ids, c
 int gs_store_commit_sealed_batch(gs_store* s, int count, const uint64_t* request_ids, const uint32_t* chunks,
                                  const uint64_t* checksums, void* stream);
 int gs_store_wait_sealed(gs_store* s);
-/* Copying put (reference try_put): sealed != 0 keeps `checksum` as given. */
+/* Copying put (reference try_put): sealed != 0 keeps `checksum` as given.
+ * parity == NULL: a cost-only entry (no payload; accounted, get() -> kOk). */
 int gs_store_put(gs_store* s, uint64_t request_id, uint32_t chunk, int kind, int n, int k,
                  uint32_t valid_tokens, uint64_t slice_len, const void* const* parity, uint64_t checksum,
                  int sealed, int* accepted);

@@ -420,6 +420,34 @@ int gs_store_put(gs_store* s, uint64_t request_id, uint32_t chunk, int kind, int
                  int sealed, int* accepted) {
   void* dst[256];
   if (k > 256) return sfail(GS_INVALID_ARGUMENT, "store_put: k too large");
+  if (!parity) {  // cost-only entry (the reference's KvPolicy::materialize = false, checkpoint.hpp:51-54):
+                  // accounted like a full one, no bytes held, get() -> kOk without a payload
+    if (!s || !accepted) return sfail(GS_INVALID_ARGUMENT, "store_put: NULL argument");
+    if (int st = gs_scheme_validate(kind, n, k)) return sfail(st, "%s", gs_last_error());
+    *accepted = 0;
+    std::lock_guard<std::mutex> lk(s->mu);
+    const gs_store::Key key{request_id, chunk};
+    if (s->entries.count(key))
+      return sfail(GS_LOGIC_ERROR, "parity store: duplicate entry for request %llu chunk %u",
+                   static_cast<unsigned long long>(request_id), chunk);
+    const uint64_t pay = static_cast<uint64_t>(k) * slice_len, cost = pay + kMetaBytes;
+    if (s->capacity != kUnlimited && s->used + cost > s->capacity) return GS_OK;
+    gs_store::Entry e;
+    e.kind = kind;
+    e.n = n;
+    e.k = k;
+    e.valid = valid_tokens;
+    e.slice_len = slice_len;
+    e.owned = false;
+    e.checksum = sealed ? checksum : 0xcbf29ce484222325ull;
+    e.sealed = true;
+    s->used += cost;
+    s->payload += pay;
+    s->peak = std::max(s->peak, s->payload);
+    s->entries.emplace(key, e);
+    *accepted = 1;
+    return GS_OK;
+  }
   if (int st = gs_store_reserve(s, request_id, chunk, kind, n, k, valid_tokens, slice_len, accepted, dst)) return st;
   if (!*accepted) return GS_OK;
   for (int i = 0; i < k; ++i)

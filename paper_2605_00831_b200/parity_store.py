@@ -133,9 +133,10 @@ class ParityStore:
         if bufs and any(b.size != chunk.slice_len for b in bufs):
             raise InvalidArgument("parity store: parity buffers must be slice_len bytes")
         acc = C.c_int()
+        # no payload: a cost-only entry (KvPolicy::materialize = false), accounted but holding no bytes
         check(L.lib().gs_store_put(self.handle, chunk.request_id, chunk.chunk_id, int(s.kind), s.n, s.k,
                                    chunk.valid_tokens, chunk.slice_len,
-                                   L.ptr_array([b.ctypes.data for b in bufs]), chunk.checksum, 1,
+                                   L.ptr_array([b.ctypes.data for b in bufs]) if bufs else None, chunk.checksum, 1,
                                    C.byref(acc)), "parity store")
         return bool(acc.value)
 
@@ -201,7 +202,7 @@ class ParityStore:
         if status != ParityGetStatus.kOk:
             return status, None
         scheme = CodingScheme(CodeKind(knk[0]), knk[1], knk[2])
-        parity = [_view(ptrs[i], sl.value) for i in range(scheme.k)]
+        parity = [_view(ptrs[i], sl.value) for i in range(scheme.k)] if ptrs[0] else []   # [] = cost-only
         return status, ParityChunk(request_id, chunk_index, scheme, parity, vt.value, sl.value, ck.value)
 
     def contains(self, request_id: int, chunk_index: int) -> bool:

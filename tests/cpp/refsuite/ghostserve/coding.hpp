@@ -52,4 +52,8 @@ inline bool gf_invert_matrix(std::vector<std::uint8_t>& m, int dim, std::vector<
 }
 }  // namespace ghostserve_gpu::detail
 
-namespace ghostserve = ghostserve_gpu;
+// A real namespace (not an alias) so the reference's own headers can reopen
+// `namespace ghostserve { ... }`; everything of the facade is visible in it.
+namespace ghostserve {
+using namespace ghostserve_gpu;
+}

@@ -1,5 +1,6 @@
 // Minimal GoogleTest-compatible shim (GTest is not installed in this image):
-// TEST, EXPECT_/ASSERT_ {EQ, NE, TRUE, FALSE, THROW, NO_THROW, DOUBLE_EQ}
+// TEST, EXPECT_/ASSERT_ {EQ, NE, LT, LE, GT, GE, TRUE, FALSE, THROW, NO_THROW,
+// DOUBLE_EQ, NEAR}
 // with `<<` messages, and a main() that runs every registered test and
 // exits with the number of failed tests. Enough to compile the reference's
 // own unit suites unmodified against the B200 library (tests/cpp/refsuite).
@@ -123,6 +124,20 @@ std::string eq_text(const char* ea, const char* eb, const A&, const B&) {
                  return true;                                                         \
                })(),                                                                  \
                "expected " #stmt " not to throw")
+#define EXPECT_LT(a, b) GSHIM_EXPECT((a) < (b), "expected " #a " < " #b)
+#define EXPECT_LE(a, b) GSHIM_EXPECT((a) <= (b), "expected " #a " <= " #b)
+#define EXPECT_GT(a, b) GSHIM_EXPECT((a) > (b), "expected " #a " > " #b)
+#define EXPECT_GE(a, b) GSHIM_EXPECT((a) >= (b), "expected " #a " >= " #b)
+#define ASSERT_LT(a, b) GSHIM_ASSERT((a) < (b), "expected " #a " < " #b)
+#define ASSERT_LE(a, b) GSHIM_ASSERT((a) <= (b), "expected " #a " <= " #b)
+#define ASSERT_GT(a, b) GSHIM_ASSERT((a) > (b), "expected " #a " > " #b)
+#define ASSERT_GE(a, b) GSHIM_ASSERT((a) >= (b), "expected " #a " >= " #b)
+#define EXPECT_NEAR(a, b, tol) \
+  GSHIM_EXPECT(std::fabs(static_cast<double>(a) - static_cast<double>(b)) <= static_cast<double>(tol), \
+               "expected |" #a " - " #b "| <= " #tol)
+#define ASSERT_NEAR(a, b, tol) \
+  GSHIM_ASSERT(std::fabs(static_cast<double>(a) - static_cast<double>(b)) <= static_cast<double>(tol), \
+               "expected |" #a " - " #b "| <= " #tol)
 #define ASSERT_THROW(stmt, ex) EXPECT_THROW(stmt, ex)
 #define ASSERT_NO_THROW(stmt) EXPECT_NO_THROW(stmt)
 

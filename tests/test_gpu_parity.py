@@ -703,3 +703,21 @@ def test_reference_kv_model_suite_runs_against_the_library():
     out = subprocess.run([exe], capture_output=True, text=True, timeout=600)
     assert out.returncode == 0, out.stdout[-3000:] + out.stderr[-3000:]
     assert "17 tests, 0 failed" in out.stdout
+
+
+@pytest.mark.parametrize("suite,cases", [("checkpoint", 17), ("recovery", 16)])
+def test_reference_orchestration_suites_run_on_the_library(suite, cases):
+    """The reference's own checkpoint_test.cpp / recovery_test.cpp compiled
+    unmodified together with the reference's own orchestration headers
+    (checkpoint.hpp, recovery.hpp, cost_model.hpp, ... unchanged) whose
+    coding / kv_layout / parity_store includes resolve to the ghostserve_gpu
+    facades: the reference's checkpoint_chunk, run_prefill_with_checkpointing,
+    DecodeCheckpointer, reconstruct_chunk and recover run on the B200 codec,
+    the device KV generator and the pinned-slab store -- incl. the 64K-token
+    RS(8,2) bit-exact recovery (recovery_test.cpp:299-317)."""
+    exe = os.path.join(ROOT, "oracle", "_ref", f"ref_{suite}_test_b200")
+    if not os.path.exists(exe):
+        pytest.skip("reference suites not built (no /root/reference at build time)")
+    out = subprocess.run([exe], capture_output=True, text=True, timeout=900)
+    assert out.returncode == 0, out.stdout[-3000:] + out.stderr[-3000:]
+    assert f"{cases} tests, 0 failed" in out.stdout

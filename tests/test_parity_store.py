@@ -40,6 +40,26 @@ def test_empty_store_accounting_and_errors():
         s.try_put(ParityChunk(1, 0, CodingScheme.reed_solomon(4, 2), [], 0, 0, 0))
 
 
+def test_cost_only_entries():
+    """KvPolicy::materialize = false (checkpoint.hpp:51-54): entries without a
+    payload are accounted like full ones (k * slice_len + 64), get() is kOk
+    with no payload, corrupt_entry is a no-op, GSRV refuses them."""
+    s = ParityStore(3 * (2 * 4096 + 64))
+    sch = CodingScheme.reed_solomon(4, 2)
+    for i in range(3):
+        assert s.try_put(ParityChunk(7, i, sch, [], 16, 4096, 0xCBF29CE484222325))
+    assert not s.try_put(ParityChunk(7, 3, sch, [], 16, 4096, 0))     # back-pressure
+    assert s.used_bytes() == 3 * (2 * 4096 + 64) and s.payload_bytes() == 3 * 8192 and s.audit()
+    st, c = s.get(7, 1)
+    assert st == ParityGetStatus.kOk and not c.payload_present() and c.slice_len == 4096
+    s.corrupt_entry(7, 1)
+    assert s.get(7, 1)[0] == ParityGetStatus.kOk
+    with pytest.raises(InvalidArgument):
+        serialize_parity_store(s)
+    s.erase_request(7)
+    assert s.entry_count() == 0 and s.used_bytes() == 0 and s.peak_payload_bytes() == 3 * 8192
+
+
 @pytest.mark.gpu
 def test_put_get_capacity_duplicate_peak_audit():
     s = ParityStore(2 * (64 + 64) + 10)
