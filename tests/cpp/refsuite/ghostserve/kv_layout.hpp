@@ -5,3 +5,10 @@
 
 #include "ghostserve/coding.hpp"
 #include "ghostserve_gpu/kv_layout.hpp"
+
+// the reference's other headers (trace.hpp) call these unqualified from
+// inside ghostserve::detail
+namespace ghostserve::detail {
+using ghostserve_gpu::detail::mix_key;
+using ghostserve_gpu::detail::splitmix64;
+}

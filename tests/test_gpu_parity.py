@@ -721,3 +721,20 @@ def test_reference_orchestration_suites_run_on_the_library(suite, cases):
     out = subprocess.run([exe], capture_output=True, text=True, timeout=900)
     assert out.returncode == 0, out.stdout[-3000:] + out.stderr[-3000:]
     assert f"{cases} tests, 0 failed" in out.stdout
+
+
+def test_reference_acceptance_criteria_on_the_library():
+    """The reference's acceptance binary (proj/tests/acceptance.cpp, 11
+    criteria) compiled unmodified on top of the facades: C1 (every scheme x
+    {1 B, 17 B, 4 KiB, 1 MiB} x every erasure pattern, bit-exact), C2 (GF vs
+    schoolbook), C3-C9 (memory ratio, checkpoint latency band, stall bound,
+    hybrid recovery, round robin, EITR/MTTR fixtures and trends) and C11 pass;
+    C10 needs the reference CLI, which cannot be built without CLI11 -- the
+    reference's own acceptance run fails it here too."""
+    exe = os.path.join(ROOT, "oracle", "_ref", "ref_acceptance_b200")
+    if not os.path.exists(exe):
+        pytest.skip("reference acceptance not built (no /root/reference at build time)")
+    out = subprocess.run([exe], capture_output=True, text=True, timeout=900)
+    for c in (1, 2, 3, 4, 5, 6, 7, 8, 9, 11):
+        assert f"[PASS] C{c}:" in out.stdout, out.stdout[-4000:]
+    assert out.returncode == 1 and "[FAIL] C10:" in out.stdout
