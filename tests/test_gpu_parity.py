@@ -705,7 +705,7 @@ def test_reference_kv_model_suite_runs_against_the_library():
     assert "17 tests, 0 failed" in out.stdout
 
 
-@pytest.mark.parametrize("suite,cases", [("checkpoint", 17), ("recovery", 16)])
+@pytest.mark.parametrize("suite,cases", [("checkpoint", 17), ("recovery", 16), ("sim", 28)])
 def test_reference_orchestration_suites_run_on_the_library(suite, cases):
     """The reference's own checkpoint_test.cpp / recovery_test.cpp compiled
     unmodified together with the reference's own orchestration headers
