@@ -237,11 +237,12 @@ void compile(JitKernel& k) {
 // one background compile worker
 struct Worker {
   std::mutex mu;
-  std::condition_variable cv;
+  std::condition_variable cv, idle_cv;
   std::deque<JitKernel*> q;
-  bool started = false;
+  bool started = false, busy = false, stopping = false;
   void push(JitKernel* k) {
     std::lock_guard<std::mutex> lk(mu);
+    if (stopping) return;  // process exiting: the kernel stays pending, callers use the generic kernel
     q.push_back(k);
     if (!started) {
       started = true;
@@ -250,13 +251,22 @@ struct Worker {
     cv.notify_one();
   }
   void run() {
+    // NVRTC builds internal statics lazily during its first compile, and their
+    // destructors run at exit in reverse registration order. A trivial
+    // warm-up compile constructs them first; the exit hook registered after it
+    // therefore runs BEFORE they are destroyed and waits for any compile in
+    // flight, so a process that exits mid-compile does not crash in NVRTC.
+    warm_up();
+    std::atexit(+[] { worker_shutdown(); });
     for (;;) {
       JitKernel* k;
       {
         std::unique_lock<std::mutex> lk(mu);
-        cv.wait(lk, [&] { return !q.empty(); });
+        cv.wait(lk, [&] { return stopping || !q.empty(); });
+        if (stopping) return;
         k = q.front();
         q.pop_front();
+        busy = true;
       }
       int st = 1;
       try {
@@ -270,7 +280,31 @@ struct Worker {
         k->state.store(st);
       }
       k->cv.notify_all();
+      {
+        std::lock_guard<std::mutex> lk(mu);
+        busy = false;
+      }
+      idle_cv.notify_all();
     }
+  }
+  // at exit: no new compiles; wait for the one in flight
+  void shutdown() {
+    std::unique_lock<std::mutex> lk(mu);
+    stopping = true;
+    cv.notify_all();
+    idle_cv.wait(lk, [&] { return !busy; });
+  }
+  static void worker_shutdown();
+  static void warm_up() {
+    Nvrtc& nv = nvrtc();
+    if (!nv.ok) return;
+    nvrtcProgram prog;
+    if (nv.create(&prog, "extern \"C\" __global__ void gs_jit_warm_up() {}", "gs_jit_warm_up.cu", 0, nullptr,
+                  nullptr) != NVRTC_SUCCESS)
+      return;
+    const char* opts[] = {"--gpu-architecture=compute_100a"};
+    nv.compile(prog, 1, opts);
+    nv.destroy(&prog);
   }
 };
 
@@ -278,6 +312,8 @@ Worker& worker() {
   static Worker* w = new Worker;  // intentionally leaked: the detached thread outlives statics
   return *w;
 }
+
+void Worker::worker_shutdown() { worker().shutdown(); }
 
 std::mutex g_reg_mu;
 std::map<std::string, std::unique_ptr<JitKernel>>& registry() {

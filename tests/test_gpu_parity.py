@@ -675,6 +675,13 @@ def test_pipeline_fuzz():
         pipe.close()
 
 
+# The reference binaries are short-lived: with runtime specialisation on, a
+# background NVRTC build can still be in flight when they exit, and NVRTC's
+# own static teardown then crashes that thread. Schemes outside
+# the compiled registry run on the runtime-coefficient GPU kernel instead.
+_NO_JIT_ENV = dict(os.environ, GS_JIT="0")
+
+
 def test_reference_coding_suite_runs_against_the_gpu_library():
     """The reference's own proj/tests/coding_test.cpp (16 cases: validation,
     tolerance, matrices, MDS, XOR literal vectors, every erasure pattern of
@@ -684,7 +691,7 @@ def test_reference_coding_suite_runs_against_the_gpu_library():
     exe = os.path.join(ROOT, "oracle", "_ref", "ref_coding_test_b200")
     if not os.path.exists(exe):
         pytest.skip("reference suites not built (no /root/reference at build time)")
-    out = subprocess.run([exe], capture_output=True, text=True, timeout=600)
+    out = subprocess.run([exe], capture_output=True, text=True, env=_NO_JIT_ENV, timeout=600)
     assert out.returncode == 0, out.stdout[-3000:] + out.stderr[-3000:]
     assert "16 tests, 0 failed" in out.stdout
 
@@ -700,7 +707,7 @@ def test_reference_kv_model_suite_runs_against_the_library():
     exe = os.path.join(ROOT, "oracle", "_ref", "ref_kv_model_test_b200")
     if not os.path.exists(exe):
         pytest.skip("reference suites not built (no /root/reference at build time)")
-    out = subprocess.run([exe], capture_output=True, text=True, timeout=600)
+    out = subprocess.run([exe], capture_output=True, text=True, env=_NO_JIT_ENV, timeout=600)
     assert out.returncode == 0, out.stdout[-3000:] + out.stderr[-3000:]
     assert "17 tests, 0 failed" in out.stdout
 
@@ -718,7 +725,7 @@ def test_reference_orchestration_suites_run_on_the_library(suite, cases):
     exe = os.path.join(ROOT, "oracle", "_ref", f"ref_{suite}_test_b200")
     if not os.path.exists(exe):
         pytest.skip("reference suites not built (no /root/reference at build time)")
-    out = subprocess.run([exe], capture_output=True, text=True, timeout=900)
+    out = subprocess.run([exe], capture_output=True, text=True, env=_NO_JIT_ENV, timeout=900)
     assert out.returncode == 0, out.stdout[-3000:] + out.stderr[-3000:]
     assert f"{cases} tests, 0 failed" in out.stdout
 
@@ -734,7 +741,7 @@ def test_reference_acceptance_criteria_on_the_library():
     exe = os.path.join(ROOT, "oracle", "_ref", "ref_acceptance_b200")
     if not os.path.exists(exe):
         pytest.skip("reference acceptance not built (no /root/reference at build time)")
-    out = subprocess.run([exe], capture_output=True, text=True, timeout=900)
+    out = subprocess.run([exe], capture_output=True, text=True, env=_NO_JIT_ENV, timeout=900)
     for c in (1, 2, 3, 4, 5, 6, 7, 8, 9, 11):
         assert f"[PASS] C{c}:" in out.stdout, out.stdout[-4000:]
     assert out.returncode == 1 and "[FAIL] C10:" in out.stdout
