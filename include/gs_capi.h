@@ -58,6 +58,10 @@ typedef struct gs_verify gs_verify;     /* an in-flight split parity verificatio
 const char* gs_status_string(int status);
 const char* gs_last_error(void);
 int gs_abi_version(void);
+/* Drop queued runtime-specialisation (NVRTC) builds and wait for the one in
+ * flight. Call before a process exits (the Python package does, atexit): a
+ * build still running while NVRTC's statics are destroyed can crash. */
+int gs_jit_quiesce(void);
 /* Number of kernels this library launched in this process (all devices). */
 uint64_t gs_kernel_launches(void);
 /* 1 if a CUDA device is usable from this process. */

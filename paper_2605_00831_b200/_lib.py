@@ -28,6 +28,7 @@ SIGNATURES = {
     "gs_status_string": (C.c_char_p, [_i]),
     "gs_last_error": (C.c_char_p, []),
     "gs_abi_version": (_i, []),
+    "gs_jit_quiesce": (_i, []),
     "gs_kernel_launches": (_u64, []),
     "gs_cuda_available": (_i, []),
     "gs_gf_mul": (_u8, [_u8, _u8]),
@@ -135,6 +136,10 @@ def lib() -> C.CDLL:
                 fn.restype = res
                 fn.argtypes = args
             _lib = handle
+            # Python's atexit runs before the C++ static teardown: no NVRTC build
+            # may still be running then (gs_jit_quiesce).
+            import atexit
+            atexit.register(handle.gs_jit_quiesce)
     return _lib
 
 

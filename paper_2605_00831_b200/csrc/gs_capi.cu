@@ -987,6 +987,11 @@ const char* gs_status_string(int status) {
 }
 const char* gs_last_error(void) { return g_err.c_str(); }
 int gs_abi_version(void) { return 1; }
+
+int gs_jit_quiesce(void) {
+  gsb::jit_quiesce();
+  return GS_OK;
+}
 uint64_t gs_kernel_launches(void) { return g_launches.load(); }
 int gs_cuda_available(void) {
   int n = 0;

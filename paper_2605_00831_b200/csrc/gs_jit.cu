@@ -287,6 +287,13 @@ struct Worker {
       idle_cv.notify_all();
     }
   }
+  // drop queued builds (they stay pending: callers keep the generic kernel)
+  // and wait for the one in flight; the worker keeps serving later requests
+  void quiesce() {
+    std::unique_lock<std::mutex> lk(mu);
+    q.clear();
+    idle_cv.wait(lk, [&] { return !busy; });
+  }
   // at exit: no new compiles; wait for the one in flight
   void shutdown() {
     std::unique_lock<std::mutex> lk(mu);
@@ -314,6 +321,12 @@ Worker& worker() {
 }
 
 void Worker::worker_shutdown() { worker().shutdown(); }
+
+}  // namespace
+
+void jit_quiesce() { worker().quiesce(); }
+
+namespace {
 
 std::mutex g_reg_mu;
 std::map<std::string, std::unique_ptr<JitKernel>>& registry() {

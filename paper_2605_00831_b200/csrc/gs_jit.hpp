@@ -36,6 +36,9 @@ cudaError_t jit_launch(JitKernel* k, const void* const* ptrs, int count, const T
 // Blocks per SM of the loaded kernel on the current device (0 if not loaded).
 int jit_occupancy(JitKernel* k);
 void jit_set_enabled(bool on);
+// Drop queued builds and wait for the one in flight (call before process
+// exit: NVRTC must not be compiling while its statics are torn down).
+void jit_quiesce();
 const char* jit_last_log(JitKernel* k);
 
 }  // namespace gsb
