@@ -112,13 +112,47 @@ __device__ __forceinline__ int load_groups(const FnvJob& j, uint32_t c, uint64_t
 
 __device__ __forceinline__ uint32_t& wd(uint4& v, int w) { return w == 0 ? v.x : w == 1 ? v.y : w == 2 ? v.z : v.w; }
 
-// Round K: bit K of every low byte, relative to the block's entry bit K.
+// e bits of bit K for the 4 positions of one word (byte j -> nibble bit j):
+// e = b_K ^ bit_K(((s ^ b) mod 2^K) * 0xB3), s_true holding the true bits < K.
 template <int K>
-__global__ void __launch_bounds__(kFT) k_fnv_round(const FnvJob j, uint8_t* __restrict__ scratch,
-                                                   uint8_t* __restrict__ agg, const uint8_t* __restrict__ entry) {
-  __shared__ uint32_t wpar[kFT / 32];
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+__device__ __forceinline__ uint32_t e_nibble(uint32_t s_true, uint32_t bw) {
   constexpr uint32_t kMask = ((1u << K) - 1u) * 0x01010101u;
+  const uint32_t x = (s_true ^ bw) & kMask;
+  const uint32_t lo = (x & 0x00FF00FFu) * 0xB3u;         // bytes 0, 2 in 16-bit lanes
+  const uint32_t hi = ((x >> 8) & 0x00FF00FFu) * 0xB3u;  // bytes 1, 3
+  const uint32_t t = ((lo >> K) & 0x00010001u) | (((hi >> K) & 0x00010001u) << 8);
+  const uint32_t e = t ^ ((bw >> K) & 0x01010101u);
+  return ((e * 0x01020408u) >> 24) & 0xFu;
+}
+__device__ __forceinline__ uint32_t spread_nibble(uint32_t nib) { return (nib * 0x00204081u) & 0x01010101u; }
+
+// exclusive XOR prefix of a thread's 64 e-bits (position order)
+__device__ __forceinline__ uint64_t exclusive_xor(uint64_t e, uint32_t& parity) {
+  e ^= e << 1;
+  e ^= e << 2;
+  e ^= e << 4;
+  e ^= e << 8;
+  e ^= e << 16;
+  e ^= e << 32;
+  parity = static_cast<uint32_t>(e >> 63);
+  return e << 1;
+}
+
+// Rounds K and K+1 (K even) in one pass. Bit K as before (relative to the
+// block's entry bit K). Bit K+1 depends on the TRUE bit K = rel_K ^ entry_K,
+// and entry_K is only known after the global scan -- so it is evaluated for
+// both values of entry_K: the h = 0 trajectory goes into the scratch byte
+// (bit K+1), its XOR with the h = 1 trajectory into a 1-bit-per-position
+// plane D, and both block aggregates into agg (bits 1, 2). The next pass (or
+// the final one) selects with entry_K and folds D back in. Halves the data
+// passes of the one-bit-per-round form.
+template <int K>
+__global__ void __launch_bounds__(kFT) k_fnv_pair(const FnvJob j, uint8_t* __restrict__ scratch,
+                                                  uint64_t* __restrict__ dplane, uint8_t* __restrict__ agg,
+                                                  const uint8_t* __restrict__ entry) {
+  __shared__ uint32_t wpar[3][kFT / 32];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const uint32_t lt = (1u << lane) - 1u;
   for (uint32_t blk = blockIdx.x; blk < j.nblocks; blk += gridDim.x) {
     const uint32_t c = blk / j.bpc, b = blk - c * j.bpc;
     const uint64_t pos0 = static_cast<uint64_t>(b) * kFB + static_cast<uint64_t>(tid) * kFPer;
@@ -126,83 +160,128 @@ __global__ void __launch_bounds__(kFT) k_fnv_round(const FnvJob j, uint8_t* __re
     const int nvalid = load_groups(j, c, pos0, d);
     uint4 s[4];
     uint4* sp = reinterpret_cast<uint4*>(scratch + static_cast<uint64_t>(blk) * kFB + tid * kFPer);
+    uint64_t* dp = dplane + static_cast<uint64_t>(blk) * kFT + tid;
+    const uint32_t ent = K > 0 ? entry[blk] : 0u;
 #pragma unroll
     for (int q = 0; q < 4; ++q) s[q] = K > 0 ? sp[q] : make_uint4(0, 0, 0, 0);
-    const uint32_t rep = K > 0 ? entry[blk] * 0x01010101u : 0u;
-    uint64_t e64 = 0;
+    if (K > 0 && ((ent >> (K - 2)) & 1u)) {  // previous pair's bit K-1: take the entry_{K-2} = 1 trajectory
+      const uint64_t dd = *dp;
 #pragma unroll
-    for (int q = 0; q < 4; ++q) {
+      for (int q = 0; q < 4; ++q)
 #pragma unroll
-      for (int w = 0; w < 4; ++w) {
-        const uint32_t bw = wd(d[q], w);
-        const uint32_t x = ((wd(s[q], w) ^ rep) ^ bw) & kMask;  // (s ^ b) mod 2^K, true bits
-        const uint32_t lo = (x & 0x00FF00FFu) * 0xB3u;           // bytes 0, 2 in 16-bit lanes
-        const uint32_t hi = ((x >> 8) & 0x00FF00FFu) * 0xB3u;    // bytes 1, 3
-        const uint32_t t = ((lo >> K) & 0x00010001u) | (((hi >> K) & 0x00010001u) << 8);
-        const uint32_t e = t ^ ((bw >> K) & 0x01010101u);
-        const uint32_t nib = ((e * 0x01020408u) >> 24) & 0xFu;  // byte j -> bit j
-        if (q < nvalid) e64 |= static_cast<uint64_t>(nib) << (16 * q + 4 * w);
-      }
+        for (int w = 0; w < 4; ++w)
+          wd(s[q], w) ^= spread_nibble(static_cast<uint32_t>(dd >> (16 * q + 4 * w)) & 0xFu) << (K - 1);
     }
-    // exclusive XOR prefix: within the thread, then across the block
-    uint64_t inc = e64;
-    inc ^= inc << 1;
-    inc ^= inc << 2;
-    inc ^= inc << 4;
-    inc ^= inc << 8;
-    inc ^= inc << 16;
-    inc ^= inc << 32;
-    const uint32_t par = static_cast<uint32_t>(inc >> 63);
-    uint64_t exc = inc << 1;
-    const uint32_t bal = __ballot_sync(0xFFFFFFFFu, par);
-    uint32_t carry = __popc(bal & ((1u << lane) - 1u)) & 1u;
-    if (lane == 0) wpar[warp] = __popc(bal) & 1u;
+    const uint32_t rep = ent * 0x01010101u;  // entry bits < K
+    // ---- bit K ----
+    uint64_t eK = 0;
+#pragma unroll
+    for (int q = 0; q < 4; ++q)
+#pragma unroll
+      for (int w = 0; w < 4; ++w)
+        if (q < nvalid) eK |= static_cast<uint64_t>(e_nibble<K>(wd(s[q], w) ^ rep, wd(d[q], w))) << (16 * q + 4 * w);
+    uint32_t parK;
+    uint64_t relK = exclusive_xor(eK, parK);
+    uint32_t bal = __ballot_sync(0xFFFFFFFFu, parK);
+    uint32_t carry = __popc(bal & lt) & 1u;
+    if (lane == 0) wpar[0][warp] = __popc(bal) & 1u;
     __syncthreads();
-    uint32_t tot = 0;
+    uint32_t totK = 0;
 #pragma unroll
     for (int w = 0; w < kFT / 32; ++w) {
-      if (w < warp) carry ^= wpar[w];
-      tot ^= wpar[w];
+      if (w < warp) carry ^= wpar[0][w];
+      totK ^= wpar[0][w];
     }
-    if (carry) exc = ~exc;
-    if (tid == 0) agg[blk] = static_cast<uint8_t>(tot);
+    if (carry) relK = ~relK;
+    // ---- bit K+1 under entry_K = 0 and entry_K = 1 ----
+    uint64_t e0 = 0, e1 = 0;
+#pragma unroll
+    for (int q = 0; q < 4; ++q)
+#pragma unroll
+      for (int w = 0; w < 4; ++w) {
+        const uint32_t sh = 16 * q + 4 * w;
+        const uint32_t rk = spread_nibble(static_cast<uint32_t>(relK >> sh) & 0xFu) << K;
+        const uint32_t base = wd(s[q], w) ^ rep;
+        if (q < nvalid) {
+          e0 |= static_cast<uint64_t>(e_nibble<K + 1>(base | rk, wd(d[q], w))) << sh;
+          e1 |= static_cast<uint64_t>(e_nibble<K + 1>(base | (rk ^ (0x01010101u << K)), wd(d[q], w))) << sh;
+        }
+      }
+    uint32_t par0, par1;
+    uint64_t r0 = exclusive_xor(e0, par0), r1 = exclusive_xor(e1, par1);
+    const uint32_t b0 = __ballot_sync(0xFFFFFFFFu, par0), b1 = __ballot_sync(0xFFFFFFFFu, par1);
+    uint32_t c0 = __popc(b0 & lt) & 1u, c1 = __popc(b1 & lt) & 1u;
+    if (lane == 0) {
+      wpar[1][warp] = __popc(b0) & 1u;
+      wpar[2][warp] = __popc(b1) & 1u;
+    }
+    __syncthreads();
+    uint32_t t0 = 0, t1 = 0;
+#pragma unroll
+    for (int w = 0; w < kFT / 32; ++w) {
+      if (w < warp) {
+        c0 ^= wpar[1][w];
+        c1 ^= wpar[2][w];
+      }
+      t0 ^= wpar[1][w];
+      t1 ^= wpar[2][w];
+    }
+    if (c0) r0 = ~r0;
+    if (c1) r1 = ~r1;
+    if (tid == 0) agg[blk] = static_cast<uint8_t>(totK | (t0 << 1) | (t1 << 2));
 #pragma unroll
     for (int q = 0; q < 4; ++q) {
 #pragma unroll
       for (int w = 0; w < 4; ++w) {
-        const uint32_t nib = static_cast<uint32_t>(exc >> (16 * q + 4 * w)) & 0xFu;
-        wd(s[q], w) |= ((nib * 0x00204081u) & 0x01010101u) << K;  // bit j -> byte j
+        const uint32_t sh = 16 * q + 4 * w;
+        wd(s[q], w) |= (spread_nibble(static_cast<uint32_t>(relK >> sh) & 0xFu) << K) |
+                       (spread_nibble(static_cast<uint32_t>(r0 >> sh) & 0xFu) << (K + 1));
       }
       sp[q] = s[q];
     }
+    *dp = r0 ^ r1;
     __syncthreads();  // wpar reuse
   }
 }
 
-// entry bit K of every block of chain blockIdx.x: bit K of h0 ^ XOR of the
-// aggregates of the chain's earlier blocks.
+// entry bits K and K+1 of every block of chain blockIdx.x: bit K = bit K of
+// h0 ^ XOR of earlier blocks' aggregates; bit K+1 likewise over the
+// aggregates of the trajectory each block's entry bit K selects.
 template <int K>
-__global__ void __launch_bounds__(1024) k_fnv_scan(const uint8_t* __restrict__ agg, uint8_t* __restrict__ entry,
-                                                   uint32_t bpc, uint64_t h0) {
+__global__ void __launch_bounds__(1024) k_fnv_scan2(const uint8_t* __restrict__ agg, uint8_t* __restrict__ entry,
+                                                    uint32_t bpc, uint64_t h0) {
   __shared__ uint32_t wpar[32];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const uint64_t base = static_cast<uint64_t>(blockIdx.x) * bpc;
   const uint32_t per = (bpc + blockDim.x - 1) / blockDim.x;
-  const uint32_t b0 = std::min<uint32_t>(bpc, tid * per), b1 = std::min<uint32_t>(bpc, b0 + per);
+  const uint32_t b0 = min(bpc, tid * per), b1 = min(bpc, b0 + per);
+  auto block_exclusive = [&](uint32_t par) -> uint32_t {
+    const uint32_t bal = __ballot_sync(0xFFFFFFFFu, par);
+    uint32_t pre = __popc(bal & ((1u << lane) - 1u)) & 1u;
+    if (lane == 0) wpar[warp] = __popc(bal) & 1u;
+    __syncthreads();
+    for (int w = 0; w < warp; ++w) pre ^= wpar[w];
+    __syncthreads();
+    return pre;
+  };
   uint32_t par = 0;
-  for (uint32_t b = b0; b < b1; ++b) par ^= agg[base + b];
-  const uint32_t bal = __ballot_sync(0xFFFFFFFFu, par);
-  uint32_t pre = __popc(bal & ((1u << lane) - 1u)) & 1u;
-  if (lane == 0) wpar[warp] = __popc(bal) & 1u;
-  __syncthreads();
-  for (int w = 0; w < warp; ++w) pre ^= wpar[w];
-  pre ^= static_cast<uint32_t>(h0 >> K) & 1u;
+  for (uint32_t b = b0; b < b1; ++b) par ^= agg[base + b] & 1u;
+  uint32_t preK = block_exclusive(par) ^ (static_cast<uint32_t>(h0 >> K) & 1u);
+  // bit K+1 aggregates under each block's now-known entry bit K
+  uint32_t p1 = 0, ek = preK;
   for (uint32_t b = b0; b < b1; ++b) {
-    if (K == 0)
-      entry[base + b] = static_cast<uint8_t>(pre);
-    else
-      entry[base + b] |= static_cast<uint8_t>(pre << K);
-    pre ^= agg[base + b];
+    const uint32_t a = agg[base + b];
+    p1 ^= (a >> (ek ? 2 : 1)) & 1u;
+    ek ^= a & 1u;
+  }
+  uint32_t preK1 = block_exclusive(p1) ^ (static_cast<uint32_t>(h0 >> (K + 1)) & 1u);
+  ek = preK;
+  for (uint32_t b = b0; b < b1; ++b) {
+    const uint32_t a = agg[base + b];
+    const uint8_t bits = static_cast<uint8_t>((ek << K) | (preK1 << (K + 1)));
+    entry[base + b] = K == 0 ? bits : static_cast<uint8_t>(entry[base + b] | bits);
+    preK1 ^= (a >> (ek ? 2 : 1)) & 1u;
+    ek ^= a & 1u;
   }
 }
 
@@ -213,6 +292,7 @@ __global__ void k_fnv_init(uint64_t* out, int n_chains, uint64_t h0, uint64_t n)
 
 // out[c] += sum over the chain's bytes of d_i * P^(N - i), d_i = (s_i ^ b_i) - s_i.
 __global__ void __launch_bounds__(kFT) k_fnv_final(const FnvJob j, const uint8_t* __restrict__ scratch,
+                                                   const uint64_t* __restrict__ dplane,
                                                    const uint8_t* __restrict__ entry,
                                                    unsigned long long* __restrict__ out) {
   __shared__ uint64_t pw[kFT];  // P^(64 t)
@@ -230,7 +310,9 @@ __global__ void __launch_bounds__(kFT) k_fnv_final(const FnvJob j, const uint8_t
     uint4 d[4];
     const int nvalid = load_groups(j, c, pos0, d);
     const uint4* sp = reinterpret_cast<const uint4*>(scratch + static_cast<uint64_t>(blk) * kFB + tid * kFPer);
-    const uint32_t rep = entry[blk] * 0x01010101u;
+    const uint32_t ent = entry[blk];
+    const uint32_t rep = ent * 0x01010101u;
+    const uint64_t dd = (ent >> 6) & 1u ? dplane[static_cast<uint64_t>(blk) * kFT + tid] : 0;  // bit 7's trajectory
     uint64_t acc = 0;
 #pragma unroll
     for (int q = 0; q < 4; ++q) {
@@ -238,7 +320,8 @@ __global__ void __launch_bounds__(kFT) k_fnv_final(const FnvJob j, const uint8_t
         uint4 s = sp[q];
 #pragma unroll
         for (int w = 0; w < 4; ++w) {
-          const uint32_t sw = wd(s, w) ^ rep, xw = sw ^ wd(d[q], w);
+          const uint32_t sw = wd(s, w) ^ rep ^ (spread_nibble(static_cast<uint32_t>(dd >> (16 * q + 4 * w)) & 0xFu) << 7),
+                         xw = sw ^ wd(d[q], w);
 #pragma unroll
           for (int by = 0; by < 4; ++by) {
             const int64_t dd = static_cast<int64_t>((xw >> (8 * by)) & 0xFFu) -
@@ -269,10 +352,10 @@ __global__ void __launch_bounds__(kFT) k_fnv_final(const FnvJob j, const uint8_t
 }
 
 template <int K>
-cudaError_t round_and_scan(const FnvJob& j, int grid, int n_chains, uint8_t* scratch, uint8_t* agg, uint8_t* entry,
-                           uint64_t h0, cudaStream_t st) {
-  k_fnv_round<K><<<grid, kFT, 0, st>>>(j, scratch, agg, entry);
-  k_fnv_scan<K><<<n_chains, 1024, 0, st>>>(agg, entry, j.bpc, h0);
+cudaError_t pair_and_scan(const FnvJob& j, int grid, int n_chains, uint8_t* scratch, uint64_t* dplane, uint8_t* agg,
+                          uint8_t* entry, uint64_t h0, cudaStream_t st) {
+  k_fnv_pair<K><<<grid, kFT, 0, st>>>(j, scratch, dplane, agg, entry);
+  k_fnv_scan2<K><<<n_chains, 1024, 0, st>>>(agg, entry, j.bpc, h0);
   return cudaGetLastError();
 }
 
@@ -319,12 +402,15 @@ extern "C" int gs_fnv1a64_device(const void* const* bufs, int n_chains, int k, u
   const uint64_t chain_scratch = bpc64 * kFB;
   int per_job = static_cast<int>(std::max<uint64_t>(1, std::min<uint64_t>(kScratchBudget / chain_scratch, kFCap / k)));
   per_job = std::min(per_job, n_chains);
-  const size_t scratch_bytes = static_cast<size_t>(per_job) * chain_scratch;
+  const size_t scratch_bytes = static_cast<size_t>(per_job) * chain_scratch;  // low bytes, then D planes (1/8)
+  const size_t dplane_bytes = scratch_bytes / 8;
   const size_t meta = static_cast<size_t>(per_job) * bpc;
   uint8_t* mem = nullptr;
-  if ((e = cudaMallocAsync(reinterpret_cast<void**>(&mem), scratch_bytes + 2 * meta, st)) != cudaSuccess)
-    return ffail(GS_CUDA_ERROR, "fnv scratch (%zu bytes): %s", scratch_bytes + 2 * meta, cudaGetErrorString(e));
-  uint8_t* agg = mem + scratch_bytes;
+  if ((e = cudaMallocAsync(reinterpret_cast<void**>(&mem), scratch_bytes + dplane_bytes + 2 * meta, st)) != cudaSuccess)
+    return ffail(GS_CUDA_ERROR, "fnv scratch (%zu bytes): %s", scratch_bytes + dplane_bytes + 2 * meta,
+                 cudaGetErrorString(e));
+  uint64_t* dplane = reinterpret_cast<uint64_t*>(mem + scratch_bytes);
+  uint8_t* agg = mem + scratch_bytes + dplane_bytes;
   uint8_t* entry = agg + meta;
   int status = GS_OK;
   for (int c0 = 0; c0 < n_chains && status == GS_OK; c0 += per_job) {
@@ -337,16 +423,12 @@ extern "C" int gs_fnv1a64_device(const void* const* bufs, int n_chains, int k, u
     j.bpc = bpc;
     j.nblocks = static_cast<uint32_t>(static_cast<uint64_t>(cnt) * bpc);
     const int grid = static_cast<int>(std::min<uint64_t>(j.nblocks, static_cast<uint64_t>(g_sms > 0 ? g_sms : 148) * 4));
-    cudaError_t r = round_and_scan<0>(j, grid, cnt, mem, agg, entry, h0, st);
-    if (r == cudaSuccess) r = round_and_scan<1>(j, grid, cnt, mem, agg, entry, h0, st);
-    if (r == cudaSuccess) r = round_and_scan<2>(j, grid, cnt, mem, agg, entry, h0, st);
-    if (r == cudaSuccess) r = round_and_scan<3>(j, grid, cnt, mem, agg, entry, h0, st);
-    if (r == cudaSuccess) r = round_and_scan<4>(j, grid, cnt, mem, agg, entry, h0, st);
-    if (r == cudaSuccess) r = round_and_scan<5>(j, grid, cnt, mem, agg, entry, h0, st);
-    if (r == cudaSuccess) r = round_and_scan<6>(j, grid, cnt, mem, agg, entry, h0, st);
-    if (r == cudaSuccess) r = round_and_scan<7>(j, grid, cnt, mem, agg, entry, h0, st);
+    cudaError_t r = pair_and_scan<0>(j, grid, cnt, mem, dplane, agg, entry, h0, st);
+    if (r == cudaSuccess) r = pair_and_scan<2>(j, grid, cnt, mem, dplane, agg, entry, h0, st);
+    if (r == cudaSuccess) r = pair_and_scan<4>(j, grid, cnt, mem, dplane, agg, entry, h0, st);
+    if (r == cudaSuccess) r = pair_and_scan<6>(j, grid, cnt, mem, dplane, agg, entry, h0, st);
     if (r == cudaSuccess) {
-      k_fnv_final<<<grid, kFT, 0, st>>>(j, mem, entry, reinterpret_cast<unsigned long long*>(d_out) + c0);
+      k_fnv_final<<<grid, kFT, 0, st>>>(j, mem, dplane, entry, reinterpret_cast<unsigned long long*>(d_out) + c0);
       r = cudaGetLastError();
     }
     if (r != cudaSuccess) status = ffail(GS_CUDA_ERROR, "fnv kernels: %s", cudaGetErrorString(r));
