@@ -16,16 +16,17 @@
 //        s'_k = s_k ^ b_k ^ bit_k(((s ^ b) mod 2^k) * 0xB3)
 //    (0xB3 is odd, so x_k * 2^k * 0xB3 adds exactly x_k at bit k). Once bits
 //    < k of every s_i are known, bit k is an XOR prefix scan of
-//    e_i = b_k ^ bit_k(...). Eight rounds (k = 0..7) of "map + XOR scan"
-//    recover every s_i without a serial chain (k_fnv_round + k_fnv_scan).
+//    e_i = b_k ^ bit_k(...). Four passes of "map + XOR scan", two bits each
+//    (k_fnv_pair + k_fnv_scan2), recover every s_i without a serial chain.
 //
 // Layout: a chain is the concatenation of k buffers of `len` bytes (the
 // parity buffers of one chunk, chained in order as ParityChunk::
 // compute_checksum does, parity_store.hpp:46-50). Blocks of 16 KiB (256
-// threads x 64 contiguous bytes). Between rounds the low bytes are kept in a
-// scratch byte array, RELATIVE to each block's entry state (so a round never
-// waits for the global scan of its own bit); the per-block entry bytes come
-// from k_fnv_scan, one CTA per chain.
+// threads x 64 contiguous bytes). Between passes the low bytes are kept in a
+// scratch byte array, RELATIVE to each block's entry state (so a pass never
+// waits for the global scan of its own bits), plus a 1-bit plane for the
+// second bit's other hypothesis; the per-block entry bytes come from
+// k_fnv_scan2, one CTA per chain.
 #include <cuda_runtime.h>
 
 #include <algorithm>
