@@ -119,11 +119,19 @@ template <int K>
 __device__ __forceinline__ uint32_t e_nibble(uint32_t s_true, uint32_t bw) {
   constexpr uint32_t kMask = ((1u << K) - 1u) * 0x01010101u;
   const uint32_t x = (s_true ^ bw) & kMask;
-  const uint32_t lo = (x & 0x00FF00FFu) * 0xB3u;         // bytes 0, 2 in 16-bit lanes
-  const uint32_t hi = ((x >> 8) & 0x00FF00FFu) * 0xB3u;  // bytes 1, 3
-  const uint32_t t = ((lo >> K) & 0x00010001u) | (((hi >> K) & 0x00010001u) << 8);
-  const uint32_t e = t ^ ((bw >> K) & 0x01010101u);
-  return ((e * 0x01020408u) >> 24) & 0xFu;
+  uint32_t e;
+  if constexpr (K <= 3) {
+    // bit K of x*0xB3 only needs x * (0xB3 mod 2^(K+1)) < 2^(2K+1) <= 2^7: the
+    // four byte lanes multiply in ONE IMAD without spilling into each other
+    constexpr uint32_t c = 0xB3u & ((2u << K) - 1u);
+    e = ((x * c) ^ bw) >> K & 0x01010101u;
+  } else {
+    const uint32_t lo = (x & 0x00FF00FFu) * 0xB3u;         // bytes 0, 2 in 16-bit lanes
+    const uint32_t hi = ((x >> 8) & 0x00FF00FFu) * 0xB3u;  // bytes 1, 3
+    const uint32_t t = ((lo >> K) & 0x00010001u) | (((hi >> K) & 0x00010001u) << 8);
+    e = t ^ ((bw >> K) & 0x01010101u);
+  }
+  return (e * 0x01020408u) >> 24;  // byte j's bit -> bit j (no other term lands in bits 28..31)
 }
 __device__ __forceinline__ uint32_t spread_nibble(uint32_t nib) { return (nib * 0x00204081u) & 0x01010101u; }
 
