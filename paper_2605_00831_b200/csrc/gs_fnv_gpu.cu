@@ -322,7 +322,8 @@ __global__ void __launch_bounds__(kFT) k_fnv_final(const FnvJob j, const uint8_t
     const uint32_t ent = entry[blk];
     const uint32_t rep = ent * 0x01010101u;
     const uint64_t dd = (ent >> 6) & 1u ? dplane[static_cast<uint64_t>(blk) * kFT + tid] : 0;  // bit 7's trajectory
-    uint64_t acc = 0;
+    // four independent 16-byte Horner chains (ILP), joined with P^16
+    uint64_t accq[4] = {0, 0, 0, 0};
 #pragma unroll
     for (int q = 0; q < 4; ++q) {
       if (q < nvalid) {
@@ -333,13 +334,22 @@ __global__ void __launch_bounds__(kFT) k_fnv_final(const FnvJob j, const uint8_t
                          xw = sw ^ wd(d[q], w);
 #pragma unroll
           for (int by = 0; by < 4; ++by) {
-            const int64_t dd = static_cast<int64_t>((xw >> (8 * by)) & 0xFFu) -
+            const int64_t di = static_cast<int64_t>((xw >> (8 * by)) & 0xFFu) -
                                static_cast<int64_t>((sw >> (8 * by)) & 0xFFu);
-            acc = (acc + static_cast<uint64_t>(dd)) * kFnvP;
+            accq[q] = (accq[q] + static_cast<uint64_t>(di)) * kFnvP;
           }
         }
       }
     }
+    constexpr uint64_t kP16 = [] {
+      uint64_t r = 1;
+      for (int i = 0; i < 16; ++i) r *= kFnvP;
+      return r;
+    }();
+    uint64_t acc = 0;
+#pragma unroll
+    for (int q = 0; q < 4; ++q)
+      if (q < nvalid) acc = acc * kP16 + accq[q];
     __syncthreads();  // pblk visible
     uint64_t contrib = 0;
     if (nvalid > 0) {
