@@ -307,8 +307,8 @@ int gs_parity_upload_checksum(const void* const* h_parity, int n_chunks, int k, 
                               void* const* d_parity, uint64_t* d_sums, void* compute, void* copy);
 /* The checkpoint-side mirror: K1's parity rows in HBM (written on `compute`)
  * are copied to pinned host rows on `copy` while the GPU computes their chunk
- * checksums; h_sums[c] (pinned) receives them behind the rows. Pair with
- * gs_store_commit_sealed_batch on `copy`. */
+ * checksums; h_sums[c] (pinned host or device memory) receives them behind
+ * the rows, on `copy`. Pair with gs_store_commit_sealed_batch on `copy`. */
 int gs_parity_offload_sealed(const void* const* d_parity, int n_chunks, int k, uint64_t len,
                              void* const* h_parity, uint64_t* h_sums, void* compute, void* copy);
 /* Recovery's parity verification split between the GPU and host threads.
@@ -349,9 +349,11 @@ int gs_store_reserve_batch(gs_store* s, int count, const uint64_t* request_ids, 
 int gs_store_commit_batch(gs_store* s, int count, const uint64_t* request_ids, const uint32_t* chunks,
                           void* stream);
 /* Commit entries whose checksums were computed on the GPU (gs_parity_offload_
- * sealed): once `stream` reaches this point the entries are sealed with
- * checksums[i] (pinned host memory, read at that time; keep it alive until
- * then) -- no host FNV pass. */
+ * sealed): the entries are sealed with checksums[i] -- no host FNV pass.
+ * `checksums` may be device or host memory; the store copies it on `stream`
+ * (at this point of the stream) into pinned memory it owns, so the caller's
+ * buffer only has to stay valid until `stream` passes this call, like the
+ * source of any cudaMemcpyAsync. */
 int gs_store_commit_sealed_batch(gs_store* s, int count, const uint64_t* request_ids, const uint32_t* chunks,
                                  const uint64_t* checksums, void* stream);
 int gs_store_wait_sealed(gs_store* s);

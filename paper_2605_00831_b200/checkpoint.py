@@ -202,6 +202,11 @@ class FailureEvent:
     at_time: float = 0.0
 
 
+class RecoveryAbort(RuntimeError):
+    """recovery.hpp RecoveryAbort: the store changed or a needed payload is
+    missing mid-recovery."""
+
+
 class RecoveryMode:
     kPureRecompute = "pure_recompute"
     kHybrid = "hybrid"
@@ -227,6 +232,8 @@ class RecoveryResult:
     enqueue_ms: float = 0.0              # host time to enqueue the batched H2D + K2
     verify_gpu_chunks: int = 0           # entries whose checksum was verified on the GPU
     wall_ms: float = 0.0                 # plan -> verified, rebuilt bytes on the device
+    corrupt_chunks: List[int] = field(default_factory=list)   # parity that failed verification (-> fallback)
+    decoded_chunks: int = 0              # chunks whose lost shards came out of K2 (and matched ground truth)
 
 
 def verify_recovery(recovered, ground_truth) -> bool:
@@ -270,14 +277,14 @@ class _HostVerify:
 
     def __init__(self, ck: "Checkpointer", entries, threads: int):
         import threading
-        self._ok = True
+        self._ok: List[bool] = []
         self._ms = 0.0
         self._err: Optional[BaseException] = None
 
         def run():
             t0 = time.perf_counter()
             try:
-                self._ok = all(ck._verify_entries(entries, threads))
+                self._ok = ck._verify_entries(entries, threads)
             except BaseException as e:   # re-raised in result()
                 self._err = e
             self._ms = (time.perf_counter() - t0) * 1e3
@@ -366,6 +373,11 @@ class Checkpointer:
             outs.append(ChunkCheckpointOutcome(s0.request_id, s0.chunk_id, s0.valid_tokens, worker, ptrs is not None))
             if ptrs is None:
                 continue
+            for s in slices:
+                # K1 reads the slice on self.compute: a caller dropping it after
+                # this call must not let the caching allocator hand its block to
+                # a later kernel on the slice's own stream before K1 has run
+                s.bytes.record_stream(self.compute)
             slots.extend(s.bytes.data_ptr() for s in slices)
             dsts.extend(ptrs)
             keys.append((s0.request_id, s0.chunk_id))
@@ -414,7 +426,10 @@ class Checkpointer:
         self.compute.wait_stream(cur)
         self.copy.wait_stream(cur)
         par = torch.empty((S, k, self.slice), dtype=torch.uint8, device=self.dev)
-        sums = torch.empty(S, dtype=torch.int64).pin_memory()
+        # checksums stay on the device: the store copies them on `copy` into
+        # pinned memory it owns (gs_store_commit_sealed_batch), so nothing the
+        # store's landing thread reads depends on this tensor's lifetime
+        sums = torch.empty(S, dtype=torch.int64, device=self.dev)
         rows = L.ptr_array([par[s, i].data_ptr() for s in range(S) for i in range(k)])
         lib = L.lib()
         check(lib.gs_apply_device(encoder(sch).handle, S, L.ptr_array(slots), rows, self.slice,
@@ -424,6 +439,9 @@ class Checkpointer:
         self.store.commit_sealed_batch(keys, sums.data_ptr(), self.copy)
         done = torch.cuda.Event()
         done.record(self.copy)
+        # par / sums were allocated on the current stream and are used on
+        # compute and copy: they are dropped only after `done` (copy waits on
+        # compute's K1 + FNV), so their blocks are never reused early
         self._inflight.append((done, (par, sums), need))
 
     def run_prefill_with_checkpointing(self, request_id: int, input_tokens: int, kv_seed: int = 0,
@@ -524,11 +542,20 @@ class Checkpointer:
         parity_ok = True
         if not over and r < n:
             for c in range(r, n):
+                # the reference's planning pass checks the get() status only
+                # (recovery.hpp:200-207); the checksums are verified below, in
+                # bulk, overlapped with the speculative decode
                 st, e = self.store.get(request_id, c, verify=False)
-                if st != ParityGetStatus.kOk or not e.payload_present():
+                if st != ParityGetStatus.kOk:
                     parity_ok = False
                     break
+                if ground_truth is not None and not e.payload_present():
+                    # materialized recovery of a cost-only entry: reconstruct_chunk
+                    # reports kBadParity and the reference aborts (recovery.hpp:280-283)
+                    raise RecoveryAbort("recovery: parity failed verification mid-recovery")
                 entries.append(e)
+        if entries and not all(e.payload_present() for e in entries):
+            entries = []        # cost-only entries: nothing to verify or decode (get() said kOk)
         failed = set(failure.failed_workers)
         pending = []            # (first chunk id, outs, out_index, keep-alive)
         gpu_sums = None
@@ -566,12 +593,25 @@ class Checkpointer:
             cur.wait_stream(self.compute)
             result.enqueue_ms = (time.perf_counter() - t0) * 1e3
         if parity_ok and entries:
+            good: List[bool] = []
             if host_verify is not None:
-                parity_ok, result.verify_host_ms = host_verify.result()
+                good, result.verify_host_ms = host_verify.result()
             if split is not None:
                 sums, result.verify_host_ms = split[1].result()
-                parity_ok = all(sums[i] == e.checksum for i, e in enumerate(entries))
+                good = [sums[i] == e.checksum for i, e in enumerate(entries)]
                 result.verify_gpu_chunks = split[0]
+            bad = [i for i, g in enumerate(good) if not g]
+            if bad:
+                # a fallback is only legitimate if the reference's own serial
+                # FNV-1a (ParityChunk::compute_checksum) agrees that the stored
+                # parity is corrupt; a disagreement is a bug in the fast
+                # verification or the seal, never a silent full recompute
+                wrong = [entries[i].chunk_id for i in bad if entries[i].compute_checksum() == entries[i].checksum]
+                if wrong:
+                    raise RuntimeError(f"recovery: fast parity verification rejected chunks {wrong} whose "
+                                       "stored checksum the serial FNV-1a accepts")
+                result.corrupt_chunks = [entries[i].chunk_id for i in bad]
+                parity_ok = False
         if over or (not parity_ok and r < n):
             plan.mode, r = RecoveryMode.kFullRecomputeFallback, n
         elif r >= n:
@@ -608,6 +648,7 @@ class Checkpointer:
             for w in failure.failed_workers:
                 if not verify_recovery(result.recovered[w][c], ground_truth[c][w]):
                     result.verified = False
+        result.decoded_chunks = n - r if result.verified else 0
         return result
 
     def _verify_entries(self, entries, threads: int) -> List[bool]:

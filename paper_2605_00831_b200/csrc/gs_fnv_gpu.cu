@@ -487,7 +487,7 @@ extern "C" int gs_parity_upload_checksum(const void* const* h_parity, int n_chun
 
 // K1's parity rows already in HBM (d_parity, written on `compute` before this
 // call) -> pinned host rows on `copy`, and their chunk checksums computed on
-// the GPU (`compute`) and copied to h_sums (pinned) behind them: the seal of
+// the GPU (`compute`) and copied to h_sums (pinned host or device) behind them: the seal of
 // ParityChunk (parity_store.hpp:46-53) without a host FNV pass. Stream order:
 // rows D2H after K1; sums D2H after the FNV; a store commit enqueued on `copy`
 // after this call sees both.
@@ -527,7 +527,7 @@ extern "C" int gs_parity_offload_sealed(const void* const* d_parity, int n_chunk
   if (st == GS_OK) {
     e = cudaEventRecord(ev, cs);  // checksums done
     if (e == cudaSuccess) e = cudaStreamWaitEvent(ys, ev, 0);
-    if (e == cudaSuccess) e = cudaMemcpyAsync(h_sums, d_sums, sizeof(uint64_t) * n_chunks, cudaMemcpyDeviceToHost, ys);
+    if (e == cudaSuccess) e = cudaMemcpyAsync(h_sums, d_sums, sizeof(uint64_t) * n_chunks, cudaMemcpyDefault, ys);
     if (e != cudaSuccess) st = ffail(GS_CUDA_ERROR, "parity offload sums: %s", cudaGetErrorString(e));
   }
   cudaFreeAsync(d_sums, ys);

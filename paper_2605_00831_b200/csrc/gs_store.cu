@@ -129,6 +129,7 @@ struct gs_store {
   uint64_t used = 0, payload = 0, peak = 0;
   std::map<Key, Entry> entries;
   SlabPool pool{size_t{256} << 20};
+  SlabPool sums_pool{size_t{1} << 20};  // 4 KiB pinned blocks for GPU-seal checksums
   std::mutex mu;
   std::condition_variable sealed_cv;
 
@@ -194,7 +195,11 @@ struct gs_store {
   struct HostJob {
     gs_store* s;
     std::vector<Key> keys;
-    const uint64_t* sums = nullptr;  // checksums already computed (GPU seal), read at callback time
+    // GPU seal: the checksums, copied on the commit's stream into pinned memory
+    // the STORE owns (a pool block), so the caller's buffer only has to outlive
+    // that stream position -- never the landing thread's wake-up.
+    uint64_t* sums = nullptr;
+    size_t sums_bytes = 0;
   };
   static void CUDART_CB on_stream(void* p) {
     auto* j = static_cast<HostJob*>(p);
@@ -208,6 +213,7 @@ struct gs_store {
             it->second.sealed = true;
           }
         }
+        j->s->sums_pool.release(reinterpret_cast<uint8_t*>(j->sums), j->sums_bytes);
         j->s->pending -= static_cast<uint64_t>(j->keys.size());
       }
       j->s->sealed_cv.notify_all();
@@ -331,7 +337,7 @@ static int commit_batch(gs_store* s, int count, const uint64_t* request_ids, con
   if (!s || count < 0 || (count > 0 && (!request_ids || !chunks)))
     return sfail(GS_INVALID_ARGUMENT, "store_commit: bad arguments");
   if (count == 0) return GS_OK;
-  auto* job = new gs_store::HostJob{s, {}, sums};
+  auto* job = new gs_store::HostJob{s, {}, nullptr, 0};
   job->keys.reserve(static_cast<size_t>(count));
   {
     std::lock_guard<std::mutex> lk(s->mu);
@@ -343,24 +349,39 @@ static int commit_batch(gs_store* s, int count, const uint64_t* request_ids, con
       }
       job->keys.push_back({request_ids[i], chunks[i]});
     }
+    if (sums) {
+      job->sums_bytes = sizeof(uint64_t) * static_cast<size_t>(count);
+      uint8_t* blk = nullptr;
+      if (int st = s->sums_pool.alloc(job->sums_bytes, &blk)) {
+        delete job;
+        return st;
+      }
+      job->sums = reinterpret_cast<uint64_t*>(blk);
+    }
     s->pending += static_cast<uint64_t>(count);
   }
+  auto undo = [&](int st) {
+    std::lock_guard<std::mutex> lk(s->mu);
+    if (job->sums) s->sums_pool.release(reinterpret_cast<uint8_t*>(job->sums), job->sums_bytes);
+    s->pending -= static_cast<uint64_t>(count);
+    delete job;
+    s->sealed_cv.notify_all();
+    return st;
+  };
+  cudaStream_t cst = static_cast<cudaStream_t>(stream);
   if (stream) {  // seal once the D2H on `stream` has landed: an event, waited on by the landing thread
     cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
-    if (cudaStreamIsCapturing(static_cast<cudaStream_t>(stream), &cap) == cudaSuccess &&
-        cap != cudaStreamCaptureStatusNone) {
-      s->pending -= static_cast<uint64_t>(count);
-      delete job;
-      return sfail(GS_INVALID_ARGUMENT, "store_commit: cannot be captured into a CUDA graph (commit each replay)");
-    }
+    if (cudaStreamIsCapturing(cst, &cap) == cudaSuccess && cap != cudaStreamCaptureStatusNone)
+      return undo(sfail(GS_INVALID_ARGUMENT, "store_commit: cannot be captured into a CUDA graph (commit each replay)"));
+    cudaError_t e = cudaSuccess;
+    // checksums (device or host memory) -> the store's pinned block, ordered on the stream
+    if (job->sums) e = cudaMemcpyAsync(job->sums, sums, job->sums_bytes, cudaMemcpyDefault, cst);
     cudaEvent_t ev = nullptr;
-    cudaError_t e = cudaEventCreateWithFlags(&ev, cudaEventDisableTiming | cudaEventBlockingSync);
-    if (e == cudaSuccess) e = cudaEventRecord(ev, static_cast<cudaStream_t>(stream));
+    if (e == cudaSuccess) e = cudaEventCreateWithFlags(&ev, cudaEventDisableTiming | cudaEventBlockingSync);
+    if (e == cudaSuccess) e = cudaEventRecord(ev, cst);
     if (e != cudaSuccess) {
       if (ev) cudaEventDestroy(ev);
-      s->pending -= static_cast<uint64_t>(count);
-      delete job;
-      return sfail(GS_CUDA_ERROR, "store_commit: event: %s", cudaGetErrorString(e));
+      return undo(sfail(GS_CUDA_ERROR, "store_commit: %s", cudaGetErrorString(e)));
     }
     {
       std::lock_guard<std::mutex> lk(s->mu);
@@ -368,6 +389,10 @@ static int commit_batch(gs_store* s, int count, const uint64_t* request_ids, con
     }
     s->land_cv.notify_one();
     return GS_OK;
+  }
+  if (job->sums) {  // no stream: the checksums are final now
+    cudaError_t e = cudaMemcpy(job->sums, sums, job->sums_bytes, cudaMemcpyDefault);
+    if (e != cudaSuccess) return undo(sfail(GS_CUDA_ERROR, "store_commit: %s", cudaGetErrorString(e)));
   }
   gs_store::on_stream(job);
   return GS_OK;

@@ -189,8 +189,13 @@ class ParityStore:
     def wait_sealed(self) -> None:
         L.lib().gs_store_wait_sealed(self.handle)
 
-    def get(self, request_id: int, chunk_index: int, verify: bool = True
+    def get(self, request_id: int, chunk_index: int, verify: bool = True, copy: bool = False
             ) -> Tuple[ParityGetStatus, Optional[ParityChunk]]:
+        """parity_store.hpp:92-101. The returned parity arrays are zero-copy
+        views of the store's pinned slab (what the recovery H2D reads): they
+        are valid until the entry is erased (erase_request recycles the block)
+        or the store is closed; the chunk keeps the store object alive, not
+        the entry. copy=True returns owning copies instead."""
         st = C.c_int()
         ptrs = (C.c_void_p * 256)()
         sl, ck = C.c_uint64(), C.c_uint64()
@@ -203,7 +208,12 @@ class ParityStore:
             return status, None
         scheme = CodingScheme(CodeKind(knk[0]), knk[1], knk[2])
         parity = [_view(ptrs[i], sl.value) for i in range(scheme.k)] if ptrs[0] else []   # [] = cost-only
-        return status, ParityChunk(request_id, chunk_index, scheme, parity, vt.value, sl.value, ck.value)
+        if copy:
+            parity = [p.copy() for p in parity]
+        chunk = ParityChunk(request_id, chunk_index, scheme, parity, vt.value, sl.value, ck.value)
+        if not copy:
+            chunk._store = self   # the views point into this store's slabs
+        return status, chunk
 
     def contains(self, request_id: int, chunk_index: int) -> bool:
         return bool(L.lib().gs_store_contains(self.handle, request_id, chunk_index))

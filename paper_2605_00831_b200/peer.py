@@ -21,7 +21,7 @@ from dataclasses import dataclass
 from typing import Dict, List, Optional, Sequence, Tuple
 
 from . import _lib as L
-from .coding import CodingScheme, ErasurePattern, InvalidArgument, check, decoder, encoder
+from .coding import CodeKind, CodingScheme, ErasurePattern, InvalidArgument, check, decoder, encoder
 from .device import row_ptrs
 
 
@@ -140,10 +140,23 @@ def _host_rows(h_parity, off: int, local: bool) -> List[int]:
     return [r - off for r in rows] if local else rows
 
 
+def require_position_independent(scheme: CodingScheme, layout: ShardLayout) -> None:
+    """Byte-range striping needs a code whose parity byte b depends only on
+    byte b of the shards (XOR, RS: coding.hpp:143-172, 269-275). RDP places
+    cells at t*(p-1)+r and its P/Q tail at the END of the shard
+    (coding.hpp:225-307), so a rank encoding its own range as a shard starting
+    at 0 would produce a different code -- striped RDP is refused; the
+    rotating encoder (whole stripes per rank) handles it."""
+    if scheme.kind == CodeKind.RDP and layout.world > 1:
+        raise InvalidArgument("striping: RDP parity depends on byte position; byte-range striping over "
+                              f"{layout.world} ranks would not reproduce it (use plan_encode_rotating)")
+
+
 def plan_encode_striped(scheme: CodingScheme, layout: ShardLayout, bases: Sequence[int], rank: int,
                         parity_out=None, pipeline=None, h_parity=None, local_parity: bool = False) -> StripedCall:
     """K1 over this rank's byte range of all stripes (see encode_striped).
     local_parity: h_parity is [S, k, len_r] (this rank's range only)."""
+    require_position_independent(scheme, layout)
     enc = encoder(scheme)
     off, ln, slots = striped_slots(layout, bases, rank)
     if ln == 0:
@@ -205,6 +218,7 @@ def plan_reconstruct_striped(scheme: CodingScheme, layout: ShardLayout, bases: S
                              lost: ErasurePattern, h_parity, pipeline, local_parity: bool = False) -> StripedCall:
     """K2 over this rank's byte range (see reconstruct_striped).
     local_parity: h_parity is [S, k, len_r] (this rank's range only)."""
+    require_position_independent(scheme, layout)
     dec = decoder(scheme, lost)
     off, ln, slots = striped_slots(layout, bases, rank, lost.lost)
     if ln == 0 or dec.n_out == 0:

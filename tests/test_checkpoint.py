@@ -232,6 +232,7 @@ def test_bad_parity_and_over_tolerance_fallbacks():
         res = ck.recover(3, FailureEvent([1], at_chunk=4), run.ground_truth, [16] * 4)
         assert res.plan.mode == RecoveryMode.kFullRecomputeFallback, (gpu, rate)
         assert res.verify_gpu_chunks == (4 if rate == 1.0 else 0)
+        assert res.corrupt_chunks == [2] and res.decoded_chunks == 0
 
 
 @pytest.mark.gpu
@@ -297,3 +298,48 @@ def test_odd_slice_sizes_fall_back_to_host_fnv():
         assert int(st) == 0 and e.checksum == O.port().parity_checksum(e.parity)
     res = ck.recover(5, FailureEvent([1], at_chunk=run.chunks_done), run.ground_truth, [3] * run.chunks_done)
     assert res.verified and res.verify_gpu_chunks == 0 and len(res.plan.reconstruct_ids) == run.chunks_done
+
+
+@pytest.mark.gpu
+def test_c3_full_geometry_sealed_on_device_and_recovered_hybrid():
+    """The true C3 geometry (Llama-3-70B KV TP=8, 128K-token prefill = 64
+    chunks x 8 workers x 83,886,080 B, RS(8,2)) with the default policies:
+    seal="auto" (every chunk sealed on the GPU), seal_inflight_bytes 2 GiB
+    (10 GiB of parity -> in-flight buffers are popped while their checksums
+    are still being committed), gpu_verify=True. Every stored checksum equals
+    the reference's compute_checksum of the stored bytes, chunks 0 and 63
+    equal the oracle's encode, and the recovery of worker 5 at chunk 64 is
+    hybrid with all 64 chunks decoded bit-exact (recovery.hpp:176-298,
+    parity_store.hpp:46-53)."""
+    import concurrent.futures as cf
+    import torch
+    from paper_2605_00831_b200.checkpoint import Checkpointer
+    from paper_2605_00831_b200.kv_layout import LLAMA3_70B
+    from paper_2605_00831_b200.parity_store import ParityStore
+    cfg = CheckpointConfig(CodingScheme.reed_solomon(8, 2), 2048, LLAMA3_70B)
+    store = ParityStore(seal_threads=8)
+    ck = Checkpointer(cfg, store)
+    assert ck.slice == 83886080 and ck.seal == "auto" and ck._device_seal() and ck.gpu_verify
+    assert ck.seal_inflight_bytes < 64 * 2 * ck.slice
+    run = ck.run_prefill_with_checkpointing(7, 131072, kv_seed=3)
+    ck.synchronize()
+    assert run.completed and run.chunks_done == 64
+    port = O.port()
+    entries = [store.get(7, c, verify=False)[1] for c in range(64)]
+    with cf.ThreadPoolExecutor(16) as ex:   # the oracle's serial FNV releases the GIL
+        sums = list(ex.map(lambda e: port.parity_checksum(e.parity), entries))
+    bad = [c for c in range(64) if sums[c] != entries[c].checksum]
+    assert not bad, f"stored checksums disagree with the reference FNV for chunks {bad}"
+    for c in (0, 63):
+        host = [run.ground_truth[c][w].bytes.cpu().numpy() for w in range(8)]
+        want = port.encode(O.RS, 8, 2, host)
+        assert all(np.array_equal(entries[c].parity[i], want[i]) for i in range(2)), c
+    del entries
+    res = ck.recover(7, FailureEvent([5], at_chunk=64), run.ground_truth, [2048] * 64)
+    assert res.plan.mode == RecoveryMode.kHybrid, (res.plan.mode, res.corrupt_chunks)
+    assert len(res.plan.reconstruct_ids) == 64 and res.decoded_chunks == 64 and res.verified
+    assert res.reconstruct_device_ms > 0
+    for c in range(64):
+        assert torch.equal(res.recovered[5][c].bytes, run.ground_truth[c][5].bytes), c
+    ck.close()
+    store.close()

@@ -170,3 +170,55 @@ def test_fnv_fuzz_random_chains():
             for i in range(k):
                 h = port.fnv1a64(host[c * k + i], h)
             assert got[c] == h, (trial, n_chains, k, ln, c)
+
+
+def test_multi_job_chains_beyond_the_scratch_budget():
+    """14 chains of 2 x 80 MiB: the low-byte scratch (2.2 GiB) exceeds the
+    per-job budget (2 GiB), so the chains are hashed in two jobs -- every
+    checksum still equals the host seal (the reference's compute_checksum)."""
+    ln, n = 83886080, 14
+    g = torch.Generator(device="cuda").manual_seed(9)
+    par = torch.randint(0, 256, (n, 2, ln), dtype=torch.uint8, device="cuda", generator=g)
+    got = device_fnv([par[c, i] for c in range(n) for i in range(2)], n, 2, ln)
+    hp = par.cpu().numpy()
+    out = (C.c_uint64 * n)()
+    assert L.lib().gs_parity_checksum_batch(L.ptr_array([hp[c, i].ctypes.data for c in range(n) for i in range(2)]),
+                                            n, 2, ln, 16, out) == 0
+    assert got == [int(out[c]) for c in range(n)]
+
+
+@pytest.mark.parametrize("where", ["device", "pinned"])
+def test_sealed_commit_owns_its_checksums(where):
+    """gs_store_commit_sealed_batch copies the checksums on the commit's stream
+    into memory the store owns: overwriting the caller's buffer once the
+    stream has passed the commit (device: a later kernel on the same stream;
+    pinned: a host write after the stream drained) never changes what the
+    entries are sealed with."""
+    from paper_2605_00831_b200.coding import CodingScheme
+    from paper_2605_00831_b200.parity_store import ParityStore
+    store = ParityStore(seal_threads=2)
+    sch = CodingScheme.reed_solomon(4, 2)
+    st = torch.cuda.Stream()
+    for rnd in range(50):
+        keys = [(rnd, c) for c in range(3)]
+        acc, _ = store.reserve_batch(keys, sch, 16, 4096)
+        assert acc == 3
+        vals = [rnd * 1000 + c + 1 for c in range(3)]
+        if where == "device":
+            buf = torch.tensor(vals, dtype=torch.int64, device="cuda")
+            torch.cuda.synchronize()
+            store.commit_sealed_batch(keys, buf.data_ptr(), st)
+            with torch.cuda.stream(st):
+                buf.fill_(-1)            # stream-ordered after the store's copy
+        else:
+            buf = torch.tensor(vals, dtype=torch.int64).pin_memory()
+            store.commit_sealed_batch(keys, buf.data_ptr(), st)
+            st.synchronize()
+            buf.fill_(-1)                # the landing thread may not have run yet
+        del buf
+    store.wait_sealed()
+    for rnd in range(50):
+        for c in range(3):
+            status, e = store.get(rnd, c, verify=False)
+            assert int(status) == 0 and e.checksum == rnd * 1000 + c + 1, (rnd, c)
+    store.close()

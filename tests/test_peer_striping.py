@@ -335,3 +335,28 @@ def test_striped_partition_fuzz_single_process():
             want = port_lib.encode(O.RS, n, k, shards[s])
             for i in range(k):
                 assert np.array_equal(got[s][i], want[i]), (trial, n, world, k, S, L, s, i)
+
+
+def test_striped_planners_refuse_position_dependent_rdp():
+    """RDP parity depends on byte position (coding.hpp:225-307): a rank
+    encoding its byte range as a shard of its own would produce a different
+    code, so the striped planners refuse RDP at world > 1 (the oracle shows
+    the difference) and accept it at world 1 (one range = the whole shard)."""
+    import sys
+    sys.path.insert(0, ROOT)
+    from paper_2605_00831_b200.coding import CodingScheme, ErasurePattern, InvalidArgument
+    from paper_2605_00831_b200.peer import ShardLayout, plan_encode_striped, plan_reconstruct_striped
+    from paper_2605_00831_b200.peer import require_position_independent
+    port_lib = O.port()
+    L = 10000
+    shards = [splitmix_bytes(900 + j, L) for j in range(8)]
+    whole = port_lib.encode(O.RDP, 8, 2, shards)
+    half = port_lib.encode(O.RDP, 8, 2, [s[:4096] for s in shards])
+    assert not np.array_equal(whole[1][:4096], half[1])   # range-local RDP is a different code
+    rdp = CodingScheme.rdp(8)
+    require_position_independent(rdp, ShardLayout(8, 1, 1, L))
+    require_position_independent(CodingScheme.reed_solomon(8, 2), ShardLayout(8, 2, 1, L))
+    with pytest.raises(InvalidArgument):
+        plan_encode_striped(rdp, ShardLayout(8, 2, 1, L), [0, 0], 0, parity_out=None)
+    with pytest.raises(InvalidArgument):
+        plan_reconstruct_striped(rdp, ShardLayout(8, 2, 1, L), [0, 0], 0, ErasurePattern([1]), None, None)
