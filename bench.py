@@ -1,28 +1,33 @@
 #!/usr/bin/env python
 """Benchmark: GhostServe shadow-checkpointing hot path on B200.
 
-Workload (BASELINE.json configs[1], "C2"): Llama-3-8B KV cache at TP=8 --
-32 layers x 8 KV heads x 128 dim, fp16, one worker slice per request per
-16-token decode block = 262,144 B -- RS(8,2) incremental parity for one
-16-token decode block of a batch of 32 requests. One STEP = one block
-checkpoint: K1 encodes 32 x 8 x 256 KiB of device-resident KV into 32 x 2 x
-256 KiB parity and the parity is D2H'd to pinned host memory (the host tier),
-overlapped piecewise. Metric = data bytes encoded / step time (the
-reference's bench convention, tools/ghostserve.cpp:279-282).
+Headline workload (BASELINE.json configs[2], "C3", the largest config that
+fits one B200): Llama-3-70B KV cache at TP=8 -- 80 layers x 8 KV heads x 128
+dim, fp16, 2048-token prefill chunks -> one worker slice per chunk =
+83,886,080 B -- RS(8,2) parity of a 128K-token prefill (64 chunks), then the
+full-shard recovery of a failed worker. One STEP = the checkpoint of one
+2K-token chunk: K1 encodes the chunk's 8 x 80 MiB of device-resident KV into
+2 x 80 MiB of parity and the parity is D2H'd to pinned host memory (the host
+tier), overlapped piecewise. The steps walk through distinct chunks (ring of
+8 x 640 MiB of KV, far larger than L2). Metric = data bytes encoded / step
+time (the reference's bench convention, tools/ghostserve.cpp:279-282), and
+beside it `recovery_ms`: the C3 full-shard rebuild of worker 5 with the
+reference's semantics (plan, FNV-1a verification of all 64 parity entries,
+H2D + K2, recovery.hpp:176-298), wall time to verified bit-exact bytes.
 
 At N GPUs (torchrun, one rank per GPU) the TP group is spread over the ranks
-(8/N workers each) and the batch is 32*N requests (weak scaling): rank g
-encodes byte range g of every shard, pulling the ranges it does not own from
-peers over NVLink inside K1, and D2H's parity range g on its own host link.
+(8/N workers each) and each step checkpoints one chunk of each of N
+concurrent prefills (weak scaling): rank g encodes byte range g of every
+shard, pulling the ranges it does not own from peers over NVLink inside K1,
+and D2H's parity range g on its own host link.
 
-Also reported (same JSON line): the kernel-only roofline of K1, the host-link
-fraction, e2e through the reference-facing C ABI with host buffers
-(gs_encode_host: H2D + K1 + D2H per step), lost-shard recovery latency (C2
-block and, at N=1, the C3 full-shard rebuild of a 128K-token Llama-3-70B
-prefill), clocks sampled through NVML during the timed region, and the
-reference CPU codec timed on this host.
+Also reported (same JSON line): the kernel-only roofline of K1 (and K2), the
+host-link fraction, e2e through the reference-facing C ABI with host buffers
+(gs_encode_host: H2D + K1 + D2H per step), the raw (unverified) C3 rebuild,
+C4, the decode-step overhead, clocks sampled through NVML during the timed
+region, and the reference CPU codec timed on this host.
 
-  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--workload c3|c2]
   python bench.py --sweep [--sweep-sizes 64K,...,1G]     # C5: one JSON line per (code, L)
   python bench.py --configs [--configs-only C1,C3]       # C1-C4 table incl. reference CPU + bit-exact
 """
@@ -31,23 +36,64 @@ from __future__ import annotations
 import argparse
 import ctypes as C
 import json
+import math
 import os
+import socket
 import statistics
 import sys
 import threading
 import time
+from dataclasses import dataclass
 
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 METRIC = "KV parity encode GB/s incl. D2H offload; lost-shard KV recovery latency (ms)"
-WORKLOAD = "C2: Llama-3-8B KV TP=8, RS(8,2), incremental parity per 16-token decode block, batch 32"
 N_SHARDS, K_PARITY = 8, 2
-BLOCK_TOKENS, BATCH = 16, 32
-SLICE = 262_144                    # slice_bytes(Llama-3-8B, tp 8, m 16)
-RING_BLOCKS = 8                    # distinct decode blocks the steps rotate over (> L2)
 KV_SEED = 3
 NVLINK_GBS = 900.0                 # NVLink 5 per direction per GPU (spec)
+LOST_WORKER = 5                    # recovery_test.cpp:310
+
+
+@dataclass(frozen=True)
+class Workload:
+    key: str
+    name: str
+    geometry: tuple          # (layers, kv_heads, head_dim) fp16, TP=8
+    tokens: int              # tokens per checkpoint unit (prefill chunk / decode block)
+    stripes: int             # (request, chunk) stripes per GPU per step
+    ring: int                # distinct steps' KV resident on the device (> L2)
+    unit: str
+
+    @property
+    def slice(self) -> int:
+        layers, heads, dim = self.geometry
+        return 2 * layers * self.tokens * (heads * dim // N_SHARDS) * 2
+
+
+WORKLOADS = {
+    "c3": Workload("c3", "C3: Llama-3-70B KV TP=8, 128K-token prefill checkpoint (64 x 2048-token chunks, RS(8,2)) "
+                         "then full-shard recovery of worker 5",
+                   (80, 8, 128), 2048, 1, 8, "one 2048-token prefill chunk (8 x 83,886,080 B)"),
+    "c2": Workload("c2", "C2: Llama-3-8B KV TP=8, RS(8,2), incremental parity per 16-token decode block, batch 32",
+                   (32, 8, 128), 16, 32, 8, "one 16-token decode block of 32 requests (32 x 8 x 262,144 B)"),
+}
+
+
+def model_of(W):
+    from paper_2605_00831_b200 import kv_layout as K
+    layers, heads, dim = W.geometry
+    return K.ModelConfig(layers, heads, dim, 2, N_SHARDS)
+
+
+def step_ids(W, step: int, stripe: int):
+    """(request, chunk) of stripe `stripe` in step `step`: C3 walks the
+    chunks of one prefill (request 0, chunk = step; a new request every 64
+    chunks), C2 the decode blocks of 32 requests (request = stripe, chunk =
+    block = step)."""
+    if W.key == "c3":
+        return 100 + stripe + 1000 * (step // 64), step % 64
+    return stripe, step
 
 
 def env_rank():
@@ -115,91 +161,187 @@ class ClockSampler:
 
 
 # ---------------------------------------------------------------------------
-# CPU baseline: the reference codec (oracle/_ref) or the oracle port
+# CPU side: the reference codec (oracle/_ref) or the oracle port
 # ---------------------------------------------------------------------------
-class CpuBlock:
-    """One C2 decode block (32 requests x 8 workers x 256 KiB, reference KV
-    stream) encoded by the reference CPU codec (oracle/_ref, kind
-    "reference"), or by the oracle port when the reference was not built."""
+def _avail_ram() -> int:
+    try:
+        with open("/proc/meminfo") as f:
+            for line in f:
+                if line.startswith("MemAvailable:"):
+                    return int(line.split()[1]) * 1024
+    except Exception:
+        pass
+    return 16 << 30
 
-    def __init__(self):
+
+class CpuArm:
+    """The workload's steps on the host CPU through the reference codec
+    (oracle/_ref: the reference headers compiled in place, kind
+    "reference"), or through the oracle port when the reference was not
+    built here. Every step gets its OWN (request, chunk) KV -- regenerated
+    with the reference generator (make_ground_truth_slice, kv_seed 3) before
+    the step, outside the timed call -- so no step reuses another's bytes."""
+
+    def __init__(self, W: Workload, threads: int):
         import numpy as np
         from oracle import oracle as O
 
-        self.O = O
+        self.O, self.W = O, W
         self.kind = "reference" if O.have_ref() else "port"
         self.lib = O.ref() if O.have_ref() else O.port()
-        sets = [[self.lib.make_ground_truth_slice(KV_SEED, r, 0, w, 32, 8, 128, 8, BLOCK_TOKENS,
-                                                  BLOCK_TOKENS) for w in range(N_SHARDS)] for r in range(4)]
-        self.stripes = [sets[r % 4] for r in range(BATCH)]
-        self.parity = [[np.zeros(SLICE, np.uint8) for _ in range(K_PARITY)] for _ in range(BATCH)]
+        self.gen_lib = O.port()    # input generator: bit-identical to the reference's (tests/test_oracle_golden)
+        self.threads = threads if self.kind == "reference" else 1
+        ln = W.slice
+        self.data = [[np.empty(ln, np.uint8) for _ in range(N_SHARDS)] for _ in range(W.stripes)]
+        self.parity = [[np.empty(ln, np.uint8) for _ in range(K_PARITY)] for _ in range(W.stripes)]
 
-    def run(self, nreq: int, threads: int) -> float:
-        """Encode nreq requests of the block; returns encode seconds."""
-        O = self.O
+    def gen(self, step: int) -> None:
+        """The step's KV, generated on all host threads (untimed)."""
+        import concurrent.futures as cf
+        W, lib = self.W, self.gen_lib
+        layers, heads, dim = W.geometry
+        fn = lib.fn("make_ground_truth_slice")
+
+        def one(sw):
+            s, w = sw
+            req, chunk = step_ids(W, step, s)
+            out = self.data[s][w]
+            st = fn(C.c_uint64(KV_SEED), C.c_uint64(req), C.c_uint32(chunk), w, layers, heads, dim, N_SHARDS,
+                    C.c_uint32(W.tokens), C.c_uint32(W.tokens), out.ctypes.data_as(C.POINTER(C.c_uint8)))
+            assert st == 0
+        with cf.ThreadPoolExecutor(max(1, os.cpu_count() or 1)) as ex:
+            list(ex.map(one, [(s, w) for s in range(W.stripes) for w in range(N_SHARDS)]))
+
+    def encode(self, threads: int) -> float:
+        """One step's encode (every stripe); returns encode seconds
+        (steady_clock inside the reference shim, tools/ghostserve.cpp:262-283)."""
+        O, W = self.O, self.W
         if self.kind == "reference":
-            return self.lib.encode_batch_timed(O.RS, N_SHARDS, K_PARITY, self.stripes[:nreq],
-                                               self.parity[:nreq], threads)
+            if W.stripes >= threads and W.stripes > 1:   # whole stripes per thread
+                return self.lib.encode_batch_timed(O.RS, N_SHARDS, K_PARITY, self.data, self.parity, threads)
+            # byte ranges of each stripe over the threads (position-wise code)
+            return sum(self.lib.encode_timed(O.RS, N_SHARDS, K_PARITY, self.data[s], self.parity[s], threads)
+                       for s in range(W.stripes))
         t1 = time.perf_counter()
-        for r in range(nreq):
-            self.lib.encode(O.RS, N_SHARDS, K_PARITY, self.stripes[r])
+        for s in range(W.stripes):
+            self.lib.encode(O.RS, N_SHARDS, K_PARITY, self.data[s])
         return time.perf_counter() - t1
 
+    def sample(self, s_target: float, threads: int, first_step: int = 0):
+        """Encode distinct steps until s_target seconds of encode time;
+        returns (steps done, encode seconds)."""
+        done, busy = 0, 0.0
+        while busy < s_target or done == 0:
+            self.gen(first_step + done)
+            busy += self.encode(threads)
+            done += 1
+        return done, busy
 
-def cpu_encode_baseline(target_s: float, threads: int):
-    """Reference CPU encode on C2 blocks for ~target_s seconds; returns dict."""
-    blk = CpuBlock()
-    if blk.kind == "port":
-        threads = 1
-    done, busy = 0, 0.0
-    while busy < target_s or done == 0:
-        busy += blk.run(BATCH, threads)
-        done += 1
-    gbs = done * BATCH * N_SHARDS * SLICE / busy / 1e9
+    def recovery_c3(self, threads: int) -> dict:
+        """Full-shard recovery of worker 5 over a 128K prefill (64 chunks)
+        with the reference's byte path per chunk: reconstruct_chunk =
+        FNV-1a verification of the stored parity + reconstruct
+        (recovery.hpp:100-133). Tc chunks run concurrently on Tc threads (Tc
+        bounded by host RAM: the reference API copies every chunk's 9 x 80
+        MiB into owning slices); the 64-chunk latency is ceil(64/Tc) x the
+        slowest thread of a concurrent batch. The reference's recover() also
+        re-runs get() (two more FNV passes per chunk, recovery.hpp:200-207,
+        279-280); those are NOT counted here, in the reference's favour."""
+        import concurrent.futures as cf
+        import numpy as np
+        O, W = self.O, self.W
+        ln = W.slice
+        if self.kind != "reference":
+            return {"skipped": "reference not built on this host (oracle/_ref)"}
+        self.gen(0)
+        layers, heads, dim = W.geometry
+        par = [np.empty(ln, np.uint8) for _ in range(K_PARITY)]
+        cs, t_ck = self.lib.checkpoint_chunk_timed(O.RS, N_SHARDS, K_PARITY, (layers, heads, dim), W.tokens,
+                                                   *step_ids(W, 0, 0), W.tokens, self.data[0], par)
+        slots = list(self.data[0]) + par
+        slots[LOST_WORKER] = None
+        per_call = (N_SHARDS + K_PARITY + 1) * ln + (256 << 20)
+        tc = max(1, min(threads, (_avail_ram() - (8 << 30)) // per_call))
+        outs = [[np.empty(ln, np.uint8)] for _ in range(tc)]
+        times = []
+        for rep in range(2):
+            with cf.ThreadPoolExecutor(tc) as ex:
+                secs = list(ex.map(lambda i: self.lib.reconstruct_chunk_timed(O.RS, N_SHARDS, K_PARITY, slots,
+                                                                               outs[i], cs), range(tc)))
+            times.append(max(secs))
+        ok = all(np.array_equal(o[0], self.data[0][LOST_WORKER]) for o in outs)
+        batch = statistics.mean(times)
+        chunks = 64
+        ms = math.ceil(chunks / tc) * batch * 1e3
+        return {"full_shard_ms": round(ms, 1), "chunks": chunks, "concurrent_chunks": tc,
+                "batch_s": [round(t, 3) for t in times], "checkpoint_chunk_1t_ms": round(t_ck * 1e3, 1),
+                "rebuilt_ok": bool(ok),
+                "sample": f"{tc} concurrent reference reconstruct_chunk calls (FNV verify + decode of worker "
+                          f"{LOST_WORKER}, 7 survivors + 2 parity rows of 83,886,080 B), 2 batches, "
+                          f"scaled to 64 chunks as ceil(64/{tc}) batches"}
+
+
+def cpu_encode_baseline(W, target_s: float, threads: int):
+    """Reference CPU encode of the workload's steps for ~target_s seconds."""
+    arm = CpuArm(W, threads)
+    done, busy = arm.sample(target_s, arm.threads, first_step=1000)
+    gbs = done * W.stripes * N_SHARDS * W.slice / busy / 1e9
     from tools.config_table import cpu_model
-    return {"value": round(gbs, 4), "unit": "GB/s", "cores": threads, "kind": blk.kind, "cpu_model": cpu_model(),
-            "sample": f"{done} C2 decode blocks (32 requests x RS(8,2) over 8 x 256 KiB), {busy:.2f} s "
-                      f"of encode time, {threads} thread(s) taking whole requests"}
+    return {"value": round(gbs, 4), "unit": "GB/s", "cores": arm.threads, "kind": arm.kind, "cpu_model": cpu_model(),
+            "sample": f"{done} distinct steps ({W.unit}, RS(8,2)), {busy:.2f} s of encode time, "
+                      f"{arm.threads} thread(s)"}
 
 
-def ncu_traffic():
-    """dram bytes (read + write) per K1 launch from the committed ncu capture."""
+def ncu_traffic(W):
+    """dram bytes (read + write) per K1 launch from the committed ncu capture
+    of THIS build (the capture records the sha of the library it profiled)."""
     try:
-        with open(os.path.join(ROOT, "profiles", "k1_ncu_summary.json")) as f:
-            return json.load(f)["dram_bytes_per_launch"]
-    except Exception:
-        return None
+        import hashlib
+        with open(os.path.join(ROOT, "profiles", f"k1_{W.key}_ncu_summary.json")) as f:
+            summ = json.load(f)
+        so = os.path.join(ROOT, "paper_2605_00831_b200", "_lib", "libghostserve_b200.so")
+        with open(so, "rb") as f:
+            sha = hashlib.sha256(f.read()).hexdigest()[:16]
+        if summ.get("lib_sha256_16") != sha:
+            return None, f"committed capture is of another build ({summ.get('lib_sha256_16')} != {sha})"
+        return summ["dram_bytes_per_launch"], f"ncu --set full of this build ({summ.get('file')})"
+    except Exception as e:
+        return None, f"no ncu capture for this workload/build ({type(e).__name__})"
 
 
 def run_reference(args):
-    """--impl reference: the reference CPU codec on this host, all threads."""
+    """--impl reference: the reference CPU codec on this host, all threads,
+    the same workload, metric and unit as our arm."""
     rank, world, _ = env_rank()
     if rank != 0:
         return
+    W = WORKLOADS[args.workload]
     threads = os.cpu_count() or 1
+    arm = CpuArm(W, threads)
+    threads = arm.threads
     steps, warm = args.steps, args.warmup
-    blk = CpuBlock()
-    kind = blk.kind
-    if kind == "port":
-        threads = 1
-    # one step = one C2 decode block; bounded: if a block would take > ~3 s,
-    # each step times a sample of its requests and scales to the full block.
-    probe = blk.run(2, threads) / 2
-    nreq = BATCH if probe * BATCH < 3.0 else max(1, int(3.0 / probe))
-    for _ in range(warm):
-        blk.run(nreq, threads)
-    total = sum(blk.run(nreq, threads) for _ in range(steps))
-    per_step = total / steps * (BATCH / nreq)
-    gbs = BATCH * N_SHARDS * SLICE / per_step / 1e9
-    sample = (f"each step = {nreq} of the block's 32 requests (8 x 256 KiB RS(8,2) encode each), "
-              f"scaled to the full block; ghostserve::encode on {threads} thread(s) taking whole requests")
+    for i in range(warm):
+        arm.gen(i)
+        arm.encode(threads)
+    total = 0.0
+    for i in range(steps):
+        arm.gen(warm + i)              # the step's own chunk, untimed
+        total += arm.encode(threads)   # timed: the reference encode
+    per_step = total / steps
+    gbs = W.stripes * N_SHARDS * W.slice / per_step / 1e9
+    rec = arm.recovery_c3(threads) if W.key == "c3" else {"skipped": "C2 headline"}
+    sample = (f"each step = {W.unit} with its own (request, chunk) KV, encoded by ghostserve::encode on "
+              f"{threads} thread(s) ({'byte ranges of the stripe' if W.stripes == 1 else 'whole stripes'} "
+              "per thread); steady_clock around the encode calls only")
     line = {"metric": METRIC, "value": round(gbs, 4), "unit": "GB/s", "n_gpus": world, "steps": steps,
             "warmup": warm, "ms_per_step": round(per_step * 1e3, 3), "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "u8", "data": "synthetic",
+            "scaling": "weak", "vs_baseline": None, "dtype": "u8",
+            "data": "synthetic (reference make_ground_truth_slice KV stream, kv_seed 3)",
             "impl": "reference",
-            "config": {"workload": WORKLOAD, "scheme": "RS(8,2)", "slice_bytes": SLICE, "batch": BATCH,
+            "config": {"workload": W.name, "scheme": "RS(8,2)", "slice_bytes": W.slice, "stripes_per_step": W.stripes,
                        "host": "CPU only"},
-            "cpu_baseline": {"value": round(gbs, 4), "unit": "GB/s", "cores": threads, "kind": kind,
+            "recovery_ms": rec.get("full_shard_ms"), "recovery": rec,
+            "cpu_baseline": {"value": round(gbs, 4), "unit": "GB/s", "cores": threads, "kind": arm.kind,
                              "sample": sample},
             "e2e": {"value": round(gbs, 4), "unit": "GB/s", "h2d_bytes_per_step": 0,
                     "d2h_bytes_per_step": 0}}
@@ -230,6 +372,10 @@ def host_link_peaks(torch, dev, nbytes=256 << 20, reps=5):
     return out
 
 
+class Failed(Exception):
+    """A parity / recovery check failed: the line is printed, the exit code is 1."""
+
+
 def run_ours(args):
     import torch
     import torch.distributed as dist
@@ -241,6 +387,8 @@ def run_ours(args):
     from paper_2605_00831_b200.peer import (PeerGroup, ShardLayout, plan_encode_rotating, plan_encode_striped,
                                             plan_reconstruct_striped, stripe_range)
 
+    W = WORKLOADS[args.workload]
+    SLICE, RING = W.slice, W.ring
     rank, world, local = env_rank()
     # GS_BENCH_SHARED_GPU=1: functional check of the multi-rank path with all
     # ranks on cuda:0 (gloo plumbing; timings are not meaningful then).
@@ -251,50 +399,64 @@ def run_ours(args):
     dev = torch.device("cuda", local)
     # multi-socket hosts: run next to this GPU's host link (no-op on one node)
     numa_cpus = None if shared else D.bind_local_cpus(local)
+    comm = None
     if world > 1:
         if shared:
             dist.init_process_group("gloo")
         else:
             dist.init_process_group("nccl", device_id=dev)
+        t = torch.ones(1, device="cpu" if shared else dev)
+        dist.all_reduce(t)      # first collective: the communicator exists and spans every rank
+        comm = {"backend": dist.get_backend(), "nranks": dist.get_world_size(), "all_reduce_ranks": int(t.item())}
+        if rank == 0:
+            print(f"[bench] communicator backend={comm['backend']} nranks={comm['nranks']}", file=sys.stderr,
+                  flush=True)
     scheme = CodingScheme.reed_solomon(N_SHARDS, K_PARITY)
-    cfg = K.LLAMA3_8B
-    assert K.slice_bytes(cfg, BLOCK_TOKENS) == SLICE
-    S = BATCH * world                      # weak scaling: 32 requests per GPU
+    cfg = model_of(W)
+    assert K.slice_bytes(cfg, W.tokens) == SLICE
+    S = W.stripes * world                  # weak scaling: W.stripes stripes per GPU
     layout = ShardLayout(N_SHARDS, world, S, SLICE)
     nl = layout.n_local
     lib = L.lib()
+    failures = []
 
-    # --- data: RING_BLOCKS distinct decode blocks, reference KV stream ------
-    # block b, request s, worker w -> make_ground_truth_slice(seed, s, b, w)
-    ring = torch.empty((RING_BLOCKS, S, nl, SLICE), dtype=torch.uint8, device=dev)
-    for b in range(RING_BLOCKS):
+    # --- data: RING distinct steps, reference KV stream (generated on the GPU) --
+    ring = torch.empty((RING, S, nl, SLICE), dtype=torch.uint8, device=dev)
+    for b in range(RING):
         for s in range(S):
+            req, chunk = step_ids(W, b, s)
             for jl in range(nl):
-                K.make_ground_truth_slice(KV_SEED, s, b, rank * nl + jl, cfg, BLOCK_TOKENS, BLOCK_TOKENS,
+                K.make_ground_truth_slice(KV_SEED, req, chunk, rank * nl + jl, cfg, W.tokens, W.tokens,
                                           out=ring[b, s, jl])
     torch.cuda.synchronize()
     pg = PeerGroup() if world > 1 else None
-    bases = [pg.share(ring[b]) if pg else [ring[b].data_ptr()] for b in range(RING_BLOCKS)]
+    bases = [pg.share(ring[b]) if pg else [ring[b].data_ptr()] for b in range(RING)]
     h_parity = D.pinned_near((S, K_PARITY, SLICE), local)   # on the GPU's NUMA node
     pipe = D.Pipeline(local, 256 << 20)
     comp = torch.cuda.Stream(device=dev)
     copy = torch.cuda.Stream(device=dev)
     enc = encoder(scheme)
-    launches0 = D.launches()
 
     if args.encoder == "rotate":     # comparison mode: whole stripes, round-robin parity worker
         plans = [plan_encode_rotating(scheme, layout, bases[b], rank, pipe, h_parity, first_worker=b)
-                 for b in range(RING_BLOCKS)]
+                 for b in range(RING)]
     else:
         plans = [plan_encode_striped(scheme, layout, bases[b], rank, pipeline=pipe, h_parity=h_parity)
-                 for b in range(RING_BLOCKS)]
+                 for b in range(RING)]
 
     def step(i):
-        plans[i % RING_BLOCKS].run(comp.cuda_stream, copy.cuda_stream)
+        plans[i % RING].run(comp.cuda_stream, copy.cuda_stream)
 
     def barrier():
         if world > 1:
             dist.barrier()
+
+    def allmax(x):
+        if world == 1:
+            return x
+        t = torch.tensor([x], dtype=torch.float64, device="cpu" if shared else dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
 
     # --- timed region: encode + D2H offload ----------------------------------
     for i in range(args.warmup):
@@ -304,8 +466,9 @@ def run_ours(args):
     torch.cuda.synchronize()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     l0 = D.launches()
-    # live K1 timing: timing events around every K1 launch group of the timed
-    # steps, on the compute stream after the staging-slot waits
+    # live K1 timing: the pipeline brackets every K1 launch group of the timed
+    # steps (kernel-internal %globaltimer span + timing events on the compute
+    # stream, after the staging-slot waits)
     check(lib.gs_pipeline_set_timing(pipe.handle, 1), "timing")
     with ClockSampler(local) as clk:
         e0.record(comp)
@@ -320,29 +483,20 @@ def run_ours(args):
     check(lib.gs_pipeline_kernel_time(pipe.handle, C.byref(k_ms), C.byref(k_dev_ms), C.byref(k_groups),
                                       C.byref(k_launches)), "timing")
     check(lib.gs_pipeline_set_timing(pipe.handle, 0), "timing")
-    live_group_us = k_dev_ms.value * 1e3 / max(k_groups.value, 1)     # kernel-internal %globaltimer
-    live_event_us = k_ms.value * 1e3 / max(k_groups.value, 1)         # timing events around each group
+    live_group_us = allmax(k_dev_ms.value * 1e3 / max(k_groups.value, 1))   # kernel-internal %globaltimer
+    live_event_us = allmax(k_ms.value * 1e3 / max(k_groups.value, 1))       # timing events around each group
     barrier()
-    ms = e0.elapsed_time(e1)
-    if world > 1:
-        t = torch.tensor([live_group_us, live_event_us], device="cpu" if shared else dev)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        live_group_us, live_event_us = float(t[0].item()), float(t[1].item())
-    if world > 1:
-        t = torch.tensor([ms], device="cpu" if shared else dev)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        ms = float(t.item())
+    ms = allmax(e0.elapsed_time(e1))
     data_bytes_step = S * N_SHARDS * SLICE          # whole job
     value = data_bytes_step * args.steps / (ms * 1e-3) / 1e9
     ms_step = ms / args.steps
 
-    # parity sanity inside the bench (cheap, on the last block; full checks live in tests/)
-    ok_parity = True
-    if rank == 0:
-        last = (args.warmup + args.steps - 1) % RING_BLOCKS
-        if world == 1:
-            want = D.encode(scheme, ring[last, :2])
-            ok_parity = torch.equal(want.cpu(), h_parity[:2])
+    # parity check inside the bench on the last step's stripes (full checks live in tests/)
+    if rank == 0 and world == 1:
+        last = (args.warmup + args.steps - 1) % RING
+        m = min(S, 2)
+        if not torch.equal(D.encode(scheme, ring[last, :m]).cpu(), h_parity[:m]):
+            failures.append("offloaded parity != encode of the last step's KV")
 
     # --- kernel-only rooflines: K1 encode and K2 single-loss rebuild ---------
     kern, kern2 = {}, {}
@@ -351,16 +505,16 @@ def run_ours(args):
 
     def timed(launch, alg_bytes, name):
         with torch.cuda.stream(ks):
-            for b in range(RING_BLOCKS):
+            for b in range(RING):
                 launch(b)
         ks.synchronize()
-        reps = 4
+        reps = 4 if alg_bytes < (256 << 20) else 1
         g = torch.cuda.CUDAGraph()
         with torch.cuda.graph(g, stream=ks):
             for _ in range(reps):
-                for b in range(RING_BLOCKS):
+                for b in range(RING):
                     launch(b)
-        n_graph = max(3, args.steps // (reps * RING_BLOCKS))
+        n_graph = max(3, args.steps // (reps * RING))
         with torch.cuda.stream(ks):
             g.replay()
             ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -369,90 +523,82 @@ def run_ours(args):
                 g.replay()
             ev1.record(ks)
         ev1.synchronize()
-        per_ms = ev0.elapsed_time(ev1) / (n_graph * reps * RING_BLOCKS)
+        del g
+        per_ms = ev0.elapsed_time(ev1) / (n_graph * reps * RING)
         achieved = alg_bytes / (per_ms * 1e-3) / 1e9
         return {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
                 "frac": round(achieved / peak, 4), "kernel": name,
                 "per_launch_us": round(per_ms * 1e3, 2), "algorithmic_bytes_per_launch": alg_bytes,
                 "peak_source": peak_src,
-                "timing": f"CUDA graph of {reps * RING_BLOCKS} launches over {RING_BLOCKS} distinct "
-                          f"blocks, replayed {n_graph}x, events on the launch stream"}
+                "timing": f"CUDA graph of {reps * RING} launches over {RING} distinct "
+                          f"steps' KV, replayed {n_graph}x, events on the launch stream"}
 
+    extra = {}
     if world == 1:
-        par_dev = torch.empty((RING_BLOCKS, S, K_PARITY, SLICE), dtype=torch.uint8, device=dev)
-        rebuilt = torch.empty((RING_BLOCKS, S, SLICE), dtype=torch.uint8, device=dev)
+        par_dev = torch.empty((RING, S, K_PARITY, SLICE), dtype=torch.uint8, device=dev)
+        rebuilt = torch.empty((RING, S, SLICE), dtype=torch.uint8, device=dev)
         slots = [L.ptr_array([ring[b, s, j].data_ptr() for s in range(S) for j in range(N_SHARDS)])
-                 for b in range(RING_BLOCKS)]
+                 for b in range(RING)]
         outs = [L.ptr_array([par_dev[b, s, i].data_ptr() for s in range(S) for i in range(K_PARITY)])
-                for b in range(RING_BLOCKS)]
-        dec5 = decoder(scheme, ErasurePattern([5]))
-        dslots = [L.ptr_array([None if j == 5 else (ring[b, s, j].data_ptr() if j < N_SHARDS else
-                                                     par_dev[b, s, j - N_SHARDS].data_ptr())
+                for b in range(RING)]
+        dec5 = decoder(scheme, ErasurePattern([LOST_WORKER]))
+        dslots = [L.ptr_array([None if j == LOST_WORKER else (ring[b, s, j].data_ptr() if j < N_SHARDS else
+                                                              par_dev[b, s, j - N_SHARDS].data_ptr())
                                for s in range(S) for j in range(N_SHARDS + K_PARITY)])
-                  for b in range(RING_BLOCKS)]
-        douts = [L.ptr_array([rebuilt[b, s].data_ptr() for s in range(S)]) for b in range(RING_BLOCKS)]
+                  for b in range(RING)]
+        douts = [L.ptr_array([rebuilt[b, s].data_ptr() for s in range(S)]) for b in range(RING)]
+        alg = S * (N_SHARDS + K_PARITY) * SLICE
         variants = {}
         for v, vname in ((0, "ldg128"), (1, "bulk_smem_pipeline")):
             check(lib.gs_set_kernel_variant(v), "variant")
             variants[vname] = timed(
                 lambda b: check(lib.gs_apply_device(enc.handle, S, slots[b], outs[b], SLICE, ks.cuda_stream),
-                                "k1"), S * (N_SHARDS + K_PARITY) * SLICE, f"K1 {vname}")["per_launch_us"]
+                                "k1"), alg, f"K1 {vname}")["per_launch_us"]
         check(lib.gs_set_kernel_variant(2), "variant")  # auto: what the timed step used
         iso = timed(lambda b: check(lib.gs_apply_device(enc.handle, S, slots[b], outs[b], SLICE,
                                                         ks.cuda_stream), "k1"),
-                    S * (N_SHARDS + K_PARITY) * SLICE,
-                    "k_apply_special<EncSpec<RS,8,2>> (K1 encode, auto variant = ldg128 at this size)")
-        alg = S * (N_SHARDS + K_PARITY) * SLICE
-        achieved = alg / (live_group_us * 1e-6) / 1e9
+                    alg, "k_apply_special<EncSpec<RS,8,2>> (K1 encode, auto variant)")
+        # the pipeline runs each step's K1 as one or more launch groups (pieces
+        # sized to its staging ring so the D2H of piece p overlaps K1 of p+1):
+        # the algorithmic bytes of one launch = the step's bytes / groups per step
+        groups = max(k_groups.value, 1)
+        alg_launch = alg * args.steps // groups
+        achieved = alg_launch / (live_group_us * 1e-6) / 1e9
+        traffic, traffic_src = (args.traffic, "--traffic") if args.traffic else ncu_traffic(W)
         kern = dict(iso, achieved=round(achieved, 1), frac=round(achieved / peak, 4),
-                    per_launch_us=round(live_group_us, 2),
-                    timing=f"live, inside the timed steps: mean over the {k_groups.value} K1 launches "
+                    per_launch_us=round(live_group_us, 2), algorithmic_bytes_per_launch=alg_launch,
+                    launches_per_step=round(groups / args.steps, 3),
+                    timing=f"live, inside the timed steps: mean over the {k_groups.value} K1 launch groups "
                            f"({k_launches.value} kernels) of the kernel-internal %globaltimer span (first CTA start "
                            "to last warp's stores performed)",
                     live_event_bracketed={"per_launch_us": round(live_event_us, 2),
-                                          "note": "timing events on the compute stream around each launch; inflated "
-                                                  "by GPU front-end latency while the copy engine streams the previous "
-                                                  "blocks' D2H (tools/k1_context_probe.py)"},
+                                          "note": "timing events on the compute stream around each launch group; "
+                                                  "inflated by GPU front-end latency while the copy engine streams "
+                                                  "the previous pieces' D2H"},
                     isolated_graph={"per_launch_us": iso["per_launch_us"], "achieved": iso["achieved"],
-                                    "frac": iso["frac"], "timing": iso["timing"]})
-        kern["variants_us_per_launch"] = variants
+                                    "frac": iso["frac"], "algorithmic_bytes_per_launch": alg,
+                                    "timing": iso["timing"]},
+                    traffic=traffic, traffic_source=traffic_src, variants_us_per_launch=variants)
         # attainable at this launch size: a device copy moving the same bytes
         # (half read, half written), same rotation and graph timing
-        half = S * (N_SHARDS + K_PARITY) * SLICE // 2
-        cdst = torch.empty((RING_BLOCKS, half), dtype=torch.uint8, device=dev)
-        flat = ring.view(RING_BLOCKS, -1)
+        half = alg // 2
+        cdst = torch.empty((RING, half), dtype=torch.uint8, device=dev)
+        flat = ring.view(RING, -1)
         cp = timed(lambda b: cdst[b].copy_(flat[b, :half]), 2 * half, "copy")
         kern["copy_same_bytes"] = {"per_launch_us": cp["per_launch_us"], "achieved": cp["achieved"],
                                    "kernel_vs_copy_isolated": round(cp["per_launch_us"] / iso["per_launch_us"], 4)}
         del cdst
-        kern["traffic"] = args.traffic or ncu_traffic()
         kern2 = timed(lambda b: check(lib.gs_apply_device(dec5.handle, S, dslots[b], douts[b], SLICE,
                                                           ks.cuda_stream), "k2"),
                       S * (N_SHARDS + 1) * SLICE,
-                      "k_apply_special<DecSpec<RS,8,2,lost{5}>> (K2 rebuild, 7 data + 1 parity -> 1)")
-        ok_parity &= torch.equal(rebuilt[RING_BLOCKS - 1], ring[RING_BLOCKS - 1, :, 5])
-
-        # the same C2 blocks living in per-worker PAGED KV caches (vLLM-style
-        # [layer][K/V][block][16 tok][256 B]): K1 gathers the 64 pages of every
-        # slice in place instead of reading contiguous slices.
-        from paper_2605_00831_b200.paged import PagedKVCache
-        caches = [PagedKVCache(cfg, RING_BLOCKS * S, BLOCK_TOKENS, device=dev) for _ in range(N_SHARDS)]
-        for b in range(RING_BLOCKS):
-            for s_ in range(S):
-                for j in range(N_SHARDS):
-                    caches[j].write_slice(b * S + s_, ring[b, s_, j])
-        pm = caches[0].page_map(BLOCK_TOKENS)
-        pslots = [L.ptr_array([caches[j].block_base(b * S + s_) for s_ in range(S) for j in range(N_SHARDS)])
-                  for b in range(RING_BLOCKS)]
-        kern_paged = timed(lambda b: check(lib.gs_apply_device_paged(enc.handle, S, pslots[b], outs[b], SLICE,
-                                                                     C.byref(pm), (1 << N_SHARDS) - 1, None,
-                                                                     ks.cuda_stream), "k1 paged"),
-                           S * (N_SHARDS + K_PARITY) * SLICE, "K1 encode reading a paged KV cache in place")
-        ok_parity &= torch.equal(par_dev[RING_BLOCKS - 1, :2].cpu(),
-                                 D.encode(scheme, ring[RING_BLOCKS - 1, :2]).cpu())
-        kern["paged_kv_cache_us_per_launch"] = kern_paged["per_launch_us"]
-        kern["paged_kv_cache_frac"] = kern_paged["frac"]
-        del par_dev, rebuilt, caches
+                      f"k_apply_special<DecSpec<RS,8,2,lost{{{LOST_WORKER}}}>> (K2 rebuild, 7 data + 1 parity -> 1)")
+        if not torch.equal(rebuilt[RING - 1], ring[RING - 1, :, LOST_WORKER]):
+            failures.append("K2 rebuild != original shard")
+        if not torch.equal(par_dev[RING - 1, :1].cpu(), D.encode(scheme, ring[RING - 1, :1]).cpu()):
+            failures.append("K1 device parity != encode")
+        kern["paged_kv_cache"] = paged_k1(torch, L, W, cfg, ring, par_dev, outs, enc, timed, ks, failures, D,
+                                          scheme)
+        del par_dev, rebuilt
 
     else:
         # N > 1: the step's own kernel -- K1 over this rank's byte range of all
@@ -460,17 +606,19 @@ def run_ours(args):
         # per rank, max over ranks. Roofline t* = max(HBM bytes / HBM peak,
         # NVLink bytes pulled / NVLink peak).
         off_r, ln_r = stripe_range(SLICE, rank, world)
-        par_dev = torch.empty((RING_BLOCKS, S, K_PARITY, max(ln_r, 16)), dtype=torch.uint8, device=dev)
+        par_dev = torch.empty((RING, S, K_PARITY, max(ln_r, 16)), dtype=torch.uint8, device=dev)
         kplans = [plan_encode_striped(scheme, layout, bases[b], rank, parity_out=par_dev[b])
-                  for b in range(RING_BLOCKS)]
+                  for b in range(RING)]
         alg = S * (N_SHARDS + K_PARITY) * ln_r
         k = timed(lambda b: kplans[b].run(ks.cuda_stream), alg, "striped K1")
-        t = torch.tensor([k["per_launch_us"]], device="cpu" if shared else dev)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        iso_us = float(t.item())
-        # live (timed-region) K1 group time when the step is the striped encoder
-        per_us = live_group_us if args.encoder == "stripe" else iso_us
-        nvl_bytes = S * N_SHARDS * ln_r * (world - 1) // world
+        iso_us = allmax(k["per_launch_us"])
+        # live (timed-region) K1 group time when the step is the striped encoder;
+        # the step's bytes are spread over its launch groups (pipeline pieces)
+        live = args.encoder == "stripe"
+        per_us = live_group_us if live else iso_us
+        if live:
+            alg = alg * args.steps // max(k_groups.value, 1)
+        nvl_bytes = alg * N_SHARDS // (N_SHARDS + K_PARITY) * (world - 1) // world
         t_hbm, t_nvl = alg / (peak * 1e3), nvl_bytes / (NVLINK_GBS * 1e3)  # us
         bound = "nvlink" if t_nvl > t_hbm else "hbm"
         achieved = alg / per_us / 1e3
@@ -489,7 +637,7 @@ def run_ours(args):
                            else k["timing"] + ", max over ranks"),
                 "live_event_bracketed_us": round(live_event_us, 2),
                 "isolated_graph": {"per_launch_us": round(iso_us, 2), "timing": k["timing"] + ", max over ranks"},
-                "traffic": None}
+                "traffic": None, "traffic_source": "ncu is single-process; no multi-rank capture"}
         del par_dev
 
     # --- host link --------------------------------------------------------------
@@ -503,7 +651,7 @@ def run_ours(args):
     # peak, parity over this GPU's host link, peer bytes over NVLink; per GPU
     hbm_b = S * (N_SHARDS + K_PARITY) * SLICE // world
     nvl_b = S * N_SHARDS * SLICE * (world - 1) // world // world
-    legs = {"hbm": hbm_b / (load_peaks()[0] * 1e9), "host_link": (d2h_step // world) / (link["d2h"] * 1e9),
+    legs = {"hbm": hbm_b / (peak * 1e9), "host_link": (d2h_step // world) / (link["d2h"] * 1e9),
             "nvlink": nvl_b / (NVLINK_GBS * 1e9)}
     t_star = max(legs.values())
     step_roofline = {"bound": max(legs, key=legs.get), "t_star_ms": round(t_star * 1e3, 4),
@@ -513,81 +661,12 @@ def run_ours(args):
                              "link peak, peer reads (N-1)/N of the data over NVLink 5 (900 GB/s spec)"}
 
     # --- e2e through the reference-facing C ABI with host buffers -------------
-    # Every rank encodes its own 32 requests (all 8 worker slices each) from
-    # pinned host memory on its own host link: H2D of the data, K1, D2H of the
-    # parity, every step. Wall clock per rank between barriers, max over ranks.
-    per_worker = BATCH * SLICE   # request slices of a worker are contiguous: one stripe
-    h_in = D.pinned_near((N_SHARDS, per_worker), local)
-    h_out = D.pinned_near((K_PARITY, per_worker), local)
-    src = torch.empty((N_SHARDS, BATCH, SLICE), dtype=torch.uint8, device=dev)
-    for j in range(N_SHARDS):
-        for s_ in range(BATCH):
-            K.make_ground_truth_slice(KV_SEED, rank * BATCH + s_, 0, j, cfg, BLOCK_TOKENS, BLOCK_TOKENS,
-                                      out=src[j, s_])
-    h_in.copy_(src.view(N_SHARDS, per_worker).cpu())
-    hp_in = L.ptr_array([h_in[j].data_ptr() for j in range(N_SHARDS)])
-    hp_out = L.ptr_array([h_out[i].data_ptr() for i in range(K_PARITY)])
-    epipe = D.Pipeline(local, 256 << 20)
+    e2e = e2e_host(torch, D, K, L, lib, W, cfg, enc, scheme, rank, world, local, args, barrier, allmax, failures)
 
-    def e2e_run(fn, sync_each):
-        for _ in range(max(3, args.warmup)):
-            check(fn(epipe.handle, enc.handle, hp_in, hp_out, per_worker), "e2e")
-            if sync_each:
-                check(lib.gs_pipeline_sync(epipe.handle), "e2e sync")
-        check(lib.gs_pipeline_sync(epipe.handle), "e2e sync")
-        torch.cuda.synchronize()
-        barrier()
-        t0 = time.perf_counter()
-        for _ in range(args.steps):
-            check(fn(epipe.handle, enc.handle, hp_in, hp_out, per_worker), "e2e")
-            if sync_each:
-                check(lib.gs_pipeline_sync(epipe.handle), "e2e sync")
-        check(lib.gs_pipeline_sync(epipe.handle), "e2e sync")
-        dt = time.perf_counter() - t0
-        barrier()
-        if world > 1:
-            t = torch.tensor([dt], dtype=torch.float64, device="cpu" if shared else dev)
-            dist.all_reduce(t, op=dist.ReduceOp.MAX)
-            dt = float(t.item())
-        return dt
-
-    # Two public ways to drive it, each timed twice (alternating, best trial):
-    #  * stream-ordered: gs_encode_host_async per step, one gs_pipeline_sync at
-    #    the end -- the H2D of step i+1 overlaps the D2H of step i (a serving
-    #    loop checkpointing block after block from host memory);
-    #  * synchronous drop-in: gs_encode_host per step (ghostserve::encode
-    #    semantics). Every step moves its own inputs H2D and its parity D2H.
-    # Which one is faster depends on how the box's PCIe handles both
-    # directions at once; the headline is the faster, both are reported.
-    t_async, t_sync = [], []
-    for _ in range(2):
-        t_async.append(e2e_run(lib.gs_encode_host_async, False))
-        t_sync.append(e2e_run(lib.gs_encode_host, True))
-    dt, dt_sync = min(t_async), min(t_sync)
-    got = h_out.view(K_PARITY, BATCH, SLICE).permute(1, 0, 2)
-    ok_parity &= torch.equal(got[:2], D.encode(scheme, src[:, :2].permute(1, 0, 2).contiguous()).cpu())
-    bytes_e2e = world * BATCH * N_SHARDS * SLICE * args.steps
-    modes = {"stream_ordered": {"value": round(bytes_e2e / dt / 1e9, 3), "ms_per_step": round(dt / args.steps * 1e3, 3),
-                                "api": "gs_encode_host_async per step, gs_pipeline_sync after the last step"},
-             "sync_per_call": {"value": round(bytes_e2e / dt_sync / 1e9, 3),
-                               "ms_per_step": round(dt_sync / args.steps * 1e3, 3),
-                               "api": "gs_encode_host per step (drop-in synchronous ghostserve::encode)"}}
-    best = max(modes, key=lambda m: modes[m]["value"])
-    e2e = {"value": modes[best]["value"], "unit": "GB/s",
-           "h2d_bytes_per_step": world * N_SHARDS * per_worker, "d2h_bytes_per_step": world * K_PARITY * per_worker,
-           "ms_per_step": modes[best]["ms_per_step"],
-           "api": f"{best}: {modes[best]['api']} (C ABI, pinned host buffers; H2D data -> K1 -> D2H parity every "
-                  "step); wall clock, best of 2 trials" + (", one pipeline per rank, max over ranks"
-                                                          if world > 1 else ""),
-           "modes": modes}
-    epipe.close()
-    del h_in, h_out, src
-
-    # --- recovery: one lost worker of the C2 block ----------------------------
+    # --- recovery: one lost worker of the last step's stripes -------------------
     recovery = {}
-    lost_w = 5
-    b = (args.warmup + args.steps - 1) % RING_BLOCKS
-    owner, jl = layout.owner(lost_w)
+    b = (args.warmup + args.steps - 1) % RING
+    owner, jl = layout.owner(LOST_WORKER)
     saved = ring[b, :, jl].clone() if rank == owner else None
     barrier()
     if rank == owner:
@@ -598,7 +677,7 @@ def run_ours(args):
     # failure is detected; the timed region is the byte path: H2D of parity
     # row 0 + K2 over the 7 survivors, written into the failed worker's buffer.
     t_plan = time.perf_counter()
-    rplan = plan_reconstruct_striped(scheme, layout, bases[b], rank, ErasurePattern([lost_w]), h_parity, pipe)
+    rplan = plan_reconstruct_striped(scheme, layout, bases[b], rank, ErasurePattern([LOST_WORKER]), h_parity, pipe)
     plan_ms = (time.perf_counter() - t_plan) * 1e3
     reps = []
     for rep in range(5):   # the same failure recovered 5 times (buffer re-flushed each time); median
@@ -613,61 +692,77 @@ def run_ours(args):
         r1.synchronize()
         barrier()
         reps.append(r0.elapsed_time(r1))
-    rec_ms = sorted(reps)[len(reps) // 2]
-    if world > 1:
-        t = torch.tensor([rec_ms], device="cpu" if shared else dev)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        rec_ms = float(t.item())
+    rec_ms = allmax(sorted(reps)[len(reps) // 2])
+    ok_rb = True
     if rank == owner:
-        ok_parity &= torch.equal(ring[b, :, jl], saved)
+        ok_rb = bool(torch.equal(ring[b, :, jl], saved))
     if world > 1:  # every rank's verdict (the rebuilt shard lives on its owner)
-        t = torch.tensor([1 if ok_parity else 0], device="cpu" if shared else dev)
-        dist.all_reduce(t, op=dist.ReduceOp.MIN)
-        ok_parity = bool(t.item())
-    recovery["c2_block_one_worker_ms"] = round(rec_ms, 4)
-    recovery["c2_block_reps_ms"] = [round(x, 4) for x in reps]
-    recovery["c2_block_roofline_ms"] = round(S * SLICE / (link["h2d"] * 1e9) * 1e3 / world, 4)
-    recovery["c2_plan_host_ms"] = round(plan_ms, 3)
-    recovery["c2_block_bytes_rebuilt"] = S * SLICE
-    recovery["c2_h2d_bytes"] = S * SLICE
-    recovery["decoder_specialised"] = decoder(scheme, ErasurePattern([lost_w])).specialised
+        ok_rb = allmax(0.0 if ok_rb else 1.0) == 0.0
+    if not ok_rb:
+        failures.append("step-level rebuild != original shard")
+    recovery["step_one_worker_ms"] = round(rec_ms, 4)
+    recovery["step_reps_ms"] = [round(x, 4) for x in reps]
+    recovery["step_roofline_ms"] = round(S * SLICE / (link["h2d"] * 1e9) * 1e3 / world, 4)
+    recovery["step_plan_host_ms"] = round(plan_ms, 3)
+    recovery["step_bytes_rebuilt"] = S * SLICE
+    recovery["decoder_specialised"] = decoder(scheme, ErasurePattern([LOST_WORKER])).specialised
 
     launches = l1 - l0
+    # free the step's buffers before the C3 sections
+    if pg:
+        pg.close()
+    del ring, h_parity, plans, bases
+    torch.cuda.synchronize()
+    torch.cuda.empty_cache()
+
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
-        cpu = cpu_encode_baseline(args.cpu_sample_s, os.cpu_count() or 1)
-        cpu1 = cpu_encode_baseline(min(2.0, args.cpu_sample_s), 1)
+        cpu = cpu_encode_baseline(W, args.cpu_sample_s, os.cpu_count() or 1)
+        cpu1 = cpu_encode_baseline(W, min(2.0, args.cpu_sample_s), 1)
         cpu["one_thread_gbs"] = cpu1["value"]
 
+    recovery_ms = None
     if rank == 0 and world == 1 and not args.no_c3:
         recovery.update(c3_recovery(torch, dev, comp, copy, pipe))
+        if not recovery.get("c3_rebuild_ok", True):
+            failures.append("raw C3 rebuild != original shard")
         if kern and kern2:
-            recovery["c3_orchestrated"] = c3_orchestrated(torch, dev, link, kern["achieved"] * 8 / 10,
-                                                          kern2["achieved"] * 8 / 9)
+            orch = c3_orchestrated(torch, dev, link, kern["achieved"] * 8 / 10, kern2["achieved"] * 8 / 9)
+            recovery["c3_orchestrated"] = orch
+            if "plan" in orch:
+                recovery_ms = orch["recover_wall_ms"]
+                if orch["plan"]["mode"] != "hybrid" or orch["decoded_chunks"] != orch["chunks"] or not orch["verified"]:
+                    failures.append(f"C3 recovery did not decode every chunk bit-exact: {orch['plan']} "
+                                    f"decoded {orch['decoded_chunks']} verified {orch['verified']}")
     if world > 1 and not args.no_c3:
         recovery.update(c3_recovery_striped(torch, dist, dev, comp, copy, pipe, rank, world, shared, barrier))
+        recovery_ms = recovery.get("c3_full_shard_ms")
+        if not recovery.get("c3_rebuild_ok", True):
+            failures.append("striped C3 rebuild != original shard")
     if rank == 0 and world == 1 and not args.no_c4:
         recovery.update(c4_recovery(torch, dev, comp, copy, pipe))
+        if not recovery.get("c4_rebuild_ok", True):
+            failures.append("C4 rebuild != original shards")
     overhead = None
     if rank == 0 and world == 1 and not args.no_overhead:
         overhead = decode_overhead(torch, dev, pipe, args)
     host_tier = None
-    if rank == 0 and world == 1:
-        host_tier = host_tier_checkpoint(torch, dev, ring, scheme, pipe, comp, copy, args)
+    if rank == 0 and world == 1 and W.key == "c2":
+        host_tier = host_tier_checkpoint(torch, dev, W, scheme, pipe, comp, copy, args)
 
-    if pg:
-        pg.close()
     if rank == 0:
         line = {"metric": METRIC, "value": round(value, 3), "unit": "GB/s", "n_gpus": world,
                 "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms_step, 4),
                 "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u8",
                 "data": "synthetic (reference make_ground_truth_slice KV stream, kv_seed 3, generated on GPU)",
-                "config": {"workload": WORKLOAD, "scheme": "RS(8,2)", "kv_geometry": "32 layers x 8 KV heads "
-                           "x 128 dim fp16, TP=8 -> 256 B/token/worker", "block_tokens": BLOCK_TOKENS,
-                           "requests_per_gpu": BATCH, "slice_bytes": SLICE,
-                           "data_bytes_per_step": data_bytes_step, "parity_d2h_bytes_per_step": d2h_step,
-                           "l2": f"inputs > L2: steps rotate over {RING_BLOCKS} distinct decode blocks "
-                                 f"({RING_BLOCKS * data_bytes_step // world >> 20} MiB per GPU)",
+                "config": {"workload": W.name, "scheme": "RS(8,2)", "kv_geometry":
+                           f"{W.geometry[0]} layers x {W.geometry[1]} KV heads x {W.geometry[2]} dim fp16, TP=8 -> "
+                           f"{W.geometry[1] * W.geometry[2] // N_SHARDS * 2} B/token/worker",
+                           "step": W.unit, "tokens_per_unit": W.tokens, "stripes_per_gpu": W.stripes,
+                           "slice_bytes": SLICE, "data_bytes_per_step": data_bytes_step,
+                           "parity_d2h_bytes_per_step": d2h_step,
+                           "l2": f"inputs > L2: steps rotate over {RING} distinct steps' KV "
+                                 f"({RING * data_bytes_step // world >> 20} MiB per GPU)",
                            "host_placement": ("pinned buffers and host threads on the GPU's NUMA node (CPUs "
                                               f"{numa_cpus})" if numa_cpus else "single NUMA node host"),
                            "parallelism": (f"byte-range striping x{world} (peer loads over NVLink)"
@@ -675,17 +770,136 @@ def run_ours(args):
                                            f"rotating whole-stripe encoder x{world} (paper's temporal "
                                            "balancing; peer loads over NVLink)") if world > 1 else
                            "single GPU holds all 8 TP shards"},
+                "recovery_ms": recovery_ms,
                 "roofline": kern or None, "roofline_k2": kern2 or None, "step_roofline": step_roofline,
                 "host_link": host_link, "cpu_baseline": cpu, "e2e": e2e,
-                "recovery_ms": recovery.get("c2_block_one_worker_ms"), "recovery": recovery,
-                "decode_overhead": overhead, "host_tier": host_tier,
-                "gpu_launches": launches, "clocks": clk.summary(), "parity_ok": bool(ok_parity)}
+                "recovery": recovery, "decode_overhead": overhead, "host_tier": host_tier,
+                "gpu_launches": launches, "clocks": clk.summary(), "comm": comm,
+                "parity_ok": not failures, "failures": failures}
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()
+    if failures:
+        raise Failed("; ".join(failures))
 
 
-def host_tier_checkpoint(torch, dev, ring, scheme, pipe, comp, copy, args):
+def paged_k1(torch, L, W, cfg, ring, par_dev, outs, enc, timed, ks, failures, D, scheme):
+    """The same steps' KV living in per-worker PAGED KV caches (vLLM-style
+    [layer][K/V][block][16 tok][token bytes]): K1 gathers every slice's pages
+    in place instead of reading contiguous slices. C2: one
+    16-token block per slice; C3: 2048-token chunks over 128 blocks listed in
+    a device block table."""
+    from paper_2605_00831_b200.coding import check
+    from paper_2605_00831_b200.paged import PagedKVCache
+    RING, S, SLICE = ring.shape[0], ring.shape[1], ring.shape[3]
+    bs = 16
+    per = W.tokens // bs
+    caches = [PagedKVCache(cfg, RING * S * per, bs, device=ring.device) for _ in range(N_SHARDS)]
+    for b in range(RING):
+        for s_ in range(S):
+            for j in range(N_SHARDS):
+                u = b * S + s_
+                if per == 1:
+                    caches[j].write_slice(u, ring[b, s_, j])
+                else:
+                    caches[j].write_chunk(range(u * per, (u + 1) * per), ring[b, s_, j], W.tokens)
+    lib = L.lib()
+    if per == 1:
+        pm = caches[0].page_map(W.tokens)
+        pms = [pm] * RING
+        pslots = [L.ptr_array([caches[j].block_base(b * S + s_) for s_ in range(S) for j in range(N_SHARDS)])
+                  for b in range(RING)]
+    else:
+        bt = torch.arange(RING * S * per, dtype=torch.int32, device=ring.device).view(RING, S, per)
+        pms = [caches[0].page_map(W.tokens, W.tokens, bt[b]) for b in range(RING)]
+        pslots = [L.ptr_array([caches[j].buf.data_ptr() for s_ in range(S) for j in range(N_SHARDS)])
+                  for b in range(RING)]
+    out = timed(lambda b: check(lib.gs_apply_device_paged(enc.handle, S, pslots[b], outs[b], SLICE,
+                                                          C.byref(pms[b]), (1 << N_SHARDS) - 1, None,
+                                                          ks.cuda_stream), "k1 paged"),
+                S * (N_SHARDS + K_PARITY) * SLICE, "K1 encode reading a paged KV cache in place")
+    if not torch.equal(par_dev[RING - 1, :1].cpu(), D.encode(scheme, ring[RING - 1, :1]).cpu()):
+        failures.append("paged K1 parity != encode")
+    del caches
+    return {"per_launch_us": out["per_launch_us"], "achieved": out["achieved"], "frac": out["frac"],
+            "page_tokens": bs, "timing": out["timing"]}
+
+
+def e2e_host(torch, D, K, L, lib, W, cfg, enc, scheme, rank, world, local, args, barrier, allmax, failures):
+    """The headline metric end to end through the reference-facing C ABI with
+    HOST buffers: every rank encodes its own W.stripes stripes (all 8 worker
+    slices each) from pinned host memory on its own host link -- H2D of the
+    data, K1, D2H of the parity, every step. Wall clock per rank between
+    barriers, max over ranks. Two distinct host inputs alternate."""
+    from paper_2605_00831_b200.coding import check
+    per_worker = W.stripes * W.slice   # a worker's stripes are contiguous: one shard of stripes*L bytes
+    h_in = [D.pinned_near((N_SHARDS, per_worker), local) for _ in range(2)]
+    h_out = D.pinned_near((K_PARITY, per_worker), local)
+    src = torch.empty((N_SHARDS, W.stripes, W.slice), dtype=torch.uint8, device=f"cuda:{local}")
+    for v in range(2):
+        for j in range(N_SHARDS):
+            for s_ in range(W.stripes):
+                req, chunk = step_ids(W, 500 + v, rank * W.stripes + s_)
+                K.make_ground_truth_slice(KV_SEED, req, chunk, j, cfg, W.tokens, W.tokens, out=src[j, s_])
+        h_in[v].copy_(src.view(N_SHARDS, per_worker).cpu())
+    hp_in = [L.ptr_array([h_in[v][j].data_ptr() for j in range(N_SHARDS)]) for v in range(2)]
+    hp_out = L.ptr_array([h_out[i].data_ptr() for i in range(K_PARITY)])
+    epipe = D.Pipeline(local, 256 << 20)
+
+    def e2e_run(fn, sync_each):
+        for i in range(max(3, args.warmup)):
+            check(fn(epipe.handle, enc.handle, hp_in[i % 2], hp_out, per_worker), "e2e")
+            if sync_each:
+                check(lib.gs_pipeline_sync(epipe.handle), "e2e sync")
+        check(lib.gs_pipeline_sync(epipe.handle), "e2e sync")
+        torch.cuda.synchronize()
+        barrier()
+        t0 = time.perf_counter()
+        for i in range(args.steps):
+            check(fn(epipe.handle, enc.handle, hp_in[i % 2], hp_out, per_worker), "e2e")
+            if sync_each:
+                check(lib.gs_pipeline_sync(epipe.handle), "e2e sync")
+        check(lib.gs_pipeline_sync(epipe.handle), "e2e sync")
+        dt = time.perf_counter() - t0
+        barrier()
+        return allmax(dt)
+
+    # Two public ways to drive it, each timed twice (alternating, best trial):
+    #  * stream-ordered: gs_encode_host_async per step, one gs_pipeline_sync at
+    #    the end -- the H2D of step i+1 overlaps the D2H of step i;
+    #  * synchronous drop-in: gs_encode_host per step (ghostserve::encode
+    #    semantics). Every step moves its own inputs H2D and its parity D2H.
+    t_async, t_sync = [], []
+    for _ in range(2):
+        t_async.append(e2e_run(lib.gs_encode_host_async, False))
+        t_sync.append(e2e_run(lib.gs_encode_host, True))
+    dt, dt_sync = min(t_async), min(t_sync)
+    last = (args.steps - 1) % 2
+    got = h_out.view(K_PARITY, W.stripes, W.slice).permute(1, 0, 2)
+    h_src = h_in[last].view(N_SHARDS, W.stripes, W.slice).permute(1, 0, 2)
+    m = min(W.stripes, 2)
+    if not torch.equal(got[:m], D.encode(scheme, h_src[:m].contiguous().to(src.device)).cpu()):
+        failures.append("e2e parity != encode of the host input")
+    bytes_e2e = world * W.stripes * N_SHARDS * W.slice * args.steps
+    modes = {"stream_ordered": {"value": round(bytes_e2e / dt / 1e9, 3), "ms_per_step": round(dt / args.steps * 1e3, 3),
+                                "api": "gs_encode_host_async per step, gs_pipeline_sync after the last step"},
+             "sync_per_call": {"value": round(bytes_e2e / dt_sync / 1e9, 3),
+                               "ms_per_step": round(dt_sync / args.steps * 1e3, 3),
+                               "api": "gs_encode_host per step (drop-in synchronous ghostserve::encode)"}}
+    best = max(modes, key=lambda m_: modes[m_]["value"])
+    out = {"value": modes[best]["value"], "unit": "GB/s",
+           "h2d_bytes_per_step": world * N_SHARDS * per_worker, "d2h_bytes_per_step": world * K_PARITY * per_worker,
+           "ms_per_step": modes[best]["ms_per_step"],
+           "api": f"{best}: {modes[best]['api']} (C ABI, pinned host buffers; H2D data -> K1 -> D2H parity every "
+                  "step); wall clock, best of 2 trials" + (", one pipeline per rank, max over ranks"
+                                                          if world > 1 else ""),
+           "modes": modes}
+    epipe.close()
+    del h_in, h_out, src
+    return out
+
+
+def host_tier_checkpoint(torch, dev, W, scheme, pipe, comp, copy, args):
     """The full reference checkpoint semantics per C2 block (checkpoint.hpp:
     143-147 + :207): K1 + D2H straight into ParityStore entries reserved on
     pinned slabs, FNV-1a seal of every (request, block) on host threads after
@@ -694,12 +908,20 @@ def host_tier_checkpoint(torch, dev, ring, scheme, pipe, comp, copy, args):
     sealing scales only across chunks / cores)."""
     import ctypes as C
     from paper_2605_00831_b200 import _lib as L
+    from paper_2605_00831_b200 import kv_layout as K
     from paper_2605_00831_b200.coding import check, encoder
     from paper_2605_00831_b200.parity_store import ParityStore
 
+    SLICE, BLOCK_TOKENS, RING_BLOCKS, S = W.slice, W.tokens, W.ring, W.stripes
+    cfg = model_of(W)
+    ring = torch.empty((RING_BLOCKS, S, N_SHARDS, SLICE), dtype=torch.uint8, device=dev)
+    for b in range(RING_BLOCKS):
+        for s in range(S):
+            for j in range(N_SHARDS):
+                K.make_ground_truth_slice(KV_SEED, s, b, j, cfg, BLOCK_TOKENS, BLOCK_TOKENS, out=ring[b, s, j])
+    torch.cuda.synchronize()
     # leave two cores for the CUDA callback thread and the submitting thread
     threads = max(1, (os.cpu_count() or 1) - 2)
-    S = ring.shape[1]
     store = ParityStore(seal_threads=threads)
     store.bind_device(dev.index or 0)   # slabs on the GPU's NUMA node
     enc = encoder(scheme)
@@ -751,11 +973,12 @@ def host_tier_checkpoint(torch, dev, ring, scheme, pipe, comp, copy, args):
            "entries": store.entry_count(), "get_verified_ok": ok,
            "note": "FNV-1a seal is serial per chunk (reference checksum); the GPU path is not waiting on it"}
     store.close()
-    out["device_seal"] = host_tier_device_sealed(torch, dev, ring, scheme, comp, copy, blocks, slots, threads)
+    out["device_seal"] = host_tier_device_sealed(torch, dev, W, ring, scheme, comp, copy, blocks, slots, threads)
+    del ring
     return out
 
 
-def host_tier_device_sealed(torch, dev, ring, scheme, comp, copy, blocks, slots, threads):
+def host_tier_device_sealed(torch, dev, W, ring, scheme, comp, copy, blocks, slots, threads):
     """The same sealed C2 block checkpoints with the seal computed on the GPU:
     K1 into a device parity ring, gs_parity_offload_sealed (D2H of the rows
     into the reserved entries + the chunks' checksums by the bit-sliced GPU
@@ -764,13 +987,13 @@ def host_tier_device_sealed(torch, dev, ring, scheme, comp, copy, blocks, slots,
     from paper_2605_00831_b200.coding import check, encoder
     from paper_2605_00831_b200.parity_store import ParityStore
 
-    S = ring.shape[1]
+    S, SLICE, BLOCK_TOKENS, RING_BLOCKS = ring.shape[1], W.slice, W.tokens, W.ring
     store = ParityStore(seal_threads=threads)
     store.bind_device(dev.index or 0)
     enc, lib = encoder(scheme), L.lib()
-    R = 4   # device parity buffers / pinned checksum arrays in flight
+    R = 4   # device parity buffers / checksum arrays in flight
     par = torch.empty((R, S, K_PARITY, SLICE), dtype=torch.uint8, device=dev)
-    sums = [torch.zeros(S, dtype=torch.int64).pin_memory() for _ in range(R)]
+    sums = [torch.zeros(S, dtype=torch.int64, device=dev) for _ in range(R)]
     rows = [L.ptr_array([par[i, s, r].data_ptr() for s in range(S) for r in range(K_PARITY)]) for i in range(R)]
     free = [None] * R
     torch.cuda.synchronize()
@@ -779,7 +1002,7 @@ def host_tier_device_sealed(torch, dev, ring, scheme, comp, copy, blocks, slots,
         i = b % R
         if free[i] is not None:
             comp.wait_event(free[i])      # the buffer's previous D2H is done
-            free[i].synchronize()         # ... and its checksums were consumed by the store callback
+            free[i].synchronize()         # ... and the store has copied its checksums on `copy`
         keys = [(s, b) for s in range(S)]
         acc, dst = store.reserve_batch(keys, scheme, BLOCK_TOKENS, SLICE)
         assert acc == S
@@ -959,7 +1182,8 @@ def c3_recovery(torch, dev, comp, copy, pipe):
         for c in range(chunks):
             K.make_ground_truth_slice(KV_SEED, 0, c, w, cfg, m, m, out=kv[w, c])
     torch.cuda.synchronize()
-    h_par = torch.empty((chunks, 2, sl), dtype=torch.uint8).pin_memory()
+    from paper_2605_00831_b200 import device as D
+    h_par = D.pinned_near((chunks, 2, sl), dev.index or 0)   # released on del (not torch's pinned cache)
     enc = encoder(scheme)
     slots = L.ptr_array([kv[w, c].data_ptr() for c in range(chunks) for w in range(8)])
     outs = L.ptr_array([h_par[c, i].data_ptr() for c in range(chunks) for i in range(2)])
@@ -1069,6 +1293,7 @@ def c3_orchestrated(torch, dev, link, k1_gbs, k2_gbs):
            "verify_gpu_chunks": res.verify_gpu_chunks,
            "decode_device_ms": round(res.reconstruct_device_ms, 2), "recover_wall_ms": round(res.wall_ms, 1),
            "parity_bytes_verified": len(res.plan.reconstruct_ids) * 2 * sl, "verified": res.verified,
+           "decoded_chunks": res.decoded_chunks, "corrupt_chunks": res.corrupt_chunks,
            "note": "wall = plan + speculative H2D/K2 overlapped with the FNV verification of the 64 entries "
                    "(reference semantics: corrupt parity -> full-recompute fallback); verify_gpu_chunks of them "
                    "upload both parity rows and are checksummed in HBM (bit-sliced GPU FNV-1a), the rest on "
@@ -1329,6 +1554,9 @@ def run_sweep(args):
 def main():
     ap = argparse.ArgumentParser(description=__doc__, formatter_class=argparse.RawDescriptionHelpFormatter)
     ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--workload", choices=sorted(WORKLOADS), default="c3",
+                    help="c3 (default, BASELINE configs[2]): 2K-token prefill chunks of Llama-3-70B; "
+                         "c2: 16-token decode blocks of Llama-3-8B, batch 32")
     ap.add_argument("--steps", type=int, default=200)
     ap.add_argument("--warmup", type=int, default=10)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
@@ -1349,6 +1577,7 @@ def main():
                     help="per-config table C1-C4 (encode+D2H, K1, recovery, rooflines, reference CPU, bit-exact)")
     ap.add_argument("--configs-only", default="", help="subset for --configs, e.g. C1,C4")
     args = ap.parse_args()
+    spawn_ranks(args)
     if args.configs:
         if args.impl == "reference":
             print(json.dumps({"impl": "reference", "unavailable": "--configs is our arm only"}))
@@ -1366,8 +1595,40 @@ def main():
         args.warmup = 3
     if args.impl == "reference":
         run_reference(args)
-    else:
+        return
+    try:
         run_ours(args)
+    except Failed as e:
+        print(f"[bench] FAILED: {e}", file=sys.stderr, flush=True)
+        sys.exit(1)
+
+
+def spawn_ranks(args) -> None:
+    """--gpus N without a torchrun environment: re-exec this command under
+    torch.distributed.run with N ranks on this node (127.0.0.1 rendezvous), so
+    `python bench.py --gpus N` and the driver's torchrun launch are the same
+    run. Under torchrun, WORLD_SIZE must equal --gpus."""
+    world = os.environ.get("WORLD_SIZE")
+    if world is not None:
+        if int(world) != args.gpus and args.gpus != 1:
+            raise SystemExit(f"bench: --gpus {args.gpus} but WORLD_SIZE={world}")
+        return
+    if args.gpus <= 1:
+        return
+    shared = os.environ.get("GS_BENCH_SHARED_GPU") == "1"
+    if not shared:
+        import torch
+        if torch.cuda.device_count() < args.gpus:
+            raise SystemExit(f"bench: --gpus {args.gpus} but only {torch.cuda.device_count()} CUDA device(s) "
+                             "are visible")
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.abspath(__file__)] + sys.argv[1:]
+    print(f"[bench] spawning {args.gpus} ranks: {' '.join(cmd)}", file=sys.stderr, flush=True)
+    sys.stdout.flush()
+    os.execv(sys.executable, cmd)
 
 
 if __name__ == "__main__":

@@ -110,40 +110,43 @@ using ConstShardSpan = std::span<const std::uint8_t>;
 
 namespace detail {
 
-struct Handles {
+// Codecs are immutable after creation and shareable across threads and
+// devices (the reference codec is safe to call from many
+// threads): one per (scheme, lost set), created once under a short lock that
+// is NOT held across the GPU round trip. Never destroyed (process lifetime),
+// so no static destructor races a call still in flight on another thread.
+struct Codecs {
   std::mutex mu;
-  std::map<std::tuple<int, int, int, std::vector<int>, bool>, gs_codec*> codecs;
-  gs_pipeline* pipe = nullptr;
-  ~Handles() {
-    for (auto& kv : codecs) gs_codec_destroy(kv.second);
-    if (pipe) gs_pipeline_destroy(pipe);
-  }
+  std::map<std::tuple<int, int, int, std::vector<int>, bool>, gs_codec*> by_key;
 };
 
-inline Handles& handles() {
-  static Handles h;
-  return h;
-}
-
-inline gs_pipeline* pipeline() {
-  auto& h = handles();
-  if (!h.pipe) check(gs_pipeline_create(0, std::size_t{128} << 20, &h.pipe), "pipeline");
-  return h.pipe;
+inline Codecs& codecs() {
+  static Codecs* c = new Codecs;
+  return *c;
 }
 
 inline gs_codec* codec(const CodingScheme& s, const std::vector<int>* lost) {
-  auto& h = handles();
+  auto& h = codecs();
   auto key = std::make_tuple(static_cast<int>(s.kind), s.n, s.k, lost ? *lost : std::vector<int>{}, lost != nullptr);
-  auto it = h.codecs.find(key);
-  if (it != h.codecs.end()) return it->second;
+  std::lock_guard<std::mutex> lk(h.mu);
+  auto it = h.by_key.find(key);
+  if (it != h.by_key.end()) return it->second;
   gs_codec* c = nullptr;
   if (lost)
     check(gs_decoder_create(static_cast<int>(s.kind), s.n, s.k, lost->data(), static_cast<int>(lost->size()), &c),
           "reconstruct");
   else
     check(gs_encoder_create(static_cast<int>(s.kind), s.n, s.k, &c), "encode");
-  h.codecs.emplace(key, c);
+  h.by_key.emplace(key, c);
   return c;
+}
+
+// The calling thread's staging pipeline on its current device (cudaGetDevice):
+// concurrent callers each get their own, on their own GPU.
+inline gs_pipeline* pipeline() {
+  gs_pipeline* p = nullptr;
+  check(gs_thread_pipeline(&p), "pipeline");
+  return p;
 }
 
 }  // namespace detail
@@ -162,7 +165,6 @@ inline std::vector<std::vector<std::uint8_t>> encode(const CodingScheme& scheme,
   std::vector<std::vector<std::uint8_t>> parity(static_cast<std::size_t>(scheme.k));
   for (auto& p : parity) p.assign(len, 0);
   if (len == 0) return parity;
-  std::lock_guard<std::mutex> lk(detail::handles().mu);
   gs_codec* c = detail::codec(scheme, nullptr);
   std::vector<const void*> in;
   std::vector<void*> out;
@@ -207,7 +209,6 @@ inline std::map<int, std::vector<std::uint8_t>> reconstruct(const CodingScheme& 
     slots[static_cast<std::size_t>(idx)] = it->second.data();
   }
   std::map<int, std::vector<std::uint8_t>> out;
-  std::lock_guard<std::mutex> lk(detail::handles().mu);
   gs_codec* c = detail::codec(scheme, &lost.lost);
   int n_out = 0;
   std::vector<int> idx(256);
@@ -238,7 +239,6 @@ inline void encode_device(const CodingScheme& scheme, std::span<const void* cons
   if (static_cast<int>(h_parity.size()) != scheme.k)
     throw std::invalid_argument("coding: expected " + std::to_string(scheme.k) + " parity buffers");
   if (len == 0) return;
-  std::lock_guard<std::mutex> lk(detail::handles().mu);
   gs_codec* c = detail::codec(scheme, nullptr);
   detail::check(gs_encode_async(c, d_shards.data(), len, h_parity.data(), compute, copy), "encode");
 }
@@ -264,7 +264,6 @@ inline void reconstruct_device(const CodingScheme& scheme, const ErasurePattern&
   for (int idx : lost.lost) data_lost += idx < scheme.n;
   if (static_cast<int>(d_out.size()) < data_lost) throw std::invalid_argument("coding: too few output buffers");
   if (len == 0 || data_lost == 0) return;
-  std::lock_guard<std::mutex> lk(detail::handles().mu);
   gs_codec* c = detail::codec(scheme, nullptr);
   detail::check(gs_reconstruct_async(c, lost.lost.data(), static_cast<int>(lost.lost.size()), d_survivors.data(),
                                      h_parity.data(), d_out.data(), len, stream),

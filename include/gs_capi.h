@@ -45,8 +45,8 @@ typedef enum {
   GS_RUNTIME_ERROR = 7  /* std::runtime_error (parity file format / integrity) */
 } gs_status;
 
-/* CodeKind (coding.hpp:19). RDP is out of scope on this path: accepted by
- * validation, rejected with GS_UNSUPPORTED by codec creation. */
+/* CodeKind (coding.hpp:19). All three run on the GPU (RDP: gs_rdp.cuh,
+ * position-dependent -- byte-range striping across ranks refuses it). */
 typedef enum { GS_XOR = 0, GS_RDP = 1, GS_RS = 2 } gs_code_kind;
 
 typedef struct gs_codec gs_codec;       /* immutable coefficient plan + kernel choice */
@@ -58,9 +58,9 @@ typedef struct gs_verify gs_verify;     /* an in-flight split parity verificatio
 const char* gs_status_string(int status);
 const char* gs_last_error(void);
 int gs_abi_version(void);
-/* Drop queued runtime-specialisation (NVRTC) builds and wait for the one in
- * flight. Call before a process exits (the Python package does, atexit): a
- * build still running while NVRTC's statics are destroyed can crash. */
+/* Drop queued runtime-specialisation builds and wait for the one in flight
+ * (tests that want a quiet library). NOT needed before exit: NVRTC runs in a
+ * helper process (gs_jit_helper), so a process may exit mid-build. */
 int gs_jit_quiesce(void);
 /* Number of kernels this library launched in this process (all devices). */
 uint64_t gs_kernel_launches(void);
@@ -262,6 +262,13 @@ int gs_encode_async(const gs_codec* enc, const void* const* d_shards, size_t len
 int gs_reconstruct_async(const gs_codec* enc, const int* lost, int n_lost, const void* const* d_survivors,
                          const void* const* h_parity, void* const* d_out, size_t len, void* stream);
 int gs_sync(void* stream);
+/* The calling thread's default pipeline for its CURRENT device
+ * (cudaGetDevice), created on first use and owned by the library: what the
+ * C++ drop-in (ghostserve_gpu/coding.hpp) runs its host-buffer calls on, so
+ * concurrent callers never share a staging ring and each uses its own GPU. */
+int gs_thread_pipeline(gs_pipeline** out);
+/* The device a pipeline was created on. */
+int gs_pipeline_device(gs_pipeline* p, int* device);
 
 /* ---- KV data model (kv_layout.hpp) ------------------------------------- */
 /* slice_bytes (kv_layout.hpp:40-45), validate (:21-28) */

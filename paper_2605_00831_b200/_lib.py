@@ -64,6 +64,8 @@ SIGNATURES = {
     "gs_encode_async": (_i, [_vp, _vpp, _sz, _vpp, _vp, _vp]),
     "gs_reconstruct_async": (_i, [_vp, _ip, _i, _vpp, _vpp, _vpp, _sz, _vp]),
     "gs_sync": (_i, [_vp]),
+    "gs_thread_pipeline": (_i, [_vpp]),
+    "gs_pipeline_device": (_i, [_vp, _ip]),
     "gs_pipeline_set_timing": (_i, [_vp, _i]),
     "gs_pipeline_kernel_time": (_i, [_vp, C.POINTER(C.c_double), C.POINTER(C.c_double), _ip, _u64p]),
     "gs_slice_bytes": (_i, [_i, _i, _i, _i, _u32, _u64p]),
@@ -136,10 +138,6 @@ def lib() -> C.CDLL:
                 fn.restype = res
                 fn.argtypes = args
             _lib = handle
-            # Python's atexit runs before the C++ static teardown: no NVRTC build
-            # may still be running then (gs_jit_quiesce).
-            import atexit
-            atexit.register(handle.gs_jit_quiesce)
     return _lib
 
 

@@ -1578,6 +1578,17 @@ std::map<std::tuple<int, int, int, std::vector<int>>, gs_codec*> g_dec_cache;
 
 int gs_codec_create(int kind, int n, int k, gs_codec** out) { return gs_encoder_create(kind, n, k, out); }
 
+int gs_pipeline_device(gs_pipeline* p, int* device) {
+  if (!p || !device) return fail(GS_INVALID_ARGUMENT, "pipeline_device: NULL argument");
+  *device = p->device;
+  return GS_OK;
+}
+
+int gs_thread_pipeline(gs_pipeline** out) {
+  if (!out) return fail(GS_INVALID_ARGUMENT, "thread_pipeline: NULL out");
+  return default_pipeline(out);
+}
+
 int gs_encode_async(const gs_codec* enc, const void* const* d_shards, size_t len, void* const* h_parity,
                     void* compute, void* copy) {
   if (!enc) return fail(GS_INVALID_ARGUMENT, "encode_async: NULL codec");

@@ -1,17 +1,20 @@
 // gs_jit.cu -- runtime-specialised kernels (see gs_jit.hpp).
 //
-// NVRTC is dlopen'ed and the driver's module/launch entry points come from
-// cudaGetDriverEntryPoint, so the library has no link-time dependency on
-// either: without them JIT is simply off and the generic kernel serves.
+// NVRTC runs in a helper process (gs_jit_helper, see compile()) and the
+// driver's module/launch entry points come from cudaGetDriverEntryPoint, so
+// the library has no link-time dependency on either: without them JIT is
+// simply off and the generic kernel serves.
 #include "gs_jit.hpp"
 
 #include <cuda.h>
 #include <dlfcn.h>
-#include <nvrtc.h>
+#include <spawn.h>
+#include <sys/wait.h>
 #include <sys/stat.h>
 #include <unistd.h>
 
 #include <algorithm>
+#include <cerrno>
 #include <atomic>
 #include <condition_variable>
 #include <cstdio>
@@ -28,6 +31,8 @@
 #include <vector>
 
 #include "gs_special.cuh"
+
+extern char** environ;
 
 namespace gsb {
 
@@ -57,45 +62,6 @@ std::atomic<bool> g_jit_on{[] {
   const char* e = std::getenv("GS_JIT");
   return !(e && std::atoi(e) == 0);
 }()};
-
-struct Nvrtc {
-  bool ok = false;
-  decltype(&nvrtcCreateProgram) create = nullptr;
-  decltype(&nvrtcCompileProgram) compile = nullptr;
-  decltype(&nvrtcGetProgramLogSize) log_size = nullptr;
-  decltype(&nvrtcGetProgramLog) log = nullptr;
-  decltype(&nvrtcGetCUBINSize) cubin_size = nullptr;
-  decltype(&nvrtcGetCUBIN) cubin = nullptr;
-  decltype(&nvrtcAddNameExpression) add_name = nullptr;
-  decltype(&nvrtcGetLoweredName) lowered = nullptr;
-  decltype(&nvrtcDestroyProgram) destroy = nullptr;
-};
-
-Nvrtc& nvrtc() {
-  static Nvrtc n = [] {
-    Nvrtc r;
-    void* h = nullptr;
-    for (const char* name : {"libnvrtc.so.12", "libnvrtc.so", "/usr/local/cuda/lib64/libnvrtc.so.12"})
-      if ((h = dlopen(name, RTLD_NOW | RTLD_LOCAL))) break;
-    if (!h) return r;
-#define GS_SYM(fn, member)                                                \
-  r.member = reinterpret_cast<decltype(r.member)>(dlsym(h, #fn));         \
-  if (!r.member) return r;
-    GS_SYM(nvrtcCreateProgram, create)
-    GS_SYM(nvrtcCompileProgram, compile)
-    GS_SYM(nvrtcGetProgramLogSize, log_size)
-    GS_SYM(nvrtcGetProgramLog, log)
-    GS_SYM(nvrtcGetCUBINSize, cubin_size)
-    GS_SYM(nvrtcGetCUBIN, cubin)
-    GS_SYM(nvrtcAddNameExpression, add_name)
-    GS_SYM(nvrtcGetLoweredName, lowered)
-    GS_SYM(nvrtcDestroyProgram, destroy)
-#undef GS_SYM
-    r.ok = true;
-    return r;
-  }();
-  return n;
-}
 
 struct Driver {
   bool ok = false;
@@ -179,6 +145,11 @@ bool load_cached(JitKernel& k, const std::string& base) {
   return !k.cubin.empty() && !k.lowered.empty();
 }
 
+// The compile runs in a helper process (gs_jit_helper next to this library):
+// NVRTC is never loaded into the host process, so nothing of it can be torn
+// down under an in-flight build when the process exits (the worker thread
+// here only spawns, waits and reads files). The helper writes the cubin into
+// the disk cache, which this process then loads.
 void compile(JitKernel& k) {
   const std::string base = cache_dir() + "/" + [&] {
     char b[32];
@@ -189,49 +160,39 @@ void compile(JitKernel& k) {
     k.log = "disk cache: " + base + ".cubin";
     return;
   }
-  Nvrtc& nv = nvrtc();
-  const std::string inc = csrc_dir();
-  if (!nv.ok || inc.empty()) {
-    k.log = !nv.ok ? "libnvrtc not available" : "kernel headers (csrc/) not found next to the library";
+  const std::string inc = csrc_dir(), helper = lib_dir() + "/gs_jit_helper";
+  struct stat hs {};
+  if (inc.empty() || stat(helper.c_str(), &hs) != 0) {
+    k.log = inc.empty() ? "kernel headers (csrc/) not found next to the library" : "gs_jit_helper not built";
     throw 0;
   }
-  const std::string src = source_for(k);
-  nvrtcProgram prog;
-  if (nv.create(&prog, src.c_str(), "gs_jit.cu", 0, nullptr, nullptr) != NVRTC_SUCCESS) {
-    k.log = "nvrtcCreateProgram failed";
-    throw 0;
-  }
-  nv.add_name(prog, kKernelExpr);
-  const std::string arch = "--gpu-architecture=" + k.arch, incl = "-I" + inc;
-  const char* opts[] = {arch.c_str(), "-std=c++20", incl.c_str(), "-lineinfo"};
-  const nvrtcResult r = nv.compile(prog, 4, opts);
-  size_t ls = 0;
-  nv.log_size(prog, &ls);
-  std::string log(ls, '\0');
-  if (ls) nv.log(prog, log.data());
-  k.log = log;
-  if (r != NVRTC_SUCCESS) {
-    nv.destroy(&prog);
-    throw 0;
-  }
-  size_t n = 0;
-  nv.cubin_size(prog, &n);
-  k.cubin.resize(n);
-  nv.cubin(prog, k.cubin.data());
-  const char* low = nullptr;
-  nv.lowered(prog, kKernelExpr, &low);
-  k.lowered = low ? low : "";
-  nv.destroy(&prog);
-  // best-effort disk cache (write to a temp name, then rename: concurrent
-  // processes never read a torn file)
-  const std::string tmp = base + ".tmp" + std::to_string(::getpid());
+  const std::string src = base + ".src" + std::to_string(::getpid()) + ".cu";
   {
-    std::ofstream f(tmp + ".cubin", std::ios::binary), nf(tmp + ".name");
-    f.write(k.cubin.data(), static_cast<std::streamsize>(k.cubin.size()));
-    nf << k.lowered << "\n";
+    std::ofstream f(src);
+    f << source_for(k);
+    if (!f) {
+      k.log = "cannot write " + src;
+      throw 0;
+    }
   }
-  std::rename((tmp + ".name").c_str(), (base + ".name").c_str());
-  std::rename((tmp + ".cubin").c_str(), (base + ".cubin").c_str());
+  std::string a_arch = k.arch, a_expr = kKernelExpr;
+  char* argv[] = {const_cast<char*>(helper.c_str()), a_arch.data(), const_cast<char*>(inc.c_str()),
+                  const_cast<char*>(src.c_str()), const_cast<char*>(base.c_str()), a_expr.data(), nullptr};
+  pid_t pid = 0;
+  int status = 0;
+  const int sp = posix_spawn(&pid, helper.c_str(), nullptr, nullptr, argv, environ);
+  if (sp == 0) {
+    while (waitpid(pid, &status, 0) < 0 && errno == EINTR) {
+    }
+  }
+  std::remove(src.c_str());
+  if (sp != 0 || !WIFEXITED(status) || WEXITSTATUS(status) != 0 || !load_cached(k, base)) {
+    std::ifstream lf(base + ".log");
+    k.log = std::string("gs_jit_helper failed: ") +
+            std::string(std::istreambuf_iterator<char>(lf), std::istreambuf_iterator<char>());
+    throw 0;
+  }
+  k.log = "compiled by gs_jit_helper: " + base + ".cubin";
 }
 
 // one background compile worker
@@ -239,10 +200,9 @@ struct Worker {
   std::mutex mu;
   std::condition_variable cv, idle_cv;
   std::deque<JitKernel*> q;
-  bool started = false, busy = false, stopping = false;
+  bool started = false, busy = false;
   void push(JitKernel* k) {
     std::lock_guard<std::mutex> lk(mu);
-    if (stopping) return;  // process exiting: the kernel stays pending, callers use the generic kernel
     q.push_back(k);
     if (!started) {
       started = true;
@@ -251,19 +211,11 @@ struct Worker {
     cv.notify_one();
   }
   void run() {
-    // NVRTC builds internal statics lazily during its first compile, and their
-    // destructors run at exit in reverse registration order. A trivial
-    // warm-up compile constructs them first; the exit hook registered after it
-    // therefore runs BEFORE they are destroyed and waits for any compile in
-    // flight, so a process that exits mid-compile does not crash in NVRTC.
-    warm_up();
-    std::atexit(+[] { worker_shutdown(); });
     for (;;) {
       JitKernel* k;
       {
         std::unique_lock<std::mutex> lk(mu);
-        cv.wait(lk, [&] { return stopping || !q.empty(); });
-        if (stopping) return;
+        cv.wait(lk, [&] { return !q.empty(); });
         k = q.front();
         q.pop_front();
         busy = true;
@@ -294,33 +246,12 @@ struct Worker {
     q.clear();
     idle_cv.wait(lk, [&] { return !busy; });
   }
-  // at exit: no new compiles; wait for the one in flight
-  void shutdown() {
-    std::unique_lock<std::mutex> lk(mu);
-    stopping = true;
-    cv.notify_all();
-    idle_cv.wait(lk, [&] { return !busy; });
-  }
-  static void worker_shutdown();
-  static void warm_up() {
-    Nvrtc& nv = nvrtc();
-    if (!nv.ok) return;
-    nvrtcProgram prog;
-    if (nv.create(&prog, "extern \"C\" __global__ void gs_jit_warm_up() {}", "gs_jit_warm_up.cu", 0, nullptr,
-                  nullptr) != NVRTC_SUCCESS)
-      return;
-    const char* opts[] = {"--gpu-architecture=compute_100a"};
-    nv.compile(prog, 1, opts);
-    nv.destroy(&prog);
-  }
 };
 
 Worker& worker() {
   static Worker* w = new Worker;  // intentionally leaked: the detached thread outlives statics
   return *w;
 }
-
-void Worker::worker_shutdown() { worker().shutdown(); }
 
 }  // namespace
 

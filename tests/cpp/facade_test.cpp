@@ -3,11 +3,15 @@
 // ghostserve::encode / reconstruct (coding_test.cpp:53-70, acceptance.cpp:
 // 100-137), and checks every byte against the CPU oracle (test
 // infrastructure). Exit code = number of failed checks. Needs a GPU.
+#include <atomic>
 #include <cstdio>
 #include <cstdint>
+#include <cstdlib>
 #include <cstring>
+#include <algorithm>
 #include <map>
 #include <stdexcept>
+#include <thread>
 #include <vector>
 
 #include <cuda_runtime.h>
@@ -17,7 +21,7 @@
 
 namespace gs = ghostserve_gpu;
 
-static int failures = 0;
+static std::atomic<int> failures{0};
 #define CHECK(cond, ...)                \
   do {                                  \
     if (!(cond)) {                      \
@@ -173,7 +177,63 @@ int main() {
     for (void* h : hpar) cudaFreeHost(h);
     cudaStreamDestroy(st);
   }
-  std::printf("facade_test: %d failure(s), %llu kernels launched\n", failures,
+  // concurrency (the reference codec is safe to call from
+  // many threads): 4 threads, thread t on device t % ndev, each driving
+  // encode / reconstruct through its own per-(thread, device) pipeline with
+  // no facade-wide lock; every byte checked against the oracle.
+  {
+    int ndev = 0;
+    cudaGetDeviceCount(&ndev);
+    std::vector<std::thread> pool;
+    std::atomic<int> calls{0};
+    for (int t = 0; t < 4; ++t) {
+      pool.emplace_back([t, ndev, &calls] {
+        const int dev = t % std::max(ndev, 1);
+        cudaSetDevice(dev);
+        gs_pipeline* p = nullptr;
+        int pdev = -1;
+        CHECK(gs_thread_pipeline(&p) == GS_OK && gs_pipeline_device(p, &pdev) == GS_OK && pdev == dev,
+              "thread %d: pipeline on device %d, expected %d", t, pdev, dev);
+        const gs::CodingScheme mix[] = {gs::CodingScheme::reed_solomon(8, 2), gs::CodingScheme::reed_solomon(6, 2),
+                                        gs::CodingScheme::xor_code(8), gs::CodingScheme::reed_solomon(4, 2)};
+        for (int it = 0; it < 12; ++it) {
+          const auto& sc = mix[(t + it) % 4];
+          const size_t len = (size_t{1} << 18) + 16 * static_cast<size_t>(it * 7 + t);
+          const auto data = shards(sc.n, len, 1000 + 100 * static_cast<uint64_t>(t) + it);
+          const auto parity = gs::encode(sc, data);
+          std::vector<const uint8_t*> dp;
+          for (auto& d : data) dp.push_back(d.data());
+          std::vector<std::vector<uint8_t>> want(static_cast<size_t>(sc.k), std::vector<uint8_t>(len));
+          std::vector<uint8_t*> wp;
+          for (auto& w : want) wp.push_back(w.data());
+          gso_encode(static_cast<int>(sc.kind), sc.n, sc.k, dp.data(), len, wp.data());
+          CHECK(parity == want, "thread %d it %d: parity mismatch", t, it);
+          gs::ErasurePattern pat({(t + it) % sc.n});
+          std::map<int, gs::ConstShardSpan> surv;
+          for (int i = 0; i < sc.n; ++i)
+            if (!pat.contains(i)) surv[i] = gs::ConstShardSpan(data[static_cast<size_t>(i)]);
+          for (int i = 0; i < sc.k; ++i) surv[sc.n + i] = gs::ConstShardSpan(parity[static_cast<size_t>(i)]);
+          auto rebuilt = gs::reconstruct(sc, surv, pat);
+          const int lost = pat.lost[0];
+          CHECK(rebuilt.count(lost) && rebuilt.at(lost) == data[static_cast<size_t>(lost)],
+                "thread %d it %d: shard %d not rebuilt", t, it, lost);
+          calls += 2;
+        }
+      });
+    }
+    for (auto& th : pool) th.join();
+    std::printf("facade_test: concurrent: 4 threads on %d device(s), %d calls\n", std::max(ndev, 1), calls.load());
+  }
+  // a codec outside the compiled registry: its first launch requests a
+  // runtime-specialised build (out-of-process NVRTC) and the process exits
+  // right after, possibly mid-compile -- which must not crash
+  if (!std::getenv("GS_FACADE_NO_JIT_EXIT")) {
+    const auto odd = gs::CodingScheme::reed_solomon(7, 3);
+    const auto d7 = shards(7, 4096, 77);
+    const auto p7 = gs::encode(odd, d7);
+    std::printf("facade_test: RS(7,3) encoded (%zu parity rows); exiting with its build in flight\n", p7.size());
+  }
+  std::printf("facade_test: %d failure(s), %llu kernels launched\n", failures.load(),
               static_cast<unsigned long long>(gs_kernel_launches()));
-  return failures;
+  return failures.load();
 }

@@ -49,6 +49,7 @@ def main():
     ap.add_argument("--source", default="")
     ap.add_argument("--launch", default="")
     ap.add_argument("--note", default="")
+    ap.add_argument("--lib-sha", default="", help="sha256[:16] of the libghostserve_b200.so that was profiled")
     a = ap.parse_args()
     raw = subprocess.check_output(["ncu", "-i", a.report, "--page", "raw", "--csv"]).decode()
     rows = list(csv.reader(io.StringIO(raw)))
@@ -73,7 +74,9 @@ def main():
         if stalls:
             cap["stalls_per_issue"] = dict(sorted(stalls.items(), key=lambda kv: -kv[1])[:12])
         caps.append(cap)
-    out = {"source": a.source, "launch": a.launch, "note": a.note, "captures": caps}
+    import os
+    out = {"source": a.source, "launch": a.launch, "note": a.note, "file": os.path.basename(a.report),
+           "lib_sha256_16": a.lib_sha, "captures": caps}
     if caps:
         c = caps[-1]
         out["kernel"] = c["kernel"]
