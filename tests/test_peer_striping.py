@@ -99,11 +99,23 @@ def test_striped_partition_reassembles_parity_cpu():
     _run(_cpu_worker)
 
 
-def _gpu_worker(rank, world, port, q):
+def _enable_peers(rank, world):
+    """Distinct devices: peer access both ways (gs_peer_enable), on top of the
+    lazy peer access the IPC mapping requests (cudaIpcMemLazyEnablePeerAccess)."""
+    from paper_2605_00831_b200 import _lib as L
+    for r in range(world):
+        if r != rank:
+            assert L.lib().gs_peer_enable(rank, r) == 0, L.last_error()
+
+
+def _gpu_worker(rank, world, port, q, distinct=False):
     import sys
     sys.path.insert(0, ROOT)
     try:
-        torch.cuda.set_device(0)
+        dev = rank if distinct else 0
+        torch.cuda.set_device(dev)
+        if distinct:
+            _enable_peers(rank, world)
         from paper_2605_00831_b200 import device as D
         from paper_2605_00831_b200.coding import CodingScheme, ErasurePattern
         from paper_2605_00831_b200.peer import (PeerGroup, ShardLayout, encode_striped,
@@ -116,7 +128,7 @@ def _gpu_worker(rank, world, port, q):
         pg = PeerGroup()
         bases = pg.share(mine)
         h_par = torch.zeros((S, K, LEN), dtype=torch.uint8).pin_memory()
-        pipe = D.Pipeline(0, 1 << 20)
+        pipe = D.Pipeline(dev, 1 << 20)
         comp, copy = torch.cuda.Stream(), torch.cuda.Stream()
         torch.cuda.synchronize()
         dist.barrier()
@@ -170,13 +182,16 @@ def test_ipc_striped_encode_and_rebuild_two_processes_one_gpu():
     _run(_gpu_worker)
 
 
-def _gpu_worker_local(rank, world, port, q):
+def _gpu_worker_local(rank, world, port, q, distinct=False):
     """The C3 flow at N ranks: each rank keeps ONLY its byte range of the
     parity in a range-local pinned slab ([S, K, len_r]), and rebuilds from it."""
     import sys
     sys.path.insert(0, ROOT)
     try:
-        torch.cuda.set_device(0)
+        dev = rank if distinct else 0
+        torch.cuda.set_device(dev)
+        if distinct:
+            _enable_peers(rank, world)
         from paper_2605_00831_b200 import device as D
         from paper_2605_00831_b200.coding import CodingScheme, ErasurePattern
         from paper_2605_00831_b200.peer import (PeerGroup, ShardLayout, plan_encode_striped,
@@ -188,7 +203,7 @@ def _gpu_worker_local(rank, world, port, q):
         mine = torch.stack([torch.from_numpy(np.stack(_shards(s)[rank * nl:(rank + 1) * nl])) for s in range(S)]).cuda()
         pg = PeerGroup()
         bases = pg.share(mine)
-        pipe = D.Pipeline(0, 1 << 20)
+        pipe = D.Pipeline(dev, 1 << 20)
         comp, copy = torch.cuda.Stream(), torch.cuda.Stream()
         from paper_2605_00831_b200.peer import stripe_range
         off, ln = stripe_range(LEN, rank, world)
@@ -235,6 +250,21 @@ def test_ipc_striped_range_local_parity_two_processes_one_gpu():
     if not torch.cuda.is_available():
         pytest.fail("GPU test collected without a CUDA device")
     _run(_gpu_worker_local)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("worker", ["full", "range_local"])
+def test_ipc_striped_two_distinct_devices(worker):
+    """The same striped encode + rebuild with each rank on its OWN GPU: K1
+    reads the peer's shards over NVLink through the IPC mapping, K2 stores
+    the rebuilt range into the owner's HBM on the other device (peer access
+    enabled both ways). Needs two visible GPUs (skipped on a 1-GPU box)."""
+    import functools
+    if not torch.cuda.is_available():
+        pytest.fail("GPU test collected without a CUDA device")
+    if torch.cuda.device_count() < 2:
+        pytest.skip("needs 2 visible GPUs (this box has 1)")
+    _run(functools.partial(_gpu_worker if worker == "full" else _gpu_worker_local, distinct=True))
 
 
 def test_rotating_assignment_covers_every_stripe_once():
