@@ -31,6 +31,7 @@
 
 #include <algorithm>
 #include <cstdarg>
+#include <cstdlib>
 #include <cstdint>
 #include <cstdio>
 #include <mutex>
@@ -378,6 +379,259 @@ cudaError_t pair_and_scan(const FnvJob& j, int grid, int n_chains, uint8_t* scra
   return cudaGetLastError();
 }
 
+
+// ===========================================================================
+// Single-pass windowed FNV (the default; GS_FNV_LEGACY=1 selects the
+// multi-pass kernels above for A/B).
+//
+// The multi-pass form streams the chain five times and a low-byte scratch
+// array eight times: ~14 B of HBM per chain byte. Here every chain byte is
+// read ONCE: a cluster of kWCS CTAs holds a window of kWCS x 32 KiB in
+// registers (64 B of data + 64 B of low-byte state per thread) and resolves
+// all eight low-byte bits on chip, one bit per round:
+//   * round K: e-bits of bit K from the TRUE bits < K (e_nibble<K>), XOR
+//     prefix per thread / warp (ballot) / CTA (smem) / cluster (DSMEM slots +
+//     barrier.cluster) -- the window's own bit-K aggregate;
+//   * the window's ENTRY bit K comes from its predecessors by a decoupled
+//     look-back over a per-window flag word in global memory (bit-K totals
+//     and exit bits, published with st.release as soon as they are known),
+//     so the windows of one chain are resolved by many clusters at once;
+//   * then the final linear sum  sum_i d_i P^(n-i)  of the window, atomically
+//     added to the chain's hash (h0 P^n added by k_fnv_init).
+// Windows are handed out in order (window-major across the chains) by an
+// atomic counter, so a window's predecessors are always owned by running
+// clusters (no residency deadlock).
+// ===========================================================================
+constexpr int kWT = 512;                         // threads per CTA
+constexpr uint32_t kWB = kWT * kFPer;            // 32 KiB per CTA per window
+constexpr int kWCS = 8;                          // CTAs per cluster (portable size)
+constexpr uint64_t kWin = static_cast<uint64_t>(kWB) * kWCS;  // 256 KiB per window
+
+__device__ __forceinline__ uint32_t ld_acquire_u32(const uint32_t* p) {
+  uint32_t v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release_u32(uint32_t* p, uint32_t v) {
+  asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ uint32_t cluster_rank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ void cluster_sync_all() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+// Store a u32 into the same smem variable of CTA `rank` of this cluster.
+__device__ __forceinline__ void st_cluster_u32(uint32_t* local, uint32_t rank, uint32_t v) {
+  uint32_t a = static_cast<uint32_t>(__cvta_generic_to_shared(local)), ra;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(ra) : "r"(a), "r"(rank));
+  asm volatile("st.shared::cluster.u32 [%0], %1;" ::"r"(ra), "r"(v) : "memory");
+}
+
+// Window flag word (one per window, zeroed per call):
+//   bits 0-7 : bit-K totals of the window's e-bits   bits 16-23: totals valid
+//   bits 8-15: exit bits (entry ^ total)             bits 24-31: exit valid
+// Entry bit K of window w of a chain (w > 0) = exit bit K of window w-1
+// = h0_K ^ XOR of the totals of windows 0..w-1. Warp 0 looks back over up to
+// 32 predecessors per step: the nearest one with its exit bit published ends
+// the walk, nearer ones contribute their totals (spin while any is missing).
+template <int K>
+__device__ __forceinline__ uint32_t lookback_entry(const uint32_t* flags, uint32_t gw, uint32_t w, uint32_t nc,
+                                                   uint64_t h0) {
+  const int lane = threadIdx.x & 31;
+  uint32_t acc = 0;
+  uint32_t back = 0;  // predecessors already folded into acc
+  for (;;) {
+    // lane l inspects predecessor w - 1 - back - l (if it exists)
+    const uint32_t dist = back + lane + 1;
+    const bool exists = dist <= w;
+    uint32_t v = 0;
+    bool have_exit = false, have_total = false;
+    if (exists) {
+      v = ld_acquire_u32(flags + (gw - dist * nc));
+      have_exit = (v >> (24 + K)) & 1u;
+      have_total = (v >> (16 + K)) & 1u;
+    }
+    // the chain start acts as a predecessor whose exit bits are h0's
+    const bool start = !exists && dist == w + 1;
+    const uint32_t stop_bal = __ballot_sync(0xFFFFFFFFu, have_exit || start);
+    const int first = stop_bal ? __ffs(stop_bal) - 1 : 32;
+    // every lane nearer than `first` must contribute its total
+    const uint32_t need = first >= 32 ? 0xFFFFFFFFu : ((1u << first) - 1u);
+    const uint32_t ok_bal = __ballot_sync(0xFFFFFFFFu, have_total);
+    if ((ok_bal & need) != need) continue;  // a nearer total is not published yet: spin
+    const uint32_t tot = __ballot_sync(0xFFFFFFFFu, have_total && ((v >> K) & 1u)) & need;
+    acc ^= __popc(tot) & 1u;
+    if (first < 32) {
+      const uint32_t ex = __shfl_sync(0xFFFFFFFFu, start ? static_cast<uint32_t>(h0 >> K) : (v >> (8 + K)), first);
+      return acc ^ (ex & 1u);
+    }
+    back += 32;
+  }
+}
+
+struct WinShared {
+  uint64_t pw[kWT];              // P^(64 t)
+  uint32_t warp_par[kWT / 32];
+  uint32_t cta_tot[8][kWCS];     // [round][cluster rank], written by every CTA of the cluster
+  uint32_t gw;                   // window index, written by rank 0
+  uint32_t entry;                // entry bit of the current round
+  unsigned long long wsum[kWT / 32];
+  uint64_t pblk;
+};
+
+template <int K>
+__device__ __forceinline__ void win_round(WinShared& sh, const FnvJob& j, uint32_t* flags, uint32_t gw, uint32_t w,
+                                          uint32_t nc, uint64_t h0, uint32_t rank, int nvalid, const uint4 (&d)[4], uint4 (&s)[4],
+                                          uint32_t& flag_word) {
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  // e-bits of bit K from the true bits < K held in s
+  uint64_t eK = 0;
+#pragma unroll
+  for (int q = 0; q < 4; ++q)
+#pragma unroll
+    for (int x = 0; x < 4; ++x)
+      if (q < nvalid)
+        eK |= static_cast<uint64_t>(e_nibble<K>(wd(s[q], x), wd(const_cast<uint4&>(d[q]), x))) << (16 * q + 4 * x);
+  uint32_t par;
+  uint64_t rel = exclusive_xor(eK, par);
+  const uint32_t bal = __ballot_sync(0xFFFFFFFFu, par);
+  uint32_t carry = __popc(bal & ((1u << lane) - 1u)) & 1u;
+  if (lane == 0) sh.warp_par[warp] = __popc(bal) & 1u;
+  __syncthreads();
+  uint32_t cta_tot = 0;
+#pragma unroll
+  for (int x = 0; x < kWT / 32; ++x) {
+    if (x < warp) carry ^= sh.warp_par[x];
+    cta_tot ^= sh.warp_par[x];
+  }
+  if (tid < kWCS) st_cluster_u32(&sh.cta_tot[K][rank], static_cast<uint32_t>(tid), cta_tot);
+  cluster_sync_all();
+  uint32_t win_tot = 0;
+#pragma unroll
+  for (int r = 0; r < kWCS; ++r) {
+    const uint32_t t = sh.cta_tot[K][r];
+    if (static_cast<uint32_t>(r) < rank) carry ^= t;
+    win_tot ^= t;
+  }
+  if (warp == 0) {
+    // publish this window's bit-K total first (successors can fold it in),
+    // then find the entry bit and publish the exit bit
+    if (rank == 0 && lane == 0) {
+      flag_word |= (win_tot << K) | (1u << (16 + K));
+      st_release_u32(flags + gw, flag_word);
+    }
+    uint32_t entry = w == 0 ? static_cast<uint32_t>(h0 >> K) & 1u : lookback_entry<K>(flags, gw, w, nc, h0);
+    if (lane == 0) {
+      sh.entry = entry;
+      if (rank == 0) {
+        flag_word |= ((entry ^ win_tot) << (8 + K)) | (1u << (24 + K));
+        st_release_u32(flags + gw, flag_word);
+      }
+    }
+  }
+  __syncthreads();
+  carry ^= sh.entry;
+  if (carry) rel = ~rel;
+#pragma unroll
+  for (int q = 0; q < 4; ++q)
+#pragma unroll
+    for (int x = 0; x < 4; ++x)
+      wd(s[q], x) |= spread_nibble(static_cast<uint32_t>(rel >> (16 * q + 4 * x)) & 0xFu) << K;
+  __syncthreads();  // sh.entry / warp_par reuse by the next round
+}
+
+__global__ void __cluster_dims__(kWCS, 1, 1) __launch_bounds__(kWT, 2)
+    k_fnv_window(const FnvJob j, uint64_t h0, uint32_t nc, uint32_t total_windows, uint32_t* counter,
+                 uint32_t* flags, unsigned long long* __restrict__ out) {
+  __shared__ WinShared sh;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const uint32_t rank = cluster_rank();
+  sh.pw[tid] = pow64(kFnvP, static_cast<uint64_t>(kFPer) * tid);
+  for (;;) {
+    if (rank == 0 && tid == 0) {
+      const uint32_t g = atomicAdd(counter, 1u);
+      for (int r = 0; r < kWCS; ++r) st_cluster_u32(&sh.gw, static_cast<uint32_t>(r), g);
+    }
+    cluster_sync_all();  // sh.gw visible in every CTA (also orders windows)
+    const uint32_t gw = sh.gw;
+    if (gw >= total_windows) break;
+    // window-major order: the windows in flight at once belong to different
+    // chains as far as there are chains, so a window's predecessor (same
+    // chain, gw - nc) has usually finished and the look-back is one read
+    const uint32_t w = gw / nc, c = gw - w * nc;
+    const uint64_t cta0 = static_cast<uint64_t>(w) * kWin + static_cast<uint64_t>(rank) * kWB;
+    const uint64_t pos0 = cta0 + static_cast<uint64_t>(tid) * kFPer;
+    uint4 d[4];
+    const int nvalid = load_groups(j, c, pos0, d);
+    uint4 s[4];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) s[q] = make_uint4(0, 0, 0, 0);
+    uint32_t fw = 0;
+    win_round<0>(sh, j, flags, gw, w, nc, h0, rank, nvalid, d, s, fw);
+    win_round<1>(sh, j, flags, gw, w, nc, h0, rank, nvalid, d, s, fw);
+    win_round<2>(sh, j, flags, gw, w, nc, h0, rank, nvalid, d, s, fw);
+    win_round<3>(sh, j, flags, gw, w, nc, h0, rank, nvalid, d, s, fw);
+    win_round<4>(sh, j, flags, gw, w, nc, h0, rank, nvalid, d, s, fw);
+    win_round<5>(sh, j, flags, gw, w, nc, h0, rank, nvalid, d, s, fw);
+    win_round<6>(sh, j, flags, gw, w, nc, h0, rank, nvalid, d, s, fw);
+    win_round<7>(sh, j, flags, gw, w, nc, h0, rank, nvalid, d, s, fw);
+    // sum over the thread's bytes of d_i P^(tend - i), four 16-byte Horner chains
+    uint64_t accq[4] = {0, 0, 0, 0};
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      if (q < nvalid) {
+#pragma unroll
+        for (int x = 0; x < 4; ++x) {
+          const uint32_t sw = wd(s[q], x), xw = sw ^ wd(d[q], x);
+#pragma unroll
+          for (int by = 0; by < 4; ++by) {
+            const int64_t di = static_cast<int64_t>((xw >> (8 * by)) & 0xFFu) -
+                               static_cast<int64_t>((sw >> (8 * by)) & 0xFFu);
+            accq[q] = (accq[q] + static_cast<uint64_t>(di)) * kFnvP;
+          }
+        }
+      }
+    }
+    constexpr uint64_t kP16 = [] {
+      uint64_t r = 1;
+      for (int i = 0; i < 16; ++i) r *= kFnvP;
+      return r;
+    }();
+    uint64_t acc = 0;
+#pragma unroll
+    for (int q = 0; q < 4; ++q)
+      if (q < nvalid) acc = acc * kP16 + accq[q];
+    const uint64_t cend = cta0 + kWB;
+    if (tid == 0) sh.pblk = cend <= j.n ? pow64(kFnvP, j.n - cend) : 0;
+    __syncthreads();
+    uint64_t contrib = 0;
+    if (nvalid > 0) {
+      const uint64_t tend = pos0 + 16u * nvalid;
+      contrib = acc * (cend <= j.n ? sh.pblk * sh.pw[kWT - 1 - tid] : pow64(kFnvP, j.n - tend));
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) contrib += __shfl_xor_sync(0xFFFFFFFFu, contrib, o);
+    if (lane == 0) sh.wsum[warp] = contrib;
+    __syncthreads();
+    if (tid == 0) {
+      uint64_t sum = 0;
+#pragma unroll
+      for (int x = 0; x < kWT / 32; ++x) sum += sh.wsum[x];
+      atomicAdd(out + c, static_cast<unsigned long long>(sum));
+    }
+    // the next window's cluster barrier (sh.gw) also separates sh.pblk / wsum reuse
+  }
+}
+
+const bool g_fnv_legacy = [] {
+  const char* e = std::getenv("GS_FNV_LEGACY");
+  return e && std::atoi(e) != 0;
+}();
+int g_win_clusters = 0;
+
 int g_sms = 0;
 std::mutex g_pool_mu;
 std::set<int> g_pool_tuned;
@@ -412,6 +666,52 @@ extern "C" int gs_fnv1a64_device(const void* const* bufs, int n_chains, int k, u
     }
   }
   const uint64_t n = static_cast<uint64_t>(k) * len;
+  if (!g_fnv_legacy) {
+    k_fnv_init<<<(n_chains + 255) / 256, 256, 0, st>>>(d_out, n_chains, h0, n);
+    if ((e = cudaGetLastError()) != cudaSuccess) return ffail(GS_CUDA_ERROR, "fnv init: %s", cudaGetErrorString(e));
+    if (n == 0) return GS_OK;
+    {
+      std::lock_guard<std::mutex> lk(g_pool_mu);
+      if (!g_win_clusters) {
+        cudaLaunchConfig_t cfg = {};
+        cfg.gridDim = dim3(kWCS, 1, 1);
+        cfg.blockDim = dim3(kWT, 1, 1);
+        int nc = 0;
+        if (cudaOccupancyMaxActiveClusters(&nc, reinterpret_cast<void*>(k_fnv_window), &cfg) != cudaSuccess || nc < 1)
+          nc = 1;
+        cudaGetLastError();
+        g_win_clusters = nc;
+      }
+    }
+    const uint64_t nw64 = (n + kWin - 1) / kWin;
+    const int per_job = std::max(1, std::min(kFCap / k, n_chains));
+    const uint64_t max_total = nw64 * static_cast<uint64_t>(per_job);
+    if (max_total > 0xFFFFFFF0ull) return ffail(GS_INVALID_ARGUMENT, "fnv1a64_device: chain too long");
+    uint32_t* ctl = nullptr;  // [counter, flags[total windows]]
+    const size_t ctl_bytes = sizeof(uint32_t) * (1 + max_total);
+    if ((e = cudaMallocAsync(reinterpret_cast<void**>(&ctl), ctl_bytes, st)) != cudaSuccess)
+      return ffail(GS_CUDA_ERROR, "fnv window flags: %s", cudaGetErrorString(e));
+    int status = GS_OK;
+    for (int c0 = 0; c0 < n_chains && status == GS_OK; c0 += per_job) {
+      const int cnt = std::min(per_job, n_chains - c0);
+      FnvJob j{};
+      for (int i = 0; i < cnt * k; ++i) j.p[i] = static_cast<const uint8_t*>(bufs[static_cast<size_t>(c0) * k + i]);
+      j.k = k;
+      j.len = len;
+      j.n = n;
+      const uint32_t total = static_cast<uint32_t>(nw64 * static_cast<uint64_t>(cnt));
+      cudaError_t r = cudaMemsetAsync(ctl, 0, sizeof(uint32_t) * (1 + static_cast<size_t>(total)), st);
+      const int clusters = static_cast<int>(std::min<uint64_t>(g_win_clusters, total));
+      if (r == cudaSuccess) {
+        k_fnv_window<<<clusters * kWCS, kWT, 0, st>>>(j, h0, static_cast<uint32_t>(cnt), total, ctl, ctl + 1,
+                                                     reinterpret_cast<unsigned long long*>(d_out) + c0);
+        r = cudaGetLastError();
+      }
+      if (r != cudaSuccess) status = ffail(GS_CUDA_ERROR, "fnv window kernel: %s", cudaGetErrorString(r));
+    }
+    cudaFreeAsync(ctl, st);
+    return status;
+  }
   const uint64_t bpc64 = (n + kFB - 1) / kFB;
   if (bpc64 > 0xFFFFFFFFull) return ffail(GS_INVALID_ARGUMENT, "fnv1a64_device: chain too long");
   const uint32_t bpc = static_cast<uint32_t>(bpc64);

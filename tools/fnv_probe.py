@@ -59,7 +59,8 @@ def main():
         res.append({"config": name, "chunks": chunks, "parity_bytes": nbytes, "gpu_ms": round(ms, 3),
                     "gpu_gbs": round(nbytes / ms / 1e6, 1), "host_ms": round(host_ms, 1),
                     "host_gbs": round(nbytes / host_ms / 1e6, 1), "host_threads": os.cpu_count(),
-                    "launches_per_call": 10, "bit_exact": ok})
+                    "launches_per_call": 10 if os.environ.get("GS_FNV_LEGACY") == "1" else 2,
+                    "kernel": "legacy multi-pass" if os.environ.get("GS_FNV_LEGACY") == "1" else "k_fnv_window", "bit_exact": ok})
         print(json.dumps(res[-1]), flush=True)
         del par, hp
 
