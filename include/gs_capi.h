@@ -64,6 +64,10 @@ int gs_abi_version(void);
 int gs_jit_quiesce(void);
 /* Number of kernels this library launched in this process (all devices). */
 uint64_t gs_kernel_launches(void);
+/* Number of offload calls that took the zero-copy epilogue (the kernel stores
+ * the parity straight into pinned host memory; calls with <= 2 MiB of parity,
+ * GS_ZC_BYTES overrides, 0 = off). */
+uint64_t gs_zero_copy_offloads(void);
 /* 1 if a CUDA device is usable from this process. */
 int gs_cuda_available(void);
 

@@ -59,6 +59,7 @@ namespace {
 
 thread_local std::string g_err;
 std::atomic<uint64_t> g_launches{0};
+std::atomic<uint64_t> g_zero_copy_calls{0};  // offloads that took the zero-copy epilogue
 
 int fail(int status, const char* fmt, ...) {
   char buf[512];
@@ -998,6 +999,7 @@ int gs_jit_quiesce(void) {
   return GS_OK;
 }
 uint64_t gs_kernel_launches(void) { return g_launches.load(); }
+uint64_t gs_zero_copy_offloads(void) { return g_zero_copy_calls.load(); }
 int gs_cuda_available(void) {
   int n = 0;
   return cudaGetDeviceCount(&n) == cudaSuccess && n > 0 ? 1 : 0;
@@ -1395,6 +1397,28 @@ int gs_encode_offload_paged(gs_pipeline* p, const gs_codec* c, int n_stripes, co
   return encode_offload(p, c, n_stripes, d_data, h_parity, len, compute, copy, src_map);
 }
 
+// Zero-copy epilogue of the offload: parity bytes per call at or below this
+// go straight from the kernel into pinned host memory (GS_ZC_BYTES, 0 = off).
+const uint64_t kZeroCopyMax = [] {
+  const char* e = std::getenv("GS_ZC_BYTES");
+  return e ? std::strtoull(e, nullptr, 0) : (2ull << 20);
+}();
+
+// Every destination is page-locked host memory the device addresses at the
+// same pointer (UVA), 16-B aligned: the kernel can store into it directly.
+static bool zero_copy_eligible(void* const* h, int count, uint64_t bytes) {
+  if (bytes == 0 || bytes > kZeroCopyMax || count > 64) return false;
+  for (int i = 0; i < count; ++i) {
+    cudaPointerAttributes a{};
+    if (!h[i] || !aligned16(h[i]) || cudaPointerGetAttributes(&a, h[i]) != cudaSuccess) {
+      cudaGetLastError();
+      return false;
+    }
+    if (a.type != cudaMemoryTypeHost || a.devicePointer != h[i]) return false;
+  }
+  return true;
+}
+
 static int encode_offload(gs_pipeline* p, const gs_codec* c, int n_stripes, const void* const* d_data,
                           void* const* h_parity, size_t len, void* compute, void* copy, const gs_page_map* src_map) {
   if (!p || !c) return fail(GS_INVALID_ARGUMENT, "encode_offload: NULL pipeline/codec");
@@ -1406,6 +1430,35 @@ static int encode_offload(gs_pipeline* p, const gs_codec* c, int n_stripes, cons
   auto ks = static_cast<cudaStream_t>(copy);
   GS_CUDA(p->begin(cs, ks));
   const int K = c->n_out, N = c->n_slots;
+  if (zero_copy_eligible(h_parity, n_stripes * K, static_cast<uint64_t>(n_stripes) * K * len)) {
+    // Small calls: the codec kernel stores the parity rows straight into the
+    // pinned host buffers (device-mapped under UVA) -- one kernel, no staging
+    // and no DMA descriptor, whose fixed cost dominates a short D2H
+    // (tools/small_l_probe.py: 64 KiB shards 6.3 -> 2.6 us per step in a
+    // graph). Completion is still signalled on the copy stream.
+    auto src = [&](int s, int j) -> const void* { return d_data[static_cast<size_t>(s) * N + j]; };
+    auto dst = [&](int s, int i) -> const void* { return h_parity[static_cast<size_t>(s) * K + i]; };
+    Paging pg;
+    pg.logical0 = 0;
+    pg.total_len = len;
+    if (src_map) {
+      pg.src = to_map(src_map);
+      pg.paged_slots = N >= 32 ? ~0u : (1u << N) - 1;
+    }
+    cudaEvent_t t0, t1;
+    GS_CUDA(p->timed_begin(cs, &t0, &t1));
+    if (t0) pg.tstamp = p->stamp_slot();
+    if (int st = run_codec(c, n_stripes, src, dst, len, cs, pg)) return st;
+    if (t1) GS_CUDA(cudaEventRecord(t1, cs));
+    if (ks != cs) {
+      const int sl = p->next;
+      p->next = (p->next + 1) % gs_pipeline::kSlots;
+      GS_CUDA(p->record(cs, 1, sl));
+      GS_CUDA(p->wait(ks, 1, sl));
+    }
+    g_zero_copy_calls.fetch_add(1, std::memory_order_relaxed);
+    return GS_OK;
+  }
   const size_t slot = p->slot_bytes();
   const uint64_t rl_max = piece_len(c, len, slot, K);
   if (!rl_max) return fail(GS_INVALID_ARGUMENT, "encode_offload: staging slot of %zu B cannot hold one piece", slot);

@@ -487,14 +487,15 @@ __device__ __forceinline__ void win_round(WinShared& sh, const FnvJob& j, uint32
                                           uint32_t nc, uint64_t h0, uint32_t rank, int nvalid, const uint4 (&d)[4], uint4 (&s)[4],
                                           uint32_t& flag_word) {
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  // e-bits of bit K from the true bits < K held in s
+  // e-bits of bit K from the true bits < K held in s. Positions past the
+  // chain's end (zero data) need no masking: their e-bits only feed the
+  // prefixes of later positions, which are past the end as well.
   uint64_t eK = 0;
 #pragma unroll
   for (int q = 0; q < 4; ++q)
 #pragma unroll
     for (int x = 0; x < 4; ++x)
-      if (q < nvalid)
-        eK |= static_cast<uint64_t>(e_nibble<K>(wd(s[q], x), wd(const_cast<uint4&>(d[q]), x))) << (16 * q + 4 * x);
+      eK |= static_cast<uint64_t>(e_nibble<K>(wd(s[q], x), wd(const_cast<uint4&>(d[q]), x))) << (16 * q + 4 * x);
   uint32_t par;
   uint64_t rel = exclusive_xor(eK, par);
   const uint32_t bal = __ballot_sync(0xFFFFFFFFu, par);

@@ -14,6 +14,7 @@ from tests.golden.vectors import splitmix_bytes
 torch = pytest.importorskip("torch")
 pytestmark = pytest.mark.gpu
 
+from paper_2605_00831_b200 import _lib as L  # noqa: E402
 from paper_2605_00831_b200 import coding as G  # noqa: E402
 from paper_2605_00831_b200 import device as D  # noqa: E402
 from paper_2605_00831_b200 import kv_layout as K  # noqa: E402
@@ -186,7 +187,9 @@ def test_one_call_abi_forms():
                                     st.cuda_stream), "encode_async")
         G.check(lib.gs_sync(st.cuda_stream), "sync")
         for i in range(k):
-            assert np.array_equal(hp[i].numpy(), want[i]), (n, k, i)
+            bad = np.nonzero(hp[i].numpy() != want[i])[0]
+            assert len(bad) == 0, (n, k, i, len(bad), bad[:8].tolist(), bad[-4:].tolist(), hp.data_ptr(),
+                                   int(lib.gs_zero_copy_offloads()))
         for e in (1, 2):
             for lost in itertools.combinations(range(n + k), e):
                 data_lost = [j for j in lost if j < n]
@@ -756,3 +759,51 @@ def test_reference_acceptance_criteria_on_the_library():
     for c in (1, 2, 3, 4, 5, 6, 7, 8, 9, 11):
         assert f"[PASS] C{c}:" in out.stdout, out.stdout[-4000:]
     assert out.returncode == 1 and "[FAIL] C10:" in out.stdout
+
+
+def test_small_offloads_take_the_zero_copy_epilogue():
+    """Offloads with <= 2 MiB of parity store the rows straight from K1 into
+    the pinned host buffers (no staging, no DMA): bit-exact, complete once the
+    COPY stream is synchronised (the offload's completion contract), eagerly
+    and replayed from a CUDA graph; a larger call still goes through the
+    staged pipeline."""
+    lib = L.lib()
+    scheme = G.CodingScheme.reed_solomon(8, 2)
+    enc = G.encoder(scheme)
+    pipe = D.Pipeline(0, 64 << 20)
+    comp, copy = torch.cuda.Stream(), torch.cuda.Stream()
+    for ln, stripes, zc in ((65536, 1, True), (262144, 4, True), (1 << 20, 4, False)):
+        data = torch.randint(0, 256, (stripes, 8, ln), dtype=torch.uint8, device="cuda")
+        hp = torch.zeros((stripes, 2, ln), dtype=torch.uint8).pin_memory()
+        slots = L.ptr_array([data[s, j].data_ptr() for s in range(stripes) for j in range(8)])
+        outs = L.ptr_array([hp[s, i].data_ptr() for s in range(stripes) for i in range(2)])
+        torch.cuda.synchronize()
+        before = lib.gs_zero_copy_offloads()
+        G.check(lib.gs_encode_offload(pipe.handle, enc.handle, stripes, slots, outs, ln, comp.cuda_stream,
+                                      copy.cuda_stream), "offload")
+        copy.synchronize()
+        assert (lib.gs_zero_copy_offloads() - before == 1) == zc, (ln, stripes)
+        assert torch.equal(hp, D.encode(scheme, data).cpu()), (ln, stripes)
+        hp.zero_()
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g, stream=comp):
+            G.check(lib.gs_encode_offload(pipe.handle, enc.handle, stripes, slots, outs, ln, comp.cuda_stream,
+                                          copy.cuda_stream), "offload")
+            comp.wait_stream(copy)
+        with torch.cuda.stream(comp):
+            g.replay()
+        comp.synchronize()
+        assert torch.equal(hp, D.encode(scheme, data).cpu()), ("graph", ln, stripes)
+        del g
+    # pageable destinations are never written by the kernel: staged path
+    data = torch.randint(0, 256, (1, 8, 4096), dtype=torch.uint8, device="cuda")
+    pageable = [np.zeros(4096, np.uint8) for _ in range(2)]
+    before = lib.gs_zero_copy_offloads()
+    G.check(lib.gs_encode_offload(pipe.handle, enc.handle, 1, L.ptr_array([data[0, j].data_ptr() for j in range(8)]),
+                                  L.ptr_array([p.ctypes.data for p in pageable]), 4096, comp.cuda_stream,
+                                  copy.cuda_stream), "offload")
+    copy.synchronize()
+    assert lib.gs_zero_copy_offloads() == before
+    want = D.encode(scheme, data).cpu().numpy()[0]
+    assert all(np.array_equal(pageable[i], want[i]) for i in range(2))
+    pipe.close()
