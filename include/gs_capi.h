@@ -258,8 +258,8 @@ int gs_pipeline_sync(gs_pipeline* p);
  *                         the lost data shards ascending (device). The
  *                         decoder (host Gauss-Jordan) is cached per pattern.
  *                         Only the parity rows the decode uses are H2D'd.
- *  gs_sync              : wait for `stream` and the calling thread's default
- *                         pipelines. */
+ *  gs_sync              : wait for `stream` (NULL = the legacy default stream)
+ *                         and the calling thread's default pipelines. */
 int gs_codec_create(int kind, int n, int k, gs_codec** out);
 int gs_encode_async(const gs_codec* enc, const void* const* d_shards, size_t len, void* const* h_parity,
                     void* compute, void* copy);

@@ -1685,7 +1685,9 @@ int gs_reconstruct_async(const gs_codec* enc, const int* lost, int n_lost, const
 }
 
 int gs_sync(void* stream) {
-  if (stream) GS_CUDA(cudaStreamSynchronize(static_cast<cudaStream_t>(stream)));
+  // NULL is the legacy default stream -- work enqueued there (gs_encode_async
+  // with compute = copy = NULL) must be waited for like any other stream's
+  GS_CUDA(cudaStreamSynchronize(static_cast<cudaStream_t>(stream)));
   for (auto& kv : t_pipes.by_dev)
     if (int st = gs_pipeline_sync(kv.second)) return st;
   return GS_OK;

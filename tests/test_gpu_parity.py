@@ -807,3 +807,23 @@ def test_small_offloads_take_the_zero_copy_epilogue():
     want = D.encode(scheme, data).cpu().numpy()[0]
     assert all(np.array_equal(pageable[i], want[i]) for i in range(2))
     pipe.close()
+
+
+def test_sync_waits_for_the_legacy_default_stream():
+    """gs_encode_async with compute = copy = NULL (the legacy default stream)
+    followed by gs_sync(NULL): the parity is complete when gs_sync returns --
+    for a zero-copy sized call and a staged 32 MiB one alike."""
+    import ctypes as C
+    lib = L.lib()
+    enc = C.c_void_p()
+    G.check(lib.gs_codec_create(2, 8, 2, C.byref(enc)), "codec_create")
+    for ln in (65536, 32 << 20):
+        data = torch.randint(0, 256, (8, ln), dtype=torch.uint8, device="cuda")
+        want = D.encode(G.CodingScheme.reed_solomon(8, 2), data.unsqueeze(0))[0].cpu()
+        hp = torch.zeros((2, ln), dtype=torch.uint8).pin_memory()
+        torch.cuda.synchronize()
+        G.check(lib.gs_encode_async(enc, L.ptr_array([data[j].data_ptr() for j in range(8)]), ln,
+                                    L.ptr_array([hp[i].data_ptr() for i in range(2)]), None, None), "encode_async")
+        G.check(lib.gs_sync(None), "sync")
+        assert torch.equal(hp, want), ln
+    lib.gs_codec_destroy(enc)
