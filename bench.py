@@ -292,9 +292,12 @@ def cpu_encode_baseline(W, target_s: float, threads: int):
                       f"{arm.threads} thread(s)"}
 
 
-def ncu_traffic(W):
-    """dram bytes (read + write) per K1 launch from the committed ncu capture
-    of THIS build (the capture records the sha of the library it profiled)."""
+def ncu_traffic(W, alg_launch):
+    """DRAM bytes (read + write) per K1 launch from the committed ncu capture
+    of THIS build (the capture records the sha of the library it profiled):
+    the capture's DRAM / algorithmic ratio applied to this run's algorithmic
+    bytes per launch (the captured launch is one pipeline piece, whose size
+    differs from the per-launch average)."""
     try:
         import hashlib
         with open(os.path.join(ROOT, "profiles", f"k1_{W.key}_ncu_summary.json")) as f:
@@ -304,7 +307,10 @@ def ncu_traffic(W):
             sha = hashlib.sha256(f.read()).hexdigest()[:16]
         if summ.get("lib_sha256_16") != sha:
             return None, f"committed capture is of another build ({summ.get('lib_sha256_16')} != {sha})"
-        return summ["dram_bytes_per_launch"], f"ncu --set full of this build ({summ.get('file')})"
+        ratio = summ["dram_bytes_per_launch"] / summ["algorithmic_bytes_per_launch"]
+        return int(ratio * alg_launch), (f"ncu --set full of this build ({summ.get('file')}): "
+                                         f"{summ['dram_bytes_per_launch']} DRAM B for "
+                                         f"{summ['algorithmic_bytes_per_launch']} algorithmic B (x{ratio:.3f})")
     except Exception as e:
         return None, f"no ncu capture for this workload/build ({type(e).__name__})"
 
@@ -470,6 +476,11 @@ def run_ours(args):
     # steps (kernel-internal %globaltimer span + timing events on the compute
     # stream, after the staging-slot waits)
     check(lib.gs_pipeline_set_timing(pipe.handle, 1), "timing")
+    # GS_PROFILE_TIMED=1: bracket exactly the timed steps with cudaProfilerStart
+    # / Stop, so `ncu --profile-from-start off` lists only their launches
+    prof = os.environ.get("GS_PROFILE_TIMED") == "1"
+    if prof:
+        torch.cuda.cudart().cudaProfilerStart()
     with ClockSampler(local) as clk:
         e0.record(comp)
         for i in range(args.steps):
@@ -477,6 +488,8 @@ def run_ours(args):
         comp.wait_stream(copy)
         e1.record(comp)
         e1.synchronize()
+    if prof:
+        torch.cuda.cudart().cudaProfilerStop()
     l1 = D.launches()
     torch.cuda.synchronize()
     k_ms, k_dev_ms, k_groups, k_launches = C.c_double(), C.c_double(), C.c_int(), C.c_uint64()
@@ -564,7 +577,7 @@ def run_ours(args):
         groups = max(k_groups.value, 1)
         alg_launch = alg * args.steps // groups
         achieved = alg_launch / (live_group_us * 1e-6) / 1e9
-        traffic, traffic_src = (args.traffic, "--traffic") if args.traffic else ncu_traffic(W)
+        traffic, traffic_src = (args.traffic, "--traffic") if args.traffic else ncu_traffic(W, alg_launch)
         kern = dict(iso, achieved=round(achieved, 1), frac=round(achieved / peak, 4),
                     per_launch_us=round(live_group_us, 2), algorithmic_bytes_per_launch=alg_launch,
                     launches_per_step=round(groups / args.steps, 3),
@@ -1099,12 +1112,18 @@ def decode_overhead(torch, dev, pipe, args):
     from paper_2605_00831_b200.coding import CodingScheme, check, encoder
 
     ctx = args.decode_ctx
-    wbytes = int(70.6e9 * 2 / 8)
+    layers, hid, cols = 80, 8192, 13440          # 80 x 8192 x 13440 bf16 = this GPU's 17.6 GB shard
+    wbytes = layers * hid * cols * 2
     kvbytes = 32 * ctx * 40960
     free, _ = torch.cuda.mem_get_info(dev)
     if free < wbytes + kvbytes + (4 << 30):
         return {"skipped": f"needs {(wbytes + kvbytes) >> 30} GiB"}
-    w = torch.zeros(wbytes // 4, dtype=torch.float32, device=dev)
+    # decode step = the weight-streaming GEMMs of batch 32 (cuBLAS bf16 on the
+    # tensor cores: [32 x 8192] @ [8192 x 13440] per layer, each layer's input
+    # the previous layer's output) + a read of the KV at the context
+    w = torch.empty((layers, hid, cols), dtype=torch.bfloat16, device=dev).normal_(0, 0.01)
+    x0 = torch.randn((32, hid), dtype=torch.bfloat16, device=dev)
+    ys = [torch.empty((32, cols), dtype=torch.bfloat16, device=dev) for _ in range(2)]
     kvc = torch.zeros(kvbytes // 4, dtype=torch.float32, device=dev)
     rng = 81920                                   # 655,360 B block slice / 8 GPUs
     data = torch.randint(0, 256, (32, 8, rng), dtype=torch.uint8, device=dev)
@@ -1117,7 +1136,10 @@ def decode_overhead(torch, dev, pipe, args):
     sink = torch.empty(2, device=dev)
 
     def step():
-        torch.amax(w, dim=0, out=sink[0])
+        x = x0
+        for li in range(layers):
+            torch.mm(x, w[li], out=ys[li % 2])
+            x = ys[li % 2][:, :hid]
         torch.amax(kvc, dim=0, out=sink[1])
 
     def ckpt():
@@ -1151,12 +1173,15 @@ def decode_overhead(torch, dev, pipe, args):
     a1.record(side)
     a1.synchronize()
     out = {"model": "Llama-3-70B KV, TP=8, batch 32, one GPU's share", "context_tokens": ctx,
+           "decode_step": "80 x bf16 GEMM [32 x 8192] @ [8192 x 13440] (cuBLAS, this GPU's 17.6 GB weight shard) "
+                          "+ KV read at the context; checkpoint: K1 over this GPU's 1/8 range of the block + D2H on "
+                          "side streams (all shards local: the 7/8 NVLink reads of a real TP=8 group are not emulated)",
            "decode_step_ms": round(base / (blocks * 16), 4),
            "block_ms_without_ckpt": round(base / blocks, 4), "block_ms_with_ckpt": round(withc / blocks, 4),
            "checkpoint_alone_ms": round(a0.elapsed_time(a1), 4),
            "overhead_pct_of_block": round((withc - base) / base * 100, 3),
            "overhead_pct_of_decode_step": round((withc - base) / blocks / (base / (blocks * 16)) * 100, 3)}
-    del w, kvc, data, h_par
+    del w, kvc, data, h_par, x0, ys
     torch.cuda.empty_cache()
     return out
 

@@ -68,6 +68,8 @@ uint64_t gs_kernel_launches(void);
  * the parity straight into pinned host memory; calls with <= 2 MiB of parity,
  * GS_ZC_BYTES overrides, 0 = off). */
 uint64_t gs_zero_copy_offloads(void);
+/* Set that threshold (bytes of parity per call; 0 disables the epilogue). */
+int gs_set_zero_copy_bytes(uint64_t bytes);
 /* 1 if a CUDA device is usable from this process. */
 int gs_cuda_available(void);
 

@@ -31,6 +31,7 @@ SIGNATURES = {
     "gs_jit_quiesce": (_i, []),
     "gs_kernel_launches": (_u64, []),
     "gs_zero_copy_offloads": (_u64, []),
+    "gs_set_zero_copy_bytes": (_i, [_u64]),
     "gs_cuda_available": (_i, []),
     "gs_gf_mul": (_u8, [_u8, _u8]),
     "gs_gf_inv": (_i, [_u8, _u8p]),

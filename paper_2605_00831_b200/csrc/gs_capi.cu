@@ -60,6 +60,13 @@ namespace {
 thread_local std::string g_err;
 std::atomic<uint64_t> g_launches{0};
 std::atomic<uint64_t> g_zero_copy_calls{0};  // offloads that took the zero-copy epilogue
+// Zero-copy epilogue of the offload: parity bytes per call at or below this
+// go straight from the kernel into pinned host memory (GS_ZC_BYTES /
+// gs_set_zero_copy_bytes, 0 = off).
+std::atomic<uint64_t> g_zero_copy_max{[] {
+  const char* e = std::getenv("GS_ZC_BYTES");
+  return e ? std::strtoull(e, nullptr, 0) : (2ull << 20);
+}()};
 
 int fail(int status, const char* fmt, ...) {
   char buf[512];
@@ -138,7 +145,11 @@ int blocks_per_sm(int dev, const void* kernel, size_t smem, int threads = kThrea
 // (LDG.128) streaming, 1 = bulk-copy smem pipeline, 2 = auto (measured on
 // B200, tools/kernel_sweep.py: the bulk pipeline wins for encoders once a
 // launch moves >= 128 MB; the register kernel everywhere else).
-std::atomic<int> g_variant{2};
+std::atomic<int> g_variant{[] {
+  const char* e = std::getenv("GS_KERNEL_VARIANT");  // 0 / 1 / 2 as gs_set_kernel_variant (A/B runs)
+  const int v = e ? std::atoi(e) : 2;
+  return v >= 0 && v <= 2 ? v : 2;
+}()};
 // Tuning override for the register kernel's resident CTAs per SM (0 = max).
 int g_ctas_per_sm = [] {
   const char* e = std::getenv("GS_CTAS_PER_SM");
@@ -1000,6 +1011,10 @@ int gs_jit_quiesce(void) {
 }
 uint64_t gs_kernel_launches(void) { return g_launches.load(); }
 uint64_t gs_zero_copy_offloads(void) { return g_zero_copy_calls.load(); }
+int gs_set_zero_copy_bytes(uint64_t bytes) {
+  g_zero_copy_max.store(bytes);
+  return GS_OK;
+}
 int gs_cuda_available(void) {
   int n = 0;
   return cudaGetDeviceCount(&n) == cudaSuccess && n > 0 ? 1 : 0;
@@ -1399,15 +1414,12 @@ int gs_encode_offload_paged(gs_pipeline* p, const gs_codec* c, int n_stripes, co
 
 // Zero-copy epilogue of the offload: parity bytes per call at or below this
 // go straight from the kernel into pinned host memory (GS_ZC_BYTES, 0 = off).
-const uint64_t kZeroCopyMax = [] {
-  const char* e = std::getenv("GS_ZC_BYTES");
-  return e ? std::strtoull(e, nullptr, 0) : (2ull << 20);
-}();
+
 
 // Every destination is page-locked host memory the device addresses at the
 // same pointer (UVA), 16-B aligned: the kernel can store into it directly.
 static bool zero_copy_eligible(void* const* h, int count, uint64_t bytes) {
-  if (bytes == 0 || bytes > kZeroCopyMax || count > 64) return false;
+  if (bytes == 0 || bytes > g_zero_copy_max.load(std::memory_order_relaxed) || count > 64) return false;
   for (int i = 0; i < count; ++i) {
     cudaPointerAttributes a{};
     if (!h[i] || !aligned16(h[i]) || cudaPointerGetAttributes(&a, h[i]) != cudaSuccess) {

@@ -1,9 +1,10 @@
-"""Small-L regime (C5, 64 KiB - 1 MiB shards, one stripe per step): the
-staged offload (K1 into staging -> D2H DMA on a copy stream) against a
-zero-copy epilogue (K1 stores the parity rows straight into the pinned host
-buffers over PCIe: one kernel per step, no DMA descriptor), eager and
+"""Small-L regime (C5, 64 KiB - 4 MiB shards, one stripe per step):
+gs_encode_offload with the zero-copy epilogue switched off (K1 into staging
+-> D2H DMA on a copy stream: round 1's path) against the offload as shipped
+(<= 2 MiB of parity: K1 stores the parity rows straight into the pinned host
+buffers over PCIe -- one kernel per step, no DMA descriptor), eager and
 replayed from a CUDA graph. Per-step time, fraction of the host-link
-roofline t* = k*L / D2H peak, bit-exact check.
+roofline t* = k*L / D2H peak (best of 5 pinned copies), bit-exact check.
 """
 import json
 import os
@@ -27,12 +28,14 @@ def main():
     comp, copy = torch.cuda.Stream(), torch.cuda.Stream()
     h = torch.empty(256 << 20, dtype=torch.uint8).pin_memory()
     dd = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    e0.record()
-    h.copy_(dd, non_blocking=True)
-    e1.record()
-    e1.synchronize()
-    d2h = (256 << 20) / (e0.elapsed_time(e1) * 1e-3) / 1e9
+    d2h = 0.0
+    for _ in range(5):   # best of 5: the first copy pays for mapping the pages
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        h.copy_(dd, non_blocking=True)
+        e1.record()
+        e1.synchronize()
+        d2h = max(d2h, (256 << 20) / (e0.elapsed_time(e1) * 1e-3) / 1e9)
     for ln in [int(x) for x in (sys.argv[1:] or ["65536", "262144", "1048576"])]:
         nbuf = max(2, min(64, (256 << 20) // (8 * ln)))
         data = torch.randint(0, 256, (nbuf, 8, ln), dtype=torch.uint8, device=dev)
@@ -40,15 +43,17 @@ def main():
         slots = [L.ptr_array([data[b, j].data_ptr() for j in range(8)]) for b in range(nbuf)]
         houts = [L.ptr_array([hp[b, i].data_ptr() for i in range(2)]) for b in range(nbuf)]
 
-        def staged(b):
+        def staged(b):   # zero-copy epilogue off: K1 -> staging -> D2H DMA
             check(lib.gs_encode_offload(pipe.handle, enc.handle, 1, slots[b], houts[b], ln, comp.cuda_stream,
                                         copy.cuda_stream), "staged")
 
-        def zc(b):
-            check(lib.gs_apply_device(enc.handle, 1, slots[b], houts[b], ln, comp.cuda_stream), "zc")
+        def zc(b):       # the offload as shipped: zero-copy epilogue for <= 2 MiB of parity
+            check(lib.gs_encode_offload(pipe.handle, enc.handle, 1, slots[b], houts[b], ln, comp.cuda_stream,
+                                        copy.cuda_stream), "zc")
 
         res = {"shard_bytes": ln, "d2h_gbs": round(d2h, 1), "t_star_us": round(2 * ln / d2h / 1e3, 3)}
-        for name, fn, two in (("staged", staged, True), ("zero_copy", zc, False)):
+        for name, fn, two in (("staged", staged, True), ("offload_as_shipped", zc, True)):
+            lib.gs_set_zero_copy_bytes(0 if name == "staged" else 2 << 20)
             for b in range(nbuf):
                 fn(b)
             torch.cuda.synchronize()
