@@ -1302,7 +1302,16 @@ def c3_orchestrated(torch, dev, link, k1_gbs, k2_gbs):
     t_sealed = time.perf_counter() - t0
     n = run.chunks_done
     r_ref = get_recompute_units(n, m, cfg.scheme, sl, CostModel())
-    res = ck.recover(11, FailureEvent([5], at_chunk=n), run.ground_truth, [m] * n, verify_threads=threads)
+    # the same failure recovered 3 times (the host threads' pace varies between
+    # runs on these VMs); every recovery is checked, the median is reported
+    runs = []
+    for _ in range(3):
+        res_i = ck.recover(11, FailureEvent([5], at_chunk=n), run.ground_truth, [m] * n, verify_threads=threads)
+        runs.append(res_i)
+        if res_i.plan.mode != "hybrid" or res_i.decoded_chunks != n or not res_i.verified:
+            break
+    res = sorted(runs, key=lambda x: x.wall_ms)[len(runs) // 2] if all(
+        x.plan.mode == "hybrid" and x.decoded_chunks == n and x.verified for x in runs) else runs[-1]
     out = {"chunks": n, "slice_bytes": sl,
            "checkpoint_device_ms": round(run.device_ms, 2),
            "checkpoint_data_gbs": round(8 * n * sl / (run.device_ms * 1e-3) / 1e9, 2),
@@ -1319,12 +1328,19 @@ def c3_orchestrated(torch, dev, link, k1_gbs, k2_gbs):
            "decode_device_ms": round(res.reconstruct_device_ms, 2), "recover_wall_ms": round(res.wall_ms, 1),
            "parity_bytes_verified": len(res.plan.reconstruct_ids) * 2 * sl, "verified": res.verified,
            "decoded_chunks": res.decoded_chunks, "corrupt_chunks": res.corrupt_chunks,
+           "verify_split": res.verify_split,
+           "recover_wall_ms_runs": [round(x.wall_ms, 1) for x in runs],
+           "runs_detail": [{"wall_ms": round(x.wall_ms, 1), "verify_ms": round(x.verify_host_ms, 1),
+                            "decode_device_ms": round(x.reconstruct_device_ms, 1), "split": x.verify_split}
+                           for x in runs],
            "note": "wall = plan + speculative H2D/K2 overlapped with the FNV verification of the 64 entries "
-                   "(reference semantics: corrupt parity -> full-recompute fallback); verify_gpu_chunks of them "
-                   "upload both parity rows and are checksummed in HBM (bit-sliced GPU FNV-1a), the rest on "
-                   "host threads, split so the host link and the host cores finish together"}
+                   "(reference semantics: corrupt parity -> full-recompute fallback), median of 3 recoveries of "
+                   "the same failure; every chunk's parity row 0 is uploaded (K2 needs it) and hashed on the GPU, "
+                   "the rest of each chain is claimed at run time by host threads (continuing the GPU's state) or "
+                   "a GPU feeder (uploading the row and continuing the chain in HBM), hosts handing a chain over "
+                   "mid-row when they fall behind (verify_split)"}
     ck.close()
-    del run, res
+    del run, res, runs
     torch.cuda.empty_cache()
     return out
 

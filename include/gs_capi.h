@@ -335,6 +335,29 @@ int gs_parity_offload_sealed(const void* const* d_parity, int n_chunks, int k, u
 int gs_verify_enqueue(const void* const* h_parity, int n_chunks, int k, uint64_t len, int n_full, int u,
                       void* const* d_parity, void* compute, void* copy, gs_verify** out);
 int gs_verify_finish(gs_verify* v, int threads, uint64_t* sums);
+/* n_full < 0: DYNAMIC split -- rows 0..u-1 of every chunk are uploaded and
+ * hashed on the GPU (d_parity rows >= u may be NULL); the rest of each chain
+ * is claimed at run time by host threads (from the front, as the GPU states
+ * land) or by a GPU feeder (from the back: remaining rows uploaded into an
+ * internal ring behind the row-0 uploads, chain continued on the GPU from
+ * the device state), so the split adapts to this host's speed.
+ * *gpu_chunks = chunks whose whole chain was hashed on the GPU. */
+int gs_verify_finish_ex(gs_verify* v, int threads, uint64_t* sums, int* gpu_chunks);
+/* Dynamic split pacing (optional, before finish): the host link's rate and
+ * one host thread's serial FNV rate (GB/s); host threads then stop claiming
+ * chunks the GPU would finish sooner (the host rate is refined online). */
+int gs_verify_set_rates(gs_verify* v, double link_gbs, double host_chain_gbs);
+/* Chains (process total) a host thread handed over to the GPU mid-chain in a
+ * dynamic split, because it had fallen behind the GPU (diagnostics). */
+uint64_t gs_verify_handoffs(void);
+/* The last dynamic split: {host threads done, feeder done, hash stream
+ * drained} in s after gs_verify_finish started, and the chunks verified by
+ * host threads / entirely on the GPU / handed over mid-chain. */
+int gs_verify_last_stats(double* out6);
+/* gs_fnv1a64_device with a per-chain seed in device memory (d_h0[c], must
+ * not alias d_out): continues chains hashed earlier. */
+int gs_fnv1a64_device_seeded(const void* const* bufs, int n_chains, int k, uint64_t len, const uint64_t* d_h0,
+                             uint64_t* d_out, void* stream);
 
 /* ---- host tier: ParityStore on pinned slabs (parity_store.hpp:31-263) ----
  * Entries are keyed (request, chunk). Reserve -> the D2H of K1 writes the k

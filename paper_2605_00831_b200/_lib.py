@@ -82,6 +82,11 @@ SIGNATURES = {
     "gs_parity_offload_sealed": (_i, [_vpp, _i, _i, _u64, _vpp, _vp, _vp, _vp]),
     "gs_verify_enqueue": (_i, [_vpp, _i, _i, _u64, _i, _i, _vpp, _vp, _vp, _vpp]),
     "gs_verify_finish": (_i, [_vp, _i, _u64p]),
+    "gs_verify_finish_ex": (_i, [_vp, _i, _u64p, _ip]),
+    "gs_verify_set_rates": (_i, [_vp, C.c_double, C.c_double]),
+    "gs_verify_handoffs": (_u64, []),
+    "gs_verify_last_stats": (_i, [C.POINTER(C.c_double)]),
+    "gs_fnv1a64_device_seeded": (_i, [_vpp, _i, _i, _u64, _vp, _vp, _vp]),
     "gs_store_create": (_i, [_u64, _i, _vpp]),
     "gs_store_destroy": (_i, [_vp]),
     "gs_store_reserve": (_i, [_vp, _u64, _u32, _i, _i, _i, _u32, _u64, _ip, _vpp]),

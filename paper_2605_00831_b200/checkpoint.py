@@ -233,6 +233,7 @@ class RecoveryResult:
     verify_gpu_chunks: int = 0           # entries whose checksum was verified on the GPU
     wall_ms: float = 0.0                 # plan -> verified, rebuilt bytes on the device
     corrupt_chunks: List[int] = field(default_factory=list)   # parity that failed verification (-> fallback)
+    verify_split: Dict[str, float] = field(default_factory=dict)  # dynamic split timeline / shares
     decoded_chunks: int = 0              # chunks whose lost shards came out of K2 (and matched ground truth)
 
 
@@ -255,19 +256,21 @@ class _VerifyFinish:
         self._n = n
         self._rc = 0
         self._ms = 0.0
+        self._gpu = C.c_int(0)
 
         def run():
             t0 = time.perf_counter()
-            self._rc = L.lib().gs_verify_finish(handle, threads, self._out)
+            self._rc = L.lib().gs_verify_finish_ex(handle, threads, self._out, C.byref(self._gpu))
             self._ms = (time.perf_counter() - t0) * 1e3
 
         self._t = threading.Thread(target=run, daemon=True)
         self._t.start()
 
     def result(self):
+        """(checksums, host ms, chunks hashed entirely on the GPU)."""
         self._t.join()
         check(self._rc, "recover verify")
-        return [int(self._out[i]) for i in range(self._n)], self._ms
+        return [int(self._out[i]) for i in range(self._n)], self._ms, int(self._gpu.value)
 
 
 class _HostVerify:
@@ -326,6 +329,11 @@ class Checkpointer:
         self.host_chain_rate = 0.9e9   # ONE serial FNV chain on one host thread (bytes/s)
         # False: verify every entry on host threads (the reference's placement)
         self.gpu_verify = True
+        # "dynamic": the part of each parity chain the decode does not upload
+        # is claimed at run time by host threads or a GPU feeder (whichever is
+        # faster on this host takes more); "static": split decided up front
+        # from host_fnv_rate / host_chain_rate (_split_plan)
+        self.verify_split = "dynamic"
         # Where checkpoint_batch seals parity (ParityChunk::seal): "host" = FNV
         # on the store's host threads after the D2H (the reference's order);
         # "device" = K1 into HBM, checksum on the GPU, D2H of rows + checksum;
@@ -597,9 +605,16 @@ class Checkpointer:
             if host_verify is not None:
                 good, result.verify_host_ms = host_verify.result()
             if split is not None:
-                sums, result.verify_host_ms = split[1].result()
+                sums, result.verify_host_ms, result.verify_gpu_chunks = split[1].result()
+                if self.verify_split == "dynamic":
+                    st6 = (C.c_double * 6)()
+                    L.lib().gs_verify_last_stats(st6)
+                    result.verify_split = {"hosts_done_ms": round(st6[0] * 1e3, 1),
+                                           "gpu_feeder_done_ms": round(st6[1] * 1e3, 1),
+                                           "hash_stream_drained_ms": round(st6[2] * 1e3, 1),
+                                           "chunks_host": int(st6[3]), "chunks_gpu": int(st6[4]),
+                                           "chunks_handed_over": int(st6[5])}
                 good = [sums[i] == e.checksum for i, e in enumerate(entries)]
-                result.verify_gpu_chunks = split[0]
             bad = [i for i, g in enumerate(good) if not g]
             if bad:
                 # a fallback is only legitimate if the reference's own serial
@@ -701,22 +716,30 @@ class Checkpointer:
         S, k = len(chunk_ids), sch.k
         threads = threads or max(1, (os.cpu_count() or 1) - 2)
         n_full, u = self._split_plan(S, failed, threads)
+        if self.verify_split == "dynamic":
+            n_full = -1            # gs_verify_enqueue: claim the rest of each chain at run time
         lib = L.lib()
-        full = torch.empty((n_full, k, self.slice), dtype=torch.uint8, device=self.dev)
-        part = torch.empty((S - n_full, u, self.slice), dtype=torch.uint8, device=self.dev)
+        nf = max(n_full, 0)
+        full = torch.empty((nf, k, self.slice), dtype=torch.uint8, device=self.dev)
+        part = torch.empty((S - nf, u, self.slice), dtype=torch.uint8, device=self.dev)
         drows: List[Optional[int]] = []
         for s in range(S):
             for i in range(k):
-                if s < n_full:
+                if s < nf:
                     drows.append(full[s, i].data_ptr())
                 else:
-                    drows.append(part[s - n_full, i].data_ptr() if i < u else None)
+                    drows.append(part[s - nf, i].data_ptr() if i < u else None)
         handle = C.c_void_p()
         check(lib.gs_verify_enqueue(L.ptr_array([e.parity[i].ctypes.data for e in entries for i in range(k)]),
                                     S, k, self.slice, n_full, u, L.ptr_array(drows), self.verify.cuda_stream,
                                     self.copy.cuda_stream, C.byref(handle)), "recover verify")
+        # K2 needs the uploaded rows (not their checksums, nor the rows the
+        # dynamic split's GPU feeder uploads later for hashing only)
+        self.compute.wait_stream(self.copy)
+        if n_full < 0:
+            check(lib.gs_verify_set_rates(handle, self.cfg.cost.host_bw / 1e9, self.host_chain_rate / 1e9),
+                  "recover verify")
         finish = _VerifyFinish(handle, S, threads)
-        self.compute.wait_stream(self.copy)   # K2 needs the uploaded rows, not their checksums
         outs = torch.empty((S, max(dec.n_out, 1), self.slice), dtype=torch.uint8, device=self.dev)
         if dec.n_out:
             slots: List[Optional[int]] = []

@@ -295,9 +295,9 @@ __global__ void __launch_bounds__(1024) k_fnv_scan2(const uint8_t* __restrict__ 
   }
 }
 
-__global__ void k_fnv_init(uint64_t* out, int n_chains, uint64_t h0, uint64_t n) {
+__global__ void k_fnv_init(uint64_t* out, int n_chains, uint64_t h0, uint64_t n, const uint64_t* h0s) {
   const int c = blockIdx.x * blockDim.x + threadIdx.x;
-  if (c < n_chains) out[c] = h0 * pow64(kFnvP, n);
+  if (c < n_chains) out[c] = (h0s ? h0s[c] : h0) * pow64(kFnvP, n);
 }
 
 // out[c] += sum over the chain's bytes of d_i * P^(N - i), d_i = (s_i ^ b_i) - s_i.
@@ -545,8 +545,8 @@ __device__ __forceinline__ void win_round(WinShared& sh, const FnvJob& j, uint32
 }
 
 __global__ void __cluster_dims__(kWCS, 1, 1) __launch_bounds__(kWT, 2)
-    k_fnv_window(const FnvJob j, uint64_t h0, uint32_t nc, uint32_t total_windows, uint32_t* counter,
-                 uint32_t* flags, unsigned long long* __restrict__ out) {
+    k_fnv_window(const FnvJob j, uint64_t h0, const uint64_t* __restrict__ h0s, uint32_t nc, uint32_t total_windows,
+                 uint32_t* counter, uint32_t* flags, unsigned long long* __restrict__ out) {
   __shared__ WinShared sh;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const uint32_t rank = cluster_rank();
@@ -563,6 +563,7 @@ __global__ void __cluster_dims__(kWCS, 1, 1) __launch_bounds__(kWT, 2)
     // chains as far as there are chains, so a window's predecessor (same
     // chain, gw - nc) has usually finished and the look-back is one read
     const uint32_t w = gw / nc, c = gw - w * nc;
+    const uint64_t hc = h0s ? h0s[c] : h0;  // the chain's seed (per-chain seeds continue earlier chains)
     const uint64_t cta0 = static_cast<uint64_t>(w) * kWin + static_cast<uint64_t>(rank) * kWB;
     const uint64_t pos0 = cta0 + static_cast<uint64_t>(tid) * kFPer;
     uint4 d[4];
@@ -571,14 +572,14 @@ __global__ void __cluster_dims__(kWCS, 1, 1) __launch_bounds__(kWT, 2)
 #pragma unroll
     for (int q = 0; q < 4; ++q) s[q] = make_uint4(0, 0, 0, 0);
     uint32_t fw = 0;
-    win_round<0>(sh, j, flags, gw, w, nc, h0, rank, nvalid, d, s, fw);
-    win_round<1>(sh, j, flags, gw, w, nc, h0, rank, nvalid, d, s, fw);
-    win_round<2>(sh, j, flags, gw, w, nc, h0, rank, nvalid, d, s, fw);
-    win_round<3>(sh, j, flags, gw, w, nc, h0, rank, nvalid, d, s, fw);
-    win_round<4>(sh, j, flags, gw, w, nc, h0, rank, nvalid, d, s, fw);
-    win_round<5>(sh, j, flags, gw, w, nc, h0, rank, nvalid, d, s, fw);
-    win_round<6>(sh, j, flags, gw, w, nc, h0, rank, nvalid, d, s, fw);
-    win_round<7>(sh, j, flags, gw, w, nc, h0, rank, nvalid, d, s, fw);
+    win_round<0>(sh, j, flags, gw, w, nc, hc, rank, nvalid, d, s, fw);
+    win_round<1>(sh, j, flags, gw, w, nc, hc, rank, nvalid, d, s, fw);
+    win_round<2>(sh, j, flags, gw, w, nc, hc, rank, nvalid, d, s, fw);
+    win_round<3>(sh, j, flags, gw, w, nc, hc, rank, nvalid, d, s, fw);
+    win_round<4>(sh, j, flags, gw, w, nc, hc, rank, nvalid, d, s, fw);
+    win_round<5>(sh, j, flags, gw, w, nc, hc, rank, nvalid, d, s, fw);
+    win_round<6>(sh, j, flags, gw, w, nc, hc, rank, nvalid, d, s, fw);
+    win_round<7>(sh, j, flags, gw, w, nc, hc, rank, nvalid, d, s, fw);
     // sum over the thread's bytes of d_i P^(tend - i), four 16-byte Horner chains
     uint64_t accq[4] = {0, 0, 0, 0};
 #pragma unroll
@@ -637,10 +638,40 @@ int g_sms = 0;
 std::mutex g_pool_mu;
 std::set<int> g_pool_tuned;
 
+// Keep the device's stream-ordered allocations mapped between calls (the
+// scratch of the FNV kernels and the verification buffers are reused at
+// every call), and cache the SM count.
+void tune_pool(int dev) {
+  std::lock_guard<std::mutex> lk(g_pool_mu);
+  if (!g_sms) cudaDeviceGetAttribute(&g_sms, cudaDevAttrMultiProcessorCount, dev);
+  if (!g_pool_tuned.count(dev)) {
+    cudaMemPool_t pool;
+    if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+      uint64_t keep = ~0ull;
+      cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+    }
+    g_pool_tuned.insert(dev);
+  }
+}
+
 }  // namespace
+
+static int fnv_device(const void* const* bufs, int n_chains, int k, uint64_t len, uint64_t h0, const uint64_t* d_h0,
+                      uint64_t* d_out, void* stream);
 
 extern "C" int gs_fnv1a64_device(const void* const* bufs, int n_chains, int k, uint64_t len, uint64_t h0,
                                  uint64_t* d_out, void* stream) {
+  return fnv_device(bufs, n_chains, k, len, h0, nullptr, d_out, stream);
+}
+
+extern "C" int gs_fnv1a64_device_seeded(const void* const* bufs, int n_chains, int k, uint64_t len,
+                                        const uint64_t* d_h0, uint64_t* d_out, void* stream) {
+  if (!d_h0 || d_h0 == d_out) return ffail(GS_INVALID_ARGUMENT, "fnv1a64_device_seeded: seeds NULL or aliasing out");
+  return fnv_device(bufs, n_chains, k, len, 0, d_h0, d_out, stream);
+}
+
+static int fnv_device(const void* const* bufs, int n_chains, int k, uint64_t len, uint64_t h0, const uint64_t* d_h0,
+                      uint64_t* d_out, void* stream) {
   if (n_chains < 0 || k < 1 || k > kFCap || (n_chains > 0 && (!bufs || !d_out)))
     return ffail(GS_INVALID_ARGUMENT, "fnv1a64_device: bad arguments");
   if (len % 16) return ffail(GS_INVALID_ARGUMENT, "fnv1a64_device: buffer length must be a multiple of 16");
@@ -654,21 +685,10 @@ extern "C" int gs_fnv1a64_device(const void* const* bufs, int n_chains, int k, u
   int dev = 0;
   cudaError_t e = cudaGetDevice(&dev);
   if (e != cudaSuccess) return ffail(GS_CUDA_ERROR, "fnv1a64_device: %s", cudaGetErrorString(e));
-  {
-    std::lock_guard<std::mutex> lk(g_pool_mu);
-    if (!g_sms) cudaDeviceGetAttribute(&g_sms, cudaDevAttrMultiProcessorCount, dev);
-    if (!g_pool_tuned.count(dev)) {  // keep the stream-ordered scratch mapped between calls
-      cudaMemPool_t pool;
-      if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
-        uint64_t keep = ~0ull;
-        cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
-      }
-      g_pool_tuned.insert(dev);
-    }
-  }
+  tune_pool(dev);
   const uint64_t n = static_cast<uint64_t>(k) * len;
-  if (!g_fnv_legacy) {
-    k_fnv_init<<<(n_chains + 255) / 256, 256, 0, st>>>(d_out, n_chains, h0, n);
+  if (!g_fnv_legacy || d_h0) {
+    k_fnv_init<<<(n_chains + 255) / 256, 256, 0, st>>>(d_out, n_chains, h0, n, d_h0);
     if ((e = cudaGetLastError()) != cudaSuccess) return ffail(GS_CUDA_ERROR, "fnv init: %s", cudaGetErrorString(e));
     if (n == 0) return GS_OK;
     {
@@ -704,7 +724,8 @@ extern "C" int gs_fnv1a64_device(const void* const* bufs, int n_chains, int k, u
       cudaError_t r = cudaMemsetAsync(ctl, 0, sizeof(uint32_t) * (1 + static_cast<size_t>(total)), st);
       const int clusters = static_cast<int>(std::min<uint64_t>(g_win_clusters, total));
       if (r == cudaSuccess) {
-        k_fnv_window<<<clusters * kWCS, kWT, 0, st>>>(j, h0, static_cast<uint32_t>(cnt), total, ctl, ctl + 1,
+        k_fnv_window<<<clusters * kWCS, kWT, 0, st>>>(j, h0, d_h0 ? d_h0 + c0 : nullptr, static_cast<uint32_t>(cnt),
+                                                     total, ctl, ctl + 1,
                                                      reinterpret_cast<unsigned long long*>(d_out) + c0);
         r = cudaGetLastError();
       }
@@ -716,7 +737,7 @@ extern "C" int gs_fnv1a64_device(const void* const* bufs, int n_chains, int k, u
   const uint64_t bpc64 = (n + kFB - 1) / kFB;
   if (bpc64 > 0xFFFFFFFFull) return ffail(GS_INVALID_ARGUMENT, "fnv1a64_device: chain too long");
   const uint32_t bpc = static_cast<uint32_t>(bpc64);
-  k_fnv_init<<<(n_chains + 255) / 256, 256, 0, st>>>(d_out, n_chains, h0, n);
+  k_fnv_init<<<(n_chains + 255) / 256, 256, 0, st>>>(d_out, n_chains, h0, n, nullptr);
   if ((e = cudaGetLastError()) != cudaSuccess) return ffail(GS_CUDA_ERROR, "fnv init: %s", cudaGetErrorString(e));
   if (n == 0) return GS_OK;
   const uint64_t chain_scratch = bpc64 * kFB;
@@ -848,6 +869,9 @@ extern "C" int gs_parity_offload_sealed(const void* const* d_parity, int n_chunk
 // hash). Host chunks go first on the copy stream so their threads start early.
 // ---------------------------------------------------------------------------
 #include <atomic>
+#include <chrono>
+#include <condition_variable>
+#include <deque>
 #include <thread>
 #include <vector>
 
@@ -861,20 +885,413 @@ struct gs_verify {
   std::vector<cudaEvent_t> group_ev;      // per split group: its states are in `pinned`
   std::vector<int> group_of;              // chunk -> group index (split chunks)
   cudaEvent_t full_ev = nullptr;          // full chunks' sums are in `pinned`
+  // dynamic mode (n_full < 0): the rows >= u of each chunk are hashed by
+  // whichever side claims the chunk first -- host threads from the front (as
+  // the chunks' GPU states arrive), a GPU feeder from the back (upload into a
+  // ring + seeded GPU FNV continuing from the state)
+  bool dynamic = false;
+  int device = 0;
+  cudaStream_t cs = nullptr, ys = nullptr;
+  uint64_t* d_state = nullptr;            // [n] chain states after rows < u (device)
+  uint64_t* d_sum = nullptr;              // [n] GPU-continued checksums (device)
+  uint64_t* gsum = nullptr;               // [n] the same, pinned
+  uint8_t* ring = nullptr;                // kRing slots x (k - u) rows x len
+  std::vector<cudaEvent_t> slot_ev;       // slot's last hash + sum D2H done
+  std::vector<cudaEvent_t> up_ev;         // slot's upload landed
+  std::mutex mu;
+  int lo = 0, hi = -1;                    // unclaimed chunks [lo, hi]
+  std::vector<char> on_gpu;               // chunk claimed by the GPU feeder
+  // claim pacing (gs_verify_set_rates): a host thread takes chunks only while
+  // it would finish them before the GPU could finish everything unclaimed
+  double link_bps = 0, host_chain_bps = 0;
+  // hand-offs: a host thread that falls behind the GPU publishes its chain
+  // state at a byte offset and the feeder finishes the chain on the GPU
+  struct Handoff {
+    int c;
+    uint64_t off;
+  };
+  std::deque<Handoff> handoffs;
+  uint64_t handoff_bytes = 0;             // queued for the GPU, not yet issued
+  uint64_t* hseed = nullptr;              // [n] host chain states of handed-off chunks (pinned)
+  uint64_t* d_seed = nullptr;             // [n] the same on the device
+  void* host_block = nullptr;             // pinned, recycled: [pinned | gsum | hseed]
+  size_t host_bytes = 0;
+  uint8_t* dev_block = nullptr;           // stream-ordered on cs: [d_state | d_sum | d_seed | ring]
+  int hosts_active = 0;
+  std::condition_variable cv;
 };
 
 namespace {
 constexpr int kSplitGroup = 4;  // chunks per GPU hash launch / host lockstep group
+constexpr int kRing = 4;        // dynamic mode: GPU-claimed chunks in flight
+std::atomic<uint64_t> g_verify_handoffs{0};  // chains a host thread handed over to the GPU
+// last dynamic verification: host threads done, feeder done, hash stream
+// drained (s after finish started), chunks by host / GPU / handed off
+std::mutex g_vstats_mu;
+double g_vstats[6] = {0, 0, 0, 0, 0, 0};
+}
+
+extern "C" uint64_t gs_verify_handoffs(void) { return g_verify_handoffs.load(); }
+
+namespace {
+// Small pinned arrays of the dynamic verification, recycled across calls:
+// cudaFreeHost synchronises the whole device (it would wait for every stream
+// of the caller -- e.g. an unrelated decode -- at the end of a verification).
+std::mutex g_pinned_mu;
+std::vector<std::pair<size_t, void*>> g_pinned_free;
+
+void* pinned_take(size_t bytes) {
+  {
+    std::lock_guard<std::mutex> lk(g_pinned_mu);
+    for (size_t i = 0; i < g_pinned_free.size(); ++i)
+      if (g_pinned_free[i].first >= bytes) {
+        void* p = g_pinned_free[i].second;
+        g_pinned_free.erase(g_pinned_free.begin() + static_cast<long>(i));
+        return p;
+      }
+  }
+  void* p = nullptr;
+  return cudaMallocHost(&p, std::max<size_t>(bytes, 4096)) == cudaSuccess ? p : nullptr;
+}
+void pinned_give(void* p, size_t bytes) {
+  if (!p) return;
+  std::lock_guard<std::mutex> lk(g_pinned_mu);
+  g_pinned_free.push_back({std::max<size_t>(bytes, 4096), p});
+}
+}  // namespace
+
+extern "C" int gs_verify_last_stats(double* out6) {
+  if (!out6) return ffail(GS_INVALID_ARGUMENT, "verify_last_stats: NULL output");
+  std::lock_guard<std::mutex> lk(g_vstats_mu);
+  for (int i = 0; i < 6; ++i) out6[i] = g_vstats[i];
+  return GS_OK;
+}
+
+// Dynamic split (n_full < 0, the recovery default): rows 0..u-1 of EVERY
+// chunk are uploaded (the decode needs them anyway) and hashed on the GPU in
+// groups; the rest of each chain is claimed at run time -- host threads take
+// chunks from the front as their GPU states land, a feeder thread takes them
+// from the back and uploads their remaining rows behind the row-0 uploads,
+// continuing the chain on the GPU from the device state. Whichever side is
+// faster on this host takes more chunks; both finish together.
+static int verify_enqueue_dynamic(const void* const* h_parity, int n_chunks, int k, uint64_t len, int u,
+                                  void* const* d_parity, cudaStream_t cs, cudaStream_t ys, gs_verify** out) {
+  constexpr uint64_t kOffset = 0xcbf29ce484222325ull;
+  auto* v = new gs_verify;
+  v->dynamic = true;
+  v->n = n_chunks;
+  v->k = k;
+  v->u = u;
+  v->len = len;
+  v->cs = cs;
+  v->ys = ys;
+  v->lo = 0;
+  v->hi = n_chunks - 1;
+  v->on_gpu.assign(n_chunks, 0);
+  cudaGetDevice(&v->device);
+  v->host_rows.resize(static_cast<size_t>(n_chunks) * k);
+  for (size_t i = 0; i < v->host_rows.size(); ++i) v->host_rows[i] = static_cast<const uint8_t*>(h_parity[i]);
+  v->group_of.assign(n_chunks, -1);
+  auto bail = [&](int st) {
+    cudaStreamSynchronize(cs);
+    cudaStreamSynchronize(ys);
+    for (auto e : v->group_ev) cudaEventDestroy(e);
+    for (auto e : v->slot_ev) cudaEventDestroy(e);
+    for (auto e : v->up_ev) cudaEventDestroy(e);
+    pinned_give(v->host_block, v->host_bytes);
+    if (v->dev_block) cudaFreeAsync(v->dev_block, cs);
+    delete v;
+    return st;
+  };
+  tune_pool(v->device);
+  const size_t nb = sizeof(uint64_t) * std::max(1, n_chunks);
+  v->host_bytes = 3 * nb;
+  v->host_block = pinned_take(v->host_bytes);
+  cudaError_t e = v->host_block ? cudaSuccess : cudaErrorMemoryAllocation;
+  if (e == cudaSuccess) {
+    v->pinned = static_cast<uint64_t*>(v->host_block);
+    v->gsum = v->pinned + std::max(1, n_chunks);
+    v->hseed = v->gsum + std::max(1, n_chunks);
+    const size_t ring = k > u ? static_cast<size_t>(kRing) * (k - u) * len : 0;
+    e = cudaMallocAsync(reinterpret_cast<void**>(&v->dev_block), 3 * nb + 256 + ring, cs);
+  }
+  if (e == cudaSuccess) {
+    v->d_state = reinterpret_cast<uint64_t*>(v->dev_block);
+    v->d_sum = v->d_state + std::max(1, n_chunks);
+    v->d_seed = v->d_sum + std::max(1, n_chunks);
+    if (k > u) v->ring = v->dev_block + (3 * nb + 255) / 256 * 256;
+    cudaEvent_t ready;  // the copy stream's ring uploads come after the stream-ordered allocation
+    e = cudaEventCreateWithFlags(&ready, cudaEventDisableTiming);
+    if (e == cudaSuccess) e = cudaEventRecord(ready, cs);
+    if (e == cudaSuccess) e = cudaStreamWaitEvent(ys, ready, 0);
+    cudaEventDestroy(ready);
+  }
+  for (int r = 0; e == cudaSuccess && k > u && r < kRing; ++r) {
+    cudaEvent_t a, b;
+    e = cudaEventCreateWithFlags(&a, cudaEventDisableTiming | cudaEventBlockingSync);
+    if (e == cudaSuccess) e = cudaEventCreateWithFlags(&b, cudaEventDisableTiming);
+    if (e == cudaSuccess) {
+      v->slot_ev.push_back(a);
+      v->up_ev.push_back(b);
+    }
+  }
+  if (e != cudaSuccess) return bail(ffail(GS_CUDA_ERROR, "verify_enqueue: %s", cudaGetErrorString(e)));
+  cudaEvent_t up;
+  if ((e = cudaEventCreateWithFlags(&up, cudaEventDisableTiming)) != cudaSuccess)
+    return bail(ffail(GS_CUDA_ERROR, "verify_enqueue: %s", cudaGetErrorString(e)));
+  int st = GS_OK;
+  for (int g0 = 0; g0 < n_chunks && st == GS_OK; g0 += kSplitGroup) {
+    const int cnt = std::min(kSplitGroup, n_chunks - g0);
+    for (int c = g0; c < g0 + cnt && e == cudaSuccess; ++c)
+      for (int i = 0; i < u && e == cudaSuccess; ++i) {
+        const size_t r = static_cast<size_t>(c) * k + i;
+        e = (!h_parity[r] || !d_parity[r]) ? cudaErrorInvalidValue
+                                           : cudaMemcpyAsync(d_parity[r], h_parity[r], len, cudaMemcpyHostToDevice, ys);
+      }
+    if (e == cudaSuccess) e = cudaEventRecord(up, ys);
+    if (e == cudaSuccess) e = cudaStreamWaitEvent(cs, up, 0);
+    if (e != cudaSuccess) {
+      st = ffail(GS_CUDA_ERROR, "verify_enqueue upload: %s", cudaGetErrorString(e));
+      break;
+    }
+    std::vector<const void*> rows(static_cast<size_t>(cnt) * u);
+    for (int c = 0; c < cnt; ++c)
+      for (int i = 0; i < u; ++i) rows[static_cast<size_t>(c) * u + i] = d_parity[static_cast<size_t>(g0 + c) * k + i];
+    if ((st = gs_fnv1a64_device(rows.data(), cnt, u, len, kOffset, v->d_state + g0, cs)) != GS_OK) break;
+    cudaEvent_t ge;
+    e = cudaEventCreateWithFlags(&ge, cudaEventDisableTiming | cudaEventBlockingSync);
+    if (e == cudaSuccess) {
+      v->group_ev.push_back(ge);
+      e = cudaMemcpyAsync(v->pinned + g0, v->d_state + g0, sizeof(uint64_t) * cnt, cudaMemcpyDeviceToHost, cs);
+    }
+    if (e == cudaSuccess) e = cudaEventRecord(ge, cs);
+    if (e != cudaSuccess) st = ffail(GS_CUDA_ERROR, "verify_enqueue: %s", cudaGetErrorString(e));
+    for (int c = g0; c < g0 + cnt; ++c) v->group_of[c] = static_cast<int>(v->group_ev.size()) - 1;
+  }
+  cudaEventDestroy(up);
+  if (st != GS_OK) return bail(st);
+  *out = v;
+  return GS_OK;
+}
+
+// The GPU feeder: hashes the remaining rows (u..k-1, one contiguous chain of
+// (k-u)*len bytes per chunk) of (a) chunks handed off by host threads, from
+// their byte offset and host state, and (b) unclaimed chunks, taken from the
+// back, from their device state. Each goes through a ring slot: upload on the
+// copy stream, seeded GPU FNV on the hash stream, checksum to pinned.
+static int verify_feeder(gs_verify* v) {
+  cudaSetDevice(v->device);
+  int issued = 0, st = GS_OK;
+  const uint64_t total = static_cast<uint64_t>(v->k - v->u) * v->len;
+  for (;;) {
+    const int r = issued % kRing;
+    if (issued >= kRing && cudaEventSynchronize(v->slot_ev[r]) != cudaSuccess)  // slot free again
+      return ffail(GS_CUDA_ERROR, "verify feeder: slot wait failed");
+    int c = -1;
+    uint64_t off = 0;
+    {
+      std::unique_lock<std::mutex> lk(v->mu);
+      for (;;) {
+        if (!v->handoffs.empty()) {
+          c = v->handoffs.front().c;
+          off = v->handoffs.front().off;
+          v->handoffs.pop_front();
+          v->handoff_bytes -= total - off;
+          v->on_gpu[c] = 2;
+          break;
+        }
+        if (v->lo <= v->hi) {
+          c = v->hi--;
+          v->on_gpu[c] = 1;
+          break;
+        }
+        if (v->hosts_active == 0) break;
+        v->cv.wait_for(lk, std::chrono::microseconds(200));
+      }
+    }
+    if (c < 0) break;
+    uint8_t* slot = v->ring + static_cast<size_t>(r) * total;
+    cudaError_t e = cudaSuccess;
+    for (uint64_t o = off; o < total && e == cudaSuccess;) {  // the chain's bytes [off, total), packed
+      const uint64_t row = o / v->len, in = o - row * v->len, n = v->len - in;
+      e = cudaMemcpyAsync(slot + (o - off), v->host_rows[static_cast<size_t>(c) * v->k + v->u + row] + in, n,
+                          cudaMemcpyHostToDevice, v->ys);
+      o += n;
+    }
+    if (e == cudaSuccess) e = cudaEventRecord(v->up_ev[r], v->ys);
+    if (e == cudaSuccess) e = cudaStreamWaitEvent(v->cs, v->up_ev[r], 0);
+    const uint64_t* seed = v->d_state + c;
+    if (e == cudaSuccess && off > 0) {
+      e = cudaMemcpyAsync(v->d_seed + c, v->hseed + c, sizeof(uint64_t), cudaMemcpyHostToDevice, v->cs);
+      seed = v->d_seed + c;
+    }
+    if (e != cudaSuccess) return ffail(GS_CUDA_ERROR, "verify feeder: %s", cudaGetErrorString(e));
+    const void* ptr = slot;
+    if ((st = gs_fnv1a64_device_seeded(&ptr, 1, 1, total - off, seed, v->d_sum + c, v->cs)) != GS_OK) return st;
+    e = cudaMemcpyAsync(v->gsum + c, v->d_sum + c, sizeof(uint64_t), cudaMemcpyDeviceToHost, v->cs);
+    if (e == cudaSuccess) e = cudaEventRecord(v->slot_ev[r], v->cs);
+    if (e != cudaSuccess) return ffail(GS_CUDA_ERROR, "verify feeder: %s", cudaGetErrorString(e));
+    ++issued;
+  }
+  return st;
+}
+
+// Chains a host thread claims at once and hashes in lockstep (FNV is one
+// serial multiply chain per stream: two chains cost a core about the latency
+// of one; C3 recovery, tools/c3_probe.py: 2 -> 157-165 ms, 3 -> 166 ms,
+// 4 -> 184 ms). GS_VERIFY_CLAIM overrides (A/B).
+static int v_claim_chains() {
+  static const int n = [] {
+    const char* e = std::getenv("GS_VERIFY_CLAIM");
+    return e ? std::atoi(e) : 2;
+  }();
+  return n;
+}
+
+static int verify_finish_dynamic(gs_verify* v, int threads, uint64_t* sums, int* gpu_chunks) {
+  using clk = std::chrono::steady_clock;
+  constexpr uint64_t kSlice = 4ull << 20;  // host progress check / hand-off granularity (bytes per chain)
+  int st = GS_OK;
+  std::atomic<int> err{0};
+  const uint64_t total = static_cast<uint64_t>(v->k - v->u) * v->len;
+  int fst = GS_OK;
+  const auto t0 = clk::now();
+  auto secs = [&] { return std::chrono::duration<double>(clk::now() - t0).count(); };
+  // pacing model: the GPU hashes the remaining rows once the row-0 uploads
+  // (already queued) have landed, at the link rate; a host thread hashes its
+  // claimed chains at host_chain_bps each (learned online)
+  const double link = v->link_bps;
+  const double t_rows0 = link > 0 ? static_cast<double>(v->n) * v->u * static_cast<double>(v->len) / link : 0;
+  double chain_bps = v->host_chain_bps;
+  auto gpu_queue_s = [&] {  // under v->mu: GPU work not yet issued
+    return link > 0 ? (static_cast<double>(v->hi - v->lo + 1) * total + v->handoff_bytes) / link : 0;
+  };
+  v->hosts_active = total > 0 ? std::max(threads, 1) : 0;
+  std::thread feeder;
+  if (total > 0) feeder = std::thread([&] { fst = verify_feeder(v); });
+  const int per = std::max(1, std::min(8, v_claim_chains()));
+  auto work = [&] {
+    for (;;) {
+      int c[8], m = 0;
+      {
+        std::lock_guard<std::mutex> lk(v->mu);
+        const double now = secs();
+        if (link > 0 && chain_bps > 0 &&
+            now + total / chain_bps >= std::max(now, t_rows0) + gpu_queue_s())  // the GPU would finish first
+          break;
+        while (m < per && v->lo <= v->hi) c[m++] = v->lo++;
+      }
+      if (m == 0) break;
+      uint64_t h[8];
+      for (int q = 0; q < m; ++q) {
+        if (cudaEventSynchronize(v->group_ev[v->group_of[c[q]]]) != cudaSuccess) {
+          err = 1;
+          break;
+        }
+        h[q] = v->pinned[c[q]];
+      }
+      if (err) break;
+      const double start = secs();
+      bool handed = false;
+      for (uint64_t o = 0; o < total;) {
+        const uint64_t row = o / v->len, in = o - row * v->len;
+        const uint64_t n = std::min<uint64_t>(kSlice, v->len - in);
+        const uint8_t* ps[8];
+        for (int q = 0; q < m; ++q) ps[q] = v->host_rows[static_cast<size_t>(c[q]) * v->k + v->u + row] + in;
+        gsb::fnv1a64_x8(ps, m, n, h);
+        o += n;
+        if (o >= total || link <= 0) continue;
+        std::lock_guard<std::mutex> lk(v->mu);
+        const double now = secs(), rate = o / std::max(now - start, 1e-6);
+        chain_bps = chain_bps > 0 ? 0.5 * chain_bps + 0.5 * rate : rate;
+        const double host_left = (total - o) / rate;
+        // the GPU's finish if it took the rest: behind the row-0 uploads, the
+        // ring already in flight and the queue; hand over only when clearly
+        // later on the host (a hand-over re-uploads the rest of the chain)
+        const double gpu_done =
+            std::max(now, t_rows0) + kRing * (total / link) + gpu_queue_s() + m * (total - o) / link;
+        // a safety net for a host that stalls (not a balancing tool: the claim
+        // pacing balances): at least a quarter of the chain done, and the host
+        // would need over twice as long as the GPU for the rest
+        if (4 * o >= total && host_left > 2e-3 && host_left > 2.0 * (gpu_done - now)) {
+          for (int q = 0; q < m; ++q) {
+            v->hseed[c[q]] = h[q];
+            v->handoffs.push_back({c[q], o});
+            v->handoff_bytes += total - o;
+          }
+          handed = true;
+          g_verify_handoffs.fetch_add(static_cast<uint64_t>(m));
+          v->cv.notify_all();
+          break;
+        }
+      }
+      if (handed) break;
+      for (int q = 0; q < m; ++q) sums[c[q]] = h[q];
+    }
+    {
+      std::lock_guard<std::mutex> lk(v->mu);
+      --v->hosts_active;
+    }
+    v->cv.notify_all();
+  };
+  if (total > 0) {
+    std::vector<std::thread> pool;
+    for (int t = 1; t < std::max(threads, 1); ++t) pool.emplace_back(work);
+    work();
+    for (auto& t : pool) t.join();
+  }
+  const double t_hosts = secs();
+  if (feeder.joinable()) feeder.join();
+  const double t_feeder = secs();
+  if (err) st = ffail(GS_CUDA_ERROR, "verify_finish: GPU chain state unavailable");
+  if (st == GS_OK && fst != GS_OK) st = fst;
+  // every D2H into pinned / gsum has landed before they are read or freed
+  cudaSetDevice(v->device);
+  if (cudaStreamSynchronize(v->cs) != cudaSuccess && st == GS_OK)
+    st = ffail(GS_CUDA_ERROR, "verify_finish: hash stream failed");
+  cudaStreamSynchronize(v->ys);
+  int on = 0;
+  if (st == GS_OK) {
+    for (int c = 0; c < v->n; ++c) {
+      if (total == 0) {
+        sums[c] = v->pinned[c];  // every row was uploaded: the state is the checksum
+        ++on;
+      } else if (v->on_gpu[c]) {
+        sums[c] = v->gsum[c];
+        on += v->on_gpu[c] == 1;
+      }
+    }
+  }
+  if (gpu_chunks) *gpu_chunks = on;
+  {
+    int handed = 0, by_host = 0;
+    for (int c = 0; c < v->n; ++c) {
+      handed += v->on_gpu[c] == 2;
+      by_host += v->on_gpu[c] == 0;
+    }
+    std::lock_guard<std::mutex> lk(g_vstats_mu);
+    const double vals[6] = {t_hosts, t_feeder, secs(), static_cast<double>(by_host), static_cast<double>(on),
+                            static_cast<double>(handed)};
+    for (int i = 0; i < 6; ++i) g_vstats[i] = vals[i];
+  }
+  for (auto e : v->group_ev) cudaEventDestroy(e);
+  for (auto e : v->slot_ev) cudaEventDestroy(e);
+  for (auto e : v->up_ev) cudaEventDestroy(e);
+  pinned_give(v->host_block, v->host_bytes);
+  cudaFreeAsync(v->dev_block, v->cs);  // stream-ordered: no device-wide synchronisation
+  delete v;
+  return st;
 }
 
 extern "C" int gs_verify_enqueue(const void* const* h_parity, int n_chunks, int k, uint64_t len, int n_full, int u,
                                  void* const* d_parity, void* compute, void* copy, gs_verify** out) {
   constexpr uint64_t kOffset = 0xcbf29ce484222325ull;
-  if (!out || n_chunks < 0 || k < 1 || u < 1 || u > k || n_full < 0 || n_full > n_chunks ||
+  if (!out || n_chunks < 0 || k < 1 || u < 1 || u > k || n_full > n_chunks ||
       (n_chunks > 0 && (!h_parity || !d_parity)))
     return ffail(GS_INVALID_ARGUMENT, "verify_enqueue: bad arguments");
   *out = nullptr;
   cudaStream_t cs = static_cast<cudaStream_t>(compute), ys = static_cast<cudaStream_t>(copy);
+  if (n_full < 0) return verify_enqueue_dynamic(h_parity, n_chunks, k, len, u, d_parity, cs, ys, out);
   auto* v = new gs_verify;
   v->n = n_chunks;
   v->n_full = n_full;
@@ -961,8 +1378,31 @@ extern "C" int gs_verify_enqueue(const void* const* h_parity, int n_chunks, int 
 
 // Blocks: host threads continue the split chunks' chains over rows u..k-1 as
 // their GPU states arrive; sums[c] = chunk c's checksum. Frees `v`.
+extern "C" int gs_verify_finish_ex(gs_verify* v, int threads, uint64_t* sums, int* gpu_chunks);
+
+extern "C" int gs_verify_set_rates(gs_verify* v, double link_gbs, double host_chain_gbs) {
+  if (!v || link_gbs < 0 || host_chain_gbs < 0) return ffail(GS_INVALID_ARGUMENT, "verify_set_rates: bad arguments");
+  v->link_bps = link_gbs * 1e9;
+  v->host_chain_bps = host_chain_gbs * 1e9;
+  return GS_OK;
+}
+
 extern "C" int gs_verify_finish(gs_verify* v, int threads, uint64_t* sums) {
+  return gs_verify_finish_ex(v, threads, sums, nullptr);
+}
+
+extern "C" int gs_verify_finish_ex(gs_verify* v, int threads, uint64_t* sums, int* gpu_chunks) {
   if (!v) return ffail(GS_INVALID_ARGUMENT, "verify_finish: NULL handle");
+  if (v->dynamic) {
+    if (v->n > 0 && !sums) {
+      uint64_t* tmp = new uint64_t[v->n];  // still drain and free the handle
+      verify_finish_dynamic(v, threads, tmp, gpu_chunks);
+      delete[] tmp;
+      return ffail(GS_INVALID_ARGUMENT, "verify_finish: NULL output");
+    }
+    return verify_finish_dynamic(v, threads, sums, gpu_chunks);
+  }
+  if (gpu_chunks) *gpu_chunks = v->n_full;
   int st = GS_OK;
   if (v->n > 0 && !sums) st = ffail(GS_INVALID_ARGUMENT, "verify_finish: NULL output");
   const int ns = v->n - v->n_full;

@@ -199,9 +199,15 @@ def test_long_request_single_failure_rs82_bit_exact():
     res = ck.recover(6, FailureEvent([5], at_chunk=32), run.ground_truth, [2048] * 32)
     assert res.plan.mode == RecoveryMode.kHybrid and res.plan.recompute_chunks == 0
     assert res.verified and len(res.plan.reconstruct_ids) == 32
-    # verification split: some entries checksummed entirely in HBM, the rest
-    # GPU-hashed over the decode's row and finished on host threads
-    assert 0 < res.verify_gpu_chunks < 32
+    # dynamic verification split (default): every chunk's row 0 hashed on the
+    # GPU, the rest of each chain claimed at run time by host threads or the
+    # GPU feeder
+    assert 0 <= res.verify_gpu_chunks <= 32 and ck.verify_split == "dynamic"
+    for threads in (1, 2):   # few host threads: the GPU feeder takes most of the chains
+        res = ck.recover(6, FailureEvent([5], at_chunk=32), run.ground_truth, [2048] * 32, verify_threads=threads)
+        assert res.verified and res.decoded_chunks == 32 and res.verify_gpu_chunks > 0, threads
+    # static split (decided from the host-rate estimates): all in HBM / all split / host only
+    ck.verify_split = "static"
     for gpu, rate, want in [(True, 1.0, 32), (True, 1e30, 0), (False, None, 0)]:
         ck.gpu_verify = gpu
         if rate:
@@ -223,8 +229,12 @@ def test_bad_parity_and_over_tolerance_fallbacks():
     ck.cfg.cost.restart_overhead = 1e9
     res = ck.recover(3, FailureEvent([1], at_chunk=4), run.ground_truth, [16] * 4)
     assert res.plan.mode == RecoveryMode.kFullRecomputeFallback   # corrupt chunk 2 -> fallback
-    # the corrupt entry caught by the GPU checksum (every entry verified in HBM)
-    # and by the host threads alone
+    # the corrupt entry caught by the dynamic split, by the GPU checksum (every
+    # entry verified in HBM), by host threads continuing GPU states, and by the
+    # host threads alone
+    res = ck.recover(3, FailureEvent([1], at_chunk=4), run.ground_truth, [16] * 4)
+    assert res.plan.mode == RecoveryMode.kFullRecomputeFallback and res.corrupt_chunks == [2]
+    ck.verify_split = "static"
     for gpu, rate in [(True, 1.0), (True, 1e30), (False, None)]:
         ck.gpu_verify = gpu
         if rate:   # 1.0: host FNV "slow" -> every entry on the GPU; 1e30: host "fast" -> all split

@@ -222,3 +222,69 @@ def test_sealed_commit_owns_its_checksums(where):
             status, e = store.get(rnd, c, verify=False)
             assert int(status) == 0 and e.checksum == rnd * 1000 + c + 1, (rnd, c)
     store.close()
+
+
+@pytest.mark.parametrize("u,threads,rates,ln", [(1, 1, None, 16384 * 5 + 32), (1, 4, None, 16384 * 5 + 32),
+                                                (2, 3, None, 16384 * 5 + 32), (3, 2, None, 16384 * 5 + 32),
+                                                (2, 4, (1000.0, 1000.0), (6 << 20) + 48),
+                                                (1, 3, (30.0, 0.5), (6 << 20) + 48)])
+def test_dynamic_split_verification(u, threads, rates, ln):
+    """gs_verify_enqueue(n_full = -1): rows < u of every chunk uploaded and
+    hashed on the GPU, the rest of each chain claimed at run time by host
+    threads (from the front) or the GPU feeder (from the back, seeded GPU
+    FNV), incl. host threads handing a chain over to the GPU mid-row when
+    they fall behind it (rates: a link so fast that every host claim hands
+    off after its first 4 MiB slice): every checksum equals
+    ParityChunk::compute_checksum, the uploaded rows equal the host rows."""
+    port = O.port()
+    rng = np.random.default_rng(500 + 10 * u + threads)
+    n, k = (13, 3) if rates is None else (6, 3)
+    host = [torch.from_numpy(rng.integers(0, 256, ln, dtype=np.uint8)).pin_memory() for _ in range(n * k)]
+    dev = torch.zeros((n, u, ln), dtype=torch.uint8, device="cuda")
+    drows = [dev[c, i].data_ptr() if i < u else None for c in range(n) for i in range(k)]
+    lib = L.lib()
+    comp, copy = torch.cuda.Stream(), torch.cuda.Stream()
+    torch.cuda.synchronize()
+    h = C.c_void_p()
+    assert lib.gs_verify_enqueue(L.ptr_array([t.data_ptr() for t in host]), n, k, ln, -1, u,
+                                 L.ptr_array(drows), comp.cuda_stream, copy.cuda_stream, C.byref(h)) == 0
+    if rates is not None:
+        assert lib.gs_verify_set_rates(h, *rates) == 0
+    out = (C.c_uint64 * n)()
+    gpu = C.c_int(-1)
+    handoffs0 = lib.gs_verify_handoffs()
+    assert lib.gs_verify_finish_ex(h, threads, out, C.byref(gpu)) == 0, lib.gs_last_error()
+    torch.cuda.synchronize()
+    assert 0 <= gpu.value <= n and (u < k or gpu.value == n)
+    if rates == (1000.0, 1000.0):
+        assert lib.gs_verify_handoffs() > handoffs0
+    for c in range(n):
+        assert out[c] == port.parity_checksum([host[c * k + i].numpy() for i in range(k)]), (c, u, threads)
+        for i in range(u):
+            assert torch.equal(dev[c, i].cpu(), host[c * k + i])
+
+
+def test_seeded_device_fnv_continues_chains():
+    """gs_fnv1a64_device_seeded: hashing the second half of each chain from
+    the device-resident state after the first half equals hashing the whole
+    chain (the continuation the dynamic verification's GPU feeder uses)."""
+    port = O.port()
+    rng = np.random.default_rng(71)
+    n, ln = 5, 16384 * 3 + 48
+    host = [rng.integers(0, 256, ln, dtype=np.uint8) for _ in range(n * 4)]
+    dev = [torch.from_numpy(x).cuda() for x in host]
+    first = torch.zeros(n, dtype=torch.int64, device="cuda")
+    both = torch.zeros(n, dtype=torch.int64, device="cuda")
+    lib = L.lib()
+    st = torch.cuda.current_stream()
+    assert lib.gs_fnv1a64_device(L.ptr_array([dev[c * 4 + i].data_ptr() for c in range(n) for i in range(2)]), n, 2,
+                                 ln, OFFSET, first.data_ptr(), st.cuda_stream) == 0
+    assert lib.gs_fnv1a64_device_seeded(L.ptr_array([dev[c * 4 + 2 + i].data_ptr() for c in range(n)
+                                                     for i in range(2)]), n, 2, ln, first.data_ptr(),
+                                        both.data_ptr(), st.cuda_stream) == 0
+    assert lib.gs_fnv1a64_device_seeded(L.ptr_array([dev[0].data_ptr()]), 1, 1, ln, first.data_ptr(),
+                                        first.data_ptr(), st.cuda_stream) == L.GS_INVALID_ARGUMENT
+    st.synchronize()
+    got = [int(v) & (2**64 - 1) for v in both.cpu().tolist()]
+    for c in range(n):
+        assert got[c] == port.parity_checksum(host[c * 4:(c + 1) * 4]), c
