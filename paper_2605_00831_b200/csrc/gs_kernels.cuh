@@ -221,10 +221,18 @@ __device__ __forceinline__ uint64_t paged_offset(const PageMap& m, uint32_t s, u
 
 // Same for byte `tile_logical + lane_off` of a CTA tile: when the whole 4 KiB
 // tile sits inside one segment (and one cache block), the page arithmetic and
-// the block-table lookup are CTA-uniform; only an add + compare remain per
-// thread. Every paged geometry of the configs (4 KiB blocks) takes this path.
-__device__ __forceinline__ uint64_t paged_offset_tile(const PageMap& m, uint32_t s, uint64_t tile_logical,
-                                                      uint32_t lane_off, bool& masked) {
+// the block-table lookup depend only on the tile (`paged_tile_base`, inputs
+// uniform across the CTA, so the compiler keeps them on the uniform datapath);
+// only an add + compare remain per thread. Every paged geometry of the
+// configs (4 KiB blocks) takes this path.
+struct PagedTile {
+  uint64_t base;    // cache offset of the tile's first byte
+  uint32_t in0;     // its offset inside the segment
+  bool fast;        // the tile stays inside one segment and one block
+};
+
+__device__ __forceinline__ PagedTile paged_tile_base(const PageMap& m, uint32_t s, uint64_t tile_logical) {
+  PagedTile pt{0, 0, false};
   const uint32_t u = static_cast<uint32_t>(tile_logical);
   const uint32_t q = fdiv(u, m.page_bytes, m.page_m);
   const uint32_t in0 = u - q * m.page_bytes;
@@ -234,15 +242,25 @@ __device__ __forceinline__ uint64_t paged_offset_tile(const PageMap& m, uint32_t
   if (in0 + static_cast<uint32_t>(kTile) <= m.page_bytes && ib0 + static_cast<uint32_t>(kTile) <= bb) {
     const uint32_t t = fdiv(q, m.layers, m.layers_m);
     const uint32_t l = q - t * m.layers;
-    const uint32_t in = in0 + lane_off;
-    masked = in >= m.valid_tokens * m.token_bytes;
-    uint64_t r = static_cast<uint64_t>(l) * m.layer_stride + static_cast<uint64_t>(t) * m.kv_stride + ib0 + lane_off;
+    uint64_t r = static_cast<uint64_t>(l) * m.layer_stride + static_cast<uint64_t>(t) * m.kv_stride + ib0;
     if (m.table) {
       const bool tile_masked = in0 >= m.valid_tokens * m.token_bytes;  // whole tile beyond valid
       const int32_t blk = tile_masked ? 0 : m.table[static_cast<uint64_t>(s) * m.table_stride + pi];
       r += static_cast<uint64_t>(blk) * m.block_bytes;
     }
-    return r;
+    pt.base = r;
+    pt.in0 = in0;
+    pt.fast = true;
+  }
+  return pt;
+}
+
+__device__ __forceinline__ uint64_t paged_offset_tile(const PageMap& m, uint32_t s, uint64_t tile_logical,
+                                                      uint32_t lane_off, bool& masked) {
+  const PagedTile pt = paged_tile_base(m, s, tile_logical);
+  if (pt.fast) {
+    masked = pt.in0 + lane_off >= m.valid_tokens * m.token_bytes;
+    return pt.base + lane_off;
   }
   return paged_offset(m, s, tile_logical + lane_off, masked);
 }
