@@ -1131,9 +1131,9 @@ def decode_overhead(torch, dev, pipe, args):
     enc = encoder(CodingScheme.reed_solomon(8, 2))
     slots = L.ptr_array([data[s, j].data_ptr() for s in range(32) for j in range(8)])
     outs = L.ptr_array([h_par[s, i].data_ptr() for s in range(32) for i in range(2)])
-    main = torch.cuda.Stream(device=dev)
-    side, side_copy = torch.cuda.Stream(device=dev), torch.cuda.Stream(device=dev)
     sink = torch.empty(2, device=dev)
+    from paper_2605_00831_b200 import device as D
+    bpipe = D.Pipeline(dev.index or 0, 64 << 20)   # the checkpoint's own pipeline (CTA cap per policy)
 
     def step():
         x = x0
@@ -1142,45 +1142,67 @@ def decode_overhead(torch, dev, pipe, args):
             x = ys[li % 2][:, :hid]
         torch.amax(kvc, dim=0, out=sink[1])
 
-    def ckpt():
-        check(L.lib().gs_encode_offload(pipe.handle, enc.handle, 32, slots, outs, rng, side.cuda_stream,
-                                        side_copy.cuda_stream), "overhead ckpt")
+    def measure(max_ctas, main_prio):
+        """(base block ms, block ms with the checkpoint, checkpoint alone ms)
+        for one placement policy; base / with runs alternate (min of 4 each)."""
+        check(L.lib().gs_pipeline_set_max_ctas(bpipe.handle, max_ctas), "max ctas")
+        main = torch.cuda.Stream(device=dev, priority=main_prio)
+        side, side_copy = torch.cuda.Stream(device=dev), torch.cuda.Stream(device=dev)
 
-    def run(blocks, with_ckpt):
-        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        with torch.cuda.stream(main):
-            e0.record(main)
-            for _ in range(blocks):
-                if with_ckpt:
-                    side.wait_stream(main)
-                    ckpt()
-                for _ in range(16):
-                    step()
-            main.wait_stream(side_copy)
-            e1.record(main)
-        e1.synchronize()
-        return e0.elapsed_time(e1)
+        def ckpt():
+            check(L.lib().gs_encode_offload(bpipe.handle, enc.handle, 32, slots, outs, rng, side.cuda_stream,
+                                            side_copy.cuda_stream), "overhead ckpt")
 
-    run(1, True)
-    run(1, False)
-    blocks = 4
-    base = min(run(blocks, False) for _ in range(3))
-    withc = min(run(blocks, True) for _ in range(3))
-    a0, a1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    a0.record(side)
-    ckpt()
-    side.wait_stream(side_copy)
-    a1.record(side)
-    a1.synchronize()
+        def run(blocks, with_ckpt):
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            with torch.cuda.stream(main):
+                e0.record(main)
+                for _ in range(blocks):
+                    if with_ckpt:
+                        side.wait_stream(main)
+                        ckpt()
+                    for _ in range(16):
+                        step()
+                main.wait_stream(side_copy)
+                e1.record(main)
+            e1.synchronize()
+            return e0.elapsed_time(e1)
+
+        run(1, True)
+        run(1, False)
+        blocks = 4
+        base, withc = [], []
+        for _ in range(4):
+            base.append(run(blocks, False))
+            withc.append(run(blocks, True))
+        a0, a1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a0.record(side)
+        ckpt()
+        side.wait_stream(side_copy)
+        a1.record(side)
+        a1.synchronize()
+        return min(base) / blocks, min(withc) / blocks, a0.elapsed_time(a1)
+
+    policies = {}
+    for name, cap, prio in (("whole_gpu", 0, 0), ("decode_high_priority", 0, -1),
+                            ("background_16_ctas", 16, -1), ("background_4_ctas", 4, -1)):
+        b_ms, w_ms, alone = measure(cap, prio)
+        policies[name] = {"max_ctas": cap, "decode_stream_priority": "high" if prio < 0 else "default",
+                          "block_ms_without_ckpt": round(b_ms, 4), "block_ms_with_ckpt": round(w_ms, 4),
+                          "checkpoint_alone_ms": round(alone, 4),
+                          "overhead_pct_of_block": round((w_ms - b_ms) / b_ms * 100, 3),
+                          "overhead_pct_of_decode_step": round((w_ms - b_ms) / (b_ms / 16) * 100, 3)}
+    # the serving policy (declared, not picked after the fact): decode on a
+    # high-priority stream, the block checkpoint capped to 16 CTAs
+    # (gs_pipeline_set_max_ctas) on default-priority side streams
+    best = "background_16_ctas"
+    bpipe.close()
     out = {"model": "Llama-3-70B KV, TP=8, batch 32, one GPU's share", "context_tokens": ctx,
            "decode_step": "80 x bf16 GEMM [32 x 8192] @ [8192 x 13440] (cuBLAS, this GPU's 17.6 GB weight shard) "
                           "+ KV read at the context; checkpoint: K1 over this GPU's 1/8 range of the block + D2H on "
                           "side streams (all shards local: the 7/8 NVLink reads of a real TP=8 group are not emulated)",
-           "decode_step_ms": round(base / (blocks * 16), 4),
-           "block_ms_without_ckpt": round(base / blocks, 4), "block_ms_with_ckpt": round(withc / blocks, 4),
-           "checkpoint_alone_ms": round(a0.elapsed_time(a1), 4),
-           "overhead_pct_of_block": round((withc - base) / base * 100, 3),
-           "overhead_pct_of_decode_step": round((withc - base) / blocks / (base / (blocks * 16)) * 100, 3)}
+           "decode_step_ms": round(policies[best]["block_ms_without_ckpt"] / 16, 4),
+           "policy": best, **{k: v for k, v in policies[best].items()}, "policies": policies}
     del w, kvc, data, h_par, x0, ys
     torch.cuda.empty_cache()
     return out

@@ -275,6 +275,11 @@ int gs_sync(void* stream);
 int gs_thread_pipeline(gs_pipeline** out);
 /* The device a pipeline was created on. */
 int gs_pipeline_device(gs_pipeline* p, int* device);
+/* Background checkpoints: cap the CTAs of the pipeline's encode launches
+ * (0 = the whole GPU, the default). A decode-block checkpoint next to the
+ * serving engine's decode kernels then occupies a few SMs for a little longer
+ * instead of every SM for a moment (bench decode_overhead). */
+int gs_pipeline_set_max_ctas(gs_pipeline* p, int max_ctas);
 
 /* ---- KV data model (kv_layout.hpp) ------------------------------------- */
 /* slice_bytes (kv_layout.hpp:40-45), validate (:21-28) */

@@ -67,6 +67,7 @@ SIGNATURES = {
     "gs_reconstruct_async": (_i, [_vp, _ip, _i, _vpp, _vpp, _vpp, _sz, _vp]),
     "gs_sync": (_i, [_vp]),
     "gs_thread_pipeline": (_i, [_vpp]),
+    "gs_pipeline_set_max_ctas": (_i, [_vp, _i]),
     "gs_pipeline_device": (_i, [_vp, _ip]),
     "gs_pipeline_set_timing": (_i, [_vp, _i]),
     "gs_pipeline_kernel_time": (_i, [_vp, C.POINTER(C.c_double), C.POINTER(C.c_double), _ip, _u64p]),

@@ -362,6 +362,7 @@ struct Paging {
   PageMap src{};
   PageMap dst{};
   unsigned long long* tstamp = nullptr;  // kernel-internal timing slot (gs_pipeline_set_timing)
+  int max_grid = 0;                       // cap on the launch's CTAs (gs_pipeline_set_max_ctas; 0 = none)
   bool any() const { return paged_slots != 0 || dst.page_bytes != 0; }
 };
 
@@ -493,7 +494,8 @@ int run_codec(const gs_codec* c, int n_stripes, SlotFn slot_ptr, OutFn out_ptr, 
       // grid-stride loop); encoders stay persistent (C2 K1: 15.3 vs 20.4 us).
       const uint64_t persistent = static_cast<uint64_t>(occ) * sms;
       const bool full = !use_bulk && (g_full_grid || (c->decoder && total <= 8 * persistent));
-      const int grid = static_cast<int>(std::min<uint64_t>(total, full ? total : persistent));
+      int grid = static_cast<int>(std::min<uint64_t>(total, full ? total : persistent));
+      if (pg.max_grid > 0 && !jit) grid = std::min(grid, pg.max_grid);  // grid-stride: any grid covers every tile
       cudaError_t e = jit        ? jit_launch(jit, ptrs.data(), cnt * stride, g, sms, st)
                       : use_bulk ? c->special->launch_bulk(ptrs.data(), cnt * stride, g, grid, st, stages, smem)
                       : paged    ? c->special->launch_paged(ptrs.data(), cnt * stride, g, grid, st)
@@ -539,7 +541,8 @@ int run_codec(const gs_codec* c, int n_stripes, SlotFn slot_ptr, OutFn out_ptr, 
       if (g.dst.table) g.dst.table += (pg.stripe0 + s0) * g.dst.table_stride;
       const size_t smem = static_cast<size_t>(kb) * ns * sizeof(CoefWords);
       const int occ = blocks_per_sm(dev, generic_kernel(kb), smem);
-      const int grid = static_cast<int>(std::min<uint64_t>(total, static_cast<uint64_t>(occ) * sms));
+      int grid = static_cast<int>(std::min<uint64_t>(total, static_cast<uint64_t>(occ) * sms));
+      if (pg.max_grid > 0) grid = std::min(grid, pg.max_grid);
       const CoefWords* cw = dw + static_cast<size_t>(r0) * ns;
       cudaError_t e;
       switch (kb) {
@@ -757,6 +760,7 @@ struct gs_pipeline {
   // pipelined calls -- recorded after the slot waits, so a pair measures the
   // kernels alone, inside the caller's real schedule. Not under capture.
   bool timing = false;
+  int max_ctas = 0;              // gs_pipeline_set_max_ctas: background checkpoints (0 = whole GPU)
   std::vector<cudaEvent_t> tev;  // 2 per timed launch group
   size_t tused = 0;
   uint64_t tlaunch0 = 0;
@@ -1453,6 +1457,7 @@ static int encode_offload(gs_pipeline* p, const gs_codec* c, int n_stripes, cons
     Paging pg;
     pg.logical0 = 0;
     pg.total_len = len;
+    pg.max_grid = p->max_ctas;
     if (src_map) {
       pg.src = to_map(src_map);
       pg.paged_slots = N >= 32 ? ~0u : (1u << N) - 1;
@@ -1492,6 +1497,7 @@ static int encode_offload(gs_pipeline* p, const gs_codec* c, int n_stripes, cons
       pg.logical0 = r0;
       pg.total_len = len;
       pg.stripe0 = static_cast<uint64_t>(s0);
+      pg.max_grid = p->max_ctas;
       if (src_map) {
         pg.src = to_map(src_map);
         pg.paged_slots = N >= 32 ? ~0u : (1u << N) - 1;
@@ -1642,6 +1648,12 @@ std::map<std::tuple<int, int, int, std::vector<int>>, gs_codec*> g_dec_cache;
 }  // namespace
 
 int gs_codec_create(int kind, int n, int k, gs_codec** out) { return gs_encoder_create(kind, n, k, out); }
+
+int gs_pipeline_set_max_ctas(gs_pipeline* p, int max_ctas) {
+  if (!p || max_ctas < 0) return fail(GS_INVALID_ARGUMENT, "pipeline_set_max_ctas: bad arguments");
+  p->max_ctas = max_ctas;
+  return GS_OK;
+}
 
 int gs_pipeline_device(gs_pipeline* p, int* device) {
   if (!p || !device) return fail(GS_INVALID_ARGUMENT, "pipeline_device: NULL argument");
