@@ -294,19 +294,17 @@ def cpu_encode_baseline(W, target_s: float, threads: int):
 
 def ncu_traffic(W, alg_launch):
     """DRAM bytes (read + write) per K1 launch from the committed ncu capture
-    of THIS build (the capture records the sha of the library it profiled):
+    of THIS build (the capture records tools/srcsha.py of the sources it profiled):
     the capture's DRAM / algorithmic ratio applied to this run's algorithmic
     bytes per launch (the captured launch is one pipeline piece, whose size
     differs from the per-launch average)."""
     try:
-        import hashlib
         with open(os.path.join(ROOT, "profiles", f"k1_{W.key}_ncu_summary.json")) as f:
             summ = json.load(f)
-        so = os.path.join(ROOT, "paper_2605_00831_b200", "_lib", "libghostserve_b200.so")
-        with open(so, "rb") as f:
-            sha = hashlib.sha256(f.read()).hexdigest()[:16]
-        if summ.get("lib_sha256_16") != sha:
-            return None, f"committed capture is of another build ({summ.get('lib_sha256_16')} != {sha})"
+        from tools.srcsha import source_sha
+        sha = source_sha()
+        if summ.get("src_sha256_16") != sha:
+            return None, f"committed capture is of other sources ({summ.get('src_sha256_16')} != {sha})"
         ratio = summ["dram_bytes_per_launch"] / summ["algorithmic_bytes_per_launch"]
         return int(ratio * alg_launch), (f"ncu --set full of this build ({summ.get('file')}): "
                                          f"{summ['dram_bytes_per_launch']} DRAM B for "

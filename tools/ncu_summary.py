@@ -50,6 +50,7 @@ def main():
     ap.add_argument("--launch", default="")
     ap.add_argument("--note", default="")
     ap.add_argument("--lib-sha", default="", help="sha256[:16] of the libghostserve_b200.so that was profiled")
+    ap.add_argument("--src-sha", default="", help="tools/srcsha.py of the sources that were profiled")
     a = ap.parse_args()
     raw = subprocess.check_output(["ncu", "-i", a.report, "--page", "raw", "--csv"]).decode()
     rows = list(csv.reader(io.StringIO(raw)))
@@ -76,7 +77,7 @@ def main():
         caps.append(cap)
     import os
     out = {"source": a.source, "launch": a.launch, "note": a.note, "file": os.path.basename(a.report),
-           "lib_sha256_16": a.lib_sha, "captures": caps}
+           "lib_sha256_16": a.lib_sha, "src_sha256_16": a.src_sha, "captures": caps}
     if caps:
         c = caps[-1]
         out["kernel"] = c["kernel"]

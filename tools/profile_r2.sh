@@ -13,6 +13,7 @@
 set -x
 mkdir -p gpurun_out
 sha256sum paper_2605_00831_b200/_lib/libghostserve_b200.so | cut -c1-16 > gpurun_out/lib_sha.txt
+python tools/srcsha.py > gpurun_out/src_sha.txt
 B="python bench.py --steps 6 --warmup 3 --no-cpu --no-c3 --no-c4 --no-overhead"
 N="ncu --set full --import-source on --clock-control none --kernel-name-base demangled"
 timeout 900 $N -k regex:EncSpec -s 4 -c 1 -f -o gpurun_out/k1_c3_r2 $B > gpurun_out/ncu_k1_c3.log 2>&1
