@@ -80,6 +80,21 @@ WORKLOADS = {
 }
 
 
+def workload_config(W, world: int) -> dict:
+    """The `config` object, identical in both arms (ours and --impl reference)
+    for the same workload and rank count; arm-specific details go in `setup`."""
+    layers, heads, dim = W.geometry
+    data = W.stripes * N_SHARDS * W.slice * world     # whole job (weak scaling: W.stripes per GPU)
+    return {"workload": W.name, "scheme": "RS(8,2)",
+            "kv_geometry": f"{layers} layers x {heads} KV heads x {dim} dim fp16, TP=8 -> "
+                           f"{heads * dim // N_SHARDS * 2} B/token/worker",
+            "step": W.unit, "tokens_per_unit": W.tokens, "stripes_per_gpu": W.stripes,
+            "slice_bytes": W.slice, "data_bytes_per_step": data, "parity_d2h_bytes_per_step": data * K_PARITY // N_SHARDS,
+            "kv_seed": 3, "n_ranks": world,
+            "l2": f"inputs > L2: every step reads (request, chunk) KV distinct from the previous "
+                  f"{W.ring - 1} steps' ({(W.ring - 1) * data >> 20} MiB > 126 MB of L2 in between)"}
+
+
 def model_of(W):
     from paper_2605_00831_b200 import kv_layout as K
     layers, heads, dim = W.geometry
@@ -342,8 +357,11 @@ def run_reference(args):
             "scaling": "weak", "vs_baseline": None, "dtype": "u8",
             "data": "synthetic (reference make_ground_truth_slice KV stream, kv_seed 3)",
             "impl": "reference",
-            "config": {"workload": W.name, "scheme": "RS(8,2)", "slice_bytes": W.slice, "stripes_per_step": W.stripes,
-                       "host": "CPU only"},
+            "config": workload_config(W, world),
+            "setup": {"host": "CPU only (the reference codec compiled in place, oracle/_ref)",
+                      "kv": "each step's (request, chunk) KV generated before the step, untimed",
+                      "sample": f"each timed step encodes one GPU's share ({W.stripes} stripe(s)); the host's "
+                                "rate does not depend on the number of GPUs in the job"},
             "recovery_ms": rec.get("full_shard_ms"), "recovery": rec,
             "cpu_baseline": {"value": round(gbs, 4), "unit": "GB/s", "cores": threads, "kind": arm.kind,
                              "sample": sample},
@@ -766,21 +784,16 @@ def run_ours(args):
                 "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms_step, 4),
                 "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u8",
                 "data": "synthetic (reference make_ground_truth_slice KV stream, kv_seed 3, generated on GPU)",
-                "config": {"workload": W.name, "scheme": "RS(8,2)", "kv_geometry":
-                           f"{W.geometry[0]} layers x {W.geometry[1]} KV heads x {W.geometry[2]} dim fp16, TP=8 -> "
-                           f"{W.geometry[1] * W.geometry[2] // N_SHARDS * 2} B/token/worker",
-                           "step": W.unit, "tokens_per_unit": W.tokens, "stripes_per_gpu": W.stripes,
-                           "slice_bytes": SLICE, "data_bytes_per_step": data_bytes_step,
-                           "parity_d2h_bytes_per_step": d2h_step,
-                           "l2": f"inputs > L2: steps rotate over {RING} distinct steps' KV "
-                                 f"({RING * data_bytes_step // world >> 20} MiB per GPU)",
-                           "host_placement": ("pinned buffers and host threads on the GPU's NUMA node (CPUs "
-                                              f"{numa_cpus})" if numa_cpus else "single NUMA node host"),
-                           "parallelism": (f"byte-range striping x{world} (peer loads over NVLink)"
-                                           if args.encoder == "stripe" else
-                                           f"rotating whole-stripe encoder x{world} (paper's temporal "
-                                           "balancing; peer loads over NVLink)") if world > 1 else
-                           "single GPU holds all 8 TP shards"},
+                "config": workload_config(W, world),
+                "setup": {"l2": f"steps rotate over {RING} distinct steps' KV resident in HBM "
+                                f"({RING * data_bytes_step // world >> 20} MiB per GPU)",
+                          "host_placement": ("pinned buffers and host threads on the GPU's NUMA node (CPUs "
+                                             f"{numa_cpus})" if numa_cpus else "single NUMA node host"),
+                          "parallelism": (f"byte-range striping x{world} (peer loads over NVLink)"
+                                          if args.encoder == "stripe" else
+                                          f"rotating whole-stripe encoder x{world} (paper's temporal "
+                                          "balancing; peer loads over NVLink)") if world > 1 else
+                          "single GPU holds all 8 TP shards"},
                 "recovery_ms": recovery_ms,
                 "roofline": kern or None, "roofline_k2": kern2 or None, "step_roofline": step_roofline,
                 "host_link": host_link, "cpu_baseline": cpu, "e2e": e2e,

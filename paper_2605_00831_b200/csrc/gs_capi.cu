@@ -166,6 +166,11 @@ const bool g_page_major = [] {
   const char* e = std::getenv("GS_PAGE_MAJOR");
   return !(e && std::atoi(e) == 0);
 }();
+// Paged K1 page-per-tile addressing (GS_TILE_PAGES=0: the general paged walk, for A/B).
+const bool g_tile_pages = [] {
+  const char* e = std::getenv("GS_TILE_PAGES");
+  return !(e && std::atoi(e) == 0);
+}();
 // RDP whole-dstripe body on the pipelined kernels (GS_RDP_FAST=0: tile kernels only, for A/B).
 const bool g_rdp_fast = [] {
   const char* e = std::getenv("GS_RDP_FAST");
@@ -486,6 +491,12 @@ int run_codec(const gs_codec* c, int n_stripes, SlotFn slot_ptr, OutFn out_ptr, 
       if (paged && !jit && !use_bulk && g_page_major) {  // page-major walk (gs_kernels.cuh TileGeom)
         g.nstripes = static_cast<uint32_t>(cnt);
         g.nstripes_m = fastdiv_magic(g.nstripes);
+        uint32_t used = 0;
+        for (int j : c->used) used |= 1u << j;
+        g.tile_pages = g_tile_pages && (pg.paged_slots & used) == used && !pg.src.table && pg.dst.page_bytes == 0 &&
+                       pg.src.page_bytes % kTile == 0 && pg.logical0 % kTile == 0 &&
+                       static_cast<uint64_t>(pg.src.valid_tokens) * pg.src.token_bytes == pg.src.page_bytes &&
+                       pg.logical0 + body <= 0xFFFFFFFFull;
       }
       if (g.src.table) g.src.table += (pg.stripe0 + s0) * g.src.table_stride;
       if (g.dst.table) g.dst.table += (pg.stripe0 + s0) * g.dst.table_stride;

@@ -179,6 +179,13 @@ struct TileGeom {
   // of 64 pages 2 MiB apart. 0 = stripe-major (contiguous slices).
   uint32_t nstripes;
   uint64_t nstripes_m;  // fastdiv_magic(nstripes)
+  // Page-per-tile source mapping (set by the host for paged K1 when every
+  // used source is a paged cache without a block table, pages are whole
+  // multiples of a tile, every token is valid, logical0 is tile-aligned and
+  // the outputs are contiguous -- the single-block decode-block checkpoint):
+  // a tile is one piece of one page, so its cache offset comes from the tile
+  // index alone, with no per-thread page arithmetic or masking.
+  uint32_t tile_pages;
 };
 
 __device__ __forceinline__ unsigned long long globaltimer_ns() {
@@ -343,6 +350,19 @@ __global__ void __launch_bounds__(kThreads) k_apply_special(const PtrTable<CAP> 
 #pragma unroll
       for (int j = 0; j < Spec::NS; ++j)
         src[j] = column_used<Spec>(j) ? ld_stream(tab.p[base + j] + off) : make_uint4(0, 0, 0, 0);
+      horner_apply<Spec>(src, out);
+#pragma unroll
+      for (int i = 0; i < Spec::NO; ++i) st_stream(const_cast<uint8_t*>(tab.p[base + g.out0 + i]) + off, out[i]);
+    } else if (g.tile_pages) {
+      const uint32_t u = static_cast<uint32_t>(g.logical0) + tin * static_cast<uint32_t>(kTile);
+      const uint32_t pg = fdiv(u, g.src.page_bytes, g.src.page_m);
+      const uint32_t kv = fdiv(pg, g.src.layers, g.src.layers_m);
+      const uint64_t soff = static_cast<uint64_t>(pg - kv * g.src.layers) * g.src.layer_stride +
+                            static_cast<uint64_t>(kv) * g.src.kv_stride + (u - pg * g.src.page_bytes) +
+                            threadIdx.x * kVec;
+#pragma unroll
+      for (int j = 0; j < Spec::NS; ++j)
+        src[j] = column_used<Spec>(j) ? ld_stream(tab.p[base + j] + soff) : make_uint4(0, 0, 0, 0);
       horner_apply<Spec>(src, out);
 #pragma unroll
       for (int i = 0; i < Spec::NO; ++i) st_stream(const_cast<uint8_t*>(tab.p[base + g.out0 + i]) + off, out[i]);

@@ -204,3 +204,27 @@ def test_paged_fuzz_geometries():
             for s in range(S):
                 assert torch.equal(reps[w].read_chunk(perm[s], chunk, valid), truth[s][w]), ctx + (w, s)
         pipe.close()
+
+
+@pytest.mark.parametrize("model,staging", [
+    (ModelConfig(32, 8, 128, 2, 8), 16 << 10),    # 4 KiB pages, pieces of 16 KiB: logical0 > 0
+    (ModelConfig(4, 16, 128, 2, 8), 64 << 10),    # 8 KiB pages (two tiles per page)
+    (ModelConfig(3, 8, 128, 2, 8), 1 << 20),      # whole slice in one piece
+])
+def test_paged_tile_pages_path_pipelined(model, staging):
+    """The page-per-tile paged K1 (single-block chunks, every token valid,
+    pages a whole number of 4 KiB tiles: gs_kernels.cuh TileGeom.tile_pages)
+    through the pipelined decode-block checkpoint, whose pieces start at
+    logical offsets > 0: parity bit-exact vs the oracle."""
+    n, k, S = 8, 2, 7
+    caches, tables, truth = build(model, n, S, 16, 16, nblocks=48, seed=5)
+    scheme = CodingScheme.reed_solomon(n, k)
+    pipe = D.Pipeline(0, staging)
+    h_par = torch.zeros((S, k, caches[0].slice_bytes), dtype=torch.uint8).pin_memory()
+    st = torch.cuda.current_stream()
+    checkpoint_blocks(pipe, scheme, caches, tables, 16, h_par, st, st)
+    st.synchronize()
+    for s in range(S):
+        want = O.port().encode(O.RS, n, k, [t.cpu().numpy() for t in truth[s]])
+        for i in range(k):
+            assert np.array_equal(h_par[s, i].numpy(), want[i]), (s, i)

@@ -97,6 +97,182 @@ __global__ void __launch_bounds__(kThreads) k_copy(const uint4* __restrict__ a, 
     st_stream(reinterpret_cast<uint8_t*>(b + i), ld_stream(reinterpret_cast<const uint8_t*>(a + i)));
 }
 
+// Shipped walk with load hints: HINT bit0 = L2::256B sector promotion on the
+// streaming loads; bit1 = L2 prefetch of the CTA's next tile (one 128-B line
+// per thread: 8 sources x 4 KiB = 256 lines) before this tile's loads.
+__device__ __forceinline__ uint4 ld_stream256(const uint8_t* p) {
+  uint4 r;
+  asm volatile("ld.global.nc.L1::no_allocate.L2::256B.v4.u32 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
+               : "l"(p));
+  return r;
+}
+__device__ __forceinline__ void prefetch_l2(const uint8_t* p) {
+  asm volatile("prefetch.global.L2::evict_last [%0];" ::"l"(p));
+}
+template <int HINT>
+__global__ void __launch_bounds__(kThreads) k_hint(const PtrTable<kPtrCap> tab, const TileGeom g) {
+  stamp_start(g);
+  for (uint32_t t = blockIdx.x; t < g.total; t += gridDim.x) {
+    if (HINT & 2) {
+      const uint32_t tn = t + gridDim.x;
+      if (tn < g.total) {
+        const uint32_t sn = tile_stripe(tn, g);
+        const uint64_t offn = static_cast<uint64_t>(tn - sn * g.tps) * kTile + (threadIdx.x & 31) * 128;
+        prefetch_l2(tab.p[sn * g.stride + (threadIdx.x >> 5)] + offn);
+      }
+    }
+    const uint32_t s = tile_stripe(t, g);
+    const uint32_t tin = t - s * g.tps;
+    const uint64_t off = static_cast<uint64_t>(tin) * kTile + threadIdx.x * kVec;
+    const int base = static_cast<int>(s) * g.stride;
+    uint4 src[8], out[2];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) src[j] = (HINT & 1) ? ld_stream256(tab.p[base + j] + off) : ld_stream(tab.p[base + j] + off);
+    horner_apply<Spec>(src, out);
+#pragma unroll
+    for (int i = 0; i < 2; ++i) st_stream(const_cast<uint8_t*>(tab.p[base + g.out0 + i]) + off, out[i]);
+  }
+  stamp_end(g);
+}
+
+// Bulk (TMA) prefetch of the CTA's next tile into L2 by one thread per source.
+__global__ void __launch_bounds__(kThreads) k_bulkpf(const PtrTable<kPtrCap> tab, const TileGeom g) {
+  stamp_start(g);
+  for (uint32_t t = blockIdx.x; t < g.total; t += gridDim.x) {
+    const uint32_t tn = t + gridDim.x;
+    if (tn < g.total && threadIdx.x < 8) {
+      const uint32_t sn = tile_stripe(tn, g);
+      const uint64_t offn = static_cast<uint64_t>(tn - sn * g.tps) * kTile;
+      asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(tab.p[sn * g.stride + threadIdx.x] + offn),
+                   "r"(kTile));
+    }
+    const uint32_t s = tile_stripe(t, g);
+    const uint64_t off = static_cast<uint64_t>(t - s * g.tps) * kTile + threadIdx.x * kVec;
+    const int base = static_cast<int>(s) * g.stride;
+    uint4 src[8], out[2];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) src[j] = ld_stream(tab.p[base + j] + off);
+    horner_apply<Spec>(src, out);
+#pragma unroll
+    for (int i = 0; i < 2; ++i) st_stream(const_cast<uint8_t*>(tab.p[base + g.out0 + i]) + off, out[i]);
+  }
+  stamp_end(g);
+}
+
+// Paged C2 (one 16-token block per slice, tile == page): the page's cache
+// offset from the tile index alone -- s = t % S (page-major), q = t / S,
+// kv = q / layers, l = q % layers -- with no per-thread page arithmetic.
+__global__ void __launch_bounds__(kThreads) k_paged_page(const PtrTable<kPtrCap> tab, const TileGeom g) {
+  stamp_start(g);
+  for (uint32_t t = blockIdx.x; t < g.total; t += gridDim.x) {
+    const uint32_t q = fdiv(t, g.nstripes, g.nstripes_m);
+    const uint32_t s = t - q * g.nstripes;
+    const uint32_t kv = fdiv(q, g.src.layers, g.src.layers_m);
+    const uint32_t l = q - kv * g.src.layers;
+    const uint64_t soff = kv * g.src.kv_stride + l * g.src.layer_stride + threadIdx.x * kVec;
+    const uint64_t doff = static_cast<uint64_t>(q) * kTile + threadIdx.x * kVec;
+    const int base = static_cast<int>(s) * g.stride;
+    uint4 src[8], out[2];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) src[j] = ld_stream(tab.p[base + j] + soff);
+    horner_apply<Spec>(src, out);
+#pragma unroll
+    for (int i = 0; i < 2; ++i) st_stream(const_cast<uint8_t*>(tab.p[base + g.out0 + i]) + doff, out[i]);
+  }
+  stamp_end(g);
+}
+
+static void paged_section(int sms, cudaStream_t st, cudaEvent_t e0, cudaEvent_t e1, unsigned long long* ts) {
+  // 8 worker caches [layers=32][2][blocks][16 tok][256 B]; ring of 8 steps x 32 stripes = 256 blocks
+  const int layers = 32, S = 32, sets = 8, blocks = S * sets;
+  const uint64_t page = 16 * 256, plane = blocks * page, cache = 2ull * layers * plane;
+  const uint64_t slice = 2ull * layers * page;  // 256 KiB
+  std::vector<uint8_t*> caches(8);
+  for (auto& c : caches) {
+    CK(cudaMalloc(&c, cache));
+    CK(cudaMemset(c, 7, cache));
+  }
+  uint8_t* par;
+  CK(cudaMalloc(&par, static_cast<uint64_t>(sets) * S * 2 * slice));
+  PageMap pm{};
+  pm.page_bytes = page;
+  pm.layers = layers;
+  pm.token_bytes = 256;
+  pm.valid_tokens = 16;
+  pm.layer_stride = 2 * plane;
+  pm.kv_stride = plane;
+  pm.table = nullptr;
+  pm.block_bytes = page;
+  pm.page_m = fastdiv_magic(pm.page_bytes);
+  pm.layers_m = fastdiv_magic(pm.layers);
+  pm.block_m = fastdiv_magic(pm.block_bytes);
+  std::vector<PtrTable<kPtrCap>> tabs(sets);
+  for (int b = 0; b < sets; ++b)
+    for (int s = 0; s < S; ++s) {
+      for (int j = 0; j < 8; ++j) tabs[b].p[s * 10 + j] = caches[j] + static_cast<uint64_t>(b * S + s) * page;
+      for (int i = 0; i < 2; ++i) tabs[b].p[s * 10 + 8 + i] = par + (static_cast<uint64_t>(b * S + s) * 2 + i) * slice;
+    }
+  TileGeom g{};
+  g.len = slice;
+  g.tps = static_cast<uint32_t>(slice / kTile);
+  g.total = g.tps * S;
+  g.stride = 10;
+  g.out0 = 8;
+  g.aligned = 1;
+  g.tps_m = fastdiv_magic(g.tps);
+  g.paged_slots = 0xFF;
+  g.src = pm;
+  g.nstripes = S;
+  g.nstripes_m = fastdiv_magic(S);
+  const uint64_t alg = static_cast<uint64_t>(S) * 10 * slice;
+  int occ = 0;
+  CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, &k_apply_special<Spec, kPtrCap, 1, true>, kThreads, 0));
+  auto run = [&](const char* label, auto launch, TileGeom gv) {
+    for (int b = 0; b < sets; ++b) launch(tabs[b], gv);
+    CK(cudaStreamSynchronize(st));
+    const int reps = 4;
+    CK(cudaEventRecord(e0, st));
+    for (int r = 0; r < reps; ++r)
+      for (int b = 0; b < sets; ++b) launch(tabs[b], gv);
+    CK(cudaEventRecord(e1, st));
+    CK(cudaEventSynchronize(e1));
+    float ms = 0;
+    CK(cudaEventElapsedTime(&ms, e0, e1));
+    const double us_ev = ms * 1e3 / (reps * sets);
+    double span = 0;
+    for (int b = 0; b < sets; ++b) {
+      unsigned long long init[2] = {~0ull, 0ull};
+      CK(cudaMemcpyAsync(ts, init, sizeof(init), cudaMemcpyHostToDevice, st));
+      TileGeom gg = gv;
+      gg.tstamp = ts;
+      launch(tabs[b], gg);
+      unsigned long long out[2];
+      CK(cudaMemcpyAsync(out, ts, sizeof(out), cudaMemcpyDeviceToHost, st));
+      CK(cudaStreamSynchronize(st));
+      span += (out[1] - out[0]) * 1e-3;
+    }
+    span /= sets;
+    std::printf("{\"geo\": \"C2 paged 16-tok blocks\", \"variant\": \"%s\", \"us_event\": %.2f, \"tbs_event\": %.3f, "
+                "\"us_span\": %.2f, \"tbs_span\": %.3f}\n",
+                label, us_ev, alg / us_ev * 1e-6, span, alg / span * 1e-6);
+    std::fflush(stdout);
+  };
+  const int grid = std::min<int>(g.total, occ * sms);
+  run("shipped paged page-major", [&](const PtrTable<kPtrCap>& t, const TileGeom& gg) {
+    k_apply_special<Spec, kPtrCap, 1, true><<<grid, kThreads, 0, st>>>(t, gg); }, g);
+  TileGeom gs = g;
+  gs.nstripes = 0;
+  run("shipped paged stripe-major", [&](const PtrTable<kPtrCap>& t, const TileGeom& gg) {
+    k_apply_special<Spec, kPtrCap, 1, true><<<grid, kThreads, 0, st>>>(t, gg); }, gs);
+  run("page-per-tile kernel", [&](const PtrTable<kPtrCap>& t, const TileGeom& gg) {
+    k_paged_page<<<grid, kThreads, 0, st>>>(t, gg); }, g);
+  run("shipped paged page-major full grid", [&](const PtrTable<kPtrCap>& t, const TileGeom& gg) {
+    k_apply_special<Spec, kPtrCap, 1, true><<<g.total, kThreads, 0, st>>>(t, gg); }, g);
+  for (auto c : caches) CK(cudaFree(c));
+  CK(cudaFree(par));
+}
+
 struct Geo {
   const char* name;
   int stripes;
@@ -117,6 +293,10 @@ int main(int argc, char** argv) {
   cudaEvent_t e0, e1;
   CK(cudaEventCreate(&e0));
   CK(cudaEventCreate(&e1));
+  if (getenv("PAGED_ONLY")) {
+    paged_section(sms, st, e0, e1, ts);
+    return 0;
+  }
   for (const Geo& G : geos) {
     const uint64_t alg = static_cast<uint64_t>(G.stripes) * 10 * G.len;  // 8 read + 2 written
     std::vector<PtrTable<kPtrCap>> tabs(sets);
@@ -181,6 +361,14 @@ int main(int argc, char** argv) {
     run("one CTA per tile", [&](const PtrTable<kPtrCap>& t, const TileGeom& gg) {
       k_apply_special<Spec, kPtrCap, 1, false><<<g.total, kThreads, 0, st>>>(t, gg);
     });
+    const int oh = occ(reinterpret_cast<const void*>(&k_hint<3>));
+    run("hint L2::256B", [&](const PtrTable<kPtrCap>& t, const TileGeom& gg) { k_hint<1><<<std::min<uint32_t>(g.total, oh * sms), kThreads, 0, st>>>(t, gg); });
+    run("hint prefetch next tile", [&](const PtrTable<kPtrCap>& t, const TileGeom& gg) { k_hint<2><<<std::min<uint32_t>(g.total, oh * sms), kThreads, 0, st>>>(t, gg); });
+    run("hint both", [&](const PtrTable<kPtrCap>& t, const TileGeom& gg) { k_hint<3><<<std::min<uint32_t>(g.total, oh * sms), kThreads, 0, st>>>(t, gg); });
+    run("hint both grid/2", [&](const PtrTable<kPtrCap>& t, const TileGeom& gg) { k_hint<3><<<std::min<uint32_t>(g.total, oh * sms / 2), kThreads, 0, st>>>(t, gg); });
+    run("bulk L2 prefetch next tile", [&](const PtrTable<kPtrCap>& t, const TileGeom& gg) { k_bulkpf<<<std::min<uint32_t>(g.total, oh * sms), kThreads, 0, st>>>(t, gg); });
+    run("bulk L2 prefetch grid/2", [&](const PtrTable<kPtrCap>& t, const TileGeom& gg) { k_bulkpf<<<std::min<uint32_t>(g.total, oh * sms / 2), kThreads, 0, st>>>(t, gg); });
+    if (getenv("SKIP_BAL")) { for (auto b : bufs) CK(cudaFree(b)); continue; }
     const int o4 = occ(reinterpret_cast<const void*>(&k_bal<4>));
     const int o6 = occ(reinterpret_cast<const void*>(&k_bal<6>));
     const int o8 = occ(reinterpret_cast<const void*>(&k_bal<8>));
