@@ -301,6 +301,13 @@ int gs_pad_partial_device(void* d_slice, int layers, int kv_heads, int head_dim,
 
 /* ---- parity seal (parity_store.hpp:19-53), host ------------------------ */
 uint64_t gs_fnv1a64(const void* bytes, size_t len, uint64_t h);
+/* 1 when the host FNV-1a (gs_fnv1a64, the checksums, the store's seal and the
+ * recovery verification) runs the bit-sliced AVX-512 chain of gs_fnv_simd.cpp
+ * (~6 GB/s per chain and core), 0 when it runs the scalar chain. */
+int gs_fnv_host_simd(void);
+/* Switch the bit-sliced chain off (0) or back on (1, when the CPU has it) for
+ * A/B runs; returns gs_fnv_host_simd() afterwards. */
+int gs_fnv_host_set_simd(int on);
 /* ParityChunk::compute_checksum: FNV-1a chained over k buffers in order */
 uint64_t gs_parity_checksum(const void* const* parity, int k, size_t len);
 /* Seal many chunks concurrently on up to `threads` host threads:

@@ -77,6 +77,8 @@ SIGNATURES = {
     "gs_pad_partial_device": (_i, [_vp, _i, _i, _i, _i, _u32, _u32, _vp]),
     "gs_fnv1a64": (_u64, [_vp, _sz, _u64]),
     "gs_parity_checksum": (_u64, [_vpp, _i, _sz]),
+    "gs_fnv_host_simd": (_i, []),
+    "gs_fnv_host_set_simd": (_i, [_i]),
     "gs_parity_checksum_batch": (_i, [_vpp, _i, _i, _sz, _i, _u64p]),
     "gs_fnv1a64_device": (_i, [_vpp, _i, _i, _u64, _u64, _vp, _vp]),
     "gs_parity_upload_checksum": (_i, [_vpp, _i, _i, _u64, _vpp, _vp, _vp, _vp]),

@@ -322,11 +322,16 @@ class Checkpointer:
         self.verify = torch.cuda.Stream(device=self.dev)   # GPU parity checksums (recover)
         self.slice = slice_bytes(cfg.model, cfg.chunk_size)
         # Aggregate host FNV-1a rate (bytes/s) used to split recovery's parity
-        # verification between host threads and the GPU (recover()): ~1.6 GB/s
-        # per hardware thread while the parity upload streams over the same
-        # host memory (measured on the B200 hosts, bench recovery.c3_orchestrated).
-        self.host_fnv_rate = 1.6e9 * max(1, (os.cpu_count() or 1) - 2)
-        self.host_chain_rate = 0.9e9   # ONE serial FNV chain on one host thread (bytes/s)
+        # verification between host threads and the GPU (recover()), and the
+        # rate of ONE chain on one host thread. The bit-sliced AVX-512 chain
+        # (gs_fnv_simd.cpp, gs_fnv_host_simd() == 1): ~6 GB/s per chain and
+        # core, 94 GB/s on the 16 host threads of the B200 boxes
+        # (tools/fnv_host_mt.cpp); the scalar chain: ~0.9 GB/s per chain, ~1.6
+        # GB/s per thread in lockstep pairs while the parity upload streams
+        # over the same host memory.
+        simd = bool(L.lib().gs_fnv_host_simd())
+        self.host_chain_rate = 5.0e9 if simd else 0.9e9
+        self.host_fnv_rate = (5.0e9 if simd else 1.6e9) * max(1, (os.cpu_count() or 1) - 2)
         # False: verify every entry on host threads (the reference's placement)
         self.gpu_verify = True
         # "dynamic": the part of each parity chain the decode does not upload

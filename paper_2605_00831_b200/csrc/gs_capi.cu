@@ -1938,12 +1938,13 @@ int gs_pad_partial_device(void* d_slice, int layers, int kv_heads, int head_dim,
 // ============================================================================
 uint64_t gs_fnv1a64(const void* bytes, size_t len, uint64_t h) {
   const uint8_t* p = static_cast<const uint8_t*>(bytes);
-  for (size_t i = 0; i < len; ++i) {
-    h ^= p[i];
-    h *= 0x100000001b3ull;
-  }
-  return h;
+  if (len >= kFnvSimdMin && fnv_simd_available()) return fnv1a64_fast(p, len, h);
+  return fnv1a64_one(p, len, h);
 }
+
+int gs_fnv_host_simd(void) { return fnv_simd_available() ? 1 : 0; }
+
+int gs_fnv_host_set_simd(int on) { return fnv_simd_set(on != 0) ? 1 : 0; }
 
 uint64_t gs_parity_checksum(const void* const* parity, int k, size_t len) {
   uint64_t h = 0xcbf29ce484222325ull;
@@ -1960,7 +1961,9 @@ int gs_parity_checksum_batch(const void* const* parity, int n_chunks, int k, siz
   // number of chains one thread advances one after another times a chain's
   // length: give each thread ONE lockstep group of ceil(chunks / threads)
   // chains (4..8) rather than several groups of four.
-  const int per = std::max(4, std::min(8, (n_chunks + threads - 1) / std::max(threads, 1)));
+  // With the SIMD chain (several GB/s per chain) one chain per claim spreads
+  // the chunks over every thread.
+  const int per = fnv_simd_available() ? 1 : std::max(4, std::min(8, (n_chunks + threads - 1) / std::max(threads, 1)));
   const int groups = (n_chunks + per - 1) / per;
   threads = std::min(threads, std::max(1, groups));
   std::atomic<int> next{0};
@@ -1972,7 +1975,7 @@ int gs_parity_checksum_batch(const void* const* parity, int n_chunks, int k, siz
       for (int i = 0; i < k; ++i) {  // chained over the k buffers in order
         const uint8_t* ps[8];
         for (int q = 0; q < m; ++q) ps[q] = static_cast<const uint8_t*>(parity[static_cast<size_t>(c0 + q) * k + i]);
-        fnv1a64_x8(ps, m, len, h);
+        fnv1a64_chains(ps, m, len, h);
       }
       for (int q = 0; q < m; ++q) out[c0 + q] = h[q];
     }

@@ -1143,9 +1143,9 @@ static int verify_feeder(gs_verify* v) {
 static int v_claim_chains() {
   static const int n = [] {
     const char* e = std::getenv("GS_VERIFY_CLAIM");
-    return e ? std::atoi(e) : 2;
+    return e ? std::atoi(e) : 0;
   }();
-  return n;
+  return n > 0 ? n : gsb::fnv_simd_available() ? 1 : 2;  // the SIMD chain needs no lockstep partner
 }
 
 static int verify_finish_dynamic(gs_verify* v, int threads, uint64_t* sums, int* gpu_chunks) {
@@ -1198,7 +1198,7 @@ static int verify_finish_dynamic(gs_verify* v, int threads, uint64_t* sums, int*
         const uint64_t n = std::min<uint64_t>(kSlice, v->len - in);
         const uint8_t* ps[8];
         for (int q = 0; q < m; ++q) ps[q] = v->host_rows[static_cast<size_t>(c[q]) * v->k + v->u + row] + in;
-        gsb::fnv1a64_x8(ps, m, n, h);
+        gsb::fnv1a64_chains(ps, m, n, h);
         o += n;
         if (o >= total || link <= 0) continue;
         std::lock_guard<std::mutex> lk(v->mu);
@@ -1424,7 +1424,7 @@ extern "C" int gs_verify_finish_ex(gs_verify* v, int threads, uint64_t* sums, in
         for (int i = v->u; i < v->k; ++i) {
           const uint8_t* ps[8];
           for (int q = 0; q < m; ++q) ps[q] = v->host_rows[static_cast<size_t>(c0 + q) * v->k + i];
-          gsb::fnv1a64_x8(ps, m, v->len, h);
+          gsb::fnv1a64_chains(ps, m, v->len, h);
         }
         for (int q = 0; q < m; ++q) sums[c0 + q] = h[q];
       }

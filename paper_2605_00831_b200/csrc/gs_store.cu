@@ -176,7 +176,7 @@ struct gs_store {
         continue;
       }
       uint64_t h[4] = {gsb::kFnvOffset, gsb::kFnvOffset, gsb::kFnvOffset, gsb::kFnvOffset};
-      if (len) gsb::fnv1a64_x4(bufs, m, len, h);
+      if (len) gsb::fnv1a64_chains(bufs, m, len, h);
       {
         std::lock_guard<std::mutex> lk(mu);
         for (int q = 0; q < m; ++q) {

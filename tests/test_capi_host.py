@@ -261,3 +261,43 @@ def test_reference_gf256_suite_runs_against_the_library():
     out = subprocess.run([exe], capture_output=True, text=True, timeout=300)
     assert out.returncode == 0, out.stdout[-2000:] + out.stderr[-2000:]
     assert "8 tests, 0 failed" in out.stdout
+
+
+def test_host_fnv_bit_sliced_chain_matches_oracle(port):
+    """The host FNV-1a (gs_fnv1a64, the checksums, the store's seal, the
+    recovery verification) takes the bit-sliced AVX-512 chain of
+    gs_fnv_simd.cpp when the CPU has it: bit-exact vs the oracle's serial
+    chain (parity_store.hpp:19-25) at lengths around the 2 KiB super-block,
+    from arbitrary chain states, at misaligned addresses, and over adversarial
+    bytes (all-zero / all-0xFF runs keep the low-byte chain in short cycles)."""
+    lib = L.lib()
+    rng = np.random.default_rng(2026)
+    big = rng.integers(0, 256, (1 << 20) + 4096, dtype=np.uint8)
+    lens = [0, 1, 511, 2047, 2048, 2049, 4095, 4096, 6144 + 17, 65536, 65536 * 3 + 2048 + 5, 1 << 20]
+    for ln in lens:
+        for off in (0, 1, 63):
+            buf = big[off: off + ln]
+            for h0 in (0xCBF29CE484222325, int(rng.integers(0, 2**63)) * 2 + 1, 0):
+                got = lib.gs_fnv1a64(buf.ctypes.data, ln, h0)
+                assert got == port.fnv1a64(buf, h0), (ln, off, hex(h0))
+    for fill in (0x00, 0xFF, 0x80, 0x01):
+        buf = np.full(8192 + 100, fill, np.uint8)
+        buf[4000] ^= 0x5A
+        assert lib.gs_fnv1a64(buf.ctypes.data, buf.size, 0xCBF29CE484222325) == port.fnv1a64(buf)
+    # the batch form (one chain per claim when the SIMD chain is present)
+    parity = [rng.integers(0, 256, 40000, dtype=np.uint8) for _ in range(2 * 9)]
+    out = (C.c_uint64 * 9)()
+    assert lib.gs_parity_checksum_batch(L.ptr_array([p.ctypes.data for p in parity]), 9, 2, 40000, 4, out) == 0
+    for c in range(9):
+        assert out[c] == port.parity_checksum(parity[2 * c: 2 * c + 2])
+    assert lib.gs_fnv_host_simd() in (0, 1)
+    # the scalar chain (gs_fnv_host_set_simd(0), the A/B switch) gives the same sums
+    buf = big[3: 3 + 70000]
+    want = port.fnv1a64(buf)
+    hw = lib.gs_fnv_host_simd()
+    try:
+        assert lib.gs_fnv_host_set_simd(0) == 0
+        assert lib.gs_fnv1a64(buf.ctypes.data, buf.size, 0xCBF29CE484222325) == want
+    finally:
+        assert lib.gs_fnv_host_set_simd(1) == hw
+    assert lib.gs_fnv1a64(buf.ctypes.data, buf.size, 0xCBF29CE484222325) == want

@@ -253,7 +253,13 @@ def test_dynamic_split_verification(u, threads, rates, ln):
     out = (C.c_uint64 * n)()
     gpu = C.c_int(-1)
     handoffs0 = lib.gs_verify_handoffs()
-    assert lib.gs_verify_finish_ex(h, threads, out, C.byref(gpu)) == 0, lib.gs_last_error()
+    # the hand-off safety net needs a host slower than the link: the scalar chain
+    simd = lib.gs_fnv_host_set_simd(0 if rates == (1000.0, 1000.0) else 1)
+    try:
+        assert lib.gs_verify_finish_ex(h, threads, out, C.byref(gpu)) == 0, lib.gs_last_error()
+    finally:
+        lib.gs_fnv_host_set_simd(1)
+    assert simd == 0 or rates != (1000.0, 1000.0)
     torch.cuda.synchronize()
     assert 0 <= gpu.value <= n and (u < k or gpu.value == n)
     if rates == (1000.0, 1000.0):
