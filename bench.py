@@ -945,7 +945,7 @@ def host_tier_checkpoint(torch, dev, W, scheme, pipe, comp, copy, args):
                 K.make_ground_truth_slice(KV_SEED, s, b, j, cfg, BLOCK_TOKENS, BLOCK_TOKENS, out=ring[b, s, j])
     torch.cuda.synchronize()
     # leave two cores for the CUDA callback thread and the submitting thread
-    threads = max(1, (os.cpu_count() or 1) - 2)
+    threads = int(os.environ.get("GS_VERIFY_THREADS", 0)) or max(1, (os.cpu_count() or 1) - 2)
     store = ParityStore(seal_threads=threads)
     store.bind_device(dev.index or 0)   # slabs on the GPU's NUMA node
     enc = encoder(scheme)
@@ -1313,10 +1313,12 @@ def c3_orchestrated(torch, dev, link, k1_gbs, k2_gbs):
         return {"c3_orchestrated_skipped": "not enough device memory"}
     cost = CostModel.measured(link["h2d"], k1_gbs, k2_gbs)
     cfg = CheckpointConfig(CodingScheme.reed_solomon(8, 2), m, cfg_m, cost)
-    threads = max(1, (os.cpu_count() or 1) - 2)
+    threads = int(os.environ.get("GS_VERIFY_THREADS", 0)) or max(1, (os.cpu_count() or 1) - 2)
     store = ParityStore(seal_threads=threads)
     store.bind_device(dev.index or 0)
     ck = Checkpointer(cfg, store, device=dev.index or 0)
+    if os.environ.get("GS_VERIFY_SPLIT"):          # A/B of the verification split (tools/c3_probe.py)
+        ck.verify_split = os.environ["GS_VERIFY_SPLIT"]
     # warm pass: the host tier's pinned slabs (10 GiB here) and the device
     # blocks of the 512 KV slices are allocated once and then recycled (store
     # free lists, torch caching allocator), as in a serving process

@@ -1407,7 +1407,11 @@ extern "C" int gs_verify_finish_ex(gs_verify* v, int threads, uint64_t* sums, in
   if (v->n > 0 && !sums) st = ffail(GS_INVALID_ARGUMENT, "verify_finish: NULL output");
   const int ns = v->n - v->n_full;
   if (st == GS_OK && ns > 0) {
-    const int per = std::max(1, std::min(8, (ns + std::max(threads, 1) - 1) / std::max(threads, 1)));
+    // one chain per claim with the SIMD chain (claims follow the upload order,
+    // so a thread never waits on a late chunk while earlier ones are ready)
+    const int per = gsb::fnv_simd_available()
+                        ? 1
+                        : std::max(1, std::min(8, (ns + std::max(threads, 1) - 1) / std::max(threads, 1)));
     const int groups = (ns + per - 1) / per;
     std::atomic<int> next{0};
     std::atomic<int> err{0};
