@@ -76,6 +76,12 @@ bool fnv_simd_available();          // hardware support and not switched off
 bool fnv_simd_set(bool on);         // gs_fnv_host_set_simd (A/B, tests); returns the new state
 uint64_t fnv1a64_fast(const uint8_t* p, size_t len, uint64_t h);
 constexpr size_t kFnvSimdMin = 2048;  // shorter runs stay scalar
+// Split form (bit-sliced when available, scalar otherwise): for any state h
+// whose low byte is l, FNV-1a over p[0..len) from h ends in
+// h * fnv_pow(len) + fnv_partial(p, len, l, &l_out), with low byte l_out --
+// the upper 56 bits of h enter only through the final multiply-add.
+uint64_t fnv_pow(uint64_t n);
+uint64_t fnv_partial(const uint8_t* p, size_t len, uint32_t l, uint32_t* l_out);
 
 // h[q] = FNV-1a of p[q][0..len) continued from h[q], for q < m (m <= 8).
 inline void fnv1a64_chains(const uint8_t* const* p, int m, size_t len, uint64_t* h) {

@@ -297,13 +297,17 @@ GS_SIMD_TARGET inline uint64_t reduce_limbs(__m512i (&a)[4]) {
   return t;
 }
 
-GS_SIMD_TARGET static uint64_t fnv_simd_impl(const uint8_t* p, size_t len, uint64_t h) {
+namespace {
+
+// The 2 KiB super-blocks of p[0 .. nsup * kSuper): advances the low byte `l`
+// and returns S = sum_i d_i P^(len-i) over them (a state h with low byte l
+// becomes h * P^(nsup * kSuper) + S).
+GS_SIMD_TARGET static uint64_t simd_blocks(const uint8_t* p, size_t nsup, uint32_t& l) {
   const Tables& tb = tables();
   const Consts k = make_consts();
   __m512i bits[8];  // entry bit j of the next block, broadcast
-  for (int j = 0; j < 8; ++j) bits[j] = _mm512_set1_epi64(((h >> j) & 1u) ? -1 : 0);
-  uint64_t acc = 0, pn = 1;
-  const size_t nsup = len / kSuper;
+  for (int j = 0; j < 8; ++j) bits[j] = _mm512_set1_epi64(((l >> j) & 1u) ? -1 : 0);
+  uint64_t acc = 0;
   __m512i a[4];
   for (int m = 0; m < 4; ++m) a[m] = _mm512_setzero_si512();
   BlockChain c0, c1;
@@ -320,16 +324,43 @@ GS_SIMD_TARGET static uint64_t fnv_simd_impl(const uint8_t* p, size_t len, uint6
       dot_block(pb + kBlock, c1.U, blk + 1, tb, k, a);
     }
     acc = acc * tb.p_super + reduce_limbs(a);
-    pn *= tb.p_super;
   }
-  h = h * pn + acc;
-  const size_t i = nsup * kSuper;
-  return fnv1a64_one(p + i, len - i, h);
+  l = 0;
+  for (int j = 0; j < 8; ++j) l |= static_cast<uint32_t>(_mm_cvtsi128_si32(_mm512_castsi512_si128(bits[j])) & 1) << j;
+  return acc;
+}
+
+inline uint32_t low_step(uint32_t l, uint8_t b) { return ((l ^ b) * 0xB3u) & 0xFFu; }
+
+}  // namespace
+
+uint64_t fnv_pow(uint64_t n) {
+  uint64_t r = 1, x = kFnvPrime;
+  for (; n; n >>= 1, x *= x)
+    if (n & 1) r *= x;
+  return r;
+}
+
+uint64_t fnv_partial(const uint8_t* p, size_t len, uint32_t l, uint32_t* l_out) {
+  uint64_t sum = 0;
+  size_t i = 0;
+  if (len >= kSuper && fnv_simd_available()) {
+    const size_t nsup = len / kSuper;
+    sum = simd_blocks(p, nsup, l);
+    i = nsup * kSuper;
+  }
+  for (; i < len; ++i) {  // h' = (h + d) P with d = (l ^ b) - l
+    const int64_t d = static_cast<int64_t>(l ^ p[i]) - static_cast<int64_t>(l);
+    sum = (sum + static_cast<uint64_t>(d)) * kFnvPrime;
+    l = low_step(l, p[i]);
+  }
+  if (l_out) *l_out = l;
+  return sum;
 }
 
 uint64_t fnv1a64_fast(const uint8_t* p, size_t len, uint64_t h) {
   if (len < kSuper || !fnv_simd_available()) return fnv1a64_one(p, len, h);
-  return fnv_simd_impl(p, len, h);
+  return h * fnv_pow(len) + fnv_partial(p, len, static_cast<uint32_t>(h & 0xFF), nullptr);
 }
 
 }  // namespace gsb
