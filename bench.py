@@ -760,12 +760,19 @@ def run_ours(args):
             recovery["c3_orchestrated"] = orch
             if "plan" in orch:
                 recovery_ms = orch["recover_wall_ms"]
+                recovery["recovery_ms_is"] = ("C3 full-shard recovery with the reference's semantics: plan, every "
+                                              "parity entry FNV-verified, H2D + K2, 64 chunks bit-exact "
+                                              "(recovery.c3_orchestrated, median of 3)")
                 if orch["plan"]["mode"] != "hybrid" or orch["decoded_chunks"] != orch["chunks"] or not orch["verified"]:
                     failures.append(f"C3 recovery did not decode every chunk bit-exact: {orch['plan']} "
                                     f"decoded {orch['decoded_chunks']} verified {orch['verified']}")
     if world > 1 and not args.no_c3:
         recovery.update(c3_recovery_striped(torch, dist, dev, comp, copy, pipe, rank, world, shared, barrier))
         recovery_ms = recovery.get("c3_full_shard_ms")
+        recovery["recovery_ms_is"] = ("C3 full-shard rebuild striped over the ranks (parity H2D on every host "
+                                      "link, survivors over NVLink, P2P store), WITHOUT the FNV verification: "
+                                      "a chunk's checksum is one chain over its whole parity, which the ranks' "
+                                      "byte ranges cannot split; verified recovery runs at N=1")
         if not recovery.get("c3_rebuild_ok", True):
             failures.append("striped C3 rebuild != original shard")
     if rank == 0 and world == 1 and not args.no_c4:
