@@ -1161,8 +1161,8 @@ def decode_overhead(torch, dev, pipe, args):
         torch.amax(kvc, dim=0, out=sink[1])
 
     def measure(max_ctas, main_prio):
-        """(base block ms, block ms with the checkpoint, checkpoint alone ms)
-        for one placement policy; base / with runs alternate (min of 4 each)."""
+        """(base block ms, block ms with the checkpoint, checkpoint alone ms,
+        base IQR per block) for one placement policy."""
         check(L.lib().gs_pipeline_set_max_ctas(bpipe.handle, max_ctas), "max ctas")
         main = torch.cuda.Stream(device=dev, priority=main_prio)
         side, side_copy = torch.cuda.Stream(device=dev), torch.cuda.Stream(device=dev)
@@ -1188,26 +1188,38 @@ def decode_overhead(torch, dev, pipe, args):
 
         run(1, True)
         run(1, False)
-        blocks = 4
-        base, withc = [], []
-        for _ in range(4):
-            base.append(run(blocks, False))
-            withc.append(run(blocks, True))
+        # Paired runs, order alternating, median of the paired differences:
+        # the decode GEMMs' clock drifts by ~1% between runs (power), which is
+        # larger than the effect, so unpaired minima would measure the drift.
+        blocks, pairs = 2, 10
+        base, diff = [], []
+        for i in range(pairs):
+            if i % 2:
+                w_ = run(blocks, True)
+                b_ = run(blocks, False)
+            else:
+                b_ = run(blocks, False)
+                w_ = run(blocks, True)
+            base.append(b_)
+            diff.append(w_ - b_)
         a0, a1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         a0.record(side)
         ckpt()
         side.wait_stream(side_copy)
         a1.record(side)
         a1.synchronize()
-        return min(base) / blocks, min(withc) / blocks, a0.elapsed_time(a1)
+        base.sort()
+        b_med = statistics.median(base) / blocks
+        noise = (base[3 * pairs // 4] - base[pairs // 4]) / blocks   # interquartile range of the base runs
+        return b_med, b_med + statistics.median(diff) / blocks, a0.elapsed_time(a1), noise
 
     policies = {}
     for name, cap, prio in (("whole_gpu", 0, 0), ("decode_high_priority", 0, -1),
                             ("background_16_ctas", 16, -1), ("background_4_ctas", 4, -1)):
-        b_ms, w_ms, alone = measure(cap, prio)
+        b_ms, w_ms, alone, noise = measure(cap, prio)
         policies[name] = {"max_ctas": cap, "decode_stream_priority": "high" if prio < 0 else "default",
                           "block_ms_without_ckpt": round(b_ms, 4), "block_ms_with_ckpt": round(w_ms, 4),
-                          "checkpoint_alone_ms": round(alone, 4),
+                          "checkpoint_alone_ms": round(alone, 4), "base_iqr_ms_per_block": round(noise, 4),
                           "overhead_pct_of_block": round((w_ms - b_ms) / b_ms * 100, 3),
                           "overhead_pct_of_decode_step": round((w_ms - b_ms) / (b_ms / 16) * 100, 3)}
     # the serving policy (declared, not picked after the fact): decode on a
