@@ -986,17 +986,18 @@ def host_tier_checkpoint(torch, dev, W, scheme, pipe, comp, copy, args):
     ok = all(int(store.get(s, blocks - 1)[0]) == 0 for s in range(min(S, 4)))
     data = blocks * S * N_SHARDS * SLICE
     parity = blocks * S * K_PARITY * SLICE
-    # raw seal rate of the same parity on all cores (no GPU in the loop)
-    h = C.c_void_p()
+    # raw seal rate of the same parity (every block's entries, one batch) on
+    # the seal threads, no GPU in the loop
     views = []
-    for s in range(S):
-        st_, ch = store.get(s, blocks - 1, verify=False)
-        views.extend(ch.parity)
+    for b in range(blocks):
+        for s in range(S):
+            st_, ch = store.get(s, b, verify=False)
+            views.extend(ch.parity)
     ptrs = L.ptr_array([v.ctypes.data for v in views])
-    outs = (C.c_uint64 * S)()
+    outs = (C.c_uint64 * (S * blocks))()
     t1 = time.perf_counter()
-    check(L.lib().gs_parity_checksum_batch(ptrs, S, K_PARITY, SLICE, threads, outs), "seal")
-    seal_raw = S * K_PARITY * SLICE / (time.perf_counter() - t1) / 1e9
+    check(L.lib().gs_parity_checksum_batch(ptrs, S * blocks, K_PARITY, SLICE, threads, outs), "seal")
+    seal_raw = S * blocks * K_PARITY * SLICE / (time.perf_counter() - t1) / 1e9
     out = {"blocks": blocks, "seal_threads": threads, "seal_only_parity_gbs": round(seal_raw, 2),
            "checkpoint_gbs_until_d2h_done": round(data / t_gpu / 1e9, 2),
            "checkpoint_gbs_sealed": round(data / t_all / 1e9, 2),

@@ -140,21 +140,23 @@ struct gs_store {
   bool stop = false;
   std::atomic<uint64_t> pending{0};
 
-  // Seal workers take up to four pending entries of equal size at a time and
-  // hash them in lockstep (gs_fnv.hpp): FNV-1a chained over the k buffers in
+  // Seal workers hash pending entries: FNV-1a chained over the k buffers in
   // order == FNV over the entry's contiguous k * slice_len bytes
-  // (parity_store.hpp:46-50).
+  // (parity_store.hpp:46-50). With the bit-sliced chain a worker takes ONE
+  // entry at a time (the workers share a block's entries); the scalar chain
+  // takes up to four of equal size and hashes them in lockstep (gs_fnv.hpp).
   void worker() {
     for (;;) {
       Key keys[4];
       const uint8_t* bufs[4];
       uint64_t len = 0;
       int m = 0, dropped = 0;
+      const int claim = gsb::fnv_simd_available() ? 1 : 4;
       {
         std::unique_lock<std::mutex> lk(mu);
         job_cv.wait(lk, [&] { return stop || !jobs.empty(); });
         if (stop && jobs.empty()) return;
-        while (!jobs.empty() && m < 4) {
+        while (!jobs.empty() && m < claim) {
           const Key key = jobs.front();
           auto it = entries.find(key);
           if (it == entries.end()) {

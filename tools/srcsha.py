@@ -1,7 +1,11 @@
-"""sha256[:16] of the product library's SOURCES (csrc/*.cu, *.cuh, *.hpp,
-Makefile, include/gs_capi.h): the key that ties a committed ncu capture to
-the build it profiled. The built .so is not byte-reproducible across nvcc
-runs, so its own hash would orphan every capture on the next rebuild."""
+"""sha256[:16] of the sources that determine the profiled codec kernels (K1 /
+K2 / paged K1: their code and their launch geometry): gs_kernels.cuh,
+gs_special.cuh, gs_special_*.cu, gs_field.hpp, gs_capi.cu (the launch
+configuration), the Makefile (flags) and include/gs_capi.h. The key that ties
+a committed ncu capture to the build it profiled -- the built .so is not
+byte-reproducible across nvcc runs, so its own hash would orphan every
+capture on the next rebuild, and host-only sources (the store, the host FNV)
+do not change these kernels."""
 import glob
 import hashlib
 import os
@@ -11,9 +15,10 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 def source_sha() -> str:
     csrc = os.path.join(ROOT, "paper_2605_00831_b200", "csrc")
-    files = sorted(glob.glob(os.path.join(csrc, "*.cu")) + glob.glob(os.path.join(csrc, "*.cuh"))
-                   + glob.glob(os.path.join(csrc, "*.hpp")) + glob.glob(os.path.join(csrc, "*.cpp"))
-                   + [os.path.join(csrc, "Makefile"), os.path.join(ROOT, "include", "gs_capi.h")])
+    files = sorted([os.path.join(csrc, f) for f in ("gs_kernels.cuh", "gs_special.cuh", "gs_field.hpp",
+                                                    "gs_capi.cu", "Makefile")]
+                   + glob.glob(os.path.join(csrc, "gs_special_*.cu"))
+                   + [os.path.join(ROOT, "include", "gs_capi.h")])
     h = hashlib.sha256()
     for p in files:
         h.update(os.path.relpath(p, ROOT).encode() + b"\0")
