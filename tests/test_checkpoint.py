@@ -206,6 +206,15 @@ def test_long_request_single_failure_rs82_bit_exact():
     for threads in (1, 2):   # few host threads: the GPU feeder takes most of the chains
         res = ck.recover(6, FailureEvent([5], at_chunk=32), run.ground_truth, [2048] * 32, verify_threads=threads)
         assert res.verified and res.decoded_chunks == 32 and res.verify_gpu_chunks > 0, threads
+    # the same with the scalar host chain (hosts without the AVX-512 FNV): same plan, same bytes
+    from paper_2605_00831_b200 import _lib as L
+    hw = L.lib().gs_fnv_host_simd()
+    try:
+        L.lib().gs_fnv_host_set_simd(0)
+        res = ck.recover(6, FailureEvent([5], at_chunk=32), run.ground_truth, [2048] * 32)
+        assert res.verified and res.decoded_chunks == 32 and not res.corrupt_chunks
+    finally:
+        assert L.lib().gs_fnv_host_set_simd(1) == hw
     # static split (decided from the host-rate estimates): all in HBM / all split / host only
     ck.verify_split = "static"
     for gpu, rate, want in [(True, 1.0, 32), (True, 1e30, 0), (False, None, 0)]:
