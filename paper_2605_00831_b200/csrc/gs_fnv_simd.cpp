@@ -228,12 +228,6 @@ GS_SIMD_TARGET inline void columns2(BlockChain& a, BlockChain& b, __m512i (&bits
   b.column<J>(bits[J], k);
   if constexpr (J < 7) columns2<J + 1>(a, b, bits, k);
 }
-template <int J>
-GS_SIMD_TARGET inline void columns1(BlockChain& a, __m512i (&bits)[8], const Consts& k) {
-  a.column<J>(bits[J], k);
-  if constexpr (J < 7) columns1<J + 1>(a, bits, k);
-}
-
 GS_SIMD_TARGET inline void load_planes(BlockChain& c, const uint8_t* p, const Consts& k) {
   for (int q = 0; q < 8; ++q) c.B[q] = to_planes64(_mm512_loadu_si512(p + 64 * q), k);
   transpose8x8q(c.B);  // B[j] = plane j of the 512 bytes
@@ -246,28 +240,6 @@ GS_SIMD_TARGET inline uint64_t hsum64(__m512i a) {
   return static_cast<uint64_t>(_mm512_reduce_add_epi64(s));
 }
 
-}  // namespace
-
-namespace {
-bool simd_hw() {
-  static const bool ok = [] {
-    __builtin_cpu_init();
-    return __builtin_cpu_supports("avx512f") && __builtin_cpu_supports("avx512bw") &&
-           __builtin_cpu_supports("avx512dq") && __builtin_cpu_supports("avx512vbmi") &&
-           __builtin_cpu_supports("avx512vnni") && __builtin_cpu_supports("gfni") &&
-           __builtin_cpu_supports("vpclmulqdq");
-  }();
-  return ok;
-}
-std::atomic<bool> g_simd_on{true};
-}  // namespace
-
-bool fnv_simd_available() { return simd_hw() && g_simd_on.load(std::memory_order_relaxed); }
-
-bool fnv_simd_set(bool on) {
-  g_simd_on.store(on, std::memory_order_relaxed);
-  return fnv_simd_available();
-}
 
 // sum_i d_i * P^(kSuper-i) contributions of one 512-byte block (index blk in
 // its super-block) into the four limb accumulators; d = b - 2 (b & l).
@@ -296,8 +268,6 @@ GS_SIMD_TARGET inline uint64_t reduce_limbs(__m512i (&a)[4]) {
   for (int m = 0; m < 4; ++m) a[m] = _mm512_setzero_si512();
   return t;
 }
-
-namespace {
 
 // The 2 KiB super-blocks of p[0 .. nsup * kSuper): advances the low byte `l`
 // and returns S = sum_i d_i P^(len-i) over them (a state h with low byte l
@@ -332,7 +302,25 @@ GS_SIMD_TARGET static uint64_t simd_blocks(const uint8_t* p, size_t nsup, uint32
 
 inline uint32_t low_step(uint32_t l, uint8_t b) { return ((l ^ b) * 0xB3u) & 0xFFu; }
 
+bool simd_hw() {
+  static const bool ok = [] {
+    __builtin_cpu_init();
+    return __builtin_cpu_supports("avx512f") && __builtin_cpu_supports("avx512bw") &&
+           __builtin_cpu_supports("avx512dq") && __builtin_cpu_supports("avx512vbmi") &&
+           __builtin_cpu_supports("avx512vnni") && __builtin_cpu_supports("gfni") &&
+           __builtin_cpu_supports("vpclmulqdq");
+  }();
+  return ok;
+}
+std::atomic<bool> g_simd_on{true};
 }  // namespace
+
+bool fnv_simd_available() { return simd_hw() && g_simd_on.load(std::memory_order_relaxed); }
+
+bool fnv_simd_set(bool on) {
+  g_simd_on.store(on, std::memory_order_relaxed);
+  return fnv_simd_available();
+}
 
 uint64_t fnv_pow(uint64_t n) {
   uint64_t r = 1, x = kFnvPrime;
