@@ -551,6 +551,9 @@ __global__ void __cluster_dims__(kWCS, 1, 1) __launch_bounds__(kWT, 2)
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const uint32_t rank = cluster_rank();
   sh.pw[tid] = pow64(kFnvP, static_cast<uint64_t>(kFPer) * tid);
+  // every CTA of the cluster has started (and initialised its shared memory)
+  // before rank 0 writes the first window index into their shared memory
+  cluster_sync_all();
   for (;;) {
     if (rank == 0 && tid == 0) {
       const uint32_t g = atomicAdd(counter, 1u);

@@ -1,6 +1,7 @@
 """Small workload for compute-sanitizer (memcheck / racecheck / synccheck):
 every kernel family once -- specialised (register + bulk-copy pipeline),
-generic (aligned, ragged tail, misaligned), paged gather/scatter, the
+generic (aligned, ragged tail, misaligned), paged gather/scatter (incl. the
+page-per-tile path), the
 offload / upload pipelines (with live kernel timing stamps), RDP (pipelined
 body + tile remainder + P/Q tail, two-column and single-column recovery) and
 a runtime-specialised (NVRTC) kernel, the GPU FNV-1a seal and the split
@@ -84,6 +85,18 @@ def main():
                    9, hp, st, st)
     st.synchronize()
     bad += not torch.equal(rep[4].read_slice(4, 9), truth[4])
+    # paged, page-per-tile path (4 KiB pages, every token valid: TileGeom.tile_pages)
+    model4k = ModelConfig(4, 8, 128, 2, 8)
+    caches4k = [PagedKVCache(model4k, 3, 16) for _ in range(8)]
+    truth4k = []
+    for j in range(8):
+        sl = make_ground_truth_slice(3, 1, 0, j, model4k, 16, 16, device="cuda")
+        caches4k[j].write_slice((j + 1) % 3, sl, 16)
+        truth4k.append(sl)
+    par4k = torch.empty((1, 2, caches4k[0].slice_bytes), dtype=torch.uint8, device="cuda")
+    encode_blocks(sch, caches4k, [[(j + 1) % 3 for j in range(8)]], 16, par4k)
+    want4k = O.port().encode(O.RS, 8, 2, [t.cpu().numpy() for t in truth4k])
+    bad += sum(not np.array_equal(par4k[0, i].cpu().numpy(), want4k[i]) for i in range(2))
     # pipelines with live kernel timing (globaltimer stamps)
     import ctypes as C
     L.lib().gs_pipeline_set_timing(pipe.handle, 1)
