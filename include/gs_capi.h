@@ -163,7 +163,7 @@ int gs_prewarm(int device);
 /* Variant of the specialised kernels for aligned bodies (process-wide):
  * 0 = register-streaming LDG.128 kernel, 1 = bulk-copy (cp.async.bulk)
  * shared-memory pipeline with producer/consumer warps, 2 = auto (default:
- * bulk for encode launches >= 128 MB, register kernel otherwise). All are
+ * bulk for encodes with shards >= 48 MiB, register kernel otherwise). All are
  * bit-identical; exposed for benchmarking and cross-checking. */
 int gs_set_kernel_variant(int variant);
 /* Runtime-specialised kernels: a codec with no compiled specialisation

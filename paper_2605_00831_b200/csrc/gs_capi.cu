@@ -160,7 +160,13 @@ int g_full_grid = [] {
   const char* e = std::getenv("GS_FULL_GRID");
   return e ? std::atoi(e) : 0;
 }();
-constexpr uint64_t kBulkAutoBytes = 128ull << 20;
+// Auto variant: the bulk TMA ring for encodes whose shards are long enough
+// (per-shard length, not launch bytes): from ~64 MiB shards the register
+// kernel can lose half its rate (allocation-dependent, tools/k1_layout_probe.py)
+// while the bulk ring holds 6 TB/s; up to 32 MiB the register kernel is as
+// fast in isolation and faster next to the pipeline's D2H (C3 pieces of
+// 32 MiB: 46 vs 48 us per launch in the timed steps).
+constexpr uint64_t kBulkAutoShardBytes = 48ull << 20;
 // Paged K1/K2 walk tiles page-major (GS_PAGE_MAJOR=0: stripe-major, for A/B).
 const bool g_page_major = [] {
   const char* e = std::getenv("GS_PAGE_MAJOR");
@@ -458,11 +464,8 @@ int run_codec(const gs_codec* c, int n_stripes, SlotFn slot_ptr, OutFn out_ptr, 
     const uint64_t body = len / kVec * kVec;
     const int stages = c->special ? bulk_stages(c->special) : 0;
     const int variant = g_variant.load(std::memory_order_relaxed);
-    const uint64_t launch_bytes = c->special ? body * static_cast<uint64_t>(n_stripes) *
-                                                   static_cast<uint64_t>(c->special->used_cols + c->n_out)
-                                             : 0;
     const bool use_bulk = c->special && !pg.any() && stages >= 2 &&
-                          (variant == 1 || (variant == 2 && !c->decoder && launch_bytes >= kBulkAutoBytes));
+                          (variant == 1 || (variant == 2 && !c->decoder && body >= kBulkAutoShardBytes));
     const uint64_t tile = static_cast<uint64_t>(use_bulk ? c->special->tile_bulk : c->special ? c->special->tile : kTile);
     const uint64_t tps64 = (body + tile - 1) / tile;
     const int stride = c->n_slots + c->n_out;
