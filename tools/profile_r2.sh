@@ -1,5 +1,7 @@
-# Round-2 GPU evidence (run under gpurun; summarised here with
-# tools/ncu_summary.py and tools/r2_summaries.py into profiles/r2_*):
+# Round-2 GPU evidence, first pass (run under gpurun; summarised here with
+# tools/ncu_summary.py, tools/launch_summary.py and tools/link_summary.py into
+# profiles/r2_*; the closing captures of the final sources are
+# tools/profile_final.sh and tools/recapture_kernels.sh):
 #  * ncu --set full of K1 / K2 / paged K1 at the C3 launch (one 2K-token chunk,
 #    8 x 80 MiB) from bench.py's own launches, K1 at the C2 launch, the GPU
 #    FNV-1a window kernel (and the legacy multi-pass one for A/B);
@@ -8,8 +10,8 @@
 #    and one chunk rebuild (H2D + K2): PCIe bytes + elapsed time;
 #  * the default bench line, the reference arm, the C5 sweep and the
 #    small-L probe; SASS opcode histograms are made locally (cuobjdump).
-# The library's sha is recorded so bench.py only reports roofline.traffic
-# for the build that was captured.
+# tools/srcsha.py (a hash of the kernel sources) is recorded so bench.py
+# only reports roofline.traffic for the sources that were captured.
 set -x
 mkdir -p gpurun_out
 sha256sum paper_2605_00831_b200/_lib/libghostserve_b200.so | cut -c1-16 > gpurun_out/lib_sha.txt
