@@ -8,6 +8,7 @@ import re
 
 import numpy as np
 import pytest
+from fuzzutil import fuzz_trials
 
 from oracle import oracle as O
 from paper_2605_00831_b200 import _lib as L
@@ -220,7 +221,7 @@ def test_random_schemes_decode_like_the_reference(port):
     ref = O.ref()
     rng = random.Random(2024)
     mul = ref.mul_table()
-    for trial in range(60):
+    for trial in range(fuzz_trials(60)):
         k = rng.randint(1, 8)
         n = rng.randint(k, min(96, 255 - k))
         ln = rng.randint(1, 24)

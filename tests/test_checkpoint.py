@@ -7,6 +7,7 @@ import random
 
 import numpy as np
 import pytest
+from fuzzutil import fuzz_trials
 
 from oracle import oracle as O
 from paper_2605_00831_b200.checkpoint import (AssignmentState, CheckpointConfig, CostModel, FailureEvent,
@@ -277,7 +278,7 @@ def test_orchestration_fuzz():
     import random
     from paper_2605_00831_b200.checkpoint import DecodeCheckpointer
     rng = random.Random(5150)
-    for trial in range(10):
+    for trial in range(fuzz_trials(10)):
         tp = rng.choice([2, 4, 6, 8])
         k = rng.randint(1, min(3, tp))
         chunk = rng.choice([4, 16, 32])

@@ -8,6 +8,7 @@ import ctypes as C
 
 import numpy as np
 import pytest
+from fuzzutil import fuzz_trials
 
 from oracle import oracle as O
 
@@ -156,7 +157,7 @@ def test_fnv_fuzz_random_chains():
     64-B thread and 16 KiB block grains) and seeds: bit-exact every time."""
     port = O.port()
     rng = np.random.default_rng(2026)
-    for trial in range(30):
+    for trial in range(fuzz_trials(30)):
         n_chains = int(rng.integers(1, 9))
         k = int(rng.integers(1, 5))
         ln = 16 * int(rng.choice([1, 3, 4, 63, 64, 65, 1023, 1024, 1025, int(rng.integers(1, 12000))]))

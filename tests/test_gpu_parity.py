@@ -7,6 +7,7 @@ import subprocess
 
 import numpy as np
 import pytest
+from fuzzutil import fuzz_trials
 
 from oracle import oracle as O
 from tests.golden.vectors import splitmix_bytes
@@ -559,7 +560,7 @@ def test_random_schemes_on_the_gpu():
     rebuild, bit-exact vs the oracle."""
     import random
     rng = random.Random(77)
-    for trial in range(24):
+    for trial in range(fuzz_trials(24)):
         k = rng.randint(1, 6)
         n = rng.randint(k, 40)
         ln = rng.choice([1, 15, 4096 + 7, 70001, 1 << 17])
@@ -634,7 +635,7 @@ def test_pipeline_fuzz():
     shards bit-exact vs the oracle, several calls in flight on one ring."""
     import random
     rng = random.Random(4242)
-    for trial in range(40):
+    for trial in range(fuzz_trials(40)):
         kind = rng.choice(["rs", "rs", "xor", "rdp"])
         if kind == "rs":
             k = rng.randint(1, 4)

@@ -3,6 +3,7 @@ partial blocks masked exactly like pad_partial; bytes checked against the
 oracle on the gathered reference-layout slices."""
 import numpy as np
 import pytest
+from fuzzutil import fuzz_trials
 
 from oracle import oracle as O
 
@@ -155,7 +156,7 @@ def test_paged_fuzz_geometries():
     import random
     from paper_2605_00831_b200.paged import checkpoint_chunks, rebuild_chunks
     rng = random.Random(31337)
-    for trial in range(30):
+    for trial in range(fuzz_trials(30)):
         tp = rng.choice([2, 4, 6, 8])
         heads = tp * rng.choice([1, 2])
         model = ModelConfig(rng.choice([1, 2, 3, 5]), heads, rng.choice([8, 16, 64, 128]), 2, tp)

@@ -16,6 +16,7 @@ import socket
 
 import numpy as np
 import pytest
+from fuzzutil import fuzz_trials
 import torch
 import torch.distributed as dist
 import torch.multiprocessing as mp
@@ -337,7 +338,7 @@ def test_striped_partition_fuzz_single_process():
     from paper_2605_00831_b200.peer import ShardLayout, striped_slots
     rng = random.Random(808)
     port_lib = O.port()
-    for trial in range(25):
+    for trial in range(fuzz_trials(25)):
         n = rng.choice([2, 4, 6, 8, 12, 16])
         world = rng.choice([w for w in (1, 2, 3, 4, 6, 8) if n % w == 0])
         k = rng.randint(1, min(4, n))
