@@ -496,8 +496,9 @@ int run_codec(const gs_codec* c, int n_stripes, SlotFn slot_ptr, OutFn out_ptr, 
         g.nstripes_m = fastdiv_magic(g.nstripes);
         uint32_t used = 0;
         for (int j : c->used) used |= 1u << j;
-        g.tile_pages = g_tile_pages && (pg.paged_slots & used) == used && !pg.src.table && pg.dst.page_bytes == 0 &&
+        g.tile_pages = g_tile_pages && (pg.paged_slots & used) == used && pg.dst.page_bytes == 0 &&
                        pg.src.page_bytes % kTile == 0 && pg.logical0 % kTile == 0 &&
+                       (!pg.src.table || pg.src.block_bytes % kTile == 0) &&
                        static_cast<uint64_t>(pg.src.valid_tokens) * pg.src.token_bytes == pg.src.page_bytes &&
                        pg.logical0 + body <= 0xFFFFFFFFull;
       }

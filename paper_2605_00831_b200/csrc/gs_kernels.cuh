@@ -180,11 +180,12 @@ struct TileGeom {
   uint32_t nstripes;
   uint64_t nstripes_m;  // fastdiv_magic(nstripes)
   // Page-per-tile source mapping (set by the host for paged K1 when every
-  // used source is a paged cache without a block table, pages are whole
-  // multiples of a tile, every token is valid, logical0 is tile-aligned and
-  // the outputs are contiguous -- the single-block decode-block checkpoint):
-  // a tile is one piece of one page, so its cache offset comes from the tile
-  // index alone, with no per-thread page arithmetic or masking.
+  // used source is a paged cache, pages -- and cache blocks, with a block
+  // table -- are whole multiples of a tile, every token is valid, logical0 is
+  // tile-aligned and the outputs are contiguous: the decode-block and prefill
+  // chunk checkpoints): a tile is one piece of one page of one block, so its
+  // cache offset comes from the tile index (and one table entry) alone, with
+  // no per-thread page arithmetic or masking.
   uint32_t tile_pages;
 };
 
@@ -357,9 +358,16 @@ __global__ void __launch_bounds__(kThreads) k_apply_special(const PtrTable<CAP> 
       const uint32_t u = static_cast<uint32_t>(g.logical0) + tin * static_cast<uint32_t>(kTile);
       const uint32_t pg = fdiv(u, g.src.page_bytes, g.src.page_m);
       const uint32_t kv = fdiv(pg, g.src.layers, g.src.layers_m);
-      const uint64_t soff = static_cast<uint64_t>(pg - kv * g.src.layers) * g.src.layer_stride +
-                            static_cast<uint64_t>(kv) * g.src.kv_stride + (u - pg * g.src.page_bytes) +
-                            threadIdx.x * kVec;
+      const uint32_t in0 = u - pg * g.src.page_bytes;
+      uint64_t soff = static_cast<uint64_t>(pg - kv * g.src.layers) * g.src.layer_stride +
+                      static_cast<uint64_t>(kv) * g.src.kv_stride + threadIdx.x * kVec;
+      if (g.src.table) {  // multi-block chunk: the tile's block from the table (whole tiles per block)
+        const uint32_t pi = fdiv(in0, g.src.block_bytes, g.src.block_m);
+        const int32_t blk = g.src.table[static_cast<uint64_t>(s) * g.src.table_stride + pi];
+        soff += static_cast<uint64_t>(blk) * g.src.block_bytes + (in0 - pi * g.src.block_bytes);
+      } else {
+        soff += in0;
+      }
 #pragma unroll
       for (int j = 0; j < Spec::NS; ++j)
         src[j] = column_used<Spec>(j) ? ld_stream(tab.p[base + j] + soff) : make_uint4(0, 0, 0, 0);
