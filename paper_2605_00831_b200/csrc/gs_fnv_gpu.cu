@@ -631,8 +631,278 @@ __global__ void __cluster_dims__(kWCS, 1, 1) __launch_bounds__(kWT, 2)
   }
 }
 
+// ===========================================================================
+// Bit-sliced cluster windows (the default; GS_FNV_WINDOW_BYTES=1 keeps the
+// byte-lane rounds above for A/B). Same windows, look-back and cluster scans
+// as k_fnv_window; only the per-thread arithmetic of a round changes: the
+// thread's 64 bytes are held as two groups of eight 32-bit bit planes (bit i
+// of plane j = bit j of byte i), and round K evaluates the column-K bits of
+// the bit-sliced product x * 0xB3 (x = s ^ b) from the lower planes with
+// carry-save full adders (one known bit per column, so each new plane adds
+// one AND / majority), then an XOR prefix inside each 32-bit word -- ~40
+// integer ops per round for 64 bytes instead of ~240. The low bytes go back
+// to byte lanes once, for the final sum.
+// ===========================================================================
+__device__ __forceinline__ uint64_t sl_t8(uint64_t x) {  // 8x8 bit transpose: byte j bit b <-> byte b bit j
+  uint64_t t = (x ^ (x >> 7)) & 0x00AA00AA00AA00AAull;
+  x = x ^ t ^ (t << 7);
+  t = (x ^ (x >> 14)) & 0x0000CCCC0000CCCCull;
+  x = x ^ t ^ (t << 14);
+  t = (x ^ (x >> 28)) & 0x00000000F0F0F0F0ull;
+  return x ^ t ^ (t << 28);
+}
+__device__ __forceinline__ void sl_bt4(uint32_t& a, uint32_t& b, uint32_t& c, uint32_t& d) {  // 4x4 byte transpose
+  const uint32_t ab_lo = __byte_perm(a, b, 0x5140), ab_hi = __byte_perm(a, b, 0x7362);
+  const uint32_t cd_lo = __byte_perm(c, d, 0x5140), cd_hi = __byte_perm(c, d, 0x7362);
+  a = __byte_perm(ab_lo, cd_lo, 0x5410);
+  b = __byte_perm(ab_lo, cd_lo, 0x7632);
+  c = __byte_perm(ab_hi, cd_hi, 0x5410);
+  d = __byte_perm(ab_hi, cd_hi, 0x7632);
+}
+// 32 bytes (w[i] byte k = byte 4i + k) <-> 8 planes (plane j bit i = bit j of byte i).
+__device__ __forceinline__ void sl_to_planes(uint32_t (&w)[8]) {
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    const uint64_t x = sl_t8(static_cast<uint64_t>(w[2 * k]) | (static_cast<uint64_t>(w[2 * k + 1]) << 32));
+    w[2 * k] = static_cast<uint32_t>(x);
+    w[2 * k + 1] = static_cast<uint32_t>(x >> 32);
+  }
+  uint32_t a = w[0], b = w[2], c = w[4], d = w[6], e = w[1], f = w[3], g = w[5], h = w[7];
+  sl_bt4(a, b, c, d);
+  sl_bt4(e, f, g, h);
+  w[0] = a; w[1] = b; w[2] = c; w[3] = d; w[4] = e; w[5] = f; w[6] = g; w[7] = h;
+}
+__device__ __forceinline__ void sl_from_planes(uint32_t (&w)[8]) {
+  uint32_t a = w[0], b = w[1], c = w[2], d = w[3], e = w[4], f = w[5], g = w[6], h = w[7];
+  sl_bt4(a, b, c, d);
+  sl_bt4(e, f, g, h);
+  const uint32_t lo[4] = {a, b, c, d}, hi[4] = {e, f, g, h};
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    const uint64_t x = sl_t8(static_cast<uint64_t>(lo[k]) | (static_cast<uint64_t>(hi[k]) << 32));
+    w[2 * k] = static_cast<uint32_t>(x);
+    w[2 * k + 1] = static_cast<uint32_t>(x >> 32);
+  }
+}
+__device__ __forceinline__ uint32_t sl_prefix32(uint32_t x) {  // inclusive prefix XOR along the bits
+  x ^= x << 1;
+  x ^= x << 2;
+  x ^= x << 4;
+  x ^= x << 8;
+  x ^= x << 16;
+  return x;
+}
+__device__ __forceinline__ uint32_t sl_maj(uint32_t a, uint32_t b, uint32_t c) { return (a & b) | (c & (a | b)); }
+
+// One 32-byte group: its planes, the x planes solved so far and the
+// carry-save state of the column sums of x * 0xB3 = x + 2x + 16x + 32x + 128x.
+struct SlCol {
+  uint32_t B[8], X[8];
+  uint32_t c12, c23, c34, s4, c45a, c45b, s5, c56a, c56b, c56c, s6, c67a, c67b, c67c, c67d;
+  template <int K>
+  __device__ __forceinline__ uint32_t g() {  // column K bits other than x_K (known bits pre-reduced)
+    if constexpr (K == 0) return 0u;
+    else if constexpr (K == 1) return X[0];
+    else if constexpr (K == 2) return X[1] ^ c12;
+    else if constexpr (K == 3) return X[2] ^ c23;
+    else if constexpr (K == 4) {
+      s4 = X[3] ^ X[0] ^ c34;
+      c45a = sl_maj(X[3], X[0], c34);
+      return s4;
+    } else if constexpr (K == 5) {
+      const uint32_t s5a = X[1] ^ X[0] ^ c45a;
+      c56a = sl_maj(X[1], X[0], c45a);
+      s5 = s5a ^ X[4] ^ c45b;
+      c56b = sl_maj(s5a, X[4], c45b);
+      return s5;
+    } else if constexpr (K == 6) {
+      const uint32_t s6a = X[2] ^ X[1] ^ c56a;
+      c67a = sl_maj(X[2], X[1], c56a);
+      const uint32_t s6b = s6a ^ c56b ^ c56c;
+      c67b = sl_maj(s6a, c56b, c56c);
+      s6 = s6b ^ X[5];
+      c67c = s6b & X[5];
+      return s6;
+    } else {
+      return X[6] ^ X[3] ^ X[2] ^ X[0] ^ c67a ^ c67b ^ c67c ^ c67d;  // only the parity of column 7
+    }
+  }
+  template <int K>
+  __device__ __forceinline__ void after() {  // carries out of column K once x_K is known
+    if constexpr (K == 1) c12 = X[1] & X[0];
+    else if constexpr (K == 2) c23 = sl_maj(X[2], X[1], c12);
+    else if constexpr (K == 3) c34 = sl_maj(X[3], X[2], c23);
+    else if constexpr (K == 4) c45b = X[4] & s4;
+    else if constexpr (K == 5) c56c = X[5] & s5;
+    else if constexpr (K == 6) c67d = X[6] & s6;
+  }
+};
+
+struct WinSharedSl {
+  uint64_t pw[kWT];                  // P^(64 t)
+  uint32_t wpar[8][kWCS];            // [round][cluster rank]: bit x = parity of warp x of that CTA
+  uint32_t gw;                       // window index, written by rank 0
+  unsigned long long wsum[kWT / 32];
+  uint64_t pblk;
+};
+
+// OR a u32 into the same smem variable of CTA `rank` of this cluster.
+__device__ __forceinline__ void or_cluster_u32(uint32_t* local, uint32_t rank, uint32_t v) {
+  uint32_t a = static_cast<uint32_t>(__cvta_generic_to_shared(local)), ra;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(ra) : "r"(a), "r"(rank));
+  asm volatile("red.shared::cluster.or.b32 [%0], %1;" ::"r"(ra), "r"(v) : "memory");
+}
+
+// One round with ONE barrier: every warp ORs its parity bit into its CTA's
+// word of this round in every CTA of the cluster, one cluster barrier, then
+// each thread derives its carry from the 8 words; every warp walks the
+// look-back itself (rank 0 / warp 0 publishes), and each round has its own
+// slots, so no barrier separates the rounds.
+template <int K>
+__device__ __forceinline__ void win_round_sl(WinSharedSl& sh, uint32_t* flags, uint32_t gw, uint32_t w, uint32_t nc,
+                                             uint64_t h0, uint32_t rank, SlCol (&G)[2], uint32_t& flag_word) {
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const uint32_t inc0 = sl_prefix32(G[0].B[K] ^ G[0].template g<K>());
+  const uint32_t inc1 = sl_prefix32(G[1].B[K] ^ G[1].template g<K>());
+  const uint32_t par0 = inc0 >> 31;
+  const uint32_t par = par0 ^ (inc1 >> 31);
+  const uint32_t bal = __ballot_sync(0xFFFFFFFFu, par);
+  uint32_t carry = __popc(bal & ((1u << lane) - 1u)) & 1u;
+  if ((__popc(bal) & 1u) && lane < kWCS) or_cluster_u32(&sh.wpar[K][rank], static_cast<uint32_t>(lane), 1u << warp);
+  cluster_sync_all();
+  uint32_t win_tot = 0;
+#pragma unroll
+  for (int r = 0; r < kWCS; ++r) {
+    const uint32_t t = __popc(sh.wpar[K][r]) & 1u;
+    if (static_cast<uint32_t>(r) < rank) carry ^= t;
+    win_tot ^= t;
+  }
+  carry ^= __popc(sh.wpar[K][rank] & ((1u << warp) - 1u)) & 1u;
+  if (rank == 0 && warp == 0 && lane == 0) {
+    flag_word |= (win_tot << K) | (1u << (16 + K));
+    st_release_u32(flags + gw, flag_word);
+  }
+  const uint32_t entry = w == 0 ? static_cast<uint32_t>(h0 >> K) & 1u : lookback_entry<K>(flags, gw, w, nc, h0);
+  if (rank == 0 && warp == 0 && lane == 0) {
+    flag_word |= ((entry ^ win_tot) << (8 + K)) | (1u << (24 + K));
+    st_release_u32(flags + gw, flag_word);
+  }
+  carry ^= entry;
+  const uint32_t L0 = (inc0 << 1) ^ (0u - carry), L1 = (inc1 << 1) ^ (0u - (carry ^ par0));
+  G[0].X[K] = L0 ^ G[0].B[K];
+  G[1].X[K] = L1 ^ G[1].B[K];
+  G[0].template after<K>();
+  G[1].template after<K>();
+}
+
+__global__ void __cluster_dims__(kWCS, 1, 1) __launch_bounds__(kWT, 2)
+    k_fnv_window_sl(const FnvJob j, uint64_t h0, const uint64_t* __restrict__ h0s, uint32_t nc, uint32_t total_windows,
+                    uint32_t* counter, uint32_t* flags, unsigned long long* __restrict__ out) {
+  __shared__ WinSharedSl sh;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const uint32_t rank = cluster_rank();
+  sh.pw[tid] = pow64(kFnvP, static_cast<uint64_t>(kFPer) * tid);
+  cluster_sync_all();  // every CTA of the cluster has started before rank 0 writes into their smem
+  for (;;) {
+    if (tid < 8 * kWCS) (&sh.wpar[0][0])[tid] = 0;  // this window's parity words (no remote OR before the barrier)
+    if (rank == 0 && tid == 0) {
+      const uint32_t g = atomicAdd(counter, 1u);
+      for (int r = 0; r < kWCS; ++r) st_cluster_u32(&sh.gw, static_cast<uint32_t>(r), g);
+    }
+    cluster_sync_all();
+    const uint32_t gw = sh.gw;
+    if (gw >= total_windows) break;
+    const uint32_t w = gw / nc, c = gw - w * nc;
+    const uint64_t hc = h0s ? h0s[c] : h0;
+    const uint64_t cta0 = static_cast<uint64_t>(w) * kWin + static_cast<uint64_t>(rank) * kWB;
+    const uint64_t pos0 = cta0 + static_cast<uint64_t>(tid) * kFPer;
+    SlCol G[2];
+    {
+      uint4 d[4];
+      load_groups(j, c, pos0, d);
+#pragma unroll
+      for (int q = 0; q < 2; ++q) {
+        uint32_t wv[8] = {d[2 * q].x, d[2 * q].y, d[2 * q].z, d[2 * q].w,
+                          d[2 * q + 1].x, d[2 * q + 1].y, d[2 * q + 1].z, d[2 * q + 1].w};
+        sl_to_planes(wv);
+#pragma unroll
+        for (int b = 0; b < 8; ++b) G[q].B[b] = wv[b];
+      }
+    }
+    uint32_t fw = 0;
+    win_round_sl<0>(sh, flags, gw, w, nc, hc, rank, G, fw);
+    win_round_sl<1>(sh, flags, gw, w, nc, hc, rank, G, fw);
+    win_round_sl<2>(sh, flags, gw, w, nc, hc, rank, G, fw);
+    win_round_sl<3>(sh, flags, gw, w, nc, hc, rank, G, fw);
+    win_round_sl<4>(sh, flags, gw, w, nc, hc, rank, G, fw);
+    win_round_sl<5>(sh, flags, gw, w, nc, hc, rank, G, fw);
+    win_round_sl<6>(sh, flags, gw, w, nc, hc, rank, G, fw);
+    win_round_sl<7>(sh, flags, gw, w, nc, hc, rank, G, fw);
+    // low bytes s = x ^ b back to byte lanes; the data re-read (cache-resident)
+    uint4 s[4], d[4];
+#pragma unroll
+    for (int q = 0; q < 2; ++q) {
+      uint32_t wv[8];
+#pragma unroll
+      for (int b = 0; b < 8; ++b) wv[b] = G[q].X[b] ^ G[q].B[b];
+      sl_from_planes(wv);
+      s[2 * q] = make_uint4(wv[0], wv[1], wv[2], wv[3]);
+      s[2 * q + 1] = make_uint4(wv[4], wv[5], wv[6], wv[7]);
+    }
+    const int nvalid = load_groups(j, c, pos0, d);
+    // sum over the thread's bytes of d_i P^(tend - i), four 16-byte Horner chains
+    uint64_t accq[4] = {0, 0, 0, 0};
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      if (q < nvalid) {
+#pragma unroll
+        for (int x = 0; x < 4; ++x) {
+          const uint32_t sw = wd(s[q], x), xw = sw ^ wd(d[q], x);
+#pragma unroll
+          for (int by = 0; by < 4; ++by) {
+            const int64_t di = static_cast<int64_t>((xw >> (8 * by)) & 0xFFu) -
+                               static_cast<int64_t>((sw >> (8 * by)) & 0xFFu);
+            accq[q] = (accq[q] + static_cast<uint64_t>(di)) * kFnvP;
+          }
+        }
+      }
+    }
+    constexpr uint64_t kP16 = [] {
+      uint64_t r = 1;
+      for (int i = 0; i < 16; ++i) r *= kFnvP;
+      return r;
+    }();
+    uint64_t acc = 0;
+#pragma unroll
+    for (int q = 0; q < 4; ++q)
+      if (q < nvalid) acc = acc * kP16 + accq[q];
+    const uint64_t cend = cta0 + kWB;
+    if (tid == 0) sh.pblk = cend <= j.n ? pow64(kFnvP, j.n - cend) : 0;
+    __syncthreads();
+    uint64_t contrib = 0;
+    if (nvalid > 0) {
+      const uint64_t tend = pos0 + 16u * nvalid;
+      contrib = acc * (cend <= j.n ? sh.pblk * sh.pw[kWT - 1 - tid] : pow64(kFnvP, j.n - tend));
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) contrib += __shfl_xor_sync(0xFFFFFFFFu, contrib, o);
+    if (lane == 0) sh.wsum[warp] = contrib;
+    __syncthreads();
+    if (tid == 0) {
+      uint64_t sum = 0;
+#pragma unroll
+      for (int x = 0; x < kWT / 32; ++x) sum += sh.wsum[x];
+      atomicAdd(out + c, static_cast<unsigned long long>(sum));
+    }
+  }
+}
+
 const bool g_fnv_legacy = [] {
   const char* e = std::getenv("GS_FNV_LEGACY");
+  return e && std::atoi(e) != 0;
+}();
+const bool g_fnv_bytes = [] {  // the byte-lane window rounds instead of the bit-sliced ones (A/B)
+  const char* e = std::getenv("GS_FNV_WINDOW_BYTES");
   return e && std::atoi(e) != 0;
 }();
 int g_win_clusters = 0;
@@ -727,9 +997,14 @@ static int fnv_device(const void* const* bufs, int n_chains, int k, uint64_t len
       cudaError_t r = cudaMemsetAsync(ctl, 0, sizeof(uint32_t) * (1 + static_cast<size_t>(total)), st);
       const int clusters = static_cast<int>(std::min<uint64_t>(g_win_clusters, total));
       if (r == cudaSuccess) {
-        k_fnv_window<<<clusters * kWCS, kWT, 0, st>>>(j, h0, d_h0 ? d_h0 + c0 : nullptr, static_cast<uint32_t>(cnt),
-                                                     total, ctl, ctl + 1,
-                                                     reinterpret_cast<unsigned long long*>(d_out) + c0);
+        if (g_fnv_bytes)
+          k_fnv_window<<<clusters * kWCS, kWT, 0, st>>>(j, h0, d_h0 ? d_h0 + c0 : nullptr, static_cast<uint32_t>(cnt),
+                                                       total, ctl, ctl + 1,
+                                                       reinterpret_cast<unsigned long long*>(d_out) + c0);
+        else
+          k_fnv_window_sl<<<clusters * kWCS, kWT, 0, st>>>(j, h0, d_h0 ? d_h0 + c0 : nullptr,
+                                                          static_cast<uint32_t>(cnt), total, ctl, ctl + 1,
+                                                          reinterpret_cast<unsigned long long*>(d_out) + c0);
         r = cudaGetLastError();
       }
       if (r != cudaSuccess) status = ffail(GS_CUDA_ERROR, "fnv window kernel: %s", cudaGetErrorString(r));
