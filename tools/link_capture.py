@@ -1,11 +1,12 @@
 """Host-link evidence for ncu (tools/profile_r2.sh): one headline step (the
 C3 checkpoint of one 2K-token chunk: K1 + piecewise D2H of 2 x 80 MiB of
-parity into pinned host memory) and one C3 chunk rebuild (H2D of parity row
-0 + K2), each bracketed by cudaProfilerStart/Stop so that
+parity into pinned host memory) one C3 chunk rebuild (H2D of parity row
+0 + K2) and one e2e call (gs_encode_host from pinned host buffers: H2D of the
+8 x 80 MiB data + K1 + D2H of the parity), each bracketed by cudaProfilerStart/Stop so that
 
   ncu --replay-mode app-range \
       --metrics pcie__read_bytes.sum,pcie__write_bytes.sum,gpu__time_duration.sum,... \
-      python tools/link_capture.py --leg encode|rebuild
+      python tools/link_capture.py --leg encode|rebuild|e2e
 
 measures the PCIe bytes and the elapsed time of the whole range -- copies
 and kernels together -- i.e. the achieved D2H / H2D GB/s against the host
@@ -27,7 +28,7 @@ from paper_2605_00831_b200.coding import CodingScheme, ErasurePattern, check, de
 
 def main():
     ap = argparse.ArgumentParser()
-    ap.add_argument("--leg", choices=["encode", "rebuild"], default="encode")
+    ap.add_argument("--leg", choices=["encode", "rebuild", "e2e"], default="encode")
     a = ap.parse_args()
     dev = torch.device("cuda", 0)
     cfg, m = K.LLAMA3_70B, 2048
@@ -60,16 +61,29 @@ def main():
                                         copy.cuda_stream), "rebuild")
     rebuild()
     torch.cuda.synchronize()
+    # e2e: the drop-in host-buffer call (gs_encode_host = ghostserve::encode
+    # semantics): H2D of the 8 x 80 MiB data, K1, D2H of the parity
+    h_kv = kv.cpu().pin_memory()
+    h_par2 = D.pinned_near((2, sl), 0)
+    hslots = L.ptr_array([h_kv[w].data_ptr() for w in range(8)])
+    houts = L.ptr_array([h_par2[i].data_ptr() for i in range(2)])
+
+    def e2e():
+        check(lib.gs_encode_host(pipe.handle, enc.handle, hslots, houts, sl), "e2e")
+    e2e()
+    torch.cuda.synchronize()
     cudart = torch.cuda.cudart()
     cudart.cudaProfilerStart()
-    encode() if a.leg == "encode" else rebuild()
+    {"encode": encode, "rebuild": rebuild, "e2e": e2e}[a.leg]()
     comp.wait_stream(copy)
     torch.cuda.synchronize()
     cudart.cudaProfilerStop()
-    ok = torch.equal(rebuilt, kv[5]) if a.leg == "rebuild" else torch.equal(
-        h_par.to(dev), D.encode(scheme, kv.unsqueeze(0))[0])
-    print(f"link_capture {a.leg}: bytes D2H {2 * sl if a.leg == 'encode' else 0}, "
-          f"H2D {sl if a.leg == 'rebuild' else 0}, ok={ok}")
+    want = D.encode(scheme, kv.unsqueeze(0))[0]
+    ok = (torch.equal(rebuilt, kv[5]) if a.leg == "rebuild" else
+          torch.equal((h_par2 if a.leg == "e2e" else h_par).to(dev), want))
+    d2h = 2 * sl if a.leg in ("encode", "e2e") else 0
+    h2d = {"encode": 0, "rebuild": sl, "e2e": 8 * sl}[a.leg]
+    print(f"link_capture {a.leg}: bytes D2H {d2h}, H2D {h2d}, ok={ok}")
 
 
 if __name__ == "__main__":

@@ -28,8 +28,9 @@ def main():
                      "together), tools/link_capture.py", "legs": {}}
     for p in a.csvs:
         v = load(p)
-        leg = "encode_step (K1 + D2H of 2 x 80 MiB parity)" if "encode" in p else \
-              "chunk_rebuild (H2D of parity row 0 + K2)"
+        leg = ("e2e_call (gs_encode_host: H2D of 8 x 80 MiB data + K1 + D2H of 2 x 80 MiB parity)" if "e2e" in p
+               else "encode_step (K1 + D2H of 2 x 80 MiB parity)" if "encode" in p
+               else "chunk_rebuild (H2D of parity row 0 + K2)")
         ns = v["gpu__time_duration.sum"][0]
         wr, rd = v["pcie__write_bytes.sum"][0], v["pcie__read_bytes.sum"][0]
         out["legs"][leg] = {"range_us": round(ns / 1e3, 1), "pcie_write_bytes (device->host)": int(wr),
