@@ -238,8 +238,7 @@ def test_paged_tile_pages_path_pipelined(model, staging):
 def test_paged_tile_pages_with_block_table(model, block, chunk, staging):
     """The page-per-tile path through a block table (tiles inside one block,
     every token valid), pipelined so pieces start mid-block: parity bit-exact
-    vs the oracle, and identical with the general paged walk
-    (gs_kernels.cuh TileGeom.tile_pages)."""
+    vs the oracle (gs_kernels.cuh TileGeom.tile_pages)."""
     from paper_2605_00831_b200.paged import checkpoint_chunks
     n, k, S = 8, 2, 5
     nblk = chunk // block
