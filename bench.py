@@ -779,6 +779,16 @@ def run_ours(args):
         recovery.update(c4_recovery(torch, dev, comp, copy, pipe))
         if not recovery.get("c4_rebuild_ok", True):
             failures.append("C4 rebuild != original shards")
+        if kern and kern2 and not args.no_c3:
+            # C4 with the reference's semantics: RS(6,2) over a 6-way shard of the same
+            # model, 16K-token prefill (8 chunks), workers 0 and 3 lost: both parity rows
+            # of every chunk are needed, so every entry is uploaded whole and verified in HBM
+            orch4 = c3_orchestrated(torch, dev, link, kern["achieved"] * 8 / 10, kern2["achieved"] * 8 / 9,
+                                    workers=6, k=2, tokens=16384, failed=(0, 3), label="c4")
+            recovery["c4_orchestrated"] = orch4
+            if "plan" in orch4 and (orch4["plan"]["mode"] != "hybrid" or orch4["decoded_chunks"] != orch4["chunks"]
+                                    or not orch4["verified"]):
+                failures.append(f"C4 recovery did not decode every chunk bit-exact: {orch4['plan']}")
     overhead = None
     if rank == 0 and world == 1 and not args.no_overhead:
         overhead = decode_overhead(torch, dev, pipe, args)
@@ -1316,13 +1326,15 @@ def c3_recovery(torch, dev, comp, copy, pipe):
     return out
 
 
-def c3_orchestrated(torch, dev, link, k1_gbs, k2_gbs):
+def c3_orchestrated(torch, dev, link, k1_gbs, k2_gbs, workers: int = 8, k: int = 2, tokens: int = 131072,
+                    failed=(5,), label: str = "c3"):
     """SURVEY §8f-2 with real timings: the reference's checkpoint/recovery
     semantics end to end on the C3 request (Llama-3-70B TP=8, 128K-token
-    prefill = 64 chunks of 2048) through the orchestration mirror:
-    run_prefill_with_checkpointing (K1 + D2H straight into ParityStore
-    entries, FNV-1a seal on host threads) and recover() after worker 5 fails
-    at chunk 64, planned by get_recompute_units (recovery.hpp:58-88) on a
+    prefill = 64 chunks of 2048; or C4: RS(6,2) over a 6-way TP shard of the
+    same model, 16K tokens, workers 0 and 3 lost) through the orchestration
+    mirror: run_prefill_with_checkpointing (K1 + D2H straight into
+    ParityStore entries, FNV-1a seal) and recover() after the failure at the
+    last chunk, planned by get_recompute_units (recovery.hpp:58-88) on a
     CostModel calibrated with this run's measured host link, K1 and K2 rates.
     Reports the plan, the FNV verification time, the batched decode time and
     the wall time to verified, rebuilt bytes."""
@@ -1332,14 +1344,14 @@ def c3_orchestrated(torch, dev, link, k1_gbs, k2_gbs):
     from paper_2605_00831_b200.coding import CodingScheme
     from paper_2605_00831_b200.parity_store import ParityStore
 
-    cfg_m = K.LLAMA3_70B
-    m, tokens = 2048, 131072
+    cfg_m = K.LLAMA3_70B if workers == 8 else K.ModelConfig(80, workers, 128, 2, workers)
+    m = 2048
     free, _ = torch.cuda.mem_get_info(dev)
     sl = K.slice_bytes(cfg_m, m)
-    if free < 64 * 8 * sl + (4 << 30):
-        return {"c3_orchestrated_skipped": "not enough device memory"}
+    if free < (tokens // m) * workers * sl + (4 << 30):
+        return {f"{label}_orchestrated_skipped": "not enough device memory"}
     cost = CostModel.measured(link["h2d"], k1_gbs, k2_gbs)
-    cfg = CheckpointConfig(CodingScheme.reed_solomon(8, 2), m, cfg_m, cost)
+    cfg = CheckpointConfig(CodingScheme.reed_solomon(workers, k), m, cfg_m, cost)
     threads = int(os.environ.get("GS_VERIFY_THREADS", 0)) or max(1, (os.cpu_count() or 1) - 2)
     store = ParityStore(seal_threads=threads)
     store.bind_device(dev.index or 0)
@@ -1353,7 +1365,7 @@ def c3_orchestrated(torch, dev, link, k1_gbs, k2_gbs):
     ck.synchronize()
     # ... and the recovery's device buffers (uploaded parity rows, rebuilt
     # shards, GPU checksum scratch) likewise
-    ck.recover(10, FailureEvent([5], at_chunk=warm.chunks_done), warm.ground_truth, [m] * warm.chunks_done,
+    ck.recover(10, FailureEvent(list(failed), at_chunk=warm.chunks_done), warm.ground_truth, [m] * warm.chunks_done,
                verify_threads=max(1, (os.cpu_count() or 1) - 2))
     del warm
     store.erase_request(10)
@@ -1368,15 +1380,16 @@ def c3_orchestrated(torch, dev, link, k1_gbs, k2_gbs):
     # runs on these VMs); every recovery is checked, the median is reported
     runs = []
     for _ in range(3):
-        res_i = ck.recover(11, FailureEvent([5], at_chunk=n), run.ground_truth, [m] * n, verify_threads=threads)
+        res_i = ck.recover(11, FailureEvent(list(failed), at_chunk=n), run.ground_truth, [m] * n,
+                           verify_threads=threads)
         runs.append(res_i)
         if res_i.plan.mode != "hybrid" or res_i.decoded_chunks != n or not res_i.verified:
             break
     res = sorted(runs, key=lambda x: x.wall_ms)[len(runs) // 2] if all(
         x.plan.mode == "hybrid" and x.decoded_chunks == n and x.verified for x in runs) else runs[-1]
-    out = {"chunks": n, "slice_bytes": sl,
+    out = {"scheme": f"RS({workers},{k})", "failed_workers": list(failed), "chunks": n, "slice_bytes": sl,
            "checkpoint_device_ms": round(run.device_ms, 2),
-           "checkpoint_data_gbs": round(8 * n * sl / (run.device_ms * 1e-3) / 1e9, 2),
+           "checkpoint_data_gbs": round(workers * n * sl / (run.device_ms * 1e-3) / 1e9, 2),
            "checkpoint_sealed_wall_ms": round(t_sealed * 1e3, 1),
            "checkpoint_enqueue_ms": round(t_enq * 1e3, 1),
            "cost_model_measured": {"host_gbs": link["h2d"], "encode_gbs": round(k1_gbs, 1),
@@ -1388,14 +1401,14 @@ def c3_orchestrated(torch, dev, link, k1_gbs, k2_gbs):
            "verify_host_ms": round(res.verify_host_ms, 1), "verify_threads": threads,
            "verify_gpu_chunks": res.verify_gpu_chunks,
            "decode_device_ms": round(res.reconstruct_device_ms, 2), "recover_wall_ms": round(res.wall_ms, 1),
-           "parity_bytes_verified": len(res.plan.reconstruct_ids) * 2 * sl, "verified": res.verified,
+           "parity_bytes_verified": len(res.plan.reconstruct_ids) * k * sl, "verified": res.verified,
            "decoded_chunks": res.decoded_chunks, "corrupt_chunks": res.corrupt_chunks,
            "verify_split": res.verify_split,
            "recover_wall_ms_runs": [round(x.wall_ms, 1) for x in runs],
            "runs_detail": [{"wall_ms": round(x.wall_ms, 1), "verify_ms": round(x.verify_host_ms, 1),
                             "decode_device_ms": round(x.reconstruct_device_ms, 1), "split": x.verify_split}
                            for x in runs],
-           "note": "wall = plan + speculative H2D/K2 overlapped with the FNV verification of the 64 entries "
+           "note": f"wall = plan + speculative H2D/K2 overlapped with the FNV verification of the {n} entries "
                    "(reference semantics: corrupt parity -> full-recompute fallback), median of 3 recoveries of "
                    "the same failure; every chunk's parity row 0 is uploaded (K2 needs it) and hashed on the GPU, "
                    "the rest of each chain is claimed at run time by host threads (continuing the GPU's state) or "
