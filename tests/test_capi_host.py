@@ -302,3 +302,17 @@ def test_host_fnv_bit_sliced_chain_matches_oracle(port):
     finally:
         assert lib.gs_fnv_host_set_simd(1) == hw
     assert lib.gs_fnv1a64(buf.ctypes.data, buf.size, 0xCBF29CE484222325) == want
+
+
+def test_process_wide_controls_without_a_gpu():
+    """The small process-wide entry points behave without a device: ABI
+    version, JIT switch (returns the previous state), JIT quiesce, zero-copy
+    threshold setter, CUDA availability probe."""
+    lib = L.lib()
+    assert lib.gs_abi_version() >= 1
+    prev = lib.gs_set_jit(0)
+    assert prev in (0, 1)
+    assert lib.gs_set_jit(prev) == 0          # the state set just before
+    assert lib.gs_jit_quiesce() == 0
+    assert lib.gs_set_zero_copy_bytes(2 << 20) == 0
+    assert lib.gs_cuda_available() in (0, 1)
