@@ -699,6 +699,7 @@ __device__ __forceinline__ uint32_t sl_maj(uint32_t a, uint32_t b, uint32_t c) {
 struct SlCol {
   uint32_t B[8], X[8];
   uint32_t c12, c23, c34, s4, c45a, c45b, s5, c56a, c56b, c56c, s6, c67a, c67b, c67c, c67d;
+  uint32_t s5a_;  // column 5's known part (two-bit rounds)
   template <int K>
   __device__ __forceinline__ uint32_t g() {  // column K bits other than x_K (known bits pre-reduced)
     if constexpr (K == 0) return 0u;
@@ -897,6 +898,337 @@ __global__ void __cluster_dims__(kWCS, 1, 1) __launch_bounds__(kWT, 2)
   }
 }
 
+// ---------------------------------------------------------------------------
+// Two bits per round (k_fnv_window_sl2, the default; GS_FNV_PAIRS=0 keeps one
+// bit per round). Bit K+1 depends on x_K, i.e. on the carry of bit K into the
+// thread, which the window-level scan only knows later -- so bit K+1 is
+// evaluated for BOTH values of that carry. A thread is then a two-state
+// transducer (f = its bit-K parity, o_s = its bit-(K+1) parity when its
+// incoming bit-K carry is s); transducers compose associatively,
+//   (a then b) = (a.f ^ b.f, o_s = a.o_s ^ b.o_{s ^ a.f}),
+// and a level of items (lanes / warps / CTAs / predecessor windows) composes
+// with bit masks: P = exclusive prefix XOR of the f bits, then the item
+// outputs for start state 0 / 1 are (o0 & ~P) | (o1 & P) / (o1 & ~P) | (o0 & P).
+// A window's transducer does not depend on its entry bits, so it is
+// published at once and the look-back composes predecessors' transducers up
+// to one with published exit bits. One cluster barrier and one look-back per
+// PAIR of bits: four per window instead of eight.
+// ---------------------------------------------------------------------------
+struct Tx {
+  uint32_t f, o0, o1;
+};
+__device__ __forceinline__ Tx tx_then(Tx a, Tx b) {  // a, then b
+  return Tx{a.f ^ b.f, a.o0 ^ (a.f ? b.o1 : b.o0), a.o1 ^ (a.f ? b.o0 : b.o1)};
+}
+__device__ __forceinline__ uint32_t excl_prefix_bits(uint32_t m) {  // bit i = XOR of bits < i
+  return sl_prefix32(m) << 1;
+}
+// Compose the items of a level given as bit masks (bit i = item i, in chain
+// order), restricted to `sel`: the composition of the selected items.
+__device__ __forceinline__ Tx tx_masks(uint32_t fm, uint32_t o0m, uint32_t o1m, uint32_t sel) {
+  fm &= sel;
+  o0m &= sel;
+  o1m &= sel;
+  const uint32_t p = excl_prefix_bits(fm);
+  const uint32_t a0 = (o0m & ~p) | (o1m & p), a1 = (o1m & ~p) | (o0m & p);
+  return Tx{static_cast<uint32_t>(__popc(fm) & 1), static_cast<uint32_t>(__popc(a0) & 1),
+            static_cast<uint32_t>(__popc(a1) & 1)};
+}
+
+// Per pair, the carry-save variables that depend on x_K (hypothesis state).
+template <int K>
+struct SlHyp {
+  uint32_t c23, c45b, s5, c56b, c67d;
+};
+// g_{K+1} for a given x_K plane (and the x_K-dependent carry-save values).
+template <int K>
+__device__ __forceinline__ uint32_t sl_next(SlCol& c, uint32_t xk, SlHyp<K>& h) {
+  if constexpr (K == 0) {
+    return xk;  // column 1 = {x1, x0}
+  } else if constexpr (K == 2) {
+    h.c23 = sl_maj(xk, c.X[1], c.c12);
+    return xk ^ h.c23;  // column 3 = {x3, x2, c23}
+  } else if constexpr (K == 4) {
+    h.c45b = xk & c.s4;
+    h.s5 = c.s5a_ ^ xk ^ h.c45b;
+    h.c56b = sl_maj(c.s5a_, xk, h.c45b);
+    return h.s5;
+  } else {
+    h.c67d = xk & c.s6;
+    return xk ^ c.X[3] ^ c.X[2] ^ c.X[0] ^ c.c67a ^ c.c67b ^ c.c67c ^ h.c67d;
+  }
+}
+// x_K-independent pre-reduction of columns K and K+1 (before the pair).
+template <int K>
+__device__ __forceinline__ uint32_t sl_pre(SlCol& c) {  // returns G_K
+  if constexpr (K == 0) {
+    return 0u;
+  } else if constexpr (K == 2) {
+    return c.X[1] ^ c.c12;
+  } else if constexpr (K == 4) {
+    c.s4 = c.X[3] ^ c.X[0] ^ c.c34;
+    c.c45a = sl_maj(c.X[3], c.X[0], c.c34);
+    c.s5a_ = c.X[1] ^ c.X[0] ^ c.c45a;
+    c.c56a = sl_maj(c.X[1], c.X[0], c.c45a);
+    return c.s4;
+  } else {
+    const uint32_t s6a = c.X[2] ^ c.X[1] ^ c.c56a;
+    c.c67a = sl_maj(c.X[2], c.X[1], c.c56a);
+    const uint32_t s6b = s6a ^ c.c56b ^ c.c56c;
+    c.c67b = sl_maj(s6a, c.c56b, c.c56c);
+    c.s6 = s6b ^ c.X[5];
+    c.c67c = s6b & c.X[5];
+    return c.s6;
+  }
+}
+// Commit the chosen hypothesis and the carries out of column K+1.
+template <int K>
+__device__ __forceinline__ void sl_commit(SlCol& c, uint32_t xk, uint32_t xk1, const SlHyp<K>& h) {
+  c.X[K] = xk;
+  c.X[K + 1] = xk1;
+  if constexpr (K == 0) {
+    c.c12 = xk1 & xk;
+  } else if constexpr (K == 2) {
+    c.c23 = h.c23;
+    c.c34 = sl_maj(xk1, xk, h.c23);
+  } else if constexpr (K == 4) {
+    c.c45b = h.c45b;
+    c.s5 = h.s5;
+    c.c56b = h.c56b;
+    c.c56c = xk1 & h.s5;
+  } else {
+    c.c67d = h.c67d;
+  }
+}
+
+struct WinSharedPair {
+  uint64_t pw[kWT];                  // P^(64 t)
+  uint32_t wm[4][3][kWCS];           // [pair][f, o0, o1][cluster rank]: bit x = warp x of that CTA
+  uint32_t gw;
+  unsigned long long wsum[kWT / 32];
+  uint64_t pblk;
+};
+
+// Window flag word, 7 bits per pair P at 7P: transducer f, o0, o1, valid;
+// exit bits K, K+1, valid.
+template <int P>
+__device__ __forceinline__ void lookback_pair(const uint32_t* flags, uint32_t gw, uint32_t w, uint32_t nc,
+                                              uint64_t h0, uint32_t& eK, uint32_t& eK1) {
+  constexpr int K = 2 * P, B = 7 * P;
+  const int lane = threadIdx.x & 31;
+  Tx acc{0, 0, 0};  // composition of the windows between the search front and w (chain order)
+  uint32_t back = 0;
+  for (;;) {
+    const uint32_t dist = back + lane + 1;  // lane l: predecessor w - dist (nearest first)
+    const bool exists = dist <= w;
+    uint32_t v = 0;
+    if (exists) v = ld_acquire_u32(flags + (gw - dist * nc));
+    const bool have_t = exists && ((v >> (B + 3)) & 1u);
+    const bool have_x = exists && ((v >> (B + 6)) & 1u);
+    const bool start = !exists && dist == w + 1;
+    const uint32_t stop_bal = __ballot_sync(0xFFFFFFFFu, have_x || start);
+    const int first = stop_bal ? __ffs(stop_bal) - 1 : 32;
+    const uint32_t need = first >= 32 ? 0xFFFFFFFFu : ((1u << first) - 1u);
+    const uint32_t ok = __ballot_sync(0xFFFFFFFFu, have_t);
+    if ((ok & need) != need) continue;  // a nearer transducer is not published yet: spin
+    // lanes < first, in chain order (farthest first): bit-reverse the lane masks
+    const uint32_t fm = __brev(__ballot_sync(0xFFFFFFFFu, (v >> B) & 1u) & need);
+    const uint32_t o0m = __brev(__ballot_sync(0xFFFFFFFFu, (v >> (B + 1)) & 1u) & need);
+    const uint32_t o1m = __brev(__ballot_sync(0xFFFFFFFFu, (v >> (B + 2)) & 1u) & need);
+    const Tx blk = tx_masks(fm, o0m, o1m, 0xFFFFFFFFu);
+    acc = tx_then(blk, acc);  // this block is farther in the chain than what acc holds
+    if (first < 32) {
+      const uint32_t ax = __shfl_sync(0xFFFFFFFFu, start ? static_cast<uint32_t>(h0 >> K) : (v >> (B + 4)), first) & 1u;
+      const uint32_t ax1 =
+          __shfl_sync(0xFFFFFFFFu, start ? static_cast<uint32_t>(h0 >> (K + 1)) : (v >> (B + 5)), first) & 1u;
+      eK = ax ^ acc.f;
+      eK1 = ax1 ^ (ax ? acc.o1 : acc.o0);
+      return;
+    }
+    back += 32;
+  }
+}
+
+template <int P>
+__device__ __forceinline__ void win_pair_sl(WinSharedPair& sh, uint32_t* flags, uint32_t gw, uint32_t w, uint32_t nc,
+                                            uint64_t h0, uint32_t rank, SlCol (&G)[2], uint32_t& flag_word) {
+  constexpr int K = 2 * P, B = 7 * P;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  // bit K (independent of the entry bits)
+  uint32_t incK[2];
+#pragma unroll
+  for (int q = 0; q < 2; ++q) incK[q] = sl_prefix32(G[q].B[K] ^ sl_pre<K>(G[q]));
+  const uint32_t pK0 = incK[0] >> 31, fT = pK0 ^ (incK[1] >> 31);
+  const uint32_t relK0 = incK[0] << 1, relK1 = (incK[1] << 1) ^ (0u - pK0);
+  // bit K+1 under both values h of the thread's incoming bit-K carry
+  SlHyp<K> hy[2][2] = {};
+  uint32_t incH[2][2], oT[2];
+#pragma unroll
+  for (int h = 0; h < 2; ++h) {
+#pragma unroll
+    for (int q = 0; q < 2; ++q) {
+      const uint32_t xk = (q == 0 ? relK0 : relK1) ^ (0u - static_cast<uint32_t>(h)) ^ G[q].B[K];
+      incH[h][q] = sl_prefix32(G[q].B[K + 1] ^ sl_next<K>(G[q], xk, hy[h][q]));
+    }
+    oT[h] = (incH[h][0] >> 31) ^ (incH[h][1] >> 31);
+  }
+  // lanes
+  const uint32_t fm = __ballot_sync(0xFFFFFFFFu, fT);
+  const uint32_t o0m = __ballot_sync(0xFFFFFFFFu, oT[0]);
+  const uint32_t o1m = __ballot_sync(0xFFFFFFFFu, oT[1]);
+  const Tx t_lanes = tx_masks(fm, o0m, o1m, (1u << lane) - 1u);
+  const Tx t_warp = tx_masks(fm, o0m, o1m, 0xFFFFFFFFu);
+  if (lane < kWCS) {
+    if (t_warp.f) or_cluster_u32(&sh.wm[P][0][rank], static_cast<uint32_t>(lane), 1u << warp);
+    if (t_warp.o0) or_cluster_u32(&sh.wm[P][1][rank], static_cast<uint32_t>(lane), 1u << warp);
+    if (t_warp.o1) or_cluster_u32(&sh.wm[P][2][rank], static_cast<uint32_t>(lane), 1u << warp);
+  }
+  cluster_sync_all();
+  // warps of this CTA before mine, and the CTAs' totals
+  const Tx t_warps = tx_masks(sh.wm[P][0][rank], sh.wm[P][1][rank], sh.wm[P][2][rank], (1u << warp) - 1u);
+  // CTA r's total computed by lane r of every warp, gathered as masks
+  Tx tc{0, 0, 0};
+  if (lane < kWCS) tc = tx_masks(sh.wm[P][0][lane], sh.wm[P][1][lane], sh.wm[P][2][lane], 0xFFFFFFFFu);
+  const uint32_t cf = __ballot_sync(0xFFFFFFFFu, tc.f) & ((1u << kWCS) - 1u);
+  const uint32_t co0 = __ballot_sync(0xFFFFFFFFu, tc.o0) & ((1u << kWCS) - 1u);
+  const uint32_t co1 = __ballot_sync(0xFFFFFFFFu, tc.o1) & ((1u << kWCS) - 1u);
+  const Tx t_ctas = tx_masks(cf, co0, co1, (1u << rank) - 1u);
+  const Tx t_win = tx_masks(cf, co0, co1, 0xFFFFFFFFu);
+  if (rank == 0 && warp == 0 && lane == 0) {
+    flag_word |= ((t_win.f | (t_win.o0 << 1) | (t_win.o1 << 2)) << B) | (1u << (B + 3));
+    st_release_u32(flags + gw, flag_word);
+  }
+  uint32_t eK, eK1;
+  if (w == 0) {
+    eK = static_cast<uint32_t>(h0 >> K) & 1u;
+    eK1 = static_cast<uint32_t>(h0 >> (K + 1)) & 1u;
+  } else {
+    lookback_pair<P>(flags, gw, w, nc, h0, eK, eK1);
+  }
+  if (rank == 0 && warp == 0 && lane == 0) {
+    const uint32_t xK = eK ^ t_win.f, xK1 = eK1 ^ (eK ? t_win.o1 : t_win.o0);
+    flag_word |= ((xK | (xK1 << 1)) << (B + 4)) | (1u << (B + 6));
+    st_release_u32(flags + gw, flag_word);
+  }
+  // this thread's incoming carries
+  const Tx before = tx_then(tx_then(t_ctas, t_warps), t_lanes);
+  const uint32_t cK = before.f ^ eK;
+  const uint32_t cK1 = (eK ? before.o1 : before.o0) ^ eK1;
+#pragma unroll
+  for (int q = 0; q < 2; ++q) {
+    const uint32_t xk = (q == 0 ? relK0 : relK1) ^ (0u - cK) ^ G[q].B[K];
+    const uint32_t inc = cK ? incH[1][q] : incH[0][q];
+    const uint32_t pre = q == 0 ? 0u : ((cK ? incH[1][0] : incH[0][0]) >> 31);
+    const uint32_t l1 = (inc << 1) ^ (0u - (pre ^ cK1));
+    const uint32_t xk1 = l1 ^ G[q].B[K + 1];
+    SlHyp<K> hs;  // the chosen hypothesis, field by field (no dynamic indexing: registers, not stack)
+    hs.c23 = cK ? hy[1][q].c23 : hy[0][q].c23;
+    hs.c45b = cK ? hy[1][q].c45b : hy[0][q].c45b;
+    hs.s5 = cK ? hy[1][q].s5 : hy[0][q].s5;
+    hs.c56b = cK ? hy[1][q].c56b : hy[0][q].c56b;
+    hs.c67d = cK ? hy[1][q].c67d : hy[0][q].c67d;
+    sl_commit<K>(G[q], xk, xk1, hs);
+  }
+}
+
+__global__ void __cluster_dims__(kWCS, 1, 1) __launch_bounds__(kWT, 2)
+    k_fnv_window_sl2(const FnvJob j, uint64_t h0, const uint64_t* __restrict__ h0s, uint32_t nc, uint32_t total_windows,
+                    uint32_t* counter, uint32_t* flags, unsigned long long* __restrict__ out) {
+  __shared__ WinSharedPair sh;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const uint32_t rank = cluster_rank();
+  sh.pw[tid] = pow64(kFnvP, static_cast<uint64_t>(kFPer) * tid);
+  cluster_sync_all();  // every CTA of the cluster has started before rank 0 writes into their smem
+  for (;;) {
+    if (tid < 4 * 3 * kWCS) (&sh.wm[0][0][0])[tid] = 0;  // this window's transducer words
+    if (rank == 0 && tid == 0) {
+      const uint32_t g = atomicAdd(counter, 1u);
+      for (int r = 0; r < kWCS; ++r) st_cluster_u32(&sh.gw, static_cast<uint32_t>(r), g);
+    }
+    cluster_sync_all();
+    const uint32_t gw = sh.gw;
+    if (gw >= total_windows) break;
+    const uint32_t w = gw / nc, c = gw - w * nc;
+    const uint64_t hc = h0s ? h0s[c] : h0;
+    const uint64_t cta0 = static_cast<uint64_t>(w) * kWin + static_cast<uint64_t>(rank) * kWB;
+    const uint64_t pos0 = cta0 + static_cast<uint64_t>(tid) * kFPer;
+    SlCol G[2];
+    {
+      uint4 d[4];
+      load_groups(j, c, pos0, d);
+#pragma unroll
+      for (int q = 0; q < 2; ++q) {
+        uint32_t wv[8] = {d[2 * q].x, d[2 * q].y, d[2 * q].z, d[2 * q].w,
+                          d[2 * q + 1].x, d[2 * q + 1].y, d[2 * q + 1].z, d[2 * q + 1].w};
+        sl_to_planes(wv);
+#pragma unroll
+        for (int b = 0; b < 8; ++b) G[q].B[b] = wv[b];
+      }
+    }
+    uint32_t fw = 0;
+    win_pair_sl<0>(sh, flags, gw, w, nc, hc, rank, G, fw);
+    win_pair_sl<1>(sh, flags, gw, w, nc, hc, rank, G, fw);
+    win_pair_sl<2>(sh, flags, gw, w, nc, hc, rank, G, fw);
+    win_pair_sl<3>(sh, flags, gw, w, nc, hc, rank, G, fw);
+    // low bytes s = x ^ b back to byte lanes; the data re-read (cache-resident)
+    uint4 s[4], d[4];
+#pragma unroll
+    for (int q = 0; q < 2; ++q) {
+      uint32_t wv[8];
+#pragma unroll
+      for (int b = 0; b < 8; ++b) wv[b] = G[q].X[b] ^ G[q].B[b];
+      sl_from_planes(wv);
+      s[2 * q] = make_uint4(wv[0], wv[1], wv[2], wv[3]);
+      s[2 * q + 1] = make_uint4(wv[4], wv[5], wv[6], wv[7]);
+    }
+    const int nvalid = load_groups(j, c, pos0, d);
+    // sum over the thread's bytes of d_i P^(tend - i), four 16-byte Horner chains
+    uint64_t accq[4] = {0, 0, 0, 0};
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      if (q < nvalid) {
+#pragma unroll
+        for (int x = 0; x < 4; ++x) {
+          const uint32_t sw = wd(s[q], x), xw = sw ^ wd(d[q], x);
+#pragma unroll
+          for (int by = 0; by < 4; ++by) {
+            const int64_t di = static_cast<int64_t>((xw >> (8 * by)) & 0xFFu) -
+                               static_cast<int64_t>((sw >> (8 * by)) & 0xFFu);
+            accq[q] = (accq[q] + static_cast<uint64_t>(di)) * kFnvP;
+          }
+        }
+      }
+    }
+    constexpr uint64_t kP16 = [] {
+      uint64_t r = 1;
+      for (int i = 0; i < 16; ++i) r *= kFnvP;
+      return r;
+    }();
+    uint64_t acc = 0;
+#pragma unroll
+    for (int q = 0; q < 4; ++q)
+      if (q < nvalid) acc = acc * kP16 + accq[q];
+    const uint64_t cend = cta0 + kWB;
+    if (tid == 0) sh.pblk = cend <= j.n ? pow64(kFnvP, j.n - cend) : 0;
+    __syncthreads();
+    uint64_t contrib = 0;
+    if (nvalid > 0) {
+      const uint64_t tend = pos0 + 16u * nvalid;
+      contrib = acc * (cend <= j.n ? sh.pblk * sh.pw[kWT - 1 - tid] : pow64(kFnvP, j.n - tend));
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) contrib += __shfl_xor_sync(0xFFFFFFFFu, contrib, o);
+    if (lane == 0) sh.wsum[warp] = contrib;
+    __syncthreads();
+    if (tid == 0) {
+      uint64_t sum = 0;
+#pragma unroll
+      for (int x = 0; x < kWT / 32; ++x) sum += sh.wsum[x];
+      atomicAdd(out + c, static_cast<unsigned long long>(sum));
+    }
+  }
+}
+
 const bool g_fnv_legacy = [] {
   const char* e = std::getenv("GS_FNV_LEGACY");
   return e && std::atoi(e) != 0;
@@ -904,6 +1236,10 @@ const bool g_fnv_legacy = [] {
 const bool g_fnv_bytes = [] {  // the byte-lane window rounds instead of the bit-sliced ones (A/B)
   const char* e = std::getenv("GS_FNV_WINDOW_BYTES");
   return e && std::atoi(e) != 0;
+}();
+const bool g_fnv_pairs = [] {  // bit-sliced rounds two bits at a time (GS_FNV_PAIRS=0: one bit, A/B)
+  const char* e = std::getenv("GS_FNV_PAIRS");
+  return !(e && std::atoi(e) == 0);
 }();
 int g_win_clusters = 0;
 
@@ -1001,6 +1337,10 @@ static int fnv_device(const void* const* bufs, int n_chains, int k, uint64_t len
           k_fnv_window<<<clusters * kWCS, kWT, 0, st>>>(j, h0, d_h0 ? d_h0 + c0 : nullptr, static_cast<uint32_t>(cnt),
                                                        total, ctl, ctl + 1,
                                                        reinterpret_cast<unsigned long long*>(d_out) + c0);
+        else if (g_fnv_pairs)
+          k_fnv_window_sl2<<<clusters * kWCS, kWT, 0, st>>>(j, h0, d_h0 ? d_h0 + c0 : nullptr,
+                                                           static_cast<uint32_t>(cnt), total, ctl, ctl + 1,
+                                                           reinterpret_cast<unsigned long long*>(d_out) + c0);
         else
           k_fnv_window_sl<<<clusters * kWCS, kWT, 0, st>>>(j, h0, d_h0 ? d_h0 + c0 : nullptr,
                                                           static_cast<uint32_t>(cnt), total, ctl, ctl + 1,

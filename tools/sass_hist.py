@@ -21,7 +21,8 @@ KERNELS = [
     ("K1 bulk (TMA smem ring) RS(8,2) encode", "gs_special_enc.o", r"k_apply_special_bulkINS_7EncSpecILi2ELi8ELi2EEE"),
     ("K1 paged RS(8,2) encode", "gs_special_enc.o", r"k_apply_specialINS_7EncSpecILi2ELi8ELi2EEELi488ELi1ELb1E"),
     ("K2 RS(8,2) lost {5}", "gs_special_dec_kreedsolomon_8_2_e1.o", r"k_apply_specialINS_7DecSpecILi2ELi8ELi2ELm32EEELi488ELi1ELb0E"),
-    ("GPU FNV-1a window, bit-sliced rounds (default)", "gs_fnv_gpu.o", r"k_fnv_window_sl"),
+    ("GPU FNV-1a window, bit-sliced, two bits per round (default)", "gs_fnv_gpu.o", r"k_fnv_window_sl2"),
+    ("GPU FNV-1a window, bit-sliced, one bit per round (GS_FNV_PAIRS=0)", "gs_fnv_gpu.o", r"k_fnv_window_slENS"),
     ("GPU FNV-1a window, byte-lane rounds (GS_FNV_WINDOW_BYTES=1)", "gs_fnv_gpu.o", r"k_fnv_windowENS"),
     ("GPU FNV-1a legacy pair pass (round 1)", "gs_fnv_gpu.o", r"k_fnv_pairILi2E"),
     ("RDP(p=11) rebuild of columns {0,10}, pipelined", "gs_rdp_pairs_p11_i0.o", r"k_rdp_recover_bulkILi488ELi11ELi0ELi10EE"),
