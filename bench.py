@@ -454,7 +454,10 @@ def run_ours(args):
     pg = PeerGroup() if world > 1 else None
     bases = [pg.share(ring[b]) if pg else [ring[b].data_ptr()] for b in range(RING)]
     h_parity = D.pinned_near((S, K_PARITY, SLICE), local)   # on the GPU's NUMA node
-    pipe = D.Pipeline(local, 256 << 20)
+    # staging ring: 320 MiB = 4 slots x 2 parity rows x 40 MiB, so a C3 shard (80 MiB) is two
+    # pieces -- K1 of piece 2 under the D2H of piece 1 (256 MiB: three pieces of 32/32/16 MiB,
+    # 219.6 vs 223 GB/s, K1 0.93 vs 0.94 of peak; one 80 MiB piece: 211 GB/s, no overlap)
+    pipe = D.Pipeline(local, int(os.environ.get("GS_BENCH_STAGING_MIB", "320")) << 20)
     comp = torch.cuda.Stream(device=dev)
     copy = torch.cuda.Stream(device=dev)
     enc = encoder(scheme)
