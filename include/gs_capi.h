@@ -314,6 +314,27 @@ uint64_t gs_parity_checksum(const void* const* parity, int k, size_t len);
  * out[c] = checksum of parity[c*k .. c*k+k-1]. */
 int gs_parity_checksum_batch(const void* const* parity, int n_chunks, int k, size_t len,
                              int threads, uint64_t* out);
+/* Continue m independent FNV-1a chains, one segment each, on up to `threads`
+ * host threads: h_out[q] = fnv1a64(bufs[q][0..lens[q]), h_in[q]) (h_out may
+ * alias h_in; a zero length passes the state through). One round of the
+ * striped verification relay (peer.py chain_striped): at N>1 every rank holds
+ * a byte range of each parity row, and a chunk's checksum (ParityChunk::seal,
+ * parity_store.hpp:19-53) is one chain through the ranks' ranges in order. */
+int gs_fnv1a64_continue_batch(const void* const* bufs, const uint64_t* lens, const uint64_t* h_in,
+                              uint64_t* h_out, int m, int threads);
+/* The same relay without rounds, for the ranks of ONE node: `board` is host
+ * memory shared by the ranks' processes (gs_relay_board_bytes(n_chunks, k,
+ * world) bytes, zeroed once), holding one tagged chain state per (chunk,
+ * chain position). Every rank calls gs_fnv_relay with the same `epoch` (> 0,
+ * a new one per call, calls on one board separated by a barrier) and rows[c*k
+ * + i] = its range of parity row i of chunk c (`len` bytes); its `threads`
+ * continue its segments as their predecessors' states appear and sums[c]
+ * receives chunk c's checksum on every rank. A peer that does not deliver
+ * within `timeout_s` seconds (<= 0: 60) makes the call fail with
+ * GS_RUNTIME_ERROR. */
+uint64_t gs_relay_board_bytes(int n_chunks, int k, int world);
+int gs_fnv_relay(void* board, uint64_t epoch, int rank, int world, const void* const* rows, uint64_t len,
+                 int n_chunks, int k, uint64_t h0, int threads, double timeout_s, uint64_t* sums);
 /* The same FNV-1a on the GPU, bit-exact (gs_fnv_gpu.cu): chain c is the k
  * device buffers bufs[c*k .. c*k+k-1] of `len` bytes each, concatenated in
  * order and hashed from h0 (0xcbf29ce484222325 = ParityChunk checksum);

@@ -80,6 +80,9 @@ SIGNATURES = {
     "gs_fnv_host_simd": (_i, []),
     "gs_fnv_host_set_simd": (_i, [_i]),
     "gs_parity_checksum_batch": (_i, [_vpp, _i, _i, _sz, _i, _u64p]),
+    "gs_fnv1a64_continue_batch": (_i, [_vpp, _u64p, _u64p, _u64p, _i, _i]),
+    "gs_relay_board_bytes": (_u64, [_i, _i, _i]),
+    "gs_fnv_relay": (_i, [_vp, _u64, _i, _i, _vpp, _u64, _i, _i, _u64, _i, C.c_double, _u64p]),
     "gs_fnv1a64_device": (_i, [_vpp, _i, _i, _u64, _u64, _vp, _vp]),
     "gs_parity_upload_checksum": (_i, [_vpp, _i, _i, _u64, _vpp, _vp, _vp, _vp]),
     "gs_parity_offload_sealed": (_i, [_vpp, _i, _i, _u64, _vpp, _vp, _vp, _vp]),

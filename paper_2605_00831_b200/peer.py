@@ -7,9 +7,12 @@ parity over that GPU's single PCIe link. Here every rank g encodes the byte
 range g of ALL shards -- reading the ranges it does not own straight out of
 the owners' HBM over NVLink inside K1 -- and D2H's parity range g on its own
 host link. No reduction is involved (NCCL has no GF(2^8) op); the only
-exchange is the peer loads, fused into the kernel. Recovery mirrors it: rank
-g uploads parity range g, pulls range g of the survivors and stores range g
-of the rebuilt shard directly into the replacement GPU's KV buffer.
+exchange on the data path is the peer loads, fused into the kernel. Recovery
+mirrors it: rank g uploads parity range g, pulls range g of the survivors and
+stores range g of the rebuilt shard directly into the replacement GPU's KV
+buffer. The entries' checksums (one FNV-1a chain over a chunk's whole parity)
+are relayed through the ranks' ranges: 8-byte chain states, one small
+all-gather per round (chain_striped).
 
 Layout: with W ranks and n TP workers (W | n), rank r holds workers
 [r*n/W, (r+1)*n/W) as a tensor [S, n/W, L] (S stripes = requests x chunks).
@@ -17,8 +20,9 @@ Layout: with W ranks and n TP workers (W | n), rank r holds workers
 from __future__ import annotations
 
 import ctypes as C
+import os
 from dataclasses import dataclass
-from typing import Dict, List, Optional, Sequence, Tuple
+from typing import Callable, Dict, List, Optional, Sequence, Tuple
 
 from . import _lib as L
 from .coding import CodeKind, CodingScheme, ErasurePattern, InvalidArgument, check, decoder, encoder
@@ -238,6 +242,157 @@ def plan_reconstruct_striped(scheme: CodingScheme, layout: ShardLayout, bases: S
     return StripedCall(L.lib().gs_reconstruct_upload,
                        (pipeline.handle, dec.handle, layout.stripes, L.ptr_array(full), L.ptr_array(outs), ln),
                        off, ln)
+
+
+FNV_OFFSET = 0xcbf29ce484222325  # ParityChunk checksum seed (parity_store.hpp:19-53)
+
+
+def dist_exchange(group=None) -> Callable:
+    """Token exchange for chain_striped over torch.distributed (a CPU-tensor
+    backend: gloo). Returns ex(local [m] uint64) -> [world, m] uint64."""
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+
+    world = dist.get_world_size(group)
+
+    def ex(local):
+        t = torch.from_numpy(np.ascontiguousarray(local).view(np.int64).copy())
+        parts = [torch.empty_like(t) for _ in range(world)]
+        dist.all_gather(parts, t, group=group)
+        return np.stack([p.numpy() for p in parts]).view(np.uint64)
+
+    return ex
+
+
+def chain_striped(rows: Sequence[int], length: int, n_chunks: int, k: int, rank: int, world: int,
+                  exchange: Callable, threads: int = 0, h0: int = FNV_OFFSET) -> List[int]:
+    """ParityChunk checksums of chunks whose parity is byte-range striped over
+    the ranks: the reference seals a chunk with ONE FNV-1a chain over its k
+    rows in order (ParityChunk::compute_checksum, parity_store.hpp:19-53;
+    verified on get, :92-101, before recover decodes, recovery.hpp:269-296),
+    so at N>1 the chain runs through the ranks' ranges: (row 0, rank 0),
+    (row 0, rank 1), ..., (row k-1, rank W-1). Every rank runs this with
+    `rows[c*k + i]` = the host address of ITS range of parity row i of chunk c
+    (`length` bytes, 0 for an empty range) and gets every chunk's checksum.
+
+    Wavefront relay: chunk c enters the ring `c mod W` rounds late, so in
+    round t chunk c is at chain position p = t - (c mod W) on rank p mod W --
+    every rank continues n_chunks/W chains per round (host threads,
+    gs_fnv1a64_continue_batch) and one all-gather of the 8-byte states hands
+    them to the next rank. k*W + W - 1 rounds; a rank's host work is its own
+    bytes only. The states passed on are plain FNV states: no hypotheses."""
+    import numpy as np
+
+    if n_chunks <= 0:
+        return []
+    npos = k * world
+    state = np.full(n_chunks, h0 & 0xFFFFFFFFFFFFFFFF, dtype=np.uint64)
+    if threads <= 0:
+        threads = max(1, (os.cpu_count() or 1) // world)
+    lib = L.lib()
+    for t in range(npos + world - 1):
+        mine, owner = [], np.full(n_chunks, -1, dtype=np.int64)
+        for c in range(n_chunks):
+            p = t - (c % world)
+            if 0 <= p < npos:
+                owner[c] = p % world
+                if p % world == rank:
+                    mine.append((c, p // world))
+        if mine:
+            m = len(mine)
+            bufs = L.ptr_array([rows[c * k + i] if length else None for c, i in mine])
+            lens = (C.c_uint64 * m)(*([length] * m))
+            hin = (C.c_uint64 * m)(*[int(state[c]) for c, _ in mine])
+            hout = (C.c_uint64 * m)()
+            check(lib.gs_fnv1a64_continue_batch(bufs, lens, hin, hout, m, threads), "chain_striped")
+            for q, (c, _) in enumerate(mine):
+                state[c] = hout[q]
+        if world > 1:
+            got = exchange(state)
+            act = owner >= 0
+            state[act] = got[owner[act], np.nonzero(act)[0]]
+    return [int(x) for x in state]
+
+
+def verify_striped(rows: Sequence[int], length: int, n_chunks: int, k: int, rank: int, world: int,
+                   exchange, expected: Sequence[int], threads: int = 0) -> List[bool]:
+    """ParityStore::get's check at N>1: chunk c's striped parity is intact iff
+    its relayed checksum equals the sealed one (every rank gets the same
+    verdicts). `exchange`: a round exchange (dist_exchange) or a RelayBoard."""
+    if isinstance(exchange, RelayBoard):
+        got = exchange.chain(rows, length, n_chunks, k, threads=threads)
+    else:
+        got = chain_striped(rows, length, n_chunks, k, rank, world, exchange, threads)
+    return [g == (e & 0xFFFFFFFFFFFFFFFF) for g, e in zip(got, expected)]
+
+
+class RelayBoard:
+    """chain_striped without rounds for the ranks of one node: the chain states
+    go through a board in host memory the ranks' processes share (a /dev/shm
+    file mapped by every rank, unlinked once all have it), and each rank's
+    threads continue its segments as soon as their predecessors' states
+    appear (gs_fnv_relay). Collective: construct, chain() and close() on
+    every rank of `group` in the same order."""
+
+    def __init__(self, max_chunks: int, k: int, group=None, timeout_s: float = 120.0):
+        import mmap
+        import uuid
+
+        import torch.distributed as dist
+
+        self.dist, self.group, self.timeout_s = dist, group, timeout_s
+        self.rank = dist.get_rank(group)
+        self.world = dist.get_world_size(group)
+        self.slots = max_chunks * k
+        size = int(L.lib().gs_relay_board_bytes(max_chunks, k, self.world))
+        if size == 0:
+            raise InvalidArgument("RelayBoard: bad shape")
+        name = [f"/dev/shm/gs-relay-{os.getpid()}-{uuid.uuid4().hex[:12]}" if self.rank == 0 else None]
+        dist.broadcast_object_list(name, src=dist.get_global_rank(group, 0) if group is not None else 0,
+                                   group=group)
+        self.path = name[0]
+        if self.rank == 0:
+            fd = os.open(self.path, os.O_CREAT | os.O_EXCL | os.O_RDWR, 0o600)
+            os.ftruncate(fd, size)  # zero-filled: every tag starts at epoch 0
+            os.close(fd)
+        dist.barrier(group=group)
+        fd = os.open(self.path, os.O_RDWR)
+        try:
+            self._mm = mmap.mmap(fd, size)
+        finally:
+            os.close(fd)
+        self._view = (C.c_char * size).from_buffer(self._mm)
+        self.addr = C.addressof(self._view)
+        dist.barrier(group=group)
+        if self.rank == 0:
+            os.unlink(self.path)
+        self.epoch = 0
+
+    def chain(self, rows: Sequence[int], length: int, n_chunks: int, k: int, threads: int = 0,
+              h0: int = FNV_OFFSET) -> List[int]:
+        """chain_striped's result (every chunk's checksum, on every rank)."""
+        if n_chunks * k > self.slots:
+            raise InvalidArgument(f"RelayBoard: {n_chunks} x {k} segments exceed the board's {self.slots}")
+        if n_chunks <= 0:
+            return []
+        if threads <= 0:
+            threads = max(1, (os.cpu_count() or 1) // self.world)
+        self.epoch += 1
+        sums = (C.c_uint64 * n_chunks)()
+        bufs = L.ptr_array(list(rows) if length else [])
+        st = L.lib().gs_fnv_relay(self.addr, self.epoch, self.rank, self.world, bufs, length, n_chunks, k,
+                                  h0 & 0xFFFFFFFFFFFFFFFF, threads, self.timeout_s, sums)
+        # the next call re-tags the slots: nobody may still be reading this epoch
+        self.dist.barrier(group=self.group)
+        check(st, "fnv_relay")
+        return list(sums)
+
+    def close(self) -> None:
+        if getattr(self, "_mm", None) is not None:
+            del self._view
+            self._mm.close()
+            self._mm = None
 
 
 def reconstruct_striped(scheme: CodingScheme, layout: ShardLayout, bases: Sequence[int], rank: int,

@@ -100,6 +100,90 @@ def test_striped_partition_reassembles_parity_cpu():
     _run(_cpu_worker)
 
 
+def _relay_worker(rank, world, port, q, length=5 * 4096 + 123, chunks=7, k=2):
+    """chain_striped: every rank holds only its byte range of each parity row;
+    the relayed checksums equal ParityChunk::compute_checksum of the whole
+    rows (oracle), on every rank; a flipped byte fails exactly its chunk."""
+    import sys
+    sys.path.insert(0, ROOT)
+    try:
+        from paper_2605_00831_b200.peer import (RelayBoard, chain_striped, dist_exchange, stripe_range,
+                                                verify_striped)
+        _init(rank, world, port)
+        rows = [splitmix_bytes(7000 + r, length) for r in range(chunks * k)]
+        want = [O.port().parity_checksum(rows[c * k:(c + 1) * k]) for c in range(chunks)]
+        off, ln = stripe_range(length, rank, world)
+        local = [np.ascontiguousarray(r[off:off + ln]) for r in rows]
+        ptrs = [a.ctypes.data if ln else 0 for a in local]
+        ex = dist_exchange()
+        board = RelayBoard(chunks + 3, k)
+        got = chain_striped(ptrs, ln, chunks, k, rank, world, ex, threads=2)
+        assert got == want, (rank, got, want)
+        for threads in (1, 3):  # the shared-memory relay, repeated on one board (epochs)
+            assert board.chain(ptrs, ln, chunks, k, threads=threads) == want, (rank, threads)
+        assert board.chain(ptrs[:2 * k], ln, 2, k) == want[:2]
+        ok = verify_striped(ptrs, ln, chunks, k, rank, world, ex, want, threads=3)
+        assert all(ok)
+        # corrupt one byte of chunk 4, row 1, in the LAST rank's range: every rank must
+        # see chunk 4 (and only chunk 4) fail
+        if rank == world - 1 and ln:
+            local[4 * k + 1][ln // 2] ^= 0x5A
+        dist.barrier()
+        last = stripe_range(length, world - 1, world)[1]
+        expect = [c != 4 or last == 0 for c in range(chunks)]
+        ok = verify_striped(ptrs, ln, chunks, k, rank, world, ex, want, threads=1)
+        assert ok == expect, (rank, ok)
+        assert verify_striped(ptrs, ln, chunks, k, rank, world, board, want, threads=2) == expect
+        board.close()
+        dist.barrier()
+        dist.destroy_process_group()
+        q.put((rank, "ok"))
+    except Exception as e:  # pragma: no cover - reported to the parent
+        q.put((rank, repr(e)))
+
+
+def test_striped_checksum_relay_cpu():
+    _run(_relay_worker)
+
+
+def test_striped_checksum_relay_three_ranks_ragged_cpu():
+    # 3 ranks over 5 pages + 123 bytes: 4 KiB-aligned ranges of unequal length
+    _run(_relay_worker, world=3)
+
+
+def test_striped_checksum_relay_single_rank():
+    import sys
+    sys.path.insert(0, ROOT)
+    from paper_2605_00831_b200.peer import chain_striped
+    rows = [splitmix_bytes(90 + r, 3000 + r) for r in range(6)]
+    # one rank: the chain is plain ParityChunk::compute_checksum (equal row lengths)
+    rows = [r[:3000] for r in rows]
+    ptrs = [r.ctypes.data for r in rows]
+    got = chain_striped(ptrs, 3000, 3, 2, 0, 1, exchange=None, threads=2)
+    assert got == [O.port().parity_checksum(rows[2 * c:2 * c + 2]) for c in range(3)]
+    assert chain_striped([], 0, 0, 2, 0, 1, exchange=None) == []
+
+
+def test_relay_board_times_out_without_the_peer():
+    """A rank whose predecessor never delivers fails (GS_RUNTIME_ERROR) after the
+    timeout instead of spinning forever; rank 0 of a 2-rank relay alone can
+    only do its own row-0 segments."""
+    import sys
+    sys.path.insert(0, ROOT)
+    from paper_2605_00831_b200 import _lib as L
+    lib = L.lib()
+    nbytes = lib.gs_relay_board_bytes(3, 2, 2)
+    assert nbytes == 3 * 2 * 2 * 16 and lib.gs_relay_board_bytes(3, 0, 2) == 0
+    board = (C.c_uint8 * nbytes)()
+    rows = [splitmix_bytes(r, 4096) for r in range(6)]
+    ptrs = L.ptr_array([r.ctypes.data for r in rows])
+    sums = (C.c_uint64 * 3)()
+    st = lib.gs_fnv_relay(board, 1, 1, 2, ptrs, 4096, 3, 2, 0xcbf29ce484222325, 2, 0.2, sums)
+    assert st == L.GS_RUNTIME_ERROR and b"timed out" in lib.gs_last_error()
+    assert lib.gs_fnv_relay(board, 0, 0, 2, ptrs, 4096, 3, 2, 1, 1, 0.2, sums) == L.GS_INVALID_ARGUMENT
+    assert lib.gs_fnv_relay(board, 2, 2, 2, ptrs, 4096, 3, 2, 1, 1, 0.2, sums) == L.GS_INVALID_ARGUMENT
+
+
 def _enable_peers(rank, world):
     """Distinct devices: peer access both ways (gs_peer_enable), on top of the
     lazy peer access the IPC mapping requests (cudaIpcMemLazyEnablePeerAccess)."""
@@ -146,6 +230,11 @@ def _gpu_worker(rank, world, port, q, distinct=False):
             want = O.port().encode(O.RS, N, K, _shards(s))
             for i in range(K):
                 assert np.array_equal(full[s, i], want[i]), (rank, s, i)
+        # the entries' seal at N>1: checksums relayed through the ranks' ranges of
+        # the pinned slabs equal ParityChunk::compute_checksum of the whole parity
+        from paper_2605_00831_b200.peer import chain_striped, dist_exchange
+        sums = chain_striped([p + off for p in D.row_ptrs(h_par)], ln, S, K, rank, world, dist_exchange())
+        assert sums == [O.port().parity_checksum(list(full[s])) for s in range(S)], rank
         # every rank holds the full parity in its host slab now (stands in for
         # the shared host tier); lose worker 5 (owned by the last rank), zero
         # its buffer, rebuild striped: each rank writes its byte range of the
