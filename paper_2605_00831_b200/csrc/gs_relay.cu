@@ -95,19 +95,22 @@ int gs_fnv_relay(void* board, uint64_t epoch, int rank, int world, const void* c
   const auto deadline = std::chrono::steady_clock::now() +
                         std::chrono::microseconds(static_cast<int64_t>((timeout_s > 0 ? timeout_s : 60.0) * 1e6));
   std::atomic<int> next{0}, failed{0};
+  // A segment takes milliseconds, so a waiting thread backs off to short
+  // sleeps after a brief spin: the ranks' relays share the node's cores, and a
+  // spinning waiter would take cycles from the threads it is waiting for.
   auto await = [&](RelaySlot& s) -> bool {
     for (uint32_t spin = 0;; ++spin) {
       if (__atomic_load_n(&s.tag, __ATOMIC_ACQUIRE) == epoch) return true;
       if (failed.load(std::memory_order_relaxed)) return false;
-      if ((spin & 1023) == 1023) {
-        if (std::chrono::steady_clock::now() > deadline) {
-          failed.store(1);
-          return false;
-        }
-        std::this_thread::yield();
-      } else {
+      if (spin < 512) {
         __builtin_ia32_pause();
+        continue;
       }
+      if ((spin & 63) == 0 && std::chrono::steady_clock::now() > deadline) {
+        failed.store(1);
+        return false;
+      }
+      std::this_thread::sleep_for(std::chrono::microseconds(20));
     }
   };
   auto work = [&] {
