@@ -773,10 +773,12 @@ def run_ours(args):
         recovery.update(c3_recovery_striped(torch, dist, dev, comp, copy, pipe, rank, world, shared, barrier))
         recovery_ms = recovery.get("c3_verified_ms")
         recovery["recovery_ms_is"] = ("C3 full-shard recovery striped over the ranks, FNV-verified: every "
-                                      "chunk's sealed checksum re-chained through the ranks' byte ranges on "
-                                      "their host threads (peer.RelayBoard) under the striped parity H2D "
-                                      "(every host link) + K2 (survivors over NVLink, P2P store); wall time, "
-                                      "max over ranks (recovery.c3_verified_ms; raw rebuild c3_full_shard_ms)")
+                                      "chunk's sealed checksum re-chained through the ranks' byte ranges "
+                                      "(peer.RelayBoard: row 0 on the GPUs as its range lands in HBM, row 1 on "
+                                      "host threads) under the striped parity H2D (every host link) + K2 "
+                                      "(survivors over NVLink, P2P store); wall time, max over ranks "
+                                      "(recovery.c3_verified_ms; host-only relay c3_verified_host_ms; raw "
+                                      "rebuild c3_full_shard_ms)")
         if not recovery.get("c3_rebuild_ok", True):
             failures.append("striped C3 rebuild != original shard")
     if rank == 0 and world == 1 and not args.no_c4:
@@ -1437,12 +1439,12 @@ def c3_recovery_striped(torch, dist, dev, comp, copy, pipe, rank, world, shared,
 
     Verified (the reference's semantics, recovery.hpp:269-296): the
     checkpoint's parity entries are sealed with ParityChunk checksums computed
-    by the striped relay (peer.chain_striped: one FNV-1a chain per chunk
-    through the ranks' byte ranges), and the recovery re-runs that relay over
-    the host slabs on every rank's host threads WHILE the striped H2D + K2
-    runs (chain states through a shared host board, peer.RelayBoard); a
-    chunk whose checksum differs is not used. `c3_verified_ms` = wall
-    time to rebuilt AND verified, max over ranks."""
+    by the striped relay (one FNV-1a chain per chunk through the ranks' byte
+    ranges, states passed through a shared host board, peer.RelayBoard), and
+    the recovery re-runs that relay WHILE the striped H2D + K2 runs -- row 0
+    on the GPUs as it lands in HBM (K2 reads it there), row 1 on host
+    threads; a chunk whose checksum differs is not used. `c3_verified_ms` =
+    wall time to rebuilt AND verified, max over ranks."""
     from paper_2605_00831_b200 import device as D
     from paper_2605_00831_b200 import kv_layout as K
     from paper_2605_00831_b200.coding import CodingScheme, ErasurePattern
@@ -1451,6 +1453,7 @@ def c3_recovery_striped(torch, dist, dev, comp, copy, pipe, rank, world, shared,
     from paper_2605_00831_b200 import _lib as L
     from paper_2605_00831_b200.peer import PeerGroup, ShardLayout, plan_encode_striped, plan_reconstruct_striped
     from paper_2605_00831_b200.peer import RelayBoard, chain_striped, stripe_range, verify_striped
+    from paper_2605_00831_b200.peer import plan_reconstruct_striped_device
     from paper_2605_00831_b200.peer import dist_exchange as chain_exchange
 
     cfg = K.LLAMA3_70B
@@ -1520,6 +1523,31 @@ def c3_recovery_striped(torch, dist, dev, comp, copy, pipe, rank, world, shared,
             full[:, o:o + arr.shape[1]] = arr
         seal_ok = seal_ok and sums[0] == L.lib().gs_parity_checksum(L.ptr_array([full[i].ctypes.data for i in range(k)]), k, sl)
     del parts
+    # the checkpoint sealed on the GPUs: K1 into HBM, D2H of this rank's range on
+    # `copy`, and the checksum relay over the rows still in HBM on a third stream
+    # (gs_fnv_relay_device with every row on the GPU)
+    relay_stream = torch.cuda.Stream(device=dev)
+    gpu_relay = ln % 16 == 0 and ln > 0
+    ckpt_sealed_ms = None
+    if gpu_relay:
+        d_par = torch.empty((chunks, k, ln), dtype=torch.uint8, device=dev)
+        k1_dev = plan_encode_striped(scheme, layout, bases, rank, parity_out=d_par)
+        drows = D.row_ptrs(d_par)
+
+        def sealed_checkpoint():
+            k1_dev.run(comp.cuda_stream)
+            k1_done = torch.cuda.Event()
+            k1_done.record(comp)
+            copy.wait_event(k1_done)
+            with torch.cuda.stream(copy):
+                h_par[:, :, :ln].copy_(d_par, non_blocking=True)
+            got = board.chain_device(drows, k, [], ln, chunks, k, relay_stream.cuda_stream,
+                                     ready=[k1_done] * chunks, threads=host_threads)
+            copy.synchronize()
+            return got
+
+        sums_g, ckpt_sealed_ms = wall(sealed_checkpoint)
+        seal_ok = seal_ok and sums_g == sums
     lost = 5
     owner, jl = layout.owner(lost)
     saved_sum = saved_fp = None
@@ -1546,8 +1574,44 @@ def c3_recovery_striped(torch, dist, dev, comp, copy, pipe, rank, world, shared,
         comp.synchronize()
         return verdict
 
-    verdict, verified_ms = wall(verified_recovery)
+    verdict, verified_host_ms = wall(verified_recovery)
     ok = all(verdict) and seal_ok
+    if rank == owner:
+        ok = ok and torch.equal(kv[:, jl, :4096], saved_fp) and bool(
+            kv[:, jl].contiguous().view(torch.int64).sum(dtype=torch.int64) == saved_sum)
+    verified_ms = verified_host_ms
+    if gpu_relay:
+        # GPU-assisted: each chunk's parity row-0 range is uploaded into HBM (K2
+        # reads it there, in groups of 8 chunks), hashed there by the seeded
+        # window kernel as it lands, and row 1 is continued on host threads
+        G = 8
+        rows0 = [[d_par[c, 0].data_ptr(), None] for c in range(chunks)]
+        k2_calls = [plan_reconstruct_striped_device(scheme, layout, bases, rank, ErasurePattern([lost]), rows0,
+                                                    range(g0, min(g0 + G, chunks))) for g0 in range(0, chunks, G)]
+        d_par.zero_()
+        if rank == owner:
+            kv[:, jl].zero_()
+        torch.cuda.synchronize()
+
+        def verified_recovery_gpu():
+            landed = []
+            for c in range(chunks):
+                with torch.cuda.stream(copy):
+                    d_par[c, 0].copy_(h_par[c, 0, :ln], non_blocking=True)
+                ev = torch.cuda.Event()
+                ev.record(copy)
+                landed.append(ev)
+            for gi, call in enumerate(k2_calls):
+                comp.wait_event(landed[min((gi + 1) * G, chunks) - 1])
+                call.run(comp.cuda_stream)
+            got = board.chain_device([r[0] for r in rows0], 1, hrows, ln, chunks, k, relay_stream.cuda_stream,
+                                     ready=landed, threads=host_threads)
+            comp.synchronize()
+            return [g == e for g, e in zip(got, sums)]
+
+        verdict_g, verified_ms = wall(verified_recovery_gpu)
+        ok = ok and all(verdict_g)
+        verdict = [a and b for a, b in zip(verdict, verdict_g)]
     if rank == owner:
         ok = ok and torch.equal(kv[:, jl, :4096], saved_fp) and bool(
             kv[:, jl].contiguous().view(torch.int64).sum(dtype=torch.int64) == saved_sum)
@@ -1556,6 +1620,8 @@ def c3_recovery_striped(torch, dist, dev, comp, copy, pipe, rank, world, shared,
     ok = bool(t.item())
     barrier()
     board.close()
+    if gpu_relay:
+        del d_par
     dist.destroy_process_group(relay_group)
     pg.close()
     del kv, h_par
@@ -1566,14 +1632,21 @@ def c3_recovery_striped(torch, dist, dev, comp, copy, pipe, rank, world, shared,
             "c3_h2d_links": world, "c3_checkpoint_ms": round(ckpt_ms, 2),
             "c3_checkpoint_data_gbs": round(n * shard / (ckpt_ms * 1e-3) / 1e9, 2), "c3_rebuild_ok": ok,
             "c3_verified_ms": round(verified_ms, 2), "c3_verified_chunks": sum(verdict),
+            "c3_verified_host_ms": round(verified_host_ms, 2),
+            "c3_checkpoint_sealed_ms": None if ckpt_sealed_ms is None else round(ckpt_sealed_ms, 2),
             "c3_seal_ms": round(seal_ms, 2), "c3_seal_rounds_ms": round(seal_rounds_ms, 2),
             "c3_seal_crosscheck_ok": bool(seal_ok),
             "c3_host_threads_per_rank": host_threads,
-            "c3_verify": ("ParityChunk checksums relayed through the ranks' byte ranges on every rank's host "
-                          "threads, chain states passed through a shared host board (peer.RelayBoard, no "
-                          "rounds), under the striped H2D + K2; c3_seal_rounds_ms = the same relay in "
-                          f"{k * world + world - 1} lockstep rounds of gloo all-gathers (peer.chain_striped), "
-                          "cross-checked equal, and chunk 0 against the plain chain over its whole parity"),
+            "c3_verify": ("ParityChunk checksums relayed through the ranks' byte ranges, chain states passed "
+                          "through a shared host board (peer.RelayBoard). c3_verified_ms: parity row-0 ranges "
+                          "H2D'd into HBM, K2 reading them there (groups of 8 chunks), row 0 hashed on the GPUs "
+                          "by the seeded window kernel as it lands, row 1 on host threads (chain_device, "
+                          "k_dev=1); c3_verified_host_ms: the whole relay on host threads under the pipelined "
+                          "H2D + K2. c3_checkpoint_sealed_ms: K1 into HBM + range D2H + the relay over the rows "
+                          "in HBM (every row on the GPUs). c3_seal_ms: the relay on host threads over the host "
+                          f"slabs; c3_seal_rounds_ms: the same in {k * world + world - 1} lockstep rounds of "
+                          "gloo all-gathers (peer.chain_striped); all cross-checked equal, and chunk 0 against "
+                          "the plain chain over its whole parity"),
             "c3_mode": f"byte-range striped over {world} GPUs (parity range H2D on every host link, survivors "
                        "over NVLink, rebuilt range P2P-stored into the failed worker's buffer)"}
 

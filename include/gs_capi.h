@@ -335,6 +335,19 @@ int gs_fnv1a64_continue_batch(const void* const* bufs, const uint64_t* lens, con
 uint64_t gs_relay_board_bytes(int n_chunks, int k, int world);
 int gs_fnv_relay(void* board, uint64_t epoch, int rank, int world, const void* const* rows, uint64_t len,
                  int n_chunks, int k, uint64_t h0, int threads, double timeout_s, uint64_t* sums);
+/* gs_fnv_relay with the first k_dev rows of every chunk hashed on this rank's
+ * GPU (the seeded window kernel, gs_fnv1a64_device_seeded, in batches of
+ * `batch` chunks on `stream`; the calling thread drives it and relays the
+ * states through the board): d_rows[c*k_dev + i] = device address of this
+ * rank's range of row i of chunk c (16-B aligned; len % 16 == 0), ready[c]
+ * (cudaEvent_t, or NULL / a NULL entry) = recorded once chunk c's device rows
+ * are complete (e.g. their H2D); rows k_dev..k-1 come from the host rows
+ * h_rows[c*k + i] on `threads` host threads. Same board, epoch and result
+ * contract as gs_fnv_relay; ranks may mix k_dev values only if all use the
+ * same k. */
+int gs_fnv_relay_device(void* board, uint64_t epoch, int rank, int world, const void* const* d_rows, int k_dev,
+                        void* const* ready, const void* const* h_rows, uint64_t len, int n_chunks, int k,
+                        uint64_t h0, int threads, int batch, void* stream, double timeout_s, uint64_t* sums);
 /* The same FNV-1a on the GPU, bit-exact (gs_fnv_gpu.cu): chain c is the k
  * device buffers bufs[c*k .. c*k+k-1] of `len` bytes each, concatenated in
  * order and hashed from h0 (0xcbf29ce484222325 = ParityChunk checksum);

@@ -83,6 +83,8 @@ SIGNATURES = {
     "gs_fnv1a64_continue_batch": (_i, [_vpp, _u64p, _u64p, _u64p, _i, _i]),
     "gs_relay_board_bytes": (_u64, [_i, _i, _i]),
     "gs_fnv_relay": (_i, [_vp, _u64, _i, _i, _vpp, _u64, _i, _i, _u64, _i, C.c_double, _u64p]),
+    "gs_fnv_relay_device": (_i, [_vp, _u64, _i, _i, _vpp, _i, _vpp, _vpp, _u64, _i, _i, _u64, _i, _i, _vp,
+                                 C.c_double, _u64p]),
     "gs_fnv1a64_device": (_i, [_vpp, _i, _i, _u64, _u64, _vp, _vp]),
     "gs_parity_upload_checksum": (_i, [_vpp, _i, _i, _u64, _vpp, _vp, _vp, _vp]),
     "gs_parity_offload_sealed": (_i, [_vpp, _i, _i, _u64, _vpp, _vp, _vp, _vp]),

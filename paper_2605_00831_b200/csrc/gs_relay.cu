@@ -2,7 +2,11 @@
 // RelayBoard): a ParityChunk checksum (parity_store.hpp:19-53) is one FNV-1a
 // chain over a chunk's whole parity rows, and with byte-range striping each
 // rank holds one range of every row, so the chain is continued range by range
-// through the ranks. Host code only (the bit-sliced chain of gs_fnv_simd.cpp).
+// through the ranks: on host threads (the bit-sliced chain of gs_fnv_simd.cpp)
+// and, for rows already in HBM, on this rank's GPU (the seeded window kernel
+// of gs_fnv_gpu.cu, gs_fnv_relay_device).
+#include <cuda_runtime.h>
+
 #include <algorithm>
 #include <atomic>
 #include <chrono>
@@ -143,3 +147,137 @@ int gs_fnv_relay(void* board, uint64_t epoch, int rank, int world, const void* c
   return GS_OK;
 }
 
+
+// gs_fnv_relay with the leading k_dev rows of every chunk hashed on this
+// rank's GPU. The calling thread drives the GPU: for each device row, in
+// batches of `batch` chunks in chunk order, it waits for the batch's
+// predecessor states on the board, uploads them as seeds, runs the seeded
+// window kernel over this rank's ranges (after the chunks' `ready` events),
+// reads the states back and publishes them. Host threads continue rows
+// k_dev..k-1 from the board as in gs_fnv_relay; they depend on GPU-published
+// states only, and the GPU workers of the ranks only on each other, so the
+// two relays cannot wait on one another in a cycle.
+int gs_fnv_relay_device(void* board, uint64_t epoch, int rank, int world, const void* const* d_rows, int k_dev,
+                        void* const* ready, const void* const* h_rows, uint64_t len, int n_chunks, int k,
+                        uint64_t h0, int threads, int batch, void* stream, double timeout_s, uint64_t* sums) {
+  if (!board || epoch == 0 || world < 1 || rank < 0 || rank >= world || n_chunks < 0 || k < 1 || k_dev < 0 ||
+      k_dev > k || batch < 1 || !sums || (n_chunks > 0 && k_dev > 0 && len && !d_rows) ||
+      (n_chunks > 0 && k_dev < k && len && !h_rows))
+    return fail(GS_INVALID_ARGUMENT, "fnv_relay_device: bad arguments");
+  if (len % 16) return fail(GS_INVALID_ARGUMENT, "fnv_relay_device: range length must be a multiple of 16");
+  RelaySlot* slots = static_cast<RelaySlot*>(board);
+  const int npos = k * world;
+  auto slot = [&](int c, int p) -> RelaySlot& { return slots[static_cast<size_t>(c) * npos + p]; };
+  const auto deadline = std::chrono::steady_clock::now() +
+                        std::chrono::microseconds(static_cast<int64_t>((timeout_s > 0 ? timeout_s : 60.0) * 1e6));
+  std::atomic<int> next{0}, failed{0};
+  auto await = [&](RelaySlot& sl) -> bool {
+    for (uint32_t spin = 0;; ++spin) {
+      if (__atomic_load_n(&sl.tag, __ATOMIC_ACQUIRE) == epoch) return true;
+      if (failed.load(std::memory_order_relaxed)) return false;
+      if (spin < 512) {
+        __builtin_ia32_pause();
+        continue;
+      }
+      if ((spin & 63) == 0 && std::chrono::steady_clock::now() > deadline) {
+        failed.store(1);
+        return false;
+      }
+      std::this_thread::sleep_for(std::chrono::microseconds(20));
+    }
+  };
+  auto publish = [&](int c, int p, uint64_t h) {
+    RelaySlot& mine = slot(c, p);
+    mine.h = h;
+    __atomic_store_n(&mine.tag, epoch, __ATOMIC_RELEASE);
+  };
+  // host rows k_dev..k-1, claimed in (row, chunk) order
+  const int host_rows = k - k_dev, segs = n_chunks * host_rows;
+  auto host_work = [&] {
+    for (int q = next.fetch_add(1); q < segs; q = next.fetch_add(1)) {
+      const int i = k_dev + q / n_chunks, c = q % n_chunks, p = i * world + rank;
+      uint64_t h = h0;
+      if (p > 0) {
+        RelaySlot& prev = slot(c, p - 1);
+        if (!await(prev)) return;
+        h = prev.h;
+      }
+      const uint8_t* b = static_cast<const uint8_t*>(len ? h_rows[static_cast<size_t>(c) * k + i] : nullptr);
+      fnv1a64_chains(&b, 1, len, &h);
+      publish(c, p, h);
+    }
+  };
+  std::vector<std::thread> pool;
+  if (segs > 0)
+    for (int t = 0; t < std::max(1, std::min(threads, segs)); ++t) pool.emplace_back(host_work);
+
+  int status = GS_OK;
+  if (k_dev > 0 && n_chunks > 0) {
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    uint64_t *h_io = nullptr, *d_io = nullptr;  // [seeds | states] x batch
+    cudaError_t e = cudaHostAlloc(reinterpret_cast<void**>(&h_io), sizeof(uint64_t) * 2 * batch, cudaHostAllocDefault);
+    if (e == cudaSuccess) e = cudaMallocAsync(reinterpret_cast<void**>(&d_io), sizeof(uint64_t) * 2 * batch, st);
+    if (e != cudaSuccess) status = fail(GS_CUDA_ERROR, "fnv_relay_device: buffers: %s", cudaGetErrorString(e));
+    std::vector<const void*> bufs(static_cast<size_t>(batch));
+    for (int i = 0; i < k_dev && status == GS_OK; ++i) {
+      const int p = i * world + rank;
+      for (int c0 = 0; c0 < n_chunks && status == GS_OK; c0 += batch) {
+        const int cnt = std::min(batch, n_chunks - c0);
+        for (int q = 0; q < cnt; ++q) {
+          uint64_t h = h0;
+          if (p > 0) {
+            RelaySlot& prev = slot(c0 + q, p - 1);
+            if (!await(prev)) {
+              status = fail(GS_RUNTIME_ERROR, "fnv_relay_device: timed out waiting for a peer rank's chain state");
+              break;
+            }
+            h = prev.h;
+          }
+          h_io[q] = h;
+          bufs[q] = d_rows[static_cast<size_t>(c0 + q) * k_dev + i];
+        }
+        if (status != GS_OK) break;
+        if (len) {
+          if (i == 0 && ready)
+            for (int q = 0; q < cnt; ++q)
+              if (ready[c0 + q] && (e = cudaStreamWaitEvent(st, static_cast<cudaEvent_t>(ready[c0 + q]), 0)) != cudaSuccess)
+                break;
+          if (e == cudaSuccess) e = cudaMemcpyAsync(d_io, h_io, sizeof(uint64_t) * cnt, cudaMemcpyHostToDevice, st);
+          if (e != cudaSuccess) {
+            status = fail(GS_CUDA_ERROR, "fnv_relay_device: %s", cudaGetErrorString(e));
+            break;
+          }
+          const int r = gs_fnv1a64_device_seeded(bufs.data(), cnt, 1, len, d_io, d_io + batch, st);
+          if (r != GS_OK) {
+            status = r;
+            break;
+          }
+          e = cudaMemcpyAsync(h_io + batch, d_io + batch, sizeof(uint64_t) * cnt, cudaMemcpyDeviceToHost, st);
+          if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+          if (e != cudaSuccess) {
+            status = fail(GS_CUDA_ERROR, "fnv_relay_device: %s", cudaGetErrorString(e));
+            break;
+          }
+        } else {
+          for (int q = 0; q < cnt; ++q) h_io[batch + q] = h_io[q];
+        }
+        for (int q = 0; q < cnt; ++q) publish(c0 + q, p, h_io[batch + q]);
+      }
+    }
+    if (d_io) {
+      cudaFreeAsync(d_io, st);
+      cudaStreamSynchronize(st);
+    }
+    if (h_io) cudaFreeHost(h_io);
+    if (status != GS_OK) failed.store(1);  // release the host threads
+  }
+  for (auto& t : pool) t.join();
+  if (status != GS_OK) return status;
+  for (int c = 0; c < n_chunks && !failed.load(); ++c) {
+    RelaySlot& last = slot(c, npos - 1);
+    if (!await(last)) break;
+    sums[c] = last.h;
+  }
+  if (failed.load()) return fail(GS_RUNTIME_ERROR, "fnv_relay_device: timed out waiting for a peer rank's chain state");
+  return GS_OK;
+}

@@ -388,11 +388,65 @@ class RelayBoard:
         check(st, "fnv_relay")
         return list(sums)
 
+    def chain_device(self, d_rows: Sequence[int], k_dev: int, h_rows: Sequence[int], length: int, n_chunks: int,
+                     k: int, stream: int, ready: Optional[Sequence] = None, threads: int = 0, batch: int = 8,
+                     h0: int = FNV_OFFSET) -> List[int]:
+        """chain() with rows 0..k_dev-1 of every chunk hashed on this rank's
+        GPU (gs_fnv_relay_device): d_rows[c*k_dev + i] = device address of this
+        rank's range of row i of chunk c, h_rows[c*k + i] = host address (rows
+        >= k_dev are read), ready[c] = a torch.cuda.Event recorded once chunk
+        c's device rows are complete (None: already complete). Runs on the
+        calling thread's current device."""
+        if n_chunks * k > self.slots:
+            raise InvalidArgument(f"RelayBoard: {n_chunks} x {k} segments exceed the board's {self.slots}")
+        if n_chunks <= 0:
+            return []
+        if threads <= 0:
+            threads = max(1, (os.cpu_count() or 1) // self.world)
+        self.epoch += 1
+        sums = (C.c_uint64 * n_chunks)()
+        dev = L.ptr_array(list(d_rows) if length and k_dev else [])
+        host = L.ptr_array(list(h_rows) if length and k_dev < k else [])
+        evs = L.ptr_array([e.cuda_event if e is not None else None for e in ready]) if ready is not None else None
+        st = L.lib().gs_fnv_relay_device(self.addr, self.epoch, self.rank, self.world, dev, k_dev, evs, host, length,
+                                         n_chunks, k, h0 & 0xFFFFFFFFFFFFFFFF, threads, batch, stream,
+                                         self.timeout_s, sums)
+        self.dist.barrier(group=self.group)
+        check(st, "fnv_relay_device")
+        return list(sums)
+
     def close(self) -> None:
         if getattr(self, "_mm", None) is not None:
             del self._view
             self._mm.close()
             self._mm = None
+
+
+def plan_reconstruct_striped_device(scheme: CodingScheme, layout: ShardLayout, bases: Sequence[int], rank: int,
+                                    lost: ErasurePattern, d_parity: Sequence[Sequence[Optional[int]]],
+                                    stripes: Sequence[int]) -> StripedCall:
+    """K2 over this rank's byte range of `stripes` with the parity already in
+    this GPU's HBM (uploaded by the caller, e.g. to checksum it there too):
+    d_parity[s][i] = device address of this rank's range of parity row i of
+    stripe s, None for a row not uploaded (the decoder reads only the first e
+    surviving rows, coding.hpp:540-544). Survivors over NVLink, rebuilt range
+    stored into the owners' buffers; one gs_apply_device launch."""
+    require_position_independent(scheme, layout)
+    dec = decoder(scheme, lost)
+    off, ln, slots = striped_slots(layout, bases, rank, lost.lost)
+    if ln == 0 or dec.n_out == 0 or not stripes:
+        return StripedCall(None, (), off, 0)
+    n, k = scheme.n, scheme.k
+    full, outs = [], []
+    for s in stripes:
+        full.extend(slots[s])
+        for i in range(k):
+            full.append(None if lost.contains(n + i) else d_parity[s][i])
+        for w in dec.out_index:
+            r, _ = layout.owner(w)
+            outs.append(bases[r] + layout.shard_offset(s, w) + off)
+    return StripedCall(L.lib().gs_apply_device, (dec.handle, len(stripes), L.ptr_array(full), L.ptr_array(outs), ln),
+                       off, ln, two_streams=False)
 
 
 def reconstruct_striped(scheme: CodingScheme, layout: ShardLayout, bases: Sequence[int], rank: int,

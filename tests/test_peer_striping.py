@@ -326,6 +326,45 @@ def _gpu_worker_local(rank, world, port, q, distinct=False):
             for s in range(S):
                 assert np.array_equal(got[s], _shards(s)[lost]), s
         dist.barrier()
+        # Verified rebuild from parity uploaded to HBM: the entries' checksums
+        # relayed through the ranks with row 0 hashed on the GPUs (seeded window
+        # kernel) and row 1 on host threads, then K2 reading the device rows.
+        from paper_2605_00831_b200.peer import RelayBoard, plan_reconstruct_striped_device
+        want_sums = [O.port().parity_checksum(O.port().encode(O.RS, N, K, _shards(s))) for s in range(S)]
+        board = RelayBoard(S, K)
+        d_loc = h_loc.to(torch.device("cuda", dev), non_blocking=True)
+        ready = torch.cuda.Event()
+        ready.record()
+        hrows = [h_loc[s, i].data_ptr() for s in range(S) for i in range(K)]
+        for k_dev in (0, 1, 2):
+            d_rows = [d_loc[s, i].data_ptr() for s in range(S) for i in range(k_dev)]
+            got = board.chain_device(d_rows, k_dev, hrows, ln, S, K, comp.cuda_stream, ready=[ready] * S,
+                                     threads=2, batch=2)
+            assert got == want_sums, (rank, k_dev, got, want_sums)
+        if rank == world - 1:   # one flipped device byte of chunk 1: chunk 1 (only) fails on every rank
+            d_loc[1, 0, 5] ^= 1
+        torch.cuda.synchronize()
+        dist.barrier()
+        got = board.chain_device([d_loc[s, 0].data_ptr() for s in range(S)], 1, hrows, ln, S, K, comp.cuda_stream)
+        assert [g == w for g, w in zip(got, want_sums)] == [s != 1 for s in range(S)], (rank, got)
+        if rank == world - 1:
+            d_loc[1, 0, 5] ^= 1
+        board.close()
+        if rank == owner:
+            mine[:, jl].zero_()
+        torch.cuda.synchronize()
+        dist.barrier()
+        plan_reconstruct_striped_device(scheme, lay, bases, rank, ErasurePattern([lost]),
+                                        [[d_loc[s, 0].data_ptr(), None] for s in range(S)],
+                                        range(S)).run(comp.cuda_stream)
+        comp.synchronize()
+        torch.cuda.synchronize()
+        dist.barrier()
+        if rank == owner:
+            got = mine[:, jl].cpu().numpy()
+            for s in range(S):
+                assert np.array_equal(got[s], _shards(s)[lost]), ("device-parity rebuild", s)
+        dist.barrier()
         pg.close()
         pipe.close()
         dist.destroy_process_group()

@@ -5,7 +5,7 @@ timeout 600 python -m pytest tests/test_peer_striping.py -q > gpurun_out/stripin
 for n in 2 4; do
   GS_BENCH_SHARED_GPU=1 timeout 1200 python bench.py --gpus $n --steps 5 --warmup 3 --no-cpu --no-overhead > gpurun_out/bench_n${n}_shared.json 2> gpurun_out/bench_n${n}_shared.err
 done
-tail -2 gpurun_out/striping_tests.log
+grep -q "rc=0" gpurun_out/striping_tests.log && tail -2 gpurun_out/striping_tests.log || tail -60 gpurun_out/striping_tests.log
 for n in 2 4; do tail -1 gpurun_out/bench_n${n}_shared.json | python -c "
 import json,sys; d=json.loads(sys.stdin.read()); r=d['recovery']
-print($n, d['value'], d.get('recovery_ms'), {k:v for k,v in r.items() if k.startswith('c3_') and k not in ('c3_mode','c3_verify')})"; tail -3 gpurun_out/bench_n${n}_shared.err; done
+print($n, d['value'], d.get('recovery_ms'), d.get('failures'), {k:v for k,v in r.items() if k.startswith('c3_') and k not in ('c3_mode','c3_verify')})"; tail -3 gpurun_out/bench_n${n}_shared.err; done
