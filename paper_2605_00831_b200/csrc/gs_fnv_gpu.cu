@@ -1537,6 +1537,10 @@ struct gs_verify {
   uint8_t* dev_block = nullptr;           // stream-ordered on cs: [d_state | d_sum | d_seed | ring]
   int hosts_active = 0;
   std::condition_variable cv;
+  // the feeder leaves unclaimed chunks to the host threads until this many
+  // seconds into finish (its uploads queue behind the row-0 uploads anyway)
+  double feeder_hold_s = 0;
+  std::chrono::steady_clock::time_point t0;
 };
 
 namespace {
@@ -1718,12 +1722,14 @@ static int verify_feeder(gs_verify* v) {
           v->on_gpu[c] = 2;
           break;
         }
-        if (v->lo <= v->hi) {
+        const bool held = std::chrono::duration<double>(std::chrono::steady_clock::now() - v->t0).count() <
+                          v->feeder_hold_s && v->hosts_active > 0;
+        if (v->lo <= v->hi && !held) {
           c = v->hi--;
           v->on_gpu[c] = 1;
           break;
         }
-        if (v->hosts_active == 0) break;
+        if (v->hosts_active == 0 && v->lo > v->hi) break;
         v->cv.wait_for(lk, std::chrono::microseconds(200));
       }
     }
@@ -1766,14 +1772,31 @@ static int v_claim_chains() {
   return n > 0 ? n : gsb::fnv_simd_available() ? 1 : 2;  // the SIMD chain needs no lockstep partner
 }
 
+// Whole chains on idle host threads (GS_VERIFY_HOST_FULL=0: off, for A/B):
+// while the next front chunk's GPU state is still in flight, a host thread
+// takes the LAST unclaimed chunk and hashes its whole chain from host memory
+// (rows 0..k-1, twice the bytes of a continuation) -- the chunks that land
+// last are then verified early, without the feeder re-uploading their other
+// rows over the link the decode is bound by.
+static bool v_host_full() {
+  static const bool on = [] {
+    const char* e = std::getenv("GS_VERIFY_HOST_FULL");
+    return !(e && e[0] == '0');
+  }();
+  return on;
+}
+
 static int verify_finish_dynamic(gs_verify* v, int threads, uint64_t* sums, int* gpu_chunks) {
   using clk = std::chrono::steady_clock;
   constexpr uint64_t kSlice = 4ull << 20;  // host progress check / hand-off granularity (bytes per chain)
+  constexpr uint64_t kOffset = 0xcbf29ce484222325ull;
   int st = GS_OK;
   std::atomic<int> err{0};
   const uint64_t total = static_cast<uint64_t>(v->k - v->u) * v->len;
+  const uint64_t head = static_cast<uint64_t>(v->u) * v->len;  // the rows the GPU hashes
   int fst = GS_OK;
   const auto t0 = clk::now();
+  v->t0 = t0;
   auto secs = [&] { return std::chrono::duration<double>(clk::now() - t0).count(); };
   // pacing model: the GPU hashes the remaining rows once the row-0 uploads
   // (already queued) have landed, at the link rate; a host thread hashes its
@@ -1784,6 +1807,8 @@ static int verify_finish_dynamic(gs_verify* v, int threads, uint64_t* sums, int*
   auto gpu_queue_s = [&] {  // under v->mu: GPU work not yet issued
     return link > 0 ? (static_cast<double>(v->hi - v->lo + 1) * total + v->handoff_bytes) / link : 0;
   };
+  const bool host_full = v_host_full() && link > 0 && chain_bps > 0;
+  if (host_full) v->feeder_hold_s = std::max(0.0, t_rows0 - kRing * (total / link));
   v->hosts_active = total > 0 ? std::max(threads, 1) : 0;
   std::thread feeder;
   if (total > 0) feeder = std::thread([&] { fst = verify_feeder(v); });
@@ -1791,22 +1816,41 @@ static int verify_finish_dynamic(gs_verify* v, int threads, uint64_t* sums, int*
   auto work = [&] {
     for (;;) {
       int c[8], m = 0;
+      bool whole = false;
       {
         std::lock_guard<std::mutex> lk(v->mu);
         const double now = secs();
-        if (link > 0 && chain_bps > 0 &&
-            now + total / chain_bps >= std::max(now, t_rows0) + gpu_queue_s())  // the GPU would finish first
-          break;
-        while (m < per && v->lo <= v->hi) c[m++] = v->lo++;
+        bool idle = false;
+        if (v->lo <= v->hi && host_full && now + (head + total) / chain_bps < t_rows0) {
+          idle = cudaEventQuery(v->group_ev[v->group_of[v->lo]]) == cudaErrorNotReady;
+          if (idle) cudaGetLastError();  // "not ready" is a status, not an error for later checks
+        }
+        if (idle) {
+          c[m++] = v->hi--;  // idle until the next state lands: a whole chain from the back
+          whole = true;
+        } else {
+          if (link > 0 && chain_bps > 0 &&
+              now + total / chain_bps >= std::max(now, t_rows0) + gpu_queue_s())  // the GPU would finish first
+            break;
+          while (m < per && v->lo <= v->hi) c[m++] = v->lo++;
+        }
       }
       if (m == 0) break;
       uint64_t h[8];
-      for (int q = 0; q < m; ++q) {
-        if (cudaEventSynchronize(v->group_ev[v->group_of[c[q]]]) != cudaSuccess) {
-          err = 1;
-          break;
+      if (whole) {
+        h[0] = kOffset;
+        for (int i = 0; i < v->u; ++i) {
+          const uint8_t* p = v->host_rows[static_cast<size_t>(c[0]) * v->k + i];
+          gsb::fnv1a64_chains(&p, 1, v->len, h);
         }
-        h[q] = v->pinned[c[q]];
+      } else {
+        for (int q = 0; q < m; ++q) {
+          if (cudaEventSynchronize(v->group_ev[v->group_of[c[q]]]) != cudaSuccess) {
+            err = 1;
+            break;
+          }
+          h[q] = v->pinned[c[q]];
+        }
       }
       if (err) break;
       const double start = secs();
