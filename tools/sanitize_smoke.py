@@ -152,6 +152,27 @@ def main():
     out = (C.c_uint64 * 3)()
     assert L.lib().gs_verify_finish(h, 2, out) == 0
     bad += sum(out[c] != want[c] for c in range(3))
+    # dynamic split (n_full = -1) with rates set, so idle host threads take whole
+    # chains from the back and the feeder serves the rest
+    dev.zero_()
+    torch.cuda.synchronize()
+    drows = [dev[c, i].data_ptr() for c in range(3) for i in range(2)]
+    assert L.lib().gs_verify_enqueue(L.ptr_array([hp[c, i].data_ptr() for c in range(3) for i in range(2)]), 3, 2,
+                                     ln, -1, 1, L.ptr_array(drows), st.cuda_stream, st.cuda_stream, C.byref(h)) == 0
+    assert L.lib().gs_verify_set_rates(h, 0.5, 0.2) == 0
+    out = (C.c_uint64 * 3)()
+    assert L.lib().gs_verify_finish(h, 2, out) == 0
+    bad += sum(out[c] != want[c] for c in range(3))
+    # the N>1 checksum relay's GPU worker on a one-rank board: row 0 hashed on the
+    # GPU (seeded window kernel), row 1 on host threads
+    ln16 = ln - ln % 16
+    board = (C.c_uint8 * L.lib().gs_relay_board_bytes(3, 2, 1))()
+    sums_r = (C.c_uint64 * 3)()
+    assert L.lib().gs_fnv_relay_device(board, 1, 0, 1, L.ptr_array([rows[c, 0].data_ptr() for c in range(3)]), 1,
+                                       None, L.ptr_array([hp[c, i].data_ptr() for c in range(3) for i in range(2)]),
+                                       ln16, 3, 2, 0xCBF29CE484222325, 2, 2, st.cuda_stream, 30.0, sums_r) == 0
+    want16 = [port.parity_checksum([host[c, 0].numpy()[:ln16], host[c, 1].numpy()[:ln16]]) for c in range(3)]
+    bad += sum(sums_r[c] != want16[c] for c in range(3))
     pipe.close()
     torch.cuda.synchronize()
     print("sanitize_smoke: mismatches =", bad, "kernels =", D.launches(), "jit status =", js.value)
