@@ -337,6 +337,7 @@ class RelayBoard:
 
     def __init__(self, max_chunks: int, k: int, group=None, timeout_s: float = 120.0):
         import mmap
+        import tempfile
         import uuid
 
         import torch.distributed as dist
@@ -348,7 +349,8 @@ class RelayBoard:
         size = int(L.lib().gs_relay_board_bytes(max_chunks, k, self.world))
         if size == 0:
             raise InvalidArgument("RelayBoard: bad shape")
-        name = [f"/dev/shm/gs-relay-{os.getpid()}-{uuid.uuid4().hex[:12]}" if self.rank == 0 else None]
+        shm = "/dev/shm" if os.path.isdir("/dev/shm") else tempfile.gettempdir()
+        name = [os.path.join(shm, f"gs-relay-{os.getpid()}-{uuid.uuid4().hex[:12]}") if self.rank == 0 else None]
         dist.broadcast_object_list(name, src=dist.get_global_rank(group, 0) if group is not None else 0,
                                    group=group)
         self.path = name[0]
