@@ -11,8 +11,10 @@ exchange on the data path is the peer loads, fused into the kernel. Recovery
 mirrors it: rank g uploads parity range g, pulls range g of the survivors and
 stores range g of the rebuilt shard directly into the replacement GPU's KV
 buffer. The entries' checksums (one FNV-1a chain over a chunk's whole parity)
-are relayed through the ranks' ranges: 8-byte chain states, one small
-all-gather per round (chain_striped).
+are relayed through the ranks' ranges as 8-byte chain states: through a board
+in host memory the ranks of a node share (RelayBoard; host threads, and the
+GPUs for rows in HBM), or in lockstep rounds of small all-gathers over any
+process group (chain_striped).
 
 Layout: with W ranks and n TP workers (W | n), rank r holds workers
 [r*n/W, (r+1)*n/W) as a tensor [S, n/W, L] (S stripes = requests x chunks).
