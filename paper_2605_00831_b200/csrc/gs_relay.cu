@@ -13,6 +13,7 @@
 #include <cstdarg>
 #include <cstdint>
 #include <cstdio>
+#include <mutex>
 #include <thread>
 #include <vector>
 
@@ -35,6 +36,32 @@ int fail(int status, const char* fmt, ...) {
   va_end(ap);
   gsb::set_last_error(buf);
   return status;
+}
+
+// Small pinned seed/state arrays of gs_fnv_relay_device, recycled across
+// calls: cudaFreeHost would synchronise the whole device at the end of every
+// relay (an unrelated decode included).
+std::mutex g_io_mu;
+std::vector<std::pair<size_t, void*>> g_io_free;
+
+void* io_take(size_t bytes) {
+  {
+    std::lock_guard<std::mutex> lk(g_io_mu);
+    for (size_t i = 0; i < g_io_free.size(); ++i)
+      if (g_io_free[i].first >= bytes) {
+        void* p = g_io_free[i].second;
+        g_io_free.erase(g_io_free.begin() + static_cast<long>(i));
+        return p;
+      }
+  }
+  void* p = nullptr;
+  return cudaHostAlloc(&p, std::max<size_t>(bytes, 4096), cudaHostAllocDefault) == cudaSuccess ? p : nullptr;
+}
+
+void io_give(void* p, size_t bytes) {
+  if (!p) return;
+  std::lock_guard<std::mutex> lk(g_io_mu);
+  g_io_free.push_back({std::max<size_t>(bytes, 4096), p});
 }
 
 }  // namespace
@@ -214,9 +241,11 @@ int gs_fnv_relay_device(void* board, uint64_t epoch, int rank, int world, const 
   int status = GS_OK;
   if (k_dev > 0 && n_chunks > 0) {
     cudaStream_t st = static_cast<cudaStream_t>(stream);
-    uint64_t *h_io = nullptr, *d_io = nullptr;  // [seeds | states] x batch
-    cudaError_t e = cudaHostAlloc(reinterpret_cast<void**>(&h_io), sizeof(uint64_t) * 2 * batch, cudaHostAllocDefault);
-    if (e == cudaSuccess) e = cudaMallocAsync(reinterpret_cast<void**>(&d_io), sizeof(uint64_t) * 2 * batch, st);
+    uint64_t *d_io = nullptr;  // [seeds | states] x batch
+    const size_t io_bytes = sizeof(uint64_t) * 2 * batch;
+    uint64_t* h_io = static_cast<uint64_t*>(io_take(io_bytes));
+    cudaError_t e = h_io ? cudaSuccess : cudaErrorMemoryAllocation;
+    if (e == cudaSuccess) e = cudaMallocAsync(reinterpret_cast<void**>(&d_io), io_bytes, st);
     if (e != cudaSuccess) status = fail(GS_CUDA_ERROR, "fnv_relay_device: buffers: %s", cudaGetErrorString(e));
     std::vector<const void*> bufs(static_cast<size_t>(batch));
     for (int i = 0; i < k_dev && status == GS_OK; ++i) {
@@ -264,11 +293,9 @@ int gs_fnv_relay_device(void* board, uint64_t epoch, int rank, int world, const 
         for (int q = 0; q < cnt; ++q) publish(c0 + q, p, h_io[batch + q]);
       }
     }
-    if (d_io) {
-      cudaFreeAsync(d_io, st);
-      cudaStreamSynchronize(st);
-    }
-    if (h_io) cudaFreeHost(h_io);
+    if (d_io) cudaFreeAsync(d_io, st);
+    cudaStreamSynchronize(st);  // h_io's last D2H has landed before it is recycled
+    io_give(h_io, io_bytes);
     if (status != GS_OK) failed.store(1);  // release the host threads
   }
   for (auto& t : pool) t.join();
