@@ -358,6 +358,22 @@ int main(int argc, char** argv) {
     run("shipped persistent grid-stride", [&](const PtrTable<kPtrCap>& t, const TileGeom& gg) {
       k_apply_special<Spec, kPtrCap, 1, false><<<std::min<uint32_t>(g.total, o0 * sms), kThreads, 0, st>>>(t, gg);
     });
+    {  // every CTA the same number of tiles: grid = ceil(total / ceil(total / (occ * sms)))
+      const uint32_t full = std::min<uint32_t>(g.total, o0 * sms);
+      const uint32_t per = (g.total + full - 1) / full;
+      const uint32_t eq = (g.total + per - 1) / per;
+      char l[96];
+      std::snprintf(l, sizeof l, "shipped grid-stride, equal tiles per CTA (grid %u x %u tiles)", eq, per);
+      run(l, [&](const PtrTable<kPtrCap>& t, const TileGeom& gg) {
+        k_apply_special<Spec, kPtrCap, 1, false><<<eq, kThreads, 0, st>>>(t, gg);
+      });
+      for (int m : {2, 3}) {  // more CTAs than resident slots: the tail is finer-grained
+        std::snprintf(l, sizeof l, "shipped grid-stride, grid %u (%dx resident)", std::min<uint32_t>(g.total, m * full), m);
+        run(l, [&](const PtrTable<kPtrCap>& t, const TileGeom& gg) {
+          k_apply_special<Spec, kPtrCap, 1, false><<<std::min<uint32_t>(g.total, m * full), kThreads, 0, st>>>(t, gg);
+        });
+      }
+    }
     run("one CTA per tile", [&](const PtrTable<kPtrCap>& t, const TileGeom& gg) {
       k_apply_special<Spec, kPtrCap, 1, false><<<g.total, kThreads, 0, st>>>(t, gg);
     });
