@@ -42,3 +42,23 @@ def test_workload_configs_are_arm_independent():
             assert c["data_bytes_per_step"] == W.stripes * 8 * W.slice * world
             assert c["parity_d2h_bytes_per_step"] * 4 == c["data_bytes_per_step"]
             json.dumps(c)
+
+
+@pytest.mark.gpu
+def test_two_rank_bench_line_on_one_gpu():
+    """`bench.py --gpus 2` re-execs itself under torch.distributed.run and
+    prints one contract line for the whole job (ranks sharing the B200:
+    GS_BENCH_SHARED_GPU=1, gloo plumbing; the C2 step striped over the two
+    ranks with peer loads through CUDA IPC; functional, not a timing)."""
+    sys.path.insert(0, ROOT)
+    import bench
+    env = dict(os.environ, GS_BENCH_SHARED_GPU="1")
+    out = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--gpus", "2", "--workload", "c2",
+                          "--steps", "5", "--warmup", "3", "--no-cpu", "--no-overhead", "--no-c3", "--no-c4"],
+                         cwd=ROOT, capture_output=True, text=True, timeout=900, env=env)
+    assert out.returncode == 0, out.stderr[-3000:]
+    line = json.loads(out.stdout.strip().splitlines()[-1])
+    assert line["n_gpus"] == 2 and line["metric"] == bench.METRIC and line["value"] > 0
+    assert line["parity_ok"] is True and line["failures"] == []
+    assert line["comm"]["nranks"] == 2 and line["config"] == bench.workload_config(bench.WORKLOADS["c2"], 2)
+    assert line["gpu_launches"] > 0
