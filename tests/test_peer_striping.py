@@ -164,6 +164,44 @@ def test_striped_checksum_relay_single_rank():
     assert chain_striped([], 0, 0, 2, 0, 1, exchange=None) == []
 
 
+def _relay_fuzz_worker(rank, world, port, q):
+    """Random shapes for both relay forms: k = 1..3 rows, 1..9 chunks, lengths
+    from a few bytes (most ranks' ranges empty) to several pages plus a ragged
+    tail, every chain checked against the oracle's ParityChunk checksum."""
+    import random
+    import sys
+    sys.path.insert(0, ROOT)
+    try:
+        from paper_2605_00831_b200.peer import RelayBoard, chain_striped, dist_exchange, stripe_range
+        _init(rank, world, port)
+        ex = dist_exchange()
+        board = RelayBoard(9, 3)
+        rng = random.Random(1234)   # same draws on every rank
+        for trial in range(fuzz_trials(12)):
+            k = rng.randint(1, 3)
+            chunks = rng.randint(1, 9)
+            length = rng.choice([rng.randint(1, 64), rng.randint(1, 4096 * world), rng.randint(4096, 6 * 4096 + 999)])
+            rows = [splitmix_bytes(10_000 * trial + r, length) for r in range(chunks * k)]
+            want = [O.port().parity_checksum(rows[c * k:(c + 1) * k]) for c in range(chunks)]
+            off, ln = stripe_range(length, rank, world)
+            local = [np.ascontiguousarray(r[off:off + ln]) for r in rows]
+            ptrs = [a.ctypes.data if ln else 0 for a in local]
+            got_r = chain_striped(ptrs, ln, chunks, k, rank, world, ex, threads=rng.randint(1, 3))
+            got_b = board.chain(ptrs, ln, chunks, k, threads=rng.randint(1, 3))
+            assert got_r == want and got_b == want, (rank, trial, k, chunks, length)
+        board.close()
+        dist.barrier()
+        dist.destroy_process_group()
+        q.put((rank, "ok"))
+    except Exception:  # pragma: no cover - reported to the parent
+        import traceback
+        q.put((rank, traceback.format_exc()))
+
+
+def test_striped_checksum_relay_fuzz_cpu():
+    _run(_relay_fuzz_worker, world=3)
+
+
 def test_relay_board_times_out_without_the_peer():
     """A rank whose predecessor never delivers fails (GS_RUNTIME_ERROR) after the
     timeout instead of spinning forever; rank 0 of a 2-rank relay alone can
