@@ -412,6 +412,56 @@ def _gpu_worker_local(rank, world, port, q, distinct=False):
         q.put((rank, traceback.format_exc()))
 
 
+def _relay_device_fuzz_worker(rank, world, port, q):
+    """chain_device over random shapes: k = 1..3 rows of which k_dev = 0..k in
+    HBM (the rest on host threads), 1..9 chunks, 16-B-multiple lengths from
+    one granule to several pages, batches of 1..4 chunks per GPU launch, with
+    and without ready events -- every chain against the oracle."""
+    import random
+    import sys
+    sys.path.insert(0, ROOT)
+    try:
+        torch.cuda.set_device(0)
+        from paper_2605_00831_b200.peer import RelayBoard, stripe_range
+        _init(rank, world, port)
+        board = RelayBoard(9, 3)
+        stream = torch.cuda.Stream()
+        rng = random.Random(77)
+        for trial in range(fuzz_trials(10)):
+            k = rng.randint(1, 3)
+            k_dev = rng.randint(0, k)
+            chunks = rng.randint(1, 9)
+            length = 16 * rng.choice([1, rng.randint(1, 256 * world), rng.randint(256, 2048)])
+            rows = [splitmix_bytes(50_000 * trial + r, length) for r in range(chunks * k)]
+            want = [O.port().parity_checksum(rows[c * k:(c + 1) * k]) for c in range(chunks)]
+            off, ln = stripe_range(length, rank, world)
+            host = torch.stack([torch.from_numpy(np.ascontiguousarray(r[off:off + ln])) for r in rows]) \
+                if ln else torch.zeros((chunks * k, 16), dtype=torch.uint8)
+            dev = host.cuda()
+            ev = torch.cuda.Event()
+            ev.record()
+            d_rows = [dev[c * k + i].data_ptr() for c in range(chunks) for i in range(k_dev)]
+            h_rows = [host[c * k + i].data_ptr() for c in range(chunks) for i in range(k)]
+            ready = [ev] * chunks if rng.random() < 0.5 else None
+            got = board.chain_device(d_rows, k_dev, h_rows, ln, chunks, k, stream.cuda_stream, ready=ready,
+                                     threads=rng.randint(1, 3), batch=rng.randint(1, 4))
+            assert got == want, (rank, trial, k, k_dev, chunks, length)
+        board.close()
+        dist.barrier()
+        dist.destroy_process_group()
+        q.put((rank, "ok"))
+    except Exception:  # pragma: no cover
+        import traceback
+        q.put((rank, traceback.format_exc()))
+
+
+@pytest.mark.gpu
+def test_striped_checksum_relay_on_gpus_fuzz_two_processes_one_gpu():
+    if not torch.cuda.is_available():
+        pytest.fail("GPU test collected without a CUDA device")
+    _run(_relay_device_fuzz_worker)
+
+
 @pytest.mark.gpu
 def test_ipc_striped_range_local_parity_two_processes_one_gpu():
     if not torch.cuda.is_available():
