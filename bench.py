@@ -19,7 +19,9 @@ At N GPUs (torchrun, one rank per GPU) the TP group is spread over the ranks
 (8/N workers each) and each step checkpoints one chunk of each of N
 concurrent prefills (weak scaling): rank g encodes byte range g of every
 shard, pulling the ranges it does not own from peers over NVLink inside K1,
-and D2H's parity range g on its own host link.
+and D2H's parity range g on its own host link; `recovery_ms` is then the
+striped C3 recovery verified by relaying every entry's checksum through the
+ranks' byte ranges (peer.RelayBoard).
 
 Also reported (same JSON line): the kernel-only roofline of K1 (and K2), the
 host-link fraction, e2e through the reference-facing C ABI with host buffers
