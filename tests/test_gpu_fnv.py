@@ -295,3 +295,29 @@ def test_seeded_device_fnv_continues_chains():
     got = [int(v) & (2**64 - 1) for v in both.cpu().tolist()]
     for c in range(n):
         assert got[c] == port.parity_checksum(host[c * 4:(c + 1) * 4]), c
+
+
+def test_offload_sealed_orders_rows_and_checksums_on_the_copy_stream():
+    """gs_parity_offload_sealed: once the COPY stream is synchronised (nothing
+    else), the rows and the checksums are in host memory -- the checksums travel
+    on the compute stream after the GPU FNV, and the copy stream waits for them
+    before anything queued after the call (a store commit reads them there)."""
+    S, k, ln = 6, 2, 3 * 65536 + 4096
+    comp, copy = torch.cuda.Stream(), torch.cuda.Stream()
+    rows = torch.randint(0, 256, (S, k, ln), dtype=torch.uint8, device="cuda")
+    h_rows = torch.zeros((S, k, ln), dtype=torch.uint8).pin_memory()
+    h_sums = torch.zeros(S, dtype=torch.int64).pin_memory()
+    torch.cuda.synchronize()
+    with torch.cuda.stream(comp):
+        torch.cuda._sleep(2_000_000)   # keep the compute stream busy: the FNV lands late
+    rc = L.lib().gs_parity_offload_sealed(L.ptr_array([rows[s, i].data_ptr() for s in range(S) for i in range(k)]),
+                                          S, k, ln,
+                                          L.ptr_array([h_rows[s, i].data_ptr() for s in range(S) for i in range(k)]),
+                                          h_sums.data_ptr(), comp.cuda_stream, copy.cuda_stream)
+    assert rc == 0, L.lib().gs_last_error()
+    copy.synchronize()
+    host = rows.cpu()
+    assert torch.equal(h_rows, host)
+    want = [O.port().parity_checksum([host[s, i].numpy() for i in range(k)]) for s in range(S)]
+    assert [int(v) & (2**64 - 1) for v in h_sums.tolist()] == want
+    torch.cuda.synchronize()
