@@ -5,6 +5,9 @@
 #  * ncu --set full of K1 at the C3 and C2 launches (bench.py's roofline.traffic
 #    reads these, keyed by tools/srcsha.py), K2 at C3, paged K1 at C2 and C3;
 #  * the launch list of exactly the timed steps of the default bench.
+# The rest of the round's closing evidence has its own scripts: tools/sanitize_run.sh
+# (compute-sanitizer), tools/soak.sh (20x fuzz), tools/gpu_relay_check.sh (the N>1
+# path with 2/4/8 ranks sharing the GPU), tools/recapture_kernels.sh (ncu only).
 set -x
 mkdir -p gpurun_out
 python tools/srcsha.py > gpurun_out/src_sha.txt
