@@ -1880,7 +1880,7 @@ def spawn_ranks(args) -> None:
     if args.gpus <= 1:
         return
     shared = os.environ.get("GS_BENCH_SHARED_GPU") == "1"
-    if not shared:
+    if not shared and args.impl != "reference":   # the reference arm runs on the host alone
         import torch
         if torch.cuda.device_count() < args.gpus:
             raise SystemExit(f"bench: --gpus {args.gpus} but only {torch.cuda.device_count()} CUDA device(s) "

@@ -32,6 +32,27 @@ def test_reference_arm_line_keeps_the_contract():
     assert line["e2e"] == {"value": line["value"], "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}
 
 
+def test_reference_arm_under_two_ranks_prints_one_line():
+    """`--impl reference --gpus 2` (re-exec under torch.distributed.run, as the
+    driver's scaling run launches it): rank 0 alone runs the reference codec and
+    prints the line with n_gpus = 2 and our arm's N=2 config; rank 1 exits 0."""
+    sys.path.insert(0, ROOT)
+    import bench
+    from oracle import oracle as O
+    if not O.have_ref():
+        pytest.skip("oracle/_ref not built")
+    env = {k: v for k, v in os.environ.items() if k not in ("WORLD_SIZE", "RANK", "LOCAL_RANK")}
+    out = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--impl", "reference", "--gpus", "2",
+                          "--workload", "c2", "--steps", "1", "--warmup", "0"], cwd=ROOT, capture_output=True,
+                         text=True, timeout=600, env=env)
+    assert out.returncode == 0, out.stderr[-2000:]
+    lines = [ln for ln in out.stdout.strip().splitlines() if ln.startswith("{")]
+    assert len(lines) == 1, out.stdout
+    line = json.loads(lines[0])
+    assert line["impl"] == "reference" and line["n_gpus"] == 2
+    assert line["config"] == bench.workload_config(bench.WORKLOADS["c2"], 2)
+
+
 def test_workload_configs_are_arm_independent():
     sys.path.insert(0, ROOT)
     import bench
