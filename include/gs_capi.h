@@ -393,6 +393,16 @@ int gs_verify_finish_ex(gs_verify* v, int threads, uint64_t* sums, int* gpu_chun
  * one host thread's serial FNV rate (GB/s); host threads then stop claiming
  * chunks the GPU would finish sooner (the host rate is refined online). */
 int gs_verify_set_rates(gs_verify* v, double link_gbs, double host_chain_gbs);
+/* Make `stream` wait until chunk `chunk`'s uploaded rows are in HBM (and hashed
+ * there): the decode can then run K2 group by group under the remaining
+ * uploads instead of after all of them. Valid after enqueue and before finish,
+ * or while a hold is taken: gs_verify_hold keeps a concurrently running
+ * gs_verify_finish from releasing the handle (it waits for the matching
+ * gs_verify_release before destroying the upload events), so a caller can
+ * start finish on another thread first and queue its K2 launches behind. */
+int gs_verify_stream_wait(gs_verify* v, int chunk, void* stream);
+int gs_verify_hold(gs_verify* v);
+int gs_verify_release(gs_verify* v);
 /* Chains (process total) a host thread handed over to the GPU mid-chain in a
  * dynamic split, because it had fallen behind the GPU (diagnostics). */
 uint64_t gs_verify_handoffs(void);

@@ -92,6 +92,9 @@ SIGNATURES = {
     "gs_verify_finish": (_i, [_vp, _i, _u64p]),
     "gs_verify_finish_ex": (_i, [_vp, _i, _u64p, _ip]),
     "gs_verify_set_rates": (_i, [_vp, C.c_double, C.c_double]),
+    "gs_verify_stream_wait": (_i, [_vp, _i, _vp]),
+    "gs_verify_hold": (_i, [_vp]),
+    "gs_verify_release": (_i, [_vp]),
     "gs_verify_handoffs": (_u64, []),
     "gs_verify_last_stats": (_i, [C.POINTER(C.c_double)]),
     "gs_fnv1a64_device_seeded": (_i, [_vpp, _i, _i, _u64, _vp, _vp, _vp]),

@@ -734,29 +734,55 @@ class Checkpointer:
                     drows.append(full[s, i].data_ptr())
                 else:
                     drows.append(part[s - nf, i].data_ptr() if i < u else None)
+        # K2 needs the uploaded rows (not their checksums, nor the rows the
+        # dynamic split's GPU feeder uploads later for hashing only). In the
+        # dynamic split it runs group by group as each group of 4 chunks lands
+        # (gs_verify_stream_wait), under the remaining uploads: one K2 after the
+        # last upload left ~8 ms of C3 rebuild (64 x 755 MB) behind the link.
+        # allocated before the uploads are queued: a caching-allocator miss may
+        # synchronise the device, which must not happen behind 5 GiB of H2D
+        outs = torch.empty((S, max(dec.n_out, 1), self.slice), dtype=torch.uint8, device=self.dev)
+
+        def build_tables():
+            launches = []
+            if dec.n_out:
+                slots: List[Optional[int]] = []
+                for s, c in enumerate(chunk_ids):
+                    row = self._survivor_row(ground_truth[c], failed)
+                    for i in range(k):
+                        row[sch.n + i] = drows[s * k + i]
+                    slots.extend(row)
+                optrs = [outs[s, b].data_ptr() for s in range(S) for b in range(dec.n_out)]
+                w, no = sch.n + k, dec.n_out
+                groups = [(0, S)] if not grouped else [(g0, min(g0 + 4, S)) for g0 in range(0, S, 4)]
+                launches = [(g1 - 1, g1 - g0, L.ptr_array(slots[g0 * w:g1 * w]),
+                             L.ptr_array(optrs[g0 * no:g1 * no])) for g0, g1 in groups]
+            return launches
+
+        grouped = n_full < 0 and os.environ.get("GS_RECOVER_K2_GROUPS", "1") != "0"   # A/B switch
         handle = C.c_void_p()
         check(lib.gs_verify_enqueue(L.ptr_array([e.parity[i].ctypes.data for e in entries for i in range(k)]),
                                     S, k, self.slice, n_full, u, L.ptr_array(drows), self.verify.cuda_stream,
                                     self.copy.cuda_stream, C.byref(handle)), "recover verify")
-        # K2 needs the uploaded rows (not their checksums, nor the rows the
-        # dynamic split's GPU feeder uploads later for hashing only)
-        self.compute.wait_stream(self.copy)
+        if not grouped:
+            self.compute.wait_stream(self.copy)
         if n_full < 0:
             check(lib.gs_verify_set_rates(handle, self.cfg.cost.host_bw / 1e9, self.host_chain_rate / 1e9),
                   "recover verify")
-        finish = _VerifyFinish(handle, S, threads)
-        outs = torch.empty((S, max(dec.n_out, 1), self.slice), dtype=torch.uint8, device=self.dev)
-        if dec.n_out:
-            slots: List[Optional[int]] = []
-            for s, c in enumerate(chunk_ids):
-                row = self._survivor_row(ground_truth[c], failed)
-                for i in range(k):
-                    row[sch.n + i] = drows[s * k + i]
-                slots.extend(row)
-            check(lib.gs_apply_device(dec.handle, S, L.ptr_array(slots),
-                                      L.ptr_array([outs[s, b].data_ptr() for s in range(S)
-                                                   for b in range(dec.n_out)]),
-                                      self.slice, self.compute.cuda_stream), "recover")
+        # the verification's host threads start now; the K2 launch tables are
+        # built while the first uploads run, under a hold on the handle (finish
+        # keeps the upload events until the launches are queued behind them)
+        check(lib.gs_verify_hold(handle), "recover verify")
+        try:
+            finish = _VerifyFinish(handle, S, threads)
+            launches = build_tables()
+            for last, cnt, sl, op in launches:
+                if grouped:
+                    check(lib.gs_verify_stream_wait(handle, last, self.compute.cuda_stream), "recover verify")
+                check(lib.gs_apply_device(dec.handle, cnt, sl, op, self.slice, self.compute.cuda_stream),
+                      "recover")
+        finally:
+            check(lib.gs_verify_release(handle), "recover verify")
         return outs, list(dec.out_index), n_full, finish, (full, part)
 
     def _survivor_row(self, gt, failed) -> List[Optional[int]]:

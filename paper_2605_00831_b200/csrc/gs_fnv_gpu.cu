@@ -1544,6 +1544,15 @@ struct gs_verify {
   // seconds into finish (its uploads queue behind the row-0 uploads anyway)
   double feeder_hold_s = 0;
   std::chrono::steady_clock::time_point t0;
+  // gs_verify_hold / gs_verify_release: a caller still queueing work behind
+  // the upload events (gs_verify_stream_wait) keeps finish from destroying them
+  int holds = 0;
+  std::mutex hold_mu;
+  std::condition_variable hold_cv;
+  void wait_unheld() {
+    std::unique_lock<std::mutex> lk(hold_mu);
+    hold_cv.wait(lk, [&] { return holds == 0; });
+  }
 };
 
 namespace {
@@ -1939,6 +1948,7 @@ static int verify_finish_dynamic(gs_verify* v, int threads, uint64_t* sums, int*
                             static_cast<double>(handed)};
     for (int i = 0; i < 6; ++i) g_vstats[i] = vals[i];
   }
+  v->wait_unheld();
   for (auto e : v->group_ev) cudaEventDestroy(e);
   for (auto e : v->slot_ev) cudaEventDestroy(e);
   for (auto e : v->up_ev) cudaEventDestroy(e);
@@ -2045,6 +2055,32 @@ extern "C" int gs_verify_enqueue(const void* const* h_parity, int n_chunks, int 
 // their GPU states arrive; sums[c] = chunk c's checksum. Frees `v`.
 extern "C" int gs_verify_finish_ex(gs_verify* v, int threads, uint64_t* sums, int* gpu_chunks);
 
+extern "C" int gs_verify_hold(gs_verify* v) {
+  if (!v) return ffail(GS_INVALID_ARGUMENT, "verify_hold: NULL handle");
+  std::lock_guard<std::mutex> lk(v->hold_mu);
+  ++v->holds;
+  return GS_OK;
+}
+
+extern "C" int gs_verify_release(gs_verify* v) {
+  if (!v) return ffail(GS_INVALID_ARGUMENT, "verify_release: NULL handle");
+  {
+    std::lock_guard<std::mutex> lk(v->hold_mu);
+    if (v->holds == 0) return ffail(GS_LOGIC_ERROR, "verify_release: not held");
+    --v->holds;
+  }
+  v->hold_cv.notify_all();
+  return GS_OK;
+}
+
+extern "C" int gs_verify_stream_wait(gs_verify* v, int chunk, void* stream) {
+  if (!v || chunk < 0 || chunk >= v->n) return ffail(GS_INVALID_ARGUMENT, "verify_stream_wait: bad arguments");
+  cudaEvent_t ev = v->group_of[chunk] >= 0 ? v->group_ev[v->group_of[chunk]] : v->full_ev;
+  if (!ev) return ffail(GS_INVALID_ARGUMENT, "verify_stream_wait: chunk %d has no upload event", chunk);
+  const cudaError_t e = cudaStreamWaitEvent(static_cast<cudaStream_t>(stream), ev, 0);
+  return e == cudaSuccess ? GS_OK : ffail(GS_CUDA_ERROR, "verify_stream_wait: %s", cudaGetErrorString(e));
+}
+
 extern "C" int gs_verify_set_rates(gs_verify* v, double link_gbs, double host_chain_gbs) {
   if (!v || link_gbs < 0 || host_chain_gbs < 0) return ffail(GS_INVALID_ARGUMENT, "verify_set_rates: bad arguments");
   v->link_bps = link_gbs * 1e9;
@@ -2110,6 +2146,7 @@ extern "C" int gs_verify_finish_ex(gs_verify* v, int threads, uint64_t* sums, in
     else
       for (int c = 0; c < v->n_full; ++c) sums[c] = v->pinned[c];
   }
+  v->wait_unheld();
   for (auto e : v->group_ev) {  // every D2H into `pinned` has landed before it is freed
     cudaEventSynchronize(e);
     cudaEventDestroy(e);
