@@ -739,11 +739,11 @@ class Checkpointer:
         # dynamic split it runs group by group as each group of 4 chunks lands
         # (gs_verify_stream_wait), under the remaining uploads: one K2 after the
         # last upload left ~8 ms of C3 rebuild (64 x 755 MB) behind the link.
-        # allocated before the uploads are queued: a caching-allocator miss may
-        # synchronise the device, which must not happen behind 5 GiB of H2D
-        outs = torch.empty((S, max(dec.n_out, 1), self.slice), dtype=torch.uint8, device=self.dev)
-
         def build_tables():
+            # allocated once the uploads are queued: a caching-allocator miss
+            # maps 5 GiB (tens of ms), which then runs under the H2D instead of
+            # delaying it
+            outs = torch.empty((S, max(dec.n_out, 1), self.slice), dtype=torch.uint8, device=self.dev)
             launches = []
             if dec.n_out:
                 slots: List[Optional[int]] = []
@@ -757,7 +757,7 @@ class Checkpointer:
                 groups = [(0, S)] if not grouped else [(g0, min(g0 + 4, S)) for g0 in range(0, S, 4)]
                 launches = [(g1 - 1, g1 - g0, L.ptr_array(slots[g0 * w:g1 * w]),
                              L.ptr_array(optrs[g0 * no:g1 * no])) for g0, g1 in groups]
-            return launches
+            return outs, launches
 
         grouped = n_full < 0 and os.environ.get("GS_RECOVER_K2_GROUPS", "1") != "0"   # A/B switch
         handle = C.c_void_p()
@@ -775,7 +775,7 @@ class Checkpointer:
         check(lib.gs_verify_hold(handle), "recover verify")
         try:
             finish = _VerifyFinish(handle, S, threads)
-            launches = build_tables()
+            outs, launches = build_tables()
             for last, cnt, sl, op in launches:
                 if grouped:
                     check(lib.gs_verify_stream_wait(handle, last, self.compute.cuda_stream), "recover verify")
