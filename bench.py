@@ -1360,10 +1360,13 @@ def c3_orchestrated(torch, dev, link, k1_gbs, k2_gbs, workers: int = 8, k: int =
         return {f"{label}_orchestrated_skipped": "not enough device memory"}
     cost = CostModel.measured(link["h2d"], k1_gbs, k2_gbs)
     cfg = CheckpointConfig(CodingScheme.reed_solomon(workers, k), m, cfg_m, cost)
-    threads = int(os.environ.get("GS_VERIFY_THREADS", 0)) or max(1, (os.cpu_count() or 1) - 2)
+    threads = max(1, (os.cpu_count() or 1) - 2)
     store = ParityStore(seal_threads=threads)
     store.bind_device(dev.index or 0)
     ck = Checkpointer(cfg, store, device=dev.index or 0)
+    # the recovery's verification on every core (its dynamic split hands a slow
+    # thread's tail to the GPU feeder; tools/c3_endgame_ab.sh)
+    threads = int(os.environ.get("GS_VERIFY_THREADS", 0)) or max(1, os.cpu_count() or 1)
     if os.environ.get("GS_VERIFY_SPLIT"):          # A/B of the verification split (tools/c3_probe.py)
         ck.verify_split = os.environ["GS_VERIFY_SPLIT"]
     # warm pass: the host tier's pinned slabs (10 GiB here) and the device
@@ -1374,7 +1377,7 @@ def c3_orchestrated(torch, dev, link, k1_gbs, k2_gbs, workers: int = 8, k: int =
     # ... and the recovery's device buffers (uploaded parity rows, rebuilt
     # shards, GPU checksum scratch) likewise
     ck.recover(10, FailureEvent(list(failed), at_chunk=warm.chunks_done), warm.ground_truth, [m] * warm.chunks_done,
-               verify_threads=max(1, (os.cpu_count() or 1) - 2))
+               verify_threads=threads)
     del warm
     store.erase_request(10)
     t0 = time.perf_counter()

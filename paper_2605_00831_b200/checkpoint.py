@@ -719,6 +719,11 @@ class Checkpointer:
         sch = self.cfg.scheme
         dec = decoder(sch, ErasurePattern(sorted(failed)))
         S, k = len(chunk_ids), sch.k
+        if self.verify_split == "dynamic":
+            # every core: the chains are serial 80 MiB units, and with the
+            # end-game hand-off the feeder absorbs a slow thread's tail
+            # (tools/c3_endgame_ab.sh: 16 threads 101-102 ms vs 14: 103-110)
+            threads = threads or max(1, os.cpu_count() or 1)
         threads = threads or max(1, (os.cpu_count() or 1) - 2)
         n_full, u = self._split_plan(S, failed, threads)
         if self.verify_split == "dynamic":

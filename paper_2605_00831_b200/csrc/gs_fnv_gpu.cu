@@ -1708,6 +1708,43 @@ static int verify_enqueue_dynamic(const void* const* h_parity, int n_chunks, int
   return GS_OK;
 }
 
+// End-game balancing of the dynamic split (GS_VERIFY_ENDGAME=0: off, for
+// A/B): idle host threads keep claiming chunks until the row-0 uploads are
+// over, and once the link is free a host thread hands the rest of its chain
+// to the GPU feeder when the upload + GPU hash of that rest (queued behind
+// the rows already handed over) would end sooner -- the chains' serial
+// 80 MiB units otherwise leave the last few chunks to a thread or two while
+// the rest idle (tools/c3_threads_trace.sh).
+static bool v_endgame() {
+  static const bool on = [] {
+    const char* e = std::getenv("GS_VERIFY_ENDGAME");
+    return !(e && e[0] == '0');
+  }();
+  return on;
+}
+
+// GS_VERIFY_TRACE=1: one stderr line per claim of the dynamic split (who,
+// chunk, whole chain or continuation, claim / state-ready / done seconds), for
+// reading where the verification's tail goes (tools/c3_probe.py).
+static bool v_trace() {
+  static const bool on = [] {
+    const char* e = std::getenv("GS_VERIFY_TRACE");
+    return e && e[0] == '1';
+  }();
+  return on;
+}
+struct VTrace {
+  int who, chunk, kind;  // who: host thread index, -1 = GPU feeder; kind: 0 continuation, 1 whole, 2 feeder, 3 handed over
+  double claim, ready, done;
+};
+static std::mutex g_vtrace_mu;
+static std::vector<VTrace> g_vtrace;
+static void vtrace_push(const VTrace& t) {
+  if (!v_trace()) return;
+  std::lock_guard<std::mutex> lk(g_vtrace_mu);
+  g_vtrace.push_back(t);
+}
+
 // The GPU feeder: hashes the remaining rows (u..k-1, one contiguous chain of
 // (k-u)*len bytes per chunk) of (a) chunks handed off by host threads, from
 // their byte offset and host state, and (b) unclaimed chunks, taken from the
@@ -1746,6 +1783,10 @@ static int verify_feeder(gs_verify* v) {
       }
     }
     if (c < 0) break;
+    if (v_trace()) {
+      const double t = std::chrono::duration<double>(std::chrono::steady_clock::now() - v->t0).count();
+      vtrace_push({-1, c, 2, t, t, t});
+    }
     uint8_t* slot = v->ring + static_cast<size_t>(r) * total;
     cudaError_t e = cudaSuccess;
     for (uint64_t o = off; o < total && e == cudaSuccess;) {  // the chain's bytes [off, total), packed
@@ -1825,10 +1866,13 @@ static int verify_finish_dynamic(gs_verify* v, int threads, uint64_t* sums, int*
   std::thread feeder;
   if (total > 0) feeder = std::thread([&] { fst = verify_feeder(v); });
   const int per = std::max(1, std::min(8, v_claim_chains()));
+  std::atomic<int> next_tid{0};
   auto work = [&] {
+    const int tid = next_tid.fetch_add(1);
     for (;;) {
       int c[8], m = 0;
       bool whole = false;
+      const double t_claim = secs();
       {
         std::lock_guard<std::mutex> lk(v->mu);
         const double now = secs();
@@ -1841,8 +1885,12 @@ static int verify_finish_dynamic(gs_verify* v, int threads, uint64_t* sums, int*
           c[m++] = v->hi--;  // idle until the next state lands: a whole chain from the back
           whole = true;
         } else {
-          if (link > 0 && chain_bps > 0 &&
-              now + total / chain_bps >= std::max(now, t_rows0) + gpu_queue_s())  // the GPU would finish first
+          // the GPU would finish first: quit, but only once the row-0 uploads
+          // are over -- before that a claim costs nothing the link could do
+          // sooner, and the end-game hand-off below gives the GPU just the
+          // chain's rest (GS_VERIFY_ENDGAME=0: the earlier rule, for A/B)
+          if (link > 0 && chain_bps > 0 && (!v_endgame() || now >= t_rows0) &&
+              now + total / chain_bps >= std::max(now, t_rows0) + gpu_queue_s())
             break;
           while (m < per && v->lo <= v->hi) c[m++] = v->lo++;
         }
@@ -1887,7 +1935,12 @@ static int verify_finish_dynamic(gs_verify* v, int threads, uint64_t* sums, int*
         // a safety net for a host that stalls (not a balancing tool: the claim
         // pacing balances): at least a quarter of the chain done, and the host
         // would need over twice as long as the GPU for the rest
-        if (4 * o >= total && host_left > 2e-3 && host_left > 2.0 * (gpu_done - now)) {
+        // end game: the link is (about to be) free and the feeder's queue is
+        // what the GPU still has to upload -- hand over the chain's rest when
+        // the GPU would finish it clearly sooner than this thread
+        const double gpu_end = std::max(now, t_rows0) + gpu_queue_s() + m * (total - o) / link + 1e-3;
+        const bool endgame = v_endgame() && now >= t_rows0 - 2e-3 && host_left > gpu_end - now + 2e-3;
+        if (endgame || (4 * o >= total && host_left > 2e-3 && host_left > 2.0 * (gpu_done - now))) {
           for (int q = 0; q < m; ++q) {
             v->hseed[c[q]] = h[q];
             v->handoffs.push_back({c[q], o});
@@ -1899,6 +1952,7 @@ static int verify_finish_dynamic(gs_verify* v, int threads, uint64_t* sums, int*
           break;
         }
       }
+      for (int q = 0; q < m; ++q) vtrace_push({tid, c[q], handed ? 3 : whole ? 1 : 0, t_claim, start, secs()});
       if (handed) break;
       for (int q = 0; q < m; ++q) sums[c[q]] = h[q];
     }
@@ -1916,6 +1970,15 @@ static int verify_finish_dynamic(gs_verify* v, int threads, uint64_t* sums, int*
   }
   const double t_hosts = secs();
   if (feeder.joinable()) feeder.join();
+  if (v_trace()) {
+    std::lock_guard<std::mutex> lk(g_vtrace_mu);
+    std::fprintf(stderr, "VTRACE begin n=%d t_rows0=%.4f chain_bps=%.3g link=%.3g threads=%d\n", v->n, t_rows0,
+                 v->host_chain_bps, link, threads);
+    for (const auto& t : g_vtrace)
+      std::fprintf(stderr, "VTRACE %d %d %d %.4f %.4f %.4f\n", t.who, t.chunk, t.kind, t.claim, t.ready, t.done);
+    std::fprintf(stderr, "VTRACE end hosts=%.4f feeder=%.4f\n", t_hosts, secs());
+    g_vtrace.clear();
+  }
   const double t_feeder = secs();
   if (err) st = ffail(GS_CUDA_ERROR, "verify_finish: GPU chain state unavailable");
   if (st == GS_OK && fst != GS_OK) st = fst;
