@@ -42,6 +42,7 @@ import math
 import os
 import socket
 import statistics
+import subprocess
 import sys
 import threading
 import time
@@ -804,6 +805,10 @@ def run_ours(args):
     if rank == 0 and world == 1 and W.key == "c2":
         host_tier = host_tier_checkpoint(torch, dev, W, scheme, pipe, comp, copy, args)
 
+    small_l = None
+    if rank == 0 and world == 1 and W.key == "c3" and not args.no_small_l:
+        small_l = small_l_summary()
+
     if rank == 0:
         line = {"metric": METRIC, "value": round(value, 3), "unit": "GB/s", "n_gpus": world,
                 "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms_step, 4),
@@ -822,7 +827,7 @@ def run_ours(args):
                 "recovery_ms": recovery_ms,
                 "roofline": kern or None, "roofline_k2": kern2 or None, "step_roofline": step_roofline,
                 "host_link": host_link, "cpu_baseline": cpu, "e2e": e2e,
-                "recovery": recovery, "decode_overhead": overhead, "host_tier": host_tier,
+                "recovery": recovery, "decode_overhead": overhead, "host_tier": host_tier, "small_l": small_l,
                 "gpu_launches": launches, "clocks": clk.summary(), "comm": comm,
                 "parity_ok": not failures, "failures": failures}
         print(json.dumps(line), flush=True)
@@ -1659,6 +1664,27 @@ def c3_recovery_striped(torch, dist, dev, comp, copy, pipe, rank, world, shared,
 # ---------------------------------------------------------------------------
 # C5: parity throughput sweep over block sizes (BASELINE.json configs[4])
 # ---------------------------------------------------------------------------
+def small_l_summary() -> dict:
+    """C5's small-shard regime in the driver-run line: RS(8,2) single-stripe
+    offload (K1 + parity D2H) at 64 KiB / 256 KiB / 1 MiB shards, eager and
+    CUDA-graph replayed, as fractions of the host-link roofline -- the same
+    rows `--sweep` prints, run in a child process on this GPU."""
+    cmd = [sys.executable, os.path.abspath(__file__), "--sweep", "--sweep-sizes", "64K,256K,1M",
+           "--sweep-codes", "RS(8,2)", "--no-cpu", "--steps", "200"]
+    try:
+        r = subprocess.run(cmd, capture_output=True, text=True, timeout=300)
+        rows = [json.loads(l) for l in r.stdout.splitlines() if l.startswith("{")]
+    except Exception as e:  # noqa: BLE001 -- reported in the line, not fatal to the headline
+        return {"error": repr(e)}
+    if not rows:
+        return {"error": f"sweep child rc={r.returncode}: {r.stderr.strip().splitlines()[-1:]}"}
+    return {"code": "RS(8,2)", "bound": "host link (parity D2H)",
+            "rows": [{"shard_bytes": x["shard_bytes"], "offload_gbs": x["offload_gbs"],
+                      "frac_eager": x["roofline_frac"], "frac_graph": x["graph"]["roofline_frac"],
+                      "parity_ok": x["parity_ok"]} for x in rows],
+            "source": "bench.py --sweep --sweep-sizes 64K,256K,1M --sweep-codes 'RS(8,2)' (child process)"}
+
+
 def _parse_size(x: str) -> int:
     x = x.strip().upper()
     mult = {"K": 1 << 10, "M": 1 << 20, "G": 1 << 30}
@@ -1747,6 +1773,7 @@ def run_sweep(args):
         return tmax(e0.elapsed_time(e1)) / (reps * len(plans)) * 1e-3
 
     codes = [("RS(8,2)", CodingScheme.reed_solomon(8, 2)), ("XOR(8)", CodingScheme.xor_code(8))]
+    codes = [c for c in codes if c[0] in args.sweep_codes.split(";")]
     for name, scheme in codes:
         n, k = scheme.n, scheme.k
         for L_ in [_parse_size(x) for x in args.sweep_sizes.split(",")]:
@@ -1840,6 +1867,8 @@ def main():
     ap.add_argument("--sweep", action="store_true", help="C5 block-size sweep instead of the C2 step")
     ap.add_argument("--sweep-sizes", default="64K,256K,1M,4M,16M,64M,256M,1G")
     ap.add_argument("--sweep-cpu-s", type=float, default=0.5)
+    ap.add_argument("--sweep-codes", default="RS(8,2);XOR(8)", help="';'-separated codes for --sweep")
+    ap.add_argument("--no-small-l", action="store_true", help="skip the C5 small-shard summary in the C3 line")
     ap.add_argument("--configs", action="store_true",
                     help="per-config table C1-C4 (encode+D2H, K1, recovery, rooflines, reference CPU, bit-exact)")
     ap.add_argument("--configs-only", default="", help="subset for --configs, e.g. C1,C4")
